@@ -1,0 +1,196 @@
+/*
+ * ffcz_cuda.h — C-ABI of the B200-native FFCz correction step (libffcz_cuda.so).
+ *
+ * The reference (/root/reference/proj) has no plugin/FFI layer; its seam is the C++ library
+ * call `ffcz::correct(original, decompressed, bounds_original, m, max_iters)`
+ * (proj/core/include/ffcz/pipeline.hpp:22-24), with a secondary seam
+ * `ffcz::alternating_projection(eps0, bounds_working, max_iters, slack)`
+ * (proj/core/include/ffcz/projection.hpp:65-70) and the transform helpers
+ * `forward_dft` / `inverse_dft` (proj/core/include/ffcz/transform.hpp:7-17).
+ * Every entry point below replaces one of those; the C++ shim in include/ffcz_cuda.hpp maps the
+ * reference's own types (ScalarField, DualBounds, CorrectionResult, ...) onto these plain-pointer
+ * signatures so callers of the reference are unchanged.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Field buffers are row-major, last index fastest, exactly as
+ *    ffcz::ScalarField::values.  Complex buffers are interleaved (re, im) doubles, exactly as
+ *    std::vector<std::complex<double>>.
+ *  - Inputs are caller-owned.  With FFCZ_INPUTS_ON_DEVICE they are device pointers on the
+ *    context's device, otherwise host pointers (copied in inside the call).
+ *  - Results are library-owned host buffers released by ffcz_cuda_result_free().
+ *  - Status codes mirror the reference's exception classes (errors.hpp:9-48); the message of the
+ *    last failure on the calling thread is ffcz_cuda_last_error().
+ *  - One CUDA stream per context; a context is internally locked (calls on one context
+ *    serialise; distinct contexts run concurrently), matching the reference's reentrancy
+ *    (SURVEY.md §8b "Threading").
+ */
+#ifndef FFCZ_CUDA_H
+#define FFCZ_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FFCZ_CUDA_ABI_VERSION 1
+
+typedef enum ffcz_cuda_status {
+    FFCZ_OK = 0,
+    FFCZ_VALIDATION_ERROR = 1, /* ffcz::validation_error: shapes, precondition, quantizer range */
+    FFCZ_SYMMETRY_ERROR = 2,   /* ffcz::symmetry_error: inverse of a non-Hermitian spectrum      */
+    FFCZ_FORMAT_ERROR = 3,     /* ffcz::format_error: archive encode/decode                      */
+    FFCZ_IO_ERROR = 4,         /* ffcz::io_error                                                 */
+    FFCZ_CUDA_ERROR = 5,       /* CUDA runtime / launch failure (no reference counterpart)      */
+    FFCZ_UNSUPPORTED = 6,      /* shape/size the device engine does not implement yet           */
+    FFCZ_OUT_OF_MEMORY = 7
+} ffcz_cuda_status;
+
+/* Sample type of the buffers passed in (the reference always holds doubles; f32 device buffers
+ * are accepted so an f32 dataset need not be widened on the host). */
+typedef enum ffcz_cuda_dtype { FFCZ_F32 = 0, FFCZ_F64 = 1 } ffcz_cuda_dtype;
+
+/* ffcz::Precision (field.hpp:12): the on-disk width tag carried into the archive. */
+typedef enum ffcz_cuda_precision { FFCZ_PRECISION_F32 = 0, FFCZ_PRECISION_F64 = 1 } ffcz_cuda_precision;
+
+typedef struct ffcz_field_desc {
+    int32_t ndim;       /* 1..3 (validate_dims, field.cpp:8-18) */
+    uint64_t dims[3];   /* row-major extents, dims[ndim-1] fastest */
+    int32_t dtype;      /* ffcz_cuda_dtype of original/decompressed/eps0 buffers */
+    int32_t precision;  /* ffcz_cuda_precision tag (ScalarField::precision) */
+} ffcz_field_desc;
+
+/* ffcz::DualBounds (bounds.hpp:11-47).  Per-point / per-component arrays cover all N samples /
+ * the FULL N-entry spectrum, as in the reference; they live where the inputs live. */
+typedef struct ffcz_bounds_desc {
+    int32_t spatial_per_point;
+    double spatial_global;
+    const double* spatial_values;  /* N, when spatial_per_point */
+    int32_t freq_per_component;
+    double freq_global;
+    const double* freq_re;         /* N, when freq_per_component */
+    const double* freq_im;         /* N, when freq_per_component */
+} ffcz_bounds_desc;
+
+/* Arithmetic policy of the projection loop.
+ *  FFCZ_POLICY_FP64: every pass in FP64 with the reference control flow (K3a/K3b split):
+ *                    iterations, flags and values follow the reference to FFT round-off.
+ *  FFCZ_POLICY_MIXED: FP32 fused passes while excess/peak > tau_switch, then FP64.
+ *  The FP64 gate (escape repair + verify) always runs in FP64. */
+typedef enum ffcz_cuda_policy { FFCZ_POLICY_FP64 = 0, FFCZ_POLICY_MIXED = 1 } ffcz_cuda_policy;
+
+/* option flags */
+#define FFCZ_INPUTS_ON_DEVICE (1u << 0) /* original/decompressed/bounds are device pointers      */
+#define FFCZ_WANT_ARCHIVE (1u << 1)     /* serialise the .ffcz archive (host Huffman + zlib)    */
+#define FFCZ_WANT_EDITS (1u << 2)       /* copy flags, int32 codes and escapes to the host      */
+#define FFCZ_WANT_CORRECTED (1u << 3)   /* copy the FP64 corrected field to the host            */
+#define FFCZ_FORCE_UNFUSED (1u << 4)    /* use the per-op (unfused) loop even for 2^k shapes    */
+
+typedef struct ffcz_cuda_options {
+    uint32_t flags;
+    int32_t policy;          /* ffcz_cuda_policy */
+    double tau_switch;       /* MIXED: switch to FP64 when max_excess/peak <= tau (default 1e-4) */
+    int32_t zlib_level;      /* archive outer stage level; 9 = reference byte-identical (default) */
+} ffcz_cuda_options;
+
+/* ffcz::ProjectionReport (projection.hpp:17-25) */
+typedef struct ffcz_cuda_report {
+    uint64_t iterations;
+    uint64_t active_spatial;
+    uint64_t active_frequency; /* counted over the FULL spectrum, as the reference */
+    int32_t converged;
+    double residual_f;
+    double residual_s;
+    double wall_time_s;        /* device time of the loop (CUDA events) */
+} ffcz_cuda_report;
+
+/* ffcz::EscapeEntry (editset.hpp:34-39) */
+typedef struct ffcz_cuda_escape {
+    int32_t frequency;
+    uint64_t index;
+    double re;
+    double im;
+} ffcz_cuda_escape;
+
+/* ffcz::CorrectionResult (pipeline.hpp:11-16) + the device-side products. */
+typedef struct ffcz_cuda_result {
+    ffcz_cuda_report report;
+    uint64_t iterations_fp32;      /* passes run by the FP32 phase (MIXED) */
+    uint64_t iterations_fp64;      /* passes run by the FP64 phase */
+    uint64_t escape_rounds;        /* escape-repair rounds run (pipeline.cpp:114-163) */
+    uint64_t escape_count;
+    int32_t verify_ok;             /* ffcz::VerifyResult against the ORIGINAL bounds, FP64 */
+    double verify_max_spatial_excess;
+    double verify_max_freq_excess;
+    /* edit set (FFCZ_WANT_EDITS): LSB-first flag bytes, int32 codes in flag order
+     * (frequency codes interleaved Re, Im), escapes ordered as the reference's std::map */
+    uint64_t n_spatial, n_frequency;
+    uint8_t* spatial_flags;   uint64_t spatial_flag_bytes;
+    uint8_t* frequency_flags; uint64_t frequency_flag_bytes;
+    int32_t* spatial_codes;   int32_t* frequency_codes;
+    ffcz_cuda_escape* escapes;
+    double* corrected;        /* FFCZ_WANT_CORRECTED: N doubles, decompressed + decoded edits */
+    uint8_t* archive;         /* FFCZ_WANT_ARCHIVE: .ffcz bytes (proj/docs/FORMAT.md) */
+    uint64_t archive_len;
+    /* timing (CUDA events on the context stream), milliseconds */
+    double t_feasible_ms;     /* inputs resident -> verified edits + corrected field resident */
+    double t_loop_ms;         /* alternating projection only */
+    double t_gate_ms;         /* compaction, quantisation, escape repair, FP64 verify */
+    double t_h2d_ms, t_d2h_ms, t_archive_ms;
+    uint64_t kernel_launches; /* kernels this call launched (incl. early-exit speculative ones) */
+} ffcz_cuda_result;
+
+typedef struct ffcz_cuda_ctx ffcz_cuda_ctx;
+
+/* Context on one device; `stream` is a cudaStream_t to run on (NULL = a private stream). */
+int ffcz_cuda_create(ffcz_cuda_ctx** out, int device, void* stream);
+void ffcz_cuda_destroy(ffcz_cuda_ctx* ctx);
+const char* ffcz_cuda_last_error(void);
+int ffcz_cuda_abi_version(void);
+void ffcz_cuda_default_options(ffcz_cuda_options* opt);
+
+/* Replaces ffcz::correct (pipeline.cpp:26-178). */
+int ffcz_cuda_correct(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const void* original,
+                      const void* decompressed, const ffcz_bounds_desc* bounds_original, int m,
+                      uint64_t max_iters, const ffcz_cuda_options* opt, ffcz_cuda_result* out);
+void ffcz_cuda_result_free(ffcz_cuda_result* r);
+
+/* Replaces ffcz::alternating_projection (projection.cpp:81-142).  eps0 is a field of
+ * field->dtype; bounds are the WORKING bounds.  Outputs (host, caller-allocated, may be NULL):
+ * spatial_edits N doubles, frequency_edits 2N doubles (FULL spectrum, interleaved),
+ * final_epsilon N doubles. */
+int ffcz_cuda_alternating_projection(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field,
+                                     const void* eps0, const ffcz_bounds_desc* bounds_working,
+                                     uint64_t max_iters, double precondition_slack,
+                                     const ffcz_cuda_options* opt, double* spatial_edits,
+                                     double* frequency_edits, double* final_epsilon,
+                                     ffcz_cuda_report* report);
+
+/* Replaces ffcz::forward_dft (transform.cpp:45-50): FP64, unnormalised; out = FULL spectrum,
+ * 2N doubles interleaved.  Host pointers. */
+int ffcz_cuda_forward_dft(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const double* x,
+                          double* spectrum_out);
+
+/* Replaces ffcz::inverse_dft (transform.cpp:64-80): 1/N-normalised inverse of a FULL spectrum
+ * (2N doubles) with the reference's imaginary-residue gate (FFCZ_SYMMETRY_ERROR).  out_precision
+ * selects the tolerance (1e-6 f32 / 1e-10 f64 of max|Re|). */
+int ffcz_cuda_inverse_dft(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const double* spectrum,
+                          int out_precision, double* x_out);
+
+/* Half-spectrum (R2C) transform in FP32 or FP64 on device pointers; out has
+ * prod(dims[:-1]) rows of (dims[-1]/2+1) complex, row-major.  Used by the engine tests and
+ * the per-pass roofline bench. dtype selects float/double for both buffers. */
+int ffcz_cuda_r2c_device(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const void* x_dev,
+                         void* half_dev);
+int ffcz_cuda_c2r_device(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const void* half_dev,
+                         void* x_dev);
+
+/* CRC-32C (archive.cpp:61-71), exported for the format tests. */
+uint32_t ffcz_cuda_crc32c(const uint8_t* data, size_t len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FFCZ_CUDA_H */

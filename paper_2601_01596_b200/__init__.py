@@ -1,0 +1,16 @@
+"""B200-native FFCz correction step (arXiv 2601.01596): C-ABI engine + Python host mirror.
+
+See DESIGN.md for the path, the HBM layout and the kernels; INTEGRATION.md for the drop-in
+boundary against the reference C++ API.
+"""
+from .ffcz import (  # noqa: F401
+    Context, CorrectionResult, CudaError, DualBounds, EscapeEntry, FfczError, FormatError,
+    ProjectionReport, SymmetryError, UnsupportedError, ValidationError, alternating_projection,
+    correct, default_context, forward_dft, inverse_dft,
+)
+
+__all__ = [
+    "Context", "CorrectionResult", "DualBounds", "EscapeEntry", "ProjectionReport", "FfczError",
+    "ValidationError", "SymmetryError", "FormatError", "CudaError", "UnsupportedError",
+    "correct", "alternating_projection", "forward_dft", "inverse_dft", "default_context",
+]

@@ -1,0 +1,248 @@
+// Host-side .ffcz archive writer.  Byte layout follows /root/reference/proj/docs/FORMAT.md and
+// the reference writer (archive.cpp:73-135, streams.cpp:21-55, huffman.cpp:156-251) so that the
+// reference's read_archive decodes it and, with zlib level 9 and identical edits, the bytes are
+// identical.
+#include "archive.hpp"
+
+#include <zlib.h>
+
+#include <algorithm>
+#include <cstring>
+#include <queue>
+#include <stdexcept>
+#include <string>
+
+namespace ffcz_host {
+
+namespace {
+
+template <class T>
+void put(std::vector<std::uint8_t>& out, T v) {
+    std::uint8_t b[sizeof(T)];
+    std::memcpy(b, &v, sizeof(T));
+    out.insert(out.end(), b, b + sizeof(T));
+}
+
+constexpr std::size_t kBlockSymbols = std::size_t(1) << 16;  // huffman.hpp:13
+
+// Code lengths from repeatedly pairing the two lightest subtrees, ordered by
+// (weight, smallest contained symbol) — the reference's deterministic tie-break
+// (huffman.cpp:74-120).  (weight, tiebreak) pairs are unique, so the pairing sequence and hence
+// every depth is implementation-independent.
+std::vector<std::uint8_t> code_lengths(const std::vector<std::uint32_t>& syms,
+                                       const std::vector<std::uint64_t>& w) {
+    const std::size_t n = syms.size();
+    if (n == 1) return {1};
+    struct Node {
+        std::uint64_t weight;
+        std::uint32_t tie;
+        int left, right;
+    };
+    std::vector<Node> nodes;
+    nodes.reserve(2 * n);
+    using Key = std::pair<std::pair<std::uint64_t, std::uint32_t>, int>;
+    std::priority_queue<Key, std::vector<Key>, std::greater<Key>> heap;
+    for (std::size_t i = 0; i < n; ++i) {
+        nodes.push_back({w[i], syms[i], -1, -1});
+        heap.push({{w[i], syms[i]}, static_cast<int>(i)});
+    }
+    while (heap.size() > 1) {
+        const int a = heap.top().second;
+        heap.pop();
+        const int b = heap.top().second;
+        heap.pop();
+        nodes.push_back({nodes[a].weight + nodes[b].weight, std::min(nodes[a].tie, nodes[b].tie), a, b});
+        const int id = static_cast<int>(nodes.size()) - 1;
+        heap.push({{nodes[id].weight, nodes[id].tie}, id});
+    }
+    std::vector<std::uint8_t> len(n, 0);
+    std::vector<std::pair<int, int>> stack{{heap.top().second, 0}};
+    while (!stack.empty()) {
+        auto [id, d] = stack.back();
+        stack.pop_back();
+        if (nodes[id].left < 0) {
+            len[id] = static_cast<std::uint8_t>(d);
+        } else {
+            stack.push_back({nodes[id].left, d + 1});
+            stack.push_back({nodes[id].right, d + 1});
+        }
+    }
+    return len;
+}
+
+struct BitSink {
+    std::vector<std::uint8_t>& out;
+    std::uint64_t acc = 0;  // pending bits, MSB-first
+    int nacc = 0;
+    std::uint64_t total = 0;
+    void put(std::uint32_t code, int len) {
+        total += static_cast<std::uint64_t>(len);
+        // flush whole bytes while keeping <= 56 pending bits
+        acc = (acc << len) | (len == 32 ? code : (code & ((1u << len) - 1u)));
+        nacc += len;
+        while (nacc >= 8) {
+            nacc -= 8;
+            out.push_back(static_cast<std::uint8_t>(acc >> nacc));
+        }
+        acc &= (nacc ? ((std::uint64_t(1) << nacc) - 1) : 0);
+    }
+    void flush() {
+        if (nacc > 0) out.push_back(static_cast<std::uint8_t>(acc << (8 - nacc)));
+        acc = 0;
+        nacc = 0;
+    }
+};
+
+void encode_block(std::vector<std::uint8_t>& out, const std::uint32_t* data, std::size_t n) {
+    std::vector<std::uint32_t> sorted(data, data + n);
+    std::sort(sorted.begin(), sorted.end());
+    std::vector<std::uint32_t> syms;
+    std::vector<std::uint64_t> counts;
+    for (std::size_t i = 0; i < n;) {
+        std::size_t j = i;
+        while (j < n && sorted[j] == sorted[i]) ++j;
+        syms.push_back(sorted[i]);
+        counts.push_back(j - i);
+        i = j;
+    }
+    const std::vector<std::uint8_t> lens = code_lengths(syms, counts);
+    // canonical order (length, symbol) and codes (huffman.cpp:124-154)
+    std::vector<std::size_t> order(syms.size());
+    for (std::size_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) {
+        return lens[a] != lens[b] ? lens[a] < lens[b] : syms[a] < syms[b];
+    });
+    std::vector<std::uint32_t> code_of(syms.size());
+    std::uint32_t code = 0;
+    int prev = 0;
+    for (std::size_t r = 0; r < order.size(); ++r) {
+        const std::size_t i = order[r];
+        code <<= (lens[i] - prev);
+        code_of[i] = code++;
+        prev = lens[i];
+    }
+    put<std::uint32_t>(out, static_cast<std::uint32_t>(n));
+    put<std::uint32_t>(out, static_cast<std::uint32_t>(syms.size()));
+    for (std::size_t i : order) {
+        put<std::uint32_t>(out, syms[i]);
+        put<std::uint8_t>(out, lens[i]);
+    }
+    const std::size_t nbits_pos = out.size();
+    put<std::uint64_t>(out, 0);
+    BitSink bs{out};
+    for (std::size_t i = 0; i < n; ++i) {
+        const std::size_t s = std::lower_bound(syms.begin(), syms.end(), data[i]) - syms.begin();
+        bs.put(code_of[s], lens[s]);
+    }
+    bs.flush();
+    std::memcpy(out.data() + nbits_pos, &bs.total, sizeof(std::uint64_t));
+}
+
+} // namespace
+
+std::uint32_t crc32c(const std::uint8_t* data, std::size_t len) {
+    static std::uint32_t table[256];
+    static bool init = [] {
+        for (std::uint32_t i = 0; i < 256; ++i) {
+            std::uint32_t c = i;
+            for (int j = 0; j < 8; ++j) c = (c >> 1) ^ (0x82F63B78u & (0u - (c & 1u)));
+            table[i] = c;
+        }
+        return true;
+    }();
+    (void)init;
+    std::uint32_t crc = 0xFFFFFFFFu;
+    for (std::size_t i = 0; i < len; ++i) crc = (crc >> 8) ^ table[(crc ^ data[i]) & 0xFFu];
+    return crc ^ 0xFFFFFFFFu;
+}
+
+std::uint32_t zigzag(std::int32_t v) {
+    return (static_cast<std::uint32_t>(v) << 1) ^ static_cast<std::uint32_t>(v >> 31);
+}
+
+std::vector<std::uint8_t> huffman_encode(const std::uint32_t* symbols, std::size_t n) {
+    std::vector<std::uint8_t> out;
+    put<std::uint64_t>(out, n);
+    for (std::size_t s = 0; s < n; s += kBlockSymbols)
+        encode_block(out, symbols + s, std::min(kBlockSymbols, n - s));
+    return out;
+}
+
+std::vector<std::uint8_t> outer_compress(const std::uint8_t* raw, std::size_t n, int level) {
+    uLongf bound = compressBound(static_cast<uLong>(n));
+    std::vector<std::uint8_t> out(sizeof(std::uint64_t) + bound);
+    const std::uint64_t raw_size = n;
+    std::memcpy(out.data(), &raw_size, sizeof(raw_size));
+    static const Bytef empty = 0;
+    const int rc = compress2(out.data() + sizeof(raw_size), &bound, n ? raw : &empty,
+                             static_cast<uLong>(n), level);
+    if (rc != Z_OK) throw std::runtime_error("outer_compress failed: zlib rc " + std::to_string(rc));
+    out.resize(sizeof(raw_size) + bound);
+    return out;
+}
+
+std::vector<std::uint8_t> write_archive(const ArchiveInput& in) {
+    std::uint64_t N = 1;
+    for (int a = 0; a < in.ndim; ++a) N *= in.dims[a];
+
+    auto index_stream = [&](const std::int32_t* codes, std::size_t n) {
+        std::vector<std::uint32_t> sym(n);
+        for (std::size_t i = 0; i < n; ++i) sym[i] = zigzag(codes[i]);
+        const std::vector<std::uint8_t> h = huffman_encode(sym.data(), n);
+        return outer_compress(h.data(), h.size(), in.zlib_level);
+    };
+    const auto sf = outer_compress(in.spatial_flags, in.spatial_flag_bytes, in.zlib_level);
+    const auto ff = outer_compress(in.frequency_flags, in.frequency_flag_bytes, in.zlib_level);
+    const auto si = index_stream(in.spatial_codes, in.n_spatial);
+    const auto fi = index_stream(in.frequency_codes, 2 * in.n_frequency);
+
+    std::vector<std::uint8_t> w;
+    w.reserve(128 + 8 * (in.spatial_per_point ? N : 1) + 16 * (in.freq_per_component ? N : 1) +
+              sf.size() + ff.size() + si.size() + fi.size() + 24 * in.n_escapes);
+    const char magic[4] = {'F', 'F', 'C', 'Z'};
+    w.insert(w.end(), magic, magic + 4);
+    put<std::uint16_t>(w, 1);
+    put<std::uint8_t>(w, static_cast<std::uint8_t>(in.ndim));
+    for (int a = 0; a < in.ndim; ++a) put<std::uint64_t>(w, in.dims[a]);
+    put<std::uint8_t>(w, static_cast<std::uint8_t>(in.precision));
+    std::uint8_t tags = 0;
+    if (in.spatial_per_point) tags |= 1u;
+    if (in.freq_per_component) tags |= 2u;
+    if (in.converged) tags |= 4u;
+    put<std::uint8_t>(w, tags);
+    auto put_doubles = [&](const double* v, std::uint64_t n) {
+        const std::size_t off = w.size();
+        w.resize(off + n * sizeof(double));
+        std::memcpy(w.data() + off, v, n * sizeof(double));
+    };
+    if (in.spatial_per_point) put_doubles(in.spatial_values, N);
+    else put<double>(w, in.spatial_global);
+    if (in.freq_per_component) {
+        put_doubles(in.freq_re, N);
+        put_doubles(in.freq_im, N);
+    } else {
+        put<double>(w, in.freq_global);
+    }
+    put<std::uint8_t>(w, static_cast<std::uint8_t>(in.m));
+    put<std::uint64_t>(w, in.n_spatial);
+    put<std::uint64_t>(w, in.n_frequency);
+    put<std::uint64_t>(w, sf.size());
+    put<std::uint64_t>(w, ff.size());
+    put<std::uint64_t>(w, si.size());
+    put<std::uint64_t>(w, fi.size());
+    put<std::uint64_t>(w, in.n_escapes);
+    put<std::uint32_t>(w, crc32c(w.data(), w.size()));
+    w.insert(w.end(), sf.begin(), sf.end());
+    w.insert(w.end(), ff.begin(), ff.end());
+    w.insert(w.end(), si.begin(), si.end());
+    w.insert(w.end(), fi.begin(), fi.end());
+    for (std::uint64_t i = 0; i < in.n_escapes; ++i) {
+        const EscapeRec& e = in.escapes[i];
+        put<std::uint64_t>(w, e.index | (e.frequency ? (std::uint64_t(1) << 63) : 0));
+        put<double>(w, e.re);
+        if (e.frequency) put<double>(w, e.im);
+    }
+    return w;
+}
+
+} // namespace ffcz_host

@@ -1,0 +1,46 @@
+// Host-side .ffcz archive serialisation (format: /root/reference/proj/docs/FORMAT.md).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+namespace ffcz_host {
+
+struct EscapeRec {
+    bool frequency;
+    std::uint64_t index;
+    double re, im;
+};
+
+struct ArchiveInput {
+    int ndim;
+    std::uint64_t dims[3];
+    int precision;  // 0 f32, 1 f64
+    bool spatial_per_point;
+    double spatial_global;
+    const double* spatial_values;  // N (host)
+    bool freq_per_component;
+    double freq_global;
+    const double* freq_re;  // N (host, full spectrum)
+    const double* freq_im;
+    int m;
+    bool converged;
+    const std::uint8_t* spatial_flags;   std::uint64_t spatial_flag_bytes;
+    const std::uint8_t* frequency_flags; std::uint64_t frequency_flag_bytes;
+    std::uint64_t n_spatial, n_frequency;
+    const std::int32_t* spatial_codes;    // n_spatial
+    const std::int32_t* frequency_codes;  // 2 * n_frequency
+    const EscapeRec* escapes;
+    std::uint64_t n_escapes;
+    int zlib_level;
+};
+
+std::uint32_t crc32c(const std::uint8_t* data, std::size_t len);
+std::uint32_t zigzag(std::int32_t v);
+// Blockwise canonical Huffman (huffman.cpp:156-251 format)
+std::vector<std::uint8_t> huffman_encode(const std::uint32_t* symbols, std::size_t n);
+// u64 raw size + zlib stream (streams.cpp:21-32 format)
+std::vector<std::uint8_t> outer_compress(const std::uint8_t* raw, std::size_t n, int level);
+std::vector<std::uint8_t> write_archive(const ArchiveInput& in);
+
+} // namespace ffcz_host

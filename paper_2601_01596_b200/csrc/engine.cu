@@ -1,0 +1,814 @@
+// Host orchestration of the FFCz correction step on one B200 + the C-ABI (include/ffcz_cuda.h).
+//
+// Control flow restates ffcz::correct (/root/reference/proj/core/src/pipeline.cpp:26-178) and
+// ffcz::alternating_projection (/root/reference/proj/core/src/projection.cpp:81-142):
+//   eps0 + preconditions -> device-resident projection loop -> FP64 gate (compaction,
+//   quantisation, overflow escapes, escape repair, verify) -> optional host archive.
+// The projection loop is enqueued speculatively in chunks; every loop kernel returns at once
+// after the on-device decision kernel has set ctl->done, so the host never syncs per iteration.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ffcz_cuda.h"
+#include "archive.hpp"
+#include "fft_plan.cuh"
+#include "kernels.cuh"
+
+using namespace ffcz_gpu;
+
+double bitsd_host(unsigned long long b);
+
+struct ffcz_cuda_ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    std::mutex mu;
+    Twiddles<double> tw64;
+    Twiddles<float> tw32;
+    std::map<std::string, std::pair<void*, size_t>> bufs;
+    Ctl* ctl = nullptr;
+    Ctl* hctl = nullptr;   // pinned mirror (one slot per in-flight chunk)
+    unsigned long long launches = 0;
+    cudaEvent_t ev[8] = {};
+
+    void* buf(const std::string& name, size_t bytes) {
+        auto it = bufs.find(name);
+        if (it != bufs.end() && it->second.second >= bytes) return it->second.first;
+        if (it != bufs.end()) {
+            FFCZ_CUDA_CHECK(cudaStreamSynchronize(st));
+            cudaFree(it->second.first);
+            bufs.erase(it);
+        }
+        void* p = nullptr;
+        FFCZ_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+        bufs[name] = {p, std::max<size_t>(bytes, 256)};
+        return p;
+    }
+    template <class T> T* b(const std::string& name, size_t count) {
+        return static_cast<T*>(buf(name, count * sizeof(T)));
+    }
+    void sync() { FFCZ_CUDA_CHECK(cudaStreamSynchronize(st)); }
+    Ctl read_ctl() {
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        sync();
+        return *hctl;
+    }
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const std::string& msg) {
+    g_last_error = msg;
+    return status;
+}
+
+template <class F>
+int guarded(ffcz_cuda_ctx* ctx, F&& f) {
+    try {
+        if (!ctx) return fail(kValidation, "null context");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        FFCZ_CUDA_CHECK(cudaSetDevice(ctx->device));
+        f();
+        return kOk;
+    } catch (const Error& e) {
+        return fail(e.status, e.what());
+    } catch (const std::bad_alloc& e) {
+        return fail(kOom, e.what());
+    } catch (const std::exception& e) {
+        return fail(kCuda, e.what());
+    }
+}
+
+inline unsigned grid_for(long long n, int threads = 256) {
+    long long b = (n + threads - 1) / threads;
+    return static_cast<unsigned>(std::max<long long>(1, std::min<long long>(b, 148LL * 16)));
+}
+
+constexpr int kPitchAlign = 16;
+
+struct Bounds {
+    SpatialB sb{nullptr, 0.0};
+    FreqB fb{nullptr, nullptr, 0.0};
+};
+
+// Copies / restricts the caller's bounds onto the device (per-component arrays -> half layout).
+Bounds upload_bounds(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_bounds_desc& bd, bool on_dev) {
+    Bounds b;
+    const long long N = g.N;
+    if (bd.spatial_per_point) {
+        if (!bd.spatial_values) throw Error(kValidation, "per-point spatial bound array is null");
+        if (on_dev) {
+            b.sb.v = bd.spatial_values;
+        } else {
+            double* d = c.b<double>("E_pp", N);
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(d, bd.spatial_values, N * sizeof(double),
+                                            cudaMemcpyHostToDevice, c.st));
+            b.sb.v = d;
+        }
+    } else {
+        if (!(bd.spatial_global > 0.0) || !std::isfinite(bd.spatial_global))
+            throw Error(kValidation, "spatial bound E must be strictly positive and finite");
+        b.sb.g = bd.spatial_global;
+    }
+    if (bd.freq_per_component) {
+        if (!bd.freq_re || !bd.freq_im)
+            throw Error(kValidation, "per-component frequency bound arrays are null");
+        const HalfGeom hg = g.hg();
+        auto restrict_lane = [&](const double* full, const char* name) {
+            const double* dfull = full;
+            if (!on_dev) {
+                double* stage = c.b<double>("bounds_stage", N);
+                FFCZ_CUDA_CHECK(cudaMemcpyAsync(stage, full, N * sizeof(double),
+                                                cudaMemcpyHostToDevice, c.st));
+                dfull = stage;
+            }
+            double* half = c.b<double>(name, g.half_elems());
+            k_gather_half<<<grid_for(g.Nc()), 256, 0, c.st>>>(dfull, half, hg);
+            FFCZ_LAUNCH_CHECK();
+            ++c.launches;
+            return half;
+        };
+        bool same = bd.freq_re == bd.freq_im;
+        if (!same && !on_dev) same = std::memcmp(bd.freq_re, bd.freq_im, N * sizeof(double)) == 0;
+        b.fb.re = restrict_lane(bd.freq_re, "D_re");
+        b.fb.im = same ? b.fb.re : restrict_lane(bd.freq_im, "D_im");
+    } else {
+        if (!(bd.freq_global > 0.0) || !std::isfinite(bd.freq_global))
+            throw Error(kValidation, "frequency bound Delta must be strictly positive and finite");
+        b.fb.g = bd.freq_global;
+    }
+    return b;
+}
+
+struct LoopResult {
+    unsigned long long passes = 0;
+    bool converged = false;
+    double residual_f = 0.0;
+    bool fused = false;
+};
+
+// The POCS loop (projection.cpp:96-126) on device.  eps holds epsilon0 on entry and the final
+// epsilon on exit; S (N) and F (half) are the accumulated edits.
+LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Bounds& bw,
+                    double fscale, bool allow_fused, double* S, double2* F) {
+    cudaStream_t st = c.st;
+    FftPlan<double> plan{g, &c.tw64};
+    const int* gate = &c.ctl->done;
+    double2* spec = c.b<double2>("spec", g.half_elems());
+    FFCZ_CUDA_CHECK(cudaMemsetAsync(S, 0, g.N * sizeof(double), st));
+    FFCZ_CUDA_CHECK(cudaMemsetAsync(F, 0, g.half_elems() * sizeof(double2), st));
+    const double invN = 1.0 / static_cast<double>(g.N);
+    const HalfGeom hg = g.hg();
+    const bool fused = allow_fused && plan.fused_ok();
+    const bool three_d = g.d[0] > 1;
+    const int za = three_d ? 0 : 1;  // the pass that completes the forward transform
+    double* tmp = fused ? nullptr : c.b<double>("real_tmp", g.N);
+
+    auto body = [&]() {
+        if (fused) {
+            plan.col(za, -1, spec, spec, gate, HookFReduce{bw.fb, fscale, c.ctl}, st);   // K3a
+            k_decide<<<1, 1, 0, st>>>(c.ctl);                                          // K4
+            plan.col(za, +1, spec, spec, gate, HookFClip<double>{bw.fb, fscale, F}, st); // K3b
+            if (three_d) plan.col(1, +1, spec, spec, gate, HookNone{}, st);
+            launch_row_fused<double>(g.n2, spec, g.P, g.rows, g.n2, invN, c.tw64, gate,
+                                     HookSClip<double>{bw.sb, fscale, S, eps}, st);      // K1
+            if (three_d) plan.col(1, -1, spec, spec, gate, HookNone{}, st);
+            c.launches += three_d ? 6 : 4;
+        } else {
+            plan.r2c(eps, spec, gate, st);
+            k_freduce<<<grid_for(g.Nc()), 256, 0, st>>>(spec, hg, bw.fb, fscale, c.ctl, gate);
+            k_decide<<<1, 1, 0, st>>>(c.ctl);
+            k_fclip<<<grid_for(g.Nc()), 256, 0, st>>>(spec, hg, bw.fb, fscale, F, gate);
+            plan.c2r(spec, spec, tmp, invN, gate, st);
+            k_sclip<<<grid_for(g.N), 256, 0, st>>>(tmp, eps, g.N, bw.sb, fscale, S, gate);
+            c.launches += 10;
+        }
+        FFCZ_LAUNCH_CHECK();
+    };
+
+    if (fused) {
+        launch_row_r2c<double>(g.n2, eps, g.n2, spec, g.P, g.rows, c.tw64, gate, st);
+        if (three_d) plan.col(1, -1, spec, spec, gate, HookNone{}, st);
+        c.launches += three_d ? 2 : 1;
+    }
+
+    // pipelined speculative chunks: keep one chunk queued behind the one being polled
+    struct Poll {
+        cudaEvent_t ev;
+        int slot;
+    };
+    static const int kChunk[] = {1, 1, 2, 4, 8};
+    int ci = 0, issued = 0;
+    std::vector<Poll> inflight;
+    auto issue_chunk = [&]() {
+        const int n = kChunk[std::min(ci++, 4)];
+        for (int i = 0; i < n; ++i) body();
+        const int slot = issued % 2;
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(&c.hctl[1 + slot], c.ctl, sizeof(Ctl),
+                                        cudaMemcpyDeviceToHost, st));
+        cudaEvent_t ev = c.ev[4 + slot];
+        FFCZ_CUDA_CHECK(cudaEventRecord(ev, st));
+        inflight.push_back({ev, slot});
+        ++issued;
+    };
+    issue_chunk();
+    for (;;) {
+        issue_chunk();
+        Poll p = inflight.front();
+        inflight.erase(inflight.begin());
+        FFCZ_CUDA_CHECK(cudaEventSynchronize(p.ev));
+        if (c.hctl[1 + p.slot].done) break;
+    }
+    const Ctl h = c.read_ctl();
+    LoopResult r;
+    r.passes = h.passes;
+    r.converged = h.converged;
+    r.residual_f = h.residual_f;
+    r.fused = fused;
+    return r;
+}
+
+} // namespace
+
+// host-side bit cast
+double bitsd_host(unsigned long long b);
+
+namespace {
+
+// bitmap -> ascending index list; returns the count
+unsigned long long compact_bits(ffcz_cuda_ctx& c, const unsigned* words, long long nwords,
+                                unsigned long long* idx) {
+    const long long nblk = std::max<long long>(1, (nwords + 1023) / 1024);
+    unsigned long long* counts = c.b<unsigned long long>("blk_counts", nblk + 1);
+    k_popc_blocks<<<static_cast<unsigned>(nblk), 1024, 0, c.st>>>(words, nwords, counts);
+    k_scan_blocks<<<1, 1024, 0, c.st>>>(counts, nblk, &c.ctl->count_a);
+    k_compact<<<static_cast<unsigned>(nblk), 1024, 0, c.st>>>(words, nwords, counts, idx);
+    FFCZ_LAUNCH_CHECK();
+    c.launches += 3;
+    return c.read_ctl().count_a;
+}
+
+struct GateOut {
+    unsigned long long n_keep_s = 0, n_keep_f = 0, n_esc_s = 0, n_esc_f = 0;
+    unsigned long long rounds = 0;
+    int verify_ok = 0;
+    double vs = 0, vf = 0;
+    unsigned long long act_s = 0, act_f = 0;
+};
+
+template <class TI>
+GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* dec,
+                 const Bounds& bo, int m, bool converged, double* eps, double* S, double2* F,
+                 double* corrected) {
+    cudaStream_t st = c.st;
+    FftPlan<double> plan{g, &c.tw64};
+    const HalfGeom hg = g.hg();
+    const long long N = g.N, Nc = g.Nc();
+    const long long ws = (N + 31) / 32, wf = (Nc + 31) / 32;
+    double* spat_cur = c.b<double>("spat_cur", N);
+    double2* freq_cur = c.b<double2>("freq_cur", g.half_elems());
+    unsigned* keep_s = c.b<unsigned>("keep_s", ws);
+    unsigned* esc_s = c.b<unsigned>("esc_s", ws);
+    unsigned* keep_f = c.b<unsigned>("keep_f", wf);
+    unsigned* esc_f = c.b<unsigned>("esc_f", wf);
+    unsigned long long* idx = c.b<unsigned long long>("idx", std::max(N, Nc));
+    int* codes_s = c.b<int>("codes_s", N);
+    int* codes_f = c.b<int>("codes_f", 2 * Nc);
+    double2* spec = c.b<double2>("spec", g.half_elems());
+    double* eps_t = c.b<double>("eps_tilde", N);
+
+    FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->act_s, 0, 2 * sizeof(unsigned long long), st));
+    k_gate_spatial<<<grid_for(N), 256, 0, st>>>(S, N, bo.sb, m, spat_cur, keep_s, esc_s, c.ctl);
+    k_gate_freq<<<grid_for(Nc), 256, 0, st>>>(F, hg, bo.fb, m, freq_cur, keep_f, esc_f, c.ctl);
+    FFCZ_LAUNCH_CHECK();
+    c.launches += 2;
+
+    GateOut o;
+    o.n_keep_s = compact_bits(c, keep_s, ws, idx);
+    k_codes_spatial<<<grid_for(o.n_keep_s), 256, 0, st>>>(idx, o.n_keep_s, S, bo.sb, m, codes_s);
+    o.n_keep_f = compact_bits(c, keep_f, wf, idx);
+    k_codes_freq<<<grid_for(o.n_keep_f), 256, 0, st>>>(idx, o.n_keep_f, F, hg, bo.fb, m, codes_f);
+    FFCZ_LAUNCH_CHECK();
+    c.launches += 2;
+
+    // S and F are consumed: reuse them as the frequency-part and delta_star buffers.
+    double* fpart = S;
+    double2* delta_star = F;
+    const double invN = 1.0 / static_cast<double>(N);
+    if (converged) {
+        plan.r2c(eps, delta_star, nullptr, st);                          // pipeline.cpp:114
+        for (int round = 0; round < 32; ++round) {                       // pipeline.cpp:116
+            FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->dirty, 0, sizeof(int), st));
+            plan.c2r(freq_cur, spec, fpart, invN, nullptr, st);          // :125-133
+            k_repair_spatial<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, fpart, eps, N, bo.sb,
+                                                              spat_cur, eps_t, esc_s, c.ctl);
+            plan.r2c(eps_t, spec, nullptr, st);                          // :137-138
+            k_repair_freq<<<grid_for(Nc), 256, 0, st>>>(delta_star, spec, hg, g.ndim, g.d[0],
+                                                        g.d[1], bo.fb, freq_cur, esc_f, c.ctl);
+            FFCZ_LAUNCH_CHECK();
+            c.launches += 8;
+            ++o.rounds;
+            if (!c.read_ctl().dirty) break;                              // :161
+        }
+    }
+    // read_archive + apply_edits + verify_bounds (pipeline.cpp:174-176) on the decoder view
+    plan.c2r(freq_cur, spec, fpart, invN, nullptr, st);
+    k_verify_spatial<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, spat_cur, fpart, N, bo.sb,
+                                                      corrected, eps_t, c.ctl);
+    plan.r2c(eps_t, spec, nullptr, st);
+    k_verify_freq<<<grid_for(Nc), 256, 0, st>>>(spec, hg, bo.fb, c.ctl);
+    FFCZ_LAUNCH_CHECK();
+    c.launches += 8;
+    const Ctl h = c.read_ctl();
+    o.vs = bitsd_host(h.vs_bits);
+    o.vf = bitsd_host(h.vf_bits);
+    o.verify_ok = (o.vs == 0.0 && o.vf == 0.0);
+    o.act_s = h.act_s;
+    o.act_f = h.act_f;
+    return o;
+}
+
+double event_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    FFCZ_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+}
+
+template <class TI>
+void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& fd,
+                   const void* orig_in, const void* dec_in, const ffcz_bounds_desc& bd, int m,
+                   uint64_t max_iters, const ffcz_cuda_options& opt, ffcz_cuda_result* out) {
+    cudaStream_t st = c.st;
+    const bool on_dev = opt.flags & FFCZ_INPUTS_ON_DEVICE;
+    const long long N = g.N;
+    FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[0], st));
+    const TI* orig = static_cast<const TI*>(orig_in);
+    const TI* dec = static_cast<const TI*>(dec_in);
+    if (!on_dev) {
+        TI* o = c.b<TI>("in_orig", N);
+        TI* d = c.b<TI>("in_dec", N);
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(o, orig_in, N * sizeof(TI), cudaMemcpyHostToDevice, st));
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(d, dec_in, N * sizeof(TI), cudaMemcpyHostToDevice, st));
+        orig = o;
+        dec = d;
+    }
+    const Bounds bo = upload_bounds(c, g, bd, on_dev);
+    FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[1], st));  // inputs resident
+
+    // compute_error + preconditions (pipeline.cpp:31-42)
+    k_ctl_init<<<1, 1, 0, st>>>(c.ctl, max_iters);
+    double* eps = c.b<double>("eps", N);
+    const double f = 1.0 - std::ldexp(1.0, -m);
+    const double slack = 1.0 / (1.0 - std::ldexp(1.0, -m)) - 1.0 + 0x1p-20;
+    k_eps0<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, eps, N, bo.sb, f, slack, 1, c.ctl);
+    FFCZ_LAUNCH_CHECK();
+    c.launches += 2;
+    Ctl h = c.read_ctl();
+    if (h.bad1 != ~0ull)
+        throw Error(kValidation, "correct: decompressed data violates the declared spatial bound "
+                                 "at index " + std::to_string(h.bad1));
+    if (m < 1 || m > 24) throw Error(kValidation, "shrink_bounds requires 1 <= m <= 24");
+    if (max_iters < 1) throw Error(kValidation, "alternating_projection: max_iters must be >= 1");
+    if (h.bad2 != ~0ull)
+        throw Error(kValidation, "alternating_projection: epsilon0 violates the spatial bound at "
+                                 "index " + std::to_string(h.bad2));
+
+    double* S = c.b<double>("S", N);
+    double2* F = c.b<double2>("F", g.half_elems());
+    FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[2], st));
+    const LoopResult lr = run_loop(c, g, eps, bo, f, !(opt.flags & FFCZ_FORCE_UNFUSED), S, F);
+    FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[3], st));
+    k_residual_s<<<grid_for(N), 256, 0, st>>>(eps, N, bo.sb, f, c.ctl);
+    ++c.launches;
+
+    double* corrected = c.b<double>("corrected", N);
+    const GateOut go = run_gate<TI>(c, g, orig, dec, bo, m, lr.converged, eps, S, F, corrected);
+    FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[6], st));
+    h = c.read_ctl();
+
+    out->report.iterations = std::max<unsigned long long>(lr.passes, 1);
+    out->report.active_spatial = go.act_s;
+    out->report.active_frequency = go.act_f;
+    out->report.converged = lr.converged;
+    out->report.residual_f = lr.residual_f;
+    out->report.residual_s = bitsd_host(h.res_s_bits);
+    out->report.wall_time_s = event_ms(c.ev[2], c.ev[3]) * 1e-3;
+    out->iterations_fp32 = 0;
+    out->iterations_fp64 = lr.passes;
+    out->escape_rounds = go.rounds;
+    out->verify_ok = go.verify_ok;
+    out->verify_max_spatial_excess = go.vs;
+    out->verify_max_freq_excess = go.vf;
+    out->n_spatial = go.n_keep_s;
+    out->n_frequency = go.n_keep_f;
+    out->t_h2d_ms = event_ms(c.ev[0], c.ev[1]);
+    out->t_loop_ms = event_ms(c.ev[2], c.ev[3]);
+    out->t_gate_ms = event_ms(c.ev[3], c.ev[6]);
+    out->t_feasible_ms = event_ms(c.ev[1], c.ev[6]);
+
+    // ---- products to the host -------------------------------------------------------------
+    const auto t_d2h0 = std::chrono::steady_clock::now();
+    const long long ws = (N + 31) / 32, wf = (g.Nc() + 31) / 32;
+    std::vector<ffcz_cuda_escape> escapes;
+    {
+        unsigned long long* idx = c.b<unsigned long long>("idx", std::max(N, g.Nc()));
+        const unsigned long long ns = compact_bits(c, c.b<unsigned>("esc_s", ws), ws, idx);
+        std::vector<unsigned long long> hidx(ns);
+        std::vector<double> hval(ns);
+        if (ns) {
+            double* vals = c.b<double>("esc_vals", 2 * ns);
+            k_gather_escapes_s<<<grid_for(ns), 256, 0, st>>>(idx, ns, c.b<double>("spat_cur", N), vals);
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(hidx.data(), idx, ns * 8, cudaMemcpyDeviceToHost, st));
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(hval.data(), vals, ns * 8, cudaMemcpyDeviceToHost, st));
+            c.sync();
+        }
+        for (unsigned long long i = 0; i < ns; ++i) escapes.push_back({0, hidx[i], hval[i], 0.0});
+        const unsigned long long nf = compact_bits(c, c.b<unsigned>("esc_f", wf), wf, idx);
+        std::vector<unsigned long long> fidx(nf);
+        std::vector<double2> fval(nf);
+        if (nf) {
+            double2* vals = c.b<double2>("esc_valf", nf);
+            k_gather_escapes_f<<<grid_for(nf), 256, 0, st>>>(idx, nf, c.b<double2>("freq_cur", g.half_elems()),
+                                                             g.hg(), vals);
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(fidx.data(), idx, nf * 8, cudaMemcpyDeviceToHost, st));
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(fval.data(), vals, nf * 16, cudaMemcpyDeviceToHost, st));
+            c.sync();
+        }
+        for (unsigned long long i = 0; i < nf; ++i)
+            escapes.push_back({1, fidx[i], fval[i].x, fval[i].y});
+        FFCZ_LAUNCH_CHECK();
+    }
+    out->escape_count = escapes.size();
+    const bool want_edits = opt.flags & (FFCZ_WANT_EDITS | FFCZ_WANT_ARCHIVE);
+    if (want_edits) {
+        out->spatial_flag_bytes = (N + 7) / 8;
+        out->frequency_flag_bytes = (g.Nc() + 7) / 8;
+        out->spatial_flags = static_cast<uint8_t*>(std::malloc(out->spatial_flag_bytes + 1));
+        out->frequency_flags = static_cast<uint8_t*>(std::malloc(out->frequency_flag_bytes + 1));
+        out->spatial_codes = static_cast<int32_t*>(std::malloc(go.n_keep_s * 4 + 4));
+        out->frequency_codes = static_cast<int32_t*>(std::malloc(go.n_keep_f * 8 + 4));
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->spatial_flags, c.b<unsigned>("keep_s", ws),
+                                        out->spatial_flag_bytes, cudaMemcpyDeviceToHost, st));
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->frequency_flags, c.b<unsigned>("keep_f", wf),
+                                        out->frequency_flag_bytes, cudaMemcpyDeviceToHost, st));
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->spatial_codes, c.b<int>("codes_s", N), go.n_keep_s * 4,
+                                        cudaMemcpyDeviceToHost, st));
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->frequency_codes, c.b<int>("codes_f", 2 * g.Nc()),
+                                        go.n_keep_f * 8, cudaMemcpyDeviceToHost, st));
+        out->escapes = static_cast<ffcz_cuda_escape*>(
+            std::malloc(sizeof(ffcz_cuda_escape) * (escapes.size() + 1)));
+        std::memcpy(out->escapes, escapes.data(), sizeof(ffcz_cuda_escape) * escapes.size());
+    }
+    if (opt.flags & FFCZ_WANT_CORRECTED) {
+        out->corrected = static_cast<double*>(std::malloc(N * sizeof(double)));
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->corrected, corrected, N * sizeof(double),
+                                        cudaMemcpyDeviceToHost, st));
+    }
+    c.sync();
+    const auto t_d2h1 = std::chrono::steady_clock::now();
+    out->t_d2h_ms = std::chrono::duration<double, std::milli>(t_d2h1 - t_d2h0).count();
+
+    if (opt.flags & FFCZ_WANT_ARCHIVE) {
+        // header bounds must be the caller's full arrays (host)
+        std::vector<double> e_host, re_host, im_host;
+        const double* e_vals = bd.spatial_values;
+        const double* re_vals = bd.freq_re;
+        const double* im_vals = bd.freq_im;
+        if (on_dev) {
+            if (bd.spatial_per_point) {
+                e_host.resize(N);
+                FFCZ_CUDA_CHECK(cudaMemcpy(e_host.data(), bd.spatial_values, N * 8, cudaMemcpyDeviceToHost));
+                e_vals = e_host.data();
+            }
+            if (bd.freq_per_component) {
+                re_host.resize(N);
+                FFCZ_CUDA_CHECK(cudaMemcpy(re_host.data(), bd.freq_re, N * 8, cudaMemcpyDeviceToHost));
+                re_vals = re_host.data();
+                if (bd.freq_im == bd.freq_re) {
+                    im_vals = re_vals;
+                } else {
+                    im_host.resize(N);
+                    FFCZ_CUDA_CHECK(cudaMemcpy(im_host.data(), bd.freq_im, N * 8, cudaMemcpyDeviceToHost));
+                    im_vals = im_host.data();
+                }
+            }
+        }
+        std::vector<ffcz_host::EscapeRec> er(escapes.size());
+        for (size_t i = 0; i < escapes.size(); ++i)
+            er[i] = {escapes[i].frequency != 0, escapes[i].index, escapes[i].re, escapes[i].im};
+        ffcz_host::ArchiveInput ai{};
+        ai.ndim = fd.ndim;
+        for (int a = 0; a < fd.ndim; ++a) ai.dims[a] = fd.dims[a];
+        ai.precision = fd.precision;
+        ai.spatial_per_point = bd.spatial_per_point;
+        ai.spatial_global = bd.spatial_global;
+        ai.spatial_values = e_vals;
+        ai.freq_per_component = bd.freq_per_component;
+        ai.freq_global = bd.freq_global;
+        ai.freq_re = re_vals;
+        ai.freq_im = im_vals;
+        ai.m = m;
+        ai.converged = lr.converged;
+        ai.spatial_flags = out->spatial_flags;
+        ai.spatial_flag_bytes = out->spatial_flag_bytes;
+        ai.frequency_flags = out->frequency_flags;
+        ai.frequency_flag_bytes = out->frequency_flag_bytes;
+        ai.n_spatial = go.n_keep_s;
+        ai.n_frequency = go.n_keep_f;
+        ai.spatial_codes = out->spatial_codes;
+        ai.frequency_codes = out->frequency_codes;
+        ai.escapes = er.data();
+        ai.n_escapes = er.size();
+        ai.zlib_level = opt.zlib_level;
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<uint8_t> bytes = ffcz_host::write_archive(ai);
+        out->t_archive_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        out->archive_len = bytes.size();
+        out->archive = static_cast<uint8_t*>(std::malloc(bytes.size() + 1));
+        std::memcpy(out->archive, bytes.data(), bytes.size());
+    }
+}
+
+} // namespace
+
+double bitsd_host(unsigned long long b) {
+    double d;
+    std::memcpy(&d, &b, sizeof(d));
+    return d;
+}
+
+template <class T>
+static void r2c_dev(ffcz_cuda_ctx& c, Twiddles<T>& tw, const Geometry& g, const T* x, cplx<T>* out) {
+    cplx<T>* half = static_cast<cplx<T>*>(c.buf("dev_half", g.half_elems() * sizeof(cplx<T>)));
+    FftPlan<T> plan{g, &tw};
+    plan.r2c(x, half, nullptr, c.st);
+    FFCZ_CUDA_CHECK(cudaMemcpy2DAsync(out, g.H * sizeof(cplx<T>), half, g.P * sizeof(cplx<T>),
+                                      g.H * sizeof(cplx<T>), g.rows, cudaMemcpyDeviceToDevice, c.st));
+    c.sync();
+}
+
+template <class T>
+static void c2r_dev(ffcz_cuda_ctx& c, Twiddles<T>& tw, const Geometry& g, const cplx<T>* in, T* x) {
+    cplx<T>* half = static_cast<cplx<T>*>(c.buf("dev_half", g.half_elems() * sizeof(cplx<T>)));
+    FFCZ_CUDA_CHECK(cudaMemcpy2DAsync(half, g.P * sizeof(cplx<T>), in, g.H * sizeof(cplx<T>),
+                                      g.H * sizeof(cplx<T>), g.rows, cudaMemcpyDeviceToDevice, c.st));
+    FftPlan<T> plan{g, &tw};
+    plan.c2r(half, half, x, static_cast<T>(1.0 / static_cast<double>(g.N)), nullptr, c.st);
+    c.sync();
+}
+
+
+// ================================ C-ABI ===========================================================
+
+extern "C" {
+
+int ffcz_cuda_abi_version(void) { return FFCZ_CUDA_ABI_VERSION; }
+const char* ffcz_cuda_last_error(void) { return g_last_error.c_str(); }
+
+void ffcz_cuda_default_options(ffcz_cuda_options* opt) {
+    opt->flags = FFCZ_WANT_EDITS;
+    opt->policy = FFCZ_POLICY_FP64;
+    opt->tau_switch = 1e-4;
+    opt->zlib_level = 9;
+}
+
+int ffcz_cuda_create(ffcz_cuda_ctx** out, int device, void* stream) {
+    try {
+        if (!out) return fail(kValidation, "null output pointer");
+        auto* c = new ffcz_cuda_ctx;
+        c->device = device;
+        FFCZ_CUDA_CHECK(cudaSetDevice(device));
+        if (stream) {
+            c->st = static_cast<cudaStream_t>(stream);
+        } else {
+            FFCZ_CUDA_CHECK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+            c->own_stream = true;
+        }
+        FFCZ_CUDA_CHECK(cudaMalloc(&c->ctl, sizeof(Ctl)));
+        FFCZ_CUDA_CHECK(cudaMallocHost(&c->hctl, 4 * sizeof(Ctl)));
+        for (auto& e : c->ev) FFCZ_CUDA_CHECK(cudaEventCreate(&e));
+        c->tw64.init();
+        c->tw32.init();
+        *out = c;
+        return kOk;
+    } catch (const Error& e) {
+        return fail(e.status, e.what());
+    } catch (const std::exception& e) {
+        return fail(kCuda, e.what());
+    }
+}
+
+void ffcz_cuda_destroy(ffcz_cuda_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->st);
+    for (auto& kv : c->bufs) cudaFree(kv.second.first);
+    if (c->ctl) cudaFree(c->ctl);
+    if (c->hctl) cudaFreeHost(c->hctl);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->own_stream) cudaStreamDestroy(c->st);
+    delete c;
+}
+
+void ffcz_cuda_result_free(ffcz_cuda_result* r) {
+    if (!r) return;
+    std::free(r->spatial_flags);
+    std::free(r->frequency_flags);
+    std::free(r->spatial_codes);
+    std::free(r->frequency_codes);
+    std::free(r->escapes);
+    std::free(r->corrected);
+    std::free(r->archive);
+    std::memset(r, 0, sizeof(*r));
+}
+
+int ffcz_cuda_correct(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const void* original,
+                      const void* decompressed, const ffcz_bounds_desc* bounds_original, int m,
+                      uint64_t max_iters, const ffcz_cuda_options* opt_in, ffcz_cuda_result* out) {
+    return guarded(ctx, [&] {
+        if (!field || !original || !decompressed || !bounds_original || !out)
+            throw Error(kValidation, "null argument");
+        std::memset(out, 0, sizeof(*out));
+        ffcz_cuda_options opt;
+        ffcz_cuda_default_options(&opt);
+        if (opt_in) opt = *opt_in;
+        if (opt.policy != FFCZ_POLICY_FP64)
+            throw Error(kUnsupported, "only FFCZ_POLICY_FP64 is implemented in this build");
+        const Geometry g = make_geometry(field->ndim, field->dims, kPitchAlign);
+        const unsigned long long l0 = ctx->launches;
+        if (field->dtype == FFCZ_F32)
+            correct_typed<float>(*ctx, g, *field, original, decompressed, *bounds_original, m,
+                                 max_iters, opt, out);
+        else
+            correct_typed<double>(*ctx, g, *field, original, decompressed, *bounds_original, m,
+                                  max_iters, opt, out);
+        out->kernel_launches = ctx->launches - l0;
+    });
+}
+
+int ffcz_cuda_alternating_projection(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field,
+                                     const void* eps0_in, const ffcz_bounds_desc* bw_desc,
+                                     uint64_t max_iters, double precondition_slack,
+                                     const ffcz_cuda_options* opt_in, double* spatial_edits,
+                                     double* frequency_edits, double* final_epsilon,
+                                     ffcz_cuda_report* report) {
+    return guarded(ctx, [&] {
+        if (!field || !eps0_in || !bw_desc || !report) throw Error(kValidation, "null argument");
+        ffcz_cuda_options opt;
+        ffcz_cuda_default_options(&opt);
+        if (opt_in) opt = *opt_in;
+        if (max_iters < 1) throw Error(kValidation, "alternating_projection: max_iters must be >= 1");
+        const Geometry g = make_geometry(field->ndim, field->dims, kPitchAlign);
+        ffcz_cuda_ctx& c = *ctx;
+        cudaStream_t st = c.st;
+        const bool on_dev = opt.flags & FFCZ_INPUTS_ON_DEVICE;
+        const long long N = g.N;
+        const Bounds bw = upload_bounds(c, g, *bw_desc, on_dev);
+        double* eps = c.b<double>("eps", N);
+        const size_t esz = field->dtype == FFCZ_F32 ? 4 : 8;
+        const void* src = eps0_in;
+        if (!on_dev) {
+            void* d = c.buf("in_eps0", N * esz);
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(d, eps0_in, N * esz, cudaMemcpyHostToDevice, st));
+            src = d;
+        }
+        // eps = eps0 (widened); precondition vs working bounds + slack (projection.cpp:88-94)
+        double* zeros = c.b<double>("zeros_in", 1);
+        (void)zeros;
+        k_ctl_init<<<1, 1, 0, st>>>(c.ctl, max_iters);
+        if (field->dtype == FFCZ_F32) {
+            float* z = c.b<float>("zero_f", N);
+            FFCZ_CUDA_CHECK(cudaMemsetAsync(z, 0, N * sizeof(float), st));
+            k_eps0<float><<<grid_for(N), 256, 0, st>>>(z, static_cast<const float*>(src), eps, N,
+                                                        bw.sb, 1.0, precondition_slack, 0, c.ctl);
+        } else {
+            double* z = c.b<double>("zero_d", N);
+            FFCZ_CUDA_CHECK(cudaMemsetAsync(z, 0, N * sizeof(double), st));
+            k_eps0<double><<<grid_for(N), 256, 0, st>>>(z, static_cast<const double*>(src), eps, N,
+                                                         bw.sb, 1.0, precondition_slack, 0, c.ctl);
+        }
+        FFCZ_LAUNCH_CHECK();
+        const Ctl h0 = c.read_ctl();
+        if (h0.bad2 != ~0ull)
+            throw Error(kValidation, "alternating_projection: epsilon0 violates the spatial bound "
+                                     "at index " + std::to_string(h0.bad2));
+        double* S = c.b<double>("S", N);
+        double2* F = c.b<double2>("F", g.half_elems());
+        FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[2], st));
+        const LoopResult lr = run_loop(c, g, eps, bw, 1.0, !(opt.flags & FFCZ_FORCE_UNFUSED), S, F);
+        FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[3], st));
+        k_residual_s<<<grid_for(N), 256, 0, st>>>(eps, N, bw.sb, 1.0, c.ctl);
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->act_s, 0, 2 * sizeof(unsigned long long), st));
+        k_count_spatial<<<grid_for(N), 256, 0, st>>>(S, N, c.ctl);
+        k_count_freq<<<grid_for(g.Nc()), 256, 0, st>>>(F, g.hg(), c.ctl);
+        FFCZ_LAUNCH_CHECK();
+        const Ctl h = c.read_ctl();
+        report->iterations = std::max<unsigned long long>(lr.passes, 1);
+        report->active_spatial = h.act_s;
+        report->active_frequency = h.act_f;
+        report->converged = lr.converged;
+        report->residual_f = lr.residual_f;
+        report->residual_s = bitsd_host(h.res_s_bits);
+        report->wall_time_s = event_ms(c.ev[2], c.ev[3]) * 1e-3;
+        if (spatial_edits)
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(spatial_edits, S, N * 8, cudaMemcpyDeviceToHost, st));
+        if (final_epsilon)
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(final_epsilon, eps, N * 8, cudaMemcpyDeviceToHost, st));
+        if (frequency_edits) {
+            double2* full = c.b<double2>("full_tmp", N);
+            k_expand_full<<<grid_for(N), 256, 0, st>>>(F, full, g.ndim, g.d[0], g.d[1], g.d[2], g.P);
+            FFCZ_LAUNCH_CHECK();
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(frequency_edits, full, N * 16, cudaMemcpyDeviceToHost, st));
+        }
+        c.sync();
+    });
+}
+
+int ffcz_cuda_forward_dft(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const double* x,
+                          double* spectrum_out) {
+    return guarded(ctx, [&] {
+        const Geometry g = make_geometry(field->ndim, field->dims, kPitchAlign);
+        ffcz_cuda_ctx& c = *ctx;
+        double* dx = c.b<double>("fx", g.N);
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(dx, x, g.N * 8, cudaMemcpyHostToDevice, c.st));
+        double2* half = c.b<double2>("fhalf", g.half_elems());
+        FftPlan<double> plan{g, &c.tw64};
+        plan.r2c(dx, half, nullptr, c.st);
+        double2* full = c.b<double2>("full_tmp", g.N);
+        k_expand_full<<<grid_for(g.N), 256, 0, c.st>>>(half, full, g.ndim, g.d[0], g.d[1], g.d[2], g.P);
+        FFCZ_LAUNCH_CHECK();
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(spectrum_out, full, g.N * 16, cudaMemcpyDeviceToHost, c.st));
+        c.sync();
+    });
+}
+
+int ffcz_cuda_inverse_dft(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const double* spectrum,
+                          int out_precision, double* x_out) {
+    return guarded(ctx, [&] {
+        const Geometry g = make_geometry(field->ndim, field->dims, kPitchAlign);
+        ffcz_cuda_ctx& c = *ctx;
+        cudaStream_t st = c.st;
+        double2* full = c.b<double2>("full_tmp", g.N);
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(full, spectrum, g.N * 16, cudaMemcpyHostToDevice, st));
+        double2* Hh = c.b<double2>("fhalf", g.half_elems());
+        double2* Ah = c.b<double2>("fhalf2", g.half_elems());
+        k_split_hermitian<<<grid_for(g.Nc()), 256, 0, st>>>(full, Hh, Ah, g.hg(), g.d[0], g.d[1]);
+        FFCZ_LAUNCH_CHECK();
+        double* re = c.b<double>("fx", g.N);
+        double* im = c.b<double>("fx2", g.N);
+        FftPlan<double> plan{g, &c.tw64};
+        const double invN = 1.0 / static_cast<double>(g.N);
+        plan.c2r(Hh, Hh, re, invN, nullptr, st);
+        plan.c2r(Ah, Ah, im, invN, nullptr, st);
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->vs_bits, 0, 2 * sizeof(unsigned long long), st));
+        k_maxabs<<<grid_for(g.N), 256, 0, st>>>(re, g.N, &c.ctl->vs_bits);
+        k_maxabs<<<grid_for(g.N), 256, 0, st>>>(im, g.N, &c.ctl->vf_bits);
+        FFCZ_LAUNCH_CHECK();
+        const Ctl h = c.read_ctl();
+        const double max_re = bitsd_host(h.vs_bits), max_im = bitsd_host(h.vf_bits);
+        // transform.cpp:64-80
+        const double tol = (out_precision == FFCZ_PRECISION_F32 ? 1e-6 : 1e-10) * std::max(max_re, 1e-300);
+        if (max_im > tol)
+            throw Error(kSymmetry, "inverse_dft: imaginary residue " + std::to_string(max_im) +
+                                       " exceeds tolerance (non-Hermitian input?)");
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(x_out, re, g.N * 8, cudaMemcpyDeviceToHost, st));
+        c.sync();
+    });
+}
+
+int ffcz_cuda_r2c_device(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const void* x_dev,
+                         void* half_dev) {
+    return guarded(ctx, [&] {
+        const Geometry g = make_geometry(field->ndim, field->dims, kPitchAlign);
+        if (field->dtype == FFCZ_F32)
+            r2c_dev<float>(*ctx, ctx->tw32, g, static_cast<const float*>(x_dev), static_cast<float2*>(half_dev));
+        else
+            r2c_dev<double>(*ctx, ctx->tw64, g, static_cast<const double*>(x_dev), static_cast<double2*>(half_dev));
+    });
+}
+
+int ffcz_cuda_c2r_device(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const void* half_dev,
+                         void* x_dev) {
+    return guarded(ctx, [&] {
+        const Geometry g = make_geometry(field->ndim, field->dims, kPitchAlign);
+        if (field->dtype == FFCZ_F32)
+            c2r_dev<float>(*ctx, ctx->tw32, g, static_cast<const float2*>(half_dev), static_cast<float*>(x_dev));
+        else
+            c2r_dev<double>(*ctx, ctx->tw64, g, static_cast<const double2*>(half_dev), static_cast<double*>(x_dev));
+    });
+}
+
+uint32_t ffcz_cuda_crc32c(const uint8_t* data, size_t len) { return ffcz_host::crc32c(data, len); }
+
+} // extern "C"

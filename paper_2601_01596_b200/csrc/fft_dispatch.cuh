@@ -1,0 +1,250 @@
+// Launch-time dispatch from runtime extents to the templated pass kernels.  Included by the
+// per-precision instantiation units (fft_f32.cu, fft_f64.cu).
+#pragma once
+
+#include <algorithm>
+
+#include "fft_plan.cuh"
+
+namespace ffcz_gpu {
+
+namespace detail {
+
+inline int pow2_floor(long long v) {
+    int p = 1;
+    while ((long long)p * 2 <= v) p *= 2;
+    return p;
+}
+inline int pow2_ceil(long long v) {
+    int p = 1;
+    while (p < v) p *= 2;
+    return p;
+}
+
+// Per-CTA complex-element budget of the exchange tile: B*L (columns) or rows*M (rows).
+// 4096 FP64 / 8192 FP32 elements = 64 KiB (+1/E padding) -> three CTAs per SM.
+template <class T> constexpr long long tile_budget() { return sizeof(T) == 8 ? 4096 : 8192; }
+
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024)
+        FFCZ_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(bytes)));
+}
+
+inline unsigned grid1(long long n, int threads) {
+    long long b = (n + threads - 1) / threads;
+    return static_cast<unsigned>(std::max<long long>(1, std::min<long long>(b, 148LL * 32)));
+}
+
+template <class T, int L, class Hook>
+void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
+               long long plane_stride, long long nplanes, int ncols, Twiddles<T>& tw,
+               const int* gate, Hook hook, cudaStream_t st) {
+    constexpr int E = L < kRadixE<T> ? L : kRadixE<T>;
+    constexpr int TT = L / E;
+    int B = static_cast<int>(std::min<long long>(tile_budget<T>() / L, 512 / TT));
+    B = std::min(B, 128);
+    B = std::min(B, pow2_ceil(ncols));
+    B = std::max(B, 1);
+    const size_t smem = col_smem_bytes<T, L, E>(B);
+    dim3 grid((ncols + B - 1) / B, static_cast<unsigned>(nplanes));
+    if (dir < 0) {
+        auto k = k_col<T, L, E, -1, Hook>;
+        set_smem(k, smem);
+        k<<<grid, TT * B, smem, st>>>(src, dst, row_stride, plane_stride, ncols, B, tw.W,
+                                       kLmax / L, gate, hook);
+    } else {
+        auto k = k_col<T, L, E, +1, Hook>;
+        set_smem(k, smem);
+        k<<<grid, TT * B, smem, st>>>(src, dst, row_stride, plane_stride, ncols, B, tw.W,
+                                       kLmax / L, gate, hook);
+    }
+    FFCZ_LAUNCH_CHECK();
+}
+
+template <class T, int M> struct RowCfg {
+    static constexpr int E = M < kRadixE<T> ? M : kRadixE<T>;
+    static constexpr int TT = M / E;
+};
+
+template <class T, int M>
+int rows_per_cta(long long nrows) {
+    constexpr int TT = RowCfg<T, M>::TT;
+    long long r = std::min<long long>(tile_budget<T>() / M, 512 / TT);
+    r = std::min<long long>(r, pow2_ceil(nrows));
+    return static_cast<int>(std::max<long long>(1, r));
+}
+
+template <class T, int M>
+void row_r2c_radix(const T* in, long long in_stride, cplx<T>* out, long long out_stride,
+                   long long nrows, Twiddles<T>& tw, const int* gate, cudaStream_t st) {
+    constexpr int E = RowCfg<T, M>::E, TT = RowCfg<T, M>::TT;
+    const int R = rows_per_cta<T, M>(nrows);
+    const size_t smem = row_smem_bytes<T, M, E>(R);
+    auto k = k_row_r2c<T, M, E, HookNone>;
+    set_smem(k, smem);
+    k<<<static_cast<unsigned>((nrows + R - 1) / R), TT * R, smem, st>>>(
+        in, in_stride, out, out_stride, nrows, tw.W, kLmax / M, kLmax / (2 * M), gate, HookNone{});
+    FFCZ_LAUNCH_CHECK();
+}
+
+template <class T, int M>
+void row_c2r_radix(const cplx<T>* in, long long in_stride, T* out, long long out_stride,
+                   long long nrows, T scale, Twiddles<T>& tw, const int* gate, cudaStream_t st) {
+    constexpr int E = RowCfg<T, M>::E, TT = RowCfg<T, M>::TT;
+    const int R = rows_per_cta<T, M>(nrows);
+    const size_t smem = row_smem_bytes<T, M, E>(R);
+    auto k = k_row_c2r<T, M, E, RealHookNone>;
+    set_smem(k, smem);
+    k<<<static_cast<unsigned>((nrows + R - 1) / R), TT * R, smem, st>>>(
+        in, in_stride, out, out_stride, nrows, tw.W, kLmax / M, kLmax / (2 * M), scale, gate,
+        RealHookNone{});
+    FFCZ_LAUNCH_CHECK();
+}
+
+template <class T, int M, class Hook>
+void row_fused_radix(cplx<T>* data, long long stride, long long nrows, long long real_stride,
+                     T scale, Twiddles<T>& tw, const int* gate, Hook hook, cudaStream_t st) {
+    constexpr int E = RowCfg<T, M>::E, TT = RowCfg<T, M>::TT;
+    const int R = rows_per_cta<T, M>(nrows);
+    const size_t smem = row_smem_bytes<T, M, E>(R);
+    auto k = k_row_c2r_r2c<T, M, E, Hook>;
+    set_smem(k, smem);
+    k<<<static_cast<unsigned>((nrows + R - 1) / R), TT * R, smem, st>>>(
+        data, stride, nrows, real_stride, tw.W, kLmax / M, kLmax / (2 * M), scale, gate, hook);
+    FFCZ_LAUNCH_CHECK();
+}
+
+} // namespace detail
+
+#define FFCZ_POW2_CASES(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
+
+template <class T, class Hook>
+void launch_col(long long L, int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
+                long long plane_stride, long long nplanes, int ncols, Twiddles<T>& tw,
+                const int* gate, Hook hook, cudaStream_t st) {
+    if (radix_col_ok(L)) {
+        switch (L) {
+#define X(n)                                                                                   \
+    case n:                                                                                    \
+        detail::col_radix<T, n, Hook>(dir, src, dst, row_stride, plane_stride, nplanes, ncols, \
+                                      tw, gate, hook, st);                                     \
+        return;
+            FFCZ_POW2_CASES(X)
+#undef X
+        }
+    }
+    if constexpr (!std::is_same_v<Hook, HookNone>) {
+        throw Error(kUnsupported, "fused column pass needs a power-of-two extent in [16, 4096]");
+    } else {
+        // direct O(L) pass: tile L x B columns in smem
+        const size_t per_col = sizeof(cplx<T>) * L;
+        if (per_col > 96 * 1024)
+            throw Error(kUnsupported, "axis extent " + std::to_string(L) +
+                                          " is neither a power of two <= 4096 nor <= 6144");
+        int B = static_cast<int>(std::max<long long>(1, std::min<long long>(48 * 1024 / per_col, 32)));
+        B = std::min(B, detail::pow2_ceil(ncols));
+        const size_t smem = per_col * B;
+        detail::set_smem(k_col_direct<T>, smem);
+        dim3 grid((ncols + B - 1) / B, static_cast<unsigned>(nplanes));
+        k_col_direct<T><<<grid, 256, smem, st>>>(src, dst, static_cast<int>(L), row_stride,
+                                                  plane_stride, ncols, B, tw.table_for(L), dir,
+                                                  gate);
+        FFCZ_LAUNCH_CHECK();
+    }
+}
+
+template <class T>
+void launch_row_r2c(long long n2, const T* in, long long in_stride, cplx<T>* out,
+                    long long out_stride, long long nrows, Twiddles<T>& tw, const int* gate,
+                    cudaStream_t st) {
+    if (radix_row_ok(n2)) {
+        switch (n2 / 2) {
+#define X(n)                                                                                   \
+    case n:                                                                                    \
+        detail::row_r2c_radix<T, n>(in, in_stride, out, out_stride, nrows, tw, gate, st);      \
+        return;
+            FFCZ_POW2_CASES(X)
+#undef X
+        }
+    }
+    const size_t smem = sizeof(T) * n2;
+    if (smem > 96 * 1024) throw Error(kUnsupported, "last-axis extent too large for direct R2C");
+    detail::set_smem(k_row_r2c_direct<T>, smem);
+    k_row_r2c_direct<T><<<static_cast<unsigned>(nrows), 256, smem, st>>>(
+        in, in_stride, out, out_stride, static_cast<int>(n2), tw.table_for(n2), gate);
+    FFCZ_LAUNCH_CHECK();
+}
+
+template <class T>
+void launch_row_c2r(long long n2, const cplx<T>* in, long long in_stride, T* out,
+                    long long out_stride, long long nrows, T scale, Twiddles<T>& tw,
+                    const int* gate, cudaStream_t st) {
+    if (radix_row_ok(n2)) {
+        switch (n2 / 2) {
+#define X(n)                                                                                   \
+    case n:                                                                                    \
+        detail::row_c2r_radix<T, n>(in, in_stride, out, out_stride, nrows, scale, tw, gate, st); \
+        return;
+            FFCZ_POW2_CASES(X)
+#undef X
+        }
+    }
+    const size_t smem = sizeof(cplx<T>) * (n2 / 2 + 1);
+    if (smem > 96 * 1024) throw Error(kUnsupported, "last-axis extent too large for direct C2R");
+    detail::set_smem(k_row_c2r_direct<T>, smem);
+    k_row_c2r_direct<T><<<static_cast<unsigned>(nrows), 256, smem, st>>>(
+        in, in_stride, out, out_stride, static_cast<int>(n2), tw.table_for(n2), scale, gate);
+    FFCZ_LAUNCH_CHECK();
+}
+
+template <class T, class Hook>
+void launch_row_fused(long long n2, cplx<T>* data, long long stride, long long nrows,
+                      long long real_stride, T scale, Twiddles<T>& tw, const int* gate, Hook hook,
+                      cudaStream_t st) {
+    if (radix_row_ok(n2)) {
+        switch (n2 / 2) {
+#define X(n)                                                                                   \
+    case n:                                                                                    \
+        detail::row_fused_radix<T, n, Hook>(data, stride, nrows, real_stride, scale, tw, gate, \
+                                            hook, st);                                         \
+        return;
+            FFCZ_POW2_CASES(X)
+#undef X
+        }
+    }
+    throw Error(kUnsupported, "fused row pass needs a power-of-two last axis in [32, 8192]");
+}
+
+template <class T>
+void FftPlan<T>::r2c(const T* x, cplx<T>* half, const int* gate, cudaStream_t st) const {
+    launch_row_r2c<T>(g.n2, x, g.n2, half, g.P, g.rows, *tw, gate, st);
+    col<HookNone>(1, -1, half, half, gate, HookNone{}, st);
+    col<HookNone>(0, -1, half, half, gate, HookNone{}, st);
+}
+
+template <class T>
+void FftPlan<T>::c2r(const cplx<T>* half, cplx<T>* work, T* x, T scale, const int* gate,
+                     cudaStream_t st) const {
+    const cplx<T>* src = half;
+    if (g.d[0] > 1) {
+        col<HookNone>(0, +1, src, work, gate, HookNone{}, st);
+        src = work;
+    }
+    if (g.d[1] > 1) {
+        col<HookNone>(1, +1, src, work, gate, HookNone{}, st);
+        src = work;
+    }
+    launch_row_c2r<T>(g.n2, src, g.P, x, g.n2, g.rows, scale, *tw, gate, st);
+}
+
+template <class T>
+bool FftPlan<T>::fused_ok() const {
+    if (!radix_row_ok(g.n2)) return false;
+    for (int a = 0; a < 2; ++a)
+        if (g.d[a] > 1 && !radix_col_ok(g.d[a])) return false;
+    return g.ndim >= 2;
+}
+
+} // namespace ffcz_gpu

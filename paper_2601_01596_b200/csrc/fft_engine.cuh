@@ -1,0 +1,525 @@
+// Hand-written FFT engine for sm_100a: batched 1-D passes of a separable R2C/C2R transform.
+//
+// Replaces the reference's FFTW c2c call (`run_c2c`, /root/reference/proj/core/src/transform.cpp:20-50)
+// with a half-spectrum (R2C/C2R) decomposition; SURVEY.md §0.5 / App. B establish that an FP64
+// half-spectrum loop is observationally identical to the reference's full c2c loop.
+//
+// Layout in HBM: a real field is row-major n0 x n1 x n2 (last axis fastest);
+// its half spectrum is row-major n0 x n1 x P complex with P = round_up(n2/2+1, 128 B/elem) so every
+// row starts 128-byte aligned (the Nyquist column k2 = n2/2 is a ragged last tile).
+//
+// Every pass is one kernel that reads each element once and writes it once (16 B/complex FP32,
+// 32 B FP64 — the per-pass algorithmic traffic of SURVEY.md §8d).  Inside a pass:
+//  * each thread owns E elements of one line in registers, strided by T = L/E
+//    (v[m] = x[t + T*m]); global loads/stores of that set are coalesced because consecutive
+//    lanes own consecutive columns (column passes) or consecutive elements (row passes);
+//  * the line is transformed by Stockham radix-E stages (radix <= 32 butterflies fully in
+//    registers with compile-time twiddles), exchanging through padded shared memory between
+//    stages (row i lives at i + i/E: the stride-E writes of stage 1 hit distinct banks);
+//  * inter-stage twiddles come from one FP64-derived table W[q] = exp(-2*pi*i*q/LMAX).
+// Fusion hooks (pre/post functors) let the projection loop put its clip / reduction into the
+// pass that produces or consumes the data.
+#pragma once
+
+#include <utility>
+
+#include "common.cuh"
+
+namespace ffcz_gpu {
+
+// cos(2*pi*q/32), q in [0, 16)
+__host__ __device__ constexpr double cos32(int q) {
+    return q == 0   ? 1.0
+           : q == 1 ? 0.98078528040323044912618223613424
+           : q == 2 ? 0.92387953251128675612818318939679
+           : q == 3 ? 0.83146961230254523707878837761791
+           : q == 4 ? 0.70710678118654752440084436210485
+           : q == 5 ? 0.55557023301960222474283081394853
+           : q == 6 ? 0.38268343236508977172845998403040
+           : q == 7 ? 0.19509032201612826784828486847702
+           : q == 8 ? 0.0
+                    : -cos32(16 - q);
+}
+// sin(2*pi*q/32), q in [0, 16)
+__host__ __device__ constexpr double sin32(int q) { return q <= 8 ? cos32(8 - q) : cos32(q - 8); }
+
+// a * exp(DIR * 2*pi*i * Q/32)
+template <int DIR, int Q, class C>
+__device__ __forceinline__ C twq(C a) {
+    using T = decltype(a.x);
+    if constexpr (Q == 0) {
+        return a;
+    } else if constexpr (Q == 8) {
+        return DIR < 0 ? cmulmi(a) : cmuli(a);
+    } else {
+        constexpr T c = static_cast<T>(cos32(Q));
+        constexpr T s = static_cast<T>(DIR * sin32(Q));
+        C r;
+        r.x = a.x * c - a.y * s;
+        r.y = a.x * s + a.y * c;
+        return r;
+    }
+}
+
+__host__ __device__ constexpr int brev_c(int i, int bits) {
+    int r = 0;
+    for (int b = 0; b < bits; ++b)
+        if (i & (1 << b)) r |= 1 << (bits - 1 - b);
+    return r;
+}
+
+template <int DIR, int R, int LEN, class C>
+__device__ __forceinline__ void dit_stages(C* a) {
+    if constexpr (LEN <= R) {
+        [&]<int... S>(std::integer_sequence<int, S...>) {
+            (
+                [&] {
+                    constexpr int s0 = S * LEN;
+                    [&]<int... J>(std::integer_sequence<int, J...>) {
+                        (
+                            [&] {
+                                C u = a[s0 + J];
+                                C v = twq<DIR, J*(32 / LEN)>(a[s0 + J + LEN / 2]);
+                                a[s0 + J] = cadd(u, v);
+                                a[s0 + J + LEN / 2] = csub(u, v);
+                            }(),
+                            ...);
+                    }(std::make_integer_sequence<int, LEN / 2>{});
+                }(),
+                ...);
+        }(std::make_integer_sequence<int, R / LEN>{});
+        dit_stages<DIR, R, LEN * 2>(a);
+    }
+}
+
+// In-register DFT of R (power of two, <= 32) points, natural order in and out.
+// DIR = -1: forward exp(-2 pi i nk/R); DIR = +1: unnormalised inverse.
+template <int DIR, int R, class C>
+__device__ __forceinline__ void dft_reg(C* a) {
+    static_assert(R >= 1 && R <= 32 && is_pow2_c(R), "radix");
+    if constexpr (R > 1) {
+        constexpr int bits = ilog2_c(R);
+        [&]<int... I>(std::integer_sequence<int, I...>) {
+            (
+                [&] {
+                    constexpr int j = brev_c(I, bits);
+                    if constexpr (j > I) {
+                        C tmp = a[I];
+                        a[I] = a[j];
+                        a[j] = tmp;
+                    }
+                }(),
+                ...);
+        }(std::make_integer_sequence<int, R>{});
+        dit_stages<DIR, R, 2>(a);
+    }
+}
+
+// ---- shared-memory exchangers ---------------------------------------------------------------
+
+// Column passes: smem tile [row i][column b], one padding row every E rows.
+template <class T, int E>
+struct XchCol {
+    cplx<T>* s;   // already offset by the thread's column b
+    int B;
+    __device__ __forceinline__ static int row(int i) { return i + i / E; }
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+    __device__ __forceinline__ void st(int i, cplx<T> v) const { s[row(i) * B] = v; }
+    __device__ __forceinline__ cplx<T> ld(int i) const { return s[row(i) * B]; }
+};
+
+// Row passes: one padded line per row; element i lives at i + i/E.
+template <class T, int E>
+struct XchRow {
+    cplx<T>* s;
+    __device__ __forceinline__ static int pos(int i) { return i + i / E; }
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+    __device__ __forceinline__ void st(int i, cplx<T> v) const { s[pos(i)] = v; }
+    __device__ __forceinline__ cplx<T> ld(int i) const { return s[pos(i)]; }
+};
+
+// ---- Stockham radix-E passes over a line of L points held as v[m] = x[t + T*m] ---------------
+// Stage radices are E, E, ..., E, L/E^k (remainder last so stage 1 writes have stride E, the
+// pattern the padding is built for).  Twiddles W_L^q = tw[q * twstride] (tw = W_LMAX table).
+template <class T, int L, int E, int NS, int DIR, class X>
+__device__ __forceinline__ void stockham(cplx<T> (&v)[E], int t, const cplx<T>* __restrict__ tw,
+                                         int twstride, const X& xch) {
+    constexpr int R = (L / NS >= E) ? E : (L / NS);
+    constexpr int NB = E / R;
+    constexpr int TT = L / E;
+    static_assert(R >= 2 && L % (NS * R) == 0, "stage");
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        cplx<T> a[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) a[r] = v[i + r * NB];
+        if constexpr (NS > 1) {
+            const int j = t + TT * i;
+            const int k = j & (NS - 1);
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                const cplx<T> w = tw[(r * k * (L / (NS * R))) * twstride];
+                a[r] = DIR < 0 ? cmul(a[r], w) : cmulc(a[r], w);
+            }
+        }
+        dft_reg<DIR, R>(a);
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[i + r * NB] = a[r];
+    }
+    if constexpr (NS * R < L) {
+        xch.sync();
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const int j = t + TT * i;
+            const int base = (j / NS) * NS * R + (j & (NS - 1));
+#pragma unroll
+            for (int r = 0; r < R; ++r) xch.st(base + r * NS, v[i + r * NB]);
+        }
+        xch.sync();
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = xch.ld(t + TT * m);
+        stockham<T, L, E, NS * R, DIR>(v, t, tw, twstride, xch);
+    }
+}
+
+// ---- hooks ------------------------------------------------------------------------------------
+// pre(v, off, c): on a loaded element before the transform; post(v, off, c): on a transformed
+// element before the store (off = element offset in the half-spectrum layout, c = k2 column).
+// finish(): once per CTA after all stores (block-level reductions); must be CTA-uniform.
+struct HookNone {
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    template <class C> __device__ __forceinline__ void post(C&, long long, int) {}
+    __device__ __forceinline__ void finish() {}
+};
+
+// ---- column pass: L-point c2c along a strided axis of the half spectrum -------------------------
+// Tile = L rows x B consecutive columns (columns = k2 < ncols inside one plane).
+// Launched with blockDim.x = (L/E) * B threads and (L + L/E) * B elements of dynamic smem.
+template <class T, int L, int E, int DIR, class Hook>
+__global__ void __launch_bounds__(512)
+    k_col(const cplx<T>* __restrict__ src, cplx<T>* __restrict__ dst, long long row_stride,
+          long long plane_stride, int ncols, int B, const cplx<T>* __restrict__ tw, int twstride,
+          const int* gate, Hook hook) {
+    if (gated(gate)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw);
+    constexpr int TT = L / E;
+    const int b = threadIdx.x % B;
+    const int t = threadIdx.x / B;
+    const int c = blockIdx.x * B + b;
+    const bool valid = c < ncols;
+    const long long base = static_cast<long long>(blockIdx.y) * plane_stride + c;
+    cplx<T> v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const long long off = base + static_cast<long long>(t + TT * m) * row_stride;
+        if (valid) {
+            v[m] = src[off];
+            hook.pre(v[m], off, c);
+        } else {
+            v[m] = mkc<T>(T(0), T(0));
+        }
+    }
+    stockham<T, L, E, 1, DIR>(v, t, tw, twstride, XchCol<T, E>{s + b, B});
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const long long off = base + static_cast<long long>(t + TT * m) * row_stride;
+        if (valid) {
+            hook.post(v[m], off, c);
+            dst[off] = v[m];
+        }
+    }
+    hook.finish();
+}
+
+template <class T, int L, int E>
+constexpr size_t col_smem_bytes(int B) {
+    return static_cast<size_t>(L + L / E) * B * sizeof(cplx<T>);
+}
+
+// ---- row passes: last (contiguous) axis, n2 = 2M real <-> M+1 complex ---------------------------
+// The n2 reals of a row are read as M complex z[j] = x[2j] + i x[2j+1]; an M-point FFT plus the
+// split/merge with W_{2M}^k gives X[0..M] (classic packed real FFT).
+
+template <int M, int E>
+constexpr int row_smem_elems() { return M + M / E + 2; }
+
+// Split Z (in smem, natural order at XchRow positions) into X[k] = Ze + W_{2M}^k Zo.
+template <class T, int M, int E>
+__device__ __forceinline__ cplx<T> r2c_split(const cplx<T>* s, int k, const cplx<T>* __restrict__ tw,
+                                             int twstride2) {
+    using X = XchRow<T, E>;
+    const cplx<T> zk = s[X::pos(k)];
+    const cplx<T> zn = s[X::pos((M - k) & (M - 1))];
+    const T h = T(0.5);
+    cplx<T> ze = mkc<T>((zk.x + zn.x) * h, (zk.y - zn.y) * h);
+    cplx<T> zo = mkc<T>((zk.y + zn.y) * h, (zn.x - zk.x) * h);
+    const cplx<T> w = tw[k * twstride2];
+    return cadd(ze, cmul(zo, w));
+}
+
+// Merge X[k], X[M-k] (smem) into Z[k] = (X_k + conj X_{M-k}) + i (X_k - conj X_{M-k}) W^{-k};
+// imaginary parts of X[0] and X[M] are dropped (= Re of the full c2c inverse).
+template <class T, int M, int E>
+__device__ __forceinline__ cplx<T> c2r_merge(const cplx<T>* s, int k, const cplx<T>* __restrict__ tw,
+                                             int twstride2) {
+    using X = XchRow<T, E>;
+    cplx<T> a = s[X::pos(k)];
+    cplx<T> b = s[X::pos(M - k)];
+    if (k == 0) {
+        a.y = T(0);
+        b.y = T(0);
+    }
+    const cplx<T> ze = mkc<T>(a.x + b.x, a.y - b.y);
+    const cplx<T> d = mkc<T>(a.x - b.x, a.y + b.y);
+    const cplx<T> w = tw[k * twstride2];
+    const cplx<T> zo = cmulc(d, w);
+    return mkc<T>(ze.x - zo.y, ze.y + zo.x);
+}
+
+// Real-output hook for C2R rows: post_real(x0, x1, n) gets the two scaled reals of sample pair
+// (n, n+1) and may modify them before the store.
+struct RealHookNone {
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    template <class T> __device__ __forceinline__ void post_real(T&, T&, long long) {}
+    __device__ __forceinline__ void finish() {}
+};
+
+// Plain R2C of rows (FP32 or FP64 real input of the same type).
+// Launched with blockDim.x = (M/E) * rows-per-CTA threads, row_smem_elems() per row of smem.
+template <class T, int M, int E, class Hook>
+__global__ void __launch_bounds__(512)
+    k_row_r2c(const T* __restrict__ in, long long in_stride, cplx<T>* __restrict__ out,
+              long long out_stride, long long nrows, const cplx<T>* __restrict__ tw, int twstride,
+              int twstride2, const int* gate, Hook hook) {
+    if (gated(gate)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int TT = M / E;
+    const int t = threadIdx.x % TT;
+    const int rb = threadIdx.x / TT;
+    const long long row = static_cast<long long>(blockIdx.x) * (blockDim.x / TT) + rb;
+    const bool valid = row < nrows;
+    cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
+    const cplx<T>* src = reinterpret_cast<const cplx<T>*>(in + (valid ? row : 0) * in_stride);
+    cplx<T> v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = valid ? src[t + TT * m] : mkc<T>(T(0), T(0));
+    const XchRow<T, E> x{s};
+    stockham<T, M, E, 1, -1>(v, t, tw, twstride, x);
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < E; ++m) x.st(t + TT * m, v[m]);
+    __syncthreads();
+    if (valid) {
+        cplx<T>* dst = out + row * out_stride;
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int k = t + TT * m;
+            cplx<T> X = r2c_split<T, M, E>(s, k, tw, twstride2);
+            hook.post(X, row * out_stride + k, k);
+            dst[k] = X;
+        }
+        if (t == 0) {
+            const cplx<T> z0 = s[0];
+            cplx<T> X = mkc<T>(z0.x - z0.y, T(0));
+            hook.post(X, row * out_stride + M, M);
+            dst[M] = X;
+        }
+    }
+    hook.finish();
+}
+
+// Plain C2R of rows: out = scale * (unnormalised inverse along the last axis).
+// Launched with blockDim.x = (M/E) * rows-per-CTA threads, row_smem_elems() per row of smem.
+template <class T, int M, int E, class Hook>
+__global__ void __launch_bounds__(512)
+    k_row_c2r(const cplx<T>* __restrict__ in, long long in_stride, T* __restrict__ out,
+              long long out_stride, long long nrows, const cplx<T>* __restrict__ tw, int twstride,
+              int twstride2, T scale, const int* gate, Hook hook) {
+    if (gated(gate)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int TT = M / E;
+    const int t = threadIdx.x % TT;
+    const int rb = threadIdx.x / TT;
+    const long long row = static_cast<long long>(blockIdx.x) * (blockDim.x / TT) + rb;
+    const bool valid = row < nrows;
+    cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
+    const XchRow<T, E> x{s};
+    const cplx<T>* src = in + (valid ? row : 0) * in_stride;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int k = t + TT * m;
+        cplx<T> X = valid ? src[k] : mkc<T>(T(0), T(0));
+        hook.pre(X, row * in_stride + k, k);
+        x.st(k, X);
+    }
+    if (t == 0) {
+        cplx<T> X = valid ? src[M] : mkc<T>(T(0), T(0));
+        hook.pre(X, row * in_stride + M, M);
+        x.st(M, X);
+    }
+    __syncthreads();
+    cplx<T> v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = c2r_merge<T, M, E>(s, t + TT * m, tw, twstride2);
+    stockham<T, M, E, 1, +1>(v, t, tw, twstride, x);
+    if (valid) {
+        cplx<T>* dst = reinterpret_cast<cplx<T>*>(out + row * out_stride);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int j = t + TT * m;
+            T x0 = v[m].x * scale, x1 = v[m].y * scale;
+            hook.post_real(x0, x1, row * out_stride + 2 * j);
+            dst[j] = mkc<T>(x0, x1);
+        }
+    }
+    hook.finish();
+}
+
+// Fused last-axis pass of the projection loop: C2R -> (scale, s-cube clip via hook) -> R2C,
+// in place on the half spectrum.  The real epsilon never round-trips HBM except for the hook's
+// own write.
+// Launched with blockDim.x = (M/E) * rows-per-CTA threads, row_smem_elems() per row of smem.
+template <class T, int M, int E, class Hook>
+__global__ void __launch_bounds__(512)
+    k_row_c2r_r2c(cplx<T>* data, long long stride, long long nrows, long long real_stride,
+                  const cplx<T>* __restrict__ tw, int twstride, int twstride2, T scale,
+                  const int* gate, Hook hook) {
+    if (gated(gate)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int TT = M / E;
+    const int t = threadIdx.x % TT;
+    const int rb = threadIdx.x / TT;
+    const long long row = static_cast<long long>(blockIdx.x) * (blockDim.x / TT) + rb;
+    const bool valid = row < nrows;
+    cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
+    const XchRow<T, E> x{s};
+    cplx<T>* rowp = data + (valid ? row : 0) * stride;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int k = t + TT * m;
+        x.st(k, valid ? rowp[k] : mkc<T>(T(0), T(0)));
+    }
+    if (t == 0) x.st(M, valid ? rowp[M] : mkc<T>(T(0), T(0)));
+    __syncthreads();
+    cplx<T> v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = c2r_merge<T, M, E>(s, t + TT * m, tw, twstride2);
+    stockham<T, M, E, 1, +1>(v, t, tw, twstride, x);
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int j = t + TT * m;
+        T x0 = v[m].x * scale, x1 = v[m].y * scale;
+        if (valid) hook.post_real(x0, x1, row * real_stride + 2 * j);
+        v[m] = mkc<T>(x0, x1);
+    }
+    stockham<T, M, E, 1, -1>(v, t, tw, twstride, x);
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < E; ++m) x.st(t + TT * m, v[m]);
+    __syncthreads();
+    if (valid) {
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int k = t + TT * m;
+            rowp[k] = r2c_split<T, M, E>(s, k, tw, twstride2);
+        }
+        if (t == 0) {
+            const cplx<T> z0 = s[0];
+            rowp[M] = mkc<T>(z0.x - z0.y, T(0));
+        }
+    }
+    hook.finish();
+}
+
+template <class T, int M, int E>
+constexpr size_t row_smem_bytes(int rows) {
+    return static_cast<size_t>(row_smem_elems<M, E>()) * rows * sizeof(cplx<T>);
+}
+
+// ---- direct DFT passes for non-power-of-two or tiny extents (test shapes) ----------------------
+// O(L) per output with an exact (n*k mod L) twiddle index into a per-L FP64-derived table.
+
+template <class T>
+__global__ void k_col_direct(const cplx<T>* __restrict__ src, cplx<T>* __restrict__ dst, int L,
+                             long long row_stride, long long plane_stride, int ncols, int B,
+                             const cplx<T>* __restrict__ wl, int dir, const int* gate) {
+    if (gated(gate)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw);
+    const long long base = static_cast<long long>(blockIdx.y) * plane_stride + blockIdx.x * B;
+    for (int e = threadIdx.x; e < L * B; e += blockDim.x) {
+        const int i = e / B, b = e % B;
+        s[e] = (blockIdx.x * B + b < ncols) ? src[base + i * row_stride + b] : mkc<T>(T(0), T(0));
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < L * B; e += blockDim.x) {
+        const int k = e / B, b = e % B;
+        if (blockIdx.x * B + b >= ncols) continue;
+        T ax = 0, ay = 0;
+        long long q = 0;
+        for (int n = 0; n < L; ++n) {
+            const cplx<T> w = wl[q];
+            const cplx<T> xv = s[n * B + b];
+            const cplx<T> p = dir < 0 ? cmul(xv, w) : cmulc(xv, w);
+            ax += p.x;
+            ay += p.y;
+            q += k;
+            if (q >= L) q -= L;
+        }
+        dst[base + static_cast<long long>(k) * row_stride + b] = mkc<T>(ax, ay);
+    }
+}
+
+template <class T>
+__global__ void k_row_r2c_direct(const T* __restrict__ in, long long in_stride,
+                                 cplx<T>* __restrict__ out, long long out_stride, int n2,
+                                 const cplx<T>* __restrict__ wl, const int* gate) {
+    if (gated(gate)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* s = reinterpret_cast<T*>(smem_raw);
+    const long long row = blockIdx.x;
+    for (int n = threadIdx.x; n < n2; n += blockDim.x) s[n] = in[row * in_stride + n];
+    __syncthreads();
+    for (int k = threadIdx.x; k <= n2 / 2; k += blockDim.x) {
+        T ax = 0, ay = 0;
+        long long q = 0;
+        for (int n = 0; n < n2; ++n) {
+            const cplx<T> w = wl[q];
+            ax += s[n] * w.x;
+            ay += s[n] * w.y;
+            q += k;
+            if (q >= n2) q -= n2;
+        }
+        out[row * out_stride + k] = mkc<T>(ax, ay);
+    }
+}
+
+template <class T>
+__global__ void k_row_c2r_direct(const cplx<T>* __restrict__ in, long long in_stride,
+                                 T* __restrict__ out, long long out_stride, int n2,
+                                 const cplx<T>* __restrict__ wl, T scale, const int* gate) {
+    if (gated(gate)) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw);
+    const long long row = blockIdx.x;
+    const int h = n2 / 2 + 1;
+    for (int k = threadIdx.x; k < h; k += blockDim.x) s[k] = in[row * in_stride + k];
+    __syncthreads();
+    const int kmax = (n2 - 1) / 2; // k with a distinct mirror partner
+    for (int n = threadIdx.x; n < n2; n += blockDim.x) {
+        T acc = s[0].x;
+        long long q = n;
+        for (int k = 1; k <= kmax; ++k) {
+            const cplx<T> w = wl[q];  // exp(-2 pi i n k / n2)
+            const cplx<T> p = cmulc(s[k], w);
+            acc += T(2) * p.x;
+            q += n;
+            if (q >= n2) q -= n2;
+        }
+        if ((n2 & 1) == 0) acc += (n & 1) ? -s[n2 / 2].x : s[n2 / 2].x;
+        out[row * out_stride + n] = acc * scale;
+    }
+}
+
+} // namespace ffcz_gpu

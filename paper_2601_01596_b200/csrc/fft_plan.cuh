@@ -1,0 +1,108 @@
+// Host-side pass planning and launch dispatch for the FFT engine.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "fft_engine.cuh"
+#include "kernels.cuh"
+
+namespace ffcz_gpu {
+
+constexpr int kLmax = 8192;   // largest pow2 row length n2 / column length handled by the radix path
+// elements per thread (= radix of the full Stockham stages): 16 complex FP32 / 8 complex FP64
+// keeps the line in <= 64 registers so 512-thread CTAs run without spills
+template <class T> constexpr int kRadixE = sizeof(T) == 8 ? 8 : 16;
+
+// Geometry of a field and its pitched half spectrum.
+struct Geometry {
+    int ndim = 0;
+    long long d[3] = {1, 1, 1};  // dims padded to 3-D at the FRONT: (d0, d1, d2), d2 = last axis
+    long long N = 0;             // samples
+    long long rows = 0;          // d0 * d1
+    long long n2 = 0;            // last axis
+    int H = 0;                   // n2/2 + 1
+    int P = 0;                   // pitch in complex elements
+    long long half_elems() const { return rows * P; }
+    long long Nc() const { return rows * H; }
+    HalfGeom hg() const { return HalfGeom{rows, H, P, n2}; }
+};
+
+Geometry make_geometry(int ndim, const uint64_t* dims, int pitch_align);
+
+// Twiddle tables, FP64-derived (long double on the host, rounded once).
+template <class T>
+struct Twiddles {
+    cplx<T>* W = nullptr;                       // W[q] = exp(-2 pi i q / kLmax), q < kLmax
+    std::map<long long, cplx<T>*> direct;      // per-L tables for the direct (non-2^k) passes
+    std::mutex mu;
+    const cplx<T>* table_for(long long L);     // W_L, length L
+    void init();
+    ~Twiddles();
+};
+
+inline bool radix_col_ok(long long L) { return is_pow2(L) && L >= 16 && L <= 4096; }
+inline bool radix_row_ok(long long n2) { return is_pow2(n2) && n2 >= 32 && n2 <= kLmax; }
+
+// ---- launchers (fft_dispatch*.cu) -----------------------------------------------------------------
+// Column pass along an axis of the half spectrum.  dir = -1 forward, +1 inverse.
+template <class T, class Hook>
+void launch_col(long long L, int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
+                long long plane_stride, long long nplanes, int ncols, Twiddles<T>& tw,
+                const int* gate, Hook hook, cudaStream_t st);
+// Row R2C: real rows (stride in_stride) -> half rows (stride out_stride).
+template <class T>
+void launch_row_r2c(long long n2, const T* in, long long in_stride, cplx<T>* out,
+                    long long out_stride, long long nrows, Twiddles<T>& tw, const int* gate,
+                    cudaStream_t st);
+// Row C2R: half rows -> real rows, scaled.
+template <class T>
+void launch_row_c2r(long long n2, const cplx<T>* in, long long in_stride, T* out,
+                    long long out_stride, long long nrows, T scale, Twiddles<T>& tw,
+                    const int* gate, cudaStream_t st);
+// Fused C2R -> hook(real) -> R2C, in place on the half rows (radix path only).
+template <class T, class Hook>
+void launch_row_fused(long long n2, cplx<T>* data, long long stride, long long nrows,
+                      long long real_stride, T scale, Twiddles<T>& tw, const int* gate, Hook hook,
+                      cudaStream_t st);
+
+// Whole-field transforms built from the passes.
+template <class T>
+struct FftPlan {
+    Geometry g;
+    Twiddles<T>* tw;
+    // x (N reals) -> half (pitched)
+    void r2c(const T* x, cplx<T>* half, const int* gate, cudaStream_t st) const;
+    // half (pitched, preserved if work != half) -> x (N reals) * scale; work is clobbered
+    void c2r(const cplx<T>* half, cplx<T>* work, T* x, T scale, const int* gate,
+             cudaStream_t st) const;
+    // single column pass along field axis `axis` (< ndim-1 in the padded 3-D frame)
+    template <class Hook>
+    void col(int axis3, int dir, const cplx<T>* src, cplx<T>* dst, const int* gate, Hook hook,
+             cudaStream_t st) const {
+        const long long L = g.d[axis3];
+        if (L == 1) {
+            if (src != dst)
+                FFCZ_CUDA_CHECK(cudaMemcpyAsync(dst, src, sizeof(cplx<T>) * g.half_elems(),
+                                                cudaMemcpyDeviceToDevice, st));
+            return;
+        }
+        long long row_stride, plane_stride, nplanes;
+        if (axis3 == 1) {  // rows inside a d1 x P plane, planes = d0
+            row_stride = g.P;
+            plane_stride = g.d[1] * g.P;
+            nplanes = g.d[0];
+        } else {           // axis 0: rows stride d1*P, planes = d1
+            row_stride = g.d[1] * g.P;
+            plane_stride = g.P;
+            nplanes = g.d[1];
+        }
+        launch_col<T, Hook>(L, dir, src, dst, row_stride, plane_stride, nplanes, g.H, *tw, gate,
+                            hook, st);
+    }
+    bool fused_ok() const;
+};
+
+} // namespace ffcz_gpu

@@ -1,0 +1,519 @@
+// Elementwise / reduction / gate kernels of the FFCz B200 engine.  See kernels.cuh for the
+// reference function each one restates.
+#include "kernels.cuh"
+
+namespace ffcz_gpu {
+
+namespace {
+
+__device__ __forceinline__ int plane_weight(int k2, long long n2) {
+    // number of FULL-spectrum entries a half entry stands for (weight 1 on the self-mirror planes)
+    return (k2 == 0 || 2LL * k2 == n2) ? 1 : 2;
+}
+
+__device__ __forceinline__ void set_bit(unsigned* words, long long i) {
+    atomicOr(&words[i >> 5], 1u << (i & 31));
+}
+
+} // namespace
+
+__global__ void k_freduce(const double2* __restrict__ spec, HalfGeom g, FreqB fb, double fscale,
+                          Ctl* ctl, const int* gate) {
+    if (gated(gate)) return;
+    HookFReduce h{fb, fscale, ctl};
+    const long long total = g.rows * g.H;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / g.H;
+        const int k2 = static_cast<int>(i - row * g.H);
+        const long long off = row * g.P + k2;
+        double2 v = spec[off];
+        h.post(v, off, k2);
+    }
+    h.finish();
+}
+
+__global__ void k_fclip(double2* spec, HalfGeom g, FreqB fb, double fscale, double2* F,
+                        const int* gate) {
+    if (gated(gate)) return;
+    HookFClip<double> h{fb, fscale, F};
+    const long long total = g.rows * g.H;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / g.H;
+        const int k2 = static_cast<int>(i - row * g.H);
+        const long long off = row * g.P + k2;
+        double2 v = spec[off];
+        h.pre(v, off, k2);
+        spec[off] = v;
+    }
+}
+
+__global__ void k_sclip(const double* __restrict__ x, double* eps, long long N, SpatialB sb,
+                        double fscale, double* S, const int* gate) {
+    if (gated(gate)) return;
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
+         n += (long long)gridDim.x * blockDim.x) {
+        const double xd = x[n];
+        const double e = sb.at(n) * fscale;
+        const double c = clamp_abs(xd, e);
+        const double d = c - xd;
+        if (d != 0.0) S[n] += d;
+        eps[n] = c;
+    }
+}
+
+template <class TI>
+__global__ void k_eps0(const TI* __restrict__ orig, const TI* __restrict__ dec, double* eps,
+                       long long N, SpatialB sb, double fscale, double slack, int check_original,
+                       Ctl* ctl) {
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
+         n += (long long)gridDim.x * blockDim.x) {
+        const double e = static_cast<double>(dec[n]) - static_cast<double>(orig[n]);
+        eps[n] = e;
+        const double E = sb.at(n);
+        if (check_original && fabs(e) > E * (1.0 + 0x1p-20))
+            atomicMin(&ctl->bad1, static_cast<unsigned long long>(n));
+        const double Ew = E * fscale;
+        if (fabs(e) > Ew * (1.0 + slack)) atomicMin(&ctl->bad2, static_cast<unsigned long long>(n));
+    }
+}
+template __global__ void k_eps0<float>(const float*, const float*, double*, long long, SpatialB,
+                                       double, double, int, Ctl*);
+template __global__ void k_eps0<double>(const double*, const double*, double*, long long,
+                                        SpatialB, double, double, int, Ctl*);
+
+__global__ void k_cast_to_double(const float* __restrict__ in, double* out, long long N) {
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
+         n += (long long)gridDim.x * blockDim.x)
+        out[n] = in[n];
+}
+
+__global__ void k_decide(Ctl* ctl) {
+    if (ctl->done) return;
+    const double peak = bitsd(ctl->peak_bits);
+    const double ex = bitsd(ctl->exc_bits);
+    const double tol = 1e-11 * peak;  // projection.cpp:40
+    if (!(ex > tol)) {
+        ctl->converged = 1;
+        ctl->residual_f = 0.0;
+        ctl->done = 1;
+    } else if (ctl->passes >= ctl->max_iters) {
+        ctl->converged = 0;
+        ctl->residual_f = ex;
+        ctl->done = 1;
+    } else {
+        ctl->passes += 1;
+    }
+    ctl->peak_bits = 0;
+    ctl->exc_bits = 0;
+}
+
+__global__ void k_ctl_init(Ctl* ctl, unsigned long long max_iters) {
+    Ctl c{};
+    c.max_iters = max_iters;
+    c.bad1 = ~0ull;
+    c.bad2 = ~0ull;
+    *ctl = c;
+}
+
+__global__ void k_residual_s(const double* __restrict__ eps, long long N, SpatialB sb,
+                             double fscale, Ctl* ctl) {
+    double m = 0.0;
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
+         n += (long long)gridDim.x * blockDim.x) {
+        const double ex = fabs(eps[n]) - sb.at(n) * fscale;
+        if (ex > m) m = ex;
+    }
+    block_max2_atomic(m, 0.0, &ctl->res_s_bits, nullptr);
+}
+
+__global__ void k_count_spatial(const double* __restrict__ S, long long N, Ctl* ctl) {
+    unsigned long long c = 0;
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
+         n += (long long)gridDim.x * blockDim.x)
+        c += S[n] != 0.0;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ctl->act_s, c);
+}
+
+__global__ void k_count_freq(const double2* __restrict__ F, HalfGeom g, Ctl* ctl) {
+    unsigned long long c = 0;
+    const long long total = g.rows * g.H;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / g.H;
+        const int k2 = static_cast<int>(i - row * g.H);
+        const double2 v = F[row * g.P + k2];
+        if (v.x != 0.0 || v.y != 0.0) c += plane_weight(k2, g.n2);
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ctl->act_f, c);
+}
+
+__global__ void k_gather_half(const double* __restrict__ full, double* half, HalfGeom g) {
+    const long long total = g.rows * g.H;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / g.H;
+        const int k2 = static_cast<int>(i - row * g.H);
+        half[row * g.P + k2] = full[row * g.n2 + k2];
+    }
+}
+
+__global__ void k_expand_full(const double2* __restrict__ half, double2* full, int ndim,
+                              long long d0, long long d1, long long d2, int P) {
+    // dims padded to 3-D: (d0, d1, d2) with d2 the last axis
+    const long long total = d0 * d1 * d2;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < total;
+         k += (long long)gridDim.x * blockDim.x) {
+        const long long k2 = k % d2;
+        const long long r = k / d2;
+        const long long k1 = r % d1, k0 = r / d1;
+        if (2 * k2 <= d2) {
+            full[k] = half[r * P + k2];
+        } else {
+            const long long m0 = k0 ? d0 - k0 : 0, m1 = k1 ? d1 - k1 : 0;
+            double2 v = half[(m0 * d1 + m1) * P + (d2 - k2)];
+            v.y = -v.y;
+            full[k] = v;
+        }
+    }
+    (void)ndim;
+}
+
+// ---- FP64 gate ---------------------------------------------------------------------------------
+
+__global__ void k_gate_spatial(const double* __restrict__ S, long long N, SpatialB sb, int m,
+                               double* spat_cur, unsigned* keep_words, unsigned* esc_words,
+                               Ctl* ctl) {
+    const long long n0 = blockIdx.x * (long long)blockDim.x;
+    for (long long base = n0; base < N; base += (long long)gridDim.x * blockDim.x) {
+        const long long n = base + threadIdx.x;
+        bool keep = false, ovf = false;
+        if (n < N) {
+            const double v = S[n];
+            const bool nz = v != 0.0;
+            const double step = ldexp(2.0 * sb.at(n), -m);       // editset.cpp:31-33
+            ovf = nz && (fabs(v) / step > kMaxIndex);            // pipeline.cpp:63-64
+            keep = nz && !ovf;
+            double cur = 0.0;
+            if (keep) {
+                const long long q = llround(v / step);           // editset.cpp:76-84
+                cur = static_cast<double>(static_cast<int>(q)) * step;  // editset.cpp:102
+            } else if (ovf) {
+                cur = v;
+            }
+            spat_cur[n] = cur;
+        }
+        const unsigned bk = __ballot_sync(0xffffffffu, keep);
+        const unsigned be = __ballot_sync(0xffffffffu, ovf);
+        if ((threadIdx.x & 31) == 0 && n < N) {
+            keep_words[n >> 5] = bk;
+            esc_words[n >> 5] = be;
+        }
+        const unsigned long long nz_w = __popc(bk) + __popc(be);
+        if ((threadIdx.x & 31) == 0 && nz_w) atomicAdd(&ctl->act_s, nz_w);
+    }
+}
+
+__global__ void k_gate_freq(const double2* __restrict__ F, HalfGeom g, FreqB fb, int m,
+                            double2* freq_cur, unsigned* keep_words, unsigned* esc_words,
+                            Ctl* ctl) {
+    const long long total = g.rows * g.H;
+    for (long long base = blockIdx.x * (long long)blockDim.x; base < total;
+         base += (long long)gridDim.x * blockDim.x) {
+        const long long h = base + threadIdx.x;
+        bool keep = false, ovf = false;
+        int w = 0;
+        if (h < total) {
+            const long long row = h / g.H;
+            const int k2 = static_cast<int>(h - row * g.H);
+            const long long off = row * g.P + k2;
+            const double2 v = F[off];
+            const bool nz = v.x != 0.0 || v.y != 0.0;
+            const double sre = ldexp(2.0 * fb.re_at(off), -m);   // editset.cpp:35-41
+            const double sim = ldexp(2.0 * fb.im_at(off), -m);
+            ovf = nz && (fabs(v.x) / sre > kMaxIndex || fabs(v.y) / sim > kMaxIndex);  // :68-69
+            keep = nz && !ovf;
+            double2 cur = make_double2(0.0, 0.0);
+            if (keep) {
+                cur.x = static_cast<double>(static_cast<int>(llround(v.x / sre))) * sre;
+                cur.y = static_cast<double>(static_cast<int>(llround(v.y / sim))) * sim;
+            } else if (ovf) {
+                cur = v;
+            }
+            freq_cur[off] = cur;
+            if (nz) w = plane_weight(k2, g.n2);
+        }
+        const unsigned bk = __ballot_sync(0xffffffffu, keep);
+        const unsigned be = __ballot_sync(0xffffffffu, ovf);
+        if ((threadIdx.x & 31) == 0 && h < total) {
+            keep_words[h >> 5] = bk;
+            esc_words[h >> 5] = be;
+        }
+        unsigned long long c = w;
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ctl->act_f, c);
+    }
+}
+
+__global__ void k_popc_blocks(const unsigned* __restrict__ words, long long nwords,
+                              unsigned long long* block_counts) {
+    __shared__ unsigned long long s[32];
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    unsigned long long c = i < nwords ? __popc(words[i]) : 0;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+        block_counts[blockIdx.x] = t;
+    }
+}
+
+// single-CTA exclusive scan (in place) with running carry; *total = sum
+__global__ void k_scan_blocks(unsigned long long* counts, long long nblocks,
+                              unsigned long long* total) {
+    __shared__ unsigned long long s[1024];
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (long long base = 0; base < nblocks; base += blockDim.x) {
+        const long long i = base + threadIdx.x;
+        const unsigned long long v = i < nblocks ? counts[i] : 0;
+        s[threadIdx.x] = v;
+        __syncthreads();
+        for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+            const unsigned long long a = threadIdx.x >= (unsigned)o ? s[threadIdx.x - o] : 0;
+            __syncthreads();
+            s[threadIdx.x] += a;
+            __syncthreads();
+        }
+        if (i < nblocks) counts[i] = carry + s[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += s[threadIdx.x];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void k_compact(const unsigned* __restrict__ words, long long nwords,
+                          const unsigned long long* __restrict__ block_offsets,
+                          unsigned long long* out_idx) {
+    __shared__ unsigned s[1024];
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const unsigned w = i < nwords ? words[i] : 0u;
+    const unsigned c = __popc(w);
+    s[threadIdx.x] = c;
+    __syncthreads();
+    for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+        const unsigned a = threadIdx.x >= (unsigned)o ? s[threadIdx.x - o] : 0u;
+        __syncthreads();
+        s[threadIdx.x] += a;
+        __syncthreads();
+    }
+    unsigned long long pos = block_offsets[blockIdx.x] + s[threadIdx.x] - c;
+    unsigned rem = w;
+    while (rem) {
+        const int b = __ffs(rem) - 1;
+        rem &= rem - 1;
+        out_idx[pos++] = static_cast<unsigned long long>(i) * 32 + b;
+    }
+}
+
+__global__ void k_codes_spatial(const unsigned long long* __restrict__ idx, long long n,
+                                const double* __restrict__ S, SpatialB sb, int m, int* codes) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long k = idx[i];
+        const double step = ldexp(2.0 * sb.at(k), -m);
+        codes[i] = static_cast<int>(llround(S[k] / step));
+    }
+}
+
+__global__ void k_codes_freq(const unsigned long long* __restrict__ idx, long long n,
+                             const double2* __restrict__ F, HalfGeom g, FreqB fb, int m,
+                             int* codes) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long h = idx[i];
+        const long long row = h / g.H;
+        const long long off = row * g.P + (h - row * g.H);
+        const double2 v = F[off];
+        const double sre = ldexp(2.0 * fb.re_at(off), -m);
+        const double sim = ldexp(2.0 * fb.im_at(off), -m);
+        codes[2 * i] = static_cast<int>(llround(v.x / sre));
+        codes[2 * i + 1] = static_cast<int>(llround(v.y / sim));
+    }
+}
+
+template <class TI>
+__global__ void k_repair_spatial(const TI* __restrict__ orig, const TI* __restrict__ dec,
+                                 const double* __restrict__ fpart, const double* __restrict__ final_eps,
+                                 long long N, SpatialB sb, double* spat_cur, double* eps_tilde,
+                                 unsigned* esc_words, Ctl* ctl) {
+    bool dirty = false;
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
+         n += (long long)gridDim.x * blockDim.x) {
+        const double e0 = static_cast<double>(dec[n]) - static_cast<double>(orig[n]);
+        const double sc = spat_cur[n];
+        const double et = e0 + sc + fpart[n];                       // pipeline.cpp:134-136
+        eps_tilde[n] = et;
+        if (fabs(et) > sb.at(n)) {                                  // pipeline.cpp:154-160
+            dirty = true;
+            spat_cur[n] = sc + (final_eps[n] - et);
+            set_bit(esc_words, n);
+        }
+    }
+    if (__any_sync(0xffffffffu, dirty) && (threadIdx.x & 31) == 0) ctl->dirty = 1;
+}
+template __global__ void k_repair_spatial<float>(const float*, const float*, const double*,
+                                                 const double*, long long, SpatialB, double*,
+                                                 double*, unsigned*, Ctl*);
+template __global__ void k_repair_spatial<double>(const double*, const double*, const double*,
+                                                  const double*, long long, SpatialB, double*,
+                                                  double*, unsigned*, Ctl*);
+
+__global__ void k_repair_freq(const double2* __restrict__ delta_star,
+                              const double2* __restrict__ delta_tilde, HalfGeom g, int ndim,
+                              long long d0, long long d1, FreqB fb, double2* freq_cur,
+                              unsigned* esc_words, Ctl* ctl) {
+    // pipeline.cpp:140-153; half rows are (k0, k1) of a 3-D grid padded as (d0, d1)
+    bool dirty = false;
+    const long long total = g.rows * g.H;
+    for (long long h = blockIdx.x * (long long)blockDim.x + threadIdx.x; h < total;
+         h += (long long)gridDim.x * blockDim.x) {
+        const long long row = h / g.H;
+        const int k2 = static_cast<int>(h - row * g.H);
+        auto violates = [&](long long r) {
+            const long long off = r * g.P + k2;
+            const double2 d = delta_tilde[off];
+            return fabs(d.x) > fb.re_at(off) || fabs(d.y) > fb.im_at(off);
+        };
+        auto repaired = [&](long long r) {
+            const long long off = r * g.P + k2;
+            const double2 c = freq_cur[off], s = delta_star[off], t = delta_tilde[off];
+            return make_double2(c.x + (s.x - t.x), c.y + (s.y - t.y));
+        };
+        const bool plane = (k2 == 0) || (2LL * k2 == g.n2);
+        long long mrow = row;
+        if (plane) {
+            const long long k1 = row % d1, k0 = row / d1;
+            mrow = (k0 ? d0 - k0 : 0) * d1 + (k1 ? d1 - k1 : 0);
+        }
+        if (mrow == row) {
+            if (violates(row)) {
+                dirty = true;
+                freq_cur[row * g.P + k2] = repaired(row);
+                set_bit(esc_words, h);
+            }
+        } else if (row < mrow) {
+            // the pair (h, hm) is owned by its smaller index; the larger index wins when both
+            // violate, because the reference visits it last (pipeline.cpp:141-152)
+            const long long hm = mrow * g.H + k2;
+            const bool va = violates(row), vb = violates(mrow);
+            if (va || vb) {
+                dirty = true;
+                double2 r = vb ? repaired(mrow) : repaired(row);
+                double2 rc = make_double2(r.x, -r.y);
+                if (vb) {
+                    freq_cur[mrow * g.P + k2] = r;
+                    freq_cur[row * g.P + k2] = rc;
+                } else {
+                    freq_cur[row * g.P + k2] = r;
+                    freq_cur[mrow * g.P + k2] = rc;
+                }
+                set_bit(esc_words, h);
+                set_bit(esc_words, hm);
+            }
+        }
+    }
+    (void)ndim;
+    if (__any_sync(0xffffffffu, dirty) && (threadIdx.x & 31) == 0) ctl->dirty = 1;
+}
+
+template <class TI>
+__global__ void k_verify_spatial(const TI* __restrict__ orig, const TI* __restrict__ dec,
+                                 const double* __restrict__ spat_cur,
+                                 const double* __restrict__ fpart, long long N, SpatialB sb,
+                                 double* corrected, double* eps_v, Ctl* ctl) {
+    double m = 0.0;
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
+         n += (long long)gridDim.x * blockDim.x) {
+        const double c = static_cast<double>(dec[n]) + spat_cur[n] + fpart[n];  // archive.cpp:271
+        corrected[n] = c;
+        const double e = c - static_cast<double>(orig[n]);                      // archive.cpp:284
+        eps_v[n] = e;
+        const double ex = fabs(e) - sb.at(n);
+        if (ex > 0.0 && ex > m) m = ex;                                         // :285-286
+    }
+    block_max2_atomic(m, 0.0, &ctl->vs_bits, nullptr);
+}
+template __global__ void k_verify_spatial<float>(const float*, const float*, const double*,
+                                                 const double*, long long, SpatialB, double*,
+                                                 double*, Ctl*);
+template __global__ void k_verify_spatial<double>(const double*, const double*, const double*,
+                                                  const double*, long long, SpatialB, double*,
+                                                  double*, Ctl*);
+
+__global__ void k_verify_freq(const double2* __restrict__ delta, HalfGeom g, FreqB fb, Ctl* ctl) {
+    double m = 0.0;
+    const long long total = g.rows * g.H;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / g.H;
+        const long long off = row * g.P + (i - row * g.H);
+        const double2 d = delta[off];
+        const double ex = fmax(fabs(d.x) - fb.re_at(off), fabs(d.y) - fb.im_at(off));  // :290-292
+        if (ex > 0.0 && ex > m) m = ex;
+    }
+    block_max2_atomic(m, 0.0, &ctl->vf_bits, nullptr);
+}
+
+__global__ void k_gather_escapes_s(const unsigned long long* __restrict__ idx, long long n,
+                                   const double* __restrict__ spat_cur, double* out_re) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out_re[i] = spat_cur[idx[i]];
+}
+
+__global__ void k_gather_escapes_f(const unsigned long long* __restrict__ idx, long long n,
+                                   const double2* __restrict__ freq_cur, HalfGeom g, double2* out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long h = idx[i];
+        const long long row = h / g.H;
+        out[i] = freq_cur[row * g.P + (h - row * g.H)];
+    }
+}
+
+__global__ void k_split_hermitian(const double2* __restrict__ full, double2* Hh, double2* Ah,
+                                  HalfGeom g, long long d0, long long d1) {
+    // Re(ifft X) = C2R(H), Im(ifft X) = C2R(A) with H = (X + conj X_m)/2, A = (X - conj X_m)/(2i)
+    const long long total = g.rows * g.H;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / g.H;
+        const long long k2 = i - row * g.H;
+        const long long k1 = row % d1, k0 = row / d1;
+        const long long mrow = (k0 ? d0 - k0 : 0) * d1 + (k1 ? d1 - k1 : 0);
+        const long long mk2 = k2 ? g.n2 - k2 : 0;
+        const double2 x = full[row * g.n2 + k2];
+        const double2 xm = full[mrow * g.n2 + mk2];
+        Hh[row * g.P + k2] = make_double2(0.5 * (x.x + xm.x), 0.5 * (x.y - xm.y));
+        const double dx = x.x - xm.x, dy = x.y + xm.y;
+        Ah[row * g.P + k2] = make_double2(0.5 * dy, -0.5 * dx);
+    }
+}
+
+__global__ void k_maxabs(const double* __restrict__ x, long long N, unsigned long long* out) {
+    double m = 0.0;
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
+         n += (long long)gridDim.x * blockDim.x)
+        m = fmax(m, fabs(x[n]));
+    block_max2_atomic(m, 0.0, out, nullptr);
+}
+
+} // namespace ffcz_gpu

@@ -1,0 +1,261 @@
+// Projection-loop hooks, control and FP64-gate kernels (sm_100a).
+//
+// Each device function cites the reference function whose arithmetic it restates; every
+// comparison / clamp / accumulation is the same IEEE-754 double operation in the same order as
+// the reference so that, given the same spectrum values, decisions and flags are identical.
+#pragma once
+
+#include "common.cuh"
+
+namespace ffcz_gpu {
+
+constexpr double kMaxIndex = 2147483520.0;  // pipeline.cpp:57 (overflow escapes)
+
+// ---- bounds ------------------------------------------------------------------------------------
+
+// Spatial bound E(n) (bounds.hpp:11-18): per-point array or one global value.
+struct SpatialB {
+    const double* v;
+    double g;
+    __device__ __forceinline__ double at(long long n) const { return v ? v[n] : g; }
+};
+
+// Frequency bound Delta (bounds.hpp:20-31) restricted to the half spectrum, stored in the
+// pitched half layout (offset = row*P + k2).  Hermitian consistency (bounds.cpp:50-54) makes the
+// half restriction lossless.
+struct FreqB {
+    const double* re;
+    const double* im;
+    double g;
+    __device__ __forceinline__ double re_at(long long off) const { return re ? re[off] : g; }
+    __device__ __forceinline__ double im_at(long long off) const { return im ? im[off] : g; }
+};
+
+// std::clamp(v, -b, b) (projection.cpp:14-16)
+template <class T>
+__device__ __forceinline__ T clamp_abs(T v, T b) {
+    return v < -b ? -b : (b < v ? b : v);
+}
+
+// ---- loop control block ------------------------------------------------------------------------
+
+struct Ctl {
+    unsigned long long peak_bits;  // max(|Re|,|Im|) of the current spectrum (as non-negative double)
+    unsigned long long exc_bits;   // max(excess, 0)
+    unsigned long long passes;
+    unsigned long long max_iters;
+    int done;
+    int converged;
+    double residual_f;
+    unsigned long long bad1, bad2;       // first index failing the correct()/loop preconditions
+    unsigned long long res_s_bits;       // residual_s
+    unsigned long long act_s, act_f;     // active counts (act_f over the FULL spectrum)
+    int dirty;                           // escape repair: a component violated this round
+    int pad0;
+    unsigned long long vs_bits, vf_bits; // verify: max spatial / frequency excess (> 0 only)
+    unsigned long long count_a, count_b; // scratch totals of compactions
+    // mixed policy
+    int phase;                           // 0: FP32 phase, 1: FP64 phase
+    int switch_now;
+    unsigned long long passes32;
+    double tau;
+};
+
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* p, double v) {
+    atomicMax(p, dbits(v));
+}
+
+// Block-wide max of two non-negative doubles, then one atomic per CTA.
+__device__ __forceinline__ void block_max2_atomic(double a, double b, unsigned long long* pa,
+                                                  unsigned long long* pb) {
+    __shared__ double sa[32], sb[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sa[w] = a;
+        sb[w] = b;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        a = l < nw ? sa[l] : 0.0;
+        b = l < nw ? sb[l] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+        if (l == 0) {
+            if (pa && a > 0.0) atomic_max_nonneg(pa, a);
+            if (pb && b > 0.0) atomic_max_nonneg(pb, b);
+        }
+    }
+}
+
+// ---- loop hooks ----------------------------------------------------------------------------------
+
+// check_convergence (projection.cpp:29-52) in one pass: peak = max(|Re|,|Im|) and
+// max_excess = max(max(|Re|-Dre, |Im|-Dim), 0).  "some excess > 1e-11*peak" <=> max_excess > tol,
+// and when violated the reference's max over violators equals the global max.
+struct HookFReduce {
+    FreqB fb;
+    double fscale;  // working = original * (1 - 2^-m) (bounds.cpp:74-85); 1.0 for working input
+    Ctl* ctl;
+    double peak = 0.0, ex = 0.0;
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    template <class C>
+    __device__ __forceinline__ void post(C& v, long long off, int) {
+        const double ar = fabs(static_cast<double>(v.x)), ai = fabs(static_cast<double>(v.y));
+        peak = fmax(peak, fmax(ar, ai));
+        const double e = fmax(ar - fb.re_at(off) * fscale, ai - fb.im_at(off) * fscale);
+        if (e > ex) ex = e;
+    }
+    __device__ __forceinline__ void finish() { block_max2_atomic(peak, ex, &ctl->peak_bits, &ctl->exc_bits); }
+};
+
+// project_onto_fcube + F accumulation (projection.cpp:54-66, 117-119): clamp Re and Im
+// independently; F += clipped - delta (read-modify-write only where the clamp moved the value).
+template <class T>
+struct HookFClip {
+    FreqB fb;
+    double fscale;
+    double2* F;
+    template <class C>
+    __device__ __forceinline__ void pre(C& v, long long off, int) {
+        const double re = v.x, im = v.y;
+        const double dre = fb.re_at(off) * fscale, dim = fb.im_at(off) * fscale;
+        const double cre = clamp_abs(re, dre), cim = clamp_abs(im, dim);
+        const double xre = cre - re, xim = cim - im;
+        if (xre != 0.0 || xim != 0.0) {
+            double2 f = F[off];
+            f.x += xre;
+            f.y += xim;
+            F[off] = f;
+        }
+        v.x = static_cast<T>(cre);
+        v.y = static_cast<T>(cim);
+    }
+    template <class C> __device__ __forceinline__ void post(C&, long long, int) {}
+    __device__ __forceinline__ void finish() {}
+};
+
+// project_onto_scube + S accumulation (projection.cpp:68-79, 121-124) on the real outputs of a
+// C2R row pass; writes the clipped epsilon (the reference's `eps = sc.clipped`).
+template <class T>
+struct HookSClip {
+    SpatialB sb;
+    double fscale;
+    double* S;
+    T* eps;
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    __device__ __forceinline__ T one(T x, long long n) const {
+        const double xd = x;
+        const double e = sb.at(n) * fscale;
+        const double c = clamp_abs(xd, e);
+        const double d = c - xd;
+        if (d != 0.0) S[n] += d;
+        return static_cast<T>(c);
+    }
+    __device__ __forceinline__ void post_real(T& x0, T& x1, long long n) {
+        x0 = one(x0, n);
+        x1 = one(x1, n + 1);
+        reinterpret_cast<typename cvec<T>::type*>(eps)[n >> 1] = mkc<T>(x0, x1);
+    }
+    __device__ __forceinline__ void finish() {}
+};
+
+// ---- elementwise kernels (unfused path / generic shapes) -------------------------------------------
+
+struct HalfGeom {
+    long long rows;  // prod(dims[:-1])
+    int H;           // n2/2 + 1
+    int P;           // pitch
+    long long n2;
+};
+
+// check_convergence over the half spectrum (projection.cpp:29-52)
+__global__ void k_freduce(const double2* __restrict__ spec, HalfGeom g, FreqB fb, double fscale,
+                          Ctl* ctl, const int* gate);
+// project_onto_fcube + F += displacement (projection.cpp:54-66, 117-119)
+__global__ void k_fclip(double2* spec, HalfGeom g, FreqB fb, double fscale, double2* F,
+                        const int* gate);
+// project_onto_scube + S += displacement; eps = clipped (projection.cpp:68-79, 121-124)
+__global__ void k_sclip(const double* __restrict__ x, double* eps, long long N, SpatialB sb,
+                        double fscale, double* S, const int* gate);
+// compute_error + both preconditions (projection.cpp:20-27,88-94; pipeline.cpp:31-37)
+template <class TI>
+__global__ void k_eps0(const TI* __restrict__ orig, const TI* __restrict__ dec, double* eps,
+                       long long N, SpatialB sb, double fscale, double slack, int check_original,
+                       Ctl* ctl);
+__global__ void k_cast_to_double(const float* __restrict__ in, double* out, long long N);
+// loop decision (projection.cpp:106-116,125)
+__global__ void k_decide(Ctl* ctl);
+__global__ void k_ctl_init(Ctl* ctl, unsigned long long max_iters);
+// report: residual_s (projection.cpp:129-133)
+__global__ void k_residual_s(const double* __restrict__ eps, long long N, SpatialB sb,
+                             double fscale, Ctl* ctl);
+__global__ void k_count_spatial(const double* __restrict__ S, long long N, Ctl* ctl);
+__global__ void k_count_freq(const double2* __restrict__ F, HalfGeom g, Ctl* ctl);
+
+// bounds: full -> half restriction of per-component arrays
+__global__ void k_gather_half(const double* __restrict__ full, double* half, HalfGeom g);
+// half <-> full spectrum expansion (expand_edits' conjugate mirror, archive.cpp:251-258)
+__global__ void k_expand_full(const double2* __restrict__ half, double2* full, int ndim,
+                              long long d0, long long d1, long long d2, int P);
+
+// ---- FP64 gate (pipeline.cpp:46-176) ---------------------------------------------------------------
+
+// compact_edits + overflow escapes + quantize->dequantize (editset.cpp:43-66,76-104;
+// pipeline.cpp:57-106).  Writes the decoder-view dense array, the keep / escape bitmaps.
+__global__ void k_gate_spatial(const double* __restrict__ S, long long N, SpatialB sb, int m,
+                               double* spat_cur, unsigned* keep_words, unsigned* esc_words,
+                               Ctl* ctl);
+__global__ void k_gate_freq(const double2* __restrict__ F, HalfGeom g, FreqB fb, int m,
+                            double2* freq_cur, unsigned* keep_words, unsigned* esc_words,
+                            Ctl* ctl);
+// bitmap compaction helpers
+__global__ void k_popc_blocks(const unsigned* __restrict__ words, long long nwords,
+                              unsigned long long* block_counts);
+__global__ void k_scan_blocks(unsigned long long* counts, long long nblocks,
+                              unsigned long long* total);
+__global__ void k_compact(const unsigned* __restrict__ words, long long nwords,
+                          const unsigned long long* __restrict__ block_offsets,
+                          unsigned long long* out_idx);
+// int32 codes of the kept edits, in flag order (editset.cpp:86-119)
+__global__ void k_codes_spatial(const unsigned long long* __restrict__ idx, long long n,
+                                const double* __restrict__ S, SpatialB sb, int m, int* codes);
+__global__ void k_codes_freq(const unsigned long long* __restrict__ idx, long long n,
+                             const double2* __restrict__ F, HalfGeom g, FreqB fb, int m,
+                             int* codes);
+// escape repair (pipeline.cpp:114-163)
+template <class TI>
+__global__ void k_repair_spatial(const TI* __restrict__ orig, const TI* __restrict__ dec,
+                                 const double* __restrict__ fpart, const double* __restrict__ final_eps,
+                                 long long N, SpatialB sb, double* spat_cur, double* eps_tilde,
+                                 unsigned* esc_words, Ctl* ctl);
+__global__ void k_repair_freq(const double2* __restrict__ delta_star,
+                              const double2* __restrict__ delta_tilde, HalfGeom g, int ndim,
+                              long long d0, long long d1, FreqB fb, double2* freq_cur,
+                              unsigned* esc_words, Ctl* ctl);
+// apply_edits + verify_bounds (archive.cpp:262-297)
+template <class TI>
+__global__ void k_verify_spatial(const TI* __restrict__ orig, const TI* __restrict__ dec,
+                                 const double* __restrict__ spat_cur,
+                                 const double* __restrict__ fpart, long long N, SpatialB sb,
+                                 double* corrected, double* eps_v, Ctl* ctl);
+__global__ void k_verify_freq(const double2* __restrict__ delta, HalfGeom g, FreqB fb, Ctl* ctl);
+__global__ void k_gather_escapes_s(const unsigned long long* __restrict__ idx, long long n,
+                                   const double* __restrict__ spat_cur, double* out_re);
+__global__ void k_gather_escapes_f(const unsigned long long* __restrict__ idx, long long n,
+                                   const double2* __restrict__ freq_cur, HalfGeom g, double2* out);
+
+// inverse_dft helpers: Hermitian / anti-Hermitian parts of a FULL spectrum on the half grid
+__global__ void k_split_hermitian(const double2* __restrict__ full, double2* Hh, double2* Ah,
+                                  HalfGeom g, long long d0, long long d1);
+__global__ void k_maxabs(const double* __restrict__ x, long long N, unsigned long long* out);
+
+} // namespace ffcz_gpu

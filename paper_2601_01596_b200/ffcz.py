@@ -1,0 +1,358 @@
+"""Python host mirror of the reference's public API for the correction path, running on the B200
+engine through the C-ABI (include/ffcz_cuda.h).
+
+Same names, argument meaning and error behaviour as the reference C++ API:
+  correct(original, decompressed, bounds, m=16, max_iters=1000)   pipeline.hpp:22-24
+  alternating_projection(eps0, bounds_working, max_iters, slack)  projection.hpp:65-70
+  forward_dft(x), inverse_dft(X, precision)                       transform.hpp:7-17
+Errors raise ValidationError / SymmetryError / FormatError like the reference's exception
+classes (errors.hpp:9-48).  There is no CPU fallback: without a GPU or the built library the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi as capi
+
+
+class FfczError(RuntimeError):
+    pass
+
+
+class ValidationError(FfczError):
+    pass
+
+
+class SymmetryError(FfczError):
+    pass
+
+
+class FormatError(FfczError):
+    pass
+
+
+class IoError(FfczError):
+    pass
+
+
+class CudaError(FfczError):
+    pass
+
+
+class UnsupportedError(FfczError):
+    pass
+
+
+_STATUS = {capi.FFCZ_VALIDATION_ERROR: ValidationError, capi.FFCZ_SYMMETRY_ERROR: SymmetryError,
+           capi.FFCZ_FORMAT_ERROR: FormatError, capi.FFCZ_IO_ERROR: IoError,
+           capi.FFCZ_CUDA_ERROR: CudaError, capi.FFCZ_UNSUPPORTED: UnsupportedError,
+           capi.FFCZ_OUT_OF_MEMORY: CudaError}
+
+
+def _check(rc):
+    if rc != capi.FFCZ_OK:
+        raise _STATUS.get(rc, FfczError)(capi.load().ffcz_cuda_last_error().decode())
+
+
+class Context:
+    """One engine context (device + stream); calls on a context serialise."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        lib = capi.load()
+        h = C.c_void_p()
+        _check(lib.ffcz_cuda_create(C.byref(h), device, C.c_void_p(stream or 0)))
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            capi.load().ffcz_cuda_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default = {}
+_lock = threading.Lock()
+
+
+def default_context(device: int = 0) -> Context:
+    with _lock:
+        if device not in _default:
+            _default[device] = Context(device)
+        return _default[device]
+
+
+# ---------------------------------------------------------------------------------------------
+
+
+@dataclass
+class DualBounds:
+    """ffcz::DualBounds (bounds.hpp:11-47): E global or per point; Delta global or per component
+    over the FULL spectrum (Re lane, Im lane)."""
+
+    spatial: float | np.ndarray
+    freq_re: float | np.ndarray
+    freq_im: float | np.ndarray | None = None
+
+    @staticmethod
+    def global_(e: float, delta: float) -> "DualBounds":
+        return DualBounds(float(e), float(delta))
+
+
+@dataclass
+class ProjectionReport:
+    iterations: int
+    active_spatial: int
+    active_frequency: int
+    converged: bool
+    residual_f: float
+    residual_s: float
+    wall_time_s: float
+
+
+@dataclass
+class EscapeEntry:
+    frequency: bool
+    index: int
+    re: float
+    im: float
+
+
+@dataclass
+class CorrectionResult:
+    """ffcz::CorrectionResult (pipeline.hpp:11-16) plus the device products."""
+
+    archive_bytes: bytes | None
+    report: ProjectionReport
+    escape_count: int
+    verify_ok: bool
+    verify_max_spatial_excess: float
+    verify_max_freq_excess: float
+    spatial_flags: np.ndarray | None
+    frequency_flags: np.ndarray | None
+    spatial_codes: np.ndarray | None
+    frequency_codes: np.ndarray | None
+    escapes: list
+    corrected: np.ndarray | None
+    escape_rounds: int
+    timings_ms: dict
+    kernel_launches: int
+
+
+def _is_torch(x):
+    return type(x).__module__.startswith("torch")
+
+
+def _field_desc(shape, dtype_code, precision):
+    d = capi.FieldDesc()
+    d.ndim = len(shape)
+    for i, s in enumerate(shape):
+        d.dims[i] = int(s)
+    d.dtype = dtype_code
+    d.precision = capi.FFCZ_PRECISION_F32 if precision == "f32" else capi.FFCZ_PRECISION_F64
+    return d
+
+
+class _Marshal:
+    """Keeps host arrays alive and produces pointers (host numpy or device torch)."""
+
+    def __init__(self):
+        self.keep = []
+
+    def ptr(self, a, dtype=np.float64):
+        if a is None:
+            return None
+        if _is_torch(a):
+            self.keep.append(a)
+            return C.c_void_p(a.data_ptr())
+        arr = np.ascontiguousarray(a, dtype=dtype)
+        self.keep.append(arr)
+        return C.c_void_p(arr.ctypes.data)
+
+
+def _bounds_desc(b: DualBounds, m: _Marshal):
+    bd = capi.BoundsDesc()
+    sp = b.spatial
+    if isinstance(sp, (float, int, np.floating)):
+        bd.spatial_per_point, bd.spatial_global = 0, float(sp)
+    else:
+        bd.spatial_per_point, bd.spatial_values = 1, m.ptr(sp)
+    re = b.freq_re
+    im = b.freq_im if b.freq_im is not None else b.freq_re
+    if isinstance(re, (float, int, np.floating)):
+        bd.freq_per_component, bd.freq_global = 0, float(re)
+    else:
+        bd.freq_per_component = 1
+        bd.freq_re = m.ptr(re)
+        bd.freq_im = bd.freq_re if im is re else m.ptr(im)
+    return bd
+
+
+def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: int = 1000,
+            precision: str | None = None, *, want_archive: bool = True, want_edits: bool = True,
+            want_corrected: bool = True, zlib_level: int = 9, fused: bool = True,
+            ctx: Context | None = None) -> CorrectionResult:
+    """ffcz::correct (pipeline.cpp:26-178) on the GPU.
+
+    original / decompressed: numpy arrays (host; float32 or float64) or CUDA torch tensors (then
+    every bound array must be a CUDA tensor too).  precision: the ScalarField precision tag
+    written into the archive ("f32" / "f64"; default from the input dtype).
+    """
+    ctx = ctx or default_context()
+    lib = capi.load()
+    on_dev = _is_torch(original)
+    if on_dev:
+        import torch
+        is32 = original.dtype == torch.float32
+        shape = tuple(original.shape)
+    else:
+        original = np.asarray(original)
+        decompressed = np.asarray(decompressed)
+        is32 = original.dtype == np.float32
+        shape = original.shape
+    if precision is None:
+        precision = "f32" if is32 else "f64"
+    dt = np.float32 if is32 else np.float64
+    mar = _Marshal()
+    fd = _field_desc(shape, capi.FFCZ_F32 if is32 else capi.FFCZ_F64, precision)
+    bd = _bounds_desc(bounds, mar)
+    opt = capi.Options()
+    lib.ffcz_cuda_default_options(C.byref(opt))
+    flags = 0
+    if on_dev:
+        flags |= capi.FFCZ_INPUTS_ON_DEVICE
+    if want_archive:
+        flags |= capi.FFCZ_WANT_ARCHIVE
+    if want_edits:
+        flags |= capi.FFCZ_WANT_EDITS
+    if want_corrected:
+        flags |= capi.FFCZ_WANT_CORRECTED
+    if not fused:
+        flags |= capi.FFCZ_FORCE_UNFUSED
+    opt.flags = flags
+    opt.zlib_level = zlib_level
+    res = capi.Result()
+    rc = lib.ffcz_cuda_correct(ctx.handle, C.byref(fd), mar.ptr(original, dt),
+                               mar.ptr(decompressed, dt), C.byref(bd), int(m), int(max_iters),
+                               C.byref(opt), C.byref(res))
+    try:
+        _check(rc)
+        N = int(np.prod(shape))
+        r = res.report
+        rep = ProjectionReport(int(r.iterations), int(r.active_spatial), int(r.active_frequency),
+                               bool(r.converged), float(r.residual_f), float(r.residual_s),
+                               float(r.wall_time_s))
+
+        def arr(p, n, dtype):
+            if not p or n == 0:
+                return np.zeros(0, dtype=dtype)
+            return np.ctypeslib.as_array(p, shape=(n,)).copy().view(dtype)
+
+        edits = want_edits or want_archive
+        sflags = fflags = scodes = fcodes = None
+        escapes = []
+        if edits:
+            sflags = arr(res.spatial_flags, int(res.spatial_flag_bytes), np.uint8)
+            fflags = arr(res.frequency_flags, int(res.frequency_flag_bytes), np.uint8)
+            scodes = arr(res.spatial_codes, int(res.n_spatial), np.int32)
+            fcodes = arr(res.frequency_codes, 2 * int(res.n_frequency), np.int32)
+            for i in range(int(res.escape_count)):
+                e = res.escapes[i]
+                escapes.append(EscapeEntry(bool(e.frequency), int(e.index), float(e.re), float(e.im)))
+        corrected = None
+        if want_corrected:
+            corrected = np.ctypeslib.as_array(res.corrected, shape=(N,)).copy().reshape(shape)
+        data = C.string_at(res.archive, res.archive_len) if want_archive else None
+        timings = {k: float(getattr(res, k)) for k in ("t_feasible_ms", "t_loop_ms", "t_gate_ms",
+                                                       "t_h2d_ms", "t_d2h_ms", "t_archive_ms")}
+        return CorrectionResult(data, rep, int(res.escape_count), bool(res.verify_ok),
+                                float(res.verify_max_spatial_excess),
+                                float(res.verify_max_freq_excess), sflags, fflags, scodes, fcodes,
+                                escapes, corrected, int(res.escape_rounds), timings,
+                                int(res.kernel_launches))
+    finally:
+        lib.ffcz_cuda_result_free(C.byref(res))
+
+
+def alternating_projection(eps0, bounds_working: DualBounds, max_iters: int,
+                           precondition_slack: float = 2.0 ** -20, *, fused: bool = True,
+                           ctx: Context | None = None):
+    """ffcz::alternating_projection (projection.cpp:81-142) on the GPU.
+
+    Returns (spatial_edits, frequency_edits FULL spectrum complex, final_epsilon, report)."""
+    ctx = ctx or default_context()
+    lib = capi.load()
+    eps0 = np.ascontiguousarray(eps0, dtype=np.float64)
+    shape = eps0.shape
+    mar = _Marshal()
+    fd = _field_desc(shape, capi.FFCZ_F64, "f64")
+    bd = _bounds_desc(bounds_working, mar)
+    opt = capi.Options()
+    lib.ffcz_cuda_default_options(C.byref(opt))
+    opt.flags = 0 if fused else capi.FFCZ_FORCE_UNFUSED
+    S = np.zeros(shape)
+    F = np.zeros(shape, dtype=np.complex128)
+    eps = np.zeros(shape)
+    rep = capi.Report()
+    _check(lib.ffcz_cuda_alternating_projection(
+        ctx.handle, C.byref(fd), C.c_void_p(eps0.ctypes.data), C.byref(bd), int(max_iters),
+        float(precondition_slack), C.byref(opt), C.c_void_p(S.ctypes.data),
+        C.c_void_p(F.ctypes.data), C.c_void_p(eps.ctypes.data), C.byref(rep)))
+    report = ProjectionReport(int(rep.iterations), int(rep.active_spatial),
+                              int(rep.active_frequency), bool(rep.converged),
+                              float(rep.residual_f), float(rep.residual_s), float(rep.wall_time_s))
+    return S, F, eps, report
+
+
+def forward_dft(x, *, ctx: Context | None = None) -> np.ndarray:
+    """ffcz::forward_dft (transform.cpp:45-50): unnormalised FP64 DFT, FULL spectrum."""
+    ctx = ctx or default_context()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.zeros(x.shape, dtype=np.complex128)
+    fd = _field_desc(x.shape, capi.FFCZ_F64, "f64")
+    _check(capi.load().ffcz_cuda_forward_dft(ctx.handle, C.byref(fd), C.c_void_p(x.ctypes.data),
+                                             C.c_void_p(out.ctypes.data)))
+    return out
+
+
+def inverse_dft(X, precision: str = "f64", *, ctx: Context | None = None) -> np.ndarray:
+    """ffcz::inverse_dft (transform.cpp:64-80): 1/N inverse with the imaginary-residue gate."""
+    ctx = ctx or default_context()
+    X = np.ascontiguousarray(X, dtype=np.complex128)
+    out = np.zeros(X.shape)
+    fd = _field_desc(X.shape, capi.FFCZ_F64, "f64")
+    _check(capi.load().ffcz_cuda_inverse_dft(
+        ctx.handle, C.byref(fd), C.c_void_p(X.ctypes.data),
+        capi.FFCZ_PRECISION_F32 if precision == "f32" else capi.FFCZ_PRECISION_F64,
+        C.c_void_p(out.ctypes.data)))
+    return out
+
+
+def r2c_device(x, out, *, ctx: Context | None = None):
+    """Half-spectrum R2C on CUDA torch tensors (float32/float64): out[..., :n/2+1] complex."""
+    import torch
+    ctx = ctx or default_context()
+    fd = _field_desc(tuple(x.shape), capi.FFCZ_F32 if x.dtype == torch.float32 else capi.FFCZ_F64,
+                     "f64")
+    _check(capi.load().ffcz_cuda_r2c_device(ctx.handle, C.byref(fd), C.c_void_p(x.data_ptr()),
+                                            C.c_void_p(out.data_ptr())))
+
+
+def c2r_device(half, x, *, ctx: Context | None = None):
+    """1/N-normalised C2R on CUDA torch tensors."""
+    import torch
+    ctx = ctx or default_context()
+    fd = _field_desc(tuple(x.shape), capi.FFCZ_F32 if x.dtype == torch.float32 else capi.FFCZ_F64,
+                     "f64")
+    _check(capi.load().ffcz_cuda_c2r_device(ctx.handle, C.byref(fd), C.c_void_p(half.data_ptr()),
+                                            C.c_void_p(x.data_ptr())))
