@@ -1,0 +1,401 @@
+"""bench.py — corrected GB/s of the FFCz correction step on B200 (BASELINE.json metric).
+
+Workload (N=1): BASELINE.json configs[1] — a 512^3 FP32 Nyx-cosmology-shaped field (log-normal
+of a power-law Gaussian random field), uniform +-0.99E base-compressor error (E = 0.1% of the
+range), power-spectrum-preserving per-component Delta (rho = 1e-3, spectrum_bound_to_freq_bounds).
+One step = one ffcz::correct() on device-resident inputs: eps0 + preconditions, the FP64
+alternating projection to convergence, the FP64 gate (compaction, quantisation, overflow and
+repair escapes, verify).  value = 4*N bytes of input corrected per second, whole job.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--n 512]
+
+N > 1 (torchrun): every rank corrects its own independent volume (weak scaling, no collective on
+the data path); timing = max over ranks of the device time.  --impl reference times the
+reference CPU implementation (oracle/_ref, the unmodified reference built from its sources) on
+a bounded sample of the same recipe on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+RHO = 1e-3
+
+
+# ---------------------------------------------------------------------------------------------
+# workload generation (synthetic, seeded; not timed)
+
+
+def nyx_field_torch(n, seed, device):
+    import torch
+    g = torch.Generator(device=device).manual_seed(seed)
+    w = torch.randn((n, n, n), generator=g, device=device, dtype=torch.float64)
+    W = torch.fft.rfftn(w)
+    del w
+    k0 = torch.fft.fftfreq(n, device=device, dtype=torch.float64) * n
+    k2 = torch.fft.rfftfreq(n, device=device, dtype=torch.float64) * n
+    kk = (k0[:, None, None] ** 2 + k0[None, :, None] ** 2 + k2[None, None, :] ** 2).sqrt_()
+    kk[0, 0, 0] = 1.0
+    W *= kk.pow_(-2.5 / 2.0)
+    del kk
+    W[0, 0, 0] = 0
+    f = torch.fft.irfftn(W, s=(n, n, n))
+    del W
+    f = torch.exp(1.5 * f / f.std() - 1.125)
+    return f.to(torch.float32)
+
+
+def rho_delta_torch(orig32):
+    """spectrum_bound_to_freq_bounds (metrics.cpp:107-128) of FFT(original), full spectrum."""
+    import torch
+    X = torch.fft.fftn(orig32.to(torch.float64))
+    mag = X.abs()
+    del X
+    mir = torch.roll(torch.flip(mag, dims=(0, 1, 2)), shifts=(1, 1, 1), dims=(0, 1, 2))
+    mm = torch.minimum(mag, mir)
+    del mir
+    floor = max(1e-12 * mag.max().item(), 1e-300)
+    del mag
+    scale = (np.sqrt(1.0 + RHO) - 1.0) / np.sqrt(2.0)
+    return torch.clamp_min(mm * scale, floor)
+
+
+def make_workload(n, seed, device):
+    import torch
+    orig = nyx_field_torch(n, seed, device)
+    E = 0.1 / 100.0 * (orig.max() - orig.min()).item()
+    g = torch.Generator(device=device).manual_seed(seed + 7)
+    u = (torch.rand(orig.shape, generator=g, device=device, dtype=torch.float64) * 2 - 1) * (0.99 * E)
+    dec = (orig.to(torch.float64) + u).to(torch.float32)
+    del u
+    delta = rho_delta_torch(orig)
+    return orig.contiguous(), dec.contiguous(), E, delta.contiguous()
+
+
+def make_workload_numpy(n, seed):
+    """Same recipe on the host (CPU baseline sample)."""
+    rng = np.random.default_rng(seed)
+    W = np.fft.rfftn(rng.standard_normal((n, n, n)))
+    k0 = np.fft.fftfreq(n) * n
+    k2 = np.fft.rfftfreq(n) * n
+    kk = np.sqrt(k0[:, None, None] ** 2 + k0[None, :, None] ** 2 + k2[None, None, :] ** 2)
+    kk[0, 0, 0] = 1.0
+    W *= kk ** (-2.5 / 2.0)
+    W[0, 0, 0] = 0
+    f = np.fft.irfftn(W, s=(n, n, n))
+    orig = np.exp(1.5 * f / f.std() - 1.125).astype(np.float32).astype(np.float64)
+    E = 0.1 / 100.0 * float(orig.max() - orig.min())
+    dec = (orig + rng.uniform(-0.99 * E, 0.99 * E, orig.shape)).astype(np.float32).astype(np.float64)
+    X = np.fft.fftn(orig)
+    mag = np.abs(X)
+    mir = np.roll(np.flip(mag), 1, axis=(0, 1, 2))
+    floor = max(1e-12 * float(mag.max()), 1e-300)
+    delta = np.maximum(np.minimum(mag, mir) * (np.sqrt(1.0 + RHO) - 1.0) / np.sqrt(2.0), floor)
+    return orig, dec, E, delta
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(name):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture, or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return d.get(name)
+
+
+def cpu_reference_sample(n, threads, steps=1):
+    """Time the unmodified reference correct() (oracle/_ref) on an n^3 sample of the recipe."""
+    env = dict(os.environ, FFCZ_SHIM_THREADS=str(threads))
+    code = (
+        "import sys, json, time; sys.path.insert(0, %r); import bench; "
+        "from oracle import ref_binding as ref; "
+        "o, d, E, D = bench.make_workload_numpy(%d, 11); ts = []\n"
+        "for _ in range(%d):\n"
+        "    r = ref.correct(o, d, E, D, None, 16, 1000, 'f32'); ts.append(r.correct_wall_s)\n"
+        "print(json.dumps({'times': ts, 'iterations': r.report.iterations, "
+        "'verify_ok': r.verify_ok}))" % (ROOT, n, steps))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=1800)
+    if out.returncode != 0:
+        raise RuntimeError(out.stderr[-2000:])
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import ref_binding as ref
+    threads = os.cpu_count() or 1
+    n = args.ref_n
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    res = cpu_reference_sample(n, threads, steps=args.warmup + args.steps)
+    ts = res["times"][args.warmup:]
+    t = float(np.mean(ts))
+    gbs = 4.0 * n ** 3 / t / 1e9
+    line = {
+        "impl": "reference", "metric": "corrected GB/s (input bytes / time to feasibility)",
+        "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config2 recipe (512^3 Nyx-like, rho=1e-3) at a bounded {n}^3 sample",
+                   "n": n},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": f"{n}^3 of the config-2 recipe, full ffcz::correct() incl. archive, "
+                                   f"FFT shim on {threads} threads"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "iterations": res["iterations"], "verify_ok": res["verify_ok"],
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--ref-n", type=int, default=64)
+    ap.add_argument("--cpu-n", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2601_01596_b200 as P
+    from paper_2601_01596_b200 import _capi
+    import ctypes as C
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    ctx = P.Context(local, stream.cuda_stream)
+    lib = _capi.load()
+
+    n = args.n
+    orig, dec, E, delta = make_workload(n, 1234 + rank, dev)
+    bounds = P.DualBounds(E, delta)
+    N = n ** 3
+
+    def step():
+        return P.correct(orig, dec, bounds, 16, 1000, "f32", want_archive=False, want_edits=False,
+                         want_corrected=False, ctx=ctx)
+
+    for _ in range(args.warmup):
+        r = step()
+    assert r.report.converged and r.verify_ok, (r.report, r.verify_ok)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    lib.ffcz_cuda_profile_enable(ctx.handle, 1)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    results = []
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            results.append(step())
+        ev1.record(stream)
+        barrier()
+    lib.ffcz_cuda_profile_enable(ctx.handle, 0)
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    ms_step = ms / args.steps
+    value = world * 4.0 * N / (ms_step * 1e-3) / 1e9
+
+    stats = (_capi.KernelStat * 16)()
+    nst = C.c_int()
+    lib.ffcz_cuda_profile_read(ctx.handle, stats, 16, C.byref(nst))
+    ks = [stats[i] for i in range(nst.value)]
+    dom = max(ks, key=lambda s: s.total_ms)
+    dom_name = dom.name.decode()
+    peak, peak_kind = measured_peak()
+    achieved = dom.bytes / (dom.total_ms * 1e-3) / 1e9 if dom.total_ms > 0 else 0.0
+    traffic = ncu_traffic(dom_name)
+    launches = int(sum(r.kernel_launches for r in results))
+    iters = [r.report.iterations for r in results]
+    loop_ms = [r.timings_ms["t_loop_ms"] for r in results]
+
+    # e2e through the public API with pinned host buffers (H2D + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        h_orig = torch.empty((n, n, n), dtype=torch.float32, pin_memory=True)
+        h_dec = torch.empty_like(h_orig, pin_memory=True)
+        h_delta = torch.empty((n, n, n), dtype=torch.float64, pin_memory=True)
+        h_orig.copy_(orig)
+        h_dec.copy_(dec)
+        h_delta.copy_(delta)
+        hb = P.DualBounds(E, h_delta.numpy())
+        o_np, d_np = h_orig.numpy(), h_dec.numpy()
+        r = P.correct(o_np, d_np, hb, 16, 1000, "f32", want_archive=False, ctx=ctx)  # warm
+        barrier()
+        t0 = time.perf_counter()
+        ksteps = max(1, min(args.steps, 3))
+        for _ in range(ksteps):
+            r = P.correct(o_np, d_np, hb, 16, 1000, "f32", want_archive=False, ctx=ctx)
+        barrier()
+        te = (time.perf_counter() - t0) / ksteps
+        if world > 1:
+            t = torch.tensor([te], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = t.item()
+        d2h = (r.spatial_flags.nbytes + r.frequency_flags.nbytes + r.spatial_codes.nbytes +
+               r.frequency_codes.nbytes + 32 * len(r.escapes) + 8 * N)
+        e2e = {"value": world * 4.0 * N / te / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": 4 * N * 2 + 8 * N, "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": te * 1e3, "steps": ksteps,
+               "includes": "H2D of original+decompressed (f32) and the Delta lane (f64) from pinned "
+                           "memory, device correct(), D2H of flags+codes+escapes+corrected (f64); "
+                           "archive serialisation reported separately"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import ref_binding as ref
+            if ref.available():
+                res = cpu_reference_sample(args.cpu_n, 1)
+                t = res["times"][0]
+                cpu = {"value": 4.0 * args.cpu_n ** 3 / t / 1e9, "unit": "GB/s", "cores": 1,
+                       "kind": "reference",
+                       "sample": f"{args.cpu_n}^3 of the same recipe, one ffcz::correct() of the "
+                                 f"unmodified reference (oracle/_ref), single thread, {t:.1f} s"}
+        except Exception as e:  # the GPU number stands without it
+            cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "reference",
+                   "sample": f"failed: {e!s:.200}"}
+
+    if rank == 0:
+        line = {
+            "metric": "corrected GB/s (input bytes / time to feasibility)",
+            "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config2: {n}^3 FP32 Nyx-like log-normal field, +-0.99E uniform "
+                                   "base error, E=0.1% range, rho=1e-3 per-component Delta; "
+                                   "one independent volume per GPU",
+                       "n": n, "m": 16, "policy": "fp64 (reference control flow)",
+                       "l2": "inputs larger than L2 (0.54 GB per field, 126 MB L2)",
+                       "parallelism": f"independent volumes x{world}"},
+            "ms_per_iteration": float(np.mean(loop_ms) / max(1.0, np.mean(iters))),
+            "iterations": iters[0],
+            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "launches": int(dom.launches),
+                         "avg_launch_ms": dom.total_ms / max(1, dom.launches),
+                         "bytes_per_launch": dom.bytes / max(1, dom.launches)},
+            "kernels": {s.name.decode(): {"launches": int(s.launches), "gated": int(s.gated),
+                                          "ms": s.total_ms,
+                                          "GBps": (s.bytes / (s.total_ms * 1e-3) / 1e9)
+                                          if s.total_ms else 0.0}
+                        for s in ks},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

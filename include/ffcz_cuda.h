@@ -186,6 +186,21 @@ int ffcz_cuda_r2c_device(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const
 int ffcz_cuda_c2r_device(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const void* half_dev,
                          void* x_dev);
 
+/* Per-kernel-class device timing (CUDA events around every launch of the engine's passes),
+ * used by bench.py for the roofline of the dominant kernel.  bytes = ALGORITHMIC bytes
+ * (each element read once + written once).  Launches shorter than 5 us are the
+ * speculative loop launches that returned at the convergence gate; they are counted in
+ * `gated` and excluded from launches / total_ms / bytes. */
+typedef struct ffcz_cuda_kernel_stat {
+    char name[40];
+    uint64_t launches;
+    uint64_t gated;
+    double total_ms;
+    double bytes;
+} ffcz_cuda_kernel_stat;
+int ffcz_cuda_profile_enable(ffcz_cuda_ctx* ctx, int enable); /* 1: clear + start, 0: stop */
+int ffcz_cuda_profile_read(ffcz_cuda_ctx* ctx, ffcz_cuda_kernel_stat* out, int max, int* n);
+
 /* CRC-32C (archive.cpp:61-71), exported for the format tests. */
 uint32_t ffcz_cuda_crc32c(const uint8_t* data, size_t len);
 

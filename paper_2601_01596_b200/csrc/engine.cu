@@ -37,6 +37,24 @@ struct ffcz_cuda_ctx {
     Ctl* hctl = nullptr;   // pinned mirror (one slot per in-flight chunk)
     unsigned long long launches = 0;
     cudaEvent_t ev[8] = {};
+    // per-kernel-class profiling (ffcz_cuda_profile_*)
+    struct ProfRec {
+        int cls;
+        cudaEvent_t a, b;
+        double bytes;
+    };
+    bool prof_on = false;
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    cudaEvent_t take_event() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            FFCZ_CUDA_CHECK(cudaEventCreate(&e));
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
 
     void* buf(const std::string& name, size_t bytes) {
         auto it = bufs.find(name);
@@ -63,6 +81,31 @@ struct ffcz_cuda_ctx {
 };
 
 namespace {
+
+enum ProfClass { kColFwdCheck = 0, kColClipInv, kColPass, kRowR2C, kRowC2R, kRowFused, kNumProf };
+const char* kProfNames[kNumProf] = {"col_fwd_check (K3a)", "col_clip_inv (K3b)", "col_pass",
+                                    "row_r2c", "row_c2r", "row_c2r_sclip_r2c (K1)"};
+
+// RAII event pair around one launch when profiling is on
+struct Prof {
+    ffcz_cuda_ctx& c;
+    int cls;
+    double bytes;
+    cudaEvent_t a = nullptr;
+    Prof(ffcz_cuda_ctx& c_, int cls_, double bytes_) : c(c_), cls(cls_), bytes(bytes_) {
+        if (c.prof_on) {
+            a = c.take_event();
+            FFCZ_CUDA_CHECK(cudaEventRecord(a, c.st));
+        }
+    }
+    ~Prof() {
+        if (a) {
+            cudaEvent_t b = c.take_event();
+            cudaEventRecord(b, c.st);
+            c.prof.push_back({cls, a, b, bytes});
+        }
+    }
+};
 
 thread_local std::string g_last_error;
 
@@ -173,15 +216,34 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
     const int za = three_d ? 0 : 1;  // the pass that completes the forward transform
     double* tmp = fused ? nullptr : c.b<double>("real_tmp", g.N);
 
+    const double pass_bytes = 32.0 * g.Nc();
+    const double dlanes = bw.fb.re ? (bw.fb.im == bw.fb.re ? 1.0 : 2.0) : 0.0;
+    const double check_bytes = pass_bytes + 8.0 * g.Nc() * dlanes;
+    const double fused_bytes = pass_bytes + 8.0 * g.N + (bw.sb.v ? 8.0 * g.N : 0.0);
     auto body = [&]() {
         if (fused) {
-            plan.col(za, -1, spec, spec, gate, HookFReduce{bw.fb, fscale, c.ctl}, st);   // K3a
-            k_decide<<<1, 1, 0, st>>>(c.ctl);                                          // K4
-            plan.col(za, +1, spec, spec, gate, HookFClip<double>{bw.fb, fscale, F}, st); // K3b
-            if (three_d) plan.col(1, +1, spec, spec, gate, HookNone{}, st);
-            launch_row_fused<double>(g.n2, spec, g.P, g.rows, g.n2, invN, c.tw64, gate,
-                                     HookSClip<double>{bw.sb, fscale, S, eps}, st);      // K1
-            if (three_d) plan.col(1, -1, spec, spec, gate, HookNone{}, st);
+            {
+                Prof p(c, kColFwdCheck, check_bytes);
+                plan.col(za, -1, spec, spec, gate, HookFReduce{bw.fb, fscale, c.ctl}, st);   // K3a
+            }
+            k_decide<<<1, 1, 0, st>>>(c.ctl);                                              // K4
+            {
+                Prof p(c, kColClipInv, check_bytes);
+                plan.col(za, +1, spec, spec, gate, HookFClip<double>{bw.fb, fscale, F}, st); // K3b
+            }
+            if (three_d) {
+                Prof p(c, kColPass, pass_bytes);
+                plan.col(1, +1, spec, spec, gate, HookNone{}, st);
+            }
+            {
+                Prof p(c, kRowFused, fused_bytes);
+                launch_row_fused<double>(g.n2, spec, g.P, g.rows, g.n2, invN, c.tw64, gate,
+                                         HookSClip<double>{bw.sb, fscale, S, eps}, st);  // K1
+            }
+            if (three_d) {
+                Prof p(c, kColPass, pass_bytes);
+                plan.col(1, -1, spec, spec, gate, HookNone{}, st);
+            }
             c.launches += three_d ? 6 : 4;
         } else {
             plan.r2c(eps, spec, gate, st);
@@ -196,8 +258,14 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
     };
 
     if (fused) {
-        launch_row_r2c<double>(g.n2, eps, g.n2, spec, g.P, g.rows, c.tw64, gate, st);
-        if (three_d) plan.col(1, -1, spec, spec, gate, HookNone{}, st);
+        {
+            Prof p(c, kRowR2C, 8.0 * g.N + 16.0 * g.Nc());
+            launch_row_r2c<double>(g.n2, eps, g.n2, spec, g.P, g.rows, c.tw64, gate, st);
+        }
+        if (three_d) {
+            Prof p(c, kColPass, pass_bytes);
+            plan.col(1, -1, spec, spec, gate, HookNone{}, st);
+        }
         c.launches += three_d ? 2 : 1;
     }
 
@@ -265,6 +333,38 @@ struct GateOut {
     unsigned long long act_s = 0, act_f = 0;
 };
 
+// whole-field FP64 transforms with one profiling record per pass
+void r2c_p(ffcz_cuda_ctx& c, const FftPlan<double>& plan, const double* x, double2* half) {
+    const Geometry& g = plan.g;
+    {
+        Prof p(c, kRowR2C, 8.0 * g.N + 16.0 * g.Nc());
+        launch_row_r2c<double>(g.n2, x, g.n2, half, g.P, g.rows, c.tw64, nullptr, c.st);
+    }
+    for (int a : {1, 0})
+        if (g.d[a] > 1) {
+            Prof p(c, kColPass, 32.0 * g.Nc());
+            plan.col(a, -1, half, half, nullptr, HookNone{}, c.st);
+        }
+    c.launches += 1 + (g.d[0] > 1) + (g.d[1] > 1);
+}
+
+void c2r_p(ffcz_cuda_ctx& c, const FftPlan<double>& plan, const double2* half, double2* work,
+           double* x, double scale) {
+    const Geometry& g = plan.g;
+    const double2* src = half;
+    for (int a : {0, 1})
+        if (g.d[a] > 1) {
+            Prof p(c, kColPass, 32.0 * g.Nc());
+            plan.col(a, +1, src, work, nullptr, HookNone{}, c.st);
+            src = work;
+        }
+    {
+        Prof p(c, kRowC2R, 8.0 * g.N + 16.0 * g.Nc());
+        launch_row_c2r<double>(g.n2, src, g.P, x, g.n2, g.rows, scale, c.tw64, nullptr, c.st);
+    }
+    c.launches += 1 + (g.d[0] > 1) + (g.d[1] > 1);
+}
+
 template <class TI>
 GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* dec,
                  const Bounds& bo, int m, bool converged, double* eps, double* S, double2* F,
@@ -305,29 +405,29 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
     double2* delta_star = F;
     const double invN = 1.0 / static_cast<double>(N);
     if (converged) {
-        plan.r2c(eps, delta_star, nullptr, st);                          // pipeline.cpp:114
+        r2c_p(c, plan, eps, delta_star);                          // pipeline.cpp:114
         for (int round = 0; round < 32; ++round) {                       // pipeline.cpp:116
             FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->dirty, 0, sizeof(int), st));
-            plan.c2r(freq_cur, spec, fpart, invN, nullptr, st);          // :125-133
+            c2r_p(c, plan, freq_cur, spec, fpart, invN);          // :125-133
             k_repair_spatial<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, fpart, eps, N, bo.sb,
                                                               spat_cur, eps_t, esc_s, c.ctl);
-            plan.r2c(eps_t, spec, nullptr, st);                          // :137-138
+            r2c_p(c, plan, eps_t, spec);                          // :137-138
             k_repair_freq<<<grid_for(Nc), 256, 0, st>>>(delta_star, spec, hg, g.ndim, g.d[0],
                                                         g.d[1], bo.fb, freq_cur, esc_f, c.ctl);
             FFCZ_LAUNCH_CHECK();
-            c.launches += 8;
+            c.launches += 2;
             ++o.rounds;
             if (!c.read_ctl().dirty) break;                              // :161
         }
     }
     // read_archive + apply_edits + verify_bounds (pipeline.cpp:174-176) on the decoder view
-    plan.c2r(freq_cur, spec, fpart, invN, nullptr, st);
+    c2r_p(c, plan, freq_cur, spec, fpart, invN);
     k_verify_spatial<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, spat_cur, fpart, N, bo.sb,
                                                       corrected, eps_t, c.ctl);
-    plan.r2c(eps_t, spec, nullptr, st);
+    r2c_p(c, plan, eps_t, spec);
     k_verify_freq<<<grid_for(Nc), 256, 0, st>>>(spec, hg, bo.fb, c.ctl);
     FFCZ_LAUNCH_CHECK();
-    c.launches += 8;
+    c.launches += 2;
     const Ctl h = c.read_ctl();
     o.vs = bitsd_host(h.vs_bits);
     o.vf = bitsd_host(h.vf_bits);
@@ -810,5 +910,40 @@ int ffcz_cuda_c2r_device(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const
 }
 
 uint32_t ffcz_cuda_crc32c(const uint8_t* data, size_t len) { return ffcz_host::crc32c(data, len); }
+
+int ffcz_cuda_profile_enable(ffcz_cuda_ctx* ctx, int enable) {
+    return guarded(ctx, [&] {
+        if (enable) {
+            ctx->sync();
+            ctx->prof.clear();
+            ctx->ev_used = 0;
+        }
+        ctx->prof_on = enable != 0;
+    });
+}
+
+int ffcz_cuda_profile_read(ffcz_cuda_ctx* ctx, ffcz_cuda_kernel_stat* out, int max, int* n) {
+    return guarded(ctx, [&] {
+        ctx->sync();
+        ffcz_cuda_kernel_stat st[kNumProf];
+        std::memset(st, 0, sizeof(st));
+        for (int k = 0; k < kNumProf; ++k)
+            std::strncpy(st[k].name, kProfNames[k], sizeof(st[k].name) - 1);
+        for (const auto& r : ctx->prof) {
+            float ms = 0;
+            FFCZ_CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+            if (ms < 0.005f) {
+                ++st[r.cls].gated;
+                continue;
+            }
+            ++st[r.cls].launches;
+            st[r.cls].total_ms += ms;
+            st[r.cls].bytes += r.bytes;
+        }
+        int k = 0;
+        for (; k < kNumProf && k < max; ++k) out[k] = st[k];
+        *n = k;
+    });
+}
 
 } // extern "C"
