@@ -188,9 +188,9 @@ int ffcz_cuda_c2r_device(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const
 
 /* Per-kernel-class device timing (CUDA events around every launch of the engine's passes),
  * used by bench.py for the roofline of the dominant kernel.  bytes = ALGORITHMIC bytes
- * (each element read once + written once).  Launches shorter than 5 us are the
- * speculative loop launches that returned at the convergence gate; they are counted in
- * `gated` and excluded from launches / total_ms / bytes. */
+ * (each element read once + written once).  Launches shorter than 20% of the
+ * longest launch of the same class and size are speculative loop launches that returned at the
+ * convergence gate; they are counted in `gated` and excluded from launches / total_ms / bytes. */
 typedef struct ffcz_cuda_kernel_stat {
     char name[40];
     uint64_t launches;

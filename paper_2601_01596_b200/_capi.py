@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libffcz_cuda.so")
+LIB_PATH = os.environ.get("FFCZ_CUDA_LIB") or os.path.join(HERE, "libffcz_cuda.so")
 
 FFCZ_OK = 0
 FFCZ_VALIDATION_ERROR = 1

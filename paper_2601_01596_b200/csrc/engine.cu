@@ -367,8 +367,8 @@ void c2r_p(ffcz_cuda_ctx& c, const FftPlan<double>& plan, const double2* half, d
 
 template <class TI>
 GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* dec,
-                 const Bounds& bo, int m, bool converged, double* eps, double* S, double2* F,
-                 double* corrected) {
+                 const Bounds& bo, int m, bool converged, bool fused, double* eps, double* S,
+                 double2* F, double* corrected) {
     cudaStream_t st = c.st;
     FftPlan<double> plan{g, &c.tw64};
     const HalfGeom hg = g.hg();
@@ -384,7 +384,7 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
     int* codes_s = c.b<int>("codes_s", N);
     int* codes_f = c.b<int>("codes_f", 2 * Nc);
     double2* spec = c.b<double2>("spec", g.half_elems());
-    double* eps_t = c.b<double>("eps_tilde", N);
+    double* eps_t = fused ? nullptr : c.b<double>("eps_tilde", N);
 
     FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->act_s, 0, 2 * sizeof(unsigned long long), st));
     k_gate_spatial<<<grid_for(N), 256, 0, st>>>(S, N, bo.sb, m, spat_cur, keep_s, esc_s, c.ctl);
@@ -400,34 +400,91 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
     FFCZ_LAUNCH_CHECK();
     c.launches += 2;
 
-    // S and F are consumed: reuse them as the frequency-part and delta_star buffers.
+    // delta_star = FFT(final_eps) is the spectrum the loop's last convergence check produced
+    // (still in `spec`); S and F are consumed, so they become the round's real / half work buffers.
+    double2* delta_star = spec;
     double* fpart = S;
-    double2* delta_star = F;
+    double2* work = F;
     const double invN = 1.0 / static_cast<double>(N);
-    if (converged) {
-        r2c_p(c, plan, eps, delta_star);                          // pipeline.cpp:114
-        for (int round = 0; round < 32; ++round) {                       // pipeline.cpp:116
-            FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->dirty, 0, sizeof(int), st));
-            c2r_p(c, plan, freq_cur, spec, fpart, invN);          // :125-133
-            k_repair_spatial<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, fpart, eps, N, bo.sb,
-                                                              spat_cur, eps_t, esc_s, c.ctl);
-            r2c_p(c, plan, eps_t, spec);                          // :137-138
-            k_repair_freq<<<grid_for(Nc), 256, 0, st>>>(delta_star, spec, hg, g.ndim, g.d[0],
-                                                        g.d[1], bo.fb, freq_cur, esc_f, c.ctl);
-            FFCZ_LAUNCH_CHECK();
-            c.launches += 2;
-            ++o.rounds;
-            if (!c.read_ctl().dirty) break;                              // :161
+    if (fused) {
+        // fused rounds: [Z inv] [Y inv] [C2R -> repair_s -> R2C] [Y fwd] [Z fwd + mark] + sparse
+        const bool three_d = g.d[0] > 1;
+        const int za = three_d ? 0 : 1;
+        const long long vw = (g.half_elems() + 31) / 32;
+        unsigned* viol = c.b<unsigned>("viol", vw);
+        const double pass = 32.0 * Nc;
+        auto inverse_and_row = [&](auto row_hook, double row_bytes) {
+            {
+                Prof p(c, kColPass, pass);
+                plan.col(za, +1, freq_cur, work, nullptr, HookNone{}, st);
+            }
+            if (three_d) {
+                Prof p(c, kColPass, pass);
+                plan.col(1, +1, work, work, nullptr, HookNone{}, st);
+            }
+            {
+                Prof p(c, kRowFused, row_bytes);
+                launch_row_fused<double>(g.n2, work, g.P, g.rows, g.n2, invN, c.tw64, nullptr,
+                                         row_hook, st);
+            }
+            if (three_d) {
+                Prof p(c, kColPass, pass);
+                plan.col(1, -1, work, work, nullptr, HookNone{}, st);
+            }
+            c.launches += three_d ? 4 : 2;
+        };
+        const double in_bytes = 2.0 * sizeof(TI) * N + 8.0 * N;
+        if (converged) {
+            for (int round = 0; round < 32; ++round) {                   // pipeline.cpp:116
+                FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->dirty, 0, sizeof(int), st));
+                FFCZ_CUDA_CHECK(cudaMemsetAsync(viol, 0, vw * sizeof(unsigned), st));
+                inverse_and_row(HookRepairS<TI>{orig, dec, spat_cur, eps, bo.sb, esc_s, c.ctl},
+                                pass + in_bytes);
+                {
+                    Prof p(c, kColFwdCheck, pass);
+                    plan.col(za, -1, work, work, nullptr, HookMarkViol{bo.fb, viol, c.ctl}, st);
+                }
+                k_repair_freq_sparse<<<grid_for(vw), 256, 0, st>>>(viol, vw, delta_star, work, hg,
+                                                                   g.d[0], g.d[1], freq_cur, esc_f);
+                FFCZ_LAUNCH_CHECK();
+                c.launches += 2;
+                ++o.rounds;
+                if (!c.read_ctl().dirty) break;                          // :161
+            }
         }
+        // apply_edits + verify_bounds on the decoder view (pipeline.cpp:174-176)
+        inverse_and_row(HookVerifyS<TI>{orig, dec, spat_cur, corrected, bo.sb, c.ctl},
+                        pass + in_bytes + 8.0 * N);
+        {
+            Prof p(c, kColFwdCheck, 16.0 * Nc);
+            plan.col(za, -1, work, work, nullptr, HookVerifyF{bo.fb, c.ctl}, st);
+        }
+        c.launches += 1;
+    } else {
+        if (converged) {
+            for (int round = 0; round < 32; ++round) {                   // pipeline.cpp:116
+                FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->dirty, 0, sizeof(int), st));
+                c2r_p(c, plan, freq_cur, work, fpart, invN);             // :125-133
+                k_repair_spatial<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, fpart, eps, N, bo.sb,
+                                                                  spat_cur, eps_t, esc_s, c.ctl);
+                r2c_p(c, plan, eps_t, work);                             // :137-138
+                k_repair_freq<<<grid_for(Nc), 256, 0, st>>>(delta_star, work, hg, g.ndim, g.d[0],
+                                                            g.d[1], bo.fb, freq_cur, esc_f, c.ctl);
+                FFCZ_LAUNCH_CHECK();
+                c.launches += 2;
+                ++o.rounds;
+                if (!c.read_ctl().dirty) break;                          // :161
+            }
+        }
+        // read_archive + apply_edits + verify_bounds (pipeline.cpp:174-176) on the decoder view
+        c2r_p(c, plan, freq_cur, work, fpart, invN);
+        k_verify_spatial<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, spat_cur, fpart, N, bo.sb,
+                                                          corrected, eps_t, c.ctl);
+        r2c_p(c, plan, eps_t, work);
+        k_verify_freq<<<grid_for(Nc), 256, 0, st>>>(work, hg, bo.fb, c.ctl);
+        FFCZ_LAUNCH_CHECK();
+        c.launches += 2;
     }
-    // read_archive + apply_edits + verify_bounds (pipeline.cpp:174-176) on the decoder view
-    c2r_p(c, plan, freq_cur, spec, fpart, invN);
-    k_verify_spatial<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, spat_cur, fpart, N, bo.sb,
-                                                      corrected, eps_t, c.ctl);
-    r2c_p(c, plan, eps_t, spec);
-    k_verify_freq<<<grid_for(Nc), 256, 0, st>>>(spec, hg, bo.fb, c.ctl);
-    FFCZ_LAUNCH_CHECK();
-    c.launches += 2;
     const Ctl h = c.read_ctl();
     o.vs = bitsd_host(h.vs_bits);
     o.vf = bitsd_host(h.vf_bits);
@@ -491,7 +548,8 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     ++c.launches;
 
     double* corrected = c.b<double>("corrected", N);
-    const GateOut go = run_gate<TI>(c, g, orig, dec, bo, m, lr.converged, eps, S, F, corrected);
+    const GateOut go = run_gate<TI>(c, g, orig, dec, bo, m, lr.converged, lr.fused, eps, S, F,
+                                    corrected);
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[6], st));
     h = c.read_ctl();
 
@@ -929,15 +987,24 @@ int ffcz_cuda_profile_read(ffcz_cuda_ctx* ctx, ffcz_cuda_kernel_stat* out, int m
         std::memset(st, 0, sizeof(st));
         for (int k = 0; k < kNumProf; ++k)
             std::strncpy(st[k].name, kProfNames[k], sizeof(st[k].name) - 1);
-        for (const auto& r : ctx->prof) {
-            float ms = 0;
-            FFCZ_CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
-            if (ms < 0.005f) {
+        // launches that returned at the convergence gate run for a small fraction of a real
+        // pass: anything under 20% of the longest launch of the same class and byte count
+        std::vector<float> dur(ctx->prof.size());
+        std::map<std::pair<int, double>, float> longest;
+        for (size_t i = 0; i < ctx->prof.size(); ++i) {
+            const auto& r = ctx->prof[i];
+            FFCZ_CUDA_CHECK(cudaEventElapsedTime(&dur[i], r.a, r.b));
+            float& l = longest[{r.cls, r.bytes}];
+            l = std::max(l, dur[i]);
+        }
+        for (size_t i = 0; i < ctx->prof.size(); ++i) {
+            const auto& r = ctx->prof[i];
+            if (dur[i] < 0.2f * longest[{r.cls, r.bytes}]) {
                 ++st[r.cls].gated;
                 continue;
             }
             ++st[r.cls].launches;
-            st[r.cls].total_ms += ms;
+            st[r.cls].total_ms += dur[i];
             st[r.cls].bytes += r.bytes;
         }
         int k = 0;

@@ -41,9 +41,10 @@ template <class T, int L, class Hook>
 void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
                long long plane_stride, long long nplanes, int ncols, Twiddles<T>& tw,
                const int* gate, Hook hook, cudaStream_t st) {
-    constexpr int E = L < kRadixE<T> ? L : kRadixE<T>;
+    constexpr int E = pick_E<T>(L);
     constexpr int TT = L / E;
-    int B = static_cast<int>(std::min<long long>(tile_budget<T>() / L, 512 / TT));
+    constexpr int MAXT = max_threads<T, E>();
+    int B = static_cast<int>(std::min<long long>(tile_budget<T>() / L, MAXT / TT));
     B = std::min(B, 128);
     B = std::min(B, pow2_ceil(ncols));
     B = std::max(B, 1);
@@ -52,26 +53,27 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
     if (dir < 0) {
         auto k = k_col<T, L, E, -1, Hook>;
         set_smem(k, smem);
-        k<<<grid, TT * B, smem, st>>>(src, dst, row_stride, plane_stride, ncols, B, tw.W,
-                                       kLmax / L, gate, hook);
+        k<<<grid, TT * B, smem, st>>>(src, dst, row_stride, plane_stride, ncols, B,
+                                       tw.stage_table(L, E), gate, hook);
     } else {
         auto k = k_col<T, L, E, +1, Hook>;
         set_smem(k, smem);
-        k<<<grid, TT * B, smem, st>>>(src, dst, row_stride, plane_stride, ncols, B, tw.W,
-                                       kLmax / L, gate, hook);
+        k<<<grid, TT * B, smem, st>>>(src, dst, row_stride, plane_stride, ncols, B,
+                                       tw.stage_table(L, E), gate, hook);
     }
     FFCZ_LAUNCH_CHECK();
 }
 
 template <class T, int M> struct RowCfg {
-    static constexpr int E = M < kRadixE<T> ? M : kRadixE<T>;
+    static constexpr int E = pick_E<T>(M);
     static constexpr int TT = M / E;
+    static constexpr int MAXT = max_threads<T, E>();
 };
 
 template <class T, int M>
 int rows_per_cta(long long nrows) {
     constexpr int TT = RowCfg<T, M>::TT;
-    long long r = std::min<long long>(tile_budget<T>() / M, 512 / TT);
+    long long r = std::min<long long>(tile_budget<T>() / M, RowCfg<T, M>::MAXT / TT);
     r = std::min<long long>(r, pow2_ceil(nrows));
     return static_cast<int>(std::max<long long>(1, r));
 }
@@ -85,7 +87,8 @@ void row_r2c_radix(const T* in, long long in_stride, cplx<T>* out, long long out
     auto k = k_row_r2c<T, M, E, HookNone>;
     set_smem(k, smem);
     k<<<static_cast<unsigned>((nrows + R - 1) / R), TT * R, smem, st>>>(
-        in, in_stride, out, out_stride, nrows, tw.W, kLmax / M, kLmax / (2 * M), gate, HookNone{});
+        in, in_stride, out, out_stride, nrows, tw.stage_table(M, E), tw.post_table(M), gate,
+        HookNone{});
     FFCZ_LAUNCH_CHECK();
 }
 
@@ -98,8 +101,8 @@ void row_c2r_radix(const cplx<T>* in, long long in_stride, T* out, long long out
     auto k = k_row_c2r<T, M, E, RealHookNone>;
     set_smem(k, smem);
     k<<<static_cast<unsigned>((nrows + R - 1) / R), TT * R, smem, st>>>(
-        in, in_stride, out, out_stride, nrows, tw.W, kLmax / M, kLmax / (2 * M), scale, gate,
-        RealHookNone{});
+        in, in_stride, out, out_stride, nrows, tw.stage_table(M, E), tw.post_table(M), scale,
+        gate, RealHookNone{});
     FFCZ_LAUNCH_CHECK();
 }
 
@@ -112,7 +115,8 @@ void row_fused_radix(cplx<T>* data, long long stride, long long nrows, long long
     auto k = k_row_c2r_r2c<T, M, E, Hook>;
     set_smem(k, smem);
     k<<<static_cast<unsigned>((nrows + R - 1) / R), TT * R, smem, st>>>(
-        data, stride, nrows, real_stride, tw.W, kLmax / M, kLmax / (2 * M), scale, gate, hook);
+        data, stride, nrows, real_stride, tw.stage_table(M, E), tw.post_table(M), scale, gate,
+        hook);
     FFCZ_LAUNCH_CHECK();
 }
 

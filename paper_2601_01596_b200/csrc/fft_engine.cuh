@@ -140,10 +140,25 @@ struct XchRow {
 
 // ---- Stockham radix-E passes over a line of L points held as v[m] = x[t + T*m] ---------------
 // Stage radices are E, E, ..., E, L/E^k (remainder last so stage 1 writes have stride E, the
-// pattern the padding is built for).  Twiddles W_L^q = tw[q * twstride] (tw = W_LMAX table).
+// pattern the padding is built for).  Inter-stage twiddles: one load of w = exp(-2 pi i k/(NS R))
+// per butterfly from a per-(L, E) table laid out stage by stage ([k], so consecutive lanes read
+// consecutive entries: one coalesced, L1-resident request per warp), then w^r by successive
+// products in registers (<= 15 products, a few ulp) — shared-memory/L1 bandwidth, not FLOPs,
+// bounds these passes.
+template <int L, int E>
+__host__ __device__ constexpr int stage_tw_offset(int NS) {
+    int off = 0;
+    for (int ns = 1; ns < NS;) {
+        const int R = (L / ns >= E) ? E : L / ns;
+        if (ns > 1) off += ns;
+        ns *= R;
+    }
+    return off;
+}
+
 template <class T, int L, int E, int NS, int DIR, class X>
 __device__ __forceinline__ void stockham(cplx<T> (&v)[E], int t, const cplx<T>* __restrict__ tw,
-                                         int twstride, const X& xch) {
+                                         const X& xch) {
     constexpr int R = (L / NS >= E) ? E : (L / NS);
     constexpr int NB = E / R;
     constexpr int TT = L / E;
@@ -156,10 +171,13 @@ __device__ __forceinline__ void stockham(cplx<T> (&v)[E], int t, const cplx<T>* 
         if constexpr (NS > 1) {
             const int j = t + TT * i;
             const int k = j & (NS - 1);
+            constexpr int OFF = stage_tw_offset<L, E>(NS);
+            const cplx<T> w1 = tw[OFF + k];
+            cplx<T> w = w1;
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                const cplx<T> w = tw[(r * k * (L / (NS * R))) * twstride];
                 a[r] = DIR < 0 ? cmul(a[r], w) : cmulc(a[r], w);
+                if (r + 1 < R) w = cmul(w, w1);
             }
         }
         dft_reg<DIR, R>(a);
@@ -178,7 +196,7 @@ __device__ __forceinline__ void stockham(cplx<T> (&v)[E], int t, const cplx<T>* 
         xch.sync();
 #pragma unroll
         for (int m = 0; m < E; ++m) v[m] = xch.ld(t + TT * m);
-        stockham<T, L, E, NS * R, DIR>(v, t, tw, twstride, xch);
+        stockham<T, L, E, NS * R, DIR>(v, t, tw, xch);
     }
 }
 
@@ -192,13 +210,27 @@ struct HookNone {
     __device__ __forceinline__ void finish() {}
 };
 
+// A hook may declare `static constexpr bool kNoStore = true` when the pass output is consumed
+// by the hook alone (e.g. the verify reduction): the store is skipped (half a pass of traffic).
+template <class H>
+constexpr bool hook_stores() {
+    if constexpr (requires { H::kNoStore; })
+        return !H::kNoStore;
+    else
+        return true;
+}
+
 // ---- column pass: L-point c2c along a strided axis of the half spectrum -------------------------
 // Tile = L rows x B consecutive columns (columns = k2 < ncols inside one plane).
+// Threads holding 32 registers of line data run 512 per CTA, 64 registers 256.
+template <class T, int E>
+constexpr int max_threads() { return E * sizeof(cplx<T>) <= 128 ? 512 : 256; }
+
 // Launched with blockDim.x = (L/E) * B threads and (L + L/E) * B elements of dynamic smem.
 template <class T, int L, int E, int DIR, class Hook>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>())
     k_col(const cplx<T>* __restrict__ src, cplx<T>* __restrict__ dst, long long row_stride,
-          long long plane_stride, int ncols, int B, const cplx<T>* __restrict__ tw, int twstride,
+          long long plane_stride, int ncols, int B, const cplx<T>* __restrict__ tw,
           const int* gate, Hook hook) {
     if (gated(gate)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -220,13 +252,13 @@ __global__ void __launch_bounds__(512)
             v[m] = mkc<T>(T(0), T(0));
         }
     }
-    stockham<T, L, E, 1, DIR>(v, t, tw, twstride, XchCol<T, E>{s + b, B});
+    stockham<T, L, E, 1, DIR>(v, t, tw, XchCol<T, E>{s + b, B});
 #pragma unroll
     for (int m = 0; m < E; ++m) {
         const long long off = base + static_cast<long long>(t + TT * m) * row_stride;
         if (valid) {
             hook.post(v[m], off, c);
-            dst[off] = v[m];
+            if constexpr (hook_stores<Hook>()) dst[off] = v[m];
         }
     }
     hook.finish();
@@ -245,24 +277,23 @@ template <int M, int E>
 constexpr int row_smem_elems() { return M + M / E + 2; }
 
 // Split Z (in smem, natural order at XchRow positions) into X[k] = Ze + W_{2M}^k Zo.
+// twp[k] = W_{2M}^k = exp(-2 pi i k / 2M), k in [0, M]
 template <class T, int M, int E>
-__device__ __forceinline__ cplx<T> r2c_split(const cplx<T>* s, int k, const cplx<T>* __restrict__ tw,
-                                             int twstride2) {
+__device__ __forceinline__ cplx<T> r2c_split(const cplx<T>* s, int k, const cplx<T>* __restrict__ twp) {
     using X = XchRow<T, E>;
     const cplx<T> zk = s[X::pos(k)];
     const cplx<T> zn = s[X::pos((M - k) & (M - 1))];
     const T h = T(0.5);
     cplx<T> ze = mkc<T>((zk.x + zn.x) * h, (zk.y - zn.y) * h);
     cplx<T> zo = mkc<T>((zk.y + zn.y) * h, (zn.x - zk.x) * h);
-    const cplx<T> w = tw[k * twstride2];
+    const cplx<T> w = twp[k];
     return cadd(ze, cmul(zo, w));
 }
 
 // Merge X[k], X[M-k] (smem) into Z[k] = (X_k + conj X_{M-k}) + i (X_k - conj X_{M-k}) W^{-k};
 // imaginary parts of X[0] and X[M] are dropped (= Re of the full c2c inverse).
 template <class T, int M, int E>
-__device__ __forceinline__ cplx<T> c2r_merge(const cplx<T>* s, int k, const cplx<T>* __restrict__ tw,
-                                             int twstride2) {
+__device__ __forceinline__ cplx<T> c2r_merge(const cplx<T>* s, int k, const cplx<T>* __restrict__ twp) {
     using X = XchRow<T, E>;
     cplx<T> a = s[X::pos(k)];
     cplx<T> b = s[X::pos(M - k)];
@@ -272,7 +303,7 @@ __device__ __forceinline__ cplx<T> c2r_merge(const cplx<T>* s, int k, const cplx
     }
     const cplx<T> ze = mkc<T>(a.x + b.x, a.y - b.y);
     const cplx<T> d = mkc<T>(a.x - b.x, a.y + b.y);
-    const cplx<T> w = tw[k * twstride2];
+    const cplx<T> w = twp[k];
     const cplx<T> zo = cmulc(d, w);
     return mkc<T>(ze.x - zo.y, ze.y + zo.x);
 }
@@ -288,10 +319,10 @@ struct RealHookNone {
 // Plain R2C of rows (FP32 or FP64 real input of the same type).
 // Launched with blockDim.x = (M/E) * rows-per-CTA threads, row_smem_elems() per row of smem.
 template <class T, int M, int E, class Hook>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>())
     k_row_r2c(const T* __restrict__ in, long long in_stride, cplx<T>* __restrict__ out,
-              long long out_stride, long long nrows, const cplx<T>* __restrict__ tw, int twstride,
-              int twstride2, const int* gate, Hook hook) {
+              long long out_stride, long long nrows, const cplx<T>* __restrict__ tw,
+              const cplx<T>* __restrict__ twp, const int* gate, Hook hook) {
     if (gated(gate)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int TT = M / E;
@@ -305,7 +336,7 @@ __global__ void __launch_bounds__(512)
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = valid ? src[t + TT * m] : mkc<T>(T(0), T(0));
     const XchRow<T, E> x{s};
-    stockham<T, M, E, 1, -1>(v, t, tw, twstride, x);
+    stockham<T, M, E, 1, -1>(v, t, tw, x);
     __syncthreads();
 #pragma unroll
     for (int m = 0; m < E; ++m) x.st(t + TT * m, v[m]);
@@ -315,7 +346,7 @@ __global__ void __launch_bounds__(512)
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const int k = t + TT * m;
-            cplx<T> X = r2c_split<T, M, E>(s, k, tw, twstride2);
+            cplx<T> X = r2c_split<T, M, E>(s, k, twp);
             hook.post(X, row * out_stride + k, k);
             dst[k] = X;
         }
@@ -332,10 +363,10 @@ __global__ void __launch_bounds__(512)
 // Plain C2R of rows: out = scale * (unnormalised inverse along the last axis).
 // Launched with blockDim.x = (M/E) * rows-per-CTA threads, row_smem_elems() per row of smem.
 template <class T, int M, int E, class Hook>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>())
     k_row_c2r(const cplx<T>* __restrict__ in, long long in_stride, T* __restrict__ out,
-              long long out_stride, long long nrows, const cplx<T>* __restrict__ tw, int twstride,
-              int twstride2, T scale, const int* gate, Hook hook) {
+              long long out_stride, long long nrows, const cplx<T>* __restrict__ tw,
+              const cplx<T>* __restrict__ twp, T scale, const int* gate, Hook hook) {
     if (gated(gate)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int TT = M / E;
@@ -361,8 +392,8 @@ __global__ void __launch_bounds__(512)
     __syncthreads();
     cplx<T> v[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = c2r_merge<T, M, E>(s, t + TT * m, tw, twstride2);
-    stockham<T, M, E, 1, +1>(v, t, tw, twstride, x);
+    for (int m = 0; m < E; ++m) v[m] = c2r_merge<T, M, E>(s, t + TT * m, twp);
+    stockham<T, M, E, 1, +1>(v, t, tw, x);
     if (valid) {
         cplx<T>* dst = reinterpret_cast<cplx<T>*>(out + row * out_stride);
 #pragma unroll
@@ -381,9 +412,9 @@ __global__ void __launch_bounds__(512)
 // own write.
 // Launched with blockDim.x = (M/E) * rows-per-CTA threads, row_smem_elems() per row of smem.
 template <class T, int M, int E, class Hook>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>())
     k_row_c2r_r2c(cplx<T>* data, long long stride, long long nrows, long long real_stride,
-                  const cplx<T>* __restrict__ tw, int twstride, int twstride2, T scale,
+                  const cplx<T>* __restrict__ tw, const cplx<T>* __restrict__ twp, T scale,
                   const int* gate, Hook hook) {
     if (gated(gate)) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -404,8 +435,8 @@ __global__ void __launch_bounds__(512)
     __syncthreads();
     cplx<T> v[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = c2r_merge<T, M, E>(s, t + TT * m, tw, twstride2);
-    stockham<T, M, E, 1, +1>(v, t, tw, twstride, x);
+    for (int m = 0; m < E; ++m) v[m] = c2r_merge<T, M, E>(s, t + TT * m, twp);
+    stockham<T, M, E, 1, +1>(v, t, tw, x);
 #pragma unroll
     for (int m = 0; m < E; ++m) {
         const int j = t + TT * m;
@@ -413,7 +444,7 @@ __global__ void __launch_bounds__(512)
         if (valid) hook.post_real(x0, x1, row * real_stride + 2 * j);
         v[m] = mkc<T>(x0, x1);
     }
-    stockham<T, M, E, 1, -1>(v, t, tw, twstride, x);
+    stockham<T, M, E, 1, -1>(v, t, tw, x);
     __syncthreads();
 #pragma unroll
     for (int m = 0; m < E; ++m) x.st(t + TT * m, v[m]);
@@ -422,7 +453,7 @@ __global__ void __launch_bounds__(512)
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const int k = t + TT * m;
-            rowp[k] = r2c_split<T, M, E>(s, k, tw, twstride2);
+            rowp[k] = r2c_split<T, M, E>(s, k, twp);
         }
         if (t == 0) {
             const cplx<T> z0 = s[0];

@@ -1,4 +1,5 @@
 // FP64 instantiations of the FFT engine + shared host helpers (geometry, twiddle tables).
+#include <algorithm>
 #include <cmath>
 
 #include "fft_dispatch.cuh"
@@ -22,18 +23,55 @@ Geometry make_geometry(int ndim, const uint64_t* dims, int pitch_align) {
     return g;
 }
 
+namespace {
+
+constexpr long double kTwoPi = 6.283185307179586476925286766559005768L;
+
 template <class T>
-void Twiddles<T>::init() {
+cplx<T>* upload(const std::vector<cplx<T>>& h) {
+    cplx<T>* d = nullptr;
+    FFCZ_CUDA_CHECK(cudaMalloc(&d, sizeof(cplx<T>) * std::max<size_t>(1, h.size())));
+    FFCZ_CUDA_CHECK(cudaMemcpy(d, h.data(), sizeof(cplx<T>) * h.size(), cudaMemcpyHostToDevice));
+    return d;
+}
+
+// exp(-2 pi i num / den), evaluated in long double and rounded once
+template <class T>
+cplx<T> wexp(long long num, long long den) {
+    const long double a = -kTwoPi * static_cast<long double>(num % den) / static_cast<long double>(den);
+    cplx<T> w;
+    w.x = static_cast<T>(std::cos(a));
+    w.y = static_cast<T>(std::sin(a));
+    return w;
+}
+
+} // namespace
+
+template <class T>
+const cplx<T>* Twiddles<T>::stage_table(int L, int E) {
     std::lock_guard<std::mutex> lk(mu);
-    if (W) return;
-    std::vector<cplx<T>> h(kLmax);
-    for (int q = 0; q < kLmax; ++q) {
-        const long double a = -2.0L * 3.14159265358979323846264338327950288L * q / kLmax;
-        h[q].x = static_cast<T>(std::cos(a));
-        h[q].y = static_cast<T>(std::sin(a));
+    auto key = std::make_pair(L, E);
+    auto it = stage.find(key);
+    if (it != stage.end()) return it->second;
+    std::vector<cplx<T>> h;
+    for (int ns = 1; ns < L;) {
+        const int R = (L / ns >= E) ? E : L / ns;
+        if (ns > 1)
+            for (int k = 0; k < ns; ++k) h.push_back(wexp<T>(k, static_cast<long long>(ns) * R));
+        ns *= R;
     }
-    FFCZ_CUDA_CHECK(cudaMalloc(&W, sizeof(cplx<T>) * kLmax));
-    FFCZ_CUDA_CHECK(cudaMemcpy(W, h.data(), sizeof(cplx<T>) * kLmax, cudaMemcpyHostToDevice));
+    if (h.empty()) h.push_back(wexp<T>(0, 1));
+    return stage[key] = upload<T>(h);
+}
+
+template <class T>
+const cplx<T>* Twiddles<T>::post_table(int M) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = post.find(M);
+    if (it != post.end()) return it->second;
+    std::vector<cplx<T>> h(M + 1);
+    for (int k = 0; k <= M; ++k) h[k] = wexp<T>(k, 2LL * M);
+    return post[M] = upload<T>(h);
 }
 
 template <class T>
@@ -42,21 +80,14 @@ const cplx<T>* Twiddles<T>::table_for(long long L) {
     auto it = direct.find(L);
     if (it != direct.end()) return it->second;
     std::vector<cplx<T>> h(L);
-    for (long long q = 0; q < L; ++q) {
-        const long double a = -2.0L * 3.14159265358979323846264338327950288L * q / L;
-        h[q].x = static_cast<T>(std::cos(a));
-        h[q].y = static_cast<T>(std::sin(a));
-    }
-    cplx<T>* d = nullptr;
-    FFCZ_CUDA_CHECK(cudaMalloc(&d, sizeof(cplx<T>) * L));
-    FFCZ_CUDA_CHECK(cudaMemcpy(d, h.data(), sizeof(cplx<T>) * L, cudaMemcpyHostToDevice));
-    direct[L] = d;
-    return d;
+    for (long long q = 0; q < L; ++q) h[q] = wexp<T>(q, L);
+    return direct[L] = upload<T>(h);
 }
 
 template <class T>
 Twiddles<T>::~Twiddles() {
-    if (W) cudaFree(W);
+    for (auto& kv : stage) cudaFree(kv.second);
+    for (auto& kv : post) cudaFree(kv.second);
     for (auto& kv : direct) cudaFree(kv.second);
 }
 
@@ -83,5 +114,21 @@ template void launch_row_fused<double, HookSClip<double>>(long long, double2*, l
                                                           long long, long long, double,
                                                           Twiddles<double>&, const int*,
                                                           HookSClip<double>, cudaStream_t);
+// FP64 gate: fused escape-repair rounds and verify
+#define FFCZ_ROW_FUSED(H)                                                                     \
+    template void launch_row_fused<double, H>(long long, double2*, long long, long long,      \
+                                              long long, double, Twiddles<double>&, const int*, \
+                                              H, cudaStream_t);
+FFCZ_ROW_FUSED(HookRepairS<float>)
+FFCZ_ROW_FUSED(HookRepairS<double>)
+FFCZ_ROW_FUSED(HookVerifyS<float>)
+FFCZ_ROW_FUSED(HookVerifyS<double>)
+#undef FFCZ_ROW_FUSED
+template void launch_col<double, HookMarkViol>(long long, int, const double2*, double2*, long long,
+                                               long long, long long, int, Twiddles<double>&,
+                                               const int*, HookMarkViol, cudaStream_t);
+template void launch_col<double, HookVerifyF>(long long, int, const double2*, double2*, long long,
+                                              long long, long long, int, Twiddles<double>&,
+                                              const int*, HookVerifyF, cudaStream_t);
 
 } // namespace ffcz_gpu

@@ -12,9 +12,25 @@
 namespace ffcz_gpu {
 
 constexpr int kLmax = 8192;   // largest pow2 row length n2 / column length handled by the radix path
-// elements per thread (= radix of the full Stockham stages): 16 complex FP32 / 8 complex FP64
-// keeps the line in <= 64 registers so 512-thread CTAs run without spills
-template <class T> constexpr int kRadixE = sizeof(T) == 8 ? 8 : 16;
+
+// Elements per thread E (= radix of the full Stockham stages) for an L-point line: the fewest
+// stages (= fewest shared-memory exchanges) with at most 64 registers of line data
+// (FP64: 8 or 16 complex, FP32: 16 or 32), the smaller E on a tie.
+__host__ __device__ constexpr int nstages_c(int L, int E) {
+    int s = 0;
+    for (int ns = 1; ns < L; ns *= (L / ns >= E ? E : L / ns)) ++s;
+    return s;
+}
+#ifndef FFCZ_E64_MAX
+#define FFCZ_E64_MAX 16
+#endif
+template <class T>
+__host__ __device__ constexpr int pick_E(int L) {
+    constexpr int lo = sizeof(T) == 8 ? 8 : 16;
+    constexpr int hi = sizeof(T) == 8 ? FFCZ_E64_MAX : 32;
+    if (L <= lo) return L;
+    return (hi > lo && nstages_c(L, hi) < nstages_c(L, lo)) ? hi : lo;
+}
 
 // Geometry of a field and its pitched half spectrum.
 struct Geometry {
@@ -27,7 +43,7 @@ struct Geometry {
     int P = 0;                   // pitch in complex elements
     long long half_elems() const { return rows * P; }
     long long Nc() const { return rows * H; }
-    HalfGeom hg() const { return HalfGeom{rows, H, P, n2}; }
+    HalfGeom hg() const { return HalfGeom{rows, H, P, n2, 1.0 / H}; }
 };
 
 Geometry make_geometry(int ndim, const uint64_t* dims, int pitch_align);
@@ -35,11 +51,14 @@ Geometry make_geometry(int ndim, const uint64_t* dims, int pitch_align);
 // Twiddle tables, FP64-derived (long double on the host, rounded once).
 template <class T>
 struct Twiddles {
-    cplx<T>* W = nullptr;                       // W[q] = exp(-2 pi i q / kLmax), q < kLmax
-    std::map<long long, cplx<T>*> direct;      // per-L tables for the direct (non-2^k) passes
+    std::map<std::pair<int, int>, cplx<T>*> stage;  // (L, E) -> Stockham stage table
+    std::map<int, cplx<T>*> post;                   // M -> W_{2M}^k, k in [0, M]
+    std::map<long long, cplx<T>*> direct;           // L -> W_L^q, q < L (direct passes)
     std::mutex mu;
-    const cplx<T>* table_for(long long L);     // W_L, length L
-    void init();
+    const cplx<T>* stage_table(int L, int E);
+    const cplx<T>* post_table(int M);
+    const cplx<T>* table_for(long long L);
+    void init() {}
     ~Twiddles();
 };
 

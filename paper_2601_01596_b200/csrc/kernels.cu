@@ -15,17 +15,44 @@ __device__ __forceinline__ void set_bit(unsigned* words, long long i) {
     atomicOr(&words[i >> 5], 1u << (i & 31));
 }
 
+// Grid-stride walk over the logical half grid h = row*H + k2 without a 64-bit division per
+// element (one division per thread, then carry arithmetic).
+struct HalfWalk {
+    long long i, row, total, stride, dq;
+    int k2, H, dr;
+    __device__ __forceinline__ explicit HalfWalk(const HalfGeom& g) {
+        H = g.H;
+        total = g.rows * g.H;
+        i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+        stride = static_cast<long long>(gridDim.x) * blockDim.x;
+        row = i / H;
+        k2 = static_cast<int>(i - row * H);
+        dq = stride / H;
+        dr = static_cast<int>(stride - dq * H);
+    }
+    __device__ __forceinline__ bool ok() const { return i < total; }
+    // the whole block's window is still inside the grid (for ballot-based kernels)
+    __device__ __forceinline__ bool block_ok() const { return i - threadIdx.x < total; }
+    __device__ __forceinline__ void next() {
+        i += stride;
+        row += dq;
+        k2 += dr;
+        if (k2 >= H) {
+            k2 -= H;
+            ++row;
+        }
+    }
+};
+
 } // namespace
 
 __global__ void k_freduce(const double2* __restrict__ spec, HalfGeom g, FreqB fb, double fscale,
                           Ctl* ctl, const int* gate) {
     if (gated(gate)) return;
     HookFReduce h{fb, fscale, ctl};
-    const long long total = g.rows * g.H;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long row = i / g.H;
-        const int k2 = static_cast<int>(i - row * g.H);
+    for (HalfWalk w(g); w.ok(); w.next()) {
+        const long long i = w.i, row = w.row;
+        const int k2 = w.k2;
         const long long off = row * g.P + k2;
         double2 v = spec[off];
         h.post(v, off, k2);
@@ -37,11 +64,9 @@ __global__ void k_fclip(double2* spec, HalfGeom g, FreqB fb, double fscale, doub
                         const int* gate) {
     if (gated(gate)) return;
     HookFClip<double> h{fb, fscale, F};
-    const long long total = g.rows * g.H;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long row = i / g.H;
-        const int k2 = static_cast<int>(i - row * g.H);
+    for (HalfWalk w(g); w.ok(); w.next()) {
+        const long long i = w.i, row = w.row;
+        const int k2 = w.k2;
         const long long off = row * g.P + k2;
         double2 v = spec[off];
         h.pre(v, off, k2);
@@ -139,11 +164,9 @@ __global__ void k_count_spatial(const double* __restrict__ S, long long N, Ctl* 
 
 __global__ void k_count_freq(const double2* __restrict__ F, HalfGeom g, Ctl* ctl) {
     unsigned long long c = 0;
-    const long long total = g.rows * g.H;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long row = i / g.H;
-        const int k2 = static_cast<int>(i - row * g.H);
+    for (HalfWalk w(g); w.ok(); w.next()) {
+        const long long i = w.i, row = w.row;
+        const int k2 = w.k2;
         const double2 v = F[row * g.P + k2];
         if (v.x != 0.0 || v.y != 0.0) c += plane_weight(k2, g.n2);
     }
@@ -152,11 +175,9 @@ __global__ void k_count_freq(const double2* __restrict__ F, HalfGeom g, Ctl* ctl
 }
 
 __global__ void k_gather_half(const double* __restrict__ full, double* half, HalfGeom g) {
-    const long long total = g.rows * g.H;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long row = i / g.H;
-        const int k2 = static_cast<int>(i - row * g.H);
+    for (HalfWalk w(g); w.ok(); w.next()) {
+        const long long i = w.i, row = w.row;
+        const int k2 = w.k2;
         half[row * g.P + k2] = full[row * g.n2 + k2];
     }
 }
@@ -221,14 +242,13 @@ __global__ void k_gate_freq(const double2* __restrict__ F, HalfGeom g, FreqB fb,
                             double2* freq_cur, unsigned* keep_words, unsigned* esc_words,
                             Ctl* ctl) {
     const long long total = g.rows * g.H;
-    for (long long base = blockIdx.x * (long long)blockDim.x; base < total;
-         base += (long long)gridDim.x * blockDim.x) {
-        const long long h = base + threadIdx.x;
+    for (HalfWalk hw(g); hw.block_ok(); hw.next()) {
+        const long long h = hw.i;
         bool keep = false, ovf = false;
         int w = 0;
         if (h < total) {
-            const long long row = h / g.H;
-            const int k2 = static_cast<int>(h - row * g.H);
+            const long long row = hw.row;
+            const int k2 = hw.k2;
             const long long off = row * g.P + k2;
             const double2 v = F[off];
             const bool nz = v.x != 0.0 || v.y != 0.0;
@@ -338,9 +358,7 @@ __global__ void k_codes_freq(const unsigned long long* __restrict__ idx, long lo
                              int* codes) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        const long long h = idx[i];
-        const long long row = h / g.H;
-        const long long off = row * g.P + (h - row * g.H);
+        const long long off = g.offset_of(static_cast<long long>(idx[i]));
         const double2 v = F[off];
         const double sre = ldexp(2.0 * fb.re_at(off), -m);
         const double sim = ldexp(2.0 * fb.im_at(off), -m);
@@ -382,11 +400,9 @@ __global__ void k_repair_freq(const double2* __restrict__ delta_star,
                               unsigned* esc_words, Ctl* ctl) {
     // pipeline.cpp:140-153; half rows are (k0, k1) of a 3-D grid padded as (d0, d1)
     bool dirty = false;
-    const long long total = g.rows * g.H;
-    for (long long h = blockIdx.x * (long long)blockDim.x + threadIdx.x; h < total;
-         h += (long long)gridDim.x * blockDim.x) {
-        const long long row = h / g.H;
-        const int k2 = static_cast<int>(h - row * g.H);
+    for (HalfWalk w(g); w.ok(); w.next()) {
+        const long long h = w.i, row = w.row;
+        const int k2 = w.k2;
         auto violates = [&](long long r) {
             const long long off = r * g.P + k2;
             const double2 d = delta_tilde[off];
@@ -460,11 +476,8 @@ template __global__ void k_verify_spatial<double>(const double*, const double*, 
 
 __global__ void k_verify_freq(const double2* __restrict__ delta, HalfGeom g, FreqB fb, Ctl* ctl) {
     double m = 0.0;
-    const long long total = g.rows * g.H;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long row = i / g.H;
-        const long long off = row * g.P + (i - row * g.H);
+    for (HalfWalk w(g); w.ok(); w.next()) {
+        const long long off = w.row * g.P + w.k2;
         const double2 d = delta[off];
         const double ex = fmax(fabs(d.x) - fb.re_at(off), fabs(d.y) - fb.im_at(off));  // :290-292
         if (ex > 0.0 && ex > m) m = ex;
@@ -483,20 +496,16 @@ __global__ void k_gather_escapes_f(const unsigned long long* __restrict__ idx, l
                                    const double2* __restrict__ freq_cur, HalfGeom g, double2* out) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        const long long h = idx[i];
-        const long long row = h / g.H;
-        out[i] = freq_cur[row * g.P + (h - row * g.H)];
+        out[i] = freq_cur[g.offset_of(static_cast<long long>(idx[i]))];
     }
 }
 
 __global__ void k_split_hermitian(const double2* __restrict__ full, double2* Hh, double2* Ah,
                                   HalfGeom g, long long d0, long long d1) {
     // Re(ifft X) = C2R(H), Im(ifft X) = C2R(A) with H = (X + conj X_m)/2, A = (X - conj X_m)/(2i)
-    const long long total = g.rows * g.H;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long row = i / g.H;
-        const long long k2 = i - row * g.H;
+    for (HalfWalk w(g); w.ok(); w.next()) {
+        const long long i = w.i, row = w.row;
+        const int k2 = w.k2;
         const long long k1 = row % d1, k0 = row / d1;
         const long long mrow = (k0 ? d0 - k0 : 0) * d1 + (k1 ? d1 - k1 : 0);
         const long long mk2 = k2 ? g.n2 - k2 : 0;
@@ -514,6 +523,57 @@ __global__ void k_maxabs(const double* __restrict__ x, long long N, unsigned lon
          n += (long long)gridDim.x * blockDim.x)
         m = fmax(m, fabs(x[n]));
     block_max2_atomic(m, 0.0, out, nullptr);
+}
+
+__global__ void k_repair_freq_sparse(const unsigned* __restrict__ viol_words, long long nwords,
+                                     const double2* __restrict__ delta_star,
+                                     const double2* __restrict__ delta_tilde, HalfGeom g,
+                                     long long d0, long long d1, double2* freq_cur,
+                                     unsigned* esc_words) {
+    for (long long wi = blockIdx.x * (long long)blockDim.x + threadIdx.x; wi < nwords;
+         wi += (long long)gridDim.x * blockDim.x) {
+        unsigned bits = viol_words[wi];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const long long off = wi * 32 + b;
+            const long long row = off / g.P;
+            const int k2 = static_cast<int>(off - row * g.P);
+            auto repaired = [&](long long o) {
+                const double2 c = freq_cur[o], s = delta_star[o], t = delta_tilde[o];
+                return make_double2(c.x + (s.x - t.x), c.y + (s.y - t.y));
+            };
+            const bool plane = (k2 == 0) || (2LL * k2 == g.n2);
+            long long mrow = row;
+            if (plane) {
+                const long long k1 = row % d1, k0 = row / d1;
+                mrow = (k0 ? d0 - k0 : 0) * d1 + (k1 ? d1 - k1 : 0);
+            }
+            if (mrow == row) {
+                freq_cur[off] = repaired(off);
+                set_bit(esc_words, row * g.H + k2);
+                continue;
+            }
+            // conjugate pair inside the half grid: the reference visits indices in ascending
+            // order, so the larger index's repair wins when both violate (pipeline.cpp:141-152)
+            const long long moff = mrow * g.P + k2;
+            const bool mviol = (viol_words[moff >> 5] >> (moff & 31)) & 1u;
+            if (row > mrow && mviol) continue;  // the smaller partner handles the pair
+            const long long lo = row < mrow ? off : moff, hi = row < mrow ? moff : off;
+            const bool hi_viol = row < mrow ? mviol : true;
+            double2 r = hi_viol ? repaired(hi) : repaired(lo);
+            const double2 rc = make_double2(r.x, -r.y);
+            if (hi_viol) {
+                freq_cur[hi] = r;
+                freq_cur[lo] = rc;
+            } else {
+                freq_cur[lo] = r;
+                freq_cur[hi] = rc;
+            }
+            set_bit(esc_words, row * g.H + k2);
+            set_bit(esc_words, mrow * g.H + k2);
+        }
+    }
 }
 
 } // namespace ffcz_gpu

@@ -168,6 +168,128 @@ struct HookSClip {
     __device__ __forceinline__ void finish() {}
 };
 
+// ---- FP64 gate hooks (fused into the round / verify passes) -----------------------------------------
+
+__device__ __forceinline__ void set_bit_g(unsigned* words, long long i) {
+    atomicOr(&words[i >> 5], 1u << (i & 31));
+}
+
+template <class TI> struct Pair2;
+template <> struct Pair2<float> { using type = float2; };
+template <> struct Pair2<double> { using type = double2; };
+
+template <class TI>
+__device__ __forceinline__ double2 load_pair(const TI* p, long long n) {
+    const typename Pair2<TI>::type v = *reinterpret_cast<const typename Pair2<TI>::type*>(p + n);
+    return make_double2(static_cast<double>(v.x), static_cast<double>(v.y));
+}
+
+// Escape repair, spatial side (pipeline.cpp:125-136, 154-160), on the real outputs of the C2R
+// half of a fused last-axis pass: eps_tilde = eps0 + spat_cur + Re(IFFT(freq_cur)); components
+// violating the ORIGINAL E are pinned to spat_cur + (final_eps - eps_tilde).  The value handed on
+// to the R2C half is eps_tilde itself, so eps_tilde never touches HBM.
+template <class TI>
+struct HookRepairS {
+    const TI* orig;
+    const TI* dec;
+    double* spat_cur;
+    const double* final_eps;
+    SpatialB sb;
+    unsigned* esc_words;
+    Ctl* ctl;
+    int dirty = 0;
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    __device__ __forceinline__ void post_real(double& x0, double& x1, long long n) {
+        const double2 o = load_pair(orig, n), d = load_pair(dec, n);
+        double2 sc = *reinterpret_cast<const double2*>(spat_cur + n);
+        const double e0 = d.x - o.x, e1 = d.y - o.y;
+        const double t0 = e0 + sc.x + x0, t1 = e1 + sc.y + x1;
+        bool w = false;
+        if (fabs(t0) > sb.at(n)) {
+            sc.x = sc.x + (final_eps[n] - t0);
+            set_bit_g(esc_words, n);
+            w = true;
+        }
+        if (fabs(t1) > sb.at(n + 1)) {
+            sc.y = sc.y + (final_eps[n + 1] - t1);
+            set_bit_g(esc_words, n + 1);
+            w = true;
+        }
+        if (w) {
+            *reinterpret_cast<double2*>(spat_cur + n) = sc;
+            dirty = 1;
+        }
+        x0 = t0;
+        x1 = t1;
+    }
+    __device__ __forceinline__ void finish() {
+        if (__syncthreads_or(dirty) && threadIdx.x == 0) ctl->dirty = 1;
+    }
+};
+
+// apply_edits + verify_bounds, spatial side (archive.cpp:262-287): corrected = dec + spat_cur +
+// Re(IFFT(freq_cur)) is written out, eps = corrected - orig goes on to the R2C half.
+template <class TI>
+struct HookVerifyS {
+    const TI* orig;
+    const TI* dec;
+    const double* spat_cur;
+    double* corrected;
+    SpatialB sb;
+    Ctl* ctl;
+    double m = 0.0;
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    __device__ __forceinline__ void post_real(double& x0, double& x1, long long n) {
+        const double2 o = load_pair(orig, n), d = load_pair(dec, n);
+        const double2 sc = *reinterpret_cast<const double2*>(spat_cur + n);
+        const double c0 = d.x + sc.x + x0, c1 = d.y + sc.y + x1;
+        *reinterpret_cast<double2*>(corrected + n) = make_double2(c0, c1);
+        x0 = c0 - o.x;
+        x1 = c1 - o.y;
+        const double ex0 = fabs(x0) - sb.at(n), ex1 = fabs(x1) - sb.at(n + 1);
+        if (ex0 > 0.0 && ex0 > m) m = ex0;
+        if (ex1 > 0.0 && ex1 > m) m = ex1;
+    }
+    __device__ __forceinline__ void finish() { block_max2_atomic(m, 0.0, &ctl->vs_bits, nullptr); }
+};
+
+// Frequency check of an escape-repair round (pipeline.cpp:140-147): marks violating components
+// of delta_tilde (against the ORIGINAL Delta) in a bitmap over storage offsets; the repair itself
+// is done sparsely afterwards (k_repair_freq_sparse) because conjugate partners live in other
+// columns.
+struct HookMarkViol {
+    FreqB fb;
+    unsigned* viol_words;
+    Ctl* ctl;
+    int any = 0;
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    template <class C>
+    __device__ __forceinline__ void post(C& v, long long off, int) {
+        if (fabs(v.x) > fb.re_at(off) || fabs(v.y) > fb.im_at(off)) {
+            set_bit_g(viol_words, off);
+            any = 1;
+        }
+    }
+    __device__ __forceinline__ void finish() {
+        if (__syncthreads_or(any) && threadIdx.x == 0) ctl->dirty = 1;
+    }
+};
+
+// verify_bounds, frequency side (archive.cpp:288-294): max positive excess; output not stored.
+struct HookVerifyF {
+    static constexpr bool kNoStore = true;
+    FreqB fb;
+    Ctl* ctl;
+    double m = 0.0;
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    template <class C>
+    __device__ __forceinline__ void post(C& v, long long off, int) {
+        const double ex = fmax(fabs(v.x) - fb.re_at(off), fabs(v.y) - fb.im_at(off));
+        if (ex > 0.0 && ex > m) m = ex;
+    }
+    __device__ __forceinline__ void finish() { block_max2_atomic(m, 0.0, &ctl->vf_bits, nullptr); }
+};
+
 // ---- elementwise kernels (unfused path / generic shapes) -------------------------------------------
 
 struct HalfGeom {
@@ -175,6 +297,14 @@ struct HalfGeom {
     int H;           // n2/2 + 1
     int P;           // pitch
     long long n2;
+    double invH;     // 1.0 / H
+    // storage offset of half-grid index h = row*H + k2 (no 64-bit integer division)
+    __device__ __forceinline__ long long offset_of(long long h) const {
+        long long q = static_cast<long long>(static_cast<double>(h) * invH);
+        long long r = h - q * H;
+        if (r < 0) { --q; r += H; } else if (r >= H) { ++q; r -= H; }
+        return q * P + r;
+    }
 };
 
 // check_convergence over the half spectrum (projection.cpp:29-52)
@@ -248,6 +378,12 @@ __global__ void k_verify_spatial(const TI* __restrict__ orig, const TI* __restri
                                  const double* __restrict__ fpart, long long N, SpatialB sb,
                                  double* corrected, double* eps_v, Ctl* ctl);
 __global__ void k_verify_freq(const double2* __restrict__ delta, HalfGeom g, FreqB fb, Ctl* ctl);
+// sparse frequency repair from the violation bitmap of HookMarkViol (pipeline.cpp:140-153)
+__global__ void k_repair_freq_sparse(const unsigned* __restrict__ viol_words, long long nwords,
+                                     const double2* __restrict__ delta_star,
+                                     const double2* __restrict__ delta_tilde, HalfGeom g,
+                                     long long d0, long long d1, double2* freq_cur,
+                                     unsigned* esc_words);
 __global__ void k_gather_escapes_s(const unsigned long long* __restrict__ idx, long long n,
                                    const double* __restrict__ spat_cur, double* out_re);
 __global__ void k_gather_escapes_f(const unsigned long long* __restrict__ idx, long long n,
