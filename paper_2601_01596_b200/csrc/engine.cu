@@ -25,6 +25,55 @@ using namespace ffcz_gpu;
 
 double bitsd_host(unsigned long long b);
 
+namespace {
+
+// Process-wide pool of pinned host blocks backing library-owned result buffers: D2H of the edit
+// set and the corrected field runs at full PCIe speed and repeated calls reuse the pinned pages.
+struct PinnedPool {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_blocks;
+    std::map<void*, size_t> sizes;
+    void* get(size_t bytes) {
+        bytes = std::max<size_t>(bytes, 64);
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = free_blocks.lower_bound(bytes);
+        if (it != free_blocks.end() && it->first <= 2 * bytes + (1 << 20)) {
+            void* p = it->second;
+            free_blocks.erase(it);
+            return p;
+        }
+        void* p = nullptr;
+        if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            p = std::malloc(bytes);  // pageable fallback (still correct, slower copies)
+            if (!p) throw std::bad_alloc();
+            sizes[p] = 0;
+        } else {
+            sizes[p] = bytes;
+        }
+        return p;
+    }
+    void put(void* p) {
+        if (!p) return;
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = sizes.find(p);
+        if (it == sizes.end()) return;
+        if (it->second == 0) {
+            std::free(p);
+            sizes.erase(it);
+        } else {
+            free_blocks.emplace(it->second, p);
+        }
+    }
+};
+
+PinnedPool& pinned() {
+    static PinnedPool* pool = new PinnedPool;  // never destroyed: results may outlive contexts
+    return *pool;
+}
+
+} // namespace
+
 struct ffcz_cuda_ctx {
     int device = 0;
     cudaStream_t st = nullptr;
@@ -82,9 +131,12 @@ struct ffcz_cuda_ctx {
 
 namespace {
 
-enum ProfClass { kColFwdCheck = 0, kColClipInv, kColPass, kRowR2C, kRowC2R, kRowFused, kNumProf };
+enum ProfClass { kColFwdCheck = 0, kColClipInv, kColPass, kRowR2C, kRowC2R, kRowFused,
+                 kElemPre, kElemGate, kElemCompact, kElemCodes, kNumProf };
 const char* kProfNames[kNumProf] = {"col_fwd_check (K3a)", "col_clip_inv (K3b)", "col_pass",
-                                    "row_r2c", "row_c2r", "row_c2r_sclip_r2c (K1)"};
+                                    "row_r2c", "row_c2r", "row_c2r_sclip_r2c (K1)",
+                                    "elem_bounds_eps0_residual", "elem_gate_quantize",
+                                    "elem_compact", "elem_codes"};
 
 // RAII event pair around one launch when profiling is on
 struct Prof {
@@ -175,7 +227,10 @@ Bounds upload_bounds(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_bounds_desc
                 dfull = stage;
             }
             double* half = c.b<double>(name, g.half_elems());
-            k_gather_half<<<grid_for(g.Nc()), 256, 0, c.st>>>(dfull, half, hg);
+            {
+                Prof p(c, kElemPre, 16.0 * g.Nc());
+                k_gather_half<<<grid_for(g.Nc()), 256, 0, c.st>>>(dfull, half, hg);
+            }
             FFCZ_LAUNCH_CHECK();
             ++c.launches;
             return half;
@@ -207,11 +262,13 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
     FftPlan<double> plan{g, &c.tw64};
     const int* gate = &c.ctl->done;
     double2* spec = c.b<double2>("spec", g.half_elems());
-    FFCZ_CUDA_CHECK(cudaMemsetAsync(S, 0, g.N * sizeof(double), st));
-    FFCZ_CUDA_CHECK(cudaMemsetAsync(F, 0, g.half_elems() * sizeof(double2), st));
     const double invN = 1.0 / static_cast<double>(g.N);
     const HalfGeom hg = g.hg();
     const bool fused = allow_fused && plan.fused_ok();
+    if (!fused) {  // the fused hooks write S and F densely on the first clip instead
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(S, 0, g.N * sizeof(double), st));
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(F, 0, g.half_elems() * sizeof(double2), st));
+    }
     const bool three_d = g.d[0] > 1;
     const int za = three_d ? 0 : 1;  // the pass that completes the forward transform
     double* tmp = fused ? nullptr : c.b<double>("real_tmp", g.N);
@@ -229,7 +286,7 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
             k_decide<<<1, 1, 0, st>>>(c.ctl);                                              // K4
             {
                 Prof p(c, kColClipInv, check_bytes);
-                plan.col(za, +1, spec, spec, gate, HookFClip<double>{bw.fb, fscale, F}, st); // K3b
+                plan.col(za, +1, spec, spec, gate, HookFClip<double>{bw.fb, fscale, F, c.ctl}, st); // K3b
             }
             if (three_d) {
                 Prof p(c, kColPass, pass_bytes);
@@ -238,7 +295,7 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
             {
                 Prof p(c, kRowFused, fused_bytes);
                 launch_row_fused<double>(g.n2, spec, g.P, g.rows, g.n2, invN, c.tw64, gate,
-                                         HookSClip<double>{bw.sb, fscale, S, eps}, st);  // K1
+                                         HookSClip<double>{bw.sb, fscale, S, eps, c.ctl}, st);  // K1
             }
             if (three_d) {
                 Prof p(c, kColPass, pass_bytes);
@@ -297,6 +354,10 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
         if (c.hctl[1 + p.slot].done) break;
     }
     const Ctl h = c.read_ctl();
+    if (fused && h.passes == 0) {  // converged at the first check: no clip ever wrote S / F
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(S, 0, g.N * sizeof(double), st));
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(F, 0, g.half_elems() * sizeof(double2), st));
+    }
     LoopResult r;
     r.passes = h.passes;
     r.converged = h.converged;
@@ -317,9 +378,12 @@ unsigned long long compact_bits(ffcz_cuda_ctx& c, const unsigned* words, long lo
                                 unsigned long long* idx) {
     const long long nblk = std::max<long long>(1, (nwords + 1023) / 1024);
     unsigned long long* counts = c.b<unsigned long long>("blk_counts", nblk + 1);
-    k_popc_blocks<<<static_cast<unsigned>(nblk), 1024, 0, c.st>>>(words, nwords, counts);
-    k_scan_blocks<<<1, 1024, 0, c.st>>>(counts, nblk, &c.ctl->count_a);
-    k_compact<<<static_cast<unsigned>(nblk), 1024, 0, c.st>>>(words, nwords, counts, idx);
+    {
+        Prof p(c, kElemCompact, 0.0);
+        k_popc_blocks<<<static_cast<unsigned>(nblk), 1024, 0, c.st>>>(words, nwords, counts);
+        k_scan_blocks<<<1, 1024, 0, c.st>>>(counts, nblk, &c.ctl->count_a);
+        k_compact<<<static_cast<unsigned>(nblk), 1024, 0, c.st>>>(words, nwords, counts, idx);
+    }
     FFCZ_LAUNCH_CHECK();
     c.launches += 3;
     return c.read_ctl().count_a;
@@ -387,16 +451,25 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
     double* eps_t = fused ? nullptr : c.b<double>("eps_tilde", N);
 
     FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->act_s, 0, 2 * sizeof(unsigned long long), st));
-    k_gate_spatial<<<grid_for(N), 256, 0, st>>>(S, N, bo.sb, m, spat_cur, keep_s, esc_s, c.ctl);
-    k_gate_freq<<<grid_for(Nc), 256, 0, st>>>(F, hg, bo.fb, m, freq_cur, keep_f, esc_f, c.ctl);
+    {
+        Prof p(c, kElemGate, 16.0 * N + 32.0 * Nc);
+        k_gate_spatial<<<grid_for(N), 256, 0, st>>>(S, N, bo.sb, m, spat_cur, keep_s, esc_s, c.ctl);
+        k_gate_freq<<<grid_for(Nc), 256, 0, st>>>(F, hg, bo.fb, m, freq_cur, keep_f, esc_f, c.ctl);
+    }
     FFCZ_LAUNCH_CHECK();
     c.launches += 2;
 
     GateOut o;
     o.n_keep_s = compact_bits(c, keep_s, ws, idx);
-    k_codes_spatial<<<grid_for(o.n_keep_s), 256, 0, st>>>(idx, o.n_keep_s, S, bo.sb, m, codes_s);
+    {
+        Prof p(c, kElemCodes, 0.0);
+        k_codes_spatial<<<grid_for(o.n_keep_s), 256, 0, st>>>(idx, o.n_keep_s, S, bo.sb, m, codes_s);
+    }
     o.n_keep_f = compact_bits(c, keep_f, wf, idx);
-    k_codes_freq<<<grid_for(o.n_keep_f), 256, 0, st>>>(idx, o.n_keep_f, F, hg, bo.fb, m, codes_f);
+    {
+        Prof p(c, kElemCodes, 0.0);
+        k_codes_freq<<<grid_for(o.n_keep_f), 256, 0, st>>>(idx, o.n_keep_f, F, hg, bo.fb, m, codes_f);
+    }
     FFCZ_LAUNCH_CHECK();
     c.launches += 2;
 
@@ -526,7 +599,10 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     double* eps = c.b<double>("eps", N);
     const double f = 1.0 - std::ldexp(1.0, -m);
     const double slack = 1.0 / (1.0 - std::ldexp(1.0, -m)) - 1.0 + 0x1p-20;
-    k_eps0<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, eps, N, bo.sb, f, slack, 1, c.ctl);
+    {
+        Prof p(c, kElemPre, (2.0 * sizeof(TI) + 8.0) * N);
+        k_eps0<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, eps, N, bo.sb, f, slack, 1, c.ctl);
+    }
     FFCZ_LAUNCH_CHECK();
     c.launches += 2;
     Ctl h = c.read_ctl();
@@ -544,7 +620,10 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[2], st));
     const LoopResult lr = run_loop(c, g, eps, bo, f, !(opt.flags & FFCZ_FORCE_UNFUSED), S, F);
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[3], st));
-    k_residual_s<<<grid_for(N), 256, 0, st>>>(eps, N, bo.sb, f, c.ctl);
+    {
+        Prof p(c, kElemPre, 8.0 * N);
+        k_residual_s<<<grid_for(N), 256, 0, st>>>(eps, N, bo.sb, f, c.ctl);
+    }
     ++c.launches;
 
     double* corrected = c.b<double>("corrected", N);
@@ -610,10 +689,10 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     if (want_edits) {
         out->spatial_flag_bytes = (N + 7) / 8;
         out->frequency_flag_bytes = (g.Nc() + 7) / 8;
-        out->spatial_flags = static_cast<uint8_t*>(std::malloc(out->spatial_flag_bytes + 1));
-        out->frequency_flags = static_cast<uint8_t*>(std::malloc(out->frequency_flag_bytes + 1));
-        out->spatial_codes = static_cast<int32_t*>(std::malloc(go.n_keep_s * 4 + 4));
-        out->frequency_codes = static_cast<int32_t*>(std::malloc(go.n_keep_f * 8 + 4));
+        out->spatial_flags = static_cast<uint8_t*>(pinned().get(out->spatial_flag_bytes + 1));
+        out->frequency_flags = static_cast<uint8_t*>(pinned().get(out->frequency_flag_bytes + 1));
+        out->spatial_codes = static_cast<int32_t*>(pinned().get(go.n_keep_s * 4 + 4));
+        out->frequency_codes = static_cast<int32_t*>(pinned().get(go.n_keep_f * 8 + 4));
         FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->spatial_flags, c.b<unsigned>("keep_s", ws),
                                         out->spatial_flag_bytes, cudaMemcpyDeviceToHost, st));
         FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->frequency_flags, c.b<unsigned>("keep_f", wf),
@@ -623,11 +702,11 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
         FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->frequency_codes, c.b<int>("codes_f", 2 * g.Nc()),
                                         go.n_keep_f * 8, cudaMemcpyDeviceToHost, st));
         out->escapes = static_cast<ffcz_cuda_escape*>(
-            std::malloc(sizeof(ffcz_cuda_escape) * (escapes.size() + 1)));
+            pinned().get(sizeof(ffcz_cuda_escape) * (escapes.size() + 1)));
         std::memcpy(out->escapes, escapes.data(), sizeof(ffcz_cuda_escape) * escapes.size());
     }
     if (opt.flags & FFCZ_WANT_CORRECTED) {
-        out->corrected = static_cast<double*>(std::malloc(N * sizeof(double)));
+        out->corrected = static_cast<double*>(pinned().get(N * sizeof(double)));
         FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->corrected, corrected, N * sizeof(double),
                                         cudaMemcpyDeviceToHost, st));
     }
@@ -692,7 +771,7 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
         out->t_archive_ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         out->archive_len = bytes.size();
-        out->archive = static_cast<uint8_t*>(std::malloc(bytes.size() + 1));
+        out->archive = static_cast<uint8_t*>(pinned().get(bytes.size() + 1));
         std::memcpy(out->archive, bytes.data(), bytes.size());
     }
 }
@@ -781,13 +860,13 @@ void ffcz_cuda_destroy(ffcz_cuda_ctx* c) {
 
 void ffcz_cuda_result_free(ffcz_cuda_result* r) {
     if (!r) return;
-    std::free(r->spatial_flags);
-    std::free(r->frequency_flags);
-    std::free(r->spatial_codes);
-    std::free(r->frequency_codes);
-    std::free(r->escapes);
-    std::free(r->corrected);
-    std::free(r->archive);
+    pinned().put(r->spatial_flags);
+    pinned().put(r->frequency_flags);
+    pinned().put(r->spatial_codes);
+    pinned().put(r->frequency_codes);
+    pinned().put(r->escapes);
+    pinned().put(r->corrected);
+    pinned().put(r->archive);
     std::memset(r, 0, sizeof(*r));
 }
 

@@ -3,6 +3,9 @@
 #pragma once
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "fft_plan.cuh"
 
@@ -32,6 +35,28 @@ void set_smem(K kernel, size_t bytes) {
                                              static_cast<int>(bytes)));
 }
 
+// Persistent grid: resident-CTA capacity of the device for this kernel configuration.
+template <class K>
+long long resident_ctas(K kernel, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, size_t>, long long> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), threads, smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int dev = 0, sms = 0, nb = 0;
+    FFCZ_CUDA_CHECK(cudaGetDevice(&dev));
+    FFCZ_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FFCZ_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem));
+    return cache[key] = static_cast<long long>(std::max(1, nb)) * sms;
+}
+
+template <class K>
+unsigned persistent_grid(K kernel, int threads, size_t smem, long long ntiles) {
+    return static_cast<unsigned>(std::max<long long>(
+        1, std::min<long long>(ntiles, resident_ctas(kernel, threads, smem))));
+}
+
 inline unsigned grid1(long long n, int threads) {
     long long b = (n + threads - 1) / threads;
     return static_cast<unsigned>(std::max<long long>(1, std::min<long long>(b, 148LL * 32)));
@@ -49,18 +74,12 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
     B = std::min(B, pow2_ceil(ncols));
     B = std::max(B, 1);
     const size_t smem = col_smem_bytes<T, L, E>(B);
-    dim3 grid((ncols + B - 1) / B, static_cast<unsigned>(nplanes));
-    if (dir < 0) {
-        auto k = k_col<T, L, E, -1, Hook>;
-        set_smem(k, smem);
-        k<<<grid, TT * B, smem, st>>>(src, dst, row_stride, plane_stride, ncols, B,
-                                       tw.stage_table(L, E), gate, hook);
-    } else {
-        auto k = k_col<T, L, E, +1, Hook>;
-        set_smem(k, smem);
-        k<<<grid, TT * B, smem, st>>>(src, dst, row_stride, plane_stride, ncols, B,
-                                       tw.stage_table(L, E), gate, hook);
-    }
+    const long long ntiles = static_cast<long long>((ncols + B - 1) / B) * nplanes;
+    auto k = dir < 0 ? k_col<T, L, E, -1, Hook> : k_col<T, L, E, +1, Hook>;
+    set_smem(k, smem);
+    const unsigned grid = persistent_grid(k, TT * B, smem, ntiles);
+    k<<<grid, TT * B, smem, st>>>(src, dst, row_stride, plane_stride, ncols, B, ntiles,
+                                   tw.stage_table(L, E), gate, hook);
     FFCZ_LAUNCH_CHECK();
 }
 
@@ -86,7 +105,7 @@ void row_r2c_radix(const T* in, long long in_stride, cplx<T>* out, long long out
     const size_t smem = row_smem_bytes<T, M, E>(R);
     auto k = k_row_r2c<T, M, E, HookNone>;
     set_smem(k, smem);
-    k<<<static_cast<unsigned>((nrows + R - 1) / R), TT * R, smem, st>>>(
+    k<<<persistent_grid(k, TT * R, smem, (nrows + R - 1) / R), TT * R, smem, st>>>(
         in, in_stride, out, out_stride, nrows, tw.stage_table(M, E), tw.post_table(M), gate,
         HookNone{});
     FFCZ_LAUNCH_CHECK();
@@ -100,7 +119,7 @@ void row_c2r_radix(const cplx<T>* in, long long in_stride, T* out, long long out
     const size_t smem = row_smem_bytes<T, M, E>(R);
     auto k = k_row_c2r<T, M, E, RealHookNone>;
     set_smem(k, smem);
-    k<<<static_cast<unsigned>((nrows + R - 1) / R), TT * R, smem, st>>>(
+    k<<<persistent_grid(k, TT * R, smem, (nrows + R - 1) / R), TT * R, smem, st>>>(
         in, in_stride, out, out_stride, nrows, tw.stage_table(M, E), tw.post_table(M), scale,
         gate, RealHookNone{});
     FFCZ_LAUNCH_CHECK();
@@ -114,7 +133,7 @@ void row_fused_radix(cplx<T>* data, long long stride, long long nrows, long long
     const size_t smem = row_smem_bytes<T, M, E>(R);
     auto k = k_row_c2r_r2c<T, M, E, Hook>;
     set_smem(k, smem);
-    k<<<static_cast<unsigned>((nrows + R - 1) / R), TT * R, smem, st>>>(
+    k<<<persistent_grid(k, TT * R, smem, (nrows + R - 1) / R), TT * R, smem, st>>>(
         data, stride, nrows, real_stride, tw.stage_table(M, E), tw.post_table(M), scale, gate,
         hook);
     FFCZ_LAUNCH_CHECK();

@@ -210,6 +210,12 @@ struct HookNone {
     __device__ __forceinline__ void finish() {}
 };
 
+// Optional per-CTA setup (e.g. reading loop state once): hook.begin() when the hook has one.
+template <class H>
+__device__ __forceinline__ void hook_begin(H& h) {
+    if constexpr (requires { h.begin(); }) h.begin();
+}
+
 // A hook may declare `static constexpr bool kNoStore = true` when the pass output is consumed
 // by the hook alone (e.g. the verify reduction): the store is skipped (half a pass of traffic).
 template <class H>
@@ -227,38 +233,46 @@ template <class T, int E>
 constexpr int max_threads() { return E * sizeof(cplx<T>) <= 128 ? 512 : 256; }
 
 // Launched with blockDim.x = (L/E) * B threads and (L + L/E) * B elements of dynamic smem.
+// Persistent: a grid sized to the resident-CTA capacity walks the tiles (tile = B consecutive
+// columns of one plane), so a pass launched after convergence retires in microseconds and
+// block reductions fold many tiles before their single atomic.
 template <class T, int L, int E, int DIR, class Hook>
 __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>())
     k_col(const cplx<T>* __restrict__ src, cplx<T>* __restrict__ dst, long long row_stride,
-          long long plane_stride, int ncols, int B, const cplx<T>* __restrict__ tw,
-          const int* gate, Hook hook) {
+          long long plane_stride, int ncols, int B, long long ntiles,
+          const cplx<T>* __restrict__ tw, const int* gate, Hook hook) {
     if (gated(gate)) return;
+    hook_begin(hook);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw);
     constexpr int TT = L / E;
     const int b = threadIdx.x % B;
     const int t = threadIdx.x / B;
-    const int c = blockIdx.x * B + b;
-    const bool valid = c < ncols;
-    const long long base = static_cast<long long>(blockIdx.y) * plane_stride + c;
-    cplx<T> v[E];
+    const int tiles_c = (ncols + B - 1) / B;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long plane = tile / tiles_c;
+        const int c = static_cast<int>(tile - plane * tiles_c) * B + b;
+        const bool valid = c < ncols;
+        const long long base = plane * plane_stride + c;
+        cplx<T> v[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) {
-        const long long off = base + static_cast<long long>(t + TT * m) * row_stride;
-        if (valid) {
-            v[m] = src[off];
-            hook.pre(v[m], off, c);
-        } else {
-            v[m] = mkc<T>(T(0), T(0));
+        for (int m = 0; m < E; ++m) {
+            const long long off = base + static_cast<long long>(t + TT * m) * row_stride;
+            if (valid) {
+                v[m] = src[off];
+                hook.pre(v[m], off, c);
+            } else {
+                v[m] = mkc<T>(T(0), T(0));
+            }
         }
-    }
-    stockham<T, L, E, 1, DIR>(v, t, tw, XchCol<T, E>{s + b, B});
+        stockham<T, L, E, 1, DIR>(v, t, tw, XchCol<T, E>{s + b, B});
 #pragma unroll
-    for (int m = 0; m < E; ++m) {
-        const long long off = base + static_cast<long long>(t + TT * m) * row_stride;
-        if (valid) {
-            hook.post(v[m], off, c);
-            if constexpr (hook_stores<Hook>()) dst[off] = v[m];
+        for (int m = 0; m < E; ++m) {
+            const long long off = base + static_cast<long long>(t + TT * m) * row_stride;
+            if (valid) {
+                hook.post(v[m], off, c);
+                if constexpr (hook_stores<Hook>()) dst[off] = v[m];
+            }
         }
     }
     hook.finish();
@@ -324,37 +338,42 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
               long long out_stride, long long nrows, const cplx<T>* __restrict__ tw,
               const cplx<T>* __restrict__ twp, const int* gate, Hook hook) {
     if (gated(gate)) return;
+    hook_begin(hook);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int TT = M / E;
     const int t = threadIdx.x % TT;
     const int rb = threadIdx.x / TT;
-    const long long row = static_cast<long long>(blockIdx.x) * (blockDim.x / TT) + rb;
-    const bool valid = row < nrows;
-    cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
-    const cplx<T>* src = reinterpret_cast<const cplx<T>*>(in + (valid ? row : 0) * in_stride);
-    cplx<T> v[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = valid ? src[t + TT * m] : mkc<T>(T(0), T(0));
-    const XchRow<T, E> x{s};
-    stockham<T, M, E, 1, -1>(v, t, tw, x);
-    __syncthreads();
-#pragma unroll
-    for (int m = 0; m < E; ++m) x.st(t + TT * m, v[m]);
-    __syncthreads();
-    if (valid) {
-        cplx<T>* dst = out + row * out_stride;
-#pragma unroll
-        for (int m = 0; m < E; ++m) {
-            const int k = t + TT * m;
-            cplx<T> X = r2c_split<T, M, E>(s, k, twp);
-            hook.post(X, row * out_stride + k, k);
-            dst[k] = X;
-        }
-        if (t == 0) {
-            const cplx<T> z0 = s[0];
-            cplx<T> X = mkc<T>(z0.x - z0.y, T(0));
-            hook.post(X, row * out_stride + M, M);
-            dst[M] = X;
+    const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        __syncthreads();  // smem of the previous tile fully consumed
+        const long long row = tile * (blockDim.x / TT) + rb;
+        const bool valid = row < nrows;
+        cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
+        const cplx<T>* src = reinterpret_cast<const cplx<T>*>(in + (valid ? row : 0) * in_stride);
+        cplx<T> v[E];
+    #pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = valid ? src[t + TT * m] : mkc<T>(T(0), T(0));
+        const XchRow<T, E> x{s};
+        stockham<T, M, E, 1, -1>(v, t, tw, x);
+        __syncthreads();
+    #pragma unroll
+        for (int m = 0; m < E; ++m) x.st(t + TT * m, v[m]);
+        __syncthreads();
+        if (valid) {
+            cplx<T>* dst = out + row * out_stride;
+    #pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int k = t + TT * m;
+                cplx<T> X = r2c_split<T, M, E>(s, k, twp);
+                hook.post(X, row * out_stride + k, k);
+                dst[k] = X;
+            }
+            if (t == 0) {
+                const cplx<T> z0 = s[0];
+                cplx<T> X = mkc<T>(z0.x - z0.y, T(0));
+                hook.post(X, row * out_stride + M, M);
+                dst[M] = X;
+            }
         }
     }
     hook.finish();
@@ -368,40 +387,45 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
               long long out_stride, long long nrows, const cplx<T>* __restrict__ tw,
               const cplx<T>* __restrict__ twp, T scale, const int* gate, Hook hook) {
     if (gated(gate)) return;
+    hook_begin(hook);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int TT = M / E;
     const int t = threadIdx.x % TT;
     const int rb = threadIdx.x / TT;
-    const long long row = static_cast<long long>(blockIdx.x) * (blockDim.x / TT) + rb;
-    const bool valid = row < nrows;
-    cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
-    const XchRow<T, E> x{s};
-    const cplx<T>* src = in + (valid ? row : 0) * in_stride;
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-        const int k = t + TT * m;
-        cplx<T> X = valid ? src[k] : mkc<T>(T(0), T(0));
-        hook.pre(X, row * in_stride + k, k);
-        x.st(k, X);
-    }
-    if (t == 0) {
-        cplx<T> X = valid ? src[M] : mkc<T>(T(0), T(0));
-        hook.pre(X, row * in_stride + M, M);
-        x.st(M, X);
-    }
-    __syncthreads();
-    cplx<T> v[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = c2r_merge<T, M, E>(s, t + TT * m, twp);
-    stockham<T, M, E, 1, +1>(v, t, tw, x);
-    if (valid) {
-        cplx<T>* dst = reinterpret_cast<cplx<T>*>(out + row * out_stride);
-#pragma unroll
+    const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        __syncthreads();  // smem of the previous tile fully consumed
+        const long long row = tile * (blockDim.x / TT) + rb;
+        const bool valid = row < nrows;
+        cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
+        const XchRow<T, E> x{s};
+        const cplx<T>* src = in + (valid ? row : 0) * in_stride;
+    #pragma unroll
         for (int m = 0; m < E; ++m) {
-            const int j = t + TT * m;
-            T x0 = v[m].x * scale, x1 = v[m].y * scale;
-            hook.post_real(x0, x1, row * out_stride + 2 * j);
-            dst[j] = mkc<T>(x0, x1);
+            const int k = t + TT * m;
+            cplx<T> X = valid ? src[k] : mkc<T>(T(0), T(0));
+            hook.pre(X, row * in_stride + k, k);
+            x.st(k, X);
+        }
+        if (t == 0) {
+            cplx<T> X = valid ? src[M] : mkc<T>(T(0), T(0));
+            hook.pre(X, row * in_stride + M, M);
+            x.st(M, X);
+        }
+        __syncthreads();
+        cplx<T> v[E];
+    #pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = c2r_merge<T, M, E>(s, t + TT * m, twp);
+        stockham<T, M, E, 1, +1>(v, t, tw, x);
+        if (valid) {
+            cplx<T>* dst = reinterpret_cast<cplx<T>*>(out + row * out_stride);
+    #pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int j = t + TT * m;
+                T x0 = v[m].x * scale, x1 = v[m].y * scale;
+                hook.post_real(x0, x1, row * out_stride + 2 * j);
+                dst[j] = mkc<T>(x0, x1);
+            }
         }
     }
     hook.finish();
@@ -417,47 +441,52 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
                   const cplx<T>* __restrict__ tw, const cplx<T>* __restrict__ twp, T scale,
                   const int* gate, Hook hook) {
     if (gated(gate)) return;
+    hook_begin(hook);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int TT = M / E;
     const int t = threadIdx.x % TT;
     const int rb = threadIdx.x / TT;
-    const long long row = static_cast<long long>(blockIdx.x) * (blockDim.x / TT) + rb;
-    const bool valid = row < nrows;
-    cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
-    const XchRow<T, E> x{s};
-    cplx<T>* rowp = data + (valid ? row : 0) * stride;
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-        const int k = t + TT * m;
-        x.st(k, valid ? rowp[k] : mkc<T>(T(0), T(0)));
-    }
-    if (t == 0) x.st(M, valid ? rowp[M] : mkc<T>(T(0), T(0)));
-    __syncthreads();
-    cplx<T> v[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = c2r_merge<T, M, E>(s, t + TT * m, twp);
-    stockham<T, M, E, 1, +1>(v, t, tw, x);
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-        const int j = t + TT * m;
-        T x0 = v[m].x * scale, x1 = v[m].y * scale;
-        if (valid) hook.post_real(x0, x1, row * real_stride + 2 * j);
-        v[m] = mkc<T>(x0, x1);
-    }
-    stockham<T, M, E, 1, -1>(v, t, tw, x);
-    __syncthreads();
-#pragma unroll
-    for (int m = 0; m < E; ++m) x.st(t + TT * m, v[m]);
-    __syncthreads();
-    if (valid) {
-#pragma unroll
+    const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        __syncthreads();  // smem of the previous tile fully consumed
+        const long long row = tile * (blockDim.x / TT) + rb;
+        const bool valid = row < nrows;
+        cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
+        const XchRow<T, E> x{s};
+        cplx<T>* rowp = data + (valid ? row : 0) * stride;
+    #pragma unroll
         for (int m = 0; m < E; ++m) {
             const int k = t + TT * m;
-            rowp[k] = r2c_split<T, M, E>(s, k, twp);
+            x.st(k, valid ? rowp[k] : mkc<T>(T(0), T(0)));
         }
-        if (t == 0) {
-            const cplx<T> z0 = s[0];
-            rowp[M] = mkc<T>(z0.x - z0.y, T(0));
+        if (t == 0) x.st(M, valid ? rowp[M] : mkc<T>(T(0), T(0)));
+        __syncthreads();
+        cplx<T> v[E];
+    #pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = c2r_merge<T, M, E>(s, t + TT * m, twp);
+        stockham<T, M, E, 1, +1>(v, t, tw, x);
+    #pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int j = t + TT * m;
+            T x0 = v[m].x * scale, x1 = v[m].y * scale;
+            if (valid) hook.post_real(x0, x1, row * real_stride + 2 * j);
+            v[m] = mkc<T>(x0, x1);
+        }
+        stockham<T, M, E, 1, -1>(v, t, tw, x);
+        __syncthreads();
+    #pragma unroll
+        for (int m = 0; m < E; ++m) x.st(t + TT * m, v[m]);
+        __syncthreads();
+        if (valid) {
+    #pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int k = t + TT * m;
+                rowp[k] = r2c_split<T, M, E>(s, k, twp);
+            }
+            if (t == 0) {
+                const cplx<T> z0 = s[0];
+                rowp[M] = mkc<T>(z0.x - z0.y, T(0));
+            }
         }
     }
     hook.finish();

@@ -119,18 +119,28 @@ struct HookFReduce {
 
 // project_onto_fcube + F accumulation (projection.cpp:54-66, 117-119): clamp Re and Im
 // independently; F += clipped - delta (read-modify-write only where the clamp moved the value).
+// With `ctl` set (fused loop), the first clip pass (passes == 1 after the decision) writes F
+// densely instead of read-modify-write: F is zero before it, so F = 0 + displacement exactly, and
+// the loop needs no separate zero fill of F.
 template <class T>
 struct HookFClip {
     FreqB fb;
     double fscale;
     double2* F;
+    const Ctl* ctl = nullptr;
+    bool first = false;
+    __device__ __forceinline__ void begin() {
+        first = ctl != nullptr && *reinterpret_cast<const volatile unsigned long long*>(&ctl->passes) == 1;
+    }
     template <class C>
     __device__ __forceinline__ void pre(C& v, long long off, int) {
         const double re = v.x, im = v.y;
         const double dre = fb.re_at(off) * fscale, dim = fb.im_at(off) * fscale;
         const double cre = clamp_abs(re, dre), cim = clamp_abs(im, dim);
         const double xre = cre - re, xim = cim - im;
-        if (xre != 0.0 || xim != 0.0) {
+        if (first) {
+            F[off] = make_double2(0.0 + xre, 0.0 + xim);
+        } else if (xre != 0.0 || xim != 0.0) {
             double2 f = F[off];
             f.x += xre;
             f.y += xim;
@@ -145,19 +155,26 @@ struct HookFClip {
 
 // project_onto_scube + S accumulation (projection.cpp:68-79, 121-124) on the real outputs of a
 // C2R row pass; writes the clipped epsilon (the reference's `eps = sc.clipped`).
+// Same first-pass dense write of S as HookFClip (S is zero before the first s-clip).
 template <class T>
 struct HookSClip {
     SpatialB sb;
     double fscale;
     double* S;
     T* eps;
+    const Ctl* ctl = nullptr;
+    bool first = false;
+    __device__ __forceinline__ void begin() {
+        first = ctl != nullptr && *reinterpret_cast<const volatile unsigned long long*>(&ctl->passes) == 1;
+    }
     template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
     __device__ __forceinline__ T one(T x, long long n) const {
         const double xd = x;
         const double e = sb.at(n) * fscale;
         const double c = clamp_abs(xd, e);
         const double d = c - xd;
-        if (d != 0.0) S[n] += d;
+        if (first) S[n] = 0.0 + d;
+        else if (d != 0.0) S[n] += d;
         return static_cast<T>(c);
     }
     __device__ __forceinline__ void post_real(T& x0, T& x1, long long n) {

@@ -149,6 +149,25 @@ class CorrectionResult:
     kernel_launches: int
 
 
+class _ResultHolder:
+    """Owns one ffcz_cuda_result; releases its library buffers exactly once."""
+
+    def __init__(self):
+        self.res = capi.Result()
+        self.live = True
+
+    def free(self):
+        if self.live:
+            capi.load().ffcz_cuda_result_free(C.byref(self.res))
+            self.live = False
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 def _is_torch(x):
     return type(x).__module__.startswith("torch")
 
@@ -201,12 +220,13 @@ def _bounds_desc(b: DualBounds, m: _Marshal):
 def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: int = 1000,
             precision: str | None = None, *, want_archive: bool = True, want_edits: bool = True,
             want_corrected: bool = True, zlib_level: int = 9, fused: bool = True,
-            ctx: Context | None = None) -> CorrectionResult:
+            copy: bool = True, ctx: Context | None = None) -> CorrectionResult:
     """ffcz::correct (pipeline.cpp:26-178) on the GPU.
 
     original / decompressed: numpy arrays (host; float32 or float64) or CUDA torch tensors (then
     every bound array must be a CUDA tensor too).  precision: the ScalarField precision tag
-    written into the archive ("f32" / "f64"; default from the input dtype).
+    written into the archive ("f32" / "f64"; default from the input dtype).  copy=False returns
+    views of the library's pinned result buffers, valid while the returned object is alive.
     """
     ctx = ctx or default_context()
     lib = capi.load()
@@ -241,7 +261,8 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
         flags |= capi.FFCZ_FORCE_UNFUSED
     opt.flags = flags
     opt.zlib_level = zlib_level
-    res = capi.Result()
+    holder = _ResultHolder()
+    res = holder.res
     rc = lib.ffcz_cuda_correct(ctx.handle, C.byref(fd), mar.ptr(original, dt),
                                mar.ptr(decompressed, dt), C.byref(bd), int(m), int(max_iters),
                                C.byref(opt), C.byref(res))
@@ -256,7 +277,8 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
         def arr(p, n, dtype):
             if not p or n == 0:
                 return np.zeros(0, dtype=dtype)
-            return np.ctypeslib.as_array(p, shape=(n,)).copy().view(dtype)
+            a = np.ctypeslib.as_array(p, shape=(n,))
+            return (a.copy() if copy else a).view(dtype)
 
         edits = want_edits or want_archive
         sflags = fflags = scodes = fcodes = None
@@ -271,17 +293,23 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
                 escapes.append(EscapeEntry(bool(e.frequency), int(e.index), float(e.re), float(e.im)))
         corrected = None
         if want_corrected:
-            corrected = np.ctypeslib.as_array(res.corrected, shape=(N,)).copy().reshape(shape)
+            corrected = np.ctypeslib.as_array(res.corrected, shape=(N,)).reshape(shape)
+            if copy:
+                corrected = corrected.copy()
         data = C.string_at(res.archive, res.archive_len) if want_archive else None
         timings = {k: float(getattr(res, k)) for k in ("t_feasible_ms", "t_loop_ms", "t_gate_ms",
                                                        "t_h2d_ms", "t_d2h_ms", "t_archive_ms")}
-        return CorrectionResult(data, rep, int(res.escape_count), bool(res.verify_ok),
-                                float(res.verify_max_spatial_excess),
-                                float(res.verify_max_freq_excess), sflags, fflags, scodes, fcodes,
-                                escapes, corrected, int(res.escape_rounds), timings,
-                                int(res.kernel_launches))
+        out = CorrectionResult(data, rep, int(res.escape_count), bool(res.verify_ok),
+                               float(res.verify_max_spatial_excess),
+                               float(res.verify_max_freq_excess), sflags, fflags, scodes, fcodes,
+                               escapes, corrected, int(res.escape_rounds), timings,
+                               int(res.kernel_launches))
+        if not copy:
+            out._holder = holder  # keeps the pinned buffers alive with the views
+        return out
     finally:
-        lib.ffcz_cuda_result_free(C.byref(res))
+        if copy:
+            holder.free()
 
 
 def alternating_projection(eps0, bounds_working: DualBounds, max_iters: int,
