@@ -201,6 +201,11 @@ typedef struct ffcz_cuda_kernel_stat {
 int ffcz_cuda_profile_enable(ffcz_cuda_ctx* ctx, int enable); /* 1: clear + start, 0: stop */
 int ffcz_cuda_profile_read(ffcz_cuda_ctx* ctx, ffcz_cuda_kernel_stat* out, int max, int* n);
 
+/* Per-pass micro-benchmark: each pass kind on a synthetic field of this geometry and dtype,
+ * `reps` launches each (tools/passbench.py, profiles/). */
+int ffcz_cuda_bench_passes(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, int reps,
+                           ffcz_cuda_kernel_stat* out, int max, int* n);
+
 /* CRC-32C (archive.cpp:61-71), exported for the format tests. */
 uint32_t ffcz_cuda_crc32c(const uint8_t* data, size_t len);
 

@@ -37,7 +37,7 @@ EXPORTS = [
     "ffcz_cuda_default_options", "ffcz_cuda_correct", "ffcz_cuda_result_free",
     "ffcz_cuda_alternating_projection", "ffcz_cuda_forward_dft", "ffcz_cuda_inverse_dft",
     "ffcz_cuda_r2c_device", "ffcz_cuda_c2r_device", "ffcz_cuda_crc32c",
-    "ffcz_cuda_profile_enable", "ffcz_cuda_profile_read",
+    "ffcz_cuda_profile_enable", "ffcz_cuda_profile_read", "ffcz_cuda_bench_passes",
 ]
 
 
@@ -125,5 +125,7 @@ def load():
     lib.ffcz_cuda_crc32c.restype = C.c_uint32
     lib.ffcz_cuda_profile_enable.argtypes = [P, C.c_int]
     lib.ffcz_cuda_profile_read.argtypes = [P, C.POINTER(KernelStat), C.c_int, C.POINTER(C.c_int)]
+    lib.ffcz_cuda_bench_passes.argtypes = [P, C.POINTER(FieldDesc), C.c_int,
+                                           C.POINTER(KernelStat), C.c_int, C.POINTER(C.c_int)]
     _lib = lib
     return lib

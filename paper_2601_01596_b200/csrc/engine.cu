@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -573,6 +574,18 @@ double event_ms(cudaEvent_t a, cudaEvent_t b) {
     return ms;
 }
 
+// FFCZ_DEBUG_TIMING=1: host timestamps of the phases of correct() on stderr (syncs the stream).
+struct DebugClock {
+    bool on = std::getenv("FFCZ_DEBUG_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(ffcz_cuda_ctx& c, const char* what) {
+        if (!on) return;
+        c.sync();
+        std::fprintf(stderr, "[ffcz] %-28s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
 template <class TI>
 void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& fd,
                    const void* orig_in, const void* dec_in, const ffcz_bounds_desc& bd, int m,
@@ -580,6 +593,8 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     cudaStream_t st = c.st;
     const bool on_dev = opt.flags & FFCZ_INPUTS_ON_DEVICE;
     const long long N = g.N;
+    DebugClock dbg;
+    dbg.mark(c, "enter");
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[0], st));
     const TI* orig = static_cast<const TI*>(orig_in);
     const TI* dec = static_cast<const TI*>(dec_in);
@@ -593,6 +608,7 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     }
     const Bounds bo = upload_bounds(c, g, bd, on_dev);
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[1], st));  // inputs resident
+    dbg.mark(c, "inputs resident");
 
     // compute_error + preconditions (pipeline.cpp:31-42)
     k_ctl_init<<<1, 1, 0, st>>>(c.ctl, max_iters);
@@ -630,6 +646,7 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     const GateOut go = run_gate<TI>(c, g, orig, dec, bo, m, lr.converged, lr.fused, eps, S, F,
                                     corrected);
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[6], st));
+    dbg.mark(c, "gate done");
     h = c.read_ctl();
 
     out->report.iterations = std::max<unsigned long long>(lr.passes, 1);
@@ -685,6 +702,7 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
         FFCZ_LAUNCH_CHECK();
     }
     out->escape_count = escapes.size();
+    dbg.mark(c, "escapes compacted");
     const bool want_edits = opt.flags & (FFCZ_WANT_EDITS | FFCZ_WANT_ARCHIVE);
     if (want_edits) {
         out->spatial_flag_bytes = (N + 7) / 8;
@@ -705,6 +723,7 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
             pinned().get(sizeof(ffcz_cuda_escape) * (escapes.size() + 1)));
         std::memcpy(out->escapes, escapes.data(), sizeof(ffcz_cuda_escape) * escapes.size());
     }
+    dbg.mark(c, "edits to host");
     if (opt.flags & FFCZ_WANT_CORRECTED) {
         out->corrected = static_cast<double*>(pinned().get(N * sizeof(double)));
         FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->corrected, corrected, N * sizeof(double),
@@ -713,6 +732,7 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     c.sync();
     const auto t_d2h1 = std::chrono::steady_clock::now();
     out->t_d2h_ms = std::chrono::duration<double, std::milli>(t_d2h1 - t_d2h0).count();
+    dbg.mark(c, "corrected to host");
 
     if (opt.flags & FFCZ_WANT_ARCHIVE) {
         // header bounds must be the caller's full arrays (host)
@@ -1088,6 +1108,88 @@ int ffcz_cuda_profile_read(ffcz_cuda_ctx* ctx, ffcz_cuda_kernel_stat* out, int m
         }
         int k = 0;
         for (; k < kNumProf && k < max; ++k) out[k] = st[k];
+        *n = k;
+    });
+}
+
+// Per-pass micro-benchmark (tools/passbench.py): every pass kind of the engine on a field of the
+// given geometry and dtype, `reps` back-to-back launches each, CUDA-event timed.
+int ffcz_cuda_bench_passes(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, int reps,
+                           ffcz_cuda_kernel_stat* out, int max, int* n) {
+    return guarded(ctx, [&] {
+        const Geometry g = make_geometry(field->ndim, field->dims, kPitchAlign);
+        ffcz_cuda_ctx& c = *ctx;
+        cudaStream_t st = c.st;
+        int k = 0;
+        auto timed = [&](const char* name, double bytes, auto&& launch) {
+            launch();  // warm (tables, attributes)
+            FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[0], st));
+            for (int r = 0; r < reps; ++r) launch();
+            FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[1], st));
+            FFCZ_CUDA_CHECK(cudaEventSynchronize(c.ev[1]));
+            if (k < max) {
+                std::memset(&out[k], 0, sizeof(out[k]));
+                std::strncpy(out[k].name, name, sizeof(out[k].name) - 1);
+                out[k].launches = reps;
+                out[k].total_ms = event_ms(c.ev[0], c.ev[1]);
+                out[k].bytes = bytes * reps;
+                ++k;
+            }
+        };
+        const double Nc = static_cast<double>(g.Nc()), N = static_cast<double>(g.N);
+        if (field->dtype == FFCZ_F64) {
+            double* x = c.b<double>("pb_x", g.N);
+            double* S = c.b<double>("pb_S", g.N);
+            double2* h = c.b<double2>("pb_h", g.half_elems());
+            double2* F = c.b<double2>("pb_F", g.half_elems());
+            FFCZ_CUDA_CHECK(cudaMemsetAsync(x, 0x3f, g.N * 8, st));
+            FFCZ_CUDA_CHECK(cudaMemsetAsync(S, 0, g.N * 8, st));
+            FFCZ_CUDA_CHECK(cudaMemsetAsync(F, 0, g.half_elems() * 16, st));
+            FftPlan<double> plan{g, &c.tw64};
+            Bounds b;
+            b.sb.g = 0.25;
+            b.fb.g = 1e-3;
+            k_ctl_init<<<1, 1, 0, st>>>(c.ctl, 1000);
+            timed("row_r2c", 8 * N + 16 * Nc, [&] {
+                launch_row_r2c<double>(g.n2, x, g.n2, h, g.P, g.rows, c.tw64, nullptr, st); });
+            timed("row_c2r", 8 * N + 16 * Nc, [&] {
+                launch_row_c2r<double>(g.n2, h, g.P, x, g.n2, g.rows, 1.0, c.tw64, nullptr, st); });
+            launch_row_r2c<double>(g.n2, x, g.n2, h, g.P, g.rows, c.tw64, nullptr, st);
+            if (plan.fused_ok())
+                timed("row_c2r_sclip_r2c (K1)", 32 * Nc + 8 * N, [&] {
+                    launch_row_fused<double>(g.n2, h, g.P, g.rows, g.n2, 1.0 / N, c.tw64, nullptr,
+                                             HookSClip<double>{b.sb, 1.0, S, x}, st); });
+            for (int a : {1, 0}) {
+                if (g.d[a] == 1) continue;
+                const std::string ax = a == 1 ? "axis_mid" : "axis_first";
+                timed(("col_fwd " + ax).c_str(), 32 * Nc, [&] {
+                    plan.col(a, -1, h, h, nullptr, HookNone{}, st); });
+                timed(("col_inv " + ax).c_str(), 32 * Nc, [&] {
+                    plan.col(a, +1, h, h, nullptr, HookNone{}, st); });
+            }
+            const int za = g.d[0] > 1 ? 0 : 1;
+            if (g.d[za] > 1 && plan.fused_ok()) {
+                timed("K3a col_fwd_check", 32 * Nc, [&] {
+                    plan.col(za, -1, h, h, nullptr, HookFReduce{b.fb, 1.0, c.ctl}, st); });
+                timed("K3b col_clip_inv (F rmw)", 64 * Nc, [&] {
+                    plan.col(za, +1, h, h, nullptr, HookFClip<double>{b.fb, 1.0, F}, st); });
+            }
+        } else {
+            float* x = c.b<float>("pb_x32", g.N);
+            float2* h = c.b<float2>("pb_h32", g.half_elems());
+            FFCZ_CUDA_CHECK(cudaMemsetAsync(x, 0x3f, g.N * 4, st));
+            FftPlan<float> plan{g, &c.tw32};
+            timed("f32 row_r2c", 4 * N + 8 * Nc, [&] {
+                launch_row_r2c<float>(g.n2, x, g.n2, h, g.P, g.rows, c.tw32, nullptr, st); });
+            timed("f32 row_c2r", 4 * N + 8 * Nc, [&] {
+                launch_row_c2r<float>(g.n2, h, g.P, x, g.n2, g.rows, 1.0f, c.tw32, nullptr, st); });
+            for (int a : {1, 0}) {
+                if (g.d[a] == 1) continue;
+                const std::string ax = a == 1 ? "axis_mid" : "axis_first";
+                timed(("f32 col_fwd " + ax).c_str(), 16 * Nc, [&] {
+                    plan.col(a, -1, h, h, nullptr, HookNone{}, st); });
+            }
+        }
         *n = k;
     });
 }

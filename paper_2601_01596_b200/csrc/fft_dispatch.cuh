@@ -3,6 +3,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -26,7 +27,15 @@ inline int pow2_ceil(long long v) {
 
 // Per-CTA complex-element budget of the exchange tile: B*L (columns) or rows*M (rows).
 // 4096 FP64 / 8192 FP32 elements = 64 KiB (+1/E padding) -> three CTAs per SM.
-template <class T> constexpr long long tile_budget() { return sizeof(T) == 8 ? 4096 : 8192; }
+// FFCZ_TILE_BUDGET64 / FFCZ_TILE_BUDGET32 override the budgets (tuning runs, tools/passbench.py).
+template <class T> long long tile_budget() {
+    static const long long v = [] {
+        const char* e = std::getenv(sizeof(T) == 8 ? "FFCZ_TILE_BUDGET64" : "FFCZ_TILE_BUDGET32");
+        const long long d = sizeof(T) == 8 ? 4096 : 8192;
+        return e ? std::max(64LL, std::atoll(e)) : d;
+    }();
+    return v;
+}
 
 template <class K>
 void set_smem(K kernel, size_t bytes) {

@@ -11,6 +11,20 @@ __device__ __forceinline__ int plane_weight(int k2, long long n2) {
     return (k2 == 0 || 2LL * k2 == n2) ? 1 : 2;
 }
 
+// block-wide sum, one atomic per CTA (per-warp atomics on one address serialise in L2)
+__device__ __forceinline__ void block_sum_atomic(unsigned long long v, unsigned long long* dst) {
+    __shared__ unsigned long long sacc[32];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sacc[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int nw = (blockDim.x + 31) >> 5;
+        v = threadIdx.x < nw ? sacc[threadIdx.x] : 0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0 && v) atomicAdd(dst, v);
+    }
+}
+
 __device__ __forceinline__ void set_bit(unsigned* words, long long i) {
     atomicOr(&words[i >> 5], 1u << (i & 31));
 }
@@ -158,8 +172,7 @@ __global__ void k_count_spatial(const double* __restrict__ S, long long N, Ctl* 
     for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
          n += (long long)gridDim.x * blockDim.x)
         c += S[n] != 0.0;
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ctl->act_s, c);
+    block_sum_atomic(c, &ctl->act_s);
 }
 
 __global__ void k_count_freq(const double2* __restrict__ F, HalfGeom g, Ctl* ctl) {
@@ -170,8 +183,7 @@ __global__ void k_count_freq(const double2* __restrict__ F, HalfGeom g, Ctl* ctl
         const double2 v = F[row * g.P + k2];
         if (v.x != 0.0 || v.y != 0.0) c += plane_weight(k2, g.n2);
     }
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ctl->act_f, c);
+    block_sum_atomic(c, &ctl->act_f);
 }
 
 __global__ void k_gather_half(const double* __restrict__ full, double* half, HalfGeom g) {
@@ -208,6 +220,7 @@ __global__ void k_expand_full(const double2* __restrict__ half, double2* full, i
 __global__ void k_gate_spatial(const double* __restrict__ S, long long N, SpatialB sb, int m,
                                double* spat_cur, unsigned* keep_words, unsigned* esc_words,
                                Ctl* ctl) {
+    unsigned long long nz_acc = 0;
     const long long n0 = blockIdx.x * (long long)blockDim.x;
     for (long long base = n0; base < N; base += (long long)gridDim.x * blockDim.x) {
         const long long n = base + threadIdx.x;
@@ -233,14 +246,15 @@ __global__ void k_gate_spatial(const double* __restrict__ S, long long N, Spatia
             keep_words[n >> 5] = bk;
             esc_words[n >> 5] = be;
         }
-        const unsigned long long nz_w = __popc(bk) + __popc(be);
-        if ((threadIdx.x & 31) == 0 && nz_w) atomicAdd(&ctl->act_s, nz_w);
+        if ((threadIdx.x & 31) == 0) nz_acc += __popc(bk) + __popc(be);
     }
+    block_sum_atomic(nz_acc, &ctl->act_s);
 }
 
 __global__ void k_gate_freq(const double2* __restrict__ F, HalfGeom g, FreqB fb, int m,
                             double2* freq_cur, unsigned* keep_words, unsigned* esc_words,
                             Ctl* ctl) {
+    unsigned long long nz_acc = 0;
     const long long total = g.rows * g.H;
     for (HalfWalk hw(g); hw.block_ok(); hw.next()) {
         const long long h = hw.i;
@@ -272,10 +286,9 @@ __global__ void k_gate_freq(const double2* __restrict__ F, HalfGeom g, FreqB fb,
             keep_words[h >> 5] = bk;
             esc_words[h >> 5] = be;
         }
-        unsigned long long c = w;
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ctl->act_f, c);
+        nz_acc += w;
     }
+    block_sum_atomic(nz_acc, &ctl->act_f);
 }
 
 __global__ void k_popc_blocks(const unsigned* __restrict__ words, long long nwords,
