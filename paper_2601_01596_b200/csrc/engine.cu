@@ -675,7 +675,9 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     std::vector<ffcz_cuda_escape> escapes;
     {
         unsigned long long* idx = c.b<unsigned long long>("idx", std::max(N, g.Nc()));
+        dbg.mark(c, "escape section start");
         const unsigned long long ns = compact_bits(c, c.b<unsigned>("esc_s", ws), ws, idx);
+        dbg.mark(c, "spatial escapes compacted");
         std::vector<unsigned long long> hidx(ns);
         std::vector<double> hval(ns);
         if (ns) {
@@ -686,7 +688,9 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
             c.sync();
         }
         for (unsigned long long i = 0; i < ns; ++i) escapes.push_back({0, hidx[i], hval[i], 0.0});
+        dbg.mark(c, "spatial escapes gathered");
         const unsigned long long nf = compact_bits(c, c.b<unsigned>("esc_f", wf), wf, idx);
+        dbg.mark(c, "freq escapes compacted");
         std::vector<unsigned long long> fidx(nf);
         std::vector<double2> fval(nf);
         if (nf) {

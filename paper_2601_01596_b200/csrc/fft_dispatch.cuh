@@ -27,14 +27,30 @@ inline int pow2_ceil(long long v) {
 
 // Per-CTA complex-element budget of the exchange tile: B*L (columns) or rows*M (rows).
 // 4096 FP64 / 8192 FP32 elements = 64 KiB (+1/E padding) -> three CTAs per SM.
-// FFCZ_TILE_BUDGET64 / FFCZ_TILE_BUDGET32 override the budgets (tuning runs, tools/passbench.py).
-template <class T> long long tile_budget() {
-    static const long long v = [] {
-        const char* e = std::getenv(sizeof(T) == 8 ? "FFCZ_TILE_BUDGET64" : "FFCZ_TILE_BUDGET32");
-        const long long d = sizeof(T) == 8 ? 4096 : 8192;
-        return e ? std::max(64LL, std::atoll(e)) : d;
-    }();
-    return v;
+// Measured on B200 at 512^3 FP64 (tools/passbench.py, profiles/r01_passbench.md):
+//  * row passes: 1024 elements per CTA (4 rows of 256) -> 90% of HBM; bigger CTAs serialise
+//    load and compute phases;
+//  * column pass along the middle axis (row stride P): 2048 (B = 4 columns, 2 CTAs/SM) -> 70%;
+//  * column pass along the first axis (row stride n1*P, >2 MB): 4096 (B = 8: 128-B row
+//    segments keep DRAM pages / TLB entries shared by concurrent CTAs) -> 50%; 64-B segments
+//    drop it to 43%, 32-B to 26%.
+// FFCZ_TILE_BUDGET{64,32}_{ROW,MID,FIRST} override them (tuning runs).
+enum class TileRole { kRow = 0, kMid = 1, kFirst = 2 };
+template <class T> long long tile_budget(TileRole role) {
+    static const long long v[3] = {
+        [] {
+            const char* e = std::getenv(sizeof(T) == 8 ? "FFCZ_TILE_BUDGET64_ROW" : "FFCZ_TILE_BUDGET32_ROW");
+            return e ? std::max(16LL, std::atoll(e)) : (sizeof(T) == 8 ? 1024LL : 2048LL);
+        }(),
+        [] {
+            const char* e = std::getenv(sizeof(T) == 8 ? "FFCZ_TILE_BUDGET64_MID" : "FFCZ_TILE_BUDGET32_MID");
+            return e ? std::max(16LL, std::atoll(e)) : (sizeof(T) == 8 ? 2048LL : 4096LL);
+        }(),
+        [] {
+            const char* e = std::getenv(sizeof(T) == 8 ? "FFCZ_TILE_BUDGET64_FIRST" : "FFCZ_TILE_BUDGET32_FIRST");
+            return e ? std::max(16LL, std::atoll(e)) : (sizeof(T) == 8 ? 4096LL : 8192LL);
+        }()};
+    return v[static_cast<int>(role)];
 }
 
 template <class K>
@@ -78,7 +94,8 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
     constexpr int E = pick_E<T>(L);
     constexpr int TT = L / E;
     constexpr int MAXT = max_threads<T, E>();
-    int B = static_cast<int>(std::min<long long>(tile_budget<T>() / L, MAXT / TT));
+    const TileRole role = row_stride > plane_stride && nplanes > 1 ? TileRole::kFirst : TileRole::kMid;
+    int B = static_cast<int>(std::min<long long>(tile_budget<T>(role) / L, MAXT / TT));
     B = std::min(B, 128);
     B = std::min(B, pow2_ceil(ncols));
     B = std::max(B, 1);
@@ -101,7 +118,7 @@ template <class T, int M> struct RowCfg {
 template <class T, int M>
 int rows_per_cta(long long nrows) {
     constexpr int TT = RowCfg<T, M>::TT;
-    long long r = std::min<long long>(tile_budget<T>() / M, RowCfg<T, M>::MAXT / TT);
+    long long r = std::min<long long>(tile_budget<T>(TileRole::kRow) / M, RowCfg<T, M>::MAXT / TT);
     r = std::min<long long>(r, pow2_ceil(nrows));
     return static_cast<int>(std::max<long long>(1, r));
 }
