@@ -293,16 +293,22 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
                 Prof p(c, kColPass, pass_bytes);
                 plan.col(1, +1, spec, spec, gate, HookNone{}, st);
             }
+            {   // K1 as C2R(+s-clip, eps written) then R2C: two 90%-of-HBM passes beat one
+                // register-bound fused pass (profiles/r01_passbench.md)
+                Prof p(c, kRowC2R, 16.0 * g.Nc() + 8.0 * g.N + (bw.sb.v ? 8.0 * g.N : 0.0));
+                launch_row_c2r_hook<double>(g.n2, spec, g.P, eps, g.n2, g.rows, invN, c.tw64, gate,
+                                            HookSClip<double>{bw.sb, fscale, S, nullptr, c.ctl},
+                                            st);
+            }
             {
-                Prof p(c, kRowFused, fused_bytes);
-                launch_row_fused<double>(g.n2, spec, g.P, g.rows, g.n2, invN, c.tw64, gate,
-                                         HookSClip<double>{bw.sb, fscale, S, eps, c.ctl}, st);  // K1
+                Prof p(c, kRowR2C, 8.0 * g.N + 16.0 * g.Nc());
+                launch_row_r2c<double>(g.n2, eps, g.n2, spec, g.P, g.rows, c.tw64, gate, st);
             }
             if (three_d) {
                 Prof p(c, kColPass, pass_bytes);
                 plan.col(1, -1, spec, spec, gate, HookNone{}, st);
             }
-            c.launches += three_d ? 6 : 4;
+            c.launches += three_d ? 7 : 5;
         } else {
             plan.r2c(eps, spec, gate, st);
             k_freduce<<<grid_for(g.Nc()), 256, 0, st>>>(spec, hg, bw.fb, fscale, c.ctl, gate);
@@ -449,7 +455,7 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
     int* codes_s = c.b<int>("codes_s", N);
     int* codes_f = c.b<int>("codes_f", 2 * Nc);
     double2* spec = c.b<double2>("spec", g.half_elems());
-    double* eps_t = fused ? nullptr : c.b<double>("eps_tilde", N);
+    double* eps_t = c.b<double>("eps_tilde", N);
 
     FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->act_s, 0, 2 * sizeof(unsigned long long), st));
     {
@@ -497,23 +503,27 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
                 plan.col(1, +1, work, work, nullptr, HookNone{}, st);
             }
             {
-                Prof p(c, kRowFused, row_bytes);
-                launch_row_fused<double>(g.n2, work, g.P, g.rows, g.n2, invN, c.tw64, nullptr,
-                                         row_hook, st);
+                Prof p(c, kRowC2R, row_bytes);
+                launch_row_c2r_hook<double>(g.n2, work, g.P, eps_t, g.n2, g.rows, invN, c.tw64,
+                                            nullptr, row_hook, st);
+            }
+            {
+                Prof p(c, kRowR2C, 8.0 * g.N + 16.0 * Nc);
+                launch_row_r2c<double>(g.n2, eps_t, g.n2, work, g.P, g.rows, c.tw64, nullptr, st);
             }
             if (three_d) {
                 Prof p(c, kColPass, pass);
                 plan.col(1, -1, work, work, nullptr, HookNone{}, st);
             }
-            c.launches += three_d ? 4 : 2;
+            c.launches += three_d ? 5 : 3;
         };
-        const double in_bytes = 2.0 * sizeof(TI) * N + 8.0 * N;
+        const double in_bytes = 2.0 * sizeof(TI) * N + 16.0 * N;  // orig, dec, spat_cur, eps_tilde
         if (converged) {
             for (int round = 0; round < 32; ++round) {                   // pipeline.cpp:116
                 FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->dirty, 0, sizeof(int), st));
                 FFCZ_CUDA_CHECK(cudaMemsetAsync(viol, 0, vw * sizeof(unsigned), st));
                 inverse_and_row(HookRepairS<TI>{orig, dec, spat_cur, eps, bo.sb, esc_s, c.ctl},
-                                pass + in_bytes);
+                                16.0 * Nc + in_bytes);
                 {
                     Prof p(c, kColFwdCheck, pass);
                     plan.col(za, -1, work, work, nullptr, HookMarkViol{bo.fb, viol, c.ctl}, st);
@@ -528,7 +538,7 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
         }
         // apply_edits + verify_bounds on the decoder view (pipeline.cpp:174-176)
         inverse_and_row(HookVerifyS<TI>{orig, dec, spat_cur, corrected, bo.sb, c.ctl},
-                        pass + in_bytes + 8.0 * N);
+                        16.0 * Nc + in_bytes + 8.0 * N);
         {
             Prof p(c, kColFwdCheck, 16.0 * Nc);
             plan.col(za, -1, work, work, nullptr, HookVerifyF{bo.fb, c.ctl}, st);
@@ -671,41 +681,36 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
 
     // ---- products to the host -------------------------------------------------------------
     const auto t_d2h0 = std::chrono::steady_clock::now();
+    const EscapeRec* escape_dev = nullptr;
     const long long ws = (N + 31) / 32, wf = (g.Nc() + 31) / 32;
-    std::vector<ffcz_cuda_escape> escapes;
+    unsigned long long n_esc = 0;
     {
         unsigned long long* idx = c.b<unsigned long long>("idx", std::max(N, g.Nc()));
         dbg.mark(c, "escape section start");
         const unsigned long long ns = compact_bits(c, c.b<unsigned>("esc_s", ws), ws, idx);
-        dbg.mark(c, "spatial escapes compacted");
-        std::vector<unsigned long long> hidx(ns);
-        std::vector<double> hval(ns);
+        EscapeRec* recs = nullptr;
         if (ns) {
-            double* vals = c.b<double>("esc_vals", 2 * ns);
-            k_gather_escapes_s<<<grid_for(ns), 256, 0, st>>>(idx, ns, c.b<double>("spat_cur", N), vals);
-            FFCZ_CUDA_CHECK(cudaMemcpyAsync(hidx.data(), idx, ns * 8, cudaMemcpyDeviceToHost, st));
-            FFCZ_CUDA_CHECK(cudaMemcpyAsync(hval.data(), vals, ns * 8, cudaMemcpyDeviceToHost, st));
-            c.sync();
+            recs = c.b<EscapeRec>("esc_recs", ns);
+            k_escape_records_s<<<grid_for(ns), 256, 0, st>>>(idx, ns, c.b<double>("spat_cur", N), recs);
+            FFCZ_LAUNCH_CHECK();
         }
-        for (unsigned long long i = 0; i < ns; ++i) escapes.push_back({0, hidx[i], hval[i], 0.0});
-        dbg.mark(c, "spatial escapes gathered");
         const unsigned long long nf = compact_bits(c, c.b<unsigned>("esc_f", wf), wf, idx);
-        dbg.mark(c, "freq escapes compacted");
-        std::vector<unsigned long long> fidx(nf);
-        std::vector<double2> fval(nf);
-        if (nf) {
-            double2* vals = c.b<double2>("esc_valf", nf);
-            k_gather_escapes_f<<<grid_for(nf), 256, 0, st>>>(idx, nf, c.b<double2>("freq_cur", g.half_elems()),
-                                                             g.hg(), vals);
-            FFCZ_CUDA_CHECK(cudaMemcpyAsync(fidx.data(), idx, nf * 8, cudaMemcpyDeviceToHost, st));
-            FFCZ_CUDA_CHECK(cudaMemcpyAsync(fval.data(), vals, nf * 16, cudaMemcpyDeviceToHost, st));
-            c.sync();
+        n_esc = ns + nf;
+        if (n_esc) {
+            // the spatial records may have to move when the buffer grows: rebuild them after
+            EscapeRec* all = c.b<EscapeRec>("esc_recs_all", n_esc);
+            if (ns) FFCZ_CUDA_CHECK(cudaMemcpyAsync(all, recs, ns * sizeof(EscapeRec), cudaMemcpyDeviceToDevice, st));
+            if (nf) {
+                k_escape_records_f<<<grid_for(nf), 256, 0, st>>>(
+                    idx, nf, c.b<double2>("freq_cur", g.half_elems()), g.hg(), all + ns);
+                FFCZ_LAUNCH_CHECK();
+            }
+            escape_dev = all;
         }
-        for (unsigned long long i = 0; i < nf; ++i)
-            escapes.push_back({1, fidx[i], fval[i].x, fval[i].y});
-        FFCZ_LAUNCH_CHECK();
+        dbg.mark(c, "escape records built");
     }
-    out->escape_count = escapes.size();
+    std::vector<ffcz_cuda_escape> escapes;  // only for the archive writer below
+    out->escape_count = n_esc;
     dbg.mark(c, "escapes compacted");
     const bool want_edits = opt.flags & (FFCZ_WANT_EDITS | FFCZ_WANT_ARCHIVE);
     if (want_edits) {
@@ -724,8 +729,10 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
         FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->frequency_codes, c.b<int>("codes_f", 2 * g.Nc()),
                                         go.n_keep_f * 8, cudaMemcpyDeviceToHost, st));
         out->escapes = static_cast<ffcz_cuda_escape*>(
-            pinned().get(sizeof(ffcz_cuda_escape) * (escapes.size() + 1)));
-        std::memcpy(out->escapes, escapes.data(), sizeof(ffcz_cuda_escape) * escapes.size());
+            pinned().get(sizeof(ffcz_cuda_escape) * (n_esc + 1)));
+        if (n_esc)
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->escapes, escape_dev, n_esc * sizeof(EscapeRec),
+                                            cudaMemcpyDeviceToHost, st));
     }
     dbg.mark(c, "edits to host");
     if (opt.flags & FFCZ_WANT_CORRECTED) {
@@ -763,9 +770,10 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
                 }
             }
         }
-        std::vector<ffcz_host::EscapeRec> er(escapes.size());
-        for (size_t i = 0; i < escapes.size(); ++i)
-            er[i] = {escapes[i].frequency != 0, escapes[i].index, escapes[i].re, escapes[i].im};
+        std::vector<ffcz_host::EscapeRec> er(n_esc);
+        for (size_t i = 0; i < n_esc; ++i)
+            er[i] = {out->escapes[i].frequency != 0, out->escapes[i].index, out->escapes[i].re,
+                     out->escapes[i].im};
         ffcz_host::ArchiveInput ai{};
         ai.ndim = fd.ndim;
         for (int a = 0; a < fd.ndim; ++a) ai.dims[a] = fd.dims[a];

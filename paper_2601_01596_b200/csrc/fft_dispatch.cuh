@@ -129,7 +129,7 @@ void row_r2c_radix(const T* in, long long in_stride, cplx<T>* out, long long out
     constexpr int E = RowCfg<T, M>::E, TT = RowCfg<T, M>::TT;
     const int R = rows_per_cta<T, M>(nrows);
     const size_t smem = row_smem_bytes<T, M, E>(R);
-    auto k = k_row_r2c<T, M, E, HookNone>;
+    auto k = TT <= 32 ? k_row_r2c_sh<T, M, E, HookNone> : k_row_r2c<T, M, E, HookNone>;
     set_smem(k, smem);
     k<<<persistent_grid(k, TT * R, smem, (nrows + R - 1) / R), TT * R, smem, st>>>(
         in, in_stride, out, out_stride, nrows, tw.stage_table(M, E), tw.post_table(M), gate,
@@ -137,17 +137,18 @@ void row_r2c_radix(const T* in, long long in_stride, cplx<T>* out, long long out
     FFCZ_LAUNCH_CHECK();
 }
 
-template <class T, int M>
+template <class T, int M, class Hook = RealHookNone>
 void row_c2r_radix(const cplx<T>* in, long long in_stride, T* out, long long out_stride,
-                   long long nrows, T scale, Twiddles<T>& tw, const int* gate, cudaStream_t st) {
+                   long long nrows, T scale, Twiddles<T>& tw, const int* gate, cudaStream_t st,
+                   Hook hook = Hook{}) {
     constexpr int E = RowCfg<T, M>::E, TT = RowCfg<T, M>::TT;
     const int R = rows_per_cta<T, M>(nrows);
     const size_t smem = row_smem_bytes<T, M, E>(R);
-    auto k = k_row_c2r<T, M, E, RealHookNone>;
+    auto k = TT <= 32 ? k_row_c2r_sh<T, M, E, Hook> : k_row_c2r<T, M, E, Hook>;
     set_smem(k, smem);
     k<<<persistent_grid(k, TT * R, smem, (nrows + R - 1) / R), TT * R, smem, st>>>(
         in, in_stride, out, out_stride, nrows, tw.stage_table(M, E), tw.post_table(M), scale,
-        gate, RealHookNone{});
+        gate, hook);
     FFCZ_LAUNCH_CHECK();
 }
 
@@ -157,7 +158,7 @@ void row_fused_radix(cplx<T>* data, long long stride, long long nrows, long long
     constexpr int E = RowCfg<T, M>::E, TT = RowCfg<T, M>::TT;
     const int R = rows_per_cta<T, M>(nrows);
     const size_t smem = row_smem_bytes<T, M, E>(R);
-    auto k = k_row_c2r_r2c<T, M, E, Hook>;
+    auto k = TT <= 32 ? k_row_c2r_r2c_sh<T, M, E, Hook> : k_row_c2r_r2c<T, M, E, Hook>;
     set_smem(k, smem);
     k<<<persistent_grid(k, TT * R, smem, (nrows + R - 1) / R), TT * R, smem, st>>>(
         data, stride, nrows, real_stride, tw.stage_table(M, E), tw.post_table(M), scale, gate,
@@ -246,6 +247,24 @@ void launch_row_c2r(long long n2, const cplx<T>* in, long long in_stride, T* out
     k_row_c2r_direct<T><<<static_cast<unsigned>(nrows), 256, smem, st>>>(
         in, in_stride, out, out_stride, static_cast<int>(n2), tw.table_for(n2), scale, gate);
     FFCZ_LAUNCH_CHECK();
+}
+
+template <class T, class Hook>
+void launch_row_c2r_hook(long long n2, const cplx<T>* in, long long in_stride, T* out,
+                         long long out_stride, long long nrows, T scale, Twiddles<T>& tw,
+                         const int* gate, Hook hook, cudaStream_t st) {
+    if (radix_row_ok(n2)) {
+        switch (n2 / 2) {
+#define X(n)                                                                                   \
+    case n:                                                                                    \
+        detail::row_c2r_radix<T, n, Hook>(in, in_stride, out, out_stride, nrows, scale, tw,    \
+                                          gate, st, hook);                                     \
+        return;
+            FFCZ_POW2_CASES(X)
+#undef X
+        }
+    }
+    throw Error(kUnsupported, "C2R with a fused epilogue needs a power-of-two last axis in [32, 8192]");
 }
 
 template <class T, class Hook>

@@ -492,6 +492,234 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     hook.finish();
 }
 
+// ---- row passes with warp-shuffle pairing (M/E <= 32) --------------------------------------------
+// The split/merge needs X[k] and X[M-k] together.  Instead of a shared-memory round trip, rows are
+// loaded in a "paired" layout: thread t holds X[t + T m] in slot m and X[M - t - T m] in slot
+// E-1-m (m < E/2; descending addresses are still coalesced), so the merge is thread-local; one
+// exchange of E/2 values with the partner lane (T - t) mod T converts to the natural layout the
+// Stockham stages need (and back for the split).  Thread 0 additionally owns the self-paired
+// index M/2 and, through slot E-1, the Nyquist X[M].
+
+template <class T>
+__device__ __forceinline__ cplx<T> shfl_c(cplx<T> v, int src, int width) {
+    v.x = __shfl_sync(0xffffffffu, v.x, src, width);
+    v.y = __shfl_sync(0xffffffffu, v.y, src, width);
+    return v;
+}
+
+// X_k, X_{M-k}, W_{2M}^k -> Z_k  (c2r_merge on registers; `dc` drops Im of X_0 and X_M)
+template <class T>
+__device__ __forceinline__ cplx<T> merge_pair(cplx<T> a, cplx<T> b, cplx<T> w, bool dc) {
+    if (dc) {
+        a.y = T(0);
+        b.y = T(0);
+    }
+    const cplx<T> ze = mkc<T>(a.x + b.x, a.y - b.y);
+    const cplx<T> d = mkc<T>(a.x - b.x, a.y + b.y);
+    const cplx<T> zo = cmulc(d, w);
+    return mkc<T>(ze.x - zo.y, ze.y + zo.x);
+}
+
+// Z_k, Z_{M-k}, W_{2M}^k -> X_k (r2c_split on registers)
+template <class T>
+__device__ __forceinline__ cplx<T> split_pair(cplx<T> zk, cplx<T> zn, cplx<T> w) {
+    const T h = T(0.5);
+    const cplx<T> ze = mkc<T>((zk.x + zn.x) * h, (zk.y - zn.y) * h);
+    const cplx<T> zo = mkc<T>((zk.y + zn.y) * h, (zn.x - zk.x) * h);
+    return cadd(ze, cmul(zo, w));
+}
+
+template <class T, int M, int E>
+__device__ __forceinline__ void load_pairs(const cplx<T>* __restrict__ rowp, int t, bool valid,
+                                           cplx<T> (&v)[E], cplx<T>& mid) {
+    constexpr int TT = M / E;
+#pragma unroll
+    for (int m = 0; m < E / 2; ++m) {
+        v[m] = valid ? rowp[t + TT * m] : mkc<T>(T(0), T(0));
+        v[E - 1 - m] = valid ? rowp[M - t - TT * m] : mkc<T>(T(0), T(0));
+    }
+    mid = (valid && t == 0) ? rowp[M / 2] : mkc<T>(T(0), T(0));
+}
+
+template <class T, int M, int E>
+__device__ __forceinline__ void merge_pairs(cplx<T> (&v)[E], cplx<T>& mid, int t,
+                                            const cplx<T>* __restrict__ twp) {
+    constexpr int TT = M / E;
+#pragma unroll
+    for (int m = 0; m < E / 2; ++m) {
+        const int k = t + TT * m;
+        const cplx<T> a = v[m], b = v[E - 1 - m];
+        const bool dc = (k == 0);
+        v[m] = merge_pair<T>(a, b, twp[k], dc);
+        v[E - 1 - m] = merge_pair<T>(b, a, twp[M - k], false);  // unused when k == 0
+    }
+    if (t == 0) mid = merge_pair<T>(mid, mid, twp[M / 2], false);
+}
+
+// paired -> natural (v[m] = Z[t + T m]); ascending so thread 0 reads slots not yet replaced
+template <class T, int M, int E>
+__device__ __forceinline__ void pairs_to_natural(cplx<T> (&v)[E], cplx<T> mid, int t) {
+    constexpr int TT = M / E;
+    const int src = (TT - t) & (TT - 1);
+#pragma unroll
+    for (int m = 0; m < E / 2; ++m) {
+        cplx<T> send = v[E - 1 - m];
+        if (t == 0) send = (m + 1 < E / 2) ? v[E - 2 - m] : mid;
+        v[E - 1 - m] = shfl_c<T>(send, src, TT);
+    }
+}
+
+// natural -> paired; descending so thread 0 reads slots not yet replaced.  Returns Z[M/2] in
+// thread 0.
+template <class T, int M, int E>
+__device__ __forceinline__ cplx<T> natural_to_pairs(cplx<T> (&v)[E], int t) {
+    constexpr int TT = M / E;
+    const int src = (TT - t) & (TT - 1);
+    const cplx<T> mid = v[E / 2];
+#pragma unroll
+    for (int m = E / 2 - 1; m >= 0; --m) {
+        cplx<T> send = v[E - 1 - m];
+        if (t == 0) send = (m == 0) ? v[0] : v[E - m];
+        v[E - 1 - m] = shfl_c<T>(send, src, TT);
+    }
+    return mid;
+}
+
+template <class T, int M, int E, class Hook>
+__device__ __forceinline__ void split_store(cplx<T> (&v)[E], cplx<T> mid, int t, bool valid,
+                                            cplx<T>* rowp, long long row_off,
+                                            const cplx<T>* __restrict__ twp, Hook& hook) {
+    constexpr int TT = M / E;
+#pragma unroll
+    for (int m = 0; m < E / 2; ++m) {
+        const int k = t + TT * m;
+        const cplx<T> zk = v[m], zn = v[E - 1 - m];
+        cplx<T> xk, xn;
+        if (k == 0) {
+            xk = mkc<T>(zk.x + zk.y, T(0));
+            xn = mkc<T>(zk.x - zk.y, T(0));
+        } else {
+            xk = split_pair<T>(zk, zn, twp[k]);
+            xn = split_pair<T>(zn, zk, twp[M - k]);
+        }
+        if (valid) {
+            hook.post(xk, row_off + k, k);
+            hook.post(xn, row_off + (M - k), M - k);
+            rowp[k] = xk;
+            rowp[M - k] = xn;
+        }
+    }
+    if (valid && t == 0) {
+        cplx<T> xm = split_pair<T>(mid, mid, twp[M / 2]);
+        hook.post(xm, row_off + M / 2, M / 2);
+        rowp[M / 2] = xm;
+    }
+}
+
+template <class T, int M, int E, class Hook>
+__global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>())
+    k_row_r2c_sh(const T* __restrict__ in, long long in_stride, cplx<T>* __restrict__ out,
+                 long long out_stride, long long nrows, const cplx<T>* __restrict__ tw,
+                 const cplx<T>* __restrict__ twp, const int* gate, Hook hook) {
+    if (gated(gate)) return;
+    hook_begin(hook);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int TT = M / E;
+    const int t = threadIdx.x % TT;
+    const int rb = threadIdx.x / TT;
+    const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        __syncthreads();
+        const long long row = tile * (blockDim.x / TT) + rb;
+        const bool valid = row < nrows;
+        cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
+        const cplx<T>* src = reinterpret_cast<const cplx<T>*>(in + (valid ? row : 0) * in_stride);
+        cplx<T> v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = valid ? src[t + TT * m] : mkc<T>(T(0), T(0));
+        stockham<T, M, E, 1, -1>(v, t, tw, XchRow<T, E>{s});
+        const cplx<T> mid = natural_to_pairs<T, M, E>(v, t);
+        split_store<T, M, E>(v, mid, t, valid, out + (valid ? row : 0) * out_stride,
+                             row * out_stride, twp, hook);
+    }
+    hook.finish();
+}
+
+template <class T, int M, int E, class Hook>
+__global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>())
+    k_row_c2r_sh(const cplx<T>* __restrict__ in, long long in_stride, T* __restrict__ out,
+                 long long out_stride, long long nrows, const cplx<T>* __restrict__ tw,
+                 const cplx<T>* __restrict__ twp, T scale, const int* gate, Hook hook) {
+    if (gated(gate)) return;
+    hook_begin(hook);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int TT = M / E;
+    const int t = threadIdx.x % TT;
+    const int rb = threadIdx.x / TT;
+    const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        __syncthreads();
+        const long long row = tile * (blockDim.x / TT) + rb;
+        const bool valid = row < nrows;
+        cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
+        cplx<T> v[E], mid;
+        load_pairs<T, M, E>(in + (valid ? row : 0) * in_stride, t, valid, v, mid);
+        merge_pairs<T, M, E>(v, mid, t, twp);
+        pairs_to_natural<T, M, E>(v, mid, t);
+        stockham<T, M, E, 1, +1>(v, t, tw, XchRow<T, E>{s});
+        if (valid) {
+            cplx<T>* dst = reinterpret_cast<cplx<T>*>(out + row * out_stride);
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int j = t + TT * m;
+                T x0 = v[m].x * scale, x1 = v[m].y * scale;
+                hook.post_real(x0, x1, row * out_stride + 2 * j);
+                dst[j] = mkc<T>(x0, x1);
+            }
+        }
+    }
+    hook.finish();
+}
+
+template <class T, int M, int E, class Hook>
+__global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>())
+    k_row_c2r_r2c_sh(cplx<T>* data, long long stride, long long nrows, long long real_stride,
+                     const cplx<T>* __restrict__ tw, const cplx<T>* __restrict__ twp, T scale,
+                     const int* gate, Hook hook) {
+    if (gated(gate)) return;
+    hook_begin(hook);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int TT = M / E;
+    const int t = threadIdx.x % TT;
+    const int rb = threadIdx.x / TT;
+    const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
+    HookNone none;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        __syncthreads();
+        const long long row = tile * (blockDim.x / TT) + rb;
+        const bool valid = row < nrows;
+        cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
+        const XchRow<T, E> x{s};
+        cplx<T>* rowp = data + (valid ? row : 0) * stride;
+        cplx<T> v[E], mid;
+        load_pairs<T, M, E>(rowp, t, valid, v, mid);
+        merge_pairs<T, M, E>(v, mid, t, twp);
+        pairs_to_natural<T, M, E>(v, mid, t);
+        stockham<T, M, E, 1, +1>(v, t, tw, x);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int j = t + TT * m;
+            T x0 = v[m].x * scale, x1 = v[m].y * scale;
+            if (valid) hook.post_real(x0, x1, row * real_stride + 2 * j);
+            v[m] = mkc<T>(x0, x1);
+        }
+        stockham<T, M, E, 1, -1>(v, t, tw, x);
+        mid = natural_to_pairs<T, M, E>(v, t);
+        split_store<T, M, E>(v, mid, t, valid, rowp, row * stride, twp, none);
+    }
+    hook.finish();
+}
+
 template <class T, int M, int E>
 constexpr size_t row_smem_bytes(int rows) {
     return static_cast<size_t>(row_smem_elems<M, E>()) * rows * sizeof(cplx<T>);

@@ -124,6 +124,16 @@ FFCZ_ROW_FUSED(HookRepairS<double>)
 FFCZ_ROW_FUSED(HookVerifyS<float>)
 FFCZ_ROW_FUSED(HookVerifyS<double>)
 #undef FFCZ_ROW_FUSED
+#define FFCZ_ROW_C2R_HOOK(H)                                                                  \
+    template void launch_row_c2r_hook<double, H>(long long, const double2*, long long, double*, \
+                                                 long long, long long, double, Twiddles<double>&, \
+                                                 const int*, H, cudaStream_t);
+FFCZ_ROW_C2R_HOOK(HookSClip<double>)
+FFCZ_ROW_C2R_HOOK(HookRepairS<float>)
+FFCZ_ROW_C2R_HOOK(HookRepairS<double>)
+FFCZ_ROW_C2R_HOOK(HookVerifyS<float>)
+FFCZ_ROW_C2R_HOOK(HookVerifyS<double>)
+#undef FFCZ_ROW_C2R_HOOK
 template void launch_col<double, HookMarkViol>(long long, int, const double2*, double2*, long long,
                                                long long, long long, int, Twiddles<double>&,
                                                const int*, HookMarkViol, cudaStream_t);

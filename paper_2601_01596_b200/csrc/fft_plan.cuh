@@ -81,6 +81,11 @@ template <class T>
 void launch_row_c2r(long long n2, const cplx<T>* in, long long in_stride, T* out,
                     long long out_stride, long long nrows, T scale, Twiddles<T>& tw,
                     const int* gate, cudaStream_t st);
+// C2R with a real-output epilogue hook (radix path only).
+template <class T, class Hook>
+void launch_row_c2r_hook(long long n2, const cplx<T>* in, long long in_stride, T* out,
+                         long long out_stride, long long nrows, T scale, Twiddles<T>& tw,
+                         const int* gate, Hook hook, cudaStream_t st);
 // Fused C2R -> hook(real) -> R2C, in place on the half rows (radix path only).
 template <class T, class Hook>
 void launch_row_fused(long long n2, cplx<T>* data, long long stride, long long nrows,

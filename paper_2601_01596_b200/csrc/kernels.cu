@@ -266,8 +266,9 @@ __global__ void k_gate_freq(const double2* __restrict__ F, HalfGeom g, FreqB fb,
             const long long off = row * g.P + k2;
             const double2 v = F[off];
             const bool nz = v.x != 0.0 || v.y != 0.0;
-            const double sre = ldexp(2.0 * fb.re_at(off), -m);   // editset.cpp:35-41
-            const double sim = ldexp(2.0 * fb.im_at(off), -m);
+            const double2 db = fb.at2(off);
+            const double sre = ldexp(2.0 * db.x, -m);   // editset.cpp:35-41
+            const double sim = ldexp(2.0 * db.y, -m);
             ovf = nz && (fabs(v.x) / sre > kMaxIndex || fabs(v.y) / sim > kMaxIndex);  // :68-69
             keep = nz && !ovf;
             double2 cur = make_double2(0.0, 0.0);
@@ -586,6 +587,25 @@ __global__ void k_repair_freq_sparse(const unsigned* __restrict__ viol_words, lo
             set_bit(esc_words, row * g.H + k2);
             set_bit(esc_words, mrow * g.H + k2);
         }
+    }
+}
+
+__global__ void k_escape_records_s(const unsigned long long* __restrict__ idx, long long n,
+                                   const double* __restrict__ spat_cur, EscapeRec* out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long k = idx[i];
+        out[i] = EscapeRec{0, 0, k, spat_cur[k], 0.0};
+    }
+}
+
+__global__ void k_escape_records_f(const unsigned long long* __restrict__ idx, long long n,
+                                   const double2* __restrict__ freq_cur, HalfGeom g, EscapeRec* out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long h = idx[i];
+        const double2 v = freq_cur[g.offset_of(static_cast<long long>(h))];
+        out[i] = EscapeRec{1, 0, h, v.x, v.y};
     }
 }
 

@@ -29,6 +29,12 @@ struct FreqB {
     double g;
     __device__ __forceinline__ double re_at(long long off) const { return re ? re[off] : g; }
     __device__ __forceinline__ double im_at(long long off) const { return im ? im[off] : g; }
+    // both lanes with one load when they share storage (rho-mode bounds: Re lane == Im lane)
+    __device__ __forceinline__ double2 at2(long long off) const {
+        if (!re) return make_double2(g, g);
+        const double r = re[off];
+        return make_double2(r, im == re ? r : im[off]);
+    }
 };
 
 // std::clamp(v, -b, b) (projection.cpp:14-16)
@@ -111,7 +117,8 @@ struct HookFReduce {
     __device__ __forceinline__ void post(C& v, long long off, int) {
         const double ar = fabs(static_cast<double>(v.x)), ai = fabs(static_cast<double>(v.y));
         peak = fmax(peak, fmax(ar, ai));
-        const double e = fmax(ar - fb.re_at(off) * fscale, ai - fb.im_at(off) * fscale);
+        const double2 d = fb.at2(off);
+        const double e = fmax(ar - d.x * fscale, ai - d.y * fscale);
         if (e > ex) ex = e;
     }
     __device__ __forceinline__ void finish() { block_max2_atomic(peak, ex, &ctl->peak_bits, &ctl->exc_bits); }
@@ -135,7 +142,8 @@ struct HookFClip {
     template <class C>
     __device__ __forceinline__ void pre(C& v, long long off, int) {
         const double re = v.x, im = v.y;
-        const double dre = fb.re_at(off) * fscale, dim = fb.im_at(off) * fscale;
+        const double2 d = fb.at2(off);
+        const double dre = d.x * fscale, dim = d.y * fscale;
         const double cre = clamp_abs(re, dre), cim = clamp_abs(im, dim);
         const double xre = cre - re, xim = cim - im;
         if (first) {
@@ -180,7 +188,7 @@ struct HookSClip {
     __device__ __forceinline__ void post_real(T& x0, T& x1, long long n) {
         x0 = one(x0, n);
         x1 = one(x1, n + 1);
-        reinterpret_cast<typename cvec<T>::type*>(eps)[n >> 1] = mkc<T>(x0, x1);
+        if (eps) reinterpret_cast<typename cvec<T>::type*>(eps)[n >> 1] = mkc<T>(x0, x1);
     }
     __device__ __forceinline__ void finish() {}
 };
@@ -282,7 +290,8 @@ struct HookMarkViol {
     template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
     template <class C>
     __device__ __forceinline__ void post(C& v, long long off, int) {
-        if (fabs(v.x) > fb.re_at(off) || fabs(v.y) > fb.im_at(off)) {
+        const double2 d = fb.at2(off);
+        if (fabs(v.x) > d.x || fabs(v.y) > d.y) {
             set_bit_g(viol_words, off);
             any = 1;
         }
@@ -301,7 +310,8 @@ struct HookVerifyF {
     template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
     template <class C>
     __device__ __forceinline__ void post(C& v, long long off, int) {
-        const double ex = fmax(fabs(v.x) - fb.re_at(off), fabs(v.y) - fb.im_at(off));
+        const double2 d = fb.at2(off);
+        const double ex = fmax(fabs(v.x) - d.x, fabs(v.y) - d.y);
         if (ex > 0.0 && ex > m) m = ex;
     }
     __device__ __forceinline__ void finish() { block_max2_atomic(m, 0.0, &ctl->vf_bits, nullptr); }
@@ -401,6 +411,18 @@ __global__ void k_repair_freq_sparse(const unsigned* __restrict__ viol_words, lo
                                      const double2* __restrict__ delta_tilde, HalfGeom g,
                                      long long d0, long long d1, double2* freq_cur,
                                      unsigned* esc_words);
+// device image of ffcz_cuda_escape (include/ffcz_cuda.h): int32 frequency, u64 index, re, im
+struct EscapeRec {
+    int frequency;
+    int pad;
+    unsigned long long index;
+    double re, im;
+};
+static_assert(sizeof(EscapeRec) == 32, "EscapeRec layout");
+__global__ void k_escape_records_s(const unsigned long long* __restrict__ idx, long long n,
+                                   const double* __restrict__ spat_cur, EscapeRec* out);
+__global__ void k_escape_records_f(const unsigned long long* __restrict__ idx, long long n,
+                                   const double2* __restrict__ freq_cur, HalfGeom g, EscapeRec* out);
 __global__ void k_gather_escapes_s(const unsigned long long* __restrict__ idx, long long n,
                                    const double* __restrict__ spat_cur, double* out_re);
 __global__ void k_gather_escapes_f(const unsigned long long* __restrict__ idx, long long n,
