@@ -343,7 +343,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = t.item()
         d2h = (r.spatial_flags.nbytes + r.frequency_flags.nbytes + r.spatial_codes.nbytes +
-               r.frequency_codes.nbytes + 32 * len(r.escapes) + 8 * N)
+               r.frequency_codes.nbytes + r.escapes.nbytes + 8 * N)
         e2e = {"value": world * 4.0 * N / te / 1e9, "unit": "GB/s",
                "lib_timings_ms": r.timings_ms,
                "h2d_bytes_per_step": 4 * N * 2 + 8 * N, "d2h_bytes_per_step": int(d2h),

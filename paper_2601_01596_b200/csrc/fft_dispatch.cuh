@@ -98,7 +98,7 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
     int B = static_cast<int>(std::min<long long>(tile_budget<T>(role) / L, MAXT / TT));
     B = std::min(B, 128);
     B = std::min(B, pow2_ceil(ncols));
-    B = std::max(B, 1);
+    B = std::max(B, (32 + TT - 1) / TT);  // whole warps (full-mask block reductions in hooks)
     const size_t smem = col_smem_bytes<T, L, E>(B);
     const long long ntiles = static_cast<long long>((ncols + B - 1) / B) * nplanes;
     auto k = dir < 0 ? k_col<T, L, E, -1, Hook> : k_col<T, L, E, +1, Hook>;
@@ -120,6 +120,8 @@ int rows_per_cta(long long nrows) {
     constexpr int TT = RowCfg<T, M>::TT;
     long long r = std::min<long long>(tile_budget<T>(TileRole::kRow) / M, RowCfg<T, M>::MAXT / TT);
     r = std::min<long long>(r, pow2_ceil(nrows));
+    // whole warps only: the paired split/merge and the block reductions use full-mask shuffles
+    r = std::max<long long>(r, (32 + TT - 1) / TT);
     return static_cast<int>(std::max<long long>(1, r));
 }
 

@@ -120,6 +120,11 @@ class ProjectionReport:
     wall_time_s: float
 
 
+# numpy image of ffcz_cuda_escape (include/ffcz_cuda.h)
+ESCAPE_DTYPE = np.dtype([("frequency", "<i4"), ("_pad", "<i4"), ("index", "<u8"), ("re", "<f8"),
+                         ("im", "<f8")])
+
+
 @dataclass
 class EscapeEntry:
     frequency: bool
@@ -142,7 +147,7 @@ class CorrectionResult:
     frequency_flags: np.ndarray | None
     spatial_codes: np.ndarray | None
     frequency_codes: np.ndarray | None
-    escapes: list
+    escapes: np.ndarray | None          # structured: frequency, index, re, im (EscapeEntry order)
     corrected: np.ndarray | None
     escape_rounds: int
     timings_ms: dict
@@ -282,15 +287,21 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
 
         edits = want_edits or want_archive
         sflags = fflags = scodes = fcodes = None
-        escapes = []
+        escapes = None
         if edits:
             sflags = arr(res.spatial_flags, int(res.spatial_flag_bytes), np.uint8)
             fflags = arr(res.frequency_flags, int(res.frequency_flag_bytes), np.uint8)
             scodes = arr(res.spatial_codes, int(res.n_spatial), np.int32)
             fcodes = arr(res.frequency_codes, 2 * int(res.n_frequency), np.int32)
-            for i in range(int(res.escape_count)):
-                e = res.escapes[i]
-                escapes.append(EscapeEntry(bool(e.frequency), int(e.index), float(e.re), float(e.im)))
+            ne = int(res.escape_count)
+            if ne and res.escapes:
+                raw = np.ctypeslib.as_array(C.cast(res.escapes, C.POINTER(C.c_uint8)),
+                                            shape=(ne * C.sizeof(capi.Escape),))
+                escapes = raw.view(ESCAPE_DTYPE)
+                if copy:
+                    escapes = escapes.copy()
+            else:
+                escapes = np.zeros(0, dtype=ESCAPE_DTYPE)
         corrected = None
         if want_corrected:
             corrected = np.ctypeslib.as_array(res.corrected, shape=(N,)).reshape(shape)
