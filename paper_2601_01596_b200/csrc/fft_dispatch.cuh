@@ -53,6 +53,15 @@ template <class T> long long tile_budget(TileRole role) {
     return v[static_cast<int>(role)];
 }
 
+// FFCZ_COL_TMA=0 selects the register-direct column pass (A/B runs); default: TMA-staged.
+inline bool col_tma_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_COL_TMA");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <class K>
 void set_smem(K kernel, size_t bytes) {
     if (bytes > 48 * 1024)
@@ -101,6 +110,27 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
     B = std::max(B, (32 + TT - 1) / TT);  // whole warps (full-mask block reductions in hooks)
     const size_t smem = col_smem_bytes<T, L, E>(B);
     const long long ntiles = static_cast<long long>((ncols + B - 1) / B) * nplanes;
+    if (col_tma_enabled()) {
+        // TMA-staged double-buffered pass: B columns per tile bounded by 1 CTA/SM of smem
+        int Bt = static_cast<int>(std::min<long long>(MAXT / TT, 128));
+        while (Bt > 1 && col_tma_smem_bytes<T, L, E>(Bt) > 220 * 1024) Bt /= 2;
+        if (const char* e = std::getenv("FFCZ_COL_TMA_B")) Bt = std::max(1, std::atoi(e));
+        Bt = std::min(Bt, pow2_ceil(ncols));
+        const size_t tsmem = col_tma_smem_bytes<T, L, E>(Bt);
+        CUtensorMap map;
+        if (TT * Bt >= 32 && Bt * sizeof(cplx<T>) >= 32 && tsmem <= 227 * 1024 &&
+            encode_col_map(&map, src, sizeof(T), ncols, L, row_stride, nplanes, plane_stride, Bt,
+                           L < 256 ? L : 256)) {
+            auto kt = dir < 0 ? k_col_tma<T, L, E, -1, Hook> : k_col_tma<T, L, E, +1, Hook>;
+            set_smem(kt, tsmem);
+            const long long nt = static_cast<long long>((ncols + Bt - 1) / Bt) * nplanes;
+            const unsigned grid = persistent_grid(kt, TT * Bt, tsmem, nt);
+            kt<<<grid, TT * Bt, tsmem, st>>>(map, dst, row_stride, plane_stride, ncols, Bt, nt,
+                                             tw.stage_table(L, E), gate, hook);
+            FFCZ_LAUNCH_CHECK();
+            return;
+        }
+    }
     auto k = dir < 0 ? k_col<T, L, E, -1, Hook> : k_col<T, L, E, +1, Hook>;
     set_smem(k, smem);
     const unsigned grid = persistent_grid(k, TT * B, smem, ntiles);

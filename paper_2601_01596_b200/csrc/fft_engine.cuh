@@ -24,6 +24,7 @@
 #include <utility>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace ffcz_gpu {
 
@@ -276,6 +277,88 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
         }
     }
     hook.finish();
+}
+
+// TMA-staged column pass.  Same tile and register layout as k_col, but the tile is brought into
+// shared memory by two 3-D TMA boxes per 256 rows (cp.async.bulk.tensor, mbarrier completion),
+// double-buffered: while tile k is transformed out of buffer k%2 (which then serves as its
+// exchange buffer), tile k+1 is already landing in the other buffer, and tile k+2 is issued the
+// moment tile k's exchanges are done — so HBM always has a tile in flight per SM (the
+// load/compute/store serialisation measured in profiles/r01_summary.md).  Out-of-range columns
+// of the ragged last tile arrive zero-filled from the TMA.
+// smem: 2 x (L + L/E) x B complex + 2 mbarriers.
+template <class T, int L, int E, int DIR, class Hook>
+__global__ void __launch_bounds__(max_threads<T, E>(), 1)
+    k_col_tma(const __grid_constant__ CUtensorMap map, cplx<T>* __restrict__ dst,
+              long long row_stride, long long plane_stride, int ncols, int B, long long ntiles,
+              const cplx<T>* __restrict__ tw, const int* gate, Hook hook) {
+    if (gated(gate)) return;
+    hook_begin(hook);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int TT = L / E;
+    constexpr int LB = L < 256 ? L : 256;
+    const int b = threadIdx.x % B;
+    const int t = threadIdx.x / B;
+    const int tiles_c = (ncols + B - 1) / B;
+    const int buf_elems = (L + L / E) * B;
+    cplx<T>* bufs = reinterpret_cast<cplx<T>*>(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(bufs + 2 * buf_elems);
+    const unsigned tile_bytes = static_cast<unsigned>(L) * B * sizeof(cplx<T>);
+    auto issue = [&](long long tile, int slot) {
+        const long long plane = tile / tiles_c;
+        const int c0 = static_cast<int>(tile - plane * tiles_c) * B;
+        mbar_arrive_expect_tx(&bars[slot], tile_bytes);
+#pragma unroll
+        for (int j = 0; j < L / LB; ++j)
+            tma_load_3d(bufs + slot * buf_elems + j * LB * B, &map, &bars[slot], 2 * c0, j * LB,
+                        static_cast<int>(plane));
+    };
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&map);
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+        if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+    }
+    unsigned phase = 0;  // bit s = parity of the next completion of buffer s
+    int slot = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, slot ^= 1) {
+        cplx<T>* s = bufs + slot * buf_elems;
+        mbar_wait(&bars[slot], (phase >> slot) & 1u);
+        phase ^= 1u << slot;
+        const long long plane = tile / tiles_c;
+        const int c = static_cast<int>(tile - plane * tiles_c) * B + b;
+        const bool valid = c < ncols;
+        const long long base = plane * plane_stride + c;
+        cplx<T> v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            v[m] = s[(t + TT * m) * B + b];
+            if (valid) hook.pre(v[m], base + static_cast<long long>(t + TT * m) * row_stride, c);
+        }
+        stockham<T, L, E, 1, DIR>(v, t, tw, XchCol<T, E>{s + b, B});
+        fence_proxy_async_smem();  // this thread's exchange writes before the async-proxy refill
+        __syncthreads();           // every thread is done with buffer `slot`
+        if (threadIdx.x == 0 && tile + 2 * gridDim.x < ntiles) issue(tile + 2 * gridDim.x, slot);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const long long off = base + static_cast<long long>(t + TT * m) * row_stride;
+            if (valid) {
+                hook.post(v[m], off, c);
+                if constexpr (hook_stores<Hook>()) dst[off] = v[m];
+            }
+        }
+    }
+    hook.finish();
+}
+
+template <class T, int L, int E>
+constexpr size_t col_tma_smem_bytes(int B) {
+    return 2 * static_cast<size_t>(L + L / E) * B * sizeof(cplx<T>) + 2 * sizeof(uint64_t);
 }
 
 template <class T, int L, int E>

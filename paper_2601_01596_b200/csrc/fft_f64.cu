@@ -6,6 +6,36 @@
 
 namespace ffcz_gpu {
 
+bool encode_col_map(CUtensorMap* map, const void* base, int scalar_bytes, long long ncols,
+                    long long L, long long row_stride, long long nplanes, long long plane_stride,
+                    int B, int LB) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) return false;
+    const long long cb = 2LL * scalar_bytes;  // bytes per complex element
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || (row_stride * cb) % 16 || (plane_stride * cb) % 16)
+        return false;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * ncols), static_cast<cuuint64_t>(L),
+                                static_cast<cuuint64_t>(nplanes)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(row_stride * cb),
+                                   static_cast<cuuint64_t>(plane_stride * cb)};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(2 * B), static_cast<cuuint32_t>(LB), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode(map, scalar_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                                     : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                              3, const_cast<void*>(base), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 Geometry make_geometry(int ndim, const uint64_t* dims, int pitch_align) {
     if (ndim < 1 || ndim > 3)
         throw Error(kValidation, "dims must have 1 to 3 axes, got " + std::to_string(ndim));
