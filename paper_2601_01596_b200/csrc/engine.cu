@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -79,12 +80,15 @@ struct ffcz_cuda_ctx {
     int device = 0;
     cudaStream_t st = nullptr;
     bool own_stream = false;
+    cudaStream_t st_copy = nullptr;  // D2H of the edit set, overlapped with repair / verify
+    cudaEvent_t ev_codes = nullptr;
     std::mutex mu;
     Twiddles<double> tw64;
     Twiddles<float> tw32;
     std::map<std::string, std::pair<void*, size_t>> bufs;
     Ctl* ctl = nullptr;
     Ctl* hctl = nullptr;   // pinned mirror (one slot per in-flight chunk)
+    Ctl* hctl_dev = nullptr;  // device alias of the mapped mirror (k_export_ctl writes it)
     unsigned long long launches = 0;
     cudaEvent_t ev[8] = {};
     // per-kernel-class profiling (ffcz_cuda_profile_*)
@@ -111,6 +115,7 @@ struct ffcz_cuda_ctx {
         if (it != bufs.end() && it->second.second >= bytes) return it->second.first;
         if (it != bufs.end()) {
             FFCZ_CUDA_CHECK(cudaStreamSynchronize(st));
+            if (st_copy) FFCZ_CUDA_CHECK(cudaStreamSynchronize(st_copy));
             cudaFree(it->second.first);
             bufs.erase(it);
         }
@@ -124,7 +129,8 @@ struct ffcz_cuda_ctx {
     }
     void sync() { FFCZ_CUDA_CHECK(cudaStreamSynchronize(st)); }
     Ctl read_ctl() {
-        FFCZ_CUDA_CHECK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        k_export_ctl<<<1, 32, 0, st>>>(ctl, hctl_dev);
+        FFCZ_LAUNCH_CHECK();
         sync();
         return *hctl;
     }
@@ -220,14 +226,16 @@ Bounds upload_bounds(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_bounds_desc
             throw Error(kValidation, "per-component frequency bound arrays are null");
         const HalfGeom hg = g.hg();
         auto restrict_lane = [&](const double* full, const char* name) {
-            const double* dfull = full;
-            if (!on_dev) {
-                double* stage = c.b<double>("bounds_stage", N);
-                FFCZ_CUDA_CHECK(cudaMemcpyAsync(stage, full, N * sizeof(double),
-                                                cudaMemcpyHostToDevice, c.st));
-                dfull = stage;
-            }
             double* half = c.b<double>(name, g.half_elems());
+            if (!on_dev) {
+                // host lane: copy only the half-grid columns k2 <= n2/2 of every row, straight
+                // into the pitched half layout (one strided DMA; half the bytes of the full lane)
+                FFCZ_CUDA_CHECK(cudaMemcpy2DAsync(half, g.P * sizeof(double), full,
+                                                  g.n2 * sizeof(double), g.H * sizeof(double),
+                                                  g.rows, cudaMemcpyHostToDevice, c.st));
+                return half;
+            }
+            const double* dfull = full;
             {
                 Prof p(c, kElemPre, 16.0 * g.Nc());
                 k_gather_half<<<grid_for(g.Nc()), 256, 0, c.st>>>(dfull, half, hg);
@@ -345,8 +353,8 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
         const int n = kChunk[std::min(ci++, 4)];
         for (int i = 0; i < n; ++i) body();
         const int slot = issued % 2;
-        FFCZ_CUDA_CHECK(cudaMemcpyAsync(&c.hctl[1 + slot], c.ctl, sizeof(Ctl),
-                                        cudaMemcpyDeviceToHost, st));
+        k_export_ctl<<<1, 32, 0, st>>>(c.ctl, &c.hctl_dev[1 + slot]);
+        FFCZ_LAUNCH_CHECK();
         cudaEvent_t ev = c.ev[4 + slot];
         FFCZ_CUDA_CHECK(cudaEventRecord(ev, st));
         inflight.push_back({ev, slot});
@@ -439,7 +447,8 @@ void c2r_p(ffcz_cuda_ctx& c, const FftPlan<double>& plan, const double2* half, d
 template <class TI>
 GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* dec,
                  const Bounds& bo, int m, bool converged, bool fused, double* eps, double* S,
-                 double2* F, double* corrected) {
+                 double2* F, double* corrected,
+                 const std::function<void(unsigned long long, unsigned long long)>& on_codes) {
     cudaStream_t st = c.st;
     FftPlan<double> plan{g, &c.tw64};
     const HalfGeom hg = g.hg();
@@ -467,18 +476,34 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
     c.launches += 2;
 
     GateOut o;
-    o.n_keep_s = compact_bits(c, keep_s, ws, idx);
-    {
-        Prof p(c, kElemCodes, 0.0);
-        k_codes_spatial<<<grid_for(o.n_keep_s), 256, 0, st>>>(idx, o.n_keep_s, S, bo.sb, m, codes_s);
-    }
-    o.n_keep_f = compact_bits(c, keep_f, wf, idx);
-    {
-        Prof p(c, kElemCodes, 0.0);
-        k_codes_freq<<<grid_for(o.n_keep_f), 256, 0, st>>>(idx, o.n_keep_f, F, hg, bo.fb, m, codes_f);
-    }
-    FFCZ_LAUNCH_CHECK();
-    c.launches += 2;
+    // counts + offsets of the keep bitmaps, then codes written straight from the bits
+    auto codes_from = [&](const unsigned* words, long long nwords, const char* cname,
+                          auto launch_codes) {
+        const long long nblk = std::max<long long>(1, (nwords + 1023) / 1024);
+        unsigned long long* counts = c.b<unsigned long long>(cname, nblk + 1);
+        {
+            Prof p(c, kElemCompact, 0.0);
+            k_popc_blocks<<<static_cast<unsigned>(nblk), 1024, 0, st>>>(words, nwords, counts);
+            k_scan_blocks<<<1, 1024, 0, st>>>(counts, nblk, &c.ctl->count_a);
+        }
+        {
+            Prof p(c, kElemCodes, 0.0);
+            launch_codes(static_cast<unsigned>(nblk), counts);
+        }
+        FFCZ_LAUNCH_CHECK();
+        c.launches += 3;
+        return c.read_ctl().count_a;
+    };
+    o.n_keep_s = codes_from(keep_s, ws, "blk_counts_s", [&](unsigned nb, unsigned long long* off) {
+        k_codes_spatial_bits<<<nb, 1024, 0, st>>>(keep_s, ws, off, S, bo.sb, m, codes_s);
+    });
+    o.n_keep_f = codes_from(keep_f, wf, "blk_counts_f", [&](unsigned nb, unsigned long long* off) {
+        k_codes_freq_bits<<<nb, 1024, 0, st>>>(keep_f, wf, off, F, hg, bo.fb, m, codes_f);
+    });
+    (void)idx;
+    // flags and codes are final here (repair rounds only add escapes): hand them to the copy
+    // stream so their D2H overlaps the repair / verify passes
+    if (on_codes) on_codes(o.n_keep_s, o.n_keep_f);
 
     // delta_star = FFT(final_eps) is the spectrum the loop's last convergence check produced
     // (still in `spec`); S and F are consumed, so they become the round's real / half work buffers.
@@ -518,12 +543,29 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
             c.launches += three_d ? 5 : 3;
         };
         const double in_bytes = 2.0 * sizeof(TI) * N + 16.0 * N;  // orig, dec, spat_cur, eps_tilde
+        auto forward_row_mid = [&](const double* x) {
+            {
+                Prof p(c, kRowR2C, 8.0 * g.N + 16.0 * Nc);
+                launch_row_r2c<double>(g.n2, x, g.n2, work, g.P, g.rows, c.tw64, nullptr, st);
+            }
+            if (three_d) {
+                Prof p(c, kColPass, pass);
+                plan.col(1, -1, work, work, nullptr, HookNone{}, st);
+            }
+            c.launches += three_d ? 2 : 1;
+        };
+        bool verified = false;
         if (converged) {
+            double* eps_v = c.b<double>("eps_verify", N);
             for (int round = 0; round < 32; ++round) {                   // pipeline.cpp:116
                 FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->dirty, 0, sizeof(int), st));
+                FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->vs_bits, 0, 2 * sizeof(unsigned long long), st));
                 FFCZ_CUDA_CHECK(cudaMemsetAsync(viol, 0, vw * sizeof(unsigned), st));
-                inverse_and_row(HookRepairS<TI>{orig, dec, spat_cur, eps, bo.sb, esc_s, c.ctl},
-                                16.0 * Nc + in_bytes);
+                // inverse once: eps_tilde for the repair check (pipeline.cpp:125-136) and, in case
+                // the round is clean, the decoder view for verify (pipeline.cpp:174-176)
+                inverse_and_row(HookRepairVerifyS<TI>{orig, dec, spat_cur, eps, bo.sb, esc_s,
+                                                      corrected, eps_v, c.ctl},
+                                16.0 * Nc + in_bytes + 24.0 * N);
                 {
                     Prof p(c, kColFwdCheck, pass);
                     plan.col(za, -1, work, work, nullptr, HookMarkViol{bo.fb, viol, c.ctl}, st);
@@ -533,17 +575,31 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
                 FFCZ_LAUNCH_CHECK();
                 c.launches += 2;
                 ++o.rounds;
-                if (!c.read_ctl().dirty) break;                          // :161
+                if (!c.read_ctl().dirty) {                               // :161
+                    // clean round: spat_cur / freq_cur are final and eps_v is their decoder
+                    // view, so its forward transform completes verify_bounds
+                    forward_row_mid(eps_v);
+                    {
+                        Prof p(c, kColFwdCheck, 16.0 * Nc);
+                        plan.col(za, -1, work, work, nullptr, HookVerifyF{bo.fb, c.ctl}, st);
+                    }
+                    ++c.launches;
+                    verified = true;
+                    break;
+                }
             }
         }
-        // apply_edits + verify_bounds on the decoder view (pipeline.cpp:174-176)
-        inverse_and_row(HookVerifyS<TI>{orig, dec, spat_cur, corrected, bo.sb, c.ctl},
-                        16.0 * Nc + in_bytes + 8.0 * N);
-        {
-            Prof p(c, kColFwdCheck, 16.0 * Nc);
-            plan.col(za, -1, work, work, nullptr, HookVerifyF{bo.fb, c.ctl}, st);
+        if (!verified) {
+            // apply_edits + verify_bounds on the decoder view (pipeline.cpp:174-176)
+            FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->vs_bits, 0, 2 * sizeof(unsigned long long), st));
+            inverse_and_row(HookVerifyS<TI>{orig, dec, spat_cur, corrected, bo.sb, c.ctl},
+                            16.0 * Nc + in_bytes + 8.0 * N);
+            {
+                Prof p(c, kColFwdCheck, 16.0 * Nc);
+                plan.col(za, -1, work, work, nullptr, HookVerifyF{bo.fb, c.ctl}, st);
+            }
+            c.launches += 1;
         }
-        c.launches += 1;
     } else {
         if (converged) {
             for (int round = 0; round < 32; ++round) {                   // pipeline.cpp:116
@@ -652,9 +708,35 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     }
     ++c.launches;
 
-    double* corrected = c.b<double>("corrected", N);
+    // the FP64 corrected field is only materialised when the caller asks for it (the reference's
+    // CorrectionResult carries no field; verify needs only its epsilon)
+    double* corrected = (opt.flags & FFCZ_WANT_CORRECTED) ? c.b<double>("corrected", N) : nullptr;
+    const bool want_edits = opt.flags & (FFCZ_WANT_EDITS | FFCZ_WANT_ARCHIVE);
+    const long long ws = (N + 31) / 32, wf = (g.Nc() + 31) / 32;
+    bool copy_pending = false;
+    auto on_codes = [&](unsigned long long ns, unsigned long long nf) {
+        if (!want_edits) return;
+        out->spatial_flag_bytes = (N + 7) / 8;
+        out->frequency_flag_bytes = (g.Nc() + 7) / 8;
+        out->spatial_flags = static_cast<uint8_t*>(pinned().get(out->spatial_flag_bytes + 1));
+        out->frequency_flags = static_cast<uint8_t*>(pinned().get(out->frequency_flag_bytes + 1));
+        out->spatial_codes = static_cast<int32_t*>(pinned().get(ns * 4 + 4));
+        out->frequency_codes = static_cast<int32_t*>(pinned().get(nf * 8 + 4));
+        FFCZ_CUDA_CHECK(cudaEventRecord(c.ev_codes, st));
+        FFCZ_CUDA_CHECK(cudaStreamWaitEvent(c.st_copy, c.ev_codes, 0));
+        cudaStream_t cs = c.st_copy;
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->spatial_flags, c.b<unsigned>("keep_s", ws),
+                                        out->spatial_flag_bytes, cudaMemcpyDeviceToHost, cs));
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->frequency_flags, c.b<unsigned>("keep_f", wf),
+                                        out->frequency_flag_bytes, cudaMemcpyDeviceToHost, cs));
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->spatial_codes, c.b<int>("codes_s", N), ns * 4,
+                                        cudaMemcpyDeviceToHost, cs));
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->frequency_codes, c.b<int>("codes_f", 2 * g.Nc()),
+                                        nf * 8, cudaMemcpyDeviceToHost, cs));
+        copy_pending = true;
+    };
     const GateOut go = run_gate<TI>(c, g, orig, dec, bo, m, lr.converged, lr.fused, eps, S, F,
-                                    corrected);
+                                    corrected, on_codes);
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[6], st));
     dbg.mark(c, "gate done");
     h = c.read_ctl();
@@ -682,7 +764,6 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     // ---- products to the host -------------------------------------------------------------
     const auto t_d2h0 = std::chrono::steady_clock::now();
     const EscapeRec* escape_dev = nullptr;
-    const long long ws = (N + 31) / 32, wf = (g.Nc() + 31) / 32;
     unsigned long long n_esc = 0;
     {
         unsigned long long* idx = c.b<unsigned long long>("idx", std::max(N, g.Nc()));
@@ -712,22 +793,7 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     std::vector<ffcz_cuda_escape> escapes;  // only for the archive writer below
     out->escape_count = n_esc;
     dbg.mark(c, "escapes compacted");
-    const bool want_edits = opt.flags & (FFCZ_WANT_EDITS | FFCZ_WANT_ARCHIVE);
     if (want_edits) {
-        out->spatial_flag_bytes = (N + 7) / 8;
-        out->frequency_flag_bytes = (g.Nc() + 7) / 8;
-        out->spatial_flags = static_cast<uint8_t*>(pinned().get(out->spatial_flag_bytes + 1));
-        out->frequency_flags = static_cast<uint8_t*>(pinned().get(out->frequency_flag_bytes + 1));
-        out->spatial_codes = static_cast<int32_t*>(pinned().get(go.n_keep_s * 4 + 4));
-        out->frequency_codes = static_cast<int32_t*>(pinned().get(go.n_keep_f * 8 + 4));
-        FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->spatial_flags, c.b<unsigned>("keep_s", ws),
-                                        out->spatial_flag_bytes, cudaMemcpyDeviceToHost, st));
-        FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->frequency_flags, c.b<unsigned>("keep_f", wf),
-                                        out->frequency_flag_bytes, cudaMemcpyDeviceToHost, st));
-        FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->spatial_codes, c.b<int>("codes_s", N), go.n_keep_s * 4,
-                                        cudaMemcpyDeviceToHost, st));
-        FFCZ_CUDA_CHECK(cudaMemcpyAsync(out->frequency_codes, c.b<int>("codes_f", 2 * g.Nc()),
-                                        go.n_keep_f * 8, cudaMemcpyDeviceToHost, st));
         out->escapes = static_cast<ffcz_cuda_escape*>(
             pinned().get(sizeof(ffcz_cuda_escape) * (n_esc + 1)));
         if (n_esc)
@@ -741,6 +807,7 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
                                         cudaMemcpyDeviceToHost, st));
     }
     c.sync();
+    if (copy_pending) FFCZ_CUDA_CHECK(cudaStreamSynchronize(c.st_copy));
     const auto t_d2h1 = std::chrono::steady_clock::now();
     out->t_d2h_ms = std::chrono::duration<double, std::milli>(t_d2h1 - t_d2h0).count();
     dbg.mark(c, "corrected to host");
@@ -864,8 +931,11 @@ int ffcz_cuda_create(ffcz_cuda_ctx** out, int device, void* stream) {
             c->own_stream = true;
         }
         FFCZ_CUDA_CHECK(cudaMalloc(&c->ctl, sizeof(Ctl)));
-        FFCZ_CUDA_CHECK(cudaMallocHost(&c->hctl, 4 * sizeof(Ctl)));
+        FFCZ_CUDA_CHECK(cudaHostAlloc(&c->hctl, 4 * sizeof(Ctl), cudaHostAllocMapped));
+        FFCZ_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hctl_dev), c->hctl, 0));
         for (auto& e : c->ev) FFCZ_CUDA_CHECK(cudaEventCreate(&e));
+        FFCZ_CUDA_CHECK(cudaStreamCreateWithFlags(&c->st_copy, cudaStreamNonBlocking));
+        FFCZ_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_codes, cudaEventDisableTiming));
         c->tw64.init();
         c->tw32.init();
         *out = c;
@@ -881,11 +951,14 @@ void ffcz_cuda_destroy(ffcz_cuda_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->st);
+    if (c->st_copy) cudaStreamSynchronize(c->st_copy);
     for (auto& kv : c->bufs) cudaFree(kv.second.first);
     if (c->ctl) cudaFree(c->ctl);
     if (c->hctl) cudaFreeHost(c->hctl);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    if (c->ev_codes) cudaEventDestroy(c->ev_codes);
+    if (c->st_copy) cudaStreamDestroy(c->st_copy);
     if (c->own_stream) cudaStreamDestroy(c->st);
     delete c;
 }

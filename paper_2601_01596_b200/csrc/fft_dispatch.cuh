@@ -111,22 +111,32 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
     const size_t smem = col_smem_bytes<T, L, E>(B);
     const long long ntiles = static_cast<long long>((ncols + B - 1) / B) * nplanes;
     if (col_tma_enabled()) {
-        // TMA-staged double-buffered pass: B columns per tile bounded by 1 CTA/SM of smem
+        // TMA-staged double-buffered pass: B columns per tile bounded by 1 CTA/SM of smem; a
+        // single-lane per-component Delta rides along as a side tile
+        const double* side = nullptr;
+        if constexpr (hook_delta<Hook>())
+            if (hook.fb.re && hook.fb.im == hook.fb.re) side = hook.fb.re;
         int Bt = static_cast<int>(std::min<long long>(MAXT / TT, 128));
-        while (Bt > 1 && col_tma_smem_bytes<T, L, E>(Bt) > 220 * 1024) Bt /= 2;
+        while (Bt > 1 && col_tma_smem_bytes<T, L, E>(Bt, side) > 220 * 1024) Bt /= 2;
         if (const char* e = std::getenv("FFCZ_COL_TMA_B")) Bt = std::max(1, std::atoi(e));
         Bt = std::min(Bt, pow2_ceil(ncols));
-        const size_t tsmem = col_tma_smem_bytes<T, L, E>(Bt);
-        CUtensorMap map;
-        if (TT * Bt >= 32 && Bt * sizeof(cplx<T>) >= 32 && tsmem <= 227 * 1024 &&
-            encode_col_map(&map, src, sizeof(T), ncols, L, row_stride, nplanes, plane_stride, Bt,
-                           L < 256 ? L : 256)) {
+        const size_t tsmem = col_tma_smem_bytes<T, L, E>(Bt, side);
+        CUtensorMap map, side_map;
+        bool ok = TT * Bt >= 32 && Bt * sizeof(cplx<T>) >= 32 && tsmem <= 227 * 1024 &&
+                  encode_col_map(&map, src, sizeof(T), ncols, L, row_stride, nplanes,
+                                 plane_stride, Bt, L < 256 ? L : 256, true);
+        if (ok && side)
+            ok = encode_col_map(&side_map, side, 8, ncols, L, row_stride, nplanes, plane_stride,
+                                Bt, L < 256 ? L : 256, false);
+        if (ok) {
+            if (!side) side_map = map;
             auto kt = dir < 0 ? k_col_tma<T, L, E, -1, Hook> : k_col_tma<T, L, E, +1, Hook>;
             set_smem(kt, tsmem);
             const long long nt = static_cast<long long>((ncols + Bt - 1) / Bt) * nplanes;
             const unsigned grid = persistent_grid(kt, TT * Bt, tsmem, nt);
-            kt<<<grid, TT * Bt, tsmem, st>>>(map, dst, row_stride, plane_stride, ncols, Bt, nt,
-                                             tw.stage_table(L, E), gate, hook);
+            kt<<<grid, TT * Bt, tsmem, st>>>(map, side_map, side != nullptr, dst, row_stride,
+                                             plane_stride, ncols, Bt, nt, tw.stage_table(L, E),
+                                             gate, hook);
             FFCZ_LAUNCH_CHECK();
             return;
         }

@@ -279,42 +279,64 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     hook.finish();
 }
 
+// Hooks that compare against the frequency bound declare kDelta and take Delta(off) as an
+// argument (pre_d / post_d), so the staged pass can hand them the value from its TMA side tile.
+template <class H>
+constexpr bool hook_delta() {
+    if constexpr (requires { H::kDelta; })
+        return H::kDelta;
+    else
+        return false;
+}
+
 // TMA-staged column pass.  Same tile and register layout as k_col, but the tile is brought into
-// shared memory by two 3-D TMA boxes per 256 rows (cp.async.bulk.tensor, mbarrier completion),
-// double-buffered: while tile k is transformed out of buffer k%2 (which then serves as its
+// shared memory by 3-D TMA boxes (cp.async.bulk.tensor, mbarrier completion, <= 256 rows per
+// box), double-buffered: while tile k is transformed out of buffer k%2 (which then serves as its
 // exchange buffer), tile k+1 is already landing in the other buffer, and tile k+2 is issued the
-// moment tile k's exchanges are done — so HBM always has a tile in flight per SM (the
-// load/compute/store serialisation measured in profiles/r01_summary.md).  Out-of-range columns
-// of the ragged last tile arrive zero-filled from the TMA.
-// smem: 2 x (L + L/E) x B complex + 2 mbarriers.
+// moment buffer k%2 is free — so HBM always has a tile in flight per SM (the load/compute/store
+// serialisation measured in profiles/r01_summary.md).  Out-of-range columns of the ragged last
+// tile arrive zero-filled.  With `has_side`, the per-component bound Delta (one FP64 lane in the
+// same pitched layout) rides along as a side tile on the same mbarrier, so the check / clip hooks
+// never wait on a dependent global load.
+// smem: 2 x (L + L/E) x B complex [+ 2 x L x B doubles side] + 2 mbarriers.
 template <class T, int L, int E, int DIR, class Hook>
 __global__ void __launch_bounds__(max_threads<T, E>(), 1)
-    k_col_tma(const __grid_constant__ CUtensorMap map, cplx<T>* __restrict__ dst,
-              long long row_stride, long long plane_stride, int ncols, int B, long long ntiles,
-              const cplx<T>* __restrict__ tw, const int* gate, Hook hook) {
+    k_col_tma(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap side_map,
+              int has_side, cplx<T>* __restrict__ dst, long long row_stride, long long plane_stride,
+              int ncols, int B, long long ntiles, const cplx<T>* __restrict__ tw, const int* gate,
+              Hook hook) {
     if (gated(gate)) return;
     hook_begin(hook);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int TT = L / E;
     constexpr int LB = L < 256 ? L : 256;
+    constexpr bool kDelta = hook_delta<Hook>();
     const int b = threadIdx.x % B;
     const int t = threadIdx.x / B;
     const int tiles_c = (ncols + B - 1) / B;
     const int buf_elems = (L + L / E) * B;
     cplx<T>* bufs = reinterpret_cast<cplx<T>*>(smem_raw);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(bufs + 2 * buf_elems);
-    const unsigned tile_bytes = static_cast<unsigned>(L) * B * sizeof(cplx<T>);
+    double* sides = reinterpret_cast<double*>(bufs + 2 * buf_elems);
+    const int side_elems = has_side ? L * B : 0;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sides + 2 * side_elems);
+    const unsigned tile_bytes = static_cast<unsigned>(L) * B * sizeof(cplx<T>) +
+                                static_cast<unsigned>(side_elems) * sizeof(double);
     auto issue = [&](long long tile, int slot) {
         const long long plane = tile / tiles_c;
         const int c0 = static_cast<int>(tile - plane * tiles_c) * B;
         mbar_arrive_expect_tx(&bars[slot], tile_bytes);
 #pragma unroll
-        for (int j = 0; j < L / LB; ++j)
+        for (int j = 0; j < L / LB; ++j) {
             tma_load_3d(bufs + slot * buf_elems + j * LB * B, &map, &bars[slot], 2 * c0, j * LB,
                         static_cast<int>(plane));
+            if (has_side)
+                tma_load_3d(sides + slot * side_elems + j * LB * B, &side_map, &bars[slot], c0,
+                            j * LB, static_cast<int>(plane));
+        }
     };
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&map);
+        if (has_side) tma_prefetch_desc(&side_map);
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         fence_mbar_init();
@@ -328,37 +350,62 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 1)
     int slot = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, slot ^= 1) {
         cplx<T>* s = bufs + slot * buf_elems;
+        const double* sd = sides + slot * side_elems;
         mbar_wait(&bars[slot], (phase >> slot) & 1u);
         phase ^= 1u << slot;
         const long long plane = tile / tiles_c;
         const int c = static_cast<int>(tile - plane * tiles_c) * B + b;
         const bool valid = c < ncols;
         const long long base = plane * plane_stride + c;
+        auto delta = [&](int m, long long off) {
+            if constexpr (kDelta) {
+                if (has_side) {
+                    const double x = sd[(t + TT * m) * B + b];
+                    return make_double2(x, x);
+                }
+                return hook.fb.at2(off);
+            } else {
+                return make_double2(0.0, 0.0);
+            }
+        };
         cplx<T> v[E];
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             v[m] = s[(t + TT * m) * B + b];
-            if (valid) hook.pre(v[m], base + static_cast<long long>(t + TT * m) * row_stride, c);
+            if (valid) {
+                const long long off = base + static_cast<long long>(t + TT * m) * row_stride;
+                if constexpr (kDelta) hook.pre_d(v[m], off, c, delta(m, off));
+                else hook.pre(v[m], off, c);
+            }
         }
         stockham<T, L, E, 1, DIR>(v, t, tw, XchCol<T, E>{s + b, B});
-        fence_proxy_async_smem();  // this thread's exchange writes before the async-proxy refill
-        __syncthreads();           // every thread is done with buffer `slot`
-        if (threadIdx.x == 0 && tile + 2 * gridDim.x < ntiles) issue(tile + 2 * gridDim.x, slot);
+        if constexpr (!kDelta) {
+            fence_proxy_async_smem();  // this thread's exchange writes before the async refill
+            __syncthreads();           // every thread is done with buffer `slot`
+            if (threadIdx.x == 0 && tile + 2 * gridDim.x < ntiles) issue(tile + 2 * gridDim.x, slot);
+        }
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const long long off = base + static_cast<long long>(t + TT * m) * row_stride;
             if (valid) {
-                hook.post(v[m], off, c);
+                if constexpr (kDelta) hook.post_d(v[m], off, c, delta(m, off));
+                else hook.post(v[m], off, c);
                 if constexpr (hook_stores<Hook>()) dst[off] = v[m];
             }
+        }
+        if constexpr (kDelta) {  // the side tile is read in the store loop: refill after it
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (threadIdx.x == 0 && tile + 2 * gridDim.x < ntiles) issue(tile + 2 * gridDim.x, slot);
         }
     }
     hook.finish();
 }
 
 template <class T, int L, int E>
-constexpr size_t col_tma_smem_bytes(int B) {
-    return 2 * static_cast<size_t>(L + L / E) * B * sizeof(cplx<T>) + 2 * sizeof(uint64_t);
+constexpr size_t col_tma_smem_bytes(int B, bool side) {
+    return 2 * static_cast<size_t>(L + L / E) * B * sizeof(cplx<T>) +
+           (side ? 2 * static_cast<size_t>(L) * B * sizeof(double) : 0) + 2 * sizeof(uint64_t);
 }
 
 template <class T, int L, int E>

@@ -8,7 +8,7 @@ namespace ffcz_gpu {
 
 bool encode_col_map(CUtensorMap* map, const void* base, int scalar_bytes, long long ncols,
                     long long L, long long row_stride, long long nplanes, long long plane_stride,
-                    int B, int LB) {
+                    int B, int LB, bool complex) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q{};
@@ -19,14 +19,16 @@ bool encode_col_map(CUtensorMap* map, const void* base, int scalar_bytes, long l
         return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }();
     if (!encode) return false;
-    const long long cb = 2LL * scalar_bytes;  // bytes per complex element
-    if ((reinterpret_cast<uintptr_t>(base) & 15) || (row_stride * cb) % 16 || (plane_stride * cb) % 16)
+    const int per = complex ? 2 : 1;                     // scalars per element
+    const long long eb = static_cast<long long>(per) * scalar_bytes;  // bytes per element
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || (row_stride * eb) % 16 ||
+        (plane_stride * eb) % 16 || (B * eb) % 16)
         return false;
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(2 * ncols), static_cast<cuuint64_t>(L),
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(per * ncols), static_cast<cuuint64_t>(L),
                                 static_cast<cuuint64_t>(nplanes)};
-    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(row_stride * cb),
-                                   static_cast<cuuint64_t>(plane_stride * cb)};
-    const cuuint32_t box[3] = {static_cast<cuuint32_t>(2 * B), static_cast<cuuint32_t>(LB), 1};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(row_stride * eb),
+                                   static_cast<cuuint64_t>(plane_stride * eb)};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(per * B), static_cast<cuuint32_t>(LB), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode(map, scalar_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
                                                      : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
@@ -163,6 +165,8 @@ FFCZ_ROW_C2R_HOOK(HookRepairS<float>)
 FFCZ_ROW_C2R_HOOK(HookRepairS<double>)
 FFCZ_ROW_C2R_HOOK(HookVerifyS<float>)
 FFCZ_ROW_C2R_HOOK(HookVerifyS<double>)
+FFCZ_ROW_C2R_HOOK(HookRepairVerifyS<float>)
+FFCZ_ROW_C2R_HOOK(HookRepairVerifyS<double>)
 #undef FFCZ_ROW_C2R_HOOK
 template void launch_col<double, HookMarkViol>(long long, int, const double2*, double2*, long long,
                                                long long, long long, int, Twiddles<double>&,

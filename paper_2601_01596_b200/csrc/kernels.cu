@@ -148,6 +148,16 @@ __global__ void k_decide(Ctl* ctl) {
     ctl->exc_bits = 0;
 }
 
+// Loop-control readback through mapped pinned memory: a one-warp kernel stores the control block
+// straight into the host mirror, so a poll never queues behind a large D2H on the copy engines.
+__global__ void k_export_ctl(const Ctl* __restrict__ ctl, Ctl* host) {
+    static_assert(sizeof(Ctl) % 8 == 0, "Ctl layout");
+    const volatile unsigned long long* s = reinterpret_cast<const volatile unsigned long long*>(ctl);
+    volatile unsigned long long* d = reinterpret_cast<volatile unsigned long long*>(host);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(Ctl) / 8); i += blockDim.x) d[i] = s[i];
+    __threadfence_system();
+}
+
 __global__ void k_ctl_init(Ctl* ctl, unsigned long long max_iters) {
     Ctl c{};
     c.max_iters = max_iters;
@@ -381,6 +391,83 @@ __global__ void k_codes_freq(const unsigned long long* __restrict__ idx, long lo
     }
 }
 
+// Codes straight from the keep bitmap (no index list): CTA b owns words [1024 b, 1024 b + 1024)
+// = the block of k_popc_blocks, whose exclusive offsets k_scan_blocks left in block_offsets.  A
+// CTA-wide scan of the per-word popcounts gives every word's output position; warp j then walks
+// words 32 j .. 32 j + 31 with lane l on element 32 w + l, so the F / S / bound loads are
+// coalesced and codes land in ascending index order (editset.cpp:86-119).
+namespace {
+template <class Emit>
+__device__ __forceinline__ void codes_from_bits(const unsigned* __restrict__ words, long long nwords,
+                                                const unsigned long long* __restrict__ block_offsets,
+                                                Emit&& emit) {
+    __shared__ unsigned s[1024];
+    __shared__ unsigned sw[1024];
+    const long long wbase = blockIdx.x * 1024LL;
+    const long long wi = wbase + threadIdx.x;
+    const unsigned w = wi < nwords ? words[wi] : 0u;
+    const unsigned c = __popc(w);
+    sw[threadIdx.x] = w;
+    // block-wide inclusive scan of popcounts: warp scans + scan of warp totals
+    unsigned v = c;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned a = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += a;
+    }
+    __shared__ unsigned wsum[32];
+    if (lane == 31) wsum[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned t = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned a = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += a;
+        }
+        wsum[lane] = t;
+    }
+    __syncthreads();
+    s[threadIdx.x] = v - c + (warp ? wsum[warp - 1] : 0u);  // exclusive prefix of this word
+    __syncthreads();
+    const unsigned long long boff = block_offsets[blockIdx.x];
+    const unsigned lt = (1u << lane) - 1u;
+    for (int k = 0; k < 32; ++k) {
+        const int wl = warp * 32 + k;
+        const long long wg = wbase + wl;
+        if (wg >= nwords) break;
+        const unsigned word = sw[wl];
+        if (!word) continue;
+        if (word >> lane & 1u) emit(wg * 32 + lane, boff + s[wl] + __popc(word & lt));
+    }
+}
+} // namespace
+
+__global__ void k_codes_spatial_bits(const unsigned* __restrict__ keep_words, long long nwords,
+                                     const unsigned long long* __restrict__ block_offsets,
+                                     const double* __restrict__ S, SpatialB sb, int m, int* codes) {
+    codes_from_bits(keep_words, nwords, block_offsets, [&](long long n, unsigned long long pos) {
+        const double step = ldexp(2.0 * sb.at(n), -m);
+        codes[pos] = static_cast<int>(llround(S[n] / step));
+    });
+}
+
+__global__ void k_codes_freq_bits(const unsigned* __restrict__ keep_words, long long nwords,
+                                  const unsigned long long* __restrict__ block_offsets,
+                                  const double2* __restrict__ F, HalfGeom g, FreqB fb, int m,
+                                  int* codes) {
+    codes_from_bits(keep_words, nwords, block_offsets, [&](long long h, unsigned long long pos) {
+        const long long off = g.offset_of(h);
+        const double2 v = F[off];
+        const double2 d = fb.at2(off);
+        const double sre = ldexp(2.0 * d.x, -m);
+        const double sim = ldexp(2.0 * d.y, -m);
+        reinterpret_cast<int2*>(codes)[pos] = make_int2(static_cast<int>(llround(v.x / sre)),
+                                                        static_cast<int>(llround(v.y / sim)));
+    });
+}
+
 template <class TI>
 __global__ void k_repair_spatial(const TI* __restrict__ orig, const TI* __restrict__ dec,
                                  const double* __restrict__ fpart, const double* __restrict__ final_eps,
@@ -473,7 +560,7 @@ __global__ void k_verify_spatial(const TI* __restrict__ orig, const TI* __restri
     for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
          n += (long long)gridDim.x * blockDim.x) {
         const double c = static_cast<double>(dec[n]) + spat_cur[n] + fpart[n];  // archive.cpp:271
-        corrected[n] = c;
+        if (corrected) corrected[n] = c;
         const double e = c - static_cast<double>(orig[n]);                      // archive.cpp:284
         eps_v[n] = e;
         const double ex = fabs(e) - sb.at(n);

@@ -112,15 +112,18 @@ struct HookFReduce {
     double fscale;  // working = original * (1 - 2^-m) (bounds.cpp:74-85); 1.0 for working input
     Ctl* ctl;
     double peak = 0.0, ex = 0.0;
+    static constexpr bool kDelta = true;  // post_d takes Delta(off) from the caller (TMA side tile)
+    template <class C> __device__ __forceinline__ void pre_d(C&, long long, int, double2) {}
     template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
     template <class C>
-    __device__ __forceinline__ void post(C& v, long long off, int) {
+    __device__ __forceinline__ void post_d(C& v, long long, int, double2 d) {
         const double ar = fabs(static_cast<double>(v.x)), ai = fabs(static_cast<double>(v.y));
         peak = fmax(peak, fmax(ar, ai));
-        const double2 d = fb.at2(off);
         const double e = fmax(ar - d.x * fscale, ai - d.y * fscale);
         if (e > ex) ex = e;
     }
+    template <class C>
+    __device__ __forceinline__ void post(C& v, long long off, int c) { post_d(v, off, c, fb.at2(off)); }
     __device__ __forceinline__ void finish() { block_max2_atomic(peak, ex, &ctl->peak_bits, &ctl->exc_bits); }
 };
 
@@ -139,10 +142,13 @@ struct HookFClip {
     __device__ __forceinline__ void begin() {
         first = ctl != nullptr && *reinterpret_cast<const volatile unsigned long long*>(&ctl->passes) == 1;
     }
+    static constexpr bool kDelta = true;
+    template <class C> __device__ __forceinline__ void post_d(C&, long long, int, double2) {}
     template <class C>
-    __device__ __forceinline__ void pre(C& v, long long off, int) {
+    __device__ __forceinline__ void pre(C& v, long long off, int c) { pre_d(v, off, c, fb.at2(off)); }
+    template <class C>
+    __device__ __forceinline__ void pre_d(C& v, long long off, int, double2 d) {
         const double re = v.x, im = v.y;
-        const double2 d = fb.at2(off);
         const double dre = d.x * fscale, dim = d.y * fscale;
         const double cre = clamp_abs(re, dre), cim = clamp_abs(im, dim);
         const double xre = cre - re, xim = cim - im;
@@ -268,7 +274,7 @@ struct HookVerifyS {
         const double2 o = load_pair(orig, n), d = load_pair(dec, n);
         const double2 sc = *reinterpret_cast<const double2*>(spat_cur + n);
         const double c0 = d.x + sc.x + x0, c1 = d.y + sc.y + x1;
-        *reinterpret_cast<double2*>(corrected + n) = make_double2(c0, c1);
+        if (corrected) *reinterpret_cast<double2*>(corrected + n) = make_double2(c0, c1);
         x0 = c0 - o.x;
         x1 = c1 - o.y;
         const double ex0 = fabs(x0) - sb.at(n), ex1 = fabs(x1) - sb.at(n + 1);
@@ -276,6 +282,63 @@ struct HookVerifyS {
         if (ex1 > 0.0 && ex1 > m) m = ex1;
     }
     __device__ __forceinline__ void finish() { block_max2_atomic(m, 0.0, &ctl->vs_bits, nullptr); }
+};
+
+// One escape-repair round fused with a speculative apply_edits + verify_bounds (archive.cpp:262-287)
+// on the same inverse transform: when the round turns out clean (no component repaired, so
+// spat_cur and freq_cur are final), the decoder view dec + spat_cur + Re(IFFT(freq_cur)) is the
+// one this pass already has, and the separate verify inverse (3 passes) is skipped.  Writes
+// eps_tilde (handed on, as HookRepairS), plus `corrected` and eps_v = corrected - orig.  The two
+// epsilons are formed exactly as the reference forms them (eps0 + s + f vs (dec + s + f) - orig).
+template <class TI>
+struct HookRepairVerifyS {
+    const TI* orig;
+    const TI* dec;
+    double* spat_cur;
+    const double* final_eps;
+    SpatialB sb;
+    unsigned* esc_words;
+    double* corrected;
+    double* eps_v;
+    Ctl* ctl;
+    int dirty = 0;
+    double m = 0.0;
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    __device__ __forceinline__ void post_real(double& x0, double& x1, long long n) {
+        const double2 o = load_pair(orig, n), d = load_pair(dec, n);
+        double2 sc = *reinterpret_cast<const double2*>(spat_cur + n);
+        const double e0 = d.x - o.x, e1 = d.y - o.y;
+        const double c0 = d.x + sc.x + x0, c1 = d.y + sc.y + x1;
+        const double v0 = c0 - o.x, v1 = c1 - o.y;
+        if (corrected) *reinterpret_cast<double2*>(corrected + n) = make_double2(c0, c1);
+        *reinterpret_cast<double2*>(eps_v + n) = make_double2(v0, v1);
+        const double E0 = sb.at(n), E1 = sb.at(n + 1);
+        const double ex0 = fabs(v0) - E0, ex1 = fabs(v1) - E1;
+        if (ex0 > 0.0 && ex0 > m) m = ex0;
+        if (ex1 > 0.0 && ex1 > m) m = ex1;
+        const double t0 = e0 + sc.x + x0, t1 = e1 + sc.y + x1;
+        bool w = false;
+        if (fabs(t0) > E0) {
+            sc.x = sc.x + (final_eps[n] - t0);
+            set_bit_g(esc_words, n);
+            w = true;
+        }
+        if (fabs(t1) > E1) {
+            sc.y = sc.y + (final_eps[n + 1] - t1);
+            set_bit_g(esc_words, n + 1);
+            w = true;
+        }
+        if (w) {
+            *reinterpret_cast<double2*>(spat_cur + n) = sc;
+            dirty = 1;
+        }
+        x0 = t0;
+        x1 = t1;
+    }
+    __device__ __forceinline__ void finish() {
+        if (__syncthreads_or(dirty) && threadIdx.x == 0) ctl->dirty = 1;
+        block_max2_atomic(m, 0.0, &ctl->vs_bits, nullptr);
+    }
 };
 
 // Frequency check of an escape-repair round (pipeline.cpp:140-147): marks violating components
@@ -288,9 +351,12 @@ struct HookMarkViol {
     Ctl* ctl;
     int any = 0;
     template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    static constexpr bool kDelta = true;
+    template <class C> __device__ __forceinline__ void pre_d(C&, long long, int, double2) {}
     template <class C>
-    __device__ __forceinline__ void post(C& v, long long off, int) {
-        const double2 d = fb.at2(off);
+    __device__ __forceinline__ void post(C& v, long long off, int c) { post_d(v, off, c, fb.at2(off)); }
+    template <class C>
+    __device__ __forceinline__ void post_d(C& v, long long off, int, double2 d) {
         if (fabs(v.x) > d.x || fabs(v.y) > d.y) {
             set_bit_g(viol_words, off);
             any = 1;
@@ -308,9 +374,12 @@ struct HookVerifyF {
     Ctl* ctl;
     double m = 0.0;
     template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    static constexpr bool kDelta = true;
+    template <class C> __device__ __forceinline__ void pre_d(C&, long long, int, double2) {}
     template <class C>
-    __device__ __forceinline__ void post(C& v, long long off, int) {
-        const double2 d = fb.at2(off);
+    __device__ __forceinline__ void post(C& v, long long off, int c) { post_d(v, off, c, fb.at2(off)); }
+    template <class C>
+    __device__ __forceinline__ void post_d(C& v, long long, int, double2 d) {
         const double ex = fmax(fabs(v.x) - d.x, fabs(v.y) - d.y);
         if (ex > 0.0 && ex > m) m = ex;
     }
@@ -352,6 +421,7 @@ __global__ void k_cast_to_double(const float* __restrict__ in, double* out, long
 // loop decision (projection.cpp:106-116,125)
 __global__ void k_decide(Ctl* ctl);
 __global__ void k_ctl_init(Ctl* ctl, unsigned long long max_iters);
+__global__ void k_export_ctl(const Ctl* __restrict__ ctl, Ctl* host);
 // report: residual_s (projection.cpp:129-133)
 __global__ void k_residual_s(const double* __restrict__ eps, long long N, SpatialB sb,
                              double fscale, Ctl* ctl);
@@ -388,6 +458,15 @@ __global__ void k_codes_spatial(const unsigned long long* __restrict__ idx, long
 __global__ void k_codes_freq(const unsigned long long* __restrict__ idx, long long n,
                              const double2* __restrict__ F, HalfGeom g, FreqB fb, int m,
                              int* codes);
+// the same codes straight from the keep bitmap + k_popc_blocks/k_scan_blocks offsets (1024
+// words per CTA, 1024 threads): no index list round trip
+__global__ void k_codes_spatial_bits(const unsigned* __restrict__ keep_words, long long nwords,
+                                     const unsigned long long* __restrict__ block_offsets,
+                                     const double* __restrict__ S, SpatialB sb, int m, int* codes);
+__global__ void k_codes_freq_bits(const unsigned* __restrict__ keep_words, long long nwords,
+                                  const unsigned long long* __restrict__ block_offsets,
+                                  const double2* __restrict__ F, HalfGeom g, FreqB fb, int m,
+                                  int* codes);
 // escape repair (pipeline.cpp:114-163)
 template <class TI>
 __global__ void k_repair_spatial(const TI* __restrict__ orig, const TI* __restrict__ dec,
