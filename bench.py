@@ -82,6 +82,226 @@ def make_workload(n, seed, device):
     return orig.contiguous(), dec.contiguous(), E, delta.contiguous()
 
 
+def grf_torch(shape, alpha, g, device):
+    """Gaussian random field with power spectrum |k|^-alpha, unit std (float64)."""
+    import torch
+    w = torch.randn(shape, generator=g, device=device, dtype=torch.float64)
+    W = torch.fft.rfftn(w)
+    del w
+    kk = None
+    for ax, n in enumerate(shape):
+        k = (torch.fft.rfftfreq(n, device=device, dtype=torch.float64) if ax == len(shape) - 1
+             else torch.fft.fftfreq(n, device=device, dtype=torch.float64)) * n
+        view = [1] * len(shape)
+        view[ax] = -1
+        k2 = (k * k).view(view)
+        kk = k2 if kk is None else kk + k2
+    kk = kk.expand(W.shape).clone()
+    kk[(0,) * len(shape)] = 1.0
+    W *= kk.pow_(-alpha / 4.0)  # amplitude ~ |k|^(-alpha/2)
+    del kk
+    W[(0,) * len(shape)] = 0
+    f = torch.fft.irfftn(W, s=shape)
+    del W
+    return f / f.std()
+
+
+def combustion_field_torch(n, seed, device):
+    """Config 4: c = 0.05(1+tanh((z - n/2 - 40 h(x,y))/8)) + 0.002 g, h a 2-D GRF
+    (alpha=3), g a 3-D GRF (alpha=11/3); axis 0 is z.  FP32."""
+    import torch
+    gen = torch.Generator(device=device).manual_seed(seed)
+    h = grf_torch((n, n), 3.0, gen, device)
+    g = grf_torch((n, n, n), 11.0 / 3.0, gen, device)
+    z = torch.arange(n, device=device, dtype=torch.float64).view(n, 1, 1)
+    s = n / 1024.0
+    g.mul_(0.002).add_(0.05 * (1.0 + torch.tanh((z - n / 2 - 40.0 * s * h[None]) / (8.0 * s))))
+    return g.to(torch.float32)
+
+
+def mean_abs_spectrum_torch(e64):
+    """mean_k |FFT(e)_k| over the FULL spectrum, from the half spectrum (Hermitian weights)."""
+    import torch
+    X = torch.fft.rfftn(e64).abs()
+    n2 = e64.shape[-1]
+    tot = 2.0 * X.sum().item() - X[..., 0].sum().item()
+    if n2 % 2 == 0:
+        tot -= X[..., -1].sum().item()
+    return tot / e64.numel()
+
+
+def make_workload_combustion(n, seed, device, c=0.6):
+    import torch
+    orig = combustion_field_torch(n, seed, device)
+    E = 0.1 / 100.0 * (orig.max() - orig.min()).item()
+    g = torch.Generator(device=device).manual_seed(seed + 7)
+    u = (torch.rand(orig.shape, generator=g, device=device, dtype=torch.float64) * 2 - 1) * (0.99 * E)
+    dec = (orig.to(torch.float64) + u).to(torch.float32)
+    del u
+    delta = c * mean_abs_spectrum_torch(dec.to(torch.float64) - orig.to(torch.float64))
+    return orig.contiguous(), dec.contiguous(), E, float(delta)
+
+
+def xrd_frames_torch(count, n, seed, device, spots=400):
+    """Config 3: per frame 2*U[0,1) background plus `spots` Gaussian spots
+    (sigma^2 = 2 px^2, amplitude 50 + 1000 U, uniform positions).  FP32, (count, n, n)."""
+    import torch
+    g = torch.Generator(device=device).manual_seed(seed)
+    img = 2.0 * torch.rand((count, n, n), generator=g, device=device, dtype=torch.float64)
+    amp = 50.0 + 1000.0 * torch.rand((count, spots), generator=g, device=device, dtype=torch.float64)
+    cy = torch.rand((count, spots), generator=g, device=device, dtype=torch.float64) * n
+    cx = torch.rand((count, spots), generator=g, device=device, dtype=torch.float64) * n
+    w = torch.arange(-7, 8, device=device)
+    iy = (cy.floor().long()[..., None] + w).clamp_(0, n - 1)          # (count, spots, 15)
+    ix = (cx.floor().long()[..., None] + w).clamp_(0, n - 1)
+    vy = torch.exp(-(iy.double() - cy[..., None]) ** 2 / 4.0)
+    vx = torch.exp(-(ix.double() - cx[..., None]) ** 2 / 4.0)
+    val = amp[..., None, None] * vy[..., :, None] * vx[..., None, :]   # (count, spots, 15, 15)
+    fidx = torch.arange(count, device=device).view(count, 1, 1, 1).expand_as(val)
+    flat = (fidx * n + iy[..., :, None]) * n + ix[..., None, :]
+    img.view(-1).index_add_(0, flat.reshape(-1), val.reshape(-1))
+    return img.to(torch.float32)
+
+
+def make_workload_frames(count, n, seed, device, c=0.8):
+    """Config 3 workload: frames, per-frame E (0.1% of the frame range) and global Delta
+    (c * mean|delta0| of the frame)."""
+    import torch
+    orig = xrd_frames_torch(count, n, seed, device)
+    flat = orig.view(count, -1)
+    E = (0.1 / 100.0 * (flat.max(dim=1).values - flat.min(dim=1).values)).double()
+    g = torch.Generator(device=device).manual_seed(seed + 7)
+    u = (torch.rand(orig.shape, generator=g, device=device, dtype=torch.float64) * 2 - 1)
+    u *= (0.99 * E).view(count, 1, 1)
+    dec = (orig.double() + u).to(torch.float32)
+    del u
+    deltas = []
+    for f0 in range(0, count, 64):
+        e = dec[f0:f0 + 64].double() - orig[f0:f0 + 64].double()
+        X = torch.fft.rfft2(e).abs()
+        tot = 2.0 * X.sum(dim=(1, 2)) - X[..., 0].sum(dim=1) - X[..., -1].sum(dim=1)
+        deltas.append(c * tot / (n * n))
+    delta = torch.cat(deltas)
+    return orig.contiguous(), dec.contiguous(), E.tolist(), delta.tolist()
+
+
+def run_frames(args, rank, world, local):
+    """Config 3: a fixed batch of frames sharded across ranks (strong scaling, no collective on
+    the data path); one step = correct_batch over this rank's frames."""
+    import torch
+    import torch.distributed as dist
+    import paper_2601_01596_b200 as P
+    from paper_2601_01596_b200 import _capi
+    import ctypes as C
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    ctx = P.Context(local, stream.cuda_stream)
+    lib = _capi.load()
+    n, total = args.frame_n, args.frames
+    mine = [f for f in range(total) if f % world == rank]
+    cnt = len(mine)
+    orig, dec, Es, Ds = make_workload_frames(cnt, n, 5 + 7919 * rank, dev)
+    torch.cuda.empty_cache()
+    bounds = [P.DualBounds(E, D) for E, D in zip(Es, Ds)]
+
+    def step(o=orig, d=dec, edits=False):
+        return P.correct_batch(o, d, bounds, 16, 1000, "f32", lanes=args.lanes,
+                               want_archive=False, want_edits=edits, want_corrected=False,
+                               copy=False, ctx=ctx)
+
+    for _ in range(args.warmup):
+        rs = step()
+    assert all(r.report.converged and r.verify_ok for r in rs)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    lib.ffcz_cuda_profile_enable(ctx.handle, 1)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rs = step()
+        ev1.record(stream)
+        barrier()
+    lib.ffcz_cuda_profile_enable(ctx.handle, 0)
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    ms_step = ms / args.steps
+    value = 4.0 * total * n * n / (ms_step * 1e-3) / 1e9
+    stats = (_capi.KernelStat * 16)()
+    nst = C.c_int()
+    lib.ffcz_cuda_profile_read(ctx.handle, stats, 16, C.byref(nst))
+    ks = [stats[i] for i in range(nst.value)]
+    iters = [r.report.iterations for r in rs]
+    launches = int(sum(r.kernel_launches for r in rs)) * args.steps
+
+    e2e = None
+    if not args.no_e2e:
+        h_o = torch.empty_like(orig, device="cpu", pin_memory=True)
+        h_d = torch.empty_like(dec, device="cpu", pin_memory=True)
+        h_o.copy_(orig)
+        h_d.copy_(dec)
+        o_np, d_np = h_o.numpy(), h_d.numpy()
+        rs = None
+        rs = step(o_np, d_np, True)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(max(1, min(args.steps, 2))):
+            rs = None
+            rs = step(o_np, d_np, True)
+        barrier()
+        te = (time.perf_counter() - t0) / max(1, min(args.steps, 2))
+        if world > 1:
+            t = torch.tensor([te], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = t.item()
+        d2h = sum(r.spatial_flags.nbytes + r.frequency_flags.nbytes + r.spatial_codes.nbytes +
+                  r.frequency_codes.nbytes + r.escapes.nbytes for r in rs)
+        e2e = {"value": 4.0 * total * n * n / te / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": 8 * cnt * n * n, "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": te * 1e3,
+               "includes": "H2D of this rank's original+decompressed frames (f32, pinned), "
+                           "device correct() of every frame, D2H of every frame's edit set"}
+    if rank == 0:
+        peak, peak_kind = measured_peak()
+        dom = max(ks, key=lambda s: s.total_ms)
+        achieved = dom.bytes / (dom.total_ms * 1e-3) / 1e9 if dom.total_ms > 0 else 0.0
+        print(json.dumps({
+            "metric": "corrected GB/s (input bytes / time to feasibility)", "value": value,
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config3: {total} frames of {n}x{n} FP32 XRD-like (background + "
+                                   "400 Gaussian spots), per-frame E=0.1% range, Delta=0.8*mean"
+                                   "|delta0|; frames sharded across ranks",
+                       "frames": total, "frame": [n, n], "lanes": args.lanes, "m": 16,
+                       "policy": "fp64 (reference control flow)",
+                       "l2": f"inputs larger than L2 ({4 * cnt * n * n / 1e9:.1f} GB per rank)",
+                       "parallelism": f"frames/{world} per rank"},
+            "iterations": {"min": int(min(iters)), "max": int(max(iters)),
+                           "mean": float(np.mean(iters))},
+            "roofline": {"bound": "hbm", "kernel": dom.name.decode(), "achieved": achieved,
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "launches": int(dom.launches),
+                         "avg_launch_ms": dom.total_ms / max(1, dom.launches),
+                         "bytes_per_launch": dom.bytes / max(1, dom.launches)},
+            "kernels": {s.name.decode(): {"launches": int(s.launches), "gated": int(s.gated),
+                                          "ms": s.total_ms,
+                                          "GBps": (s.bytes / (s.total_ms * 1e-3) / 1e9)
+                                          if s.total_ms else 0.0} for s in ks},
+            "e2e": e2e, "cpu_baseline": None, "gpu_launches": launches,
+            "clocks": clk.summary()}))
+    ctx.close()
+
+
 def make_workload_numpy(n, seed):
     """Same recipe on the host (CPU baseline sample)."""
     rng = np.random.default_rng(seed)
@@ -236,6 +456,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--config", default="nyx", choices=["nyx", "combustion", "frames"],
+                    help="nyx = BASELINE configs[1] (default); combustion = configs[3] recipe; "
+                         "frames = configs[2] (batched 2-D frames, sharded)")
+    ap.add_argument("--frames", type=int, default=1024)
+    ap.add_argument("--frame-n", type=int, default=2048)
+    ap.add_argument("--lanes", type=int, default=8)
     ap.add_argument("--ref-n", type=int, default=64)
     ap.add_argument("--cpu-n", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -255,6 +481,11 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.config == "frames":
+        run_frames(args, rank, world, local)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     import paper_2601_01596_b200 as P
     from paper_2601_01596_b200 import _capi
     import ctypes as C
@@ -265,7 +496,16 @@ def main():
     lib = _capi.load()
 
     n = args.n
-    orig, dec, E, delta = make_workload(n, 1234 + rank, dev)
+    if args.config == "nyx":
+        orig, dec, E, delta = make_workload(n, 1234 + rank, dev)
+        workload = (f"config2: {n}^3 FP32 Nyx-like log-normal field, +-0.99E uniform base error, "
+                    "E=0.1% range, rho=1e-3 per-component Delta; one independent volume per GPU")
+    else:
+        orig, dec, E, delta = make_workload_combustion(n, 4321 + rank, dev)
+        workload = (f"config4 recipe: {n}^3 FP32 combustion-like front, +-0.99E uniform base "
+                    "error, E=0.1% range, global Delta=0.6*mean|delta0|; one independent volume "
+                    "per GPU")
+    torch.cuda.empty_cache()  # the engine allocates its own device state with cudaMalloc
     bounds = P.DualBounds(E, delta)
     N = n ** 3
 
@@ -319,11 +559,16 @@ def main():
     if not args.no_e2e:
         h_orig = torch.empty((n, n, n), dtype=torch.float32, pin_memory=True)
         h_dec = torch.empty_like(h_orig, pin_memory=True)
-        h_delta = torch.empty((n, n, n), dtype=torch.float64, pin_memory=True)
         h_orig.copy_(orig)
         h_dec.copy_(dec)
-        h_delta.copy_(delta)
-        hb = P.DualBounds(E, h_delta.numpy())
+        if isinstance(delta, float):
+            hb = P.DualBounds(E, delta)
+            h2d_delta = 0
+        else:
+            h_delta = torch.empty((n, n, n), dtype=torch.float64, pin_memory=True)
+            h_delta.copy_(delta)
+            hb = P.DualBounds(E, h_delta.numpy())
+            h2d_delta = 8 * (N // n) * (n // 2 + 1)
         o_np, d_np = h_orig.numpy(), h_dec.numpy()
         r = None
         for _ in range(2):  # warm the pinned result pool (two generations of result buffers)
@@ -347,7 +592,7 @@ def main():
                r.frequency_codes.nbytes + r.escapes.nbytes)
         e2e = {"value": world * 4.0 * N / te / 1e9, "unit": "GB/s",
                "lib_timings_ms": r.timings_ms,
-               "h2d_bytes_per_step": 4 * N * 2 + 8 * (N // n) * (n // 2 + 1),
+               "h2d_bytes_per_step": 4 * N * 2 + h2d_delta,
                "d2h_bytes_per_step": int(d2h),
                "ms_per_step": te * 1e3, "steps": ksteps,
                "includes": "H2D of original+decompressed (f32) and the half-grid columns of the "
@@ -377,11 +622,9 @@ def main():
             "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config2: {n}^3 FP32 Nyx-like log-normal field, +-0.99E uniform "
-                                   "base error, E=0.1% range, rho=1e-3 per-component Delta; "
-                                   "one independent volume per GPU",
+            "config": {"workload": workload,
                        "n": n, "m": 16, "policy": "fp64 (reference control flow)",
-                       "l2": "inputs larger than L2 (0.54 GB per field, 126 MB L2)",
+                       "l2": f"inputs larger than L2 ({4 * N / 1e9:.2f} GB per field, 126 MB L2)",
                        "parallelism": f"independent volumes x{world}"},
             "ms_per_iteration": float(np.mean(loop_ms) / max(1.0, np.mean(iters))),
             "lib_timings_ms": {k: float(np.mean([r.timings_ms[k] for r in results]))

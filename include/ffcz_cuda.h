@@ -156,6 +156,17 @@ int ffcz_cuda_correct(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const vo
                       uint64_t max_iters, const ffcz_cuda_options* opt, ffcz_cuda_result* out);
 void ffcz_cuda_result_free(ffcz_cuda_result* r);
 
+/* Batched frames (BASELINE config 3: many independent 2-D frames): nframes independent
+ * ffcz::correct() calls (pipeline.cpp:26-178) on frames of shape `frame` stored back to back in
+ * `original` / `decompressed` (host or device per opt->flags); bounds[i] / out[i] are frame i's
+ * DualBounds and CorrectionResult (free each with ffcz_cuda_result_free).  `lanes` host threads
+ * (<= 0: 8) each drive a sub-context with its own stream; the context stream is ordered before
+ * and after the batch.  Results are identical to one ffcz_cuda_correct() per frame. */
+int ffcz_cuda_correct_batch(ffcz_cuda_ctx* ctx, const ffcz_field_desc* frame, uint64_t nframes,
+                            const void* original, const void* decompressed,
+                            const ffcz_bounds_desc* bounds, int m, uint64_t max_iters,
+                            const ffcz_cuda_options* opt, int lanes, ffcz_cuda_result* out);
+
 /* Replaces ffcz::alternating_projection (projection.cpp:81-142).  eps0 is a field of
  * field->dtype; bounds are the WORKING bounds.  Outputs (host, caller-allocated, may be NULL):
  * spatial_edits N doubles, frequency_edits 2N doubles (FULL spectrum, interleaved),

@@ -34,7 +34,8 @@ FFCZ_FORCE_UNFUSED = 1 << 4
 # every symbol include/ffcz_cuda.h declares
 EXPORTS = [
     "ffcz_cuda_create", "ffcz_cuda_destroy", "ffcz_cuda_last_error", "ffcz_cuda_abi_version",
-    "ffcz_cuda_default_options", "ffcz_cuda_correct", "ffcz_cuda_result_free",
+    "ffcz_cuda_default_options", "ffcz_cuda_correct", "ffcz_cuda_correct_batch",
+    "ffcz_cuda_result_free",
     "ffcz_cuda_alternating_projection", "ffcz_cuda_forward_dft", "ffcz_cuda_inverse_dft",
     "ffcz_cuda_r2c_device", "ffcz_cuda_c2r_device", "ffcz_cuda_crc32c",
     "ffcz_cuda_profile_enable", "ffcz_cuda_profile_read", "ffcz_cuda_bench_passes",
@@ -112,6 +113,9 @@ def load():
     lib.ffcz_cuda_default_options.restype = None
     lib.ffcz_cuda_correct.argtypes = [P, C.POINTER(FieldDesc), P, P, C.POINTER(BoundsDesc),
                                       C.c_int, C.c_uint64, C.POINTER(Options), C.POINTER(Result)]
+    lib.ffcz_cuda_correct_batch.argtypes = [P, C.POINTER(FieldDesc), C.c_uint64, P, P,
+                                            C.POINTER(BoundsDesc), C.c_int, C.c_uint64,
+                                            C.POINTER(Options), C.c_int, C.POINTER(Result)]
     lib.ffcz_cuda_result_free.argtypes = [C.POINTER(Result)]
     lib.ffcz_cuda_result_free.restype = None
     lib.ffcz_cuda_alternating_projection.argtypes = [

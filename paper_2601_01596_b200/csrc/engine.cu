@@ -13,8 +13,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <atomic>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -86,6 +88,7 @@ struct ffcz_cuda_ctx {
     Twiddles<double> tw64;
     Twiddles<float> tw32;
     std::map<std::string, std::pair<void*, size_t>> bufs;
+    std::vector<ffcz_cuda_ctx*> lanes;  // ffcz_cuda_correct_batch: sub-contexts, one stream each
     Ctl* ctl = nullptr;
     Ctl* hctl = nullptr;   // pinned mirror (one slot per in-flight chunk)
     Ctl* hctl_dev = nullptr;  // device alias of the mapped mirror (k_export_ctl writes it)
@@ -197,6 +200,19 @@ inline unsigned grid_for(long long n, int threads = 256) {
 
 constexpr int kPitchAlign = 16;
 
+// The column axis whose pass completes the forward transform (and starts the inverse), i.e. the
+// pass that carries the f-cube check / clip / mark / verify hooks.  For 3-D fields this is the
+// MIDDLE axis (row stride P: a tile's rows sit inside one plane, so the hooks' F / Delta accesses
+// stay TLB- and DRAM-page-local), with the outer axis transformed first.  FFCZ_COMPLETE_AXIS=0
+// restores the outer axis (A/B runs).  2-D fields have only axis 1.
+inline int complete_axis(bool three_d) {
+    static const int v = [] {
+        const char* e = std::getenv("FFCZ_COMPLETE_AXIS");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return three_d ? v : 1;
+}
+
 struct Bounds {
     SpatialB sb{nullptr, 0.0};
     FreqB fb{nullptr, nullptr, 0.0};
@@ -279,7 +295,8 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
         FFCZ_CUDA_CHECK(cudaMemsetAsync(F, 0, g.half_elems() * sizeof(double2), st));
     }
     const bool three_d = g.d[0] > 1;
-    const int za = three_d ? 0 : 1;  // the pass that completes the forward transform
+    const int za = complete_axis(three_d);  // the pass that completes the forward transform
+    const int mid = 1 - za;                   // the other column axis (3-D only)
     double* tmp = fused ? nullptr : c.b<double>("real_tmp", g.N);
 
     const double pass_bytes = 32.0 * g.Nc();
@@ -299,7 +316,7 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
             }
             if (three_d) {
                 Prof p(c, kColPass, pass_bytes);
-                plan.col(1, +1, spec, spec, gate, HookNone{}, st);
+                plan.col(mid, +1, spec, spec, gate, HookNone{}, st);
             }
             {   // K1 as C2R(+s-clip, eps written) then R2C: two 90%-of-HBM passes beat one
                 // register-bound fused pass (profiles/r01_passbench.md)
@@ -314,7 +331,7 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
             }
             if (three_d) {
                 Prof p(c, kColPass, pass_bytes);
-                plan.col(1, -1, spec, spec, gate, HookNone{}, st);
+                plan.col(mid, -1, spec, spec, gate, HookNone{}, st);
             }
             c.launches += three_d ? 7 : 5;
         } else {
@@ -336,7 +353,7 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
         }
         if (three_d) {
             Prof p(c, kColPass, pass_bytes);
-            plan.col(1, -1, spec, spec, gate, HookNone{}, st);
+            plan.col(mid, -1, spec, spec, gate, HookNone{}, st);
         }
         c.launches += three_d ? 2 : 1;
     }
@@ -514,7 +531,8 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
     if (fused) {
         // fused rounds: [Z inv] [Y inv] [C2R -> repair_s -> R2C] [Y fwd] [Z fwd + mark] + sparse
         const bool three_d = g.d[0] > 1;
-        const int za = three_d ? 0 : 1;
+        const int za = complete_axis(three_d);
+        const int mid = 1 - za;
         const long long vw = (g.half_elems() + 31) / 32;
         unsigned* viol = c.b<unsigned>("viol", vw);
         const double pass = 32.0 * Nc;
@@ -525,7 +543,7 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
             }
             if (three_d) {
                 Prof p(c, kColPass, pass);
-                plan.col(1, +1, work, work, nullptr, HookNone{}, st);
+                plan.col(mid, +1, work, work, nullptr, HookNone{}, st);
             }
             {
                 Prof p(c, kRowC2R, row_bytes);
@@ -538,7 +556,7 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
             }
             if (three_d) {
                 Prof p(c, kColPass, pass);
-                plan.col(1, -1, work, work, nullptr, HookNone{}, st);
+                plan.col(mid, -1, work, work, nullptr, HookNone{}, st);
             }
             c.launches += three_d ? 5 : 3;
         };
@@ -550,7 +568,7 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
             }
             if (three_d) {
                 Prof p(c, kColPass, pass);
-                plan.col(1, -1, work, work, nullptr, HookNone{}, st);
+                plan.col(mid, -1, work, work, nullptr, HookNone{}, st);
             }
             c.launches += three_d ? 2 : 1;
         };
@@ -949,6 +967,8 @@ int ffcz_cuda_create(ffcz_cuda_ctx** out, int device, void* stream) {
 
 void ffcz_cuda_destroy(ffcz_cuda_ctx* c) {
     if (!c) return;
+    for (ffcz_cuda_ctx* l : c->lanes) ffcz_cuda_destroy(l);
+    c->lanes.clear();
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->st);
     if (c->st_copy) cudaStreamSynchronize(c->st_copy);
@@ -996,6 +1016,95 @@ int ffcz_cuda_correct(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const vo
             correct_typed<double>(*ctx, g, *field, original, decompressed, *bounds_original, m,
                                   max_iters, opt, out);
         out->kernel_launches = ctx->launches - l0;
+    });
+}
+
+// Batched frames (BASELINE config 3): every frame is an independent ffcz::correct() call
+// (pipeline.cpp:26-178), with its own bounds, iterations and edit set.  Frames are pulled by
+// `lanes` host threads, each driving its own sub-context (stream + device state), so the small
+// per-frame passes and the per-frame control syncs of one lane overlap the others' work on the
+// GPU.  Results are bit-identical to one ffcz_cuda_correct() per frame.  The batch is ordered
+// on the context stream: lanes start after the work already queued there, and the context stream
+// waits for every lane before the call returns (CUDA events around the call time the batch).
+int ffcz_cuda_correct_batch(ffcz_cuda_ctx* ctx, const ffcz_field_desc* frame, uint64_t nframes,
+                            const void* original, const void* decompressed,
+                            const ffcz_bounds_desc* bounds, int m, uint64_t max_iters,
+                            const ffcz_cuda_options* opt_in, int lanes, ffcz_cuda_result* out) {
+    return guarded(ctx, [&] {
+        if (!frame || !original || !decompressed || !bounds || !out)
+            throw Error(kValidation, "null argument");
+        ffcz_cuda_options opt;
+        ffcz_cuda_default_options(&opt);
+        if (opt_in) opt = *opt_in;
+        if (opt.policy != FFCZ_POLICY_FP64)
+            throw Error(kUnsupported, "only FFCZ_POLICY_FP64 is implemented in this build");
+        for (uint64_t i = 0; i < nframes; ++i) std::memset(&out[i], 0, sizeof(out[i]));
+        if (nframes == 0) return;
+        const Geometry g = make_geometry(frame->ndim, frame->dims, kPitchAlign);
+        const size_t esz = frame->dtype == FFCZ_F32 ? 4 : 8;
+        if (lanes <= 0) lanes = 8;
+        const int nl = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(lanes), nframes));
+        while (static_cast<int>(ctx->lanes.size()) < nl) {
+            ffcz_cuda_ctx* l = nullptr;
+            if (ffcz_cuda_create(&l, ctx->device, nullptr) != kOk)
+                throw Error(kCuda, std::string("lane context: ") + g_last_error);
+            ctx->lanes.push_back(l);
+        }
+        FFCZ_CUDA_CHECK(cudaEventRecord(ctx->ev[7], ctx->st));
+        for (int i = 0; i < nl; ++i) {
+            ffcz_cuda_ctx* l = ctx->lanes[i];
+            FFCZ_CUDA_CHECK(cudaStreamWaitEvent(l->st, ctx->ev[7], 0));
+            if (l->prof_on != ctx->prof_on) {
+                l->prof_on = ctx->prof_on;
+                l->prof.clear();
+                l->ev_used = 0;
+            }
+        }
+        std::atomic<uint64_t> next{0};
+        std::mutex err_mu;
+        int err_status = kOk;
+        std::string err_msg;
+        auto work = [&](ffcz_cuda_ctx* l) {
+            try {
+                FFCZ_CUDA_CHECK(cudaSetDevice(l->device));
+                std::lock_guard<std::mutex> lk(l->mu);
+                for (;;) {
+                    const uint64_t i = next.fetch_add(1);
+                    if (i >= nframes) break;
+                    {
+                        std::lock_guard<std::mutex> ek(err_mu);
+                        if (err_status != kOk) break;
+                    }
+                    const char* o = static_cast<const char*>(original) + i * g.N * esz;
+                    const char* d = static_cast<const char*>(decompressed) + i * g.N * esz;
+                    const unsigned long long l0 = l->launches;
+                    if (frame->dtype == FFCZ_F32)
+                        correct_typed<float>(*l, g, *frame, o, d, bounds[i], m, max_iters, opt, &out[i]);
+                    else
+                        correct_typed<double>(*l, g, *frame, o, d, bounds[i], m, max_iters, opt, &out[i]);
+                    out[i].kernel_launches = l->launches - l0;
+                }
+            } catch (const Error& e) {
+                std::lock_guard<std::mutex> ek(err_mu);
+                if (err_status == kOk) { err_status = e.status; err_msg = e.what(); }
+            } catch (const std::exception& e) {
+                std::lock_guard<std::mutex> ek(err_mu);
+                if (err_status == kOk) { err_status = kCuda; err_msg = e.what(); }
+            }
+        };
+        std::vector<std::thread> th;
+        for (int i = 1; i < nl; ++i) th.emplace_back(work, ctx->lanes[i]);
+        work(ctx->lanes[0]);
+        for (auto& t : th) t.join();
+        for (int i = 0; i < nl; ++i) {
+            ffcz_cuda_ctx* l = ctx->lanes[i];
+            FFCZ_CUDA_CHECK(cudaEventRecord(l->ev[7], l->st));
+            FFCZ_CUDA_CHECK(cudaStreamWaitEvent(ctx->st, l->ev[7], 0));
+        }
+        if (err_status != kOk) {
+            for (uint64_t i = 0; i < nframes; ++i) ffcz_cuda_result_free(&out[i]);
+            throw Error(err_status, "frame batch: " + err_msg);
+        }
     });
 }
 
@@ -1155,12 +1264,16 @@ uint32_t ffcz_cuda_crc32c(const uint8_t* data, size_t len) { return ffcz_host::c
 
 int ffcz_cuda_profile_enable(ffcz_cuda_ctx* ctx, int enable) {
     return guarded(ctx, [&] {
-        if (enable) {
-            ctx->sync();
-            ctx->prof.clear();
-            ctx->ev_used = 0;
+        std::vector<ffcz_cuda_ctx*> all{ctx};
+        all.insert(all.end(), ctx->lanes.begin(), ctx->lanes.end());
+        for (ffcz_cuda_ctx* c : all) {
+            if (enable) {
+                c->sync();
+                c->prof.clear();
+                c->ev_used = 0;
+            }
+            c->prof_on = enable != 0;
         }
-        ctx->prof_on = enable != 0;
     });
 }
 
@@ -1173,16 +1286,22 @@ int ffcz_cuda_profile_read(ffcz_cuda_ctx* ctx, ffcz_cuda_kernel_stat* out, int m
             std::strncpy(st[k].name, kProfNames[k], sizeof(st[k].name) - 1);
         // launches that returned at the convergence gate run for a small fraction of a real
         // pass: anything under 20% of the longest launch of the same class and byte count
-        std::vector<float> dur(ctx->prof.size());
+        // records of the context and of its batch lanes
+        std::vector<ffcz_cuda_ctx::ProfRec> recs = ctx->prof;
+        for (ffcz_cuda_ctx* l : ctx->lanes) {
+            l->sync();
+            recs.insert(recs.end(), l->prof.begin(), l->prof.end());
+        }
+        std::vector<float> dur(recs.size());
         std::map<std::pair<int, double>, float> longest;
-        for (size_t i = 0; i < ctx->prof.size(); ++i) {
-            const auto& r = ctx->prof[i];
+        for (size_t i = 0; i < recs.size(); ++i) {
+            const auto& r = recs[i];
             FFCZ_CUDA_CHECK(cudaEventElapsedTime(&dur[i], r.a, r.b));
             float& l = longest[{r.cls, r.bytes}];
             l = std::max(l, dur[i]);
         }
-        for (size_t i = 0; i < ctx->prof.size(); ++i) {
-            const auto& r = ctx->prof[i];
+        for (size_t i = 0; i < recs.size(); ++i) {
+            const auto& r = recs[i];
             if (dur[i] < 0.2f * longest[{r.cls, r.bytes}]) {
                 ++st[r.cls].gated;
                 continue;
@@ -1252,7 +1371,7 @@ int ffcz_cuda_bench_passes(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, int
                 timed(("col_inv " + ax).c_str(), 32 * Nc, [&] {
                     plan.col(a, +1, h, h, nullptr, HookNone{}, st); });
             }
-            const int za = g.d[0] > 1 ? 0 : 1;
+            const int za = complete_axis(g.d[0] > 1);
             if (g.d[za] > 1 && plan.fused_ok()) {
                 timed("K3a col_fwd_check", 32 * Nc, [&] {
                     plan.col(za, -1, h, h, nullptr, HookFReduce{b.fb, 1.0, c.ctl}, st); });

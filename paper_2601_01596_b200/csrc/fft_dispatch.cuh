@@ -62,6 +62,16 @@ inline bool col_tma_enabled() {
     return on;
 }
 
+// FFCZ_COL_TMA1: 0 = never use the single-landing column pass, 1 = wherever it fits,
+// unset = only where double buffering would fall below 128-B row segments.
+inline int tma1_mode() {
+    static const int m = [] {
+        const char* e = std::getenv("FFCZ_COL_TMA1");
+        return e ? (e[0] == '0' ? 0 : 1) : 2;
+    }();
+    return m;
+}
+
 template <class K>
 void set_smem(K kernel, size_t bytes) {
     if (bytes > 48 * 1024)
@@ -120,6 +130,31 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
         while (Bt > 1 && col_tma_smem_bytes<T, L, E>(Bt, side) > 220 * 1024) Bt /= 2;
         if (const char* e = std::getenv("FFCZ_COL_TMA_B")) Bt = std::max(1, std::atoi(e));
         Bt = std::min(Bt, pow2_ceil(ncols));
+        if constexpr (L >= 512) {
+            // single landing buffer + scalar exchange when double buffering cannot reach 128-B
+            // row segments (k_col_tma1); FFCZ_COL_TMA1=0 disables, =1 forces it where it fits
+            constexpr int NT1 = 512;
+            const int mode = tma1_mode();
+            int B1 = std::min(NT1 / TT, 128);
+            while (B1 > 1 && col_tma1_smem_bytes<T, L, E>(B1) > 220 * 1024) B1 /= 2;
+            B1 = std::min(B1, pow2_ceil(ncols));
+            const bool want = !side && mode != 0 && TT * B1 >= 32 &&
+                              (mode == 1 || (B1 > Bt && Bt * sizeof(cplx<T>) < 128));
+            CUtensorMap map1;
+            if (want && encode_col_map(&map1, src, sizeof(T), ncols, L, row_stride, nplanes,
+                                       plane_stride, B1, L < 256 ? L : 256, true)) {
+                auto kt = dir < 0 ? k_col_tma1<T, L, E, -1, Hook, NT1>
+                                  : k_col_tma1<T, L, E, +1, Hook, NT1>;
+                const size_t sm1 = col_tma1_smem_bytes<T, L, E>(B1);
+                set_smem(kt, sm1);
+                const long long nt = static_cast<long long>((ncols + B1 - 1) / B1) * nplanes;
+                const unsigned grid = persistent_grid(kt, TT * B1, sm1, nt);
+                kt<<<grid, TT * B1, sm1, st>>>(map1, dst, row_stride, plane_stride, ncols, B1, nt,
+                                               tw.stage_table(L, E), gate, hook);
+                FFCZ_LAUNCH_CHECK();
+                return;
+            }
+        }
         const size_t tsmem = col_tma_smem_bytes<T, L, E>(Bt, side);
         CUtensorMap map, side_map;
         bool ok = TT * Bt >= 32 && Bt * sizeof(cplx<T>) >= 32 && tsmem <= 227 * 1024 &&

@@ -129,6 +129,27 @@ struct XchCol {
     __device__ __forceinline__ cplx<T> ld(int i) const { return s[row(i) * B]; }
 };
 
+// Column passes with a scalar exchange buffer: real and imaginary parts are exchanged in two
+// rounds through (L + L/E) x B scalars, half the shared memory of XchCol (k_col_tma1).
+template <class T, int E>
+struct XchColS {
+    static constexpr bool kSplit = true;
+    T* s;   // already offset by the thread's column b
+    int B;
+    __device__ __forceinline__ static int row(int i) { return i + i / E; }
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+    __device__ __forceinline__ void st(int i, T v) const { s[row(i) * B] = v; }
+    __device__ __forceinline__ T ld(int i) const { return s[row(i) * B]; }
+};
+
+template <class X>
+constexpr bool xch_split() {
+    if constexpr (requires { X::kSplit; })
+        return X::kSplit;
+    else
+        return false;
+}
+
 // Row passes: one padded line per row; element i lives at i + i/E.
 template <class T, int E>
 struct XchRow {
@@ -186,17 +207,40 @@ __device__ __forceinline__ void stockham(cplx<T> (&v)[E], int t, const cplx<T>* 
         for (int r = 0; r < R; ++r) v[i + r * NB] = a[r];
     }
     if constexpr (NS * R < L) {
-        xch.sync();
+        if constexpr (xch_split<X>()) {
+            // two scalar rounds (Re, then Im); v keeps the pre-exchange slot order for the Im
+            // round because only the .x halves have been replaced
 #pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            const int j = t + TT * i;
-            const int base = (j / NS) * NS * R + (j & (NS - 1));
+            for (int part = 0; part < 2; ++part) {
+                xch.sync();
 #pragma unroll
-            for (int r = 0; r < R; ++r) xch.st(base + r * NS, v[i + r * NB]);
+                for (int i = 0; i < NB; ++i) {
+                    const int j = t + TT * i;
+                    const int base = (j / NS) * NS * R + (j & (NS - 1));
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        xch.st(base + r * NS, part == 0 ? v[i + r * NB].x : v[i + r * NB].y);
+                }
+                xch.sync();
+#pragma unroll
+                for (int m = 0; m < E; ++m) {
+                    if (part == 0) v[m].x = xch.ld(t + TT * m);
+                    else v[m].y = xch.ld(t + TT * m);
+                }
+            }
+        } else {
+            xch.sync();
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                const int j = t + TT * i;
+                const int base = (j / NS) * NS * R + (j & (NS - 1));
+#pragma unroll
+                for (int r = 0; r < R; ++r) xch.st(base + r * NS, v[i + r * NB]);
+            }
+            xch.sync();
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = xch.ld(t + TT * m);
         }
-        xch.sync();
-#pragma unroll
-        for (int m = 0; m < E; ++m) v[m] = xch.ld(t + TT * m);
         stockham<T, L, E, NS * R, DIR>(v, t, tw, xch);
     }
 }
@@ -400,6 +444,91 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 1)
         }
     }
     hook.finish();
+}
+
+// TMA-staged column pass for tiles too large to double-buffer (FP64 L >= 1024 at B = 8 columns,
+// FP32 L >= 1024 at B = 16: 128-B row segments, which the first-axis pass needs to stay near the
+// DRAM page / TLB sweet spot — 64-B segments measured 0.38 of HBM at 1024^3).  One dense TMA
+// landing buffer (L x B complex) plus a separate scalar exchange buffer (XchColS): the next
+// tile's box load is issued as soon as this tile's elements are in registers, so it lands while
+// the current tile is transformed, hooked and stored.  Delta of kDelta hooks is read from global
+// memory (the per-component side tile stays with k_col_tma).
+// smem: L x B complex + (L + L/E) x B scalars + 1 mbarrier.
+template <class T, int L, int E, int DIR, class Hook, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    k_col_tma1(const __grid_constant__ CUtensorMap map, cplx<T>* __restrict__ dst,
+               long long row_stride, long long plane_stride, int ncols, int B, long long ntiles,
+               const cplx<T>* __restrict__ tw, const int* gate, Hook hook) {
+    if (gated(gate)) return;
+    hook_begin(hook);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int TT = L / E;
+    constexpr int LB = L < 256 ? L : 256;
+    constexpr bool kDelta = hook_delta<Hook>();
+    const int b = threadIdx.x % B;
+    const int t = threadIdx.x / B;
+    const int tiles_c = (ncols + B - 1) / B;
+    cplx<T>* land = reinterpret_cast<cplx<T>*>(smem_raw);
+    T* xs = reinterpret_cast<T*>(land + L * B);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(
+        smem_raw + ((static_cast<size_t>(L) * B * sizeof(cplx<T>) +
+                     static_cast<size_t>(L + L / E) * B * sizeof(T) + 15) & ~size_t(15)));
+    const unsigned tile_bytes = static_cast<unsigned>(L) * B * sizeof(cplx<T>);
+    auto issue = [&](long long tile) {
+        const long long plane = tile / tiles_c;
+        const int c0 = static_cast<int>(tile - plane * tiles_c) * B;
+        mbar_arrive_expect_tx(bar, tile_bytes);
+#pragma unroll
+        for (int j = 0; j < L / LB; ++j)
+            tma_load_3d(land + j * LB * B, &map, bar, 2 * c0, j * LB, static_cast<int>(plane));
+    };
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&map);
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < ntiles) issue(blockIdx.x);
+    unsigned phase = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        const long long plane = tile / tiles_c;
+        const int c = static_cast<int>(tile - plane * tiles_c) * B + b;
+        const bool valid = c < ncols;
+        const long long base = plane * plane_stride + c;
+        cplx<T> v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = land[(t + TT * m) * B + b];
+        fence_proxy_async_smem();  // generic reads of the landing buffer before the async refill
+        __syncthreads();
+        if (threadIdx.x == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x);
+        if (valid) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const long long off = base + static_cast<long long>(t + TT * m) * row_stride;
+                if constexpr (kDelta) hook.pre_d(v[m], off, c, hook.fb.at2(off));
+                else hook.pre(v[m], off, c);
+            }
+        }
+        stockham<T, L, E, 1, DIR>(v, t, tw, XchColS<T, E>{xs + b, B});
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const long long off = base + static_cast<long long>(t + TT * m) * row_stride;
+            if (valid) {
+                if constexpr (kDelta) hook.post_d(v[m], off, c, hook.fb.at2(off));
+                else hook.post(v[m], off, c);
+                if constexpr (hook_stores<Hook>()) dst[off] = v[m];
+            }
+        }
+    }
+    hook.finish();
+}
+
+template <class T, int L, int E>
+constexpr size_t col_tma1_smem_bytes(int B) {
+    return ((static_cast<size_t>(L) * B * sizeof(cplx<T>) +
+             static_cast<size_t>(L + L / E) * B * sizeof(T) + 15) & ~size_t(15)) + 16;
 }
 
 template <class T, int L, int E>

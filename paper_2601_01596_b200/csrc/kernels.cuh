@@ -155,7 +155,10 @@ struct HookFClip {
         if (first) {
             F[off] = make_double2(0.0 + xre, 0.0 + xim);
         } else if (xre != 0.0 || xim != 0.0) {
-            double2 f = F[off];
+            // read through the non-coherent path: element `off` is read once, by this thread,
+            // before its own store, so the compiler may hoist the loads of the whole register
+            // set above the pass's stores (no exposed latency per clipped element)
+            double2 f = __ldg(&F[off]);
             f.x += xre;
             f.y += xim;
             F[off] = f;
@@ -188,7 +191,7 @@ struct HookSClip {
         const double c = clamp_abs(xd, e);
         const double d = c - xd;
         if (first) S[n] = 0.0 + d;
-        else if (d != 0.0) S[n] += d;
+        else if (d != 0.0) S[n] = __ldg(&S[n]) + d;  // see HookFClip
         return static_cast<T>(c);
     }
     __device__ __forceinline__ void post_real(T& x0, T& x1, long long n) {

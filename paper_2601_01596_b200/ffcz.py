@@ -222,35 +222,8 @@ def _bounds_desc(b: DualBounds, m: _Marshal):
     return bd
 
 
-def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: int = 1000,
-            precision: str | None = None, *, want_archive: bool = True, want_edits: bool = True,
-            want_corrected: bool = True, zlib_level: int = 9, fused: bool = True,
-            copy: bool = True, ctx: Context | None = None) -> CorrectionResult:
-    """ffcz::correct (pipeline.cpp:26-178) on the GPU.
-
-    original / decompressed: numpy arrays (host; float32 or float64) or CUDA torch tensors (then
-    every bound array must be a CUDA tensor too).  precision: the ScalarField precision tag
-    written into the archive ("f32" / "f64"; default from the input dtype).  copy=False returns
-    views of the library's pinned result buffers, valid while the returned object is alive.
-    """
-    ctx = ctx or default_context()
+def _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level):
     lib = capi.load()
-    on_dev = _is_torch(original)
-    if on_dev:
-        import torch
-        is32 = original.dtype == torch.float32
-        shape = tuple(original.shape)
-    else:
-        original = np.asarray(original)
-        decompressed = np.asarray(decompressed)
-        is32 = original.dtype == np.float32
-        shape = original.shape
-    if precision is None:
-        precision = "f32" if is32 else "f64"
-    dt = np.float32 if is32 else np.float64
-    mar = _Marshal()
-    fd = _field_desc(shape, capi.FFCZ_F32 if is32 else capi.FFCZ_F64, precision)
-    bd = _bounds_desc(bounds, mar)
     opt = capi.Options()
     lib.ffcz_cuda_default_options(C.byref(opt))
     flags = 0
@@ -266,61 +239,148 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
         flags |= capi.FFCZ_FORCE_UNFUSED
     opt.flags = flags
     opt.zlib_level = zlib_level
-    holder = _ResultHolder()
+    return opt
+
+
+def _convert(holder, shape, want_archive, want_edits, want_corrected, copy):
+    """ffcz_cuda_result -> CorrectionResult (views of the pinned buffers when copy=False)."""
     res = holder.res
+    N = int(np.prod(shape))
+    r = res.report
+    rep = ProjectionReport(int(r.iterations), int(r.active_spatial), int(r.active_frequency),
+                           bool(r.converged), float(r.residual_f), float(r.residual_s),
+                           float(r.wall_time_s))
+
+    def arr(p, n, dtype):
+        if not p or n == 0:
+            return np.zeros(0, dtype=dtype)
+        a = np.ctypeslib.as_array(p, shape=(n,))
+        return (a.copy() if copy else a).view(dtype)
+
+    edits = want_edits or want_archive
+    sflags = fflags = scodes = fcodes = None
+    escapes = None
+    if edits:
+        sflags = arr(res.spatial_flags, int(res.spatial_flag_bytes), np.uint8)
+        fflags = arr(res.frequency_flags, int(res.frequency_flag_bytes), np.uint8)
+        scodes = arr(res.spatial_codes, int(res.n_spatial), np.int32)
+        fcodes = arr(res.frequency_codes, 2 * int(res.n_frequency), np.int32)
+        ne = int(res.escape_count)
+        if ne and res.escapes:
+            raw = np.ctypeslib.as_array(C.cast(res.escapes, C.POINTER(C.c_uint8)),
+                                        shape=(ne * C.sizeof(capi.Escape),))
+            escapes = raw.view(ESCAPE_DTYPE)
+            if copy:
+                escapes = escapes.copy()
+        else:
+            escapes = np.zeros(0, dtype=ESCAPE_DTYPE)
+    corrected = None
+    if want_corrected:
+        corrected = np.ctypeslib.as_array(res.corrected, shape=(N,)).reshape(shape)
+        if copy:
+            corrected = corrected.copy()
+    data = C.string_at(res.archive, res.archive_len) if want_archive else None
+    timings = {k: float(getattr(res, k)) for k in ("t_feasible_ms", "t_loop_ms", "t_gate_ms",
+                                                   "t_h2d_ms", "t_d2h_ms", "t_archive_ms")}
+    out = CorrectionResult(data, rep, int(res.escape_count), bool(res.verify_ok),
+                           float(res.verify_max_spatial_excess),
+                           float(res.verify_max_freq_excess), sflags, fflags, scodes, fcodes,
+                           escapes, corrected, int(res.escape_rounds), timings,
+                           int(res.kernel_launches))
+    if copy:
+        holder.free()
+    else:
+        out._holder = holder  # keeps the pinned buffers alive with the views
+    return out
+
+
+def _field_of(original, decompressed):
+    """(on_dev, is32, shape, original, decompressed) of numpy / CUDA torch inputs."""
+    on_dev = _is_torch(original)
+    if on_dev:
+        import torch
+        is32 = original.dtype == torch.float32
+        shape = tuple(original.shape)
+    else:
+        original = np.asarray(original)
+        decompressed = np.asarray(decompressed)
+        is32 = original.dtype == np.float32
+        shape = original.shape
+    return on_dev, is32, shape, original, decompressed
+
+
+def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: int = 1000,
+            precision: str | None = None, *, want_archive: bool = True, want_edits: bool = True,
+            want_corrected: bool = True, zlib_level: int = 9, fused: bool = True,
+            copy: bool = True, ctx: Context | None = None) -> CorrectionResult:
+    """ffcz::correct (pipeline.cpp:26-178) on the GPU.
+
+    original / decompressed: numpy arrays (host; float32 or float64) or CUDA torch tensors (then
+    every bound array must be a CUDA tensor too).  precision: the ScalarField precision tag
+    written into the archive ("f32" / "f64"; default from the input dtype).  copy=False returns
+    views of the library's pinned result buffers, valid while the returned object is alive.
+    """
+    ctx = ctx or default_context()
+    lib = capi.load()
+    on_dev, is32, shape, original, decompressed = _field_of(original, decompressed)
+    if precision is None:
+        precision = "f32" if is32 else "f64"
+    dt = np.float32 if is32 else np.float64
+    mar = _Marshal()
+    fd = _field_desc(shape, capi.FFCZ_F32 if is32 else capi.FFCZ_F64, precision)
+    bd = _bounds_desc(bounds, mar)
+    opt = _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level)
+    holder = _ResultHolder()
     rc = lib.ffcz_cuda_correct(ctx.handle, C.byref(fd), mar.ptr(original, dt),
                                mar.ptr(decompressed, dt), C.byref(bd), int(m), int(max_iters),
-                               C.byref(opt), C.byref(res))
+                               C.byref(opt), C.byref(holder.res))
     try:
         _check(rc)
-        N = int(np.prod(shape))
-        r = res.report
-        rep = ProjectionReport(int(r.iterations), int(r.active_spatial), int(r.active_frequency),
-                               bool(r.converged), float(r.residual_f), float(r.residual_s),
-                               float(r.wall_time_s))
+    except Exception:
+        holder.free()
+        raise
+    return _convert(holder, shape, want_archive, want_edits, want_corrected, copy)
 
-        def arr(p, n, dtype):
-            if not p or n == 0:
-                return np.zeros(0, dtype=dtype)
-            a = np.ctypeslib.as_array(p, shape=(n,))
-            return (a.copy() if copy else a).view(dtype)
 
-        edits = want_edits or want_archive
-        sflags = fflags = scodes = fcodes = None
-        escapes = None
-        if edits:
-            sflags = arr(res.spatial_flags, int(res.spatial_flag_bytes), np.uint8)
-            fflags = arr(res.frequency_flags, int(res.frequency_flag_bytes), np.uint8)
-            scodes = arr(res.spatial_codes, int(res.n_spatial), np.int32)
-            fcodes = arr(res.frequency_codes, 2 * int(res.n_frequency), np.int32)
-            ne = int(res.escape_count)
-            if ne and res.escapes:
-                raw = np.ctypeslib.as_array(C.cast(res.escapes, C.POINTER(C.c_uint8)),
-                                            shape=(ne * C.sizeof(capi.Escape),))
-                escapes = raw.view(ESCAPE_DTYPE)
-                if copy:
-                    escapes = escapes.copy()
-            else:
-                escapes = np.zeros(0, dtype=ESCAPE_DTYPE)
-        corrected = None
-        if want_corrected:
-            corrected = np.ctypeslib.as_array(res.corrected, shape=(N,)).reshape(shape)
-            if copy:
-                corrected = corrected.copy()
-        data = C.string_at(res.archive, res.archive_len) if want_archive else None
-        timings = {k: float(getattr(res, k)) for k in ("t_feasible_ms", "t_loop_ms", "t_gate_ms",
-                                                       "t_h2d_ms", "t_d2h_ms", "t_archive_ms")}
-        out = CorrectionResult(data, rep, int(res.escape_count), bool(res.verify_ok),
-                               float(res.verify_max_spatial_excess),
-                               float(res.verify_max_freq_excess), sflags, fflags, scodes, fcodes,
-                               escapes, corrected, int(res.escape_rounds), timings,
-                               int(res.kernel_launches))
-        if not copy:
-            out._holder = holder  # keeps the pinned buffers alive with the views
-        return out
-    finally:
-        if copy:
-            holder.free()
+def correct_batch(original, decompressed, bounds, m: int = 16, max_iters: int = 1000,
+                  precision: str | None = None, *, lanes: int = 8, want_archive: bool = True,
+                  want_edits: bool = True, want_corrected: bool = True, zlib_level: int = 9,
+                  fused: bool = True, copy: bool = True,
+                  ctx: Context | None = None) -> list[CorrectionResult]:
+    """Independent ffcz::correct() of every frame of a batch (BASELINE config 3).
+
+    original / decompressed: arrays of shape (frames, *frame_shape), numpy or CUDA torch.
+    bounds: one DualBounds per frame (a single DualBounds is used for every frame).  Returns one
+    CorrectionResult per frame, identical to correct() on that frame alone.
+    """
+    ctx = ctx or default_context()
+    lib = capi.load()
+    on_dev, is32, shape, original, decompressed = _field_of(original, decompressed)
+    nf, frame = int(shape[0]), tuple(shape[1:])
+    if precision is None:
+        precision = "f32" if is32 else "f64"
+    dt = np.float32 if is32 else np.float64
+    if isinstance(bounds, DualBounds):
+        bounds = [bounds] * nf
+    if len(bounds) != nf:
+        raise ValidationError(f"correct_batch: {len(bounds)} bounds for {nf} frames")
+    mar = _Marshal()
+    fd = _field_desc(frame, capi.FFCZ_F32 if is32 else capi.FFCZ_F64, precision)
+    bds = (capi.BoundsDesc * max(1, nf))()
+    for i, b in enumerate(bounds):
+        bds[i] = _bounds_desc(b, mar)
+    opt = _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level)
+    res = (capi.Result * max(1, nf))()
+    rc = lib.ffcz_cuda_correct_batch(ctx.handle, C.byref(fd), nf, mar.ptr(original, dt),
+                                     mar.ptr(decompressed, dt), bds, int(m), int(max_iters),
+                                     C.byref(opt), int(lanes), res)
+    _check(rc)
+    outs = []
+    for i in range(nf):
+        h = _ResultHolder()
+        C.memmove(C.byref(h.res), C.byref(res[i]), C.sizeof(capi.Result))
+        outs.append(_convert(h, frame, want_archive, want_edits, want_corrected, copy))
+    return outs
 
 
 def alternating_projection(eps0, bounds_working: DualBounds, max_iters: int,

@@ -35,15 +35,23 @@ def run(shape, dtype, reps, ctx, peak):
 
 
 def main():
-    n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
+    # argv[1]: n (n^3 and 2048^2) or a comma list of shapes "AxBxC,..."; argv[3]: f64|f32|both
+    spec = sys.argv[1] if len(sys.argv) > 1 else "512"
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+    which = sys.argv[3] if len(sys.argv) > 3 else "both"
+    dts = {"f64": (1,), "f32": (0,), "both": (1, 0)}[which]
     peak = 6548.2
     pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(pk):
         peak = json.load(open(pk))["hbm_gbs"]
     ctx = P.Context(0)
-    for shape in [(n, n, n), (2048, 2048)]:
-        for dt in (1, 0):
+    if "x" in spec:
+        shapes = [tuple(int(v) for v in sh.split("x")) for sh in spec.split(",")]
+    else:
+        n = int(spec)
+        shapes = [(n, n, n), (2048, 2048)]
+    for shape in shapes:
+        for dt in dts:
             run(shape, dt, reps, ctx, peak)
 
 
