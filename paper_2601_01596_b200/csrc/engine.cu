@@ -205,6 +205,16 @@ constexpr int kPitchAlign = 16;
 // MIDDLE axis (row stride P: a tile's rows sit inside one plane, so the hooks' F / Delta accesses
 // stay TLB- and DRAM-page-local), with the outer axis transformed first.  FFCZ_COMPLETE_AXIS=0
 // restores the outer axis (A/B runs).  2-D fields have only axis 1.
+// FFCZ_F_REBUILD=0: accumulate F in every clip pass (read-modify-write) instead of marking the
+// moved components and rebuilding F once at the gate (HookFClip::moved, HookFRebuild).
+inline bool f_rebuild_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_F_REBUILD");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 inline int complete_axis(bool three_d) {
     static const int v = [] {
         const char* e = std::getenv("FFCZ_COMPLETE_AXIS");
@@ -277,12 +287,14 @@ struct LoopResult {
     bool converged = false;
     double residual_f = 0.0;
     bool fused = false;
+    const unsigned char* moved = nullptr;  // rebuild mode: F is complete only after pass 1
 };
 
 // The POCS loop (projection.cpp:96-126) on device.  eps holds epsilon0 on entry and the final
 // epsilon on exit; S (N) and F (half) are the accumulated edits.
 LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Bounds& bw,
-                    double fscale, bool allow_fused, double* S, double2* F) {
+                    double fscale, bool allow_fused, double* S, double2* F,
+                    bool allow_rebuild = true) {
     cudaStream_t st = c.st;
     FftPlan<double> plan{g, &c.tw64};
     const int* gate = &c.ctl->done;
@@ -295,6 +307,11 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
         FFCZ_CUDA_CHECK(cudaMemsetAsync(F, 0, g.half_elems() * sizeof(double2), st));
     }
     const bool three_d = g.d[0] > 1;
+    unsigned char* moved = nullptr;
+    if (fused && allow_rebuild && f_rebuild_enabled()) {
+        moved = c.b<unsigned char>("f_moved", g.half_elems());
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(moved, 0, g.half_elems(), st));
+    }
     const int za = complete_axis(three_d);  // the pass that completes the forward transform
     const int mid = 1 - za;                   // the other column axis (3-D only)
     double* tmp = fused ? nullptr : c.b<double>("real_tmp", g.N);
@@ -312,7 +329,8 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
             k_decide<<<1, 1, 0, st>>>(c.ctl);                                              // K4
             {
                 Prof p(c, kColClipInv, check_bytes);
-                plan.col(za, +1, spec, spec, gate, HookFClip<double>{bw.fb, fscale, F, c.ctl}, st); // K3b
+                plan.col(za, +1, spec, spec, gate,
+                         HookFClip<double>{bw.fb, fscale, F, c.ctl, moved}, st);          // K3b
             }
             if (three_d) {
                 Prof p(c, kColPass, pass_bytes);
@@ -395,6 +413,7 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
     r.converged = h.converged;
     r.residual_f = h.residual_f;
     r.fused = fused;
+    r.moved = moved;
     return r;
 }
 
@@ -463,7 +482,7 @@ void c2r_p(ffcz_cuda_ctx& c, const FftPlan<double>& plan, const double2* half, d
 
 template <class TI>
 GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* dec,
-                 const Bounds& bo, int m, bool converged, bool fused, double* eps, double* S,
+                 const Bounds& bo, int m, const LoopResult& lr, double* eps, double* S,
                  double2* F, double* corrected,
                  const std::function<void(unsigned long long, unsigned long long)>& on_codes) {
     cudaStream_t st = c.st;
@@ -483,6 +502,33 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
     double2* spec = c.b<double2>("spec", g.half_elems());
     double* eps_t = c.b<double>("eps_tilde", N);
 
+    const bool converged = lr.converged, fused = lr.fused;
+    if (lr.moved && lr.passes >= 2) {
+        // F = mask(delta_final - FFT(eps0 + S)): one forward transform replaces the F
+        // read-modify-writes of clip passes 2.. (HookFClip::moved); delta_final is `spec`
+        const bool three_d = g.d[0] > 1;
+        const int za = complete_axis(three_d);
+        double* x = eps_t;
+        double2* work = freq_cur;  // free until k_gate_freq below
+        {
+            Prof p(c, kElemPre, (2.0 * sizeof(TI) + 16.0) * N);
+            k_eps0_plus_s<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, S, x, N);
+        }
+        {
+            Prof p(c, kRowR2C, 8.0 * g.N + 16.0 * Nc);
+            launch_row_r2c<double>(g.n2, x, g.n2, work, g.P, g.rows, c.tw64, nullptr, st);
+        }
+        if (three_d) {
+            Prof p(c, kColPass, 32.0 * Nc);
+            plan.col(1 - za, -1, work, work, nullptr, HookNone{}, st);
+        }
+        {
+            Prof p(c, kColFwdCheck, 48.0 * Nc + Nc);
+            plan.col(za, -1, work, work, nullptr, HookFRebuild{spec, F, lr.moved}, st);
+        }
+        FFCZ_LAUNCH_CHECK();
+        c.launches += three_d ? 4 : 3;
+    }
     FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->act_s, 0, 2 * sizeof(unsigned long long), st));
     {
         Prof p(c, kElemGate, 16.0 * N + 32.0 * Nc);
@@ -753,8 +799,7 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
                                         nf * 8, cudaMemcpyDeviceToHost, cs));
         copy_pending = true;
     };
-    const GateOut go = run_gate<TI>(c, g, orig, dec, bo, m, lr.converged, lr.fused, eps, S, F,
-                                    corrected, on_codes);
+    const GateOut go = run_gate<TI>(c, g, orig, dec, bo, m, lr, eps, S, F, corrected, on_codes);
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[6], st));
     dbg.mark(c, "gate done");
     h = c.read_ctl();
@@ -1157,7 +1202,9 @@ int ffcz_cuda_alternating_projection(ffcz_cuda_ctx* ctx, const ffcz_field_desc* 
         double* S = c.b<double>("S", N);
         double2* F = c.b<double2>("F", g.half_elems());
         FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[2], st));
-        const LoopResult lr = run_loop(c, g, eps, bw, 1.0, !(opt.flags & FFCZ_FORCE_UNFUSED), S, F);
+        // F is returned: accumulate it in every clip pass (no gate-side rebuild here)
+        const LoopResult lr = run_loop(c, g, eps, bw, 1.0, !(opt.flags & FFCZ_FORCE_UNFUSED), S, F,
+                                       false);
         FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[3], st));
         k_residual_s<<<grid_for(N), 256, 0, st>>>(eps, N, bw.sb, 1.0, c.ctl);
         FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->act_s, 0, 2 * sizeof(unsigned long long), st));

@@ -122,6 +122,18 @@ template __global__ void k_eps0<float>(const float*, const float*, double*, long
 template __global__ void k_eps0<double>(const double*, const double*, double*, long long,
                                         SpatialB, double, double, int, Ctl*);
 
+template <class TI>
+__global__ void k_eps0_plus_s(const TI* __restrict__ orig, const TI* __restrict__ dec,
+                              const double* __restrict__ S, double* out, long long N) {
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
+         n += (long long)gridDim.x * blockDim.x)
+        out[n] = (static_cast<double>(dec[n]) - static_cast<double>(orig[n])) + S[n];
+}
+template __global__ void k_eps0_plus_s<float>(const float*, const float*, const double*, double*,
+                                              long long);
+template __global__ void k_eps0_plus_s<double>(const double*, const double*, const double*,
+                                               double*, long long);
+
 __global__ void k_cast_to_double(const float* __restrict__ in, double* out, long long N) {
     for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
          n += (long long)gridDim.x * blockDim.x)

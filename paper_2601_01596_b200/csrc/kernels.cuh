@@ -138,6 +138,11 @@ struct HookFClip {
     double fscale;
     double2* F;
     const Ctl* ctl = nullptr;
+    // rebuild mode (fused loop): after the first clip pass, F is not read-modify-written; the
+    // pass only marks `moved[off] = 1` where a clamp moved a component, and the gate rebuilds
+    // F = mask(delta_final - FFT(eps0 + S)) once (HookFRebuild) — the loop's invariant
+    // eps = eps0 + S + IFFT(F) (projection.cpp:117-124) makes that the same sum.
+    unsigned char* moved = nullptr;
     bool first = false;
     __device__ __forceinline__ void begin() {
         first = ctl != nullptr && *reinterpret_cast<const volatile unsigned long long*>(&ctl->passes) == 1;
@@ -152,7 +157,10 @@ struct HookFClip {
         const double dre = d.x * fscale, dim = d.y * fscale;
         const double cre = clamp_abs(re, dre), cim = clamp_abs(im, dim);
         const double xre = cre - re, xim = cim - im;
-        if (first) {
+        if (moved) {
+            if (first) F[off] = make_double2(0.0 + xre, 0.0 + xim);
+            if (xre != 0.0 || xim != 0.0) moved[off] = 1;
+        } else if (first) {
             F[off] = make_double2(0.0 + xre, 0.0 + xim);
         } else if (xre != 0.0 || xim != 0.0) {
             // read through the non-coherent path: element `off` is read once, by this thread,
@@ -201,6 +209,32 @@ struct HookSClip {
     }
     __device__ __forceinline__ void finish() {}
 };
+
+// Rebuild of the accumulated frequency edits at the end of a rebuild-mode loop: the pass
+// transforms eps0 + S forward; F = delta_final - that, where any clip ever moved the component,
+// else exactly 0 (the reference's F is exactly 0 where it never clipped, editset.cpp:43-66).
+struct HookFRebuild {
+    static constexpr bool kNoStore = true;
+    const double2* delta;
+    double2* F;
+    const unsigned char* moved;
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    template <class C>
+    __device__ __forceinline__ void post(C& v, long long off, int) {
+        double2 f = make_double2(0.0, 0.0);
+        if (moved[off]) {
+            const double2 d = __ldg(&delta[off]);
+            f = make_double2(d.x - v.x, d.y - v.y);
+        }
+        F[off] = f;
+    }
+    __device__ __forceinline__ void finish() {}
+};
+
+// eps0 + S (the forward input of the F rebuild), eps0 = dec - orig as k_eps0 forms it
+template <class TI>
+__global__ void k_eps0_plus_s(const TI* __restrict__ orig, const TI* __restrict__ dec,
+                              const double* __restrict__ S, double* out, long long N);
 
 // ---- FP64 gate hooks (fused into the round / verify passes) -----------------------------------------
 
