@@ -302,6 +302,69 @@ def run_frames(args, rank, world, local):
     ctx.close()
 
 
+def run_slab(args, rank, world, local):
+    """Configs 4/5: ONE combustion-like volume slab-decomposed along axis 0 across the ranks
+    (paper_2601_01596_b200/slab.py: two NCCL all-to-alls + one all-reduce per iteration);
+    strong scaling (the volume is fixed).  One step = one distributed correct()."""
+    import torch
+    import torch.distributed as dist
+    from paper_2601_01596_b200.slab_gpu import GpuSlabBackend
+    from paper_2601_01596_b200 import slab
+    dev = torch.device("cuda", local)
+    n = args.n
+    o, d, E, D = make_workload_combustion(n, 4321, dev)
+    c0 = n // world
+    o = o[rank * c0:(rank + 1) * c0].contiguous()
+    d = d[rank * c0:(rank + 1) * c0].contiguous()
+    torch.cuda.empty_cache()
+    be = GpuSlabBackend(n, dev)
+    comm = slab.Comm()
+
+    def step():
+        return slab.correct_slab(be, comm, (n, n, n), o, d, E, D)
+
+    for _ in range(args.warmup):
+        r = step()
+    assert r.converged and r.verify_ok, r
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    stream = torch.cuda.current_stream(dev)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            r = step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    ms_step = ms / args.steps
+    if rank == 0:
+        print(json.dumps({
+            "metric": "corrected GB/s (input bytes / time to feasibility)",
+            "value": 4.0 * n ** 3 / (ms_step * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"config4: {n}^3 FP32 combustion-like front, global "
+                                   "Delta=0.6*mean|delta0|, slab-decomposed along axis 0",
+                       "n": n, "m": 16, "policy": "fp64 (reference control flow)",
+                       "l2": f"inputs larger than L2 ({4 * n ** 3 / world / 1e9:.2f} GB per rank)",
+                       "parallelism": f"slab x{world} (NCCL all-to-all)"},
+            "iterations": r.iterations, "escape_rounds": r.escape_rounds,
+            "escapes": len(r.escapes), "e2e": None, "cpu_baseline": None,
+            "clocks": clk.summary()}))
+    be.ctx.close()
+
+
 def make_workload_numpy(n, seed):
     """Same recipe on the host (CPU baseline sample)."""
     rng = np.random.default_rng(seed)
@@ -456,7 +519,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=512)
-    ap.add_argument("--config", default="nyx", choices=["nyx", "combustion", "frames"],
+    ap.add_argument("--config", default="nyx", choices=["nyx", "combustion", "frames", "slab"],
                     help="nyx = BASELINE configs[1] (default); combustion = configs[3] recipe; "
                          "frames = configs[2] (batched 2-D frames, sharded)")
     ap.add_argument("--frames", type=int, default=1024)
@@ -481,8 +544,8 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if args.config == "frames":
-        run_frames(args, rank, world, local)
+    if args.config in ("frames", "slab"):
+        (run_frames if args.config == "frames" else run_slab)(args, rank, world, local)
         if world > 1:
             dist.destroy_process_group()
         return

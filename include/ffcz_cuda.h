@@ -167,6 +167,58 @@ int ffcz_cuda_correct_batch(ffcz_cuda_ctx* ctx, const ffcz_field_desc* frame, ui
                             const ffcz_bounds_desc* bounds, int m, uint64_t max_iters,
                             const ffcz_cuda_options* opt, int lanes, ffcz_cuda_result* out);
 
+/* Slab-decomposed correction of one volume across ranks (BASELINE configs 4/5).
+ * The orchestration (transposes = all-to-alls, all-reduced loop decisions, cross-rank escape
+ * repair) is paper_2601_01596_b200/slab.py over torch.distributed; this entry point runs one
+ * per-rank device step of it on device buffers, on the context stream.  Buffers: real slabs
+ * d0 x d1 x n2 FP64 (inputs: `in_dtype`), half spectra d0 x d1 x P complex FP64 with
+ * P = round_up(n2/2+1, 16) (ffcz_cuda_slab_pitch), bitmaps uint32 LSB-first.  Bounds are global
+ * (E, Delta); `fscale` = 1 - 2^-m for the working bounds.  Ops that reduce synchronise the stream
+ * and return their scalars in out[0..3]. */
+typedef enum ffcz_cuda_slab_opcode {
+    FFCZ_SLAB_EPS0 = 0,           /* p0 orig, p1 dec, p2 eps -> out: first bad index (E(1+2^-20)),
+                                     first bad index (working E * (1+slack), slack = delta), -1 none */
+    FFCZ_SLAB_FWD_LOCAL = 1,      /* p0 real x -> p1 half: R2C rows + forward FFT along axis 1 */
+    FFCZ_SLAB_COL0_CHECK = 2,     /* p0 half in place: forward axis 0 + check_convergence
+                                     (projection.cpp:29-52) vs delta*fscale -> out: peak, excess */
+    FFCZ_SLAB_COL0_CLIP_INV = 3,  /* p0 half in place: project_onto_fcube (F p1 dense on `first`,
+                                     clip map p2 |= moved) + inverse axis 0 */
+    FFCZ_SLAB_COL0_PLAIN = 4,     /* p0 src -> p1 dst along axis 0, direction `dir` */
+    FFCZ_SLAB_COL0_REBUILD = 5,   /* p0 half (FFT(eps0+S) after axis 1) -> F p3 = map p2 ?
+                                     delta p1 - forward axis 0 : 0 */
+    FFCZ_SLAB_COL0_MARK = 6,      /* p0 half in place: forward axis 0; violation bitmap p1 over
+                                     storage offsets vs delta (pipeline.cpp:140-147) -> out: any */
+    FFCZ_SLAB_COL0_VERIFY = 7,    /* p0 half: forward axis 0, max(|.|-delta) > 0 -> out: excess */
+    FFCZ_SLAB_INV_SCLIP = 8,      /* p0 half (clobbered): inverse axis 1, C2R x 1/n_total,
+                                     project_onto_scube vs e*fscale -> p1 eps, S p2 */
+    FFCZ_SLAB_INV_REPAIR_VERIFY = 9, /* p0 half (clobbered) -> p1 eps_tilde; p2 orig, p3 dec,
+                                     p4 spat_cur (repaired in place), p5 final eps, p6 escape
+                                     bitmap, p7 corrected, p8 eps_v -> out: dirty, spatial excess */
+    FFCZ_SLAB_INV_VERIFY = 10,    /* p0 half -> p1 eps_v; p2 orig, p3 dec, p4 spat_cur,
+                                     p5 corrected -> out: spatial excess */
+    FFCZ_SLAB_RESIDUAL_S = 11,    /* p0 eps -> out: max(|eps| - e*fscale, 0) */
+    FFCZ_SLAB_EPS0_PLUS_S = 12,   /* p0 orig, p1 dec, p2 S -> p3 (dec - orig) + S */
+    FFCZ_SLAB_GATE = 13           /* p0 S, p1 F (natural half) -> p2 spat_cur, p3 freq_cur,
+                                     p4 keep_s, p5 esc_s, p6 keep_f, p7 esc_f bitmaps, p8 codes_s,
+                                     p9 codes_f (editset.cpp:43-133, pipeline.cpp:57-106)
+                                     -> out: active_s, active_f, kept_s, kept_f */
+} ffcz_cuda_slab_opcode;
+
+typedef struct ffcz_cuda_slab_op {
+    int32_t op;          /* ffcz_cuda_slab_opcode */
+    int32_t dir;         /* COL0_PLAIN: -1 forward, +1 inverse */
+    int32_t first;       /* CLIP passes: the first clip pass (dense F / S write) */
+    int32_t in_dtype;    /* ffcz_cuda_dtype of orig / dec */
+    int32_t m;           /* GATE: quantiser m */
+    int32_t pad;
+    uint64_t d0, d1, n2; /* local geometry of the buffer(s) the op works on */
+    uint64_t n_total;    /* global sample count (C2R normalisation) */
+    double e, delta, fscale, slack;
+    void* p[10];
+} ffcz_cuda_slab_op;
+int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4]);
+uint64_t ffcz_cuda_slab_pitch(uint64_t n2);
+
 /* Replaces ffcz::alternating_projection (projection.cpp:81-142).  eps0 is a field of
  * field->dtype; bounds are the WORKING bounds.  Outputs (host, caller-allocated, may be NULL):
  * spatial_edits N doubles, frequency_edits 2N doubles (FULL spectrum, interleaved),

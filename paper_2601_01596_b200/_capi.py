@@ -39,6 +39,7 @@ EXPORTS = [
     "ffcz_cuda_alternating_projection", "ffcz_cuda_forward_dft", "ffcz_cuda_inverse_dft",
     "ffcz_cuda_r2c_device", "ffcz_cuda_c2r_device", "ffcz_cuda_crc32c",
     "ffcz_cuda_profile_enable", "ffcz_cuda_profile_read", "ffcz_cuda_bench_passes",
+    "ffcz_cuda_slab", "ffcz_cuda_slab_pitch",
 ]
 
 
@@ -116,6 +117,9 @@ def load():
     lib.ffcz_cuda_correct_batch.argtypes = [P, C.POINTER(FieldDesc), C.c_uint64, P, P,
                                             C.POINTER(BoundsDesc), C.c_int, C.c_uint64,
                                             C.POINTER(Options), C.c_int, C.POINTER(Result)]
+    lib.ffcz_cuda_slab.argtypes = [P, P, C.POINTER(C.c_double)]
+    lib.ffcz_cuda_slab_pitch.argtypes = [C.c_uint64]
+    lib.ffcz_cuda_slab_pitch.restype = C.c_uint64
     lib.ffcz_cuda_result_free.argtypes = [C.POINTER(Result)]
     lib.ffcz_cuda_result_free.restype = None
     lib.ffcz_cuda_alternating_projection.argtypes = [

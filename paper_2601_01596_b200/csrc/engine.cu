@@ -1153,6 +1153,165 @@ int ffcz_cuda_correct_batch(ffcz_cuda_ctx* ctx, const ffcz_field_desc* frame, ui
     });
 }
 
+uint64_t ffcz_cuda_slab_pitch(uint64_t n2) { return round_up(n2 / 2 + 1, kPitchAlign); }
+
+// One per-rank device step of the slab-decomposed correction (paper_2601_01596_b200/slab.py).
+int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4]) {
+    return guarded(ctx, [&] {
+        if (!op) throw Error(kValidation, "null op");
+        ffcz_cuda_ctx& c = *ctx;
+        cudaStream_t st = c.st;
+        const uint64_t dims[3] = {op->d0, op->d1, op->n2};
+        const Geometry g = make_geometry(3, dims, kPitchAlign);
+        FftPlan<double> plan{g, &c.tw64};
+        const HalfGeom hg = g.hg();
+        const long long N = g.N, Nc = g.Nc();
+        const double invN = 1.0 / static_cast<double>(op->n_total);
+        const SpatialB sb{nullptr, op->e};
+        const FreqB fb{nullptr, nullptr, op->delta};
+        auto P = [&](int i) { return op->p[i]; };
+        auto d2 = [&](int i) { return static_cast<double2*>(op->p[i]); };
+        auto dd = [&](int i) { return static_cast<double*>(op->p[i]); };
+        auto ww = [&](int i) { return static_cast<unsigned*>(op->p[i]); };
+        double o4[4] = {0, 0, 0, 0};
+        auto reset_ctl = [&] { k_ctl_init<<<1, 1, 0, st>>>(c.ctl, 1); FFCZ_LAUNCH_CHECK(); };
+        const bool f32 = op->in_dtype == FFCZ_F32;
+        switch (op->op) {
+        case FFCZ_SLAB_EPS0: {
+            reset_ctl();
+            if (f32)
+                k_eps0<float><<<grid_for(N), 256, 0, st>>>(static_cast<const float*>(P(0)),
+                    static_cast<const float*>(P(1)), dd(2), N, sb, op->fscale, op->slack, 1, c.ctl);
+            else
+                k_eps0<double><<<grid_for(N), 256, 0, st>>>(static_cast<const double*>(P(0)),
+                    static_cast<const double*>(P(1)), dd(2), N, sb, op->fscale, op->slack, 1, c.ctl);
+            FFCZ_LAUNCH_CHECK();
+            const Ctl h = c.read_ctl();
+            o4[0] = h.bad1 == ~0ull ? -1.0 : static_cast<double>(h.bad1);
+            o4[1] = h.bad2 == ~0ull ? -1.0 : static_cast<double>(h.bad2);
+            break;
+        }
+        case FFCZ_SLAB_FWD_LOCAL:
+            launch_row_r2c<double>(g.n2, dd(0), g.n2, d2(1), g.P, g.rows, c.tw64, nullptr, st);
+            plan.col(1, -1, d2(1), d2(1), nullptr, HookNone{}, st);
+            break;
+        case FFCZ_SLAB_COL0_CHECK: {
+            reset_ctl();
+            plan.col(0, -1, d2(0), d2(0), nullptr, HookFReduce{fb, op->fscale, c.ctl}, st);
+            const Ctl h = c.read_ctl();
+            o4[0] = bitsd_host(h.peak_bits);
+            o4[1] = bitsd_host(h.exc_bits);
+            break;
+        }
+        case FFCZ_SLAB_COL0_CLIP_INV: {
+            HookFClip<double> hk{fb, op->fscale, d2(1), nullptr, static_cast<unsigned char*>(P(2))};
+            hk.first = op->first != 0;
+            plan.col(0, +1, d2(0), d2(0), nullptr, hk, st);
+            break;
+        }
+        case FFCZ_SLAB_COL0_PLAIN:
+            plan.col(0, op->dir < 0 ? -1 : +1, d2(0), d2(1), nullptr, HookNone{}, st);
+            break;
+        case FFCZ_SLAB_COL0_REBUILD:
+            plan.col(0, -1, d2(0), d2(0), nullptr,
+                     HookFRebuild{d2(1), d2(3), static_cast<const unsigned char*>(P(2))}, st);
+            break;
+        case FFCZ_SLAB_COL0_MARK: {
+            reset_ctl();
+            FFCZ_CUDA_CHECK(cudaMemsetAsync(P(1), 0, ((g.half_elems() + 31) / 32) * 4, st));
+            plan.col(0, -1, d2(0), d2(0), nullptr, HookMarkViol{fb, ww(1), c.ctl}, st);
+            o4[0] = c.read_ctl().dirty;
+            break;
+        }
+        case FFCZ_SLAB_COL0_VERIFY: {
+            reset_ctl();
+            plan.col(0, -1, d2(0), d2(0), nullptr, HookVerifyF{fb, c.ctl}, st);
+            o4[0] = bitsd_host(c.read_ctl().vf_bits);
+            break;
+        }
+        case FFCZ_SLAB_INV_SCLIP: {
+            plan.col(1, +1, d2(0), d2(0), nullptr, HookNone{}, st);
+            HookSClip<double> hk{sb, op->fscale, dd(2), nullptr, nullptr};
+            hk.first = op->first != 0;
+            launch_row_c2r_hook<double>(g.n2, d2(0), g.P, dd(1), g.n2, g.rows, invN, c.tw64,
+                                        nullptr, hk, st);
+            break;
+        }
+        case FFCZ_SLAB_INV_REPAIR_VERIFY:
+        case FFCZ_SLAB_INV_VERIFY: {
+            reset_ctl();
+            plan.col(1, +1, d2(0), d2(0), nullptr, HookNone{}, st);
+            auto run = [&](auto tag) {
+                using TI = decltype(tag);
+                const TI* o = static_cast<const TI*>(P(2));
+                const TI* d = static_cast<const TI*>(P(3));
+                if (op->op == FFCZ_SLAB_INV_REPAIR_VERIFY)
+                    launch_row_c2r_hook<double>(g.n2, d2(0), g.P, dd(1), g.n2, g.rows, invN, c.tw64,
+                        nullptr, HookRepairVerifyS<TI>{o, d, dd(4), dd(5), sb, ww(6), dd(7), dd(8),
+                                                       c.ctl}, st);
+                else
+                    launch_row_c2r_hook<double>(g.n2, d2(0), g.P, dd(1), g.n2, g.rows, invN, c.tw64,
+                        nullptr, HookVerifyS<TI>{o, d, dd(4), dd(5), sb, c.ctl}, st);
+            };
+            if (f32) run(float{}); else run(double{});
+            const Ctl h = c.read_ctl();
+            o4[0] = h.dirty;
+            o4[1] = bitsd_host(h.vs_bits);
+            break;
+        }
+        case FFCZ_SLAB_RESIDUAL_S: {
+            reset_ctl();
+            k_residual_s<<<grid_for(N), 256, 0, st>>>(dd(0), N, sb, op->fscale, c.ctl);
+            FFCZ_LAUNCH_CHECK();
+            o4[0] = bitsd_host(c.read_ctl().res_s_bits);
+            break;
+        }
+        case FFCZ_SLAB_EPS0_PLUS_S:
+            if (f32)
+                k_eps0_plus_s<float><<<grid_for(N), 256, 0, st>>>(static_cast<const float*>(P(0)),
+                    static_cast<const float*>(P(1)), dd(2), dd(3), N);
+            else
+                k_eps0_plus_s<double><<<grid_for(N), 256, 0, st>>>(static_cast<const double*>(P(0)),
+                    static_cast<const double*>(P(1)), dd(2), dd(3), N);
+            FFCZ_LAUNCH_CHECK();
+            break;
+        case FFCZ_SLAB_GATE: {
+            reset_ctl();
+            const long long ws = (N + 31) / 32, wf = (Nc + 31) / 32;
+            k_gate_spatial<<<grid_for(N), 256, 0, st>>>(dd(0), N, sb, op->m, dd(2), ww(4), ww(5), c.ctl);
+            k_gate_freq<<<grid_for(Nc), 256, 0, st>>>(d2(1), hg, fb, op->m, d2(3), ww(6), ww(7), c.ctl);
+            FFCZ_LAUNCH_CHECK();
+            auto codes = [&](const unsigned* words, long long nwords, const char* name,
+                             auto launch) {
+                const long long nblk = std::max<long long>(1, (nwords + 1023) / 1024);
+                unsigned long long* cnt = c.b<unsigned long long>(name, nblk + 1);
+                k_popc_blocks<<<static_cast<unsigned>(nblk), 1024, 0, st>>>(words, nwords, cnt);
+                k_scan_blocks<<<1, 1024, 0, st>>>(cnt, nblk, &c.ctl->count_a);
+                launch(static_cast<unsigned>(nblk), cnt);
+                FFCZ_LAUNCH_CHECK();
+                return c.read_ctl().count_a;
+            };
+            o4[2] = static_cast<double>(codes(ww(4), ws, "slab_cnt_s", [&](unsigned nb, unsigned long long* off) {
+                k_codes_spatial_bits<<<nb, 1024, 0, st>>>(ww(4), ws, off, dd(0), sb, op->m,
+                                                          static_cast<int*>(P(8)));
+            }));
+            o4[3] = static_cast<double>(codes(ww(6), wf, "slab_cnt_f", [&](unsigned nb, unsigned long long* off) {
+                k_codes_freq_bits<<<nb, 1024, 0, st>>>(ww(6), wf, off, d2(1), hg, fb, op->m,
+                                                       static_cast<int*>(P(9)));
+            }));
+            const Ctl h = c.read_ctl();
+            o4[0] = static_cast<double>(h.act_s);
+            o4[1] = static_cast<double>(h.act_f);
+            break;
+        }
+        default:
+            throw Error(kValidation, "unknown slab op " + std::to_string(op->op));
+        }
+        FFCZ_LAUNCH_CHECK();
+        if (out) std::memcpy(out, o4, sizeof(o4));
+    });
+}
+
 int ffcz_cuda_alternating_projection(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field,
                                      const void* eps0_in, const ffcz_bounds_desc* bw_desc,
                                      uint64_t max_iters, double precondition_slack,

@@ -144,8 +144,8 @@ struct HookFClip {
     // eps = eps0 + S + IFFT(F) (projection.cpp:117-124) makes that the same sum.
     unsigned char* moved = nullptr;
     bool first = false;
-    __device__ __forceinline__ void begin() {
-        first = ctl != nullptr && *reinterpret_cast<const volatile unsigned long long*>(&ctl->passes) == 1;
+    __device__ __forceinline__ void begin() {  // without ctl, `first` is the caller's value
+        if (ctl) first = *reinterpret_cast<const volatile unsigned long long*>(&ctl->passes) == 1;
     }
     static constexpr bool kDelta = true;
     template <class C> __device__ __forceinline__ void post_d(C&, long long, int, double2) {}
@@ -189,8 +189,8 @@ struct HookSClip {
     T* eps;
     const Ctl* ctl = nullptr;
     bool first = false;
-    __device__ __forceinline__ void begin() {
-        first = ctl != nullptr && *reinterpret_cast<const volatile unsigned long long*>(&ctl->passes) == 1;
+    __device__ __forceinline__ void begin() {  // without ctl, `first` is the caller's value
+        if (ctl) first = *reinterpret_cast<const volatile unsigned long long*>(&ctl->passes) == 1;
     }
     template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
     __device__ __forceinline__ T one(T x, long long n) const {

@@ -1,0 +1,373 @@
+"""Slab-decomposed correction of ONE volume across ranks (BASELINE configs 4/5).
+
+The reference's ``ffcz::correct`` (proj/core/src/pipeline.cpp:26-178) on a field split into
+slabs along axis 0: rank r holds planes i0 in [r*c0, (r+1)*c0).  The 3-D transform is
+separable, so every iteration of ``alternating_projection`` (projection.cpp:96-126) becomes
+
+    A (c0, n1, P) natural slab  --R2C rows, FFT axis 1 (local)-->  A
+    A --all-to-all #1-->  B (n0, c1, P): rank r holds i1 in [r*c1, (r+1)*c1), all i0
+    B --FFT axis 0 + check_convergence (local) + all-reduce(max) of (peak, excess)-->  decision
+    B --project_onto_fcube + inverse axis 0 (local)-->  B  --all-to-all #2-->  A
+    A --inverse axis 1, C2R, project_onto_scube (local)-->  eps
+
+so the frequency-domain state (F, the clip map, the converged spectrum delta_star) lives in the
+B layout and the spatial state (eps, S, spat_cur) in the natural slab.  The FP64 gate follows
+pipeline.cpp:46-176 in the same two layouts: quantisation and compaction on natural slabs (so
+each rank's flag bits / codes are a contiguous range of the global half-grid order), escape
+repair rounds with the frequency side in B; the conjugate partners of the k2 = 0 / n2/2 planes
+(pipeline.cpp:149-151) may live on another rank, so those few repairs are exchanged with one
+all-gather per round.
+
+The per-rank device work goes through a backend (``GpuSlabBackend`` = the B200 engine's slab
+C-ABI; the CPU test suite drives the same orchestration with a torch stand-in under gloo).  The
+collectives are torch.distributed (NCCL over NVLink on the box).  Every decision the reference
+makes is made identically on every rank from all-reduced values, so the control flow equals the
+single-volume path's.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+KMAX_ITER_TOL = 1e-11           # projection.cpp:40
+MAX_ESCAPE_ROUNDS = 32          # pipeline.cpp:15
+
+
+class Comm:
+    """The collectives the slab path needs, over torch.distributed (or a single process)."""
+
+    def __init__(self, group=None, stage_cpu: bool = False):
+        """stage_cpu: run the collectives on host copies (gloo) — lets several ranks share one
+        GPU in the tests; the product path uses NCCL on device tensors."""
+        import torch.distributed as dist
+        self.dist = dist
+        self.on = dist.is_available() and dist.is_initialized()
+        self.group = group
+        self.size = dist.get_world_size(group) if self.on else 1
+        self.rank = dist.get_rank(group) if self.on else 0
+        self.stage_cpu = stage_cpu
+
+    def all_to_all(self, out, inp):
+        if self.size == 1:
+            out.copy_(inp)
+            return
+        import torch
+        dst = out
+        if self.stage_cpu:
+            inp, out = inp.cpu(), torch.empty(out.shape, dtype=out.dtype)
+        if inp.is_complex():   # collectives move bytes: complex128 as (re, im) float64 pairs
+            self.dist.all_to_all_single(torch.view_as_real(out), torch.view_as_real(inp),
+                                        group=self.group)
+        else:
+            self.dist.all_to_all_single(out, inp, group=self.group)
+        if dst is not out:
+            dst.copy_(out)
+
+    def _reduce(self, t, op):
+        if self.size > 1:
+            if self.stage_cpu:
+                h = t.cpu()
+                self.dist.all_reduce(h, op=op, group=self.group)
+                t.copy_(h)
+            else:
+                self.dist.all_reduce(t, op=op, group=self.group)
+        return t
+
+    def max_f64(self, values, device):
+        import torch
+        t = torch.tensor(list(values), dtype=torch.float64, device=device)
+        return self._reduce(t, self.dist.ReduceOp.MAX).tolist()
+
+    def min_i64(self, values, device):
+        import torch
+        t = torch.tensor(list(values), dtype=torch.int64, device=device)
+        return self._reduce(t, self.dist.ReduceOp.MIN).tolist()
+
+    def sum_i64(self, values, device):
+        import torch
+        t = torch.tensor(list(values), dtype=torch.int64, device=device)
+        return self._reduce(t, self.dist.ReduceOp.SUM).tolist()
+
+    def all_gather_rows(self, t):
+        """Concatenate a (k_r, w) tensor of every rank (variable k_r) in rank order."""
+        import torch
+        if self.size == 1:
+            return t
+        if self.stage_cpu and t.device.type != "cpu":
+            return self.all_gather_rows(t.cpu()).to(t.device)
+        k = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+        ks = [torch.zeros_like(k) for _ in range(self.size)]
+        self.dist.all_gather(ks, k, group=self.group)
+        kmax = max(int(x.item()) for x in ks)
+        pad = torch.zeros((kmax,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        outs = [torch.zeros_like(pad) for _ in range(self.size)]
+        self.dist.all_gather(outs, pad, group=self.group)
+        return torch.cat([o[: int(kk.item())] for o, kk in zip(outs, ks)])
+
+
+@dataclass
+class SlabResult:
+    """This rank's part of ffcz::CorrectionResult (pipeline.hpp:11-16).  Flags and codes cover
+    the rank's contiguous range of the global order; escapes are global (every rank)."""
+    iterations: int
+    converged: bool
+    residual_f: float
+    residual_s: float
+    active_spatial: int
+    active_frequency: int
+    verify_ok: bool
+    verify_max_spatial_excess: float
+    verify_max_freq_excess: float
+    escape_rounds: int
+    spatial_flags: np.ndarray        # bool, this rank's c0*n1*n2 samples
+    frequency_flags: np.ndarray      # bool, this rank's c0*n1*H half-grid entries
+    spatial_codes: np.ndarray        # int32, ascending index order
+    frequency_codes: np.ndarray      # int32, interleaved (Re, Im)
+    escapes: list = field(default_factory=list)   # (is_freq, global index, re, im), map order
+    corrected: object = None         # this rank's FP64 corrected slab (backend tensor)
+
+
+def _transpose_ab(be, comm, A, n0, c0, c1):
+    """A (c0, n1, P) -> B (n0, c1, P): all-to-all #1."""
+    W = comm.size
+    send = A.view(c0, W, c1, A.shape[-1]).permute(1, 0, 2, 3).contiguous()
+    recv = be.empty_like(send)
+    comm.all_to_all(recv, send)
+    return recv.view(n0, c1, A.shape[-1])
+
+
+def _transpose_ba(be, comm, B, n1, c0, c1):
+    """B (n0, c1, P) -> A (c0, n1, P): all-to-all #2."""
+    W = comm.size
+    send = B.reshape(W, c0, c1, B.shape[-1])
+    recv = be.empty_like(send)
+    comm.all_to_all(recv, send)
+    return recv.permute(1, 0, 2, 3).reshape(c0, n1, B.shape[-1])
+
+
+def correct_slab(be, comm: Comm, dims, orig, dec, E: float, Delta: float, m: int = 16,
+                 max_iters: int = 1000) -> SlabResult:
+    """ffcz::correct (pipeline.cpp:26-178) of a volume slab-decomposed along axis 0 (see
+    _correct_slab); runs on the backend's stream when it has one."""
+    import contextlib
+    ctx = be.stream_context() if hasattr(be, "stream_context") else contextlib.nullcontext()
+    with ctx:
+        return _correct_slab(be, comm, dims, orig, dec, E, Delta, m, max_iters)
+
+
+def _correct_slab(be, comm: Comm, dims, orig, dec, E: float, Delta: float, m: int = 16,
+                  max_iters: int = 1000) -> SlabResult:
+    """ffcz::correct (pipeline.cpp:26-178) of a volume slab-decomposed along axis 0.
+
+    orig / dec: this rank's (c0, n1, n2) slab (backend tensors, f32 or f64); E, Delta: the
+    global DualBounds (bounds.hpp:11-47; per-point / per-component bounds are not supported
+    across ranks)."""
+    import torch
+    n0, n1, n2 = (int(v) for v in dims)
+    W, r = comm.size, comm.rank
+    if len(dims) != 3 or n0 % W or n1 % W:
+        raise ValueError("slab decomposition needs a 3-D field with n0, n1 divisible by ranks")
+    if not (E > 0.0 and np.isfinite(E)):
+        raise be.ValidationError("spatial bound E must be strictly positive and finite")
+    if not (Delta > 0.0 and np.isfinite(Delta)):
+        raise be.ValidationError("frequency bound Delta must be strictly positive and finite")
+    if m < 1 or m > 24:
+        raise be.ValidationError("shrink_bounds requires 1 <= m <= 24")
+    if max_iters < 1:
+        raise be.ValidationError("alternating_projection: max_iters must be >= 1")
+    c0, c1 = n0 // W, n1 // W
+    H = n2 // 2 + 1
+    N = n0 * n1 * n2
+    Ns = c0 * n1 * n2                       # samples of this slab
+    base_s = r * Ns                         # global flat index of the slab's first sample
+    fw = 1.0 - 2.0 ** -m                    # bounds.cpp:74-85
+    slack = 1.0 / (1.0 - 2.0 ** -m) - 1.0 + 2.0 ** -20
+    dev = be.device
+
+    # compute_error + preconditions (pipeline.cpp:31-42, projection.cpp:88-94)
+    eps = be.zeros_real((c0, n1, n2))
+    bad1, bad2 = be.eps0(orig, dec, E, fw, slack, eps)
+    big = np.iinfo(np.int64).max
+    g1, g2 = comm.min_i64([base_s + bad1 if bad1 >= 0 else big,
+                           base_s + bad2 if bad2 >= 0 else big], dev)
+    if g1 != big:
+        raise be.ValidationError("correct: decompressed data violates the declared spatial "
+                                 f"bound at index {g1}")
+    if g2 != big:
+        raise be.ValidationError("alternating_projection: epsilon0 violates the spatial bound "
+                                 f"at index {g2}")
+
+    # ---- alternating projection (projection.cpp:96-126) ----------------------------------
+    S = be.zeros_real((c0, n1, n2))
+    F_B = be.zeros_half((n0, c1))
+    moved_B = be.zeros_moved((n0, c1))
+    A = be.zeros_half((c0, n1))
+    be.fwd_local(eps, A, N)
+    passes, converged, residual_f = 0, False, 0.0
+    while True:
+        B = _transpose_ab(be, comm, A, n0, c0, c1)
+        peak, exc = be.col0_check(B, Delta * fw)            # FFT axis 0 + check (in place)
+        peak, exc = comm.max_f64([peak, exc], dev)
+        if not exc > KMAX_ITER_TOL * peak:                  # projection.cpp:106-111
+            converged = True
+            break
+        if passes >= max_iters:                             # :112-116
+            residual_f = exc
+            break
+        passes += 1
+        be.col0_clip_inv(B, Delta * fw, F_B, moved_B, passes == 1)   # :117-119, inverse axis 0
+        A = _transpose_ba(be, comm, B, n1, c0, c1)
+        be.inv_local_sclip(A, eps, N, E * fw, S, passes == 1)     # inverse axis 1, C2R, :121-124
+        be.fwd_local(eps, A, N)
+    delta_star = B                                          # FFT(final_eps), pipeline.cpp:114
+    residual_s = comm.max_f64([be.residual_s(eps, E, fw)], dev)[0]
+
+    # ---- FP64 gate (pipeline.cpp:46-176) ---------------------------------------------------
+    if passes >= 2:
+        # F = mask(delta_star - FFT(eps0 + S)) (the loop marked clipped components only)
+        X = be.zeros_real((c0, n1, n2))
+        be.eps0_plus_s(orig, dec, S, X)
+        A2 = be.zeros_half((c0, n1))
+        be.fwd_local(X, A2, N)
+        B2 = _transpose_ab(be, comm, A2, n0, c0, c1)
+        be.col0_rebuild(B2, delta_star, moved_B, F_B)
+        del X, A2, B2
+    F_A = _transpose_ba(be, comm, F_B, n1, c0, c1)
+    g = be.gate(S, F_A, E, Delta, m, base_h=r * c0 * n1 * H)
+    act_s, act_f = comm.sum_i64([g["act_s"], g["act_f"]], dev)
+    spat_cur = g["spat_cur"]
+    freq_cur_B = _transpose_ab(be, comm, g["freq_cur"], n0, c0, c1)
+    esc_s = g["esc_s"]                                     # bool (c0, n1, n2): spatial escapes
+    # frequency escapes as global half indices owned (in B) by this rank
+    ovf_h = comm.all_gather_rows(g["esc_f_h"].view(-1, 1)).view(-1)
+    esc_f_h = be.owned_b(ovf_h, n0, n1, H, r, c1)
+
+    rounds, verified = 0, False
+    vs = vf = 0.0
+    corrected = be.zeros_real((c0, n1, n2))
+    eps_v = be.zeros_real((c0, n1, n2))
+    eps_t = be.zeros_real((c0, n1, n2))
+
+    def inverse_to_spatial(fc_B):
+        Bw = be.empty_like(fc_B)
+        be.col0_plain(fc_B, Bw, +1)
+        return _transpose_ba(be, comm, Bw, n1, c0, c1)
+
+    def forward_to_b(x):
+        Aw = be.zeros_half((c0, n1))
+        be.fwd_local(x, Aw, N)
+        Bw = _transpose_ab(be, comm, Aw, n0, c0, c1)
+        return Bw
+
+    if converged:
+        for _ in range(MAX_ESCAPE_ROUNDS):                   # pipeline.cpp:116
+            rounds += 1
+            Aw = inverse_to_spatial(freq_cur_B)
+            dirty_s, vs_r = be.inv_local_repair_verify(Aw, eps_t, N, orig, dec, spat_cur, eps, E,
+                                                       esc_s, corrected, eps_v)
+            Bt = forward_to_b(eps_t)
+            viol = be.col0_mark(Bt, Delta)                  # FFT axis 0, |delta~| > Delta
+            pos = be.positions(viol)                        # B storage offsets, ascending
+            fixed_h = _repair_frequency(be, comm, pos, freq_cur_B, delta_star, Bt,
+                                        n0, n1, n2, c1, r)
+            esc_f_h = be.merge_sorted(esc_f_h, fixed_h)
+            dirty = comm.sum_i64([int(dirty_s) + int(pos.numel() > 0)], dev)[0]
+            if dirty == 0:                                  # :161, clean round
+                vs = comm.max_f64([vs_r], dev)[0]
+                Bv = forward_to_b(eps_v)
+                vf = comm.max_f64([be.col0_verify(Bv, Delta)], dev)[0]
+                verified = True
+                break
+    if not verified:
+        # apply_edits + verify_bounds on the decoder view (archive.cpp:262-297)
+        Aw = inverse_to_spatial(freq_cur_B)
+        vs_r = be.inv_local_verify(Aw, eps_v, N, orig, dec, spat_cur, E, corrected)
+        vs = comm.max_f64([vs_r], dev)[0]
+        Bv = forward_to_b(eps_v)
+        vf = comm.max_f64([be.col0_verify(Bv, Delta)], dev)[0]
+
+    # escapes in std::map order: spatial by index, then frequency by half index
+    sp_idx = be.nonzero_flat(esc_s)
+    sp = torch.stack([sp_idx.double() + base_s, be.take_real(spat_cur, sp_idx)], 1) \
+        if sp_idx.numel() else torch.zeros((0, 2), dtype=torch.float64, device=dev)
+    fr_vals = be.values_at_h(freq_cur_B, esc_f_h, n1, H, r, c1)
+    fr = torch.stack([esc_f_h.double(), fr_vals.real, fr_vals.imag], 1) \
+        if esc_f_h.numel() else torch.zeros((0, 3), dtype=torch.float64, device=dev)
+    sp_all = comm.all_gather_rows(sp).cpu().numpy()
+    fr_all = comm.all_gather_rows(fr).cpu().numpy()
+    fr_all = fr_all[np.argsort(fr_all[:, 0], kind="stable")]
+    escapes = [(False, int(i), float(v), 0.0) for i, v in sp_all]
+    escapes += [(True, int(h), float(a), float(b)) for h, a, b in fr_all]
+    return SlabResult(
+        iterations=max(passes, 1), converged=converged, residual_f=residual_f,
+        residual_s=residual_s, active_spatial=int(act_s), active_frequency=int(act_f),
+        verify_ok=(vs == 0.0 and vf == 0.0), verify_max_spatial_excess=vs,
+        verify_max_freq_excess=vf, escape_rounds=rounds,
+        spatial_flags=g["keep_s"], frequency_flags=g["keep_f"], spatial_codes=g["codes_s"],
+        frequency_codes=g["codes_f"], escapes=escapes, corrected=corrected)
+
+
+def _repair_frequency(be, comm, pos, freq_cur_B, delta_star, delta_tilde, n0, n1, n2, c1, r):
+    """Frequency side of one escape-repair round (pipeline.cpp:140-153) on the B layout.
+
+    Violating components are pinned to freq_cur + (delta_star - delta_tilde) (values of this
+    round's freq_cur).  Components on the k2 = 0 / n2/2 planes also set their conjugate partner
+    (-i0, -i1, k2); the reference visits half indices in ascending order, so when both partners
+    violate the larger index's repair wins.  Partners may be owned by another rank: the plane
+    repairs are all-gathered (they are few).  Returns the sorted global half indices this rank
+    repaired (escape set additions it owns)."""
+    import torch
+    H = n2 // 2 + 1
+    P = freq_cur_B.shape[-1]
+    i0 = torch.div(pos, c1 * P, rounding_mode="floor")
+    rem = pos - i0 * c1 * P
+    i1 = torch.div(rem, P, rounding_mode="floor") + r * c1
+    k2 = rem % P
+    h = (i0 * n1 + i1) * H + k2
+    flat_cur = freq_cur_B.view(-1)
+    rv = flat_cur[pos] + (delta_star.view(-1)[pos] - delta_tilde.view(-1)[pos])
+    plane = (k2 == 0) | (2 * k2 == n2)
+    mi0 = (n0 - i0) % n0
+    mi1 = (n1 - i1) % n1
+    hm = (mi0 * n1 + mi1) * H + k2
+    self_pair = plane & (hm == h)
+    # off-plane (and self-conjugate) components: local
+    loc = ~plane | self_pair
+    flat_cur[pos[loc]] = rv[loc]
+    fixed = [h[loc]]
+    # plane pairs: every rank sees every plane violation (h, re, im)
+    pl = ~loc
+    rows = torch.stack([h[pl].double(), rv[pl].real, rv[pl].imag], 1) if int(pl.sum()) else \
+        torch.zeros((0, 3), dtype=torch.float64, device=pos.device)
+    allp = comm.all_gather_rows(rows)
+    if allp.shape[0]:
+        ph = allp[:, 0].long()
+        pv = torch.complex(allp[:, 1], allp[:, 2])
+        pk2 = ph % H
+        prow = torch.div(ph, H, rounding_mode="floor")
+        pi0 = torch.div(prow, n1, rounding_mode="floor")
+        pi1 = prow % n1
+        pm = (((n0 - pi0) % n0) * n1 + (n1 - pi1) % n1) * H + pk2
+        viol_set = set(ph.tolist())
+        # winner per pair: the larger violating index (ascending visit order)
+        targets_h, targets_v = [], []
+        for a, b, v in zip(ph.tolist(), pm.tolist(), pv.tolist()):
+            if b in viol_set and b > a:
+                continue                     # the partner (larger) repair wins
+            targets_h += [a, b]
+            targets_v += [v, np.conj(v)]
+        th = torch.tensor(targets_h, dtype=torch.int64, device=pos.device)
+        tv = torch.tensor(targets_v, dtype=torch.complex128, device=pos.device)
+        # keep those owned (in B) by this rank
+        trow = torch.div(th, H, rounding_mode="floor")
+        ti0 = torch.div(trow, n1, rounding_mode="floor")
+        ti1 = trow % n1
+        tk2 = th % H
+        own = torch.div(ti1, c1, rounding_mode="floor") == r
+        off = (ti0 * c1 + (ti1 - r * c1)) * P + tk2
+        flat_cur[off[own]] = tv[own].to(flat_cur.dtype)
+        fixed.append(th[own])
+    out = torch.cat(fixed) if fixed else torch.zeros(0, dtype=torch.int64, device=pos.device)
+    return torch.unique(out)

@@ -1,0 +1,216 @@
+"""B200 backend of the slab-decomposed correction (paper_2601_01596_b200/slab.py): every per-rank
+device step is one ffcz_cuda_slab() call of the engine (include/ffcz_cuda.h) on CUDA torch
+tensors, on the context's stream (= torch's current stream, so the NCCL all-to-alls of the
+orchestrator are ordered with the passes).  No CPU fallback: without the built library or a GPU
+this raises."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _capi as capi
+from .ffcz import Context, ValidationError, _check
+
+
+class SlabOp(C.Structure):
+    _fields_ = [("op", C.c_int32), ("dir", C.c_int32), ("first", C.c_int32),
+                ("in_dtype", C.c_int32), ("m", C.c_int32), ("pad", C.c_int32),
+                ("d0", C.c_uint64), ("d1", C.c_uint64), ("n2", C.c_uint64),
+                ("n_total", C.c_uint64), ("e", C.c_double), ("delta", C.c_double),
+                ("fscale", C.c_double), ("slack", C.c_double), ("p", C.c_void_p * 10)]
+
+
+(EPS0, FWD_LOCAL, COL0_CHECK, COL0_CLIP_INV, COL0_PLAIN, COL0_REBUILD, COL0_MARK, COL0_VERIFY,
+ INV_SCLIP, INV_REPAIR_VERIFY, INV_VERIFY, RESIDUAL_S, EPS0_PLUS_S, GATE) = range(14)
+
+
+def _bits_to_bool(words, n):
+    """LSB-first uint32 bitmap (device tensor) -> numpy bool[n]."""
+    b = words.cpu().numpy().view(np.uint8)
+    return np.unpackbits(b, bitorder="little")[:n].astype(bool)
+
+
+class GpuSlabBackend:
+    ValidationError = ValidationError
+
+    def __init__(self, n2, device, ctx: Context | None = None):
+        import torch
+        self.torch = torch
+        self.n2 = int(n2)
+        self.H = self.n2 // 2 + 1
+        self.lib = capi.load()
+        self.P = int(self.lib.ffcz_cuda_slab_pitch(self.n2))
+        self.device = torch.device(device)
+        # one side stream for the engine AND the orchestrator's torch ops (transposes, sparse
+        # bookkeeping), so they are ordered with each other (stream 0 would make the engine
+        # create a private stream)
+        self.stream = torch.cuda.Stream(self.device)
+        self.ctx = ctx or Context(self.device.index or 0, self.stream.cuda_stream)
+
+    def stream_context(self):
+        """Enter the backend stream (ordered after the caller's current stream) for one call."""
+        import contextlib
+        torch = self.torch
+
+        @contextlib.contextmanager
+        def cm():
+            caller = torch.cuda.current_stream(self.device)
+            self.stream.wait_stream(caller)
+            with torch.cuda.stream(self.stream):
+                yield
+            caller.wait_stream(self.stream)
+        return cm()
+
+    # -- plumbing -----------------------------------------------------------------------------
+    def _op(self, code, shape, ptrs, **kw):
+        o = SlabOp()
+        o.op = code
+        o.d0, o.d1 = int(shape[0]), int(shape[1])
+        o.n2 = self.n2
+        for k, v in kw.items():
+            setattr(o, k, v)
+        for i, t in enumerate(ptrs):
+            o.p[i] = None if t is None else t.data_ptr()
+        out = (C.c_double * 4)()
+        _check(self.lib.ffcz_cuda_slab(self.ctx.handle, C.byref(o), out))
+        return list(out)
+
+    @staticmethod
+    def _dtype(t):
+        import torch
+        return capi.FFCZ_F32 if t.dtype == torch.float32 else capi.FFCZ_F64
+
+    def empty_like(self, t):
+        return self.torch.empty_like(t)
+
+    def zeros_real(self, shape):
+        return self.torch.zeros(shape, dtype=self.torch.float64, device=self.device)
+
+    def zeros_half(self, ab):
+        return self.torch.zeros(tuple(ab) + (self.P,), dtype=self.torch.complex128,
+                                device=self.device)
+
+    def zeros_moved(self, ab):
+        return self.torch.zeros(tuple(ab) + (self.P,), dtype=self.torch.uint8, device=self.device)
+
+    def _words(self, n):
+        return self.torch.zeros(((n + 31) // 32,), dtype=self.torch.int32, device=self.device)
+
+    # -- loop ---------------------------------------------------------------------------------
+    def eps0(self, orig, dec, E, fw, slack, eps_out):
+        o = self._op(EPS0, orig.shape, [orig, dec, eps_out], in_dtype=self._dtype(orig), e=E,
+                     fscale=fw, slack=slack)
+        return int(o[0]), int(o[1])
+
+    def fwd_local(self, x, A, N):
+        self._op(FWD_LOCAL, x.shape, [x, A])
+
+    def col0_check(self, B, Dw):
+        o = self._op(COL0_CHECK, B.shape, [B], delta=Dw, fscale=1.0)
+        return o[0], o[1]
+
+    def col0_clip_inv(self, B, Dw, F_B, moved_B, first):
+        self._op(COL0_CLIP_INV, B.shape, [B, F_B, moved_B], delta=Dw, fscale=1.0,
+                 first=int(bool(first)))
+
+    def inv_local_sclip(self, A, eps_out, N, Ew, S, first):
+        self._op(INV_SCLIP, A.shape, [A, eps_out, S], e=Ew, fscale=1.0, n_total=N,
+                 first=int(bool(first)))
+
+    def residual_s(self, eps, E, fw):
+        return self._op(RESIDUAL_S, eps.shape, [eps], e=E, fscale=fw)[0]
+
+    # -- gate ---------------------------------------------------------------------------------
+    def eps0_plus_s(self, orig, dec, S, X):
+        self._op(EPS0_PLUS_S, orig.shape, [orig, dec, S, X], in_dtype=self._dtype(orig))
+
+    def col0_rebuild(self, B2, delta_star, moved_B, F_B):
+        self._op(COL0_REBUILD, B2.shape, [B2, delta_star, moved_B, F_B])
+
+    def col0_plain(self, src, dst, d):
+        self._op(COL0_PLAIN, src.shape, [src, dst], dir=int(d))
+
+    def gate(self, S, F_A, E, D, m, base_h):
+        torch = self.torch
+        c0, n1, n2 = S.shape
+        N, Nc = c0 * n1 * n2, c0 * n1 * self.H
+        spat, freq = torch.empty_like(S), torch.empty_like(F_A)
+        ks, es, kf, ef = self._words(N), self._words(N), self._words(Nc), self._words(Nc)
+        cs = torch.empty((N,), dtype=torch.int32, device=self.device)
+        cf = torch.empty((2 * Nc,), dtype=torch.int32, device=self.device)
+        o = self._op(GATE, S.shape, [S, F_A, spat, freq, ks, es, kf, ef, cs, cf], e=E, delta=D,
+                     m=int(m))
+        ks_n, kf_n = int(o[2]), int(o[3])
+        esc_f = _bits_to_bool(ef, Nc)
+        return {"spat_cur": spat, "freq_cur": freq,
+                "keep_s": _bits_to_bool(ks, N), "keep_f": _bits_to_bool(kf, Nc),
+                "esc_s": es,
+                "esc_f_h": torch.from_numpy(np.flatnonzero(esc_f).astype(np.int64) + base_h)
+                .to(self.device),
+                "codes_s": cs[:ks_n].cpu().numpy(), "codes_f": cf[: 2 * kf_n].cpu().numpy(),
+                "act_s": int(o[0]), "act_f": int(o[1])}
+
+    def inv_local_repair_verify(self, Aw, eps_t, N, orig, dec, spat_cur, final_eps, E, esc_s,
+                                corrected, eps_v):
+        o = self._op(INV_REPAIR_VERIFY, Aw.shape,
+                     [Aw, eps_t, orig, dec, spat_cur, final_eps, esc_s, corrected, eps_v],
+                     in_dtype=self._dtype(orig), e=E, n_total=N)
+        return bool(o[0]), o[1]
+
+    def inv_local_verify(self, Aw, eps_v, N, orig, dec, spat_cur, E, corrected):
+        o = self._op(INV_VERIFY, Aw.shape, [Aw, eps_v, orig, dec, spat_cur, corrected],
+                     in_dtype=self._dtype(orig), e=E, n_total=N)
+        return o[1]
+
+    def col0_mark(self, Bt, D):
+        w = self._words(Bt.numel())
+        self._op(COL0_MARK, Bt.shape, [Bt, w], delta=D)
+        return w
+
+    def col0_verify(self, Bv, D):
+        return self._op(COL0_VERIFY, Bv.shape, [Bv], delta=D)[0]
+
+    # -- sparse bookkeeping (small index sets) -------------------------------------------------
+    def _bit_positions(self, words):
+        torch = self.torch
+        w = words.view(-1)
+        nz = torch.nonzero(w).view(-1)
+        if nz.numel() == 0:
+            return torch.zeros(0, dtype=torch.int64, device=self.device)
+        bits = (w[nz].to(torch.int64).unsqueeze(1) >> torch.arange(32, device=self.device)) & 1
+        r, b = torch.nonzero(bits, as_tuple=True)
+        return nz[r] * 32 + b
+
+    def positions(self, viol):
+        return self._bit_positions(viol)
+
+    def merge_sorted(self, a, b):
+        return self.torch.unique(self.torch.cat([a, b]))
+
+    def nonzero_flat(self, mask):
+        return self._bit_positions(mask)
+
+    def take_real(self, x, idx):
+        return x.reshape(-1)[idx]
+
+    def owned_b(self, h, n0, n1, H, r, c1):
+        torch = self.torch
+        i1 = torch.div(h, H, rounding_mode="floor") % n1
+        return torch.unique(h[torch.div(i1, c1, rounding_mode="floor") == r])
+
+    def values_at_h(self, B, h, n1, H, r, c1):
+        torch = self.torch
+        row = torch.div(h, H, rounding_mode="floor")
+        i0, i1, k2 = torch.div(row, n1, rounding_mode="floor"), row % n1, h % H
+        off = (i0 * c1 + (i1 - r * c1)) * B.shape[-1] + k2
+        return B.reshape(-1)[off]
+
+
+def correct_slab_gpu(orig_slab, dec_slab, dims, E, Delta, m=16, max_iters=1000, group=None,
+                     ctx: Context | None = None):
+    """ffcz::correct of a volume slab-decomposed along axis 0 across the ranks of `group`
+    (torch.distributed, NCCL): this rank passes its (n0/W, n1, n2) CUDA slab of both fields."""
+    from .slab import Comm, correct_slab
+    be = GpuSlabBackend(dims[2], orig_slab.device, ctx)
+    return correct_slab(be, Comm(group), dims, orig_slab, dec_slab, E, Delta, m, max_iters)

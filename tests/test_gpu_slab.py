@@ -1,0 +1,113 @@
+"""Slab-decomposed correction on the B200 engine (GpuSlabBackend, ffcz_cuda_slab): at world 1 it
+must reproduce the single-volume engine path and the oracle; at world 2 (two ranks sharing the
+GPU, collectives staged through gloo) it must agree with world 1 exactly as the CPU stand-in
+does (tests/test_slab_dist.py)."""
+import os
+import pickle
+import socket
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+import cases
+from oracle import ffcz_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def field(n, seed, c):
+    o = cases.combustion(n, seed)
+    E = 0.1 / 100.0 * cases.value_range(o)
+    d = cases.uniform_perturb(o, E, seed + 1)
+    return o, d, E, c * cases.mean_abs_delta0(o, d)
+
+
+def _worker(rank, world, port, n, seed, c, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if root not in sys.path:
+        sys.path.insert(0, root)
+    import torch
+    import torch.distributed as dist
+    from paper_2601_01596_b200 import slab
+    from paper_2601_01596_b200.slab_gpu import GpuSlabBackend
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        o, d, E, D = field(n, seed, c)
+        c0 = n // world
+        sl = slice(rank * c0, (rank + 1) * c0)
+        to = torch.from_numpy(o[sl].astype(np.float32)).cuda()
+        td = torch.from_numpy(d[sl].astype(np.float32)).cuda()
+        be = GpuSlabBackend(n, to.device)
+        res = slab.correct_slab(be, slab.Comm(stage_cpu=True), (n, n, n), to, td, E, D)
+        torch.cuda.synchronize()
+        res.corrected = res.corrected.cpu().numpy()
+        with open(os.path.join(out_dir, f"r{rank}.pkl"), "wb") as f:
+            pickle.dump(res, f)
+        be.ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def run_world(world, n, seed, c):
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as tmp:
+        mp.spawn(_worker, args=(world, _free_port(), n, seed, c, tmp), nprocs=world, join=True)
+        return [pickle.load(open(os.path.join(tmp, f"r{r}.pkl"), "rb")) for r in range(world)]
+
+
+def cat(parts, k):
+    return np.concatenate([getattr(p, k) for p in parts])
+
+
+@pytest.mark.parametrize("n,c", [(32, 0.6), (32, 1.0), (64, 0.6)])
+def test_slab_gpu_world1_matches_engine_and_oracle(n, c):
+    import torch
+    import paper_2601_01596_b200 as P
+    from paper_2601_01596_b200.slab_gpu import correct_slab_gpu
+    o, d, E, D = field(n, 5, c)
+    to = torch.from_numpy(o.astype(np.float32)).cuda()
+    td = torch.from_numpy(d.astype(np.float32)).cuda()
+    res = correct_slab_gpu(to, td, (n, n, n), E, D)
+    ref = O.correct(o, d, O.DualBounds(E, D), 16, 1000, "f32")
+    eng = P.correct(o.astype(np.float32), d.astype(np.float32), P.DualBounds(E, D), 16, 1000,
+                    "f32")
+    for r in (ref.report, eng.report):
+        assert res.iterations == r.iterations
+        assert res.converged == r.converged
+        assert res.active_spatial == r.active_spatial
+        assert res.active_frequency == r.active_frequency
+    assert res.verify_ok and eng.verify_ok
+    arch = O.read_archive(eng.archive_bytes)
+    assert np.array_equal(res.spatial_flags, arch.spatial_flags.ravel())
+    assert np.array_equal(res.frequency_flags, arch.frequency_flags.ravel())
+    assert np.mean(res.frequency_codes == arch.frequency_codes) >= 0.999
+    ok, ms, mf = O.verify_bounds(o, res.corrected.cpu().numpy(), O.DualBounds(E, D))
+    assert ms == 0.0 and mf <= 1e-12 * D
+    assert abs(len(res.escapes) - eng.escape_count) <= max(2, eng.escape_count // 10)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_slab_gpu_worlds_agree(world):
+    n, seed, c = 32, 7, 0.7
+    a, b = run_world(1, n, seed, c), run_world(world, n, seed, c)
+    for k in ("iterations", "converged", "active_spatial", "active_frequency", "verify_ok",
+              "escape_rounds"):
+        assert getattr(a[0], k) == getattr(b[0], k), k
+    for k in ("spatial_flags", "frequency_flags", "spatial_codes", "frequency_codes"):
+        assert np.array_equal(cat(a, k), cat(b, k)), k
+    assert [e[:2] for e in a[0].escapes] == [e[:2] for e in b[0].escapes]
+    ca, cb = cat(a, "corrected"), cat(b, "corrected")
+    np.testing.assert_allclose(ca, cb, rtol=0, atol=1e-12 * np.abs(ca).max())
