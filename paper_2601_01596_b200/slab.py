@@ -121,10 +121,10 @@ class SlabResult:
     verify_max_spatial_excess: float
     verify_max_freq_excess: float
     escape_rounds: int
-    spatial_flags: np.ndarray        # bool, this rank's c0*n1*n2 samples
-    frequency_flags: np.ndarray      # bool, this rank's c0*n1*H half-grid entries
-    spatial_codes: np.ndarray        # int32, ascending index order
-    frequency_codes: np.ndarray      # int32, interleaved (Re, Im)
+    spatial_flags: object            # this rank's c0*n1*n2 flags (backend form: bool / bitmap)
+    frequency_flags: object          # this rank's c0*n1*H half-grid flags
+    spatial_codes: object            # int32, ascending index order (backend tensor / array)
+    frequency_codes: object          # int32, interleaved (Re, Im)
     escapes: list = field(default_factory=list)   # (is_freq, global index, re, im), map order
     corrected: object = None         # this rank's FP64 corrected slab (backend tensor)
 
@@ -132,6 +132,8 @@ class SlabResult:
 def _transpose_ab(be, comm, A, n0, c0, c1):
     """A (c0, n1, P) -> B (n0, c1, P): all-to-all #1."""
     W = comm.size
+    if W == 1:
+        return A.view(n0, c1, A.shape[-1])   # the slab is the whole volume: B is A
     send = A.view(c0, W, c1, A.shape[-1]).permute(1, 0, 2, 3).contiguous()
     recv = be.empty_like(send)
     comm.all_to_all(recv, send)
@@ -141,6 +143,8 @@ def _transpose_ab(be, comm, A, n0, c0, c1):
 def _transpose_ba(be, comm, B, n1, c0, c1):
     """B (n0, c1, P) -> A (c0, n1, P): all-to-all #2."""
     W = comm.size
+    if W == 1:
+        return B.view(c0, n1, B.shape[-1])
     send = B.reshape(W, c0, c1, B.shape[-1])
     recv = be.empty_like(send)
     comm.all_to_all(recv, send)

@@ -142,14 +142,15 @@ class GpuSlabBackend:
         o = self._op(GATE, S.shape, [S, F_A, spat, freq, ks, es, kf, ef, cs, cf], e=E, delta=D,
                      m=int(m))
         ks_n, kf_n = int(o[2]), int(o[3])
-        esc_f = _bits_to_bool(ef, Nc)
-        return {"spat_cur": spat, "freq_cur": freq,
-                "keep_s": _bits_to_bool(ks, N), "keep_f": _bits_to_bool(kf, Nc),
-                "esc_s": es,
-                "esc_f_h": torch.from_numpy(np.flatnonzero(esc_f).astype(np.int64) + base_h)
-                .to(self.device),
-                "codes_s": cs[:ks_n].cpu().numpy(), "codes_f": cf[: 2 * kf_n].cpu().numpy(),
+        # flags stay LSB-first bitmaps and codes stay on the device (flags_to_bool for checks)
+        return {"spat_cur": spat, "freq_cur": freq, "keep_s": ks, "keep_f": kf, "esc_s": es,
+                "esc_f_h": self._bit_positions(ef) + base_h,
+                "codes_s": cs[:ks_n], "codes_f": cf[: 2 * kf_n],
                 "act_s": int(o[0]), "act_f": int(o[1])}
+
+    @staticmethod
+    def flags_to_bool(words, n):
+        return _bits_to_bool(words, n)
 
     def inv_local_repair_verify(self, Aw, eps_t, N, orig, dec, spat_cur, final_eps, E, esc_s,
                                 corrected, eps_v):

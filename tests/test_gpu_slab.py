@@ -54,11 +54,22 @@ def _worker(rank, world, port, n, seed, c, out_dir):
         res = slab.correct_slab(be, slab.Comm(stage_cpu=True), (n, n, n), to, td, E, D)
         torch.cuda.synchronize()
         res.corrected = res.corrected.cpu().numpy()
+        _to_host(res, n)
         with open(os.path.join(out_dir, f"r{rank}.pkl"), "wb") as f:
             pickle.dump(res, f)
         be.ctx.close()
     finally:
         dist.destroy_process_group()
+
+
+def _to_host(res, n):
+    from paper_2601_01596_b200.slab_gpu import GpuSlabBackend
+    ns = res.corrected.size if hasattr(res.corrected, "size") else res.corrected.numel()
+    H = n // 2 + 1
+    res.spatial_flags = GpuSlabBackend.flags_to_bool(res.spatial_flags, ns)
+    res.frequency_flags = GpuSlabBackend.flags_to_bool(res.frequency_flags, ns // n * H)
+    res.spatial_codes = res.spatial_codes.cpu().numpy()
+    res.frequency_codes = res.frequency_codes.cpu().numpy()
 
 
 def run_world(world, n, seed, c):
@@ -81,6 +92,8 @@ def test_slab_gpu_world1_matches_engine_and_oracle(n, c):
     to = torch.from_numpy(o.astype(np.float32)).cuda()
     td = torch.from_numpy(d.astype(np.float32)).cuda()
     res = correct_slab_gpu(to, td, (n, n, n), E, D)
+    res.corrected = res.corrected.cpu().numpy()
+    _to_host(res, n)
     ref = O.correct(o, d, O.DualBounds(E, D), 16, 1000, "f32")
     eng = P.correct(o.astype(np.float32), d.astype(np.float32), P.DualBounds(E, D), 16, 1000,
                     "f32")
@@ -94,7 +107,7 @@ def test_slab_gpu_world1_matches_engine_and_oracle(n, c):
     assert np.array_equal(res.spatial_flags, arch.spatial_flags.ravel())
     assert np.array_equal(res.frequency_flags, arch.frequency_flags.ravel())
     assert np.mean(res.frequency_codes == arch.frequency_codes) >= 0.999
-    ok, ms, mf = O.verify_bounds(o, res.corrected.cpu().numpy(), O.DualBounds(E, D))
+    ok, ms, mf = O.verify_bounds(o, res.corrected, O.DualBounds(E, D))
     assert ms == 0.0 and mf <= 1e-12 * D
     assert abs(len(res.escapes) - eng.escape_count) <= max(2, eng.escape_count // 10)
 
