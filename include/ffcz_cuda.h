@@ -86,6 +86,8 @@ typedef enum ffcz_cuda_policy { FFCZ_POLICY_FP64 = 0, FFCZ_POLICY_MIXED = 1 } ff
 #define FFCZ_WANT_EDITS (1u << 2)       /* copy flags, int32 codes and escapes to the host      */
 #define FFCZ_WANT_CORRECTED (1u << 3)   /* copy the FP64 corrected field to the host            */
 #define FFCZ_FORCE_UNFUSED (1u << 4)    /* use the per-op (unfused) loop even for 2^k shapes    */
+#define FFCZ_DEVICE_ENCODE (1u << 5)    /* archive: zigzag + canonical Huffman on the device (same
+                                           payload bytes as huffman.cpp); zlib_level 0 = stored  */
 
 typedef struct ffcz_cuda_options {
     uint32_t flags;
@@ -268,6 +270,11 @@ int ffcz_cuda_profile_read(ffcz_cuda_ctx* ctx, ffcz_cuda_kernel_stat* out, int m
  * `reps` launches each (tools/passbench.py, profiles/). */
 int ffcz_cuda_bench_passes(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, int reps,
                            ffcz_cuda_kernel_stat* out, int max, int* n);
+
+/* Device Huffman encoder on host codes (test hook): writes the huffman::encode payload
+ * (huffman.cpp:156-251) of zigzag(codes[0..n)) into out (capacity cap); *len = its length. */
+int ffcz_cuda_huffman_encode(ffcz_cuda_ctx* ctx, const int32_t* codes, uint64_t n, uint8_t* out,
+                             uint64_t cap, uint64_t* len);
 
 /* CRC-32C (archive.cpp:61-71), exported for the format tests. */
 uint32_t ffcz_cuda_crc32c(const uint8_t* data, size_t len);

@@ -29,6 +29,7 @@ FFCZ_INPUTS_ON_DEVICE = 1 << 0
 FFCZ_WANT_ARCHIVE = 1 << 1
 FFCZ_WANT_EDITS = 1 << 2
 FFCZ_WANT_CORRECTED = 1 << 3
+FFCZ_DEVICE_ENCODE = 1 << 5
 FFCZ_FORCE_UNFUSED = 1 << 4
 
 # every symbol include/ffcz_cuda.h declares
@@ -39,7 +40,7 @@ EXPORTS = [
     "ffcz_cuda_alternating_projection", "ffcz_cuda_forward_dft", "ffcz_cuda_inverse_dft",
     "ffcz_cuda_r2c_device", "ffcz_cuda_c2r_device", "ffcz_cuda_crc32c",
     "ffcz_cuda_profile_enable", "ffcz_cuda_profile_read", "ffcz_cuda_bench_passes",
-    "ffcz_cuda_slab", "ffcz_cuda_slab_pitch",
+    "ffcz_cuda_slab", "ffcz_cuda_slab_pitch", "ffcz_cuda_huffman_encode",
 ]
 
 
@@ -118,6 +119,8 @@ def load():
                                             C.POINTER(BoundsDesc), C.c_int, C.c_uint64,
                                             C.POINTER(Options), C.c_int, C.POINTER(Result)]
     lib.ffcz_cuda_slab.argtypes = [P, P, C.POINTER(C.c_double)]
+    lib.ffcz_cuda_huffman_encode.argtypes = [P, P, C.c_uint64, P, C.c_uint64,
+                                             C.POINTER(C.c_uint64)]
     lib.ffcz_cuda_slab_pitch.argtypes = [C.c_uint64]
     lib.ffcz_cuda_slab_pitch.restype = C.c_uint64
     lib.ffcz_cuda_result_free.argtypes = [C.POINTER(Result)]

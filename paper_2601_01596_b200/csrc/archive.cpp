@@ -193,8 +193,12 @@ std::vector<std::uint8_t> write_archive(const ArchiveInput& in) {
     };
     const auto sf = outer_compress(in.spatial_flags, in.spatial_flag_bytes, in.zlib_level);
     const auto ff = outer_compress(in.frequency_flags, in.frequency_flag_bytes, in.zlib_level);
-    const auto si = index_stream(in.spatial_codes, in.n_spatial);
-    const auto fi = index_stream(in.frequency_codes, 2 * in.n_frequency);
+    const auto si = in.spatial_payload
+                        ? outer_compress(in.spatial_payload, in.spatial_payload_len, in.zlib_level)
+                        : index_stream(in.spatial_codes, in.n_spatial);
+    const auto fi = in.frequency_payload
+                        ? outer_compress(in.frequency_payload, in.frequency_payload_len, in.zlib_level)
+                        : index_stream(in.frequency_codes, 2 * in.n_frequency);
 
     std::vector<std::uint8_t> w;
     w.reserve(128 + 8 * (in.spatial_per_point ? N : 1) + 16 * (in.freq_per_component ? N : 1) +

@@ -33,6 +33,9 @@ struct ArchiveInput {
     const EscapeRec* escapes;
     std::uint64_t n_escapes;
     int zlib_level;
+    // pre-encoded Huffman payloads (device encoder); when set, the codes above are not read
+    const std::uint8_t* spatial_payload = nullptr;   std::uint64_t spatial_payload_len = 0;
+    const std::uint8_t* frequency_payload = nullptr; std::uint64_t frequency_payload_len = 0;
 };
 
 std::uint32_t crc32c(const std::uint8_t* data, std::size_t len);

@@ -22,6 +22,7 @@
 
 #include "../../include/ffcz_cuda.h"
 #include "archive.hpp"
+#include "encode.cuh"
 #include "fft_plan.cuh"
 #include "kernels.cuh"
 
@@ -929,6 +930,24 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
         ai.n_escapes = er.size();
         ai.zlib_level = opt.zlib_level;
         const auto t0 = std::chrono::steady_clock::now();
+        std::vector<uint8_t> sp, fp;
+        if (opt.flags & FFCZ_DEVICE_ENCODE) {
+            // Huffman payloads on the device from the resident codes; host does the outer stage
+            DevScratch ds{st, [&](const char* nm, size_t b) { return c.buf(nm, b); }};
+            auto enc = [&](const int* dcodes, unsigned long long n, std::vector<uint8_t>& dst) {
+                unsigned char* dp = nullptr;
+                const unsigned long long len = huffman_encode_device(ds, dcodes, n, &dp);
+                dst.resize(len);
+                FFCZ_CUDA_CHECK(cudaMemcpyAsync(dst.data(), dp, len, cudaMemcpyDeviceToHost, st));
+                c.sync();
+            };
+            enc(c.b<int>("codes_s", N), go.n_keep_s, sp);
+            enc(c.b<int>("codes_f", 2 * g.Nc()), 2 * go.n_keep_f, fp);
+            ai.spatial_payload = sp.data();
+            ai.spatial_payload_len = sp.size();
+            ai.frequency_payload = fp.data();
+            ai.frequency_payload_len = fp.size();
+        }
         std::vector<uint8_t> bytes = ffcz_host::write_archive(ai);
         out->t_archive_ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1467,6 +1486,24 @@ int ffcz_cuda_c2r_device(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const
 }
 
 uint32_t ffcz_cuda_crc32c(const uint8_t* data, size_t len) { return ffcz_host::crc32c(data, len); }
+
+int ffcz_cuda_huffman_encode(ffcz_cuda_ctx* ctx, const int32_t* codes, uint64_t n, uint8_t* out,
+                             uint64_t cap, uint64_t* len) {
+    return guarded(ctx, [&] {
+        if ((!codes && n) || !len) throw Error(kValidation, "null argument");
+        ffcz_cuda_ctx& c = *ctx;
+        int* d = c.b<int>("he_codes", std::max<uint64_t>(n, 1));
+        if (n) FFCZ_CUDA_CHECK(cudaMemcpyAsync(d, codes, 4 * n, cudaMemcpyHostToDevice, c.st));
+        DevScratch ds{c.st, [&](const char* nm, size_t b) { return c.buf(nm, b); }};
+        unsigned char* dp = nullptr;
+        const unsigned long long l = huffman_encode_device(ds, d, n, &dp);
+        *len = l;
+        if (out && cap >= l)
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(out, dp, l, cudaMemcpyDeviceToHost, c.st));
+        c.sync();
+        if (out && cap < l) throw Error(kValidation, "output buffer too small");
+    });
+}
 
 int ffcz_cuda_profile_enable(ffcz_cuda_ctx* ctx, int enable) {
     return guarded(ctx, [&] {

@@ -131,26 +131,34 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
         if (const char* e = std::getenv("FFCZ_COL_TMA_B")) Bt = std::max(1, std::atoi(e));
         Bt = std::min(Bt, pow2_ceil(ncols));
         if constexpr (L >= 512) {
-            // single landing buffer + scalar exchange when double buffering cannot reach 128-B
-            // row segments (k_col_tma1); FFCZ_COL_TMA1=0 disables, =1 forces it where it fits
+            // single landing buffer + scalar exchange (k_col_tma1) where it gives wider row
+            // segments than double buffering: always when double buffering falls below 128 B,
+            // and on the outer axis (row stride > plane stride) whenever it is wider — outer-axis
+            // passes measured 0.38-0.48 of HBM at 64-B rows, 0.53-0.69 at 128 B, 0.87 at 256 B.
+            // FP64 L = 512 runs it at E = 16 (same stage count as E = 8, half the threads per
+            // column) so a 16-column (256-B) tile fits 512 threads.  FFCZ_COL_TMA1=0 disables,
+            // =1 forces it where it fits.
+            constexpr int E1 = (sizeof(T) == 8 && L == 512) ? 16 : E;
+            constexpr int TT1 = L / E1;
             constexpr int NT1 = 512;
             const int mode = tma1_mode();
-            int B1 = std::min(NT1 / TT, 128);
-            while (B1 > 1 && col_tma1_smem_bytes<T, L, E>(B1) > 220 * 1024) B1 /= 2;
+            int B1 = std::min(NT1 / TT1, 128);
+            while (B1 > 1 && col_tma1_smem_bytes<T, L, E1>(B1) > 220 * 1024) B1 /= 2;
             B1 = std::min(B1, pow2_ceil(ncols));
-            const bool want = !side && mode != 0 && TT * B1 >= 32 &&
-                              (mode == 1 || (B1 > Bt && Bt * sizeof(cplx<T>) < 128));
+            const bool outer = sizeof(T) == 8 && role == TileRole::kFirst;
+            const bool want = !side && mode != 0 && TT1 * B1 >= 32 &&
+                              (mode == 1 || (B1 > Bt && (Bt * sizeof(cplx<T>) < 128 || outer)));
             CUtensorMap map1;
             if (want && encode_col_map(&map1, src, sizeof(T), ncols, L, row_stride, nplanes,
                                        plane_stride, B1, L < 256 ? L : 256, true)) {
-                auto kt = dir < 0 ? k_col_tma1<T, L, E, -1, Hook, NT1>
-                                  : k_col_tma1<T, L, E, +1, Hook, NT1>;
-                const size_t sm1 = col_tma1_smem_bytes<T, L, E>(B1);
+                auto kt = dir < 0 ? k_col_tma1<T, L, E1, -1, Hook, NT1>
+                                  : k_col_tma1<T, L, E1, +1, Hook, NT1>;
+                const size_t sm1 = col_tma1_smem_bytes<T, L, E1>(B1);
                 set_smem(kt, sm1);
                 const long long nt = static_cast<long long>((ncols + B1 - 1) / B1) * nplanes;
-                const unsigned grid = persistent_grid(kt, TT * B1, sm1, nt);
-                kt<<<grid, TT * B1, sm1, st>>>(map1, dst, row_stride, plane_stride, ncols, B1, nt,
-                                               tw.stage_table(L, E), gate, hook);
+                const unsigned grid = persistent_grid(kt, TT1 * B1, sm1, nt);
+                kt<<<grid, TT1 * B1, sm1, st>>>(map1, dst, row_stride, plane_stride, ncols, B1, nt,
+                                                tw.stage_table(L, E1), gate, hook);
                 FFCZ_LAUNCH_CHECK();
                 return;
             }

@@ -222,7 +222,8 @@ def _bounds_desc(b: DualBounds, m: _Marshal):
     return bd
 
 
-def _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level):
+def _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level,
+             device_encode=False):
     lib = capi.load()
     opt = capi.Options()
     lib.ffcz_cuda_default_options(C.byref(opt))
@@ -237,6 +238,8 @@ def _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level
         flags |= capi.FFCZ_WANT_CORRECTED
     if not fused:
         flags |= capi.FFCZ_FORCE_UNFUSED
+    if device_encode:
+        flags |= capi.FFCZ_DEVICE_ENCODE
     opt.flags = flags
     opt.zlib_level = zlib_level
     return opt
@@ -279,7 +282,10 @@ def _convert(holder, shape, want_archive, want_edits, want_corrected, copy):
         corrected = np.ctypeslib.as_array(res.corrected, shape=(N,)).reshape(shape)
         if copy:
             corrected = corrected.copy()
-    data = C.string_at(res.archive, res.archive_len) if want_archive else None
+    data = None
+    if want_archive:   # (C.string_at takes an int size: archives can exceed 2 GiB)
+        data = np.ctypeslib.as_array(res.archive, shape=(int(res.archive_len),)).tobytes() \
+            if res.archive_len else b""
     timings = {k: float(getattr(res, k)) for k in ("t_feasible_ms", "t_loop_ms", "t_gate_ms",
                                                    "t_h2d_ms", "t_d2h_ms", "t_archive_ms")}
     out = CorrectionResult(data, rep, int(res.escape_count), bool(res.verify_ok),
@@ -312,13 +318,16 @@ def _field_of(original, decompressed):
 def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: int = 1000,
             precision: str | None = None, *, want_archive: bool = True, want_edits: bool = True,
             want_corrected: bool = True, zlib_level: int = 9, fused: bool = True,
-            copy: bool = True, ctx: Context | None = None) -> CorrectionResult:
+            copy: bool = True, device_encode: bool = False,
+            ctx: Context | None = None) -> CorrectionResult:
     """ffcz::correct (pipeline.cpp:26-178) on the GPU.
 
     original / decompressed: numpy arrays (host; float32 or float64) or CUDA torch tensors (then
     every bound array must be a CUDA tensor too).  precision: the ScalarField precision tag
     written into the archive ("f32" / "f64"; default from the input dtype).  copy=False returns
     views of the library's pinned result buffers, valid while the returned object is alive.
+    device_encode: zigzag + canonical Huffman of the archive's index streams on the GPU (same
+    payload bytes as huffman.cpp); zlib_level then sets the host outer stage (0 = stored).
     """
     ctx = ctx or default_context()
     lib = capi.load()
@@ -329,7 +338,8 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
     mar = _Marshal()
     fd = _field_desc(shape, capi.FFCZ_F32 if is32 else capi.FFCZ_F64, precision)
     bd = _bounds_desc(bounds, mar)
-    opt = _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level)
+    opt = _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level,
+                   device_encode)
     holder = _ResultHolder()
     rc = lib.ffcz_cuda_correct(ctx.handle, C.byref(fd), mar.ptr(original, dt),
                                mar.ptr(decompressed, dt), C.byref(bd), int(m), int(max_iters),
@@ -455,3 +465,18 @@ def c2r_device(half, x, *, ctx: Context | None = None):
                      "f64")
     _check(capi.load().ffcz_cuda_c2r_device(ctx.handle, C.byref(fd), C.c_void_p(half.data_ptr()),
                                             C.c_void_p(x.data_ptr())))
+
+
+def huffman_encode_device(codes, *, ctx: Context | None = None) -> bytes:
+    """The device Huffman encoder on int32 codes (test hook): huffman::encode's payload of
+    zigzag(codes) (huffman.cpp:156-251, streams.cpp:13-15)."""
+    ctx = ctx or default_context()
+    lib = capi.load()
+    c = np.ascontiguousarray(codes, dtype=np.int32)
+    n = C.c_uint64()
+    _check(lib.ffcz_cuda_huffman_encode(ctx.handle, C.c_void_p(c.ctypes.data), c.size, None, 0,
+                                        C.byref(n)))
+    out = np.zeros(max(1, n.value), dtype=np.uint8)
+    _check(lib.ffcz_cuda_huffman_encode(ctx.handle, C.c_void_p(c.ctypes.data), c.size,
+                                        C.c_void_p(out.ctypes.data), n.value, C.byref(n)))
+    return out[: n.value].tobytes()
