@@ -271,6 +271,16 @@ int ffcz_cuda_profile_read(ffcz_cuda_ctx* ctx, ffcz_cuda_kernel_stat* out, int m
 int ffcz_cuda_bench_passes(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, int reps,
                            ffcz_cuda_kernel_stat* out, int max, int* n);
 
+/* Replaces ffcz::apply_edits(decompressed, ffcz::read_archive(bytes)) (archive.cpp:137-273):
+ * corrected = decompressed + spatial edits + Re(IFFT(frequency edits)) in FP64.  The host parses
+ * the container (header, CRC-32C, zlib stages: FFCZ_FORMAT_ERROR on a corrupt archive); the
+ * Huffman index streams are decoded, dequantised and scattered on the device.  `field` gives the
+ * decompressed field's dims (must match the archive) and dtype; with FFCZ_INPUTS_ON_DEVICE in
+ * `flags`, decompressed and corrected (N doubles) are device pointers, else host. */
+int ffcz_cuda_apply_archive(ffcz_cuda_ctx* ctx, const uint8_t* archive, uint64_t len,
+                            const ffcz_field_desc* field, const void* decompressed, uint32_t flags,
+                            double* corrected);
+
 /* Device Huffman encoder on host codes (test hook): writes the huffman::encode payload
  * (huffman.cpp:156-251) of zigzag(codes[0..n)) into out (capacity cap); *len = its length. */
 int ffcz_cuda_huffman_encode(ffcz_cuda_ctx* ctx, const int32_t* codes, uint64_t n, uint8_t* out,

@@ -6,11 +6,11 @@ boundary against the reference C++ API.
 from .ffcz import (  # noqa: F401
     Context, CorrectionResult, CudaError, DualBounds, EscapeEntry, FfczError, FormatError,
     ProjectionReport, SymmetryError, UnsupportedError, ValidationError, alternating_projection,
-    correct, correct_batch, default_context, forward_dft, inverse_dft,
+    apply_archive, correct, correct_batch, default_context, forward_dft, inverse_dft,
 )
 
 __all__ = [
     "Context", "CorrectionResult", "DualBounds", "EscapeEntry", "ProjectionReport", "FfczError",
     "ValidationError", "SymmetryError", "FormatError", "CudaError", "UnsupportedError",
-    "correct", "correct_batch", "alternating_projection", "forward_dft", "inverse_dft", "default_context",
+    "correct", "correct_batch", "apply_archive", "alternating_projection", "forward_dft", "inverse_dft", "default_context",
 ]

@@ -41,6 +41,7 @@ EXPORTS = [
     "ffcz_cuda_r2c_device", "ffcz_cuda_c2r_device", "ffcz_cuda_crc32c",
     "ffcz_cuda_profile_enable", "ffcz_cuda_profile_read", "ffcz_cuda_bench_passes",
     "ffcz_cuda_slab", "ffcz_cuda_slab_pitch", "ffcz_cuda_huffman_encode",
+    "ffcz_cuda_apply_archive",
 ]
 
 
@@ -119,6 +120,8 @@ def load():
                                             C.POINTER(BoundsDesc), C.c_int, C.c_uint64,
                                             C.POINTER(Options), C.c_int, C.POINTER(Result)]
     lib.ffcz_cuda_slab.argtypes = [P, P, C.POINTER(C.c_double)]
+    lib.ffcz_cuda_apply_archive.argtypes = [P, P, C.c_uint64, C.POINTER(FieldDesc), P, C.c_uint32,
+                                            P]
     lib.ffcz_cuda_huffman_encode.argtypes = [P, P, C.c_uint64, P, C.c_uint64,
                                              C.POINTER(C.c_uint64)]
     lib.ffcz_cuda_slab_pitch.argtypes = [C.c_uint64]

@@ -249,4 +249,129 @@ std::vector<std::uint8_t> write_archive(const ArchiveInput& in) {
     return w;
 }
 
+
+namespace {
+
+struct ArchiveError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+struct Reader {
+    const std::uint8_t* p;
+    std::size_t n, off = 0;
+    template <class T> T pod() {
+        if (off + sizeof(T) > n) throw ArchiveError("read_archive: truncated archive");
+        T v;
+        std::memcpy(&v, p + off, sizeof(T));
+        off += sizeof(T);
+        return v;
+    }
+    const std::uint8_t* take(std::size_t k) {
+        if (off + k > n) throw ArchiveError("read_archive: truncated archive");
+        const std::uint8_t* q = p + off;
+        off += k;
+        return q;
+    }
+};
+
+std::vector<std::uint8_t> outer_decompress(const std::uint8_t* frame, std::size_t len) {
+    if (len < sizeof(std::uint64_t)) throw ArchiveError("outer frame truncated");
+    std::uint64_t raw = 0;
+    std::memcpy(&raw, frame, sizeof(raw));
+    std::vector<std::uint8_t> out(raw);
+    if (raw == 0) return out;
+    uLongf got = static_cast<uLongf>(raw);
+    const int rc = uncompress(out.data(), &got, frame + sizeof(raw),
+                              static_cast<uLong>(len - sizeof(raw)));
+    if (rc != Z_OK || got != raw) throw ArchiveError("outer_decompress failed: corrupt frame");
+    return out;
+}
+
+} // namespace
+
+ParsedArchive parse_archive(const std::uint8_t* bytes, std::size_t len) {
+    Reader r{bytes, len};
+    ParsedArchive a;
+    const std::uint8_t* magic = r.take(4);
+    if (std::memcmp(magic, "FFCZ", 4) != 0) throw ArchiveError("read_archive: bad magic");
+    if (r.pod<std::uint16_t>() != 1) throw ArchiveError("read_archive: unsupported version");
+    a.ndim = r.pod<std::uint8_t>();
+    if (a.ndim < 1 || a.ndim > 3) throw ArchiveError("read_archive: bad dimensionality");
+    std::uint64_t N = 1;
+    for (int i = 0; i < a.ndim; ++i) {
+        a.dims[i] = r.pod<std::uint64_t>();
+        if (a.dims[i] == 0) throw ArchiveError("read_archive: zero extent");
+        N *= a.dims[i];
+    }
+    const std::uint8_t prec = r.pod<std::uint8_t>();
+    if (prec > 1) throw ArchiveError("read_archive: bad precision tag");
+    a.precision = prec;
+    const std::uint8_t tags = r.pod<std::uint8_t>();
+    a.spatial_per_point = tags & 1u;
+    a.freq_per_component = tags & 2u;
+    a.converged = tags & 4u;
+    if (a.spatial_per_point) a.spatial_values = r.take(8 * N);
+    else a.spatial_global = r.pod<double>();
+    if (a.freq_per_component) {
+        a.freq_re = r.take(8 * N);
+        a.freq_im = r.take(8 * N);
+    } else {
+        a.freq_global = r.pod<double>();
+    }
+    a.m = r.pod<std::uint8_t>();
+    if (a.m < 1 || a.m > 24) throw ArchiveError("read_archive: bad quantization width");
+    a.n_spatial = r.pod<std::uint64_t>();
+    a.n_frequency = r.pod<std::uint64_t>();
+    const std::uint64_t lsf = r.pod<std::uint64_t>(), lff = r.pod<std::uint64_t>();
+    const std::uint64_t lsi = r.pod<std::uint64_t>(), lfi = r.pod<std::uint64_t>();
+    const std::uint64_t nesc = r.pod<std::uint64_t>();
+    const std::size_t header_len = r.off;
+    if (crc32c(bytes, header_len) != r.pod<std::uint32_t>())
+        throw ArchiveError("read_archive: header checksum mismatch");
+    const std::uint8_t* sf = r.take(lsf);
+    const std::uint8_t* ff = r.take(lff);
+    const std::uint8_t* si = r.take(lsi);
+    const std::uint8_t* fi = r.take(lfi);
+    a.spatial_flags = outer_decompress(sf, lsf);
+    a.frequency_flags = outer_decompress(ff, lff);
+    std::uint64_t Nh = N / a.dims[a.ndim - 1] * (a.dims[a.ndim - 1] / 2 + 1);
+    if (a.spatial_flags.size() != (N + 7) / 8 || a.frequency_flags.size() != (Nh + 7) / 8)
+        throw ArchiveError("decode_streams: flag payload length mismatch");
+    a.spatial_payload = outer_decompress(si, lsi);
+    a.frequency_payload = outer_decompress(fi, lfi);
+    a.escapes.resize(nesc);
+    for (auto& e : a.escapes) {
+        const std::uint64_t packed = r.pod<std::uint64_t>();
+        e.frequency = packed >> 63;
+        e.index = packed & ~(std::uint64_t(1) << 63);
+        e.re = r.pod<double>();
+        e.im = e.frequency ? r.pod<double>() : 0.0;
+        if (e.index >= (e.frequency ? Nh : N))
+            throw ArchiveError("read_archive: escape index out of range");
+    }
+    if (r.off != len) throw ArchiveError("read_archive: trailing bytes");
+    return a;
+}
+
+std::uint64_t huffman_blocks(const std::vector<std::uint8_t>& payload,
+                             std::vector<std::uint64_t>& block_off,
+                             std::vector<std::uint64_t>& block_first) {
+    Reader r{payload.data(), payload.size()};
+    const std::uint64_t total = r.pod<std::uint64_t>();
+    std::uint64_t done = 0;
+    while (done < total) {
+        block_off.push_back(r.off);
+        block_first.push_back(done);
+        const std::uint32_t n = r.pod<std::uint32_t>();
+        const std::uint32_t d = r.pod<std::uint32_t>();
+        if (d == 0 || d > n) throw ArchiveError("huffman: bad table size");
+        r.take(5ull * d);
+        const std::uint64_t nbits = r.pod<std::uint64_t>();
+        r.take((nbits + 7) / 8);
+        done += n;
+    }
+    if (done != total || r.off != payload.size())
+        throw ArchiveError("huffman: stream length mismatch");
+    return total;
+}
 } // namespace ffcz_host

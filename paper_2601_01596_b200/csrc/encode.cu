@@ -369,4 +369,103 @@ unsigned long long huffman_encode_device(DevScratch& s, const int* codes, unsign
     return total;
 }
 
+
+// ---- decoding (huffman.cpp:186-243), one thread per block -------------------------------------
+
+namespace {
+
+__device__ __forceinline__ unsigned get_u32(const unsigned char* p) {
+    return p[0] | (p[1] << 8) | (p[2] << 16) | (static_cast<unsigned>(p[3]) << 24);
+}
+__device__ __forceinline__ unsigned long long get_u64(const unsigned char* p) {
+    unsigned long long v = 0;
+    for (int k = 7; k >= 0; --k) v = (v << 8) | p[k];
+    return v;
+}
+
+__global__ void k_huff_decode(const unsigned char* __restrict__ payload,
+                              const unsigned long long* __restrict__ block_off,
+                              const unsigned long long* __restrict__ block_first, long long nb,
+                              int* out, int* err) {
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nb;
+         b += (long long)gridDim.x * blockDim.x) {
+        const unsigned char* p = payload + block_off[b];
+        const unsigned n = get_u32(p), d = get_u32(p + 4);
+        const unsigned char* tab = p + 8;
+        unsigned count[33], first_code[33], first_idx[33];
+        for (int l = 0; l <= 32; ++l) count[l] = 0;
+        int max_len = 0;
+        unsigned prev_len = 0, prev_sym = 0;
+        bool bad = false;
+        for (unsigned j = 0; j < d; ++j) {
+            const unsigned sym = get_u32(tab + 5ull * j), len = tab[5ull * j + 4];
+            if (len == 0 || len > 32) bad = true;                   // huffman.cpp:196
+            // canonical (length, symbol) order, as both writers emit it
+            if (j && (len < prev_len || (len == prev_len && sym <= prev_sym))) bad = true;
+            prev_len = len;
+            prev_sym = sym;
+            if (!bad) ++count[len];
+            max_len = len > static_cast<unsigned>(max_len) ? len : max_len;
+        }
+        if (bad) {
+            atomicExch(err, 1);
+            continue;
+        }
+        unsigned code = 0, idx = 0;
+        for (int l = 1; l <= max_len; ++l) {  // huffman.cpp:205-215
+            code <<= 1;
+            first_code[l] = code;
+            first_idx[l] = idx;
+            code += count[l];
+            idx += count[l];
+        }
+        const unsigned long long nbits = get_u64(tab + 5ull * d);
+        const unsigned char* bits = tab + 5ull * d + 8;
+        unsigned long long pos = 0;
+        int* o = out + block_first[b];
+        for (unsigned i = 0; i < n; ++i) {
+            unsigned c = 0;
+            int l = 1;
+            for (;; ++l) {
+                if (l > max_len || pos >= nbits) {
+                    atomicExch(err, 2);
+                    return;
+                }
+                c = (c << 1) | ((bits[pos >> 3] >> (7 - (pos & 7))) & 1u);
+                ++pos;
+                const unsigned rel = c - first_code[l];
+                if (c >= first_code[l] && rel < count[l]) {
+                    const unsigned sym = get_u32(tab + 5ull * (first_idx[l] + rel));
+                    o[i] = static_cast<int>((sym >> 1) ^ (~(sym & 1u) + 1u));  // unzigzag
+                    break;
+                }
+            }
+        }
+    }
+}
+
+} // namespace
+
+void huffman_decode_device(DevScratch& s, const unsigned char* payload, unsigned long long len,
+                           const unsigned long long* block_off, const unsigned long long* block_first,
+                           long long nb, int* codes_out) {
+    cudaStream_t st = s.stream;
+    if (nb == 0) return;
+    auto* dp = static_cast<unsigned char*>(s.get("hd_payload", len));
+    auto* doff = static_cast<unsigned long long*>(s.get("hd_off", 8 * nb));
+    auto* dfirst = static_cast<unsigned long long*>(s.get("hd_first", 8 * nb));
+    auto* err = static_cast<int*>(s.get("hd_err", 4));
+    FFCZ_CUDA_CHECK(cudaMemcpyAsync(dp, payload, len, cudaMemcpyHostToDevice, st));
+    FFCZ_CUDA_CHECK(cudaMemcpyAsync(doff, block_off, 8 * nb, cudaMemcpyHostToDevice, st));
+    FFCZ_CUDA_CHECK(cudaMemcpyAsync(dfirst, block_first, 8 * nb, cudaMemcpyHostToDevice, st));
+    FFCZ_CUDA_CHECK(cudaMemsetAsync(err, 0, 4, st));
+    k_huff_decode<<<static_cast<unsigned>((nb + 31) / 32), 32, 0, st>>>(dp, doff, dfirst, nb,
+                                                                        codes_out, err);
+    FFCZ_LAUNCH_CHECK();
+    int h = 0;
+    FFCZ_CUDA_CHECK(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, st));
+    FFCZ_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (h == 1) throw Error(kFormat, "huffman: bad code length or non-canonical table");
+    if (h == 2) throw Error(kFormat, "huffman: invalid code");
+}
 } // namespace ffcz_gpu

@@ -21,4 +21,11 @@ struct DevScratch {
 unsigned long long huffman_encode_device(DevScratch& s, const int* codes, unsigned long long n,
                                          unsigned char** payload);
 
+// Decodes a huffman::encode payload (host bytes + its block directory, archive.hpp
+// huffman_blocks) into n int32 codes on the device (unzigzag'ed).  Throws Error(kFormat) on a
+// corrupt stream.
+void huffman_decode_device(DevScratch& s, const unsigned char* payload, unsigned long long len,
+                           const unsigned long long* block_off, const unsigned long long* block_first,
+                           long long nb, int* codes_out);
+
 } // namespace ffcz_gpu

@@ -1172,6 +1172,125 @@ int ffcz_cuda_correct_batch(ffcz_cuda_ctx* ctx, const ffcz_field_desc* frame, ui
     });
 }
 
+// apply_edits(decompressed, read_archive(bytes)) (archive.cpp:137-273) on the device: the host
+// parses the container (header, CRC-32C, zlib outer stages), the device decodes the Huffman
+// index streams, dequantises + scatters the edits and escapes, inverts the half spectrum and adds.
+int ffcz_cuda_apply_archive(ffcz_cuda_ctx* ctx, const uint8_t* archive, uint64_t len,
+                            const ffcz_field_desc* field, const void* decompressed, uint32_t flags,
+                            double* corrected) {
+    return guarded(ctx, [&] {
+        if (!archive || !field || !decompressed || !corrected) throw Error(kValidation, "null argument");
+        ffcz_host::ParsedArchive a;
+        try {
+            a = ffcz_host::parse_archive(archive, len);
+        } catch (const std::runtime_error& e) {
+            throw Error(kFormat, e.what());
+        }
+        bool same = field->ndim == a.ndim;
+        for (int i = 0; same && i < a.ndim; ++i) same = field->dims[i] == a.dims[i];
+        if (!same) throw Error(kValidation, "apply_edits: field dims do not match archive dims");
+        ffcz_cuda_ctx& c = *ctx;
+        cudaStream_t st = c.st;
+        const Geometry g = make_geometry(a.ndim, a.dims, kPitchAlign);
+        const HalfGeom hg = g.hg();
+        const long long N = g.N, Nc = g.Nc();
+        const bool on_dev = flags & FFCZ_INPUTS_ON_DEVICE;
+        const size_t esz = field->dtype == FFCZ_F32 ? 4 : 8;
+        const void* dec = decompressed;
+        if (!on_dev) {
+            void* d = c.buf("ap_dec", N * esz);
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(d, decompressed, N * esz, cudaMemcpyHostToDevice, st));
+            dec = d;
+        }
+        ffcz_bounds_desc bd{};
+        bd.spatial_per_point = a.spatial_per_point;
+        bd.spatial_global = a.spatial_global;
+        bd.spatial_values = reinterpret_cast<const double*>(a.spatial_values);
+        bd.freq_per_component = a.freq_per_component;
+        bd.freq_global = a.freq_global;
+        bd.freq_re = reinterpret_cast<const double*>(a.freq_re);
+        bd.freq_im = reinterpret_cast<const double*>(a.freq_im);
+        const Bounds b = upload_bounds(c, g, bd, false);
+        const long long ws = (N + 31) / 32, wf = (Nc + 31) / 32;
+        unsigned* ks = c.b<unsigned>("ap_keep_s", ws);
+        unsigned* kf = c.b<unsigned>("ap_keep_f", wf);
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(ks, 0, 4 * ws, st));
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(kf, 0, 4 * wf, st));
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(ks, a.spatial_flags.data(), a.spatial_flags.size(),
+                                        cudaMemcpyHostToDevice, st));
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(kf, a.frequency_flags.data(), a.frequency_flags.size(),
+                                        cudaMemcpyHostToDevice, st));
+        DevScratch ds{st, [&](const char* nm, size_t bytes) { return c.buf(nm, bytes); }};
+        auto decode = [&](const std::vector<uint8_t>& payload, unsigned long long want,
+                          const char* name) {
+            std::vector<std::uint64_t> off, first;
+            unsigned long long total = 0;
+            try {
+                total = ffcz_host::huffman_blocks(payload, off, first);
+            } catch (const std::runtime_error& e) {
+                throw Error(kFormat, e.what());
+            }
+            if (total != want) throw Error(kFormat, "read_archive: edit count mismatch");
+            int* codes = c.b<int>(name, std::max<unsigned long long>(total, 1));
+            huffman_decode_device(ds, payload.data(), payload.size(),
+                                  reinterpret_cast<const unsigned long long*>(off.data()),
+                                  reinterpret_cast<const unsigned long long*>(first.data()),
+                                  static_cast<long long>(off.size()), codes);
+            return codes;
+        };
+        int* cs = decode(a.spatial_payload, a.n_spatial, "ap_codes_s");
+        int* cf = decode(a.frequency_payload, 2 * a.n_frequency, "ap_codes_f");
+        double* spat = c.b<double>("ap_spat", N);
+        double2* freq = c.b<double2>("ap_freq", g.half_elems());
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(spat, 0, 8 * N, st));
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(freq, 0, 16 * g.half_elems(), st));
+        auto scatter = [&](const unsigned* words, long long nwords, unsigned long long want,
+                           const char* name, auto launch) {
+            const long long nblk = std::max<long long>(1, (nwords + 1023) / 1024);
+            unsigned long long* cnt = c.b<unsigned long long>(name, nblk + 1);
+            k_popc_blocks<<<static_cast<unsigned>(nblk), 1024, 0, st>>>(words, nwords, cnt);
+            k_scan_blocks<<<1, 1024, 0, st>>>(cnt, nblk, &c.ctl->count_a);
+            launch(static_cast<unsigned>(nblk), cnt);
+            FFCZ_LAUNCH_CHECK();
+            if (c.read_ctl().count_a != want)                        // archive.cpp:205-208
+                throw Error(kFormat, "read_archive: edit count mismatch");
+        };
+        scatter(ks, ws, a.n_spatial, "ap_cnt_s", [&](unsigned nb, unsigned long long* o) {
+            k_dequant_spatial_bits<<<nb, 1024, 0, st>>>(ks, ws, o, cs, b.sb, a.m, spat);
+        });
+        scatter(kf, wf, a.n_frequency, "ap_cnt_f", [&](unsigned nb, unsigned long long* o) {
+            k_dequant_freq_bits<<<nb, 1024, 0, st>>>(kf, wf, o, cf, hg, b.fb, a.m, freq);
+        });
+        if (!a.escapes.empty()) {
+            std::vector<EscapeRec> er(a.escapes.size());
+            for (size_t i = 0; i < er.size(); ++i)
+                er[i] = {a.escapes[i].frequency ? 1 : 0, 0, a.escapes[i].index, a.escapes[i].re,
+                         a.escapes[i].im};
+            EscapeRec* de = c.b<EscapeRec>("ap_esc", er.size());
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(de, er.data(), er.size() * sizeof(EscapeRec),
+                                            cudaMemcpyHostToDevice, st));
+            k_scatter_escapes<<<grid_for(er.size()), 256, 0, st>>>(de, er.size(), spat, freq, hg);
+            FFCZ_LAUNCH_CHECK();
+            c.sync();  // `er` is pageable and goes out of scope
+        }
+        FftPlan<double> plan{g, &c.tw64};
+        double* fpart = c.b<double>("ap_fpart", N);
+        double2* work = c.b<double2>("ap_work", g.half_elems());
+        c2r_p(c, plan, freq, work, fpart, 1.0 / static_cast<double>(N));
+        double* out = on_dev ? corrected : c.b<double>("ap_out", N);
+        if (field->dtype == FFCZ_F32)
+            k_apply_sum<float><<<grid_for(N), 256, 0, st>>>(static_cast<const float*>(dec), spat,
+                                                             fpart, out, N);
+        else
+            k_apply_sum<double><<<grid_for(N), 256, 0, st>>>(static_cast<const double*>(dec), spat,
+                                                              fpart, out, N);
+        FFCZ_LAUNCH_CHECK();
+        if (!on_dev)
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(corrected, out, 8 * N, cudaMemcpyDeviceToHost, st));
+        c.sync();
+    });
+}
+
 uint64_t ffcz_cuda_slab_pitch(uint64_t n2) { return round_up(n2 / 2 + 1, kPitchAlign); }
 
 // One per-rank device step of the slab-decomposed correction (paper_2601_01596_b200/slab.py).

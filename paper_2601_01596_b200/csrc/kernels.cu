@@ -480,6 +480,53 @@ __global__ void k_codes_freq_bits(const unsigned* __restrict__ keep_words, long 
     });
 }
 
+// dequantize_edits (editset.cpp:106-133) scattered to the flagged positions (expand_edits,
+// archive.cpp:227-260): dense arrays must be zero on entry
+__global__ void k_dequant_spatial_bits(const unsigned* __restrict__ keep_words, long long nwords,
+                                       const unsigned long long* __restrict__ block_offsets,
+                                       const int* __restrict__ codes, SpatialB sb, int m,
+                                       double* spat) {
+    codes_from_bits(keep_words, nwords, block_offsets, [&](long long n, unsigned long long pos) {
+        spat[n] = static_cast<double>(codes[pos]) * ldexp(2.0 * sb.at(n), -m);
+    });
+}
+
+__global__ void k_dequant_freq_bits(const unsigned* __restrict__ keep_words, long long nwords,
+                                    const unsigned long long* __restrict__ block_offsets,
+                                    const int* __restrict__ codes, HalfGeom g, FreqB fb, int m,
+                                    double2* freq) {
+    codes_from_bits(keep_words, nwords, block_offsets, [&](long long h, unsigned long long pos) {
+        const long long off = g.offset_of(h);
+        const double2 d = fb.at2(off);
+        const int2 c = reinterpret_cast<const int2*>(codes)[pos];
+        freq[off] = make_double2(static_cast<double>(c.x) * ldexp(2.0 * d.x, -m),
+                                 static_cast<double>(c.y) * ldexp(2.0 * d.y, -m));
+    });
+}
+
+__global__ void k_scatter_escapes(const EscapeRec* __restrict__ recs, long long n, double* spat,
+                                  double2* freq, HalfGeom g) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const EscapeRec e = recs[i];
+        if (e.frequency) freq[g.offset_of(static_cast<long long>(e.index))] = make_double2(e.re, e.im);
+        else spat[e.index] = e.re;
+    }
+}
+
+// apply_edits (archive.cpp:262-273): decompressed + spatial + Re(IFFT(frequency))
+template <class TI>
+__global__ void k_apply_sum(const TI* __restrict__ dec, const double* __restrict__ spat,
+                            const double* __restrict__ fpart, double* out, long long N) {
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
+         n += (long long)gridDim.x * blockDim.x)
+        out[n] = static_cast<double>(dec[n]) + spat[n] + fpart[n];
+}
+template __global__ void k_apply_sum<float>(const float*, const double*, const double*, double*,
+                                            long long);
+template __global__ void k_apply_sum<double>(const double*, const double*, const double*, double*,
+                                             long long);
+
 template <class TI>
 __global__ void k_repair_spatial(const TI* __restrict__ orig, const TI* __restrict__ dec,
                                  const double* __restrict__ fpart, const double* __restrict__ final_eps,

@@ -535,6 +535,20 @@ struct EscapeRec {
     double re, im;
 };
 static_assert(sizeof(EscapeRec) == 32, "EscapeRec layout");
+// decoder side (expand_edits / apply_edits, archive.cpp:227-273)
+__global__ void k_dequant_spatial_bits(const unsigned* __restrict__ keep_words, long long nwords,
+                                       const unsigned long long* __restrict__ block_offsets,
+                                       const int* __restrict__ codes, SpatialB sb, int m,
+                                       double* spat);
+__global__ void k_dequant_freq_bits(const unsigned* __restrict__ keep_words, long long nwords,
+                                    const unsigned long long* __restrict__ block_offsets,
+                                    const int* __restrict__ codes, HalfGeom g, FreqB fb, int m,
+                                    double2* freq);
+__global__ void k_scatter_escapes(const EscapeRec* __restrict__ recs, long long n, double* spat,
+                                  double2* freq, HalfGeom g);
+template <class TI>
+__global__ void k_apply_sum(const TI* __restrict__ dec, const double* __restrict__ spat,
+                            const double* __restrict__ fpart, double* out, long long N);
 __global__ void k_escape_records_s(const unsigned long long* __restrict__ idx, long long n,
                                    const double* __restrict__ spat_cur, EscapeRec* out);
 __global__ void k_escape_records_f(const unsigned long long* __restrict__ idx, long long n,

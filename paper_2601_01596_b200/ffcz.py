@@ -177,6 +177,16 @@ def _is_torch(x):
     return type(x).__module__.startswith("torch")
 
 
+def _order_after_torch(*tensors):
+    """Device tensors handed to the engine were produced on torch's current stream; the engine
+    runs on its context's own stream, so wait for torch's work on them first."""
+    for t in tensors:
+        if t is not None and _is_torch(t) and t.is_cuda:
+            import torch
+            torch.cuda.current_stream(t.device).synchronize()
+            return
+
+
 def _field_desc(shape, dtype_code, precision):
     d = capi.FieldDesc()
     d.ndim = len(shape)
@@ -340,6 +350,8 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
     bd = _bounds_desc(bounds, mar)
     opt = _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level,
                    device_encode)
+    if on_dev:
+        _order_after_torch(original, decompressed, bounds.spatial, bounds.freq_re, bounds.freq_im)
     holder = _ResultHolder()
     rc = lib.ffcz_cuda_correct(ctx.handle, C.byref(fd), mar.ptr(original, dt),
                                mar.ptr(decompressed, dt), C.byref(bd), int(m), int(max_iters),
@@ -380,6 +392,8 @@ def correct_batch(original, decompressed, bounds, m: int = 16, max_iters: int = 
     for i, b in enumerate(bounds):
         bds[i] = _bounds_desc(b, mar)
     opt = _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level)
+    if on_dev:
+        _order_after_torch(original, decompressed)
     res = (capi.Result * max(1, nf))()
     rc = lib.ffcz_cuda_correct_batch(ctx.handle, C.byref(fd), nf, mar.ptr(original, dt),
                                      mar.ptr(decompressed, dt), bds, int(m), int(max_iters),
@@ -453,6 +467,7 @@ def r2c_device(x, out, *, ctx: Context | None = None):
     ctx = ctx or default_context()
     fd = _field_desc(tuple(x.shape), capi.FFCZ_F32 if x.dtype == torch.float32 else capi.FFCZ_F64,
                      "f64")
+    _order_after_torch(x, out)
     _check(capi.load().ffcz_cuda_r2c_device(ctx.handle, C.byref(fd), C.c_void_p(x.data_ptr()),
                                             C.c_void_p(out.data_ptr())))
 
@@ -463,6 +478,7 @@ def c2r_device(half, x, *, ctx: Context | None = None):
     ctx = ctx or default_context()
     fd = _field_desc(tuple(x.shape), capi.FFCZ_F32 if x.dtype == torch.float32 else capi.FFCZ_F64,
                      "f64")
+    _order_after_torch(half, x)
     _check(capi.load().ffcz_cuda_c2r_device(ctx.handle, C.byref(fd), C.c_void_p(half.data_ptr()),
                                             C.c_void_p(x.data_ptr())))
 
@@ -480,3 +496,34 @@ def huffman_encode_device(codes, *, ctx: Context | None = None) -> bytes:
     _check(lib.ffcz_cuda_huffman_encode(ctx.handle, C.c_void_p(c.ctypes.data), c.size,
                                         C.c_void_p(out.ctypes.data), n.value, C.byref(n)))
     return out[: n.value].tobytes()
+
+
+def apply_archive(archive: bytes, decompressed, *, ctx: Context | None = None):
+    """ffcz::apply_edits(decompressed, ffcz::read_archive(archive)) (archive.cpp:137-273) on the
+    GPU: the FP64 corrected field (numpy for host input, CUDA torch tensor for device input)."""
+    ctx = ctx or default_context()
+    lib = capi.load()
+    on_dev = _is_torch(decompressed)
+    if on_dev:
+        import torch
+        is32 = decompressed.dtype == torch.float32
+        shape = tuple(decompressed.shape)
+        out = torch.empty(shape, dtype=torch.float64, device=decompressed.device)
+        _order_after_torch(decompressed)
+        dptr, optr = C.c_void_p(decompressed.data_ptr()), C.c_void_p(out.data_ptr())
+        keep = (decompressed,)
+    else:
+        d = np.asarray(decompressed)
+        is32 = d.dtype == np.float32
+        d = np.ascontiguousarray(d, dtype=np.float32 if is32 else np.float64)
+        shape = d.shape
+        out = np.empty(shape, dtype=np.float64)
+        dptr, optr = C.c_void_p(d.ctypes.data), C.c_void_p(out.ctypes.data)
+        keep = (d,)
+    fd = _field_desc(shape, capi.FFCZ_F32 if is32 else capi.FFCZ_F64, "f64")
+    buf = np.frombuffer(archive, dtype=np.uint8)
+    _check(lib.ffcz_cuda_apply_archive(ctx.handle, C.c_void_p(buf.ctypes.data), buf.size,
+                                       C.byref(fd), dptr,
+                                       capi.FFCZ_INPUTS_ON_DEVICE if on_dev else 0, optr))
+    del keep
+    return out
