@@ -484,7 +484,7 @@ void c2r_p(ffcz_cuda_ctx& c, const FftPlan<double>& plan, const double2* half, d
 template <class TI>
 GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* dec,
                  const Bounds& bo, int m, const LoopResult& lr, double* eps, double* S,
-                 double2* F, double* corrected,
+                 double2* F, double2* spec, double* corrected,
                  const std::function<void(unsigned long long, unsigned long long)>& on_codes) {
     cudaStream_t st = c.st;
     FftPlan<double> plan{g, &c.tw64};
@@ -500,7 +500,6 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
     unsigned long long* idx = c.b<unsigned long long>("idx", std::max(N, Nc));
     int* codes_s = c.b<int>("codes_s", N);
     int* codes_f = c.b<int>("codes_f", 2 * Nc);
-    double2* spec = c.b<double2>("spec", g.half_elems());
     double* eps_t = c.b<double>("eps_tilde", N);
 
     const bool converged = lr.converged, fused = lr.fused;
@@ -718,6 +717,12 @@ struct DebugClock {
 };
 
 template <class TI>
+void finish_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& fd, const TI* orig,
+                  const TI* dec, const ffcz_bounds_desc& bd, const Bounds& bo, int m,
+                  const LoopResult& lr, double* eps, double* S, double2* F, double2* delta_star,
+                  const ffcz_cuda_options& opt, ffcz_cuda_result* out);
+
+template <class TI>
 void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& fd,
                    const void* orig_in, const void* dec_in, const ffcz_bounds_desc& bd, int m,
                    uint64_t max_iters, const ffcz_cuda_options& opt, ffcz_cuda_result* out) {
@@ -767,6 +772,28 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[2], st));
     const LoopResult lr = run_loop(c, g, eps, bo, f, !(opt.flags & FFCZ_FORCE_UNFUSED), S, F);
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[3], st));
+    finish_typed<TI>(c, g, fd, orig, dec, bd, bo, m, lr, eps, S, F,
+                     c.b<double2>("spec", g.half_elems()), opt, out);
+    out->report.wall_time_s = event_ms(c.ev[2], c.ev[3]) * 1e-3;
+    out->t_h2d_ms = event_ms(c.ev[0], c.ev[1]);
+    out->t_loop_ms = event_ms(c.ev[2], c.ev[3]);
+    out->t_feasible_ms = event_ms(c.ev[1], c.ev[6]);
+}
+
+// Residual, FP64 gate and products of one field whose projection loop has run (pipeline.cpp:
+// 46-176): shared by correct() and the batched-frame path (each frame's state in the batch
+// arrays).  Records ev[3] -> ev[6] around the gate.
+template <class TI>
+void finish_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& fd, const TI* orig,
+                  const TI* dec, const ffcz_bounds_desc& bd, const Bounds& bo, int m,
+                  const LoopResult& lr, double* eps, double* S, double2* F, double2* delta_star,
+                  const ffcz_cuda_options& opt, ffcz_cuda_result* out) {
+    cudaStream_t st = c.st;
+    const bool on_dev = opt.flags & FFCZ_INPUTS_ON_DEVICE;
+    const long long N = g.N;
+    const double f = 1.0 - std::ldexp(1.0, -m);
+    DebugClock dbg;
+    FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[3], st));
     {
         Prof p(c, kElemPre, 8.0 * N);
         k_residual_s<<<grid_for(N), 256, 0, st>>>(eps, N, bo.sb, f, c.ctl);
@@ -800,10 +827,11 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
                                         nf * 8, cudaMemcpyDeviceToHost, cs));
         copy_pending = true;
     };
-    const GateOut go = run_gate<TI>(c, g, orig, dec, bo, m, lr, eps, S, F, corrected, on_codes);
+    const GateOut go = run_gate<TI>(c, g, orig, dec, bo, m, lr, eps, S, F, delta_star, corrected,
+                                    on_codes);
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[6], st));
     dbg.mark(c, "gate done");
-    h = c.read_ctl();
+    const Ctl h = c.read_ctl();
 
     out->report.iterations = std::max<unsigned long long>(lr.passes, 1);
     out->report.active_spatial = go.act_s;
@@ -811,7 +839,6 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     out->report.converged = lr.converged;
     out->report.residual_f = lr.residual_f;
     out->report.residual_s = bitsd_host(h.res_s_bits);
-    out->report.wall_time_s = event_ms(c.ev[2], c.ev[3]) * 1e-3;
     out->iterations_fp32 = 0;
     out->iterations_fp64 = lr.passes;
     out->escape_rounds = go.rounds;
@@ -820,10 +847,7 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     out->verify_max_freq_excess = go.vf;
     out->n_spatial = go.n_keep_s;
     out->n_frequency = go.n_keep_f;
-    out->t_h2d_ms = event_ms(c.ev[0], c.ev[1]);
-    out->t_loop_ms = event_ms(c.ev[2], c.ev[3]);
     out->t_gate_ms = event_ms(c.ev[3], c.ev[6]);
-    out->t_feasible_ms = event_ms(c.ev[1], c.ev[6]);
 
     // ---- products to the host -------------------------------------------------------------
     const auto t_d2h0 = std::chrono::steady_clock::now();
@@ -988,6 +1012,229 @@ static void c2r_dev(ffcz_cuda_ctx& c, Twiddles<T>& tw, const Geometry& g, const 
 
 // ================================ C-ABI ===========================================================
 
+namespace {
+
+// Runs fn(lane_ctx, item) for items [0, n) on `nl` lane sub-contexts (host threads, one stream
+// each), ordered after the work already queued on ctx->st; ctx->st waits for every lane before
+// returning.  The first exception of any lane is rethrown.
+void run_on_lanes(ffcz_cuda_ctx* ctx, int nl, uint64_t n,
+                  const std::function<void(ffcz_cuda_ctx&, uint64_t)>& fn) {
+    while (static_cast<int>(ctx->lanes.size()) < nl) {
+        ffcz_cuda_ctx* l = nullptr;
+        if (ffcz_cuda_create(&l, ctx->device, nullptr) != kOk)
+            throw Error(kCuda, std::string("lane context: ") + g_last_error);
+        ctx->lanes.push_back(l);
+    }
+    FFCZ_CUDA_CHECK(cudaEventRecord(ctx->ev[7], ctx->st));
+    for (int i = 0; i < nl; ++i) {
+        ffcz_cuda_ctx* l = ctx->lanes[i];
+        FFCZ_CUDA_CHECK(cudaStreamWaitEvent(l->st, ctx->ev[7], 0));
+        if (l->prof_on != ctx->prof_on) {
+            l->prof_on = ctx->prof_on;
+            l->prof.clear();
+            l->ev_used = 0;
+        }
+    }
+    std::atomic<uint64_t> next{0};
+    std::mutex err_mu;
+    int err_status = kOk;
+    std::string err_msg;
+    auto work = [&](ffcz_cuda_ctx* l) {
+        try {
+            FFCZ_CUDA_CHECK(cudaSetDevice(l->device));
+            std::lock_guard<std::mutex> lk(l->mu);
+            for (;;) {
+                const uint64_t i = next.fetch_add(1);
+                if (i >= n) break;
+                {
+                    std::lock_guard<std::mutex> ek(err_mu);
+                    if (err_status != kOk) break;
+                }
+                fn(*l, i);
+            }
+        } catch (const Error& e) {
+            std::lock_guard<std::mutex> ek(err_mu);
+            if (err_status == kOk) { err_status = e.status; err_msg = e.what(); }
+        } catch (const std::exception& e) {
+            std::lock_guard<std::mutex> ek(err_mu);
+            if (err_status == kOk) { err_status = kCuda; err_msg = e.what(); }
+        }
+    };
+    std::vector<std::thread> th;
+    for (int i = 1; i < nl; ++i) th.emplace_back(work, ctx->lanes[i]);
+    work(ctx->lanes[0]);
+    for (auto& t : th) t.join();
+    for (int i = 0; i < nl; ++i) {
+        ffcz_cuda_ctx* l = ctx->lanes[i];
+        FFCZ_CUDA_CHECK(cudaEventRecord(l->ev[7], l->st));
+        FFCZ_CUDA_CHECK(cudaStreamWaitEvent(ctx->st, l->ev[7], 0));
+    }
+    if (err_status != kOk) throw Error(err_status, "frame batch: " + err_msg);
+}
+
+// FFCZ_FRAMES_FUSED=0: always use per-frame correct() on lanes
+inline bool frames_fused_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_FRAMES_FUSED");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// Batched frames with ONE projection loop over the whole stack (config 3): every pass covers
+// all frames (axis-1 column passes with planes = frames, row passes over all rows), each frame
+// has its own control block / bounds / decision, and the tiles of converged frames are skipped
+// so each frame's state stops exactly where its own loop would (kernels.cuh, FrameBatch).  The
+// FP64 gate of each frame then runs on the lanes (finish_typed on the frame's slices).  Frames
+// are processed in groups sized to a device-memory budget.
+template <class TI>
+void correct_frames_fused(ffcz_cuda_ctx& c, const ffcz_field_desc& fd, uint64_t nframes,
+                          const void* orig_in, const void* dec_in, const ffcz_bounds_desc* bd,
+                          int m, uint64_t max_iters, const ffcz_cuda_options& opt, int nl,
+                          ffcz_cuda_result* out) {
+    if (m < 1 || m > 24) throw Error(kValidation, "shrink_bounds requires 1 <= m <= 24");
+    if (max_iters < 1) throw Error(kValidation, "alternating_projection: max_iters must be >= 1");
+    cudaStream_t st = c.st;
+    const bool on_dev = opt.flags & FFCZ_INPUTS_ON_DEVICE;
+    const Geometry gf = make_geometry(fd.ndim, fd.dims, kPitchAlign);
+    const long long Nf = gf.N, Hf = gf.half_elems(), n1 = gf.d[1], n2 = gf.n2;
+    const double fw = 1.0 - std::ldexp(1.0, -m);
+    const double slack = 1.0 / (1.0 - std::ldexp(1.0, -m)) - 1.0 + 0x1p-20;
+    const double per_frame = 16.0 * Nf + 33.0 * Hf + (on_dev ? 0.0 : 2.0 * sizeof(TI) * Nf);
+    const double budget = 48e9;
+    const uint64_t G = std::max<uint64_t>(1, std::min<uint64_t>(
+        nframes, static_cast<uint64_t>(budget / per_frame)));
+    const uint64_t dims3[3] = {G, static_cast<uint64_t>(n1), static_cast<uint64_t>(n2)};
+    for (uint64_t g0 = 0; g0 < nframes; g0 += G) {
+        const long long Gc = static_cast<long long>(std::min<uint64_t>(G, nframes - g0));
+        const uint64_t dimsc[3] = {static_cast<uint64_t>(Gc), dims3[1], dims3[2]};
+        const Geometry gb = make_geometry(3, dimsc, kPitchAlign);
+        FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[0], st));
+        const TI* orig = static_cast<const TI*>(orig_in) + g0 * Nf;
+        const TI* dec = static_cast<const TI*>(dec_in) + g0 * Nf;
+        if (!on_dev) {
+            TI* o = c.b<TI>("fr_orig", Gc * Nf);
+            TI* d = c.b<TI>("fr_dec", Gc * Nf);
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(o, orig, Gc * Nf * sizeof(TI), cudaMemcpyHostToDevice, st));
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(d, dec, Gc * Nf * sizeof(TI), cudaMemcpyHostToDevice, st));
+            orig = o;
+            dec = d;
+        }
+        std::vector<double> hE(Gc), hD(Gc);
+        for (long long i = 0; i < Gc; ++i) {
+            hE[i] = bd[g0 + i].spatial_global;
+            hD[i] = bd[g0 + i].freq_global;
+            if (!(hE[i] > 0.0) || !std::isfinite(hE[i]))
+                throw Error(kValidation, "spatial bound E must be strictly positive and finite");
+            if (!(hD[i] > 0.0) || !std::isfinite(hD[i]))
+                throw Error(kValidation, "frequency bound Delta must be strictly positive and finite");
+        }
+        double* dE = c.b<double>("fr_E", Gc);
+        double* dD = c.b<double>("fr_D", Gc);
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(dE, hE.data(), 8 * Gc, cudaMemcpyHostToDevice, st));
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(dD, hD.data(), 8 * Gc, cudaMemcpyHostToDevice, st));
+        FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[1], st));
+        // compute_error + preconditions of every frame (pipeline.cpp:31-42)
+        FrameCtl* fc = c.b<FrameCtl>("fr_ctl", Gc);
+        k_frames_init<<<grid_for(Gc), 256, 0, st>>>(fc, Gc, max_iters);
+        k_ctl_init<<<1, 1, 0, st>>>(c.ctl, max_iters);
+        double* eps = c.b<double>("fr_eps", Gc * Nf);
+        k_eps0_frames<TI><<<grid_for(Gc * Nf), 256, 0, st>>>(orig, dec, eps, Gc * Nf, Nf, dE, fw,
+                                                             slack, c.ctl);
+        FFCZ_LAUNCH_CHECK();
+        const Ctl h0 = c.read_ctl();  // also orders the pageable hE / hD copies
+        if (h0.bad1 != ~0ull)
+            throw Error(kValidation, "correct: decompressed data violates the declared spatial "
+                                     "bound at index " + std::to_string(h0.bad1 % Nf) +
+                                     " (frame " + std::to_string(g0 + h0.bad1 / Nf) + ")");
+        if (h0.bad2 != ~0ull)
+            throw Error(kValidation, "alternating_projection: epsilon0 violates the spatial bound "
+                                     "at index " + std::to_string(h0.bad2 % Nf) + " (frame " +
+                                     std::to_string(g0 + h0.bad2 / Nf) + ")");
+        double* S = c.b<double>("fr_S", Gc * Nf);
+        double2* F = c.b<double2>("fr_F", Gc * Hf);
+        double2* spec = c.b<double2>("fr_spec", Gc * Hf);
+        unsigned char* moved = c.b<unsigned char>("fr_moved", Gc * Hf);
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(moved, 0, Gc * Hf, st));
+        const FrameBatch fbt{fc, dE, dD, fw, n1};
+        FftPlan<double> plan{gb, &c.tw64};
+        const int* gate = &c.ctl->done;
+        const double invN = 1.0 / static_cast<double>(Nf);
+        FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[2], st));
+        launch_row_r2c_hook<double>(n2, eps, n2, spec, gb.P, gb.rows, c.tw64, nullptr,
+                                    HookSkipB<true>{fbt}, st);
+        c.launches += 3;
+        auto body = [&]() {
+            plan.col(1, -1, spec, spec, gate, HookFReduceB{fbt}, st);                  // K3a
+            k_decide_frames<<<grid_for(Gc), 256, 0, st>>>(fc, Gc, c.ctl);              // K4
+            plan.col(1, +1, spec, spec, gate, HookFClipB<double>{fbt, F, moved}, st);  // K3b
+            launch_row_c2r_hook<double>(n2, spec, gb.P, eps, n2, gb.rows, invN, c.tw64, gate,
+                                        HookSClipB<double>{fbt, S}, st);               // K1a
+            launch_row_r2c_hook<double>(n2, eps, n2, spec, gb.P, gb.rows, c.tw64, gate,
+                                        HookSkipB<true>{fbt}, st);                     // K1b
+            FFCZ_LAUNCH_CHECK();
+            c.launches += 5;
+        };
+        static const int kChunk[] = {1, 1, 2, 4, 8};
+        int ci = 0, issued = 0;
+        std::vector<std::pair<cudaEvent_t, int>> inflight;
+        auto issue_chunk = [&]() {
+            const int k = kChunk[std::min(ci++, 4)];
+            for (int i = 0; i < k; ++i) body();
+            const int slot = issued % 2;
+            k_export_ctl<<<1, 32, 0, st>>>(c.ctl, &c.hctl_dev[1 + slot]);
+            FFCZ_LAUNCH_CHECK();
+            cudaEvent_t ev = c.ev[4 + slot];
+            FFCZ_CUDA_CHECK(cudaEventRecord(ev, st));
+            inflight.push_back({ev, slot});
+            ++issued;
+        };
+        issue_chunk();
+        for (;;) {
+            issue_chunk();
+            auto p = inflight.front();
+            inflight.erase(inflight.begin());
+            FFCZ_CUDA_CHECK(cudaEventSynchronize(p.first));
+            if (c.hctl[1 + p.second].done) break;
+        }
+        FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[3], st));
+        std::vector<FrameCtl> hfc(Gc);
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(hfc.data(), fc, sizeof(FrameCtl) * Gc, cudaMemcpyDeviceToHost, st));
+        c.sync();
+        for (long long i = 0; i < Gc; ++i)
+            if (hfc[i].passes == 0) {  // converged at the first check: no clip wrote S / F
+                FFCZ_CUDA_CHECK(cudaMemsetAsync(S + i * Nf, 0, 8 * Nf, st));
+                FFCZ_CUDA_CHECK(cudaMemsetAsync(F + i * Hf, 0, 16 * Hf, st));
+            }
+        const double t_in = event_ms(c.ev[0], c.ev[1]);
+        const double t_loop = event_ms(c.ev[2], c.ev[3]);
+        // per-frame FP64 gate on the lanes
+        run_on_lanes(&c, nl, static_cast<uint64_t>(Gc), [&](ffcz_cuda_ctx& l, uint64_t i) {
+            LoopResult lr;
+            lr.passes = hfc[i].passes;
+            lr.converged = hfc[i].converged;
+            lr.residual_f = hfc[i].residual_f;
+            lr.fused = true;
+            lr.moved = moved + i * Hf;
+            Bounds bo;
+            bo.sb.g = hE[i];
+            bo.fb.g = hD[i];
+            ffcz_cuda_result* r = &out[g0 + i];
+            const unsigned long long l0 = l.launches;
+            finish_typed<TI>(l, gf, fd, orig + i * Nf, dec + i * Nf, bd[g0 + i], bo, m, lr,
+                             eps + i * Nf, S + i * Nf, F + i * Hf, spec + i * Hf, opt, r);
+            r->kernel_launches = l.launches - l0;
+            r->report.wall_time_s = t_loop / Gc * 1e-3;   // the loop is shared by the group
+            r->t_loop_ms = t_loop / Gc;
+            r->t_h2d_ms = t_in / Gc;
+            r->t_feasible_ms = r->t_loop_ms + r->t_gate_ms;
+        });
+        c.sync();
+    }
+}
+
+} // namespace
+
 extern "C" {
 
 int ffcz_cuda_abi_version(void) { return FFCZ_CUDA_ABI_VERSION; }
@@ -1083,13 +1330,14 @@ int ffcz_cuda_correct(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const vo
     });
 }
 
+
 // Batched frames (BASELINE config 3): every frame is an independent ffcz::correct() call
-// (pipeline.cpp:26-178), with its own bounds, iterations and edit set.  Frames are pulled by
-// `lanes` host threads, each driving its own sub-context (stream + device state), so the small
-// per-frame passes and the per-frame control syncs of one lane overlap the others' work on the
-// GPU.  Results are bit-identical to one ffcz_cuda_correct() per frame.  The batch is ordered
-// on the context stream: lanes start after the work already queued there, and the context stream
-// waits for every lane before the call returns (CUDA events around the call time the batch).
+// (pipeline.cpp:26-178), with its own bounds, iterations and edit set.  Power-of-two 2-D frames
+// (>= 64 x 64) with global bounds run ONE projection loop over the whole stack
+// (correct_frames_fused) and their per-frame gates on the lanes; anything else runs whole
+// per-frame correct() calls on the lanes (host threads, one sub-context and stream each).  Results
+// equal one ffcz_cuda_correct() per frame (FFT round-off of the batched passes aside).  The
+// batch is ordered on the context stream.
 int ffcz_cuda_correct_batch(ffcz_cuda_ctx* ctx, const ffcz_field_desc* frame, uint64_t nframes,
                             const void* original, const void* decompressed,
                             const ffcz_bounds_desc* bounds, int m, uint64_t max_iters,
@@ -1108,66 +1356,34 @@ int ffcz_cuda_correct_batch(ffcz_cuda_ctx* ctx, const ffcz_field_desc* frame, ui
         const size_t esz = frame->dtype == FFCZ_F32 ? 4 : 8;
         if (lanes <= 0) lanes = 8;
         const int nl = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(lanes), nframes));
-        while (static_cast<int>(ctx->lanes.size()) < nl) {
-            ffcz_cuda_ctx* l = nullptr;
-            if (ffcz_cuda_create(&l, ctx->device, nullptr) != kOk)
-                throw Error(kCuda, std::string("lane context: ") + g_last_error);
-            ctx->lanes.push_back(l);
-        }
-        FFCZ_CUDA_CHECK(cudaEventRecord(ctx->ev[7], ctx->st));
-        for (int i = 0; i < nl; ++i) {
-            ffcz_cuda_ctx* l = ctx->lanes[i];
-            FFCZ_CUDA_CHECK(cudaStreamWaitEvent(l->st, ctx->ev[7], 0));
-            if (l->prof_on != ctx->prof_on) {
-                l->prof_on = ctx->prof_on;
-                l->prof.clear();
-                l->ev_used = 0;
+        bool fused = frames_fused_enabled() && frame->ndim == 2 &&
+                     !(opt.flags & FFCZ_FORCE_UNFUSED) && g.d[1] >= 64 && g.n2 >= 64 &&
+                     radix_col_ok(g.d[1]) && radix_row_ok(g.n2);
+        for (uint64_t i = 0; fused && i < nframes; ++i)
+            fused = !bounds[i].spatial_per_point && !bounds[i].freq_per_component;
+        try {
+            if (fused) {
+                if (frame->dtype == FFCZ_F32)
+                    correct_frames_fused<float>(*ctx, *frame, nframes, original, decompressed,
+                                                bounds, m, max_iters, opt, nl, out);
+                else
+                    correct_frames_fused<double>(*ctx, *frame, nframes, original, decompressed,
+                                                 bounds, m, max_iters, opt, nl, out);
+                return;
             }
-        }
-        std::atomic<uint64_t> next{0};
-        std::mutex err_mu;
-        int err_status = kOk;
-        std::string err_msg;
-        auto work = [&](ffcz_cuda_ctx* l) {
-            try {
-                FFCZ_CUDA_CHECK(cudaSetDevice(l->device));
-                std::lock_guard<std::mutex> lk(l->mu);
-                for (;;) {
-                    const uint64_t i = next.fetch_add(1);
-                    if (i >= nframes) break;
-                    {
-                        std::lock_guard<std::mutex> ek(err_mu);
-                        if (err_status != kOk) break;
-                    }
-                    const char* o = static_cast<const char*>(original) + i * g.N * esz;
-                    const char* d = static_cast<const char*>(decompressed) + i * g.N * esz;
-                    const unsigned long long l0 = l->launches;
-                    if (frame->dtype == FFCZ_F32)
-                        correct_typed<float>(*l, g, *frame, o, d, bounds[i], m, max_iters, opt, &out[i]);
-                    else
-                        correct_typed<double>(*l, g, *frame, o, d, bounds[i], m, max_iters, opt, &out[i]);
-                    out[i].kernel_launches = l->launches - l0;
-                }
-            } catch (const Error& e) {
-                std::lock_guard<std::mutex> ek(err_mu);
-                if (err_status == kOk) { err_status = e.status; err_msg = e.what(); }
-            } catch (const std::exception& e) {
-                std::lock_guard<std::mutex> ek(err_mu);
-                if (err_status == kOk) { err_status = kCuda; err_msg = e.what(); }
-            }
-        };
-        std::vector<std::thread> th;
-        for (int i = 1; i < nl; ++i) th.emplace_back(work, ctx->lanes[i]);
-        work(ctx->lanes[0]);
-        for (auto& t : th) t.join();
-        for (int i = 0; i < nl; ++i) {
-            ffcz_cuda_ctx* l = ctx->lanes[i];
-            FFCZ_CUDA_CHECK(cudaEventRecord(l->ev[7], l->st));
-            FFCZ_CUDA_CHECK(cudaStreamWaitEvent(ctx->st, l->ev[7], 0));
-        }
-        if (err_status != kOk) {
+            run_on_lanes(ctx, nl, nframes, [&](ffcz_cuda_ctx& l, uint64_t i) {
+                const char* o = static_cast<const char*>(original) + i * g.N * esz;
+                const char* d = static_cast<const char*>(decompressed) + i * g.N * esz;
+                const unsigned long long l0 = l.launches;
+                if (frame->dtype == FFCZ_F32)
+                    correct_typed<float>(l, g, *frame, o, d, bounds[i], m, max_iters, opt, &out[i]);
+                else
+                    correct_typed<double>(l, g, *frame, o, d, bounds[i], m, max_iters, opt, &out[i]);
+                out[i].kernel_launches = l.launches - l0;
+            });
+        } catch (...) {
             for (uint64_t i = 0; i < nframes; ++i) ffcz_cuda_result_free(&out[i]);
-            throw Error(err_status, "frame batch: " + err_msg);
+            throw;
         }
     });
 }

@@ -208,17 +208,18 @@ int rows_per_cta(long long nrows) {
     return static_cast<int>(std::max<long long>(1, r));
 }
 
-template <class T, int M>
+template <class T, int M, class Hook = HookNone>
 void row_r2c_radix(const T* in, long long in_stride, cplx<T>* out, long long out_stride,
-                   long long nrows, Twiddles<T>& tw, const int* gate, cudaStream_t st) {
+                   long long nrows, Twiddles<T>& tw, const int* gate, cudaStream_t st,
+                   Hook hook = Hook{}) {
     constexpr int E = RowCfg<T, M>::E, TT = RowCfg<T, M>::TT;
     const int R = rows_per_cta<T, M>(nrows);
     const size_t smem = row_smem_bytes<T, M, E>(R);
-    auto k = TT <= 32 ? k_row_r2c_sh<T, M, E, HookNone> : k_row_r2c<T, M, E, HookNone>;
+    auto k = TT <= 32 ? k_row_r2c_sh<T, M, E, Hook> : k_row_r2c<T, M, E, Hook>;
     set_smem(k, smem);
     k<<<persistent_grid(k, TT * R, smem, (nrows + R - 1) / R), TT * R, smem, st>>>(
         in, in_stride, out, out_stride, nrows, tw.stage_table(M, E), tw.post_table(M), gate,
-        HookNone{});
+        hook);
     FFCZ_LAUNCH_CHECK();
 }
 
@@ -310,6 +311,24 @@ void launch_row_r2c(long long n2, const T* in, long long in_stride, cplx<T>* out
     k_row_r2c_direct<T><<<static_cast<unsigned>(nrows), 256, smem, st>>>(
         in, in_stride, out, out_stride, static_cast<int>(n2), tw.table_for(n2), gate);
     FFCZ_LAUNCH_CHECK();
+}
+
+template <class T, class Hook>
+void launch_row_r2c_hook(long long n2, const T* in, long long in_stride, cplx<T>* out,
+                         long long out_stride, long long nrows, Twiddles<T>& tw, const int* gate,
+                         Hook hook, cudaStream_t st) {
+    if (radix_row_ok(n2)) {
+        switch (n2 / 2) {
+#define X(n)                                                                                   \
+    case n:                                                                                    \
+        detail::row_r2c_radix<T, n, Hook>(in, in_stride, out, out_stride, nrows, tw, gate, st, \
+                                          hook);                                               \
+        return;
+            FFCZ_POW2_CASES(X)
+#undef X
+        }
+    }
+    throw Error(kUnsupported, "R2C with a hook needs a power-of-two last axis in [32, 8192]");
 }
 
 template <class T>

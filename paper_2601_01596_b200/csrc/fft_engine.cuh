@@ -261,6 +261,17 @@ __device__ __forceinline__ void hook_begin(H& h) {
     if constexpr (requires { h.begin(); }) h.begin();
 }
 
+// A tiled hook (kTiled, batched frames) is asked per tile whether to skip it (its frame has
+// converged) and brackets every processed tile with tile_begin(unit) / tile_end() (CTA-uniform;
+// unit = plane for column passes, first row for row passes).
+template <class H>
+constexpr bool hook_tiled() {
+    if constexpr (requires { H::kTiled; })
+        return H::kTiled;
+    else
+        return false;
+}
+
 // A hook may declare `static constexpr bool kNoStore = true` when the pass output is consumed
 // by the hook alone (e.g. the verify reduction): the store is skipped (half a pass of traffic).
 template <class H>
@@ -296,6 +307,10 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     const int tiles_c = (ncols + B - 1) / B;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long plane = tile / tiles_c;
+        if constexpr (hook_tiled<Hook>()) {
+            if (hook.tile_skip(plane)) continue;
+            hook.tile_begin(plane);
+        }
         const int c = static_cast<int>(tile - plane * tiles_c) * B + b;
         const bool valid = c < ncols;
         const long long base = plane * plane_stride + c;
@@ -318,6 +333,10 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
                 hook.post(v[m], off, c);
                 if constexpr (hook_stores<Hook>()) dst[off] = v[m];
             }
+        }
+        if constexpr (hook_tiled<Hook>()) {
+            hook.tile_end();
+            __syncthreads();  // the next tile's exchange reuses the shared tile
         }
     }
     hook.finish();
@@ -398,6 +417,15 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 1)
         mbar_wait(&bars[slot], (phase >> slot) & 1u);
         phase ^= 1u << slot;
         const long long plane = tile / tiles_c;
+        if constexpr (hook_tiled<Hook>()) {
+            if (hook.tile_skip(plane)) {  // frame done: drop the tile, keep the pipeline going
+                fence_proxy_async_smem();
+                __syncthreads();
+                if (threadIdx.x == 0 && tile + 2 * gridDim.x < ntiles) issue(tile + 2 * gridDim.x, slot);
+                continue;
+            }
+            hook.tile_begin(plane);
+        }
         const int c = static_cast<int>(tile - plane * tiles_c) * B + b;
         const bool valid = c < ncols;
         const long long base = plane * plane_stride + c;
@@ -442,6 +470,7 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 1)
             __syncthreads();
             if (threadIdx.x == 0 && tile + 2 * gridDim.x < ntiles) issue(tile + 2 * gridDim.x, slot);
         }
+        if constexpr (hook_tiled<Hook>()) hook.tile_end();
     }
     hook.finish();
 }
@@ -494,6 +523,15 @@ __global__ void __launch_bounds__(NT, 1)
         mbar_wait(bar, phase);
         phase ^= 1u;
         const long long plane = tile / tiles_c;
+        if constexpr (hook_tiled<Hook>()) {
+            if (hook.tile_skip(plane)) {  // frame done: drop the tile, keep the pipeline going
+                fence_proxy_async_smem();
+                __syncthreads();
+                if (threadIdx.x == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x);
+                continue;
+            }
+            hook.tile_begin(plane);
+        }
         const int c = static_cast<int>(tile - plane * tiles_c) * B + b;
         const bool valid = c < ncols;
         const long long base = plane * plane_stride + c;
@@ -521,6 +559,7 @@ __global__ void __launch_bounds__(NT, 1)
                 if constexpr (hook_stores<Hook>()) dst[off] = v[m];
             }
         }
+        if constexpr (hook_tiled<Hook>()) hook.tile_end();
     }
     hook.finish();
 }
@@ -605,6 +644,11 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         __syncthreads();  // smem of the previous tile fully consumed
+        if constexpr (hook_tiled<Hook>()) {
+            const long long u = tile * (blockDim.x / TT);
+            if (hook.tile_skip(u)) continue;
+            hook.tile_begin(u);
+        }
         const long long row = tile * (blockDim.x / TT) + rb;
         const bool valid = row < nrows;
         cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
@@ -634,6 +678,7 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
                 dst[M] = X;
             }
         }
+        if constexpr (hook_tiled<Hook>()) hook.tile_end();
     }
     hook.finish();
 }
@@ -654,6 +699,11 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         __syncthreads();  // smem of the previous tile fully consumed
+        if constexpr (hook_tiled<Hook>()) {
+            const long long u = tile * (blockDim.x / TT);
+            if (hook.tile_skip(u)) continue;
+            hook.tile_begin(u);
+        }
         const long long row = tile * (blockDim.x / TT) + rb;
         const bool valid = row < nrows;
         cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
@@ -686,6 +736,7 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
                 dst[j] = mkc<T>(x0, x1);
             }
         }
+        if constexpr (hook_tiled<Hook>()) hook.tile_end();
     }
     hook.finish();
 }
@@ -708,6 +759,11 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         __syncthreads();  // smem of the previous tile fully consumed
+        if constexpr (hook_tiled<Hook>()) {
+            const long long u = tile * (blockDim.x / TT);
+            if (hook.tile_skip(u)) continue;
+            hook.tile_begin(u);
+        }
         const long long row = tile * (blockDim.x / TT) + rb;
         const bool valid = row < nrows;
         cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
@@ -747,6 +803,7 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
                 rowp[M] = mkc<T>(z0.x - z0.y, T(0));
             }
         }
+        if constexpr (hook_tiled<Hook>()) hook.tile_end();
     }
     hook.finish();
 }
@@ -889,6 +946,11 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         __syncthreads();
+        if constexpr (hook_tiled<Hook>()) {
+            const long long u = tile * (blockDim.x / TT);
+            if (hook.tile_skip(u)) continue;
+            hook.tile_begin(u);
+        }
         const long long row = tile * (blockDim.x / TT) + rb;
         const bool valid = row < nrows;
         cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
@@ -900,6 +962,7 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
         const cplx<T> mid = natural_to_pairs<T, M, E>(v, t);
         split_store<T, M, E>(v, mid, t, valid, out + (valid ? row : 0) * out_stride,
                              row * out_stride, twp, hook);
+        if constexpr (hook_tiled<Hook>()) hook.tile_end();
     }
     hook.finish();
 }
@@ -918,6 +981,11 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         __syncthreads();
+        if constexpr (hook_tiled<Hook>()) {
+            const long long u = tile * (blockDim.x / TT);
+            if (hook.tile_skip(u)) continue;
+            hook.tile_begin(u);
+        }
         const long long row = tile * (blockDim.x / TT) + rb;
         const bool valid = row < nrows;
         cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
@@ -936,6 +1004,7 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
                 dst[j] = mkc<T>(x0, x1);
             }
         }
+        if constexpr (hook_tiled<Hook>()) hook.tile_end();
     }
     hook.finish();
 }
@@ -955,6 +1024,11 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     HookNone none;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         __syncthreads();
+        if constexpr (hook_tiled<Hook>()) {
+            const long long u = tile * (blockDim.x / TT);
+            if (hook.tile_skip(u)) continue;
+            hook.tile_begin(u);
+        }
         const long long row = tile * (blockDim.x / TT) + rb;
         const bool valid = row < nrows;
         cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
@@ -975,6 +1049,7 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
         stockham<T, M, E, 1, -1>(v, t, tw, x);
         mid = natural_to_pairs<T, M, E>(v, t);
         split_store<T, M, E>(v, mid, t, valid, rowp, row * stride, twp, none);
+        if constexpr (hook_tiled<Hook>()) hook.tile_end();
     }
     hook.finish();
 }

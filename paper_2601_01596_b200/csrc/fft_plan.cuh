@@ -76,6 +76,11 @@ template <class T>
 void launch_row_r2c(long long n2, const T* in, long long in_stride, cplx<T>* out,
                     long long out_stride, long long nrows, Twiddles<T>& tw, const int* gate,
                     cudaStream_t st);
+// Row R2C with an output hook (tiled hooks skip the rows of converged frames).
+template <class T, class Hook>
+void launch_row_r2c_hook(long long n2, const T* in, long long in_stride, cplx<T>* out,
+                         long long out_stride, long long nrows, Twiddles<T>& tw, const int* gate,
+                         Hook hook, cudaStream_t st);
 // Row C2R: half rows -> real rows, scaled.
 template <class T>
 void launch_row_c2r(long long n2, const cplx<T>* in, long long in_stride, T* out,

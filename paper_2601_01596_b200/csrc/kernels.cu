@@ -134,6 +134,63 @@ template __global__ void k_eps0_plus_s<float>(const float*, const float*, const 
 template __global__ void k_eps0_plus_s<double>(const double*, const double*, const double*,
                                                double*, long long);
 
+__global__ void k_frames_init(FrameCtl* fc, long long nframes, unsigned long long max_iters) {
+    for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < nframes;
+         f += (long long)gridDim.x * blockDim.x) {
+        FrameCtl c{};
+        c.max_iters = max_iters;
+        fc[f] = c;
+    }
+}
+
+__global__ void k_decide_frames(FrameCtl* fc, long long nframes, Ctl* ctl) {
+    for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < nframes;
+         f += (long long)gridDim.x * blockDim.x) {
+        FrameCtl& c = fc[f];
+        if (c.done) continue;
+        const double peak = bitsd(c.peak_bits);
+        const double ex = bitsd(c.exc_bits);
+        bool fin = false;
+        if (!(ex > 1e-11 * peak)) {           // projection.cpp:40, 106-111
+            c.converged = 1;
+            c.residual_f = 0.0;
+            fin = true;
+        } else if (c.passes >= c.max_iters) { // :112-116
+            c.converged = 0;
+            c.residual_f = ex;
+            fin = true;
+        } else {
+            c.passes += 1;
+        }
+        c.peak_bits = 0;
+        c.exc_bits = 0;
+        if (fin) {
+            c.done = 1;
+            if (atomicAdd(&ctl->count_b, 1ull) + 1 == static_cast<unsigned long long>(nframes))
+                ctl->done = 1;
+        }
+    }
+}
+
+template <class TI>
+__global__ void k_eps0_frames(const TI* __restrict__ orig, const TI* __restrict__ dec, double* eps,
+                              long long N, long long frameN, const double* __restrict__ E,
+                              double fscale, double slack, Ctl* ctl) {
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
+         n += (long long)gridDim.x * blockDim.x) {
+        const double e = static_cast<double>(dec[n]) - static_cast<double>(orig[n]);
+        eps[n] = e;
+        const double Eb = E[n / frameN];
+        if (fabs(e) > Eb * (1.0 + 0x1p-20)) atomicMin(&ctl->bad1, static_cast<unsigned long long>(n));
+        if (fabs(e) > Eb * fscale * (1.0 + slack))
+            atomicMin(&ctl->bad2, static_cast<unsigned long long>(n));
+    }
+}
+template __global__ void k_eps0_frames<float>(const float*, const float*, double*, long long,
+                                              long long, const double*, double, double, Ctl*);
+template __global__ void k_eps0_frames<double>(const double*, const double*, double*, long long,
+                                               long long, const double*, double, double, Ctl*);
+
 __global__ void k_cast_to_double(const float* __restrict__ in, double* out, long long N) {
     for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
          n += (long long)gridDim.x * blockDim.x)
@@ -239,36 +296,51 @@ __global__ void k_expand_full(const double2* __restrict__ half, double2* full, i
 
 // ---- FP64 gate ---------------------------------------------------------------------------------
 
+// The spatial gate processes U grid-stride windows per trip with all loads issued first (U
+// independent loads in flight per thread: 662 -> 484 us at 512^3; the same unroll made the
+// frequency gate slower, 693 -> 800 us, so it keeps one window per trip).
+constexpr int kGateU = 4;
+
 __global__ void k_gate_spatial(const double* __restrict__ S, long long N, SpatialB sb, int m,
                                double* spat_cur, unsigned* keep_words, unsigned* esc_words,
                                Ctl* ctl) {
     unsigned long long nz_acc = 0;
-    const long long n0 = blockIdx.x * (long long)blockDim.x;
-    for (long long base = n0; base < N; base += (long long)gridDim.x * blockDim.x) {
-        const long long n = base + threadIdx.x;
-        bool keep = false, ovf = false;
-        if (n < N) {
-            const double v = S[n];
-            const bool nz = v != 0.0;
-            const double step = ldexp(2.0 * sb.at(n), -m);       // editset.cpp:31-33
-            ovf = nz && (fabs(v) / step > kMaxIndex);            // pipeline.cpp:63-64
-            keep = nz && !ovf;
-            double cur = 0.0;
-            if (keep) {
-                const long long q = llround(v / step);           // editset.cpp:76-84
-                cur = static_cast<double>(static_cast<int>(q)) * step;  // editset.cpp:102
-            } else if (ovf) {
-                cur = v;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long base = blockIdx.x * (long long)blockDim.x; base < N; base += kGateU * stride) {
+        double v[kGateU], E[kGateU];
+#pragma unroll
+        for (int u = 0; u < kGateU; ++u) {
+            const long long n = base + u * stride + threadIdx.x;
+            v[u] = n < N ? S[n] : 0.0;
+            E[u] = n < N ? sb.at(n) : 1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kGateU; ++u) {
+            const long long n = base + u * stride + threadIdx.x;
+            if (base + u * stride >= N) break;                   // warp-uniform
+            bool keep = false, ovf = false;
+            if (n < N) {
+                const bool nz = v[u] != 0.0;
+                const double step = ldexp(2.0 * E[u], -m);       // editset.cpp:31-33
+                ovf = nz && (fabs(v[u]) / step > kMaxIndex);     // pipeline.cpp:63-64
+                keep = nz && !ovf;
+                double cur = 0.0;
+                if (keep) {
+                    const long long q = llround(v[u] / step);    // editset.cpp:76-84
+                    cur = static_cast<double>(static_cast<int>(q)) * step;  // editset.cpp:102
+                } else if (ovf) {
+                    cur = v[u];
+                }
+                spat_cur[n] = cur;
             }
-            spat_cur[n] = cur;
+            const unsigned bk = __ballot_sync(0xffffffffu, keep);
+            const unsigned be = __ballot_sync(0xffffffffu, ovf);
+            if ((threadIdx.x & 31) == 0 && n < N) {
+                keep_words[n >> 5] = bk;
+                esc_words[n >> 5] = be;
+            }
+            if ((threadIdx.x & 31) == 0) nz_acc += __popc(bk) + __popc(be);
         }
-        const unsigned bk = __ballot_sync(0xffffffffu, keep);
-        const unsigned be = __ballot_sync(0xffffffffu, ovf);
-        if ((threadIdx.x & 31) == 0 && n < N) {
-            keep_words[n >> 5] = bk;
-            esc_words[n >> 5] = be;
-        }
-        if ((threadIdx.x & 31) == 0) nz_acc += __popc(bk) + __popc(be);
     }
     block_sum_atomic(nz_acc, &ctl->act_s);
 }
@@ -445,39 +517,95 @@ __device__ __forceinline__ void codes_from_bits(const unsigned* __restrict__ wor
     __syncthreads();
     const unsigned long long boff = block_offsets[blockIdx.x];
     const unsigned lt = (1u << lane) - 1u;
-    for (int k = 0; k < 32; ++k) {
-        const int wl = warp * 32 + k;
-        const long long wg = wbase + wl;
-        if (wg >= nwords) break;
-        const unsigned word = sw[wl];
-        if (!word) continue;
-        if (word >> lane & 1u) emit(wg * 32 + lane, boff + s[wl] + __popc(word & lt));
+    if constexpr (requires { emit.batched; }) {
+        // four words per step: the emitter issues all four elements' loads before any store
+        for (int k0 = 0; k0 < 32; k0 += 4) {
+            long long nn[4];
+            unsigned long long pp[4];
+            bool act[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int wl = warp * 32 + k0 + u;
+                const long long wg = wbase + wl;
+                const unsigned word = wg < nwords ? sw[wl] : 0u;
+                act[u] = (word >> lane) & 1u;
+                nn[u] = wg * 32 + lane;
+                pp[u] = boff + s[wl] + __popc(word & lt);
+            }
+            emit(nn, pp, act);
+        }
+    } else {
+        for (int k = 0; k < 32; ++k) {
+            const int wl = warp * 32 + k;
+            const long long wg = wbase + wl;
+            if (wg >= nwords) break;
+            const unsigned word = sw[wl];
+            if (!word) continue;
+            if (word >> lane & 1u) emit(wg * 32 + lane, boff + s[wl] + __popc(word & lt));
+        }
     }
 }
+
+// batched emitters of the two code kernels (loads of four elements first, then the stores)
+struct EmitCodesS {
+    static constexpr bool batched = true;
+    const double* __restrict__ S;
+    SpatialB sb;
+    int m;
+    int* codes;
+    __device__ __forceinline__ void operator()(const long long (&n)[4],
+                                               const unsigned long long (&pos)[4],
+                                               const bool (&act)[4]) const {
+        double v[4], e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            v[u] = act[u] ? S[n[u]] : 0.0;
+            e[u] = act[u] ? sb.at(n[u]) : 1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (act[u]) codes[pos[u]] = static_cast<int>(llround(v[u] / ldexp(2.0 * e[u], -m)));
+    }
+};
+
+struct EmitCodesF {
+    static constexpr bool batched = true;
+    const double2* __restrict__ F;
+    HalfGeom g;
+    FreqB fb;
+    int m;
+    int* codes;
+    __device__ __forceinline__ void operator()(const long long (&h)[4],
+                                               const unsigned long long (&pos)[4],
+                                               const bool (&act)[4]) const {
+        double2 v[4], d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long off = act[u] ? g.offset_of(h[u]) : 0;
+            v[u] = act[u] ? F[off] : make_double2(0.0, 0.0);
+            d[u] = act[u] ? fb.at2(off) : make_double2(1.0, 1.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (act[u])
+                reinterpret_cast<int2*>(codes)[pos[u]] =
+                    make_int2(static_cast<int>(llround(v[u].x / ldexp(2.0 * d[u].x, -m))),
+                              static_cast<int>(llround(v[u].y / ldexp(2.0 * d[u].y, -m))));
+    }
+};
 } // namespace
 
 __global__ void k_codes_spatial_bits(const unsigned* __restrict__ keep_words, long long nwords,
                                      const unsigned long long* __restrict__ block_offsets,
                                      const double* __restrict__ S, SpatialB sb, int m, int* codes) {
-    codes_from_bits(keep_words, nwords, block_offsets, [&](long long n, unsigned long long pos) {
-        const double step = ldexp(2.0 * sb.at(n), -m);
-        codes[pos] = static_cast<int>(llround(S[n] / step));
-    });
+    codes_from_bits(keep_words, nwords, block_offsets, EmitCodesS{S, sb, m, codes});
 }
 
 __global__ void k_codes_freq_bits(const unsigned* __restrict__ keep_words, long long nwords,
                                   const unsigned long long* __restrict__ block_offsets,
                                   const double2* __restrict__ F, HalfGeom g, FreqB fb, int m,
                                   int* codes) {
-    codes_from_bits(keep_words, nwords, block_offsets, [&](long long h, unsigned long long pos) {
-        const long long off = g.offset_of(h);
-        const double2 v = F[off];
-        const double2 d = fb.at2(off);
-        const double sre = ldexp(2.0 * d.x, -m);
-        const double sim = ldexp(2.0 * d.y, -m);
-        reinterpret_cast<int2*>(codes)[pos] = make_int2(static_cast<int>(llround(v.x / sre)),
-                                                        static_cast<int>(llround(v.y / sim)));
-    });
+    codes_from_bits(keep_words, nwords, block_offsets, EmitCodesF{F, g, fb, m, codes});
 }
 
 // dequantize_edits (editset.cpp:106-133) scattered to the flagged positions (expand_edits,

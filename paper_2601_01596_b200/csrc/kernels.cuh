@@ -236,6 +236,146 @@ template <class TI>
 __global__ void k_eps0_plus_s(const TI* __restrict__ orig, const TI* __restrict__ dec,
                               const double* __restrict__ S, double* out, long long N);
 
+// ---- batched frames (BASELINE config 3): one projection loop over a stack of 2-D frames --------
+// Every frame keeps its own control block, bounds and decision (each frame is an independent
+// correct(), pipeline.cpp:26-178); the passes run over the whole stack and skip the tiles of
+// frames that have converged, so a frame's state freezes exactly where its own loop stops.
+// Tiled hooks (kTiled) get tile_skip / tile_begin / tile_end around every tile (CTA-uniform);
+// `unit` is the tile's plane (column passes along axis 1: plane = frame) or its first row (row
+// passes: frame = row / rows_per_frame).
+struct FrameCtl {
+    unsigned long long peak_bits, exc_bits, passes, max_iters;
+    int done, converged;
+    double residual_f;
+};
+
+struct FrameBatch {
+    FrameCtl* fc;
+    const double* E;          // spatial bound per frame
+    const double* D;          // frequency bound per frame
+    double fscale;            // 1 - 2^-m (working bounds)
+    long long rows_per_frame; // n1
+    __device__ __forceinline__ long long frame_of(long long unit, bool rows) const {
+        return rows ? unit / rows_per_frame : unit;
+    }
+    __device__ __forceinline__ bool done(long long f) const {
+        return *reinterpret_cast<const volatile int*>(&fc[f].done) != 0;
+    }
+    __device__ __forceinline__ bool first(long long f) const {
+        return *reinterpret_cast<const volatile unsigned long long*>(&fc[f].passes) == 1;
+    }
+};
+
+template <bool kRows>
+struct HookSkipB {  // plain pass that only skips converged frames
+    static constexpr bool kTiled = true;
+    FrameBatch fb;
+    __device__ __forceinline__ bool tile_skip(long long u) const { return fb.done(fb.frame_of(u, kRows)); }
+    __device__ __forceinline__ void tile_begin(long long) {}
+    __device__ __forceinline__ void tile_end() {}
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    template <class C> __device__ __forceinline__ void post(C&, long long, int) {}
+    template <class T> __device__ __forceinline__ void post_real(T&, T&, long long) {}
+    __device__ __forceinline__ void finish() {}
+};
+
+// check_convergence per frame (projection.cpp:29-52), flushed per tile to the frame's block
+struct HookFReduceB {
+    static constexpr bool kTiled = true;
+    FrameBatch fb;
+    long long frame = 0;
+    double d = 0.0, peak = 0.0, ex = 0.0;
+    __device__ __forceinline__ bool tile_skip(long long u) const { return fb.done(u); }
+    __device__ __forceinline__ void tile_begin(long long u) {
+        frame = u;
+        d = fb.D[u] * fb.fscale;
+        peak = 0.0;
+        ex = 0.0;
+    }
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    template <class C>
+    __device__ __forceinline__ void post(C& v, long long, int) {
+        const double ar = fabs(static_cast<double>(v.x)), ai = fabs(static_cast<double>(v.y));
+        peak = fmax(peak, fmax(ar, ai));
+        const double e = fmax(ar - d, ai - d);
+        if (e > ex) ex = e;
+    }
+    __device__ __forceinline__ void tile_end() {
+        block_max2_atomic(peak, ex, &fb.fc[frame].peak_bits, &fb.fc[frame].exc_bits);
+    }
+    __device__ __forceinline__ void finish() {}
+};
+
+// project_onto_fcube per frame (projection.cpp:54-66): F dense on the frame's first clip, clip
+// map afterwards (HookFClip rebuild mode)
+template <class T>
+struct HookFClipB {
+    static constexpr bool kTiled = true;
+    FrameBatch fb;
+    double2* F;
+    unsigned char* moved;
+    double d = 0.0;
+    bool first = false;
+    __device__ __forceinline__ bool tile_skip(long long u) const { return fb.done(u); }
+    __device__ __forceinline__ void tile_begin(long long u) {
+        d = fb.D[u] * fb.fscale;
+        first = fb.first(u);
+    }
+    template <class C>
+    __device__ __forceinline__ void pre(C& v, long long off, int) {
+        const double re = v.x, im = v.y;
+        const double cre = clamp_abs(re, d), cim = clamp_abs(im, d);
+        const double xre = cre - re, xim = cim - im;
+        if (first) F[off] = make_double2(0.0 + xre, 0.0 + xim);
+        if (xre != 0.0 || xim != 0.0) moved[off] = 1;
+        v.x = static_cast<T>(cre);
+        v.y = static_cast<T>(cim);
+    }
+    template <class C> __device__ __forceinline__ void post(C&, long long, int) {}
+    __device__ __forceinline__ void tile_end() {}
+    __device__ __forceinline__ void finish() {}
+};
+
+// project_onto_scube per frame (projection.cpp:68-79) on the C2R outputs
+template <class T>
+struct HookSClipB {
+    static constexpr bool kTiled = true;
+    FrameBatch fb;
+    double* S;
+    double e = 0.0;
+    bool first = false;
+    __device__ __forceinline__ bool tile_skip(long long u) const { return fb.done(fb.frame_of(u, true)); }
+    __device__ __forceinline__ void tile_begin(long long u) {
+        const long long f = fb.frame_of(u, true);
+        e = fb.E[f] * fb.fscale;
+        first = fb.first(f);
+    }
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    __device__ __forceinline__ T one(T x, long long n) const {
+        const double xd = x;
+        const double c = clamp_abs(xd, e);
+        const double dd = c - xd;
+        if (first) S[n] = 0.0 + dd;
+        else if (dd != 0.0) S[n] = __ldg(&S[n]) + dd;
+        return static_cast<T>(c);
+    }
+    __device__ __forceinline__ void post_real(T& x0, T& x1, long long n) {
+        x0 = one(x0, n);
+        x1 = one(x1, n + 1);
+    }
+    __device__ __forceinline__ void tile_end() {}
+    __device__ __forceinline__ void finish() {}
+};
+
+// loop decision per frame (projection.cpp:106-116); the last frame to finish sets ctl->done
+__global__ void k_decide_frames(FrameCtl* fc, long long nframes, Ctl* ctl);
+__global__ void k_frames_init(FrameCtl* fc, long long nframes, unsigned long long max_iters);
+// compute_error + preconditions of every frame (pipeline.cpp:31-42; first failing index)
+template <class TI>
+__global__ void k_eps0_frames(const TI* __restrict__ orig, const TI* __restrict__ dec, double* eps,
+                              long long N, long long frameN, const double* __restrict__ E,
+                              double fscale, double slack, Ctl* ctl);
+
 // ---- FP64 gate hooks (fused into the round / verify passes) -----------------------------------------
 
 __device__ __forceinline__ void set_bit_g(unsigned* words, long long i) {
