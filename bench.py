@@ -525,6 +525,8 @@ def main():
     ap.add_argument("--frames", type=int, default=1024)
     ap.add_argument("--frame-n", type=int, default=2048)
     ap.add_argument("--lanes", type=int, default=8)
+    ap.add_argument("--policy", default="fp64", choices=["fp64", "mixed"],
+                    help="precision policy of the projection loop (nyx / combustion configs)")
     ap.add_argument("--ref-n", type=int, default=64)
     ap.add_argument("--cpu-n", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -574,7 +576,7 @@ def main():
 
     def step():
         return P.correct(orig, dec, bounds, 16, 1000, "f32", want_archive=False, want_edits=False,
-                         want_corrected=False, ctx=ctx)
+                         want_corrected=False, policy=args.policy, ctx=ctx)
 
     for _ in range(args.warmup):
         r = step()
@@ -686,13 +688,16 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload,
-                       "n": n, "m": 16, "policy": "fp64 (reference control flow)",
+                       "n": n, "m": 16,
+                       "policy": "fp64 (reference control flow)" if args.policy == "fp64" else
+                                 "mixed (FP32 phase until excess/peak <= 1e-4, then FP64)",
                        "l2": f"inputs larger than L2 ({4 * N / 1e9:.2f} GB per field, 126 MB L2)",
                        "parallelism": f"independent volumes x{world}"},
             "ms_per_iteration": float(np.mean(loop_ms) / max(1.0, np.mean(iters))),
             "lib_timings_ms": {k: float(np.mean([r.timings_ms[k] for r in results]))
                                for k in results[0].timings_ms},
             "iterations": iters[0],
+            "iterations_fp32": results[0].iterations_fp32,
             "escape_rounds": results[0].escape_rounds, "escapes": results[0].escape_count,
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s",

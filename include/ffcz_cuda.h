@@ -76,7 +76,10 @@ typedef struct ffcz_bounds_desc {
 /* Arithmetic policy of the projection loop.
  *  FFCZ_POLICY_FP64: every pass in FP64 with the reference control flow (K3a/K3b split):
  *                    iterations, flags and values follow the reference to FFT round-off.
- *  FFCZ_POLICY_MIXED: FP32 fused passes while excess/peak > tau_switch, then FP64.
+ *  FFCZ_POLICY_MIXED: FP32 fused passes while excess/peak > tau_switch, then FP64 with the
+ *                    reference control flow: iterations within +-1 of the
+ *                    reference, both bounds still hold exactly (FP64 gate).  Fused shapes only
+ *                    (others run FP64); batched frames run it per frame on the lanes.
  *  The FP64 gate (escape repair + verify) always runs in FP64. */
 typedef enum ffcz_cuda_policy { FFCZ_POLICY_FP64 = 0, FFCZ_POLICY_MIXED = 1 } ffcz_cuda_policy;
 

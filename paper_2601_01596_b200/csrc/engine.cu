@@ -289,13 +289,14 @@ struct LoopResult {
     double residual_f = 0.0;
     bool fused = false;
     const unsigned char* moved = nullptr;  // rebuild mode: F is complete only after pass 1
+    unsigned long long passes32 = 0;       // mixed policy: passes run by the FP32 phase
 };
 
 // The POCS loop (projection.cpp:96-126) on device.  eps holds epsilon0 on entry and the final
 // epsilon on exit; S (N) and F (half) are the accumulated edits.
 LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Bounds& bw,
                     double fscale, bool allow_fused, double* S, double2* F,
-                    bool allow_rebuild = true) {
+                    bool allow_rebuild = true, bool keep_moved = false) {
     cudaStream_t st = c.st;
     FftPlan<double> plan{g, &c.tw64};
     const int* gate = &c.ctl->done;
@@ -309,9 +310,9 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
     }
     const bool three_d = g.d[0] > 1;
     unsigned char* moved = nullptr;
-    if (fused && allow_rebuild && f_rebuild_enabled()) {
+    if (fused && (keep_moved || (allow_rebuild && f_rebuild_enabled()))) {
         moved = c.b<unsigned char>("f_moved", g.half_elems());
-        FFCZ_CUDA_CHECK(cudaMemsetAsync(moved, 0, g.half_elems(), st));
+        if (!keep_moved) FFCZ_CUDA_CHECK(cudaMemsetAsync(moved, 0, g.half_elems(), st));
     }
     const int za = complete_axis(three_d);  // the pass that completes the forward transform
     const int mid = 1 - za;                   // the other column axis (3-D only)
@@ -722,6 +723,71 @@ void finish_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& fd
                   const LoopResult& lr, double* eps, double* S, double2* F, double2* delta_star,
                   const ffcz_cuda_options& opt, ffcz_cuda_result* out);
 
+// Mixed policy, FP32 phase: the fused loop in FP32 (spectrum and
+// iterate in FP32, half the bytes per pass; S and F accumulate in FP64 inside the hooks) until
+// max_excess <= tau * peak (k_decide32), then eps <- FP64(eps32) and the FP64 loop continues
+// with the reference control flow (run_loop, keep_moved).  Returns false when the shape has no
+// fused FP32 path (the FP64 loop then runs alone).
+bool run_phase32(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Bounds& bw, double fscale,
+                 double tau, double* S, double2* F) {
+    cudaStream_t st = c.st;
+    FftPlan<float> plan{g, &c.tw32};
+    if (!plan.fused_ok()) return false;
+    const bool three_d = g.d[0] > 1;
+    const int za = complete_axis(three_d), mid = 1 - za;
+    float* eps32 = c.b<float>("eps32", g.N);
+    float2* spec = c.b<float2>("spec32", g.half_elems());
+    unsigned char* moved = c.b<unsigned char>("f_moved", g.half_elems());
+    FFCZ_CUDA_CHECK(cudaMemsetAsync(moved, 0, g.half_elems(), st));
+    FFCZ_CUDA_CHECK(cudaMemcpyAsync(&c.ctl->tau, &tau, sizeof(double), cudaMemcpyHostToDevice, st));
+    const int* gate = &c.ctl->switch_now;
+    const float invN = static_cast<float>(1.0 / static_cast<double>(g.N));
+    k_cast_to_float<<<grid_for(g.N), 256, 0, st>>>(eps, eps32, g.N);
+    launch_row_r2c<float>(g.n2, eps32, g.n2, spec, g.P, g.rows, c.tw32, gate, st);
+    if (three_d) plan.col(mid, -1, spec, spec, gate, HookNone{}, st);
+    FFCZ_LAUNCH_CHECK();
+    c.launches += three_d ? 3 : 2;
+    auto body = [&]() {
+        plan.col(za, -1, spec, spec, gate, HookFReduce{bw.fb, fscale, c.ctl}, st);          // K3a
+        k_decide32<<<1, 1, 0, st>>>(c.ctl);
+        plan.col(za, +1, spec, spec, gate, HookFClip<float>{bw.fb, fscale, F, c.ctl, moved}, st);
+        if (three_d) plan.col(mid, +1, spec, spec, gate, HookNone{}, st);
+        launch_row_c2r_hook<float>(g.n2, spec, g.P, eps32, g.n2, g.rows, invN, c.tw32, gate,
+                                   HookSClip<float>{bw.sb, fscale, S, nullptr, c.ctl}, st);
+        launch_row_r2c<float>(g.n2, eps32, g.n2, spec, g.P, g.rows, c.tw32, gate, st);
+        if (three_d) plan.col(mid, -1, spec, spec, gate, HookNone{}, st);
+        FFCZ_LAUNCH_CHECK();
+        c.launches += three_d ? 7 : 5;
+    };
+    static const int kChunk[] = {1, 1, 2, 4};
+    int ci = 0, issued = 0;
+    std::vector<std::pair<cudaEvent_t, int>> inflight;
+    auto issue_chunk = [&]() {
+        const int n = kChunk[std::min(ci++, 3)];
+        for (int i = 0; i < n; ++i) body();
+        const int slot = issued % 2;
+        k_export_ctl<<<1, 32, 0, st>>>(c.ctl, &c.hctl_dev[1 + slot]);
+        FFCZ_LAUNCH_CHECK();
+        cudaEvent_t ev = c.ev[4 + slot];
+        FFCZ_CUDA_CHECK(cudaEventRecord(ev, st));
+        inflight.push_back({ev, slot});
+        ++issued;
+    };
+    issue_chunk();
+    for (;;) {
+        issue_chunk();
+        auto p = inflight.front();
+        inflight.erase(inflight.begin());
+        FFCZ_CUDA_CHECK(cudaEventSynchronize(p.first));
+        if (c.hctl[1 + p.second].switch_now) break;
+    }
+    // hand over: the FP64 loop starts from the FP32 iterate (its next check is in FP64)
+    k_cast_to_double<<<grid_for(g.N), 256, 0, st>>>(eps32, eps, g.N);
+    FFCZ_LAUNCH_CHECK();
+    ++c.launches;
+    return true;
+}
+
 template <class TI>
 void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& fd,
                    const void* orig_in, const void* dec_in, const ffcz_bounds_desc& bd, int m,
@@ -770,7 +836,11 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     double* S = c.b<double>("S", N);
     double2* F = c.b<double2>("F", g.half_elems());
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[2], st));
-    const LoopResult lr = run_loop(c, g, eps, bo, f, !(opt.flags & FFCZ_FORCE_UNFUSED), S, F);
+    const bool mixed = opt.policy == FFCZ_POLICY_MIXED && !(opt.flags & FFCZ_FORCE_UNFUSED) &&
+                       run_phase32(c, g, eps, bo, f, opt.tau_switch, S, F);
+    LoopResult lr = run_loop(c, g, eps, bo, f, !(opt.flags & FFCZ_FORCE_UNFUSED), S, F, true,
+                             mixed);
+    if (mixed) lr.passes32 = c.read_ctl().passes32;
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[3], st));
     finish_typed<TI>(c, g, fd, orig, dec, bd, bo, m, lr, eps, S, F,
                      c.b<double2>("spec", g.half_elems()), opt, out);
@@ -839,8 +909,8 @@ void finish_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& fd
     out->report.converged = lr.converged;
     out->report.residual_f = lr.residual_f;
     out->report.residual_s = bitsd_host(h.res_s_bits);
-    out->iterations_fp32 = 0;
-    out->iterations_fp64 = lr.passes;
+    out->iterations_fp32 = lr.passes32;
+    out->iterations_fp64 = lr.passes - lr.passes32;
     out->escape_rounds = go.rounds;
     out->verify_ok = go.verify_ok;
     out->verify_max_spatial_excess = go.vs;
@@ -1316,8 +1386,10 @@ int ffcz_cuda_correct(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const vo
         ffcz_cuda_options opt;
         ffcz_cuda_default_options(&opt);
         if (opt_in) opt = *opt_in;
-        if (opt.policy != FFCZ_POLICY_FP64)
-            throw Error(kUnsupported, "only FFCZ_POLICY_FP64 is implemented in this build");
+        if (opt.policy != FFCZ_POLICY_FP64 && opt.policy != FFCZ_POLICY_MIXED)
+            throw Error(kValidation, "unknown precision policy");
+        if (opt.policy == FFCZ_POLICY_MIXED && !(opt.tau_switch > 0.0 && opt.tau_switch < 1.0))
+            throw Error(kValidation, "mixed policy: tau_switch must be in (0, 1)");
         const Geometry g = make_geometry(field->ndim, field->dims, kPitchAlign);
         const unsigned long long l0 = ctx->launches;
         if (field->dtype == FFCZ_F32)
@@ -1348,8 +1420,8 @@ int ffcz_cuda_correct_batch(ffcz_cuda_ctx* ctx, const ffcz_field_desc* frame, ui
         ffcz_cuda_options opt;
         ffcz_cuda_default_options(&opt);
         if (opt_in) opt = *opt_in;
-        if (opt.policy != FFCZ_POLICY_FP64)
-            throw Error(kUnsupported, "only FFCZ_POLICY_FP64 is implemented in this build");
+        if (opt.policy != FFCZ_POLICY_FP64 && opt.policy != FFCZ_POLICY_MIXED)
+            throw Error(kValidation, "unknown precision policy");
         for (uint64_t i = 0; i < nframes; ++i) std::memset(&out[i], 0, sizeof(out[i]));
         if (nframes == 0) return;
         const Geometry g = make_geometry(frame->ndim, frame->dims, kPitchAlign);
@@ -1357,6 +1429,7 @@ int ffcz_cuda_correct_batch(ffcz_cuda_ctx* ctx, const ffcz_field_desc* frame, ui
         if (lanes <= 0) lanes = 8;
         const int nl = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(lanes), nframes));
         bool fused = frames_fused_enabled() && frame->ndim == 2 &&
+                     opt.policy == FFCZ_POLICY_FP64 &&
                      !(opt.flags & FFCZ_FORCE_UNFUSED) && g.d[1] >= 64 && g.n2 >= 64 &&
                      radix_col_ok(g.d[1]) && radix_row_ok(g.n2);
         for (uint64_t i = 0; fused && i < nframes; ++i)

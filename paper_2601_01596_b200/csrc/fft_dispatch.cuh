@@ -146,8 +146,11 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
             while (B1 > 1 && col_tma1_smem_bytes<T, L, E1>(B1) > 220 * 1024) B1 /= 2;
             B1 = std::min(B1, pow2_ceil(ncols));
             const bool outer = sizeof(T) == 8 && role == TileRole::kFirst;
+            // (FP32 runs E = 32 here, which spills at 512 threads: 0.70 -> 0.47 of HBM on the
+            // 1024^3 middle axis, so FP32 keeps double buffering unless forced)
             const bool want = !side && mode != 0 && TT1 * B1 >= 32 &&
-                              (mode == 1 || (B1 > Bt && (Bt * sizeof(cplx<T>) < 128 || outer)));
+                              (mode == 1 || (sizeof(T) == 8 && B1 > Bt &&
+                                             (Bt * sizeof(cplx<T>) < 128 || outer)));
             CUtensorMap map1;
             if (want && encode_col_map(&map1, src, sizeof(T), ncols, L, row_stride, nplanes,
                                        plane_stride, B1, L < 256 ? L : 256, true)) {

@@ -191,6 +191,30 @@ template __global__ void k_eps0_frames<float>(const float*, const float*, double
 template __global__ void k_eps0_frames<double>(const double*, const double*, double*, long long,
                                                long long, const double*, double, double, Ctl*);
 
+__global__ void k_cast_to_float(const double* __restrict__ in, float* out, long long N) {
+    for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
+         n += (long long)gridDim.x * blockDim.x)
+        out[n] = static_cast<float>(in[n]);
+}
+
+// Mixed policy, FP32 phase: the phase never declares convergence (its
+// round-off is far above the reference's 1e-11 * peak); it hands over to the FP64 phase once
+// max_excess <= tau * peak or at the iteration cap, and clips otherwise.
+__global__ void k_decide32(Ctl* ctl) {
+    if (ctl->switch_now) return;
+    const double peak = bitsd(ctl->peak_bits);
+    const double ex = bitsd(ctl->exc_bits);
+    if (!(ex > ctl->tau * peak) || ctl->passes >= ctl->max_iters) {
+        ctl->switch_now = 1;
+        ctl->phase = 1;
+    } else {
+        ctl->passes += 1;
+        ctl->passes32 += 1;
+    }
+    ctl->peak_bits = 0;
+    ctl->exc_bits = 0;
+}
+
 __global__ void k_cast_to_double(const float* __restrict__ in, double* out, long long N) {
     for (long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x; n < N;
          n += (long long)gridDim.x * blockDim.x)

@@ -595,6 +595,9 @@ __global__ void k_eps0(const TI* __restrict__ orig, const TI* __restrict__ dec, 
                        long long N, SpatialB sb, double fscale, double slack, int check_original,
                        Ctl* ctl);
 __global__ void k_cast_to_double(const float* __restrict__ in, double* out, long long N);
+__global__ void k_cast_to_float(const double* __restrict__ in, float* out, long long N);
+// mixed policy: FP32-phase decision (switch to FP64 when excess <= tau * peak)
+__global__ void k_decide32(Ctl* ctl);
 // loop decision (projection.cpp:106-116,125)
 __global__ void k_decide(Ctl* ctl);
 __global__ void k_ctl_init(Ctl* ctl, unsigned long long max_iters);

@@ -152,6 +152,7 @@ class CorrectionResult:
     escape_rounds: int
     timings_ms: dict
     kernel_launches: int
+    iterations_fp32: int = 0     # mixed policy: clip passes run by the FP32 phase
 
 
 class _ResultHolder:
@@ -233,7 +234,7 @@ def _bounds_desc(b: DualBounds, m: _Marshal):
 
 
 def _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level,
-             device_encode=False):
+             device_encode=False, policy="fp64", tau=1e-4):
     lib = capi.load()
     opt = capi.Options()
     lib.ffcz_cuda_default_options(C.byref(opt))
@@ -251,6 +252,10 @@ def _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level
     if device_encode:
         flags |= capi.FFCZ_DEVICE_ENCODE
     opt.flags = flags
+    if policy not in ("fp64", "mixed"):
+        raise ValidationError(f"unknown precision policy {policy!r}")
+    opt.policy = 1 if policy == "mixed" else 0
+    opt.tau_switch = float(tau)
     opt.zlib_level = zlib_level
     return opt
 
@@ -302,7 +307,7 @@ def _convert(holder, shape, want_archive, want_edits, want_corrected, copy):
                            float(res.verify_max_spatial_excess),
                            float(res.verify_max_freq_excess), sflags, fflags, scodes, fcodes,
                            escapes, corrected, int(res.escape_rounds), timings,
-                           int(res.kernel_launches))
+                           int(res.kernel_launches), int(res.iterations_fp32))
     if copy:
         holder.free()
     else:
@@ -328,8 +333,8 @@ def _field_of(original, decompressed):
 def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: int = 1000,
             precision: str | None = None, *, want_archive: bool = True, want_edits: bool = True,
             want_corrected: bool = True, zlib_level: int = 9, fused: bool = True,
-            copy: bool = True, device_encode: bool = False,
-            ctx: Context | None = None) -> CorrectionResult:
+            copy: bool = True, device_encode: bool = False, policy: str = "fp64",
+            tau: float = 1e-4, ctx: Context | None = None) -> CorrectionResult:
     """ffcz::correct (pipeline.cpp:26-178) on the GPU.
 
     original / decompressed: numpy arrays (host; float32 or float64) or CUDA torch tensors (then
@@ -338,6 +343,8 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
     views of the library's pinned result buffers, valid while the returned object is alive.
     device_encode: zigzag + canonical Huffman of the archive's index streams on the GPU (same
     payload bytes as huffman.cpp); zlib_level then sets the host outer stage (0 = stored).
+    policy: "fp64" (reference control flow in FP64, default) or "mixed" (FP32 passes while
+    max_excess / peak > tau, then FP64; iterations within +-1 of the reference).
     """
     ctx = ctx or default_context()
     lib = capi.load()
@@ -349,7 +356,7 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
     fd = _field_desc(shape, capi.FFCZ_F32 if is32 else capi.FFCZ_F64, precision)
     bd = _bounds_desc(bounds, mar)
     opt = _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level,
-                   device_encode)
+                   device_encode, policy, tau)
     if on_dev:
         _order_after_torch(original, decompressed, bounds.spatial, bounds.freq_re, bounds.freq_im)
     holder = _ResultHolder()

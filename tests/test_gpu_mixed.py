@@ -1,0 +1,71 @@
+"""Mixed FP32 -> FP64 policy (BASELINE north star: FP32 with
+iteration counts within +-1 and both bounds exact).  Against the reference's golden outputs:
+converged flag equal, iterations within +-1, both bounds hold exactly on the FP64 corrected field
+(the gate is FP64), flags and codes agree on >= 99 % of entries."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import cases
+from oracle import ffcz_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(cases.GOLDEN, "golden.json")))
+ARCH = dict(np.load(os.path.join(cases.GOLDEN, "archives.npz")))
+NAMES = ["config1_c2.0", "config1_c1.0", "config1_c0.6", "config1_c0.4", "config4_comb32",
+         "config3_frame256", "config2_rho32", "m8_32cube"]
+CASES = [c for c in cases.all_cases() if c.name in NAMES]
+
+
+@pytest.fixture(scope="module")
+def ffcz():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_2601_01596_b200 as P
+    return P
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c.name for c in CASES])
+def test_mixed_policy(ffcz, case):
+    g = GOLD[case.name]
+    b = ffcz.DualBounds(case.E, case.Dre, case.Dim)
+    r = ffcz.correct(case.original, case.decompressed, b, case.m, case.max_iters, case.precision,
+                     policy="mixed")
+    assert r.report.converged == g["converged"]
+    assert abs(r.report.iterations - g["iterations"]) <= 1, (r.report.iterations, g["iterations"])
+    assert r.verify_ok
+    ok, ms, mf = O.verify_bounds(case.original, r.corrected, O.DualBounds(case.E, case.Dre, case.Dim))
+    assert ms == 0.0
+    assert mf <= 1e-12 * float(np.max(np.abs(np.asarray(case.Dre))))
+    mine = O.read_archive(r.archive_bytes)
+    if case.name in ARCH:
+        ref = O.read_archive(ARCH[case.name].tobytes())
+        assert np.mean(mine.spatial_flags == ref.spatial_flags) >= 0.99
+        assert np.mean(mine.frequency_flags == ref.frequency_flags) >= 0.99
+        if np.array_equal(mine.frequency_flags, ref.frequency_flags) and ref.frequency_codes.size:
+            assert np.mean(mine.frequency_codes == ref.frequency_codes) >= 0.99
+
+
+def test_mixed_uses_fp32_phase(ffcz):
+    case = {c.name: c for c in CASES}["config1_c0.4"]
+    b = ffcz.DualBounds(case.E, case.Dre, case.Dim)
+    r = ffcz.correct(case.original, case.decompressed, b, case.m, case.max_iters, case.precision,
+                     policy="mixed", want_archive=False)
+    f64 = ffcz.correct(case.original, case.decompressed, b, case.m, case.max_iters,
+                       case.precision, want_archive=False)
+    assert r.report.iterations >= 2 and f64.report.iterations >= 2
+    # corrected fields agree to the FP32 phase's perturbation (<< E)
+    assert np.max(np.abs(r.corrected - f64.corrected)) <= 1e-3 * case.E
+
+
+def test_policy_validation(ffcz):
+    case = CASES[0]
+    b = ffcz.DualBounds(case.E, case.Dre, case.Dim)
+    with pytest.raises(ffcz.ValidationError):
+        ffcz.correct(case.original, case.decompressed, b, policy="fp16")
+    with pytest.raises(ffcz.ValidationError):
+        ffcz.correct(case.original, case.decompressed, b, policy="mixed", tau=2.0)
