@@ -51,13 +51,16 @@ def test_mixed_policy(ffcz, case):
 
 
 def test_mixed_uses_fp32_phase(ffcz):
-    case = {c.name: c for c in CASES}["config1_c0.4"]
+    case = {c.name: c for c in CASES}["config1_c1.0"]   # 11 iterations in the reference
     b = ffcz.DualBounds(case.E, case.Dre, case.Dim)
     r = ffcz.correct(case.original, case.decompressed, b, case.m, case.max_iters, case.precision,
                      policy="mixed", want_archive=False)
     f64 = ffcz.correct(case.original, case.decompressed, b, case.m, case.max_iters,
                        case.precision, want_archive=False)
-    assert r.report.iterations >= 2 and f64.report.iterations >= 2
+    assert f64.iterations_fp32 == 0
+    assert r.iterations_fp32 >= 1                           # the FP32 phase ran
+    assert r.report.iterations - r.iterations_fp32 >= 1     # and handed over to FP64
+    assert abs(r.report.iterations - f64.report.iterations) <= 1
     # corrected fields agree to the FP32 phase's perturbation (<< E)
     assert np.max(np.abs(r.corrected - f64.corrected)) <= 1e-3 * case.E
 
