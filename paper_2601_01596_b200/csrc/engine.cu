@@ -206,6 +206,17 @@ constexpr int kPitchAlign = 16;
 // MIDDLE axis (row stride P: a tile's rows sit inside one plane, so the hooks' F / Delta accesses
 // stay TLB- and DRAM-page-local), with the outer axis transformed first.  FFCZ_COMPLETE_AXIS=0
 // restores the outer axis (A/B runs).  2-D fields have only axis 1.
+// FFCZ_EPS0_FUSION=1: form eps0 inside the first R2C instead of a separate eps0 pass.  Off by
+// default: measured at 512^3 the fused kernel (840 us, 2.5 TB/s) is slower than the two passes
+// it replaces (376 + 343 us), so the separate pass stays.
+inline bool eps0_fusion_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_EPS0_FUSION");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 // FFCZ_F_REBUILD=0: accumulate F in every clip pass (read-modify-write) instead of marking the
 // moved components and rebuilding F once at the gate (HookFClip::moved, HookFRebuild).
 inline bool f_rebuild_enabled() {
@@ -290,13 +301,15 @@ struct LoopResult {
     bool fused = false;
     const unsigned char* moved = nullptr;  // rebuild mode: F is complete only after pass 1
     unsigned long long passes32 = 0;       // mixed policy: passes run by the FP32 phase
+    bool s_zero = false;                   // fused loop: no spatial clip ever moved a sample
 };
 
 // The POCS loop (projection.cpp:96-126) on device.  eps holds epsilon0 on entry and the final
 // epsilon on exit; S (N) and F (half) are the accumulated edits.
 LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Bounds& bw,
                     double fscale, bool allow_fused, double* S, double2* F,
-                    bool allow_rebuild = true, bool keep_moved = false) {
+                    bool allow_rebuild = true, bool keep_moved = false,
+                    bool have_r2c = false) {
     cudaStream_t st = c.st;
     FftPlan<double> plan{g, &c.tw64};
     const int* gate = &c.ctl->done;
@@ -367,7 +380,7 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
     };
 
     if (fused) {
-        {
+        if (!have_r2c) {  // (else the caller's fused eps0 + R2C already filled `spec`)
             Prof p(c, kRowR2C, 8.0 * g.N + 16.0 * g.Nc());
             launch_row_r2c<double>(g.n2, eps, g.n2, spec, g.P, g.rows, c.tw64, gate, st);
         }
@@ -416,6 +429,7 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
     r.residual_f = h.residual_f;
     r.fused = fused;
     r.moved = moved;
+    r.s_zero = fused && !h.s_any;
     return r;
 }
 
@@ -532,12 +546,22 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
     }
     FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->act_s, 0, 2 * sizeof(unsigned long long), st));
     {
-        Prof p(c, kElemGate, 16.0 * N + 32.0 * Nc);
-        k_gate_spatial<<<grid_for(N), 256, 0, st>>>(S, N, bo.sb, m, spat_cur, keep_s, esc_s, c.ctl);
+        Prof p(c, kElemGate, (lr.s_zero ? 0.0 : 16.0 * N) + 32.0 * Nc);
+        if (lr.s_zero) {
+            // S is identically zero (no spatial clip moved a sample): no spatial edits, no
+            // overflow escapes, spat_cur = 0 (editset.cpp:43-66 on an all-zero S)
+            FFCZ_CUDA_CHECK(cudaMemsetAsync(spat_cur, 0, N * sizeof(double), st));
+            FFCZ_CUDA_CHECK(cudaMemsetAsync(keep_s, 0, ws * sizeof(unsigned), st));
+            FFCZ_CUDA_CHECK(cudaMemsetAsync(esc_s, 0, ws * sizeof(unsigned), st));
+        } else {
+            k_gate_spatial<<<grid_for(N), 256, 0, st>>>(S, N, bo.sb, m, spat_cur, keep_s, esc_s,
+                                                        c.ctl);
+            ++c.launches;
+        }
         k_gate_freq<<<grid_for(Nc), 256, 0, st>>>(F, hg, bo.fb, m, freq_cur, keep_f, esc_f, c.ctl);
     }
     FFCZ_LAUNCH_CHECK();
-    c.launches += 2;
+    ++c.launches;
 
     GateOut o;
     // counts + offsets of the keep bitmaps, then codes written straight from the bits
@@ -558,7 +582,7 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
         c.launches += 3;
         return c.read_ctl().count_a;
     };
-    o.n_keep_s = codes_from(keep_s, ws, "blk_counts_s", [&](unsigned nb, unsigned long long* off) {
+    o.n_keep_s = lr.s_zero ? 0 : codes_from(keep_s, ws, "blk_counts_s", [&](unsigned nb, unsigned long long* off) {
         k_codes_spatial_bits<<<nb, 1024, 0, st>>>(keep_s, ws, off, S, bo.sb, m, codes_s);
     });
     o.n_keep_f = codes_from(keep_f, wf, "blk_counts_f", [&](unsigned nb, unsigned long long* off) {
@@ -620,17 +644,20 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
             c.launches += three_d ? 2 : 1;
         };
         bool verified = false;
+        bool sc_zero = lr.s_zero;  // spat_cur stays zero until a spatial repair
         if (converged) {
             double* eps_v = c.b<double>("eps_verify", N);
             for (int round = 0; round < 32; ++round) {                   // pipeline.cpp:116
                 FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->dirty, 0, sizeof(int), st));
+                FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->dirty_s, 0, sizeof(int), st));
                 FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->vs_bits, 0, 2 * sizeof(unsigned long long), st));
                 FFCZ_CUDA_CHECK(cudaMemsetAsync(viol, 0, vw * sizeof(unsigned), st));
                 // inverse once: eps_tilde for the repair check (pipeline.cpp:125-136) and, in case
                 // the round is clean, the decoder view for verify (pipeline.cpp:174-176)
-                inverse_and_row(HookRepairVerifyS<TI>{orig, dec, spat_cur, eps, bo.sb, esc_s,
-                                                      corrected, eps_v, c.ctl},
-                                16.0 * Nc + in_bytes + 24.0 * N);
+                HookRepairVerifyS<TI> hk{orig, dec, spat_cur, eps, bo.sb, esc_s, corrected, eps_v,
+                                         c.ctl};
+                hk.sc_zero = sc_zero;
+                inverse_and_row(hk, 16.0 * Nc + in_bytes - (sc_zero ? 8.0 * N : 0.0) + 24.0 * N);
                 {
                     Prof p(c, kColFwdCheck, pass);
                     plan.col(za, -1, work, work, nullptr, HookMarkViol{bo.fb, viol, c.ctl}, st);
@@ -640,7 +667,9 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
                 FFCZ_LAUNCH_CHECK();
                 c.launches += 2;
                 ++o.rounds;
-                if (!c.read_ctl().dirty) {                               // :161
+                const Ctl hr = c.read_ctl();
+                if (hr.dirty_s) sc_zero = false;
+                if (!hr.dirty) {                                         // :161
                     // clean round: spat_cur / freq_cur are final and eps_v is their decoder
                     // view, so its forward transform completes verify_bounds
                     forward_row_mid(eps_v);
@@ -817,7 +846,16 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     double* eps = c.b<double>("eps", N);
     const double f = 1.0 - std::ldexp(1.0, -m);
     const double slack = 1.0 / (1.0 - std::ldexp(1.0, -m)) - 1.0 + 0x1p-20;
-    {
+    // FP64 fused loop: eps0 is formed inside the first R2C (it is never needed in HBM unless the
+    // loop converges at its first check); otherwise materialise it
+    bool eps0_in_r2c = false;
+    if (opt.policy == FFCZ_POLICY_FP64 && !(opt.flags & FFCZ_FORCE_UNFUSED) &&
+        FftPlan<double>{g, &c.tw64}.fused_ok() && eps0_fusion_enabled() && m >= 1 && m <= 24) {
+        Prof p(c, kRowR2C, (2.0 * sizeof(TI)) * N + 16.0 * g.Nc());
+        eps0_in_r2c = launch_row_r2c_eps0<TI>(g.n2, orig, dec, c.b<double2>("spec", g.half_elems()),
+                                              g.P, g.rows, c.tw64, bo.sb, f, slack, c.ctl, st);
+    }
+    if (!eps0_in_r2c) {
         Prof p(c, kElemPre, (2.0 * sizeof(TI) + 8.0) * N);
         k_eps0<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, eps, N, bo.sb, f, slack, 1, c.ctl);
     }
@@ -839,8 +877,13 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     const bool mixed = opt.policy == FFCZ_POLICY_MIXED && !(opt.flags & FFCZ_FORCE_UNFUSED) &&
                        run_phase32(c, g, eps, bo, f, opt.tau_switch, S, F);
     LoopResult lr = run_loop(c, g, eps, bo, f, !(opt.flags & FFCZ_FORCE_UNFUSED), S, F, true,
-                             mixed);
+                             mixed, eps0_in_r2c);
     if (mixed) lr.passes32 = c.read_ctl().passes32;
+    if (eps0_in_r2c && lr.passes == 0) {  // the final epsilon is eps0 itself
+        k_eps0<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, eps, N, bo.sb, f, slack, 0, c.ctl);
+        FFCZ_LAUNCH_CHECK();
+        ++c.launches;
+    }
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[3], st));
     finish_typed<TI>(c, g, fd, orig, dec, bd, bo, m, lr, eps, S, F,
                      c.b<double2>("spec", g.half_elems()), opt, out);
@@ -864,11 +907,14 @@ void finish_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& fd
     const double f = 1.0 - std::ldexp(1.0, -m);
     DebugClock dbg;
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[3], st));
-    {
+    // residual_s (projection.cpp:129-133): after an FP64 s-clip every |eps| <= E exactly
+    // (clamp), so it is 0 unless the final epsilon is eps0 or an FP32 iterate
+    FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->res_s_bits, 0, sizeof(unsigned long long), st));
+    if (lr.passes == lr.passes32) {
         Prof p(c, kElemPre, 8.0 * N);
         k_residual_s<<<grid_for(N), 256, 0, st>>>(eps, N, bo.sb, f, c.ctl);
+        ++c.launches;
     }
-    ++c.launches;
 
     // the FP64 corrected field is only materialised when the caller asks for it (the reference's
     // CorrectionResult carries no field; verify needs only its epsilon)

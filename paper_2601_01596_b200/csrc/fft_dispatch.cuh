@@ -316,6 +316,36 @@ void launch_row_r2c(long long n2, const T* in, long long in_stride, cplx<T>* out
     FFCZ_LAUNCH_CHECK();
 }
 
+// eps0 fused into the first R2C (k_row_r2c_eps0_sh); false when the row length has no
+// warp-paired FP64 variant (the caller then runs k_eps0 + R2C)
+template <class TI>
+bool launch_row_r2c_eps0(long long n2, const TI* orig, const TI* dec, double2* out,
+                         long long out_stride, long long nrows, Twiddles<double>& tw, SpatialB sb,
+                         double fscale, double slack, Ctl* ctl, cudaStream_t st) {
+    if (!radix_row_ok(n2)) return false;
+    bool done = false;
+    switch (n2 / 2) {
+#define X(n)                                                                                   \
+    case n:                                                                                    \
+        if constexpr (detail::RowCfg<double, n>::TT <= 32 && n >= 32) {                        \
+            constexpr int E = detail::RowCfg<double, n>::E, TT = detail::RowCfg<double, n>::TT; \
+            const int R = detail::rows_per_cta<double, n>(nrows);                              \
+            const size_t smem = row_smem_bytes<double, n, E>(R);                               \
+            auto k = k_row_r2c_eps0_sh<TI, n, E, SpatialB, Ctl>;                               \
+            detail::set_smem(k, smem);                                                         \
+            k<<<detail::persistent_grid(k, TT * R, smem, (nrows + R - 1) / R), TT * R, smem,   \
+                st>>>(orig, dec, n2, out, out_stride, nrows, tw.stage_table(n, E),             \
+                      tw.post_table(n), sb, fscale, slack, ctl);                               \
+            FFCZ_LAUNCH_CHECK();                                                               \
+            done = true;                                                                       \
+        }                                                                                      \
+        break;
+        FFCZ_POW2_CASES(X)
+#undef X
+    }
+    return done;
+}
+
 template <class T, class Hook>
 void launch_row_r2c_hook(long long n2, const T* in, long long in_stride, cplx<T>* out,
                          long long out_stride, long long nrows, Twiddles<T>& tw, const int* gate,

@@ -967,6 +967,62 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     hook.finish();
 }
 
+// First forward pass of correct() with compute_error fused in (pipeline.cpp:31-42): rows of
+// eps0 = dec - orig are formed in registers from the two input fields (never stored), the two
+// preconditions are checked on the way (first failing index -> bad1 / bad2), and the R2C
+// proceeds as k_row_r2c_sh.  Saves the separate eps0 pass (read 2 fields + write eps).
+template <class TI, int M, int E, class SB, class CTL>
+__global__ void __launch_bounds__(max_threads<double, E>(), 512 / max_threads<double, E>())
+    k_row_r2c_eps0_sh(const TI* __restrict__ orig, const TI* __restrict__ dec, long long n2,
+                      double2* __restrict__ out, long long out_stride, long long nrows,
+                      const double2* __restrict__ tw, const double2* __restrict__ twp, SB sb,
+                      double fscale, double slack, CTL* ctl) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int TT = M / E;
+    const int t = threadIdx.x % TT;
+    const int rb = threadIdx.x / TT;
+    const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
+    HookNone none;
+    unsigned long long bad1 = ~0ull, bad2 = ~0ull;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        __syncthreads();
+        const long long row = tile * (blockDim.x / TT) + rb;
+        const bool valid = row < nrows;
+        double2* s = reinterpret_cast<double2*>(smem_raw) + rb * row_smem_elems<M, E>();
+        double2 v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const long long n = (valid ? row : 0) * n2 + 2 * (t + TT * m);
+            double e0 = 0.0, e1 = 0.0;
+            if (valid) {
+                if constexpr (sizeof(TI) == 4) {
+                    const float2 o = *reinterpret_cast<const float2*>(orig + n);
+                    const float2 d = *reinterpret_cast<const float2*>(dec + n);
+                    e0 = static_cast<double>(d.x) - static_cast<double>(o.x);
+                    e1 = static_cast<double>(d.y) - static_cast<double>(o.y);
+                } else {
+                    const double2 o = *reinterpret_cast<const double2*>(orig + n);
+                    const double2 d = *reinterpret_cast<const double2*>(dec + n);
+                    e0 = d.x - o.x;
+                    e1 = d.y - o.y;
+                }
+                const double E0 = sb.at(n), E1 = sb.at(n + 1);
+                if (fabs(e0) > E0 * (1.0 + 0x1p-20) && static_cast<unsigned long long>(n) < bad1) bad1 = n;
+                if (fabs(e1) > E1 * (1.0 + 0x1p-20) && static_cast<unsigned long long>(n + 1) < bad1) bad1 = n + 1;
+                if (fabs(e0) > E0 * fscale * (1.0 + slack) && static_cast<unsigned long long>(n) < bad2) bad2 = n;
+                if (fabs(e1) > E1 * fscale * (1.0 + slack) && static_cast<unsigned long long>(n + 1) < bad2) bad2 = n + 1;
+            }
+            v[m] = make_double2(e0, e1);
+        }
+        stockham<double, M, E, 1, -1>(v, t, tw, XchRow<double, E>{s});
+        const double2 mid = natural_to_pairs<double, M, E>(v, t);
+        split_store<double, M, E>(v, mid, t, valid, out + (valid ? row : 0) * out_stride,
+                                  row * out_stride, twp, none);
+    }
+    if (bad1 != ~0ull) atomicMin(&ctl->bad1, bad1);
+    if (bad2 != ~0ull) atomicMin(&ctl->bad2, bad2);
+}
+
 template <class T, int M, int E, class Hook>
 __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>())
     k_row_c2r_sh(const cplx<T>* __restrict__ in, long long in_stride, T* __restrict__ out,

@@ -81,6 +81,11 @@ template <class T, class Hook>
 void launch_row_r2c_hook(long long n2, const T* in, long long in_stride, cplx<T>* out,
                          long long out_stride, long long nrows, Twiddles<T>& tw, const int* gate,
                          Hook hook, cudaStream_t st);
+// First R2C of correct() with compute_error + preconditions fused in (FP64 output).
+template <class TI>
+bool launch_row_r2c_eps0(long long n2, const TI* orig, const TI* dec, double2* out,
+                         long long out_stride, long long nrows, Twiddles<double>& tw, SpatialB sb,
+                         double fscale, double slack, Ctl* ctl, cudaStream_t st);
 // Row C2R: half rows -> real rows, scaled.
 template <class T>
 void launch_row_c2r(long long n2, const cplx<T>* in, long long in_stride, T* out,

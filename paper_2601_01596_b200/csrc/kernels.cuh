@@ -65,6 +65,8 @@ struct Ctl {
     int switch_now;
     unsigned long long passes32;
     double tau;
+    int s_any;    // a spatial clip moved some sample (S is not identically zero)
+    int dirty_s;  // escape repair: a spatial component was repaired this round
 };
 
 __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* p, double v) {
@@ -189,17 +191,19 @@ struct HookSClip {
     T* eps;
     const Ctl* ctl = nullptr;
     bool first = false;
+    int any = 0;  // a clip moved some sample of this CTA (reported as ctl->s_any)
     __device__ __forceinline__ void begin() {  // without ctl, `first` is the caller's value
         if (ctl) first = *reinterpret_cast<const volatile unsigned long long*>(&ctl->passes) == 1;
     }
     template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
-    __device__ __forceinline__ T one(T x, long long n) const {
+    __device__ __forceinline__ T one(T x, long long n) {
         const double xd = x;
         const double e = sb.at(n) * fscale;
         const double c = clamp_abs(xd, e);
         const double d = c - xd;
         if (first) S[n] = 0.0 + d;
         else if (d != 0.0) S[n] = __ldg(&S[n]) + d;  // see HookFClip
+        any |= d != 0.0;
         return static_cast<T>(c);
     }
     __device__ __forceinline__ void post_real(T& x0, T& x1, long long n) {
@@ -207,7 +211,10 @@ struct HookSClip {
         x1 = one(x1, n + 1);
         if (eps) reinterpret_cast<typename cvec<T>::type*>(eps)[n >> 1] = mkc<T>(x0, x1);
     }
-    __device__ __forceinline__ void finish() {}
+    __device__ __forceinline__ void finish() {
+        if (__syncthreads_or(any) && threadIdx.x == 0 && ctl)
+            const_cast<Ctl*>(ctl)->s_any = 1;
+    }
 };
 
 // Rebuild of the accumulated frequency edits at the end of a rebuild-mode loop: the pass
@@ -478,12 +485,13 @@ struct HookRepairVerifyS {
     double* corrected;
     double* eps_v;
     Ctl* ctl;
+    bool sc_zero = false;  // spat_cur is identically zero (no spatial edits): skip its load
     int dirty = 0;
     double m = 0.0;
     template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
     __device__ __forceinline__ void post_real(double& x0, double& x1, long long n) {
         const double2 o = load_pair(orig, n), d = load_pair(dec, n);
-        double2 sc = *reinterpret_cast<const double2*>(spat_cur + n);
+        double2 sc = sc_zero ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(spat_cur + n);
         const double e0 = d.x - o.x, e1 = d.y - o.y;
         const double c0 = d.x + sc.x + x0, c1 = d.y + sc.y + x1;
         const double v0 = c0 - o.x, v1 = c1 - o.y;
@@ -513,7 +521,10 @@ struct HookRepairVerifyS {
         x1 = t1;
     }
     __device__ __forceinline__ void finish() {
-        if (__syncthreads_or(dirty) && threadIdx.x == 0) ctl->dirty = 1;
+        if (__syncthreads_or(dirty) && threadIdx.x == 0) {
+            ctl->dirty = 1;
+            ctl->dirty_s = 1;
+        }
         block_max2_atomic(m, 0.0, &ctl->vs_bits, nullptr);
     }
 };
