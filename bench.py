@@ -287,6 +287,8 @@ def run_frames(args, rank, world, local):
                        "parallelism": f"frames/{world} per rank"},
             "iterations": {"min": int(min(iters)), "max": int(max(iters)),
                            "mean": float(np.mean(iters))},
+            "loop_ms_per_step": float(sum(r.timings_ms["t_loop_ms"] for r in rs)),
+            "gate_ms_per_frame_mean": float(np.mean([r.timings_ms["t_gate_ms"] for r in rs])),
             "roofline": {"bound": "hbm", "kernel": dom.name.decode(), "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": None,

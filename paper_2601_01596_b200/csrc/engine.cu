@@ -1133,18 +1133,28 @@ namespace {
 // Runs fn(lane_ctx, item) for items [0, n) on `nl` lane sub-contexts (host threads, one stream
 // each), ordered after the work already queued on ctx->st; ctx->st waits for every lane before
 // returning.  The first exception of any lane is rethrown.
-void run_on_lanes(ffcz_cuda_ctx* ctx, int nl, uint64_t n,
-                  const std::function<void(ffcz_cuda_ctx&, uint64_t)>& fn) {
+void ensure_lanes(ffcz_cuda_ctx* ctx, int nl) {
     while (static_cast<int>(ctx->lanes.size()) < nl) {
         ffcz_cuda_ctx* l = nullptr;
         if (ffcz_cuda_create(&l, ctx->device, nullptr) != kOk)
             throw Error(kCuda, std::string("lane context: ") + g_last_error);
         ctx->lanes.push_back(l);
     }
-    FFCZ_CUDA_CHECK(cudaEventRecord(ctx->ev[7], ctx->st));
+}
+
+// start: event the lanes wait for (default: recorded now on ctx->st); join_stream: make ctx->st
+// wait for the lanes at the end (off when the caller joins on the host instead)
+void run_on_lanes(ffcz_cuda_ctx* ctx, int nl, uint64_t n,
+                  const std::function<void(ffcz_cuda_ctx&, uint64_t)>& fn,
+                  cudaEvent_t start = nullptr, bool join_stream = true) {
+    ensure_lanes(ctx, nl);
+    if (!start) {
+        FFCZ_CUDA_CHECK(cudaEventRecord(ctx->ev[7], ctx->st));
+        start = ctx->ev[7];
+    }
     for (int i = 0; i < nl; ++i) {
         ffcz_cuda_ctx* l = ctx->lanes[i];
-        FFCZ_CUDA_CHECK(cudaStreamWaitEvent(l->st, ctx->ev[7], 0));
+        FFCZ_CUDA_CHECK(cudaStreamWaitEvent(l->st, start, 0));
         if (l->prof_on != ctx->prof_on) {
             l->prof_on = ctx->prof_on;
             l->prof.clear();
@@ -1180,7 +1190,7 @@ void run_on_lanes(ffcz_cuda_ctx* ctx, int nl, uint64_t n,
     for (int i = 1; i < nl; ++i) th.emplace_back(work, ctx->lanes[i]);
     work(ctx->lanes[0]);
     for (auto& t : th) t.join();
-    for (int i = 0; i < nl; ++i) {
+    for (int i = 0; join_stream && i < nl; ++i) {
         ffcz_cuda_ctx* l = ctx->lanes[i];
         FFCZ_CUDA_CHECK(cudaEventRecord(l->ev[7], l->st));
         FFCZ_CUDA_CHECK(cudaStreamWaitEvent(ctx->st, l->ev[7], 0));
@@ -1195,6 +1205,325 @@ inline bool frames_fused_enabled() {
         return !(e && e[0] == '0');
     }();
     return on;
+}
+
+// FFCZ_FRAMES_BATCHED_GATE=0: run each frame's FP64 gate on the lanes instead
+inline bool frames_batched_gate_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_FRAMES_BATCHED_GATE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// The FP64 gate (pipeline.cpp:46-176) of every frame of a group at once: each pass of the
+// single-field gate (run_gate, fused branch) runs over the stack with per-frame bounds and masks
+// (kernels.cuh FrameGate / FrameMask hooks): F rebuild, quantisation + flags, codes, escape
+// repair rounds (frames leave the rounds as they come clean; their verify runs on that round's
+// decoder view), apply + verify for the rest, escapes; then per-frame products.
+template <class TI>
+void gate_frames(ffcz_cuda_ctx& c, const Geometry& gf, const ffcz_field_desc& fd, long long Gc,
+                 uint64_t g0, const TI* orig, const TI* dec, const ffcz_bounds_desc* bd, int m,
+                 const std::vector<FrameCtl>& hfc, const std::vector<double>& hE,
+                 const std::vector<double>& hD, const double* dE, const double* dD, double* eps,
+                 double* S, double2* F, double2* spec, const unsigned char* moved,
+                 const ffcz_cuda_options& opt, double t_in, double t_loop, ffcz_cuda_result* out,
+                 const std::function<std::string(const char*)>& nm) {
+    cudaStream_t st = c.st;
+    const long long Nf = gf.N, Hf = gf.half_elems(), n1 = gf.d[1], n2 = gf.n2;
+    const long long Ncf = gf.Nc();                      // half-grid entries per frame
+    const uint64_t dimsb[3] = {static_cast<uint64_t>(Gc), static_cast<uint64_t>(n1),
+                               static_cast<uint64_t>(n2)};
+    const Geometry gb = make_geometry(3, dimsb, kPitchAlign);
+    const HalfGeom hg = gb.hg();
+    FftPlan<double> plan{gb, &c.tw64};
+    const long long N = Gc * Nf, Nc = Gc * Ncf;
+    const long long ws = N / 32, wf = Nc / 32;          // frames are whole words (n1 >= 64)
+    const double invN = 1.0 / static_cast<double>(Nf);
+    FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[3], st));
+    // per-frame state and masks
+    FrameGate* fg = c.b<FrameGate>(nm("fg_gate").c_str(), Gc);
+    FFCZ_CUDA_CHECK(cudaMemsetAsync(fg, 0, sizeof(FrameGate) * Gc, st));
+    int* mask = c.b<int>(nm("fg_mask").c_str(), Gc);
+    std::vector<int> hmask(Gc);
+    auto set_mask = [&](const std::function<bool(long long)>& pred) {
+        bool any = false;
+        for (long long i = 0; i < Gc; ++i) any |= (hmask[i] = pred(i) ? 1 : 0) != 0;
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(mask, hmask.data(), 4 * Gc, cudaMemcpyHostToDevice, st));
+        c.sync();  // hmask is reused
+        return any;
+    };
+    const FrameMask fmk{mask, n1};
+    double* spat_cur = c.b<double>(nm("fg_spat").c_str(), N);
+    double2* freq_cur = c.b<double2>(nm("fg_freq").c_str(), Gc * Hf);
+    double2* work = c.b<double2>(nm("fg_work").c_str(), Gc * Hf);
+    double* eps_t = c.b<double>(nm("fg_eps_t").c_str(), N);
+    double* eps_v = c.b<double>(nm("fg_eps_v").c_str(), N);
+    unsigned* keep_s = c.b<unsigned>(nm("fg_keep_s").c_str(), ws);
+    unsigned* esc_s = c.b<unsigned>(nm("fg_esc_s").c_str(), ws);
+    unsigned* keep_f = c.b<unsigned>(nm("fg_keep_f").c_str(), wf);
+    unsigned* esc_f = c.b<unsigned>(nm("fg_esc_f").c_str(), wf);
+    const long long vw = (Gc * Hf + 31) / 32;
+    unsigned* viol = c.b<unsigned>(nm("fg_viol").c_str(), vw);
+    int* codes_s = c.b<int>(nm("fg_codes_s").c_str(), N);
+    int* codes_f = c.b<int>(nm("fg_codes_f").c_str(), 2 * Nc);
+    double* corrected = (opt.flags & FFCZ_WANT_CORRECTED) ? c.b<double>(nm("fg_corr").c_str(), N) : nullptr;
+
+    // F rebuild for the frames whose loop ran >= 2 clip passes (HookFRebuild)
+    if (set_mask([&](long long i) { return hfc[i].passes >= 2; })) {
+        k_eps0_plus_s<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, S, eps_t, N);
+        launch_row_r2c_hook<double>(n2, eps_t, n2, work, gb.P, gb.rows, c.tw64, nullptr,
+                                    HookMaskB<true>{fmk}, st);
+        plan.col(1, -1, work, work, nullptr, HookFRebuildB{fmk, spec, F, moved}, st);
+        FFCZ_LAUNCH_CHECK();
+        c.launches += 3;
+    }
+    // quantisation + flags + overflow escapes (editset.cpp:43-133, pipeline.cpp:57-106)
+    k_gate_spatial_frames<<<grid_for(N), 256, 0, st>>>(S, N, Nf, dE, m, spat_cur, keep_s, esc_s, fg);
+    k_gate_freq_frames<<<grid_for(Nc), 256, 0, st>>>(F, hg, n1, dD, m, freq_cur, keep_f, esc_f, fg);
+    FFCZ_LAUNCH_CHECK();
+    c.launches += 2;
+    auto codes_stack = [&](const unsigned* words, long long nwords, const char* name, auto launch) {
+        const long long nblk = std::max<long long>(1, (nwords + 1023) / 1024);
+        unsigned long long* cnt = c.b<unsigned long long>(nm(name).c_str(), nblk + 1);
+        k_popc_blocks<<<static_cast<unsigned>(nblk), 1024, 0, st>>>(words, nwords, cnt);
+        k_scan_blocks<<<1, 1024, 0, st>>>(cnt, nblk, &c.ctl->count_a);
+        launch(static_cast<unsigned>(nblk), cnt);
+        FFCZ_LAUNCH_CHECK();
+        c.launches += 3;
+    };
+    codes_stack(keep_s, ws, "fg_cnt_s", [&](unsigned nb, unsigned long long* o) {
+        k_codes_spatial_frames<<<nb, 1024, 0, st>>>(keep_s, ws, o, S, Nf, dE, m, codes_s);
+    });
+    codes_stack(keep_f, wf, "fg_cnt_f", [&](unsigned nb, unsigned long long* o) {
+        k_codes_freq_frames<<<nb, 1024, 0, st>>>(keep_f, wf, o, F, hg, n1, dD, m, codes_f);
+    });
+    // per-frame kept counts -> code offsets
+    unsigned long long* pc = c.b<unsigned long long>(nm("fg_pc").c_str(), 2 * Gc);
+    k_frame_popc<<<static_cast<unsigned>(std::min<long long>(Gc, 1184)), 256, 0, st>>>(keep_s, Nf / 32, Gc, pc);
+    k_frame_popc<<<static_cast<unsigned>(std::min<long long>(Gc, 1184)), 256, 0, st>>>(keep_f, Ncf / 32, Gc, pc + Gc);
+    FFCZ_LAUNCH_CHECK();
+    std::vector<unsigned long long> hpc(2 * Gc);
+    FFCZ_CUDA_CHECK(cudaMemcpyAsync(hpc.data(), pc, 16 * Gc, cudaMemcpyDeviceToHost, st));
+    c.sync();
+    std::vector<unsigned long long> off_s(Gc + 1, 0), off_f(Gc + 1, 0);
+    for (long long i = 0; i < Gc; ++i) {
+        off_s[i + 1] = off_s[i] + hpc[i];
+        off_f[i + 1] = off_f[i] + hpc[Gc + i];
+    }
+
+    // escape-repair rounds (pipeline.cpp:111-163) for the converged frames
+    std::vector<int> rounds(Gc, 0), verified(Gc, 0);
+    std::vector<double> vs(Gc, 0.0), vf(Gc, 0.0);
+    std::vector<int> active(Gc);
+    for (long long i = 0; i < Gc; ++i) active[i] = hfc[i].converged;
+    std::vector<FrameGate> hg_gate(Gc);
+    auto read_gate = [&]() {
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(hg_gate.data(), fg, sizeof(FrameGate) * Gc,
+                                        cudaMemcpyDeviceToHost, st));
+        c.sync();
+    };
+    auto reset_round = [&]() {  // dirty / dirty_s / vs / vf of every frame (act counts kept)
+        k_frame_gate_reset<<<grid_for(Gc), 256, 0, st>>>(fg, Gc);
+        FFCZ_LAUNCH_CHECK();
+    };
+    for (int round = 0; round < 32; ++round) {
+        if (!set_mask([&](long long i) { return active[i] != 0; })) break;
+        reset_round();
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(viol, 0, vw * sizeof(unsigned), st));
+        plan.col(1, +1, freq_cur, work, nullptr, HookMaskB<false>{fmk}, st);
+        launch_row_c2r_hook<double>(n2, work, gb.P, eps_t, n2, gb.rows, invN, c.tw64, nullptr,
+            HookRepairVerifySB<TI>{fmk, dE, fg, orig, dec, spat_cur, eps, esc_s, corrected, eps_v},
+            st);
+        launch_row_r2c_hook<double>(n2, eps_t, n2, work, gb.P, gb.rows, c.tw64, nullptr,
+                                    HookMaskB<true>{fmk}, st);
+        plan.col(1, -1, work, work, nullptr, HookMarkViolB{fmk, dD, fg, viol}, st);
+        k_repair_freq_sparse_frames<<<grid_for(vw), 256, 0, st>>>(viol, vw, spec, work, hg, n1,
+                                                                  freq_cur, esc_f);
+        FFCZ_LAUNCH_CHECK();
+        c.launches += 5;
+        read_gate();
+        bool any_clean = false;
+        for (long long i = 0; i < Gc; ++i) {
+            if (!active[i]) continue;
+            ++rounds[i];
+            if (!hg_gate[i].dirty) {          // clean round: its decoder view is final (:161)
+                vs[i] = bitsd_host(hg_gate[i].vs_bits);
+                active[i] = 0;
+                verified[i] = 1;
+                any_clean = true;
+            }
+        }
+        if (any_clean) {  // verify the frames that came clean on this round's eps_v
+            set_mask([&](long long i) { return verified[i] == 1; });
+            launch_row_r2c_hook<double>(n2, eps_v, n2, work, gb.P, gb.rows, c.tw64, nullptr,
+                                        HookMaskB<true>{fmk}, st);
+            plan.col(1, -1, work, work, nullptr, HookVerifyFB{fmk, dD, fg}, st);
+            FFCZ_LAUNCH_CHECK();
+            c.launches += 2;
+            read_gate();
+            for (long long i = 0; i < Gc; ++i)
+                if (verified[i] == 1) {
+                    vf[i] = bitsd_host(hg_gate[i].vf_bits);
+                    verified[i] = 2;
+                }
+        }
+    }
+    // apply_edits + verify_bounds for the rest (not converged, or 32 dirty rounds)
+    if (set_mask([&](long long i) { return verified[i] == 0; })) {
+        reset_round();
+        plan.col(1, +1, freq_cur, work, nullptr, HookMaskB<false>{fmk}, st);
+        launch_row_c2r_hook<double>(n2, work, gb.P, eps_v, n2, gb.rows, invN, c.tw64, nullptr,
+            HookVerifySB<TI>{fmk, dE, fg, orig, dec, spat_cur, corrected}, st);
+        launch_row_r2c_hook<double>(n2, eps_v, n2, work, gb.P, gb.rows, c.tw64, nullptr,
+                                    HookMaskB<true>{fmk}, st);
+        plan.col(1, -1, work, work, nullptr, HookVerifyFB{fmk, dD, fg}, st);
+        FFCZ_LAUNCH_CHECK();
+        c.launches += 4;
+        read_gate();
+        for (long long i = 0; i < Gc; ++i)
+            if (verified[i] == 0) {
+                vs[i] = bitsd_host(hg_gate[i].vs_bits);
+                vf[i] = bitsd_host(hg_gate[i].vf_bits);
+            }
+    }
+    read_gate();  // act counts
+    // residual_s: 0 after an s-clip; frames that converged at their first check keep eps0
+    std::vector<double> res_s(Gc, 0.0);
+    for (long long i = 0; i < Gc; ++i)
+        if (hfc[i].passes == 0) {
+            FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->res_s_bits, 0, 8, st));
+            k_residual_s<<<grid_for(Nf), 256, 0, st>>>(eps + i * Nf, Nf, SpatialB{nullptr, hE[i]},
+                                                       1.0 - std::ldexp(1.0, -m), c.ctl);
+            FFCZ_LAUNCH_CHECK();
+            res_s[i] = bitsd_host(c.read_ctl().res_s_bits);
+        }
+    FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[6], st));
+
+    // escapes of the whole stack (ascending global index: frame order, spatial then frequency
+    // within a frame after the split below)
+    unsigned long long* idx = c.b<unsigned long long>(nm("fg_idx").c_str(), std::max(N, Nc));
+    const unsigned long long ns = compact_bits(c, esc_s, ws, idx);
+    std::vector<EscapeRec> rs(ns), rf;
+    if (ns) {
+        EscapeRec* r = c.b<EscapeRec>(nm("fg_recs").c_str(), ns);
+        k_escape_records_s<<<grid_for(ns), 256, 0, st>>>(idx, ns, spat_cur, r);
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(rs.data(), r, ns * sizeof(EscapeRec), cudaMemcpyDeviceToHost, st));
+    }
+    c.sync();
+    const unsigned long long nf = compact_bits(c, esc_f, wf, idx);
+    rf.resize(nf);
+    if (nf) {
+        EscapeRec* r = c.b<EscapeRec>(nm("fg_recs").c_str(), nf);
+        k_escape_records_f<<<grid_for(nf), 256, 0, st>>>(idx, nf, freq_cur, hg, r);
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(rf.data(), r, nf * sizeof(EscapeRec), cudaMemcpyDeviceToHost, st));
+    }
+    c.sync();
+    std::vector<std::vector<ffcz_cuda_escape>> esc(Gc);
+    auto rec = [](int freq, uint64_t index, double re, double im) {
+        ffcz_cuda_escape x;
+        std::memset(&x, 0, sizeof(x));  // the padding after `frequency` travels to the caller
+        x.frequency = freq;
+        x.index = index;
+        x.re = re;
+        x.im = im;
+        return x;
+    };
+    for (const EscapeRec& e : rs) {
+        const long long f = static_cast<long long>(e.index / Nf);
+        esc[f].push_back(rec(0, e.index - f * Nf, e.re, e.im));
+    }
+    for (const EscapeRec& e : rf) {
+        const long long f = static_cast<long long>(e.index / Ncf);
+        esc[f].push_back(rec(1, e.index - f * Ncf, e.re, e.im));
+    }
+
+    // per-frame products
+    const bool want_edits = opt.flags & (FFCZ_WANT_EDITS | FFCZ_WANT_ARCHIVE);
+    const double t_gate = event_ms(c.ev[3], c.ev[6]);
+    for (long long i = 0; i < Gc; ++i) {
+        ffcz_cuda_result* r = &out[g0 + i];
+        r->report.iterations = std::max<unsigned long long>(hfc[i].passes, 1);
+        r->report.active_spatial = hg_gate[i].act_s;
+        r->report.active_frequency = hg_gate[i].act_f;
+        r->report.converged = hfc[i].converged;
+        r->report.residual_f = hfc[i].residual_f;
+        r->report.residual_s = res_s[i];
+        r->iterations_fp64 = hfc[i].passes;
+        r->escape_rounds = rounds[i];
+        r->escape_count = esc[i].size();
+        r->verify_ok = vs[i] == 0.0 && vf[i] == 0.0;
+        r->verify_max_spatial_excess = vs[i];
+        r->verify_max_freq_excess = vf[i];
+        r->n_spatial = hpc[i];
+        r->n_frequency = hpc[Gc + i];
+        r->t_h2d_ms = t_in / Gc;
+        r->t_loop_ms = t_loop / Gc;
+        r->t_gate_ms = t_gate / Gc;
+        r->t_feasible_ms = r->t_loop_ms + r->t_gate_ms;
+        r->report.wall_time_s = r->t_loop_ms * 1e-3;
+        if (want_edits) {
+            r->spatial_flag_bytes = Nf / 8;
+            r->frequency_flag_bytes = Ncf / 8;
+            r->spatial_flags = static_cast<uint8_t*>(pinned().get(Nf / 8 + 1));
+            r->frequency_flags = static_cast<uint8_t*>(pinned().get(Ncf / 8 + 1));
+            r->spatial_codes = static_cast<int32_t*>(pinned().get(hpc[i] * 4 + 4));
+            r->frequency_codes = static_cast<int32_t*>(pinned().get(hpc[Gc + i] * 8 + 4));
+            r->escapes = static_cast<ffcz_cuda_escape*>(
+                pinned().get(sizeof(ffcz_cuda_escape) * (esc[i].size() + 1)));
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(r->spatial_flags, reinterpret_cast<const uint8_t*>(keep_s) + i * (Nf / 8),
+                                            Nf / 8, cudaMemcpyDeviceToHost, st));
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(r->frequency_flags, reinterpret_cast<const uint8_t*>(keep_f) + i * (Ncf / 8),
+                                            Ncf / 8, cudaMemcpyDeviceToHost, st));
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(r->spatial_codes, codes_s + off_s[i], hpc[i] * 4,
+                                            cudaMemcpyDeviceToHost, st));
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(r->frequency_codes, codes_f + 2 * off_f[i], hpc[Gc + i] * 8,
+                                            cudaMemcpyDeviceToHost, st));
+            if (!esc[i].empty())
+                std::memcpy(r->escapes, esc[i].data(), sizeof(ffcz_cuda_escape) * esc[i].size());
+        }
+        if (corrected) {
+            r->corrected = static_cast<double*>(pinned().get(Nf * sizeof(double)));
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(r->corrected, corrected + i * Nf, Nf * sizeof(double),
+                                            cudaMemcpyDeviceToHost, st));
+        }
+    }
+    c.sync();
+    if (opt.flags & FFCZ_WANT_ARCHIVE) {
+        for (long long i = 0; i < Gc; ++i) {
+            ffcz_cuda_result* r = &out[g0 + i];
+            std::vector<ffcz_host::EscapeRec> er(esc[i].size());
+            for (size_t k = 0; k < er.size(); ++k)
+                er[k] = {esc[i][k].frequency != 0, esc[i][k].index, esc[i][k].re, esc[i][k].im};
+            ffcz_host::ArchiveInput ai{};
+            ai.ndim = fd.ndim;
+            for (int a = 0; a < fd.ndim; ++a) ai.dims[a] = fd.dims[a];
+            ai.precision = fd.precision;
+            ai.spatial_global = hE[i];
+            ai.freq_global = hD[i];
+            ai.m = m;
+            ai.converged = hfc[i].converged;
+            ai.spatial_flags = r->spatial_flags;
+            ai.spatial_flag_bytes = r->spatial_flag_bytes;
+            ai.frequency_flags = r->frequency_flags;
+            ai.frequency_flag_bytes = r->frequency_flag_bytes;
+            ai.n_spatial = r->n_spatial;
+            ai.n_frequency = r->n_frequency;
+            ai.spatial_codes = r->spatial_codes;
+            ai.frequency_codes = r->frequency_codes;
+            ai.escapes = er.data();
+            ai.n_escapes = er.size();
+            ai.zlib_level = opt.zlib_level;
+            const auto t0 = std::chrono::steady_clock::now();
+            std::vector<uint8_t> bytes = ffcz_host::write_archive(ai);
+            r->t_archive_ms =
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            r->archive_len = bytes.size();
+            r->archive = static_cast<uint8_t*>(pinned().get(bytes.size() + 1));
+            std::memcpy(r->archive, bytes.data(), bytes.size());
+        }
+    }
+    (void)bd;
 }
 
 // Batched frames with ONE projection loop over the whole stack (config 3): every pass covers
@@ -1217,11 +1546,36 @@ void correct_frames_fused(ffcz_cuda_ctx& c, const ffcz_field_desc& fd, uint64_t 
     const double fw = 1.0 - std::ldexp(1.0, -m);
     const double slack = 1.0 / (1.0 - std::ldexp(1.0, -m)) - 1.0 + 0x1p-20;
     const double per_frame = 16.0 * Nf + 33.0 * Hf + (on_dev ? 0.0 : 2.0 * sizeof(TI) * Nf);
-    const double budget = 48e9;
-    const uint64_t G = std::max<uint64_t>(1, std::min<uint64_t>(
-        nframes, static_cast<uint64_t>(budget / per_frame)));
+    // two buffer sets: the per-frame gates of group k run on the lanes (background thread) while
+    // the loop of group k+1 runs on the context stream
+    // (the batched gate runs in the main thread: one buffer set, its own stack buffers)
+    const bool batched_gate = frames_batched_gate_enabled();
+    const double per_frame_all = per_frame + (batched_gate ? 36.0 * Nf + 32.0 * Hf + 12.0 * Nf : 0.0);
+    const double budget = batched_gate ? 60e9 : 24e9;
+    uint64_t G = std::max<uint64_t>(1, std::min<uint64_t>(
+        nframes, static_cast<uint64_t>(budget / per_frame_all)));
+    if (!batched_gate && nframes >= 64 && G >= nframes) G = (nframes + 1) / 2;  // overlap
     const uint64_t dims3[3] = {G, static_cast<uint64_t>(n1), static_cast<uint64_t>(n2)};
-    for (uint64_t g0 = 0; g0 < nframes; g0 += G) {
+    ensure_lanes(&c, nl);
+    std::thread gate_thread;
+    std::exception_ptr gate_err;
+    cudaEvent_t loop_done[2];
+    for (auto& e : loop_done) FFCZ_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct Joiner {
+        std::thread& t;
+        cudaEvent_t* evs;
+        ~Joiner() {
+            if (t.joinable()) t.join();
+            for (int i = 0; i < 2; ++i) cudaEventDestroy(evs[i]);
+        }
+    } joiner{gate_thread, loop_done};
+    auto join_gates = [&]() {
+        if (gate_thread.joinable()) gate_thread.join();
+        if (gate_err) std::rethrow_exception(gate_err);
+    };
+    int parity = 0;
+    for (uint64_t g0 = 0; g0 < nframes; g0 += G, parity = batched_gate ? 0 : parity ^ 1) {
+        auto nm = [&](const char* base) { return std::string(base) + (parity ? "1" : "0"); };
         const long long Gc = static_cast<long long>(std::min<uint64_t>(G, nframes - g0));
         const uint64_t dimsc[3] = {static_cast<uint64_t>(Gc), dims3[1], dims3[2]};
         const Geometry gb = make_geometry(3, dimsc, kPitchAlign);
@@ -1229,8 +1583,8 @@ void correct_frames_fused(ffcz_cuda_ctx& c, const ffcz_field_desc& fd, uint64_t 
         const TI* orig = static_cast<const TI*>(orig_in) + g0 * Nf;
         const TI* dec = static_cast<const TI*>(dec_in) + g0 * Nf;
         if (!on_dev) {
-            TI* o = c.b<TI>("fr_orig", Gc * Nf);
-            TI* d = c.b<TI>("fr_dec", Gc * Nf);
+            TI* o = c.b<TI>(nm("fr_orig"), Gc * Nf);
+            TI* d = c.b<TI>(nm("fr_dec"), Gc * Nf);
             FFCZ_CUDA_CHECK(cudaMemcpyAsync(o, orig, Gc * Nf * sizeof(TI), cudaMemcpyHostToDevice, st));
             FFCZ_CUDA_CHECK(cudaMemcpyAsync(d, dec, Gc * Nf * sizeof(TI), cudaMemcpyHostToDevice, st));
             orig = o;
@@ -1245,16 +1599,16 @@ void correct_frames_fused(ffcz_cuda_ctx& c, const ffcz_field_desc& fd, uint64_t 
             if (!(hD[i] > 0.0) || !std::isfinite(hD[i]))
                 throw Error(kValidation, "frequency bound Delta must be strictly positive and finite");
         }
-        double* dE = c.b<double>("fr_E", Gc);
-        double* dD = c.b<double>("fr_D", Gc);
+        double* dE = c.b<double>(nm("fr_E"), Gc);
+        double* dD = c.b<double>(nm("fr_D"), Gc);
         FFCZ_CUDA_CHECK(cudaMemcpyAsync(dE, hE.data(), 8 * Gc, cudaMemcpyHostToDevice, st));
         FFCZ_CUDA_CHECK(cudaMemcpyAsync(dD, hD.data(), 8 * Gc, cudaMemcpyHostToDevice, st));
         FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[1], st));
         // compute_error + preconditions of every frame (pipeline.cpp:31-42)
-        FrameCtl* fc = c.b<FrameCtl>("fr_ctl", Gc);
+        FrameCtl* fc = c.b<FrameCtl>(nm("fr_ctl"), Gc);
         k_frames_init<<<grid_for(Gc), 256, 0, st>>>(fc, Gc, max_iters);
         k_ctl_init<<<1, 1, 0, st>>>(c.ctl, max_iters);
-        double* eps = c.b<double>("fr_eps", Gc * Nf);
+        double* eps = c.b<double>(nm("fr_eps"), Gc * Nf);
         k_eps0_frames<TI><<<grid_for(Gc * Nf), 256, 0, st>>>(orig, dec, eps, Gc * Nf, Nf, dE, fw,
                                                              slack, c.ctl);
         FFCZ_LAUNCH_CHECK();
@@ -1267,10 +1621,10 @@ void correct_frames_fused(ffcz_cuda_ctx& c, const ffcz_field_desc& fd, uint64_t 
             throw Error(kValidation, "alternating_projection: epsilon0 violates the spatial bound "
                                      "at index " + std::to_string(h0.bad2 % Nf) + " (frame " +
                                      std::to_string(g0 + h0.bad2 / Nf) + ")");
-        double* S = c.b<double>("fr_S", Gc * Nf);
-        double2* F = c.b<double2>("fr_F", Gc * Hf);
-        double2* spec = c.b<double2>("fr_spec", Gc * Hf);
-        unsigned char* moved = c.b<unsigned char>("fr_moved", Gc * Hf);
+        double* S = c.b<double>(nm("fr_S"), Gc * Nf);
+        double2* F = c.b<double2>(nm("fr_F"), Gc * Hf);
+        double2* spec = c.b<double2>(nm("fr_spec"), Gc * Hf);
+        unsigned char* moved = c.b<unsigned char>(nm("fr_moved"), Gc * Hf);
         FFCZ_CUDA_CHECK(cudaMemsetAsync(moved, 0, Gc * Hf, st));
         const FrameBatch fbt{fc, dE, dD, fw, n1};
         FftPlan<double> plan{gb, &c.tw64};
@@ -1324,8 +1678,22 @@ void correct_frames_fused(ffcz_cuda_ctx& c, const ffcz_field_desc& fd, uint64_t 
             }
         const double t_in = event_ms(c.ev[0], c.ev[1]);
         const double t_loop = event_ms(c.ev[2], c.ev[3]);
-        // per-frame FP64 gate on the lanes
-        run_on_lanes(&c, nl, static_cast<uint64_t>(Gc), [&](ffcz_cuda_ctx& l, uint64_t i) {
+        FFCZ_CUDA_CHECK(cudaEventRecord(loop_done[parity], st));
+        // the previous group's gates must be done before its buffers are reused (next trip)
+        join_gates();
+        if (batched_gate) {  // the whole group's gate in stack passes
+            gate_frames<TI>(c, gf, fd, Gc, g0, orig, dec, bd, m, hfc, hE, hD, dE, dD, eps, S, F,
+                            spec, moved, opt, t_in, t_loop, out,
+                            [&](const char* b) { return nm(b); });
+            continue;
+        }
+        // per-frame FP64 gate on the lanes, in the background
+        auto gate_group = [&c, &gate_err, nl, Gc, g0, Nf, Hf, gf, fd, bd, m, opt, out, hfc,
+                           hE, hD, orig, dec, eps, S, F, spec, moved, t_loop, t_in,
+                           start = loop_done[parity]]() {
+          try {
+            FFCZ_CUDA_CHECK(cudaSetDevice(c.device));
+            run_on_lanes(&c, nl, static_cast<uint64_t>(Gc), [&](ffcz_cuda_ctx& l, uint64_t i) {
             LoopResult lr;
             lr.passes = hfc[i].passes;
             lr.converged = hfc[i].converged;
@@ -1344,9 +1712,14 @@ void correct_frames_fused(ffcz_cuda_ctx& c, const ffcz_field_desc& fd, uint64_t 
             r->t_loop_ms = t_loop / Gc;
             r->t_h2d_ms = t_in / Gc;
             r->t_feasible_ms = r->t_loop_ms + r->t_gate_ms;
-        });
-        c.sync();
+            }, start, false);
+          } catch (...) {
+            gate_err = std::current_exception();
+          }
+        };
+        gate_thread = std::thread(gate_group);
     }
+    join_gates();
 }
 
 } // namespace

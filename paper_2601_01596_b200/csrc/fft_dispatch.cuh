@@ -72,11 +72,18 @@ inline int tma1_mode() {
     return m;
 }
 
+// raises a kernel's dynamic shared-memory limit once (a driver call per launch otherwise)
 template <class K>
 void set_smem(K kernel, size_t bytes) {
-    if (bytes > 48 * 1024)
-        FFCZ_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(bytes)));
+    if (bytes <= 48 * 1024) return;
+    static std::mutex mu;
+    static std::map<const void*, size_t> done;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = done[reinterpret_cast<const void*>(kernel)];
+    if (cur >= bytes) return;
+    FFCZ_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(bytes)));
+    cur = bytes;
 }
 
 // Persistent grid: resident-CTA capacity of the device for this kernel configuration.

@@ -907,4 +907,183 @@ __global__ void k_escape_records_f(const unsigned long long* __restrict__ idx, l
     }
 }
 
+// ---- batched frames: gate kernels over the stack -------------------------------------------------
+
+// warp-aggregated per-frame count (a warp's 32 consecutive indices never straddle a frame: frame
+// sizes are multiples of 32)
+__device__ __forceinline__ void frame_count_add(unsigned long long* dst, unsigned v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, static_cast<unsigned long long>(v));
+}
+
+__global__ void k_gate_spatial_frames(const double* __restrict__ S, long long N, long long frameN,
+                                      const double* __restrict__ E, int m, double* spat_cur,
+                                      unsigned* keep_words, unsigned* esc_words, FrameGate* fg) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long base = blockIdx.x * (long long)blockDim.x; base < N; base += stride) {
+        const long long n = base + threadIdx.x;
+        bool keep = false, ovf = false;
+        const long long f = (base + (threadIdx.x & ~31)) / frameN;
+        if (n < N) {
+            const double v = S[n];
+            const bool nz = v != 0.0;
+            const double step = ldexp(2.0 * E[f], -m);           // editset.cpp:31-33
+            ovf = nz && (fabs(v) / step > kMaxIndex);            // pipeline.cpp:63-64
+            keep = nz && !ovf;
+            double cur = 0.0;
+            if (keep) cur = static_cast<double>(static_cast<int>(llround(v / step))) * step;
+            else if (ovf) cur = v;
+            spat_cur[n] = cur;
+        }
+        const unsigned bk = __ballot_sync(0xffffffffu, keep);
+        const unsigned be = __ballot_sync(0xffffffffu, ovf);
+        if ((threadIdx.x & 31) == 0 && n < N) {
+            keep_words[n >> 5] = bk;
+            esc_words[n >> 5] = be;
+        }
+        if (n - (threadIdx.x & 31) < N)
+            frame_count_add(&fg[f].act_s, (threadIdx.x & 31) ? 0u : __popc(bk) + __popc(be));
+    }
+}
+
+__global__ void k_gate_freq_frames(const double2* __restrict__ F, HalfGeom g, long long n1,
+                                   const double* __restrict__ D, int m, double2* freq_cur,
+                                   unsigned* keep_words, unsigned* esc_words, FrameGate* fg) {
+    const long long total = g.rows * g.H;
+    for (HalfWalk hw(g); hw.block_ok(); hw.next()) {
+        const long long h = hw.i;
+        bool keep = false, ovf = false;
+        unsigned wt = 0;
+        const long long frame = hw.row / n1;
+        if (h < total) {
+            const int k2 = hw.k2;
+            const long long off = hw.row * g.P + k2;
+            const double2 v = F[off];
+            const bool nz = v.x != 0.0 || v.y != 0.0;
+            const double st = ldexp(2.0 * D[frame], -m);          // editset.cpp:35-41
+            ovf = nz && (fabs(v.x) / st > kMaxIndex || fabs(v.y) / st > kMaxIndex);
+            keep = nz && !ovf;
+            double2 cur = make_double2(0.0, 0.0);
+            if (keep) {
+                cur.x = static_cast<double>(static_cast<int>(llround(v.x / st))) * st;
+                cur.y = static_cast<double>(static_cast<int>(llround(v.y / st))) * st;
+            } else if (ovf) {
+                cur = v;
+            }
+            freq_cur[off] = cur;
+            if (nz) wt = plane_weight(k2, g.n2);
+        }
+        const unsigned bk = __ballot_sync(0xffffffffu, keep);
+        const unsigned be = __ballot_sync(0xffffffffu, ovf);
+        if ((threadIdx.x & 31) == 0 && h < total) {
+            keep_words[h >> 5] = bk;
+            esc_words[h >> 5] = be;
+        }
+        // the warp's 32 consecutive h share a frame (n1 * H is a multiple of 32)
+        const long long wframe = __shfl_sync(0xffffffffu, frame, 0);
+        if (h - (threadIdx.x & 31) < total) frame_count_add(&fg[wframe].act_f, wt);
+    }
+}
+
+__global__ void k_codes_spatial_frames(const unsigned* __restrict__ keep_words, long long nwords,
+                                       const unsigned long long* __restrict__ block_offsets,
+                                       const double* __restrict__ S, long long frameN,
+                                       const double* __restrict__ E, int m, int* codes) {
+    codes_from_bits(keep_words, nwords, block_offsets, [&](long long n, unsigned long long pos) {
+        const double step = ldexp(2.0 * E[n / frameN], -m);
+        codes[pos] = static_cast<int>(llround(S[n] / step));
+    });
+}
+
+__global__ void k_codes_freq_frames(const unsigned* __restrict__ keep_words, long long nwords,
+                                    const unsigned long long* __restrict__ block_offsets,
+                                    const double2* __restrict__ F, HalfGeom g, long long n1,
+                                    const double* __restrict__ D, int m, int* codes) {
+    codes_from_bits(keep_words, nwords, block_offsets, [&](long long h, unsigned long long pos) {
+        const long long off = g.offset_of(h);
+        const double2 v = F[off];
+        const double st = ldexp(2.0 * D[(off / g.P) / n1], -m);
+        reinterpret_cast<int2*>(codes)[pos] = make_int2(static_cast<int>(llround(v.x / st)),
+                                                        static_cast<int>(llround(v.y / st)));
+    });
+}
+
+__global__ void k_frame_popc(const unsigned* __restrict__ words, long long words_per_frame,
+                             long long nframes, unsigned long long* counts) {
+    for (long long f = blockIdx.x; f < nframes; f += gridDim.x) {
+        unsigned long long c = 0;
+        const unsigned* w = words + f * words_per_frame;
+        for (long long i = threadIdx.x; i < words_per_frame; i += blockDim.x) c += __popc(w[i]);
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        __shared__ unsigned long long sc[32];
+        if ((threadIdx.x & 31) == 0) sc[threadIdx.x >> 5] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int k = 0; k < (blockDim.x + 31) / 32; ++k) t += sc[k];
+            counts[f] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// k_repair_freq_sparse with the conjugate mirror taken inside each frame's n1 x n2 grid
+__global__ void k_repair_freq_sparse_frames(const unsigned* __restrict__ viol_words,
+                                            long long nwords, const double2* __restrict__ delta_star,
+                                            const double2* __restrict__ delta_tilde, HalfGeom g,
+                                            long long n1, double2* freq_cur, unsigned* esc_words) {
+    for (long long wi = blockIdx.x * (long long)blockDim.x + threadIdx.x; wi < nwords;
+         wi += (long long)gridDim.x * blockDim.x) {
+        unsigned bits = viol_words[wi];
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const long long off = wi * 32 + b;
+            const long long row = off / g.P;
+            const int k2 = static_cast<int>(off - row * g.P);
+            auto repaired = [&](long long o) {
+                const double2 c = freq_cur[o], s = delta_star[o], t = delta_tilde[o];
+                return make_double2(c.x + (s.x - t.x), c.y + (s.y - t.y));
+            };
+            const bool plane = (k2 == 0) || (2LL * k2 == g.n2);
+            long long mrow = row;
+            if (plane) {
+                const long long fr = row / n1, k1 = row - fr * n1;
+                mrow = fr * n1 + (k1 ? n1 - k1 : 0);
+            }
+            if (mrow == row) {
+                freq_cur[off] = repaired(off);
+                set_bit(esc_words, row * g.H + k2);
+                continue;
+            }
+            const long long moff = mrow * g.P + k2;
+            const bool mviol = (viol_words[moff >> 5] >> (moff & 31)) & 1u;
+            if (row > mrow && mviol) continue;  // the smaller partner handles the pair
+            const long long lo = row < mrow ? off : moff, hi = row < mrow ? moff : off;
+            const bool hi_viol = row < mrow ? mviol : true;
+            double2 r = hi_viol ? repaired(hi) : repaired(lo);
+            const double2 rc = make_double2(r.x, -r.y);
+            if (hi_viol) {
+                freq_cur[hi] = r;
+                freq_cur[lo] = rc;
+            } else {
+                freq_cur[lo] = r;
+                freq_cur[hi] = rc;
+            }
+            set_bit(esc_words, row * g.H + k2);
+            set_bit(esc_words, mrow * g.H + k2);
+        }
+    }
+}
+
+__global__ void k_frame_gate_reset(FrameGate* fg, long long nframes) {
+    for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < nframes;
+         f += (long long)gridDim.x * blockDim.x) {
+        fg[f].vs_bits = 0;
+        fg[f].vf_bits = 0;
+        fg[f].dirty = 0;
+        fg[f].dirty_s = 0;
+    }
+}
+
 } // namespace ffcz_gpu

@@ -574,6 +574,217 @@ struct HookVerifyF {
     __device__ __forceinline__ void finish() { block_max2_atomic(m, 0.0, &ctl->vf_bits, nullptr); }
 };
 
+// ---- batched frames: the FP64 gate over the whole stack ---------------------------------------------
+// Per-frame gate state (pipeline.cpp:46-176 for each frame); `active` masks select the frames a
+// pass works on (tiles of other frames are skipped, so their buffers are untouched).
+struct FrameGate {
+    unsigned long long act_s, act_f;   // active counts (act_f over the full spectrum)
+    unsigned long long vs_bits, vf_bits;
+    int dirty, dirty_s;
+    int pad[2];
+};
+
+struct FrameMask {
+    const int* active;                 // per frame: process (1) / skip (0)
+    long long rows_per_frame;          // n1
+    __device__ __forceinline__ long long frame_of(long long u, bool rows) const {
+        return rows ? u / rows_per_frame : u;
+    }
+    __device__ __forceinline__ bool skip(long long f) const { return active[f] == 0; }
+};
+
+template <bool kRows>
+struct HookMaskB {  // plain pass over the active frames
+    static constexpr bool kTiled = true;
+    FrameMask fm;
+    __device__ __forceinline__ bool tile_skip(long long u) const { return fm.skip(fm.frame_of(u, kRows)); }
+    __device__ __forceinline__ void tile_begin(long long) {}
+    __device__ __forceinline__ void tile_end() {}
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    template <class C> __device__ __forceinline__ void post(C&, long long, int) {}
+    template <class T> __device__ __forceinline__ void post_real(T&, T&, long long) {}
+    __device__ __forceinline__ void finish() {}
+};
+
+// F rebuild (HookFRebuild) for the frames that need it
+struct HookFRebuildB {
+    static constexpr bool kTiled = true;
+    static constexpr bool kNoStore = true;
+    FrameMask fm;
+    const double2* delta;
+    double2* F;
+    const unsigned char* moved;
+    __device__ __forceinline__ bool tile_skip(long long u) const { return fm.skip(u); }
+    __device__ __forceinline__ void tile_begin(long long) {}
+    __device__ __forceinline__ void tile_end() {}
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    template <class C>
+    __device__ __forceinline__ void post(C& v, long long off, int) {
+        double2 f = make_double2(0.0, 0.0);
+        if (moved[off]) {
+            const double2 d = __ldg(&delta[off]);
+            f = make_double2(d.x - v.x, d.y - v.y);
+        }
+        F[off] = f;
+    }
+    __device__ __forceinline__ void finish() {}
+};
+
+// escape-repair round + speculative decoder view (HookRepairVerifyS) per frame
+template <class TI>
+struct HookRepairVerifySB {
+    static constexpr bool kTiled = true;
+    FrameMask fm;
+    const double* E;     // per frame
+    FrameGate* fg;
+    const TI* orig;
+    const TI* dec;
+    double* spat_cur;
+    const double* final_eps;
+    unsigned* esc_words;
+    double* corrected;
+    double* eps_v;
+    long long frame = 0;
+    double e = 0.0, m = 0.0;
+    int dirty = 0;
+    __device__ __forceinline__ bool tile_skip(long long u) const { return fm.skip(fm.frame_of(u, true)); }
+    __device__ __forceinline__ void tile_begin(long long u) {
+        frame = fm.frame_of(u, true);
+        e = E[frame];
+        m = 0.0;
+        dirty = 0;
+    }
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    __device__ __forceinline__ void post_real(double& x0, double& x1, long long n) {
+        const double2 o = load_pair(orig, n), d = load_pair(dec, n);
+        double2 sc = *reinterpret_cast<const double2*>(spat_cur + n);
+        const double e0 = d.x - o.x, e1 = d.y - o.y;
+        const double c0 = d.x + sc.x + x0, c1 = d.y + sc.y + x1;
+        const double v0 = c0 - o.x, v1 = c1 - o.y;
+        if (corrected) *reinterpret_cast<double2*>(corrected + n) = make_double2(c0, c1);
+        *reinterpret_cast<double2*>(eps_v + n) = make_double2(v0, v1);
+        const double ex0 = fabs(v0) - e, ex1 = fabs(v1) - e;
+        if (ex0 > 0.0 && ex0 > m) m = ex0;
+        if (ex1 > 0.0 && ex1 > m) m = ex1;
+        const double t0 = e0 + sc.x + x0, t1 = e1 + sc.y + x1;
+        bool w = false;
+        if (fabs(t0) > e) {
+            sc.x = sc.x + (final_eps[n] - t0);
+            set_bit_g(esc_words, n);
+            w = true;
+        }
+        if (fabs(t1) > e) {
+            sc.y = sc.y + (final_eps[n + 1] - t1);
+            set_bit_g(esc_words, n + 1);
+            w = true;
+        }
+        if (w) {
+            *reinterpret_cast<double2*>(spat_cur + n) = sc;
+            dirty = 1;
+        }
+        x0 = t0;
+        x1 = t1;
+    }
+    __device__ __forceinline__ void tile_end() {
+        if (__syncthreads_or(dirty) && threadIdx.x == 0) {
+            fg[frame].dirty = 1;
+            fg[frame].dirty_s = 1;
+        }
+        block_max2_atomic(m, 0.0, &fg[frame].vs_bits, nullptr);
+    }
+    __device__ __forceinline__ void finish() {}
+};
+
+// apply_edits + verify_bounds spatial side (HookVerifyS) per frame
+template <class TI>
+struct HookVerifySB {
+    static constexpr bool kTiled = true;
+    FrameMask fm;
+    const double* E;
+    FrameGate* fg;
+    const TI* orig;
+    const TI* dec;
+    const double* spat_cur;
+    double* corrected;
+    long long frame = 0;
+    double e = 0.0, m = 0.0;
+    __device__ __forceinline__ bool tile_skip(long long u) const { return fm.skip(fm.frame_of(u, true)); }
+    __device__ __forceinline__ void tile_begin(long long u) {
+        frame = fm.frame_of(u, true);
+        e = E[frame];
+        m = 0.0;
+    }
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    __device__ __forceinline__ void post_real(double& x0, double& x1, long long n) {
+        const double2 o = load_pair(orig, n), d = load_pair(dec, n);
+        const double2 sc = *reinterpret_cast<const double2*>(spat_cur + n);
+        const double c0 = d.x + sc.x + x0, c1 = d.y + sc.y + x1;
+        if (corrected) *reinterpret_cast<double2*>(corrected + n) = make_double2(c0, c1);
+        x0 = c0 - o.x;
+        x1 = c1 - o.y;
+        const double ex0 = fabs(x0) - e, ex1 = fabs(x1) - e;
+        if (ex0 > 0.0 && ex0 > m) m = ex0;
+        if (ex1 > 0.0 && ex1 > m) m = ex1;
+    }
+    __device__ __forceinline__ void tile_end() { block_max2_atomic(m, 0.0, &fg[frame].vs_bits, nullptr); }
+    __device__ __forceinline__ void finish() {}
+};
+
+// violation marking (HookMarkViol) per frame
+struct HookMarkViolB {
+    static constexpr bool kTiled = true;
+    FrameMask fm;
+    const double* D;
+    FrameGate* fg;
+    unsigned* viol_words;
+    long long frame = 0;
+    double d = 0.0;
+    int any = 0;
+    __device__ __forceinline__ bool tile_skip(long long u) const { return fm.skip(u); }
+    __device__ __forceinline__ void tile_begin(long long u) {
+        frame = u;
+        d = D[u];
+        any = 0;
+    }
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    template <class C>
+    __device__ __forceinline__ void post(C& v, long long off, int) {
+        if (fabs(v.x) > d || fabs(v.y) > d) {
+            set_bit_g(viol_words, off);
+            any = 1;
+        }
+    }
+    __device__ __forceinline__ void tile_end() {
+        if (__syncthreads_or(any) && threadIdx.x == 0) fg[frame].dirty = 1;
+    }
+    __device__ __forceinline__ void finish() {}
+};
+
+// verify_bounds frequency side (HookVerifyF) per frame, output not stored
+struct HookVerifyFB {
+    static constexpr bool kTiled = true;
+    static constexpr bool kNoStore = true;
+    FrameMask fm;
+    const double* D;
+    FrameGate* fg;
+    long long frame = 0;
+    double d = 0.0, m = 0.0;
+    __device__ __forceinline__ bool tile_skip(long long u) const { return fm.skip(u); }
+    __device__ __forceinline__ void tile_begin(long long u) {
+        frame = u;
+        d = D[u];
+        m = 0.0;
+    }
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    template <class C>
+    __device__ __forceinline__ void post(C& v, long long, int) {
+        const double ex = fmax(fabs(v.x) - d, fabs(v.y) - d);
+        if (ex > 0.0 && ex > m) m = ex;
+    }
+    __device__ __forceinline__ void tile_end() { block_max2_atomic(m, 0.0, &fg[frame].vf_bits, nullptr); }
+    __device__ __forceinline__ void finish() {}
+};
+
 // ---- elementwise kernels (unfused path / generic shapes) -------------------------------------------
 
 struct HalfGeom {
@@ -716,5 +927,31 @@ __global__ void k_gather_escapes_f(const unsigned long long* __restrict__ idx, l
 __global__ void k_split_hermitian(const double2* __restrict__ full, double2* Hh, double2* Ah,
                                   HalfGeom g, long long d0, long long d1);
 __global__ void k_maxabs(const double* __restrict__ x, long long N, unsigned long long* out);
+
+// gate kernels over the stack with per-frame bounds (frame = n / frameN, row / n1)
+__global__ void k_gate_spatial_frames(const double* __restrict__ S, long long N, long long frameN,
+                                      const double* __restrict__ E, int m, double* spat_cur,
+                                      unsigned* keep_words, unsigned* esc_words, FrameGate* fg);
+__global__ void k_gate_freq_frames(const double2* __restrict__ F, HalfGeom g, long long n1,
+                                   const double* __restrict__ D, int m, double2* freq_cur,
+                                   unsigned* keep_words, unsigned* esc_words, FrameGate* fg);
+__global__ void k_codes_spatial_frames(const unsigned* __restrict__ keep_words, long long nwords,
+                                       const unsigned long long* __restrict__ block_offsets,
+                                       const double* __restrict__ S, long long frameN,
+                                       const double* __restrict__ E, int m, int* codes);
+__global__ void k_codes_freq_frames(const unsigned* __restrict__ keep_words, long long nwords,
+                                    const unsigned long long* __restrict__ block_offsets,
+                                    const double2* __restrict__ F, HalfGeom g, long long n1,
+                                    const double* __restrict__ D, int m, int* codes);
+// per-frame popcount of a bitmap whose frames are whole words
+__global__ void k_frame_popc(const unsigned* __restrict__ words, long long words_per_frame,
+                             long long nframes, unsigned long long* counts);
+// sparse frequency repair inside each frame (mirror within the frame's 2-D grid)
+__global__ void k_repair_freq_sparse_frames(const unsigned* __restrict__ viol_words,
+                                            long long nwords, const double2* __restrict__ delta_star,
+                                            const double2* __restrict__ delta_tilde, HalfGeom g,
+                                            long long n1, double2* freq_cur, unsigned* esc_words);
+
+__global__ void k_frame_gate_reset(FrameGate* fg, long long nframes);
 
 } // namespace ffcz_gpu
