@@ -62,6 +62,15 @@ inline bool col_tma_enabled() {
     return on;
 }
 
+// FFCZ_COL_C2=0 disables the 2-CTA cluster column pass (A/B runs)
+inline bool c2_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_COL_C2");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // FFCZ_COL_TMA1: 0 = never use the single-landing column pass, 1 = wherever it fits,
 // unset = only where double buffering would fall below 128-B row segments.
 inline int tma1_mode() {
@@ -137,6 +146,55 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
         while (Bt > 1 && col_tma_smem_bytes<T, L, E>(Bt, side) > 220 * 1024) Bt /= 2;
         if (const char* e = std::getenv("FFCZ_COL_TMA_B")) Bt = std::max(1, std::atoi(e));
         Bt = std::min(Bt, pow2_ceil(ncols));
+        if constexpr (L >= 1024 && sizeof(T) == 8) {
+            // 2-CTA cluster (k_col_c2): each CTA lands half the rows, so tiles reach 256-B (L =
+            // 1024) / 128-B (L = 2048) rows.  FFCZ_COL_C2=0 disables it.
+            constexpr int E2 = 16, TT2 = (L / 2) / E2, NT2 = 512;
+            int B2 = std::min(NT2 / TT2, 128);
+            while (B2 > 1 && col_c2_smem_bytes<T, L, E2>(B2) > 220 * 1024) B2 /= 2;
+            B2 = std::min(B2, pow2_ceil(ncols));
+            CUtensorMap map2;
+            if (!side && c2_enabled() && TT2 * B2 >= 32 && B2 * sizeof(cplx<T>) >= 128 &&
+                encode_col_map(&map2, src, sizeof(T), ncols, L, row_stride, nplanes, plane_stride,
+                               B2, (L / 2) < 256 ? (L / 2) : 256, true)) {
+                auto kt = dir < 0 ? k_col_c2<T, L, E2, -1, Hook, NT2> : k_col_c2<T, L, E2, +1, Hook, NT2>;
+                const size_t sm2 = col_c2_smem_bytes<T, L, E2>(B2);
+                set_smem(kt, sm2);
+                const long long nt = static_cast<long long>((ncols + B2 - 1) / B2) * nplanes;
+                cudaLaunchConfig_t cfg = {};
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = 2;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                cfg.blockDim = dim3(TT2 * B2);
+                cfg.dynamicSmemBytes = sm2;
+                cfg.stream = st;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                static std::mutex mu;
+                static std::map<std::pair<const void*, size_t>, int> clusters;
+                int ncl = 0;
+                {
+                    std::lock_guard<std::mutex> lk(mu);
+                    auto key = std::make_pair(reinterpret_cast<const void*>(kt), sm2 * 1024 + B2);
+                    auto it = clusters.find(key);
+                    if (it == clusters.end()) {
+                        cfg.gridDim = dim3(2 * 148);
+                        FFCZ_CUDA_CHECK(cudaOccupancyMaxActiveClusters(&ncl, kt, &cfg));
+                        clusters[key] = ncl;
+                    } else {
+                        ncl = it->second;
+                    }
+                }
+                const long long pairs = std::max<long long>(1, std::min<long long>(nt, ncl));
+                cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+                FFCZ_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kt, map2, dst, row_stride, plane_stride,
+                                                   ncols, B2, nt, tw.stage_table(L / 2, E2),
+                                                   tw.post_table(L / 2), gate, hook));
+                return;
+            }
+        }
         if constexpr (L >= 512) {
             // single landing buffer + scalar exchange (k_col_tma1) where it gives wider row
             // segments than double buffering: always when double buffering falls below 128 B,

@@ -21,6 +21,8 @@
 // pass that produces or consumes the data.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include <utility>
 
 #include "common.cuh"
@@ -562,6 +564,124 @@ __global__ void __launch_bounds__(NT, 1)
         if constexpr (hook_tiled<Hook>()) hook.tile_end();
     }
     hook.finish();
+}
+
+// Column pass of an L-point line split over a 2-CTA cluster (DSMEM): CTA h of the pair lands
+// rows [h L/2, (h+1) L/2) of a B-column tile by TMA, so a tile can be twice as wide as one SM's
+// shared memory allows (FP64: L = 1024 at 16 columns = 256-B rows, L = 2048 at 8 columns =
+// 128-B rows — the outer / 2048-point passes measured 0.38-0.67 of HBM at 64-128-B rows).
+// One decimation-in-frequency radix-2 stage across the pair: CTA 0 forms u_i = x_i + x_{i+L/2},
+// CTA 1 forms v_i = (x_i - x_{i+L/2}) W_L^{+-i}, reading the partner's landing tile through
+// distributed shared memory; each then runs an L/2-point Stockham transform and stores rows
+// 2q + h.  The next tile's box is issued once both CTAs have read the landing buffers, so it
+// lands during the L/2-point transform and the stores.  Pre-hooks run on the landing tile
+// (owner only) before the exchange; post-hooks on the stored elements.
+// smem per CTA: (L/2) x B complex (landing) + (L/2 + L/2/E) x B scalars (exchange) + mbarrier.
+template <class T, int L, int E, int DIR, class Hook, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    k_col_c2(const __grid_constant__ CUtensorMap map, cplx<T>* __restrict__ dst,
+             long long row_stride, long long plane_stride, int ncols, int B, long long ntiles,
+             const cplx<T>* __restrict__ tw, const cplx<T>* __restrict__ twl, const int* gate,
+             Hook hook) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    if (gated(gate)) return;  // uniform over the pair: both CTAs read the same flag
+    hook_begin(hook);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int LH = L / 2;
+    constexpr int TT = LH / E;
+    constexpr int LB = LH < 256 ? LH : 256;
+    const unsigned h = cluster.block_rank();
+    const int b = threadIdx.x % B;
+    const int t = threadIdx.x / B;
+    const int tiles_c = (ncols + B - 1) / B;
+    cplx<T>* land = reinterpret_cast<cplx<T>*>(smem_raw);
+    T* xs = reinterpret_cast<T*>(land + LH * B);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(
+        smem_raw + ((static_cast<size_t>(LH) * B * sizeof(cplx<T>) +
+                     static_cast<size_t>(LH + LH / E) * B * sizeof(T) + 15) & ~size_t(15)));
+    const cplx<T>* peer = cluster.map_shared_rank(land, h ^ 1u);
+    const unsigned tile_bytes = static_cast<unsigned>(LH) * B * sizeof(cplx<T>);
+    const long long pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+    auto issue = [&](long long tile) {
+        const long long plane = tile / tiles_c;
+        const int c0 = static_cast<int>(tile - plane * tiles_c) * B;
+        mbar_arrive_expect_tx(bar, tile_bytes);
+#pragma unroll
+        for (int j = 0; j < LH / LB; ++j)
+            tma_load_3d(land + j * LB * B, &map, bar, 2 * c0, static_cast<int>(h) * LH + j * LB,
+                        static_cast<int>(plane));
+    };
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&map);
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && pair < ntiles) issue(pair);
+    unsigned phase = 0;
+    for (long long tile = pair; tile < ntiles; tile += npairs) {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        const long long plane = tile / tiles_c;
+        bool skip = false;
+        if constexpr (hook_tiled<Hook>()) {
+            skip = hook.tile_skip(plane);
+            if (!skip) hook.tile_begin(plane);
+        }
+        const int c = static_cast<int>(tile - plane * tiles_c) * B + b;
+        const bool valid = c < ncols;
+        const long long base = plane * plane_stride + c;
+        if (!skip && valid) {  // pre-hooks on the owned half, in place
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int i = t + TT * m;
+                const long long off = base + static_cast<long long>(h * LH + i) * row_stride;
+                cplx<T> x = land[i * B + b];
+                hook.pre(x, off, c);
+                land[i * B + b] = x;
+            }
+        }
+        cluster.sync();  // both halves landed and pre-hooked
+        cplx<T> v[E];
+        if (!skip) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int i = t + TT * m;
+                const cplx<T> mine = land[i * B + b], other = peer[i * B + b];
+                const cplx<T> a = h ? other : mine, bb = h ? mine : other;  // x_i, x_{i+L/2}
+                if (h == 0) {
+                    v[m] = cadd(a, bb);
+                } else {
+                    const cplx<T> w = twl[i];  // W_L^i = exp(-2 pi i i / L)
+                    v[m] = DIR < 0 ? cmul(csub(a, bb), w) : cmulc(csub(a, bb), w);
+                }
+            }
+        }
+        fence_proxy_async_smem();
+        cluster.sync();  // both CTAs are done with both landing tiles
+        if (threadIdx.x == 0 && tile + npairs < ntiles) issue(tile + npairs);
+        if (skip) continue;
+        stockham<T, LH, E, 1, DIR>(v, t, tw, XchColS<T, E>{xs + b, B});
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const long long r = 2LL * (t + TT * m) + h;
+            const long long off = base + r * row_stride;
+            if (valid) {
+                hook.post(v[m], off, c);
+                if constexpr (hook_stores<Hook>()) dst[off] = v[m];
+            }
+        }
+        if constexpr (hook_tiled<Hook>()) hook.tile_end();
+    }
+    hook.finish();
+    cluster.sync();  // no CTA exits while its partner may still read its shared memory
+}
+
+template <class T, int L, int E>
+constexpr size_t col_c2_smem_bytes(int B) {
+    return ((static_cast<size_t>(L / 2) * B * sizeof(cplx<T>) +
+             static_cast<size_t>(L / 2 + L / 2 / E) * B * sizeof(T) + 15) & ~size_t(15)) + 16;
 }
 
 template <class T, int L, int E>
