@@ -62,11 +62,14 @@ inline bool col_tma_enabled() {
     return on;
 }
 
-// FFCZ_COL_C2=0 disables the 2-CTA cluster column pass (A/B runs)
+// FFCZ_COL_C2=1 enables the 2-CTA cluster column pass.  Off by default: correct (parity suite)
+// but measured slower than the single-CTA passes it replaces — 0.50 of HBM vs 0.67-0.75 at
+// 1024^3 and 0.50 vs 0.69 on 2048-point lines (two cluster barriers per tile and no overlap of
+// the DSMEM exchange with the next tile's load); kept for the deeper-pipelined version.
 inline bool c2_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("FFCZ_COL_C2");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     return on;
 }
@@ -148,7 +151,7 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
         Bt = std::min(Bt, pow2_ceil(ncols));
         if constexpr (L >= 1024 && sizeof(T) == 8) {
             // 2-CTA cluster (k_col_c2): each CTA lands half the rows, so tiles reach 256-B (L =
-            // 1024) / 128-B (L = 2048) rows.  FFCZ_COL_C2=0 disables it.
+            // 1024) / 128-B (L = 2048) rows (opt-in, see c2_enabled).
             constexpr int E2 = 16, TT2 = (L / 2) / E2, NT2 = 512;
             int B2 = std::min(NT2 / TT2, 128);
             while (B2 > 1 && col_c2_smem_bytes<T, L, E2>(B2) > 220 * 1024) B2 /= 2;
