@@ -928,6 +928,17 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     hook.finish();
 }
 
+// Input prefetch for C2R epilogue hooks (k_row_c2r_sh): a hook with kPrefetch names two input
+// fields (prefetch_src(k, first_sample)), their scalar size (prefetch_scalar_bytes) and takes the
+// shared-memory copies per tile (use_prefetch(orig_s, dec_s, first_sample)).
+template <class H>
+constexpr bool hook_prefetch() {
+    if constexpr (requires { H::kPrefetch; })
+        return H::kPrefetch;
+    else
+        return false;
+}
+
 // ---- row passes with warp-shuffle pairing (M/E <= 32) --------------------------------------------
 // The split/merge needs X[k] and X[M-k] together.  Instead of a shared-memory round trip, rows are
 // loaded in a "paired" layout: thread t holds X[t + T m] in slot m and X[M - t - T m] in slot
@@ -1155,6 +1166,24 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     const int t = threadIdx.x % TT;
     const int rb = threadIdx.x / TT;
     const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
+    // hooks that read input fields per output sample (escape repair / verify) get the tile's rows
+    // of those fields prefetched into shared memory by bulk copies issued at the start of the
+    // tile, so the loads land while the rows are transformed (hook_prefetch)
+    constexpr bool kPf = hook_prefetch<Hook>();
+    const int R = blockDim.x / TT;
+    const long long n2r = 2LL * M;  // reals per row
+    unsigned char* pf_base = smem_raw + static_cast<size_t>(row_smem_elems<M, E>()) * R * sizeof(cplx<T>);
+    uint64_t* pf_bar = nullptr;
+    size_t pf_bytes_row = 0;
+    if constexpr (kPf) {
+        pf_bytes_row = static_cast<size_t>(n2r) * hook.prefetch_scalar_bytes();
+        pf_bar = reinterpret_cast<uint64_t*>(pf_base + 2 * pf_bytes_row * R);
+        if (threadIdx.x == 0) {
+            mbar_init(pf_bar, 1);
+            fence_mbar_init();
+        }
+    }
+    unsigned pf_phase = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         __syncthreads();
         if constexpr (hook_tiled<Hook>()) {
@@ -1162,7 +1191,19 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
             if (hook.tile_skip(u)) continue;
             hook.tile_begin(u);
         }
-        const long long row = tile * (blockDim.x / TT) + rb;
+        const long long row0 = tile * R;
+        if constexpr (kPf) {
+            if (threadIdx.x == 0) {
+                const long long nr = nrows - row0 < R ? nrows - row0 : R;
+                const unsigned bytes = static_cast<unsigned>(pf_bytes_row * nr);
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx(pf_bar, 2 * bytes);
+                bulk_load(pf_base, hook.prefetch_src(0, row0 * out_stride), bytes, pf_bar);
+                bulk_load(pf_base + pf_bytes_row * R, hook.prefetch_src(1, row0 * out_stride), bytes,
+                          pf_bar);
+            }
+        }
+        const long long row = row0 + rb;
         const bool valid = row < nrows;
         cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
         cplx<T> v[E], mid;
@@ -1170,6 +1211,11 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
         merge_pairs<T, M, E>(v, mid, t, twp);
         pairs_to_natural<T, M, E>(v, mid, t);
         stockham<T, M, E, 1, +1>(v, t, tw, XchRow<T, E>{s});
+        if constexpr (kPf) {
+            mbar_wait(pf_bar, pf_phase);
+            pf_phase ^= 1u;
+            hook.use_prefetch(pf_base, pf_base + pf_bytes_row * R, row0 * out_stride);
+        }
         if (valid) {
             cplx<T>* dst = reinterpret_cast<cplx<T>*>(out + row * out_stride);
 #pragma unroll

@@ -488,9 +488,24 @@ struct HookRepairVerifyS {
     bool sc_zero = false;  // spat_cur is identically zero (no spatial edits): skip its load
     int dirty = 0;
     double m = 0.0;
+    // orig / dec rows prefetched into shared memory by the row kernel (hook_prefetch)
+    static constexpr bool kPrefetch = true;
+    const TI* po = nullptr;
+    const TI* pd = nullptr;
+    long long pbase = 0;
+    __host__ __device__ static constexpr unsigned prefetch_scalar_bytes() { return sizeof(TI); }
+    __device__ __forceinline__ const void* prefetch_src(int k, long long n0) const {
+        return (k ? dec : orig) + n0;
+    }
+    __device__ __forceinline__ void use_prefetch(const void* o, const void* d, long long n0) {
+        po = static_cast<const TI*>(o);
+        pd = static_cast<const TI*>(d);
+        pbase = n0;
+    }
     template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
     __device__ __forceinline__ void post_real(double& x0, double& x1, long long n) {
-        const double2 o = load_pair(orig, n), d = load_pair(dec, n);
+        const double2 o = po ? load_pair(po, n - pbase) : load_pair(orig, n);
+        const double2 d = pd ? load_pair(pd, n - pbase) : load_pair(dec, n);
         double2 sc = sc_zero ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(spat_cur + n);
         const double e0 = d.x - o.x, e1 = d.y - o.y;
         const double c0 = d.x + sc.x + x0, c1 = d.y + sc.y + x1;
