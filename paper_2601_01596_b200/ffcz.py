@@ -374,7 +374,7 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
 def correct_batch(original, decompressed, bounds, m: int = 16, max_iters: int = 1000,
                   precision: str | None = None, *, lanes: int = 8, want_archive: bool = True,
                   want_edits: bool = True, want_corrected: bool = True, zlib_level: int = 9,
-                  fused: bool = True, copy: bool = True,
+                  fused: bool = True, copy: bool = True, policy: str = "fp64", tau: float = 1e-4,
                   ctx: Context | None = None) -> list[CorrectionResult]:
     """Independent ffcz::correct() of every frame of a batch (BASELINE config 3).
 
@@ -398,7 +398,8 @@ def correct_batch(original, decompressed, bounds, m: int = 16, max_iters: int = 
     bds = (capi.BoundsDesc * max(1, nf))()
     for i, b in enumerate(bounds):
         bds[i] = _bounds_desc(b, mar)
-    opt = _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level)
+    opt = _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level,
+                   False, policy, tau)
     if on_dev:
         _order_after_torch(original, decompressed)
     res = (capi.Result * max(1, nf))()

@@ -117,3 +117,31 @@ def test_batch_error_is_reported(ffcz):
     bounds[1] = ffcz.DualBounds(1e-12, bs[1][1])  # precondition violated on frame 1
     with pytest.raises(ffcz.ValidationError):
         ffcz.correct_batch(o, d, bounds, 16, 1000, "f32", lanes=2)
+
+
+def test_batch_lanes_path_per_point_bounds(ffcz):
+    """Per-point E sends the batch down the per-frame lanes path; still equal to correct()."""
+    o, d, bs = frames(64, 3, seed0=900, spots=6)
+    bounds = []
+    for i, (E, D) in enumerate(bs):
+        e = np.full(o[i].shape, E)
+        e[::7, ::5] *= 1.5
+        bounds.append(ffcz.DualBounds(e, D))
+    rb = ffcz.correct_batch(o.astype(np.float32), d.astype(np.float32), bounds, 16, 1000, "f32",
+                            lanes=2)
+    for i in range(3):
+        ri = ffcz.correct(o[i].astype(np.float32), d[i].astype(np.float32), bounds[i], 16, 1000,
+                          "f32")
+        same_result(rb[i], ri)
+
+
+def test_batch_mixed_policy_runs_per_frame(ffcz):
+    o, d, bs = frames(64, 2, seed0=950, spots=6)
+    bounds = [ffcz.DualBounds(E, D) for E, D in bs]
+    rb = ffcz.correct_batch(o.astype(np.float32), d.astype(np.float32), bounds, 16, 1000, "f32",
+                            lanes=2, policy="mixed")
+    for i in range(2):
+        ri = ffcz.correct(o[i].astype(np.float32), d[i].astype(np.float32), bounds[i], 16, 1000,
+                          "f32", policy="mixed")
+        same_result(rb[i], ri)
+        assert rb[i].verify_ok
