@@ -5,22 +5,11 @@
 namespace ffcz_gpu {
 
 // FP64 gate: fused escape-repair rounds and verify
-#define FFCZ_ROW_FUSED(H)                                                                     \
-    template void launch_row_fused<double, H>(long long, double2*, long long, long long,      \
-                                              long long, double, Twiddles<double>&, const int*, \
-                                              H, cudaStream_t);
-FFCZ_ROW_FUSED(HookRepairS<float>)
-FFCZ_ROW_FUSED(HookRepairS<double>)
-FFCZ_ROW_FUSED(HookVerifyS<float>)
-FFCZ_ROW_FUSED(HookVerifyS<double>)
-#undef FFCZ_ROW_FUSED
 #define FFCZ_ROW_C2R_HOOK(H)                                                                  \
     template void launch_row_c2r_hook<double, H>(long long, const double2*, long long, double*, \
                                                  long long, long long, double, Twiddles<double>&, \
                                                  const int*, H, cudaStream_t);
 FFCZ_ROW_C2R_HOOK(HookSClip<double>)
-FFCZ_ROW_C2R_HOOK(HookRepairS<float>)
-FFCZ_ROW_C2R_HOOK(HookRepairS<double>)
 FFCZ_ROW_C2R_HOOK(HookVerifyS<float>)
 FFCZ_ROW_C2R_HOOK(HookVerifyS<double>)
 FFCZ_ROW_C2R_HOOK(HookRepairVerifyS<float>)

@@ -399,49 +399,6 @@ __device__ __forceinline__ double2 load_pair(const TI* p, long long n) {
     return make_double2(static_cast<double>(v.x), static_cast<double>(v.y));
 }
 
-// Escape repair, spatial side (pipeline.cpp:125-136, 154-160), on the real outputs of the C2R
-// half of a fused last-axis pass: eps_tilde = eps0 + spat_cur + Re(IFFT(freq_cur)); components
-// violating the ORIGINAL E are pinned to spat_cur + (final_eps - eps_tilde).  The value handed on
-// to the R2C half is eps_tilde itself, so eps_tilde never touches HBM.
-template <class TI>
-struct HookRepairS {
-    const TI* orig;
-    const TI* dec;
-    double* spat_cur;
-    const double* final_eps;
-    SpatialB sb;
-    unsigned* esc_words;
-    Ctl* ctl;
-    int dirty = 0;
-    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
-    __device__ __forceinline__ void post_real(double& x0, double& x1, long long n) {
-        const double2 o = load_pair(orig, n), d = load_pair(dec, n);
-        double2 sc = *reinterpret_cast<const double2*>(spat_cur + n);
-        const double e0 = d.x - o.x, e1 = d.y - o.y;
-        const double t0 = e0 + sc.x + x0, t1 = e1 + sc.y + x1;
-        bool w = false;
-        if (fabs(t0) > sb.at(n)) {
-            sc.x = sc.x + (final_eps[n] - t0);
-            set_bit_g(esc_words, n);
-            w = true;
-        }
-        if (fabs(t1) > sb.at(n + 1)) {
-            sc.y = sc.y + (final_eps[n + 1] - t1);
-            set_bit_g(esc_words, n + 1);
-            w = true;
-        }
-        if (w) {
-            *reinterpret_cast<double2*>(spat_cur + n) = sc;
-            dirty = 1;
-        }
-        x0 = t0;
-        x1 = t1;
-    }
-    __device__ __forceinline__ void finish() {
-        if (__syncthreads_or(dirty) && threadIdx.x == 0) ctl->dirty = 1;
-    }
-};
-
 // apply_edits + verify_bounds, spatial side (archive.cpp:262-287): corrected = dec + spat_cur +
 // Re(IFFT(freq_cur)) is written out, eps = corrected - orig goes on to the R2C half.
 template <class TI>
@@ -472,7 +429,8 @@ struct HookVerifyS {
 // on the same inverse transform: when the round turns out clean (no component repaired, so
 // spat_cur and freq_cur are final), the decoder view dec + spat_cur + Re(IFFT(freq_cur)) is the
 // one this pass already has, and the separate verify inverse (3 passes) is skipped.  Writes
-// eps_tilde (handed on, as HookRepairS), plus `corrected` and eps_v = corrected - orig.  The two
+// eps_tilde (handed on to the R2C; the pinned components get spat_cur + (final_eps - eps_tilde),
+// pipeline.cpp:154-160), plus `corrected` and eps_v = corrected - orig.  The two
 // epsilons are formed exactly as the reference forms them (eps0 + s + f vs (dec + s + f) - orig).
 template <class TI>
 struct HookRepairVerifyS {
