@@ -153,6 +153,7 @@ class CorrectionResult:
     timings_ms: dict
     kernel_launches: int
     iterations_fp32: int = 0     # mixed policy: clip passes run by the FP32 phase
+    iterations_fp64: int = 0     # clip passes run in FP64
 
 
 class _ResultHolder:
@@ -307,7 +308,8 @@ def _convert(holder, shape, want_archive, want_edits, want_corrected, copy):
                            float(res.verify_max_spatial_excess),
                            float(res.verify_max_freq_excess), sflags, fflags, scodes, fcodes,
                            escapes, corrected, int(res.escape_rounds), timings,
-                           int(res.kernel_launches), int(res.iterations_fp32))
+                           int(res.kernel_launches), int(res.iterations_fp32),
+                           int(res.iterations_fp64))
     if copy:
         holder.free()
     else:
