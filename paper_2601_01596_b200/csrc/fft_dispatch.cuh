@@ -8,6 +8,7 @@
 #include <mutex>
 #include <tuple>
 
+#include "fft_mixed.cuh"
 #include "fft_plan.cuh"
 
 namespace ffcz_gpu {
@@ -325,6 +326,40 @@ void row_fused_radix(cplx<T>* data, long long stride, long long nrows, long long
     FFCZ_LAUNCH_CHECK();
 }
 
+// Mixed-radix passes (fft_mixed.cuh) take every extent that is not on the power-of-two path when
+// the two ping-pong buffers of one line fit; FFCZ_MIXED=0 keeps the O(L) direct passes (A/B).
+inline bool mixed_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_MIXED");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+constexpr size_t kMixedSmemMax = 200 * 1024;
+inline bool mixed_pipe_enabled() {  // FFCZ_MIXED_PIPE=0: the one-tile-per-CTA column pass (A/B)
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_MIXED_PIPE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+inline size_t mixed_smem_target() {  // FFCZ_MIXED_SMEM=<KB> for tile-size sweeps
+    static const size_t t = [] {
+        const char* e = std::getenv("FFCZ_MIXED_SMEM");
+        return e ? static_cast<size_t>(std::atoi(e)) * 1024 : size_t(64 * 1024);
+    }();
+    return t;
+}
+// lines per CTA: as many as fit the target (at least one line within the maximum), at most 16
+template <class T>
+inline int mixed_lines(long long L, long long nlines) {
+    const size_t per = 2 * sizeof(cplx<T>) * static_cast<size_t>(L);
+    if (per > kMixedSmemMax) return 0;
+    long long b = std::max<long long>(1, static_cast<long long>(mixed_smem_target() / per));
+    b = std::min<long long>({b, 16, std::max<long long>(1, nlines)});
+    return static_cast<int>(b);
+}
+
 } // namespace detail
 
 #define FFCZ_POW2_CASES(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
@@ -347,6 +382,38 @@ void launch_col(long long L, int dir, const cplx<T>* src, cplx<T>* dst, long lon
     if constexpr (!std::is_same_v<Hook, HookNone>) {
         throw Error(kUnsupported, "fused column pass needs a power-of-two extent in [16, 4096]");
     } else {
+        if (detail::mixed_pipe_enabled() && detail::mixed_enabled()) {
+            // 3 rotating tile buffers, B columns each (at most 16), within ~96 KB per CTA
+            const size_t per = 3 * sizeof(cplx<T>) * static_cast<size_t>(L);
+            if (per <= detail::kMixedSmemMax) {
+                static const long long kb = [] {
+                    const char* e = std::getenv("FFCZ_MIXED_PIPE_KB");
+                    return e ? std::atoll(e) : 96LL;
+                }();
+                long long Bm = std::max<long long>(1, static_cast<long long>(kb * 1024 / per));
+                Bm = std::min<long long>({Bm, 16, static_cast<long long>(ncols)});
+                const size_t smem = per * Bm;
+                const long long ntiles = nplanes * ((ncols + Bm - 1) / Bm);
+                auto k = k_col_mixed_pipe<T>;
+                detail::set_smem(k, smem);
+                const unsigned grid = detail::persistent_grid(k, 256, smem, ntiles);
+                k<<<grid, 256, smem, st>>>(src, dst, make_mixed_plan(L), row_stride, plane_stride,
+                                           ncols, static_cast<int>(Bm), ntiles, tw.table_for(L),
+                                           dir, gate);
+                FFCZ_LAUNCH_CHECK();
+                return;
+            }
+        }
+        if (const int Bm = detail::mixed_enabled() ? detail::mixed_lines<T>(L, ncols) : 0) {
+            const size_t smem = 2 * sizeof(cplx<T>) * L * Bm;
+            detail::set_smem(k_col_mixed<T>, smem);
+            dim3 grid((ncols + Bm - 1) / Bm, static_cast<unsigned>(nplanes));
+            k_col_mixed<T><<<grid, 256, smem, st>>>(src, dst, make_mixed_plan(L), row_stride,
+                                                     plane_stride, ncols, Bm, tw.table_for(L),
+                                                     dir, gate);
+            FFCZ_LAUNCH_CHECK();
+            return;
+        }
         // direct O(L) pass: tile L x B columns in smem
         const size_t per_col = sizeof(cplx<T>) * L;
         if (per_col > 96 * 1024)
@@ -377,6 +444,16 @@ void launch_row_r2c(long long n2, const T* in, long long in_stride, cplx<T>* out
             FFCZ_POW2_CASES(X)
 #undef X
         }
+    }
+    const long long Lm = (n2 % 2 == 0) ? n2 / 2 : n2;  // packed real row: n2/2 points
+    if (const int R = detail::mixed_enabled() ? detail::mixed_lines<T>(Lm + 1, nrows) : 0) {
+        const size_t smem = 2 * sizeof(cplx<T>) * (Lm + 1) * R;
+        detail::set_smem(k_row_r2c_mixed<T>, smem);
+        k_row_r2c_mixed<T><<<static_cast<unsigned>((nrows + R - 1) / R), 256, smem, st>>>(
+            in, in_stride, out, out_stride, nrows, static_cast<int>(n2), R, make_mixed_plan(Lm),
+            tw.table_for(n2), gate);
+        FFCZ_LAUNCH_CHECK();
+        return;
     }
     const size_t smem = sizeof(T) * n2;
     if (smem > 96 * 1024) throw Error(kUnsupported, "last-axis extent too large for direct R2C");
@@ -447,6 +524,16 @@ void launch_row_c2r(long long n2, const cplx<T>* in, long long in_stride, T* out
             FFCZ_POW2_CASES(X)
 #undef X
         }
+    }
+    const long long Lm = (n2 % 2 == 0) ? n2 / 2 : n2;
+    if (const int R = detail::mixed_enabled() ? detail::mixed_lines<T>(Lm + 1, nrows) : 0) {
+        const size_t smem = 2 * sizeof(cplx<T>) * (Lm + 1) * R;
+        detail::set_smem(k_row_c2r_mixed<T>, smem);
+        k_row_c2r_mixed<T><<<static_cast<unsigned>((nrows + R - 1) / R), 256, smem, st>>>(
+            in, in_stride, out, out_stride, nrows, static_cast<int>(n2), R, make_mixed_plan(Lm),
+            tw.table_for(n2), scale, gate);
+        FFCZ_LAUNCH_CHECK();
+        return;
     }
     const size_t smem = sizeof(cplx<T>) * (n2 / 2 + 1);
     if (smem > 96 * 1024) throw Error(kUnsupported, "last-axis extent too large for direct C2R");
