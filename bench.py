@@ -468,13 +468,16 @@ def measured_peak():
     return 6650.0, "fallback"
 
 
-def ncu_traffic(name):
+def ncu_traffic(name, n=None):
     """dram bytes per launch of the dominant kernel from the committed ncu capture, or None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(path):
         return None
     with open(path) as f:
         d = json.load(f)
+    # the capture is of one size (_n^3); another size has no measured traffic
+    if n is not None and d.get("_n") not in (None, n):
+        return None
     return d.get(name)
 
 
@@ -627,7 +630,7 @@ def main():
     dom_name = dom.name.decode()
     peak, peak_kind = measured_peak()
     achieved = dom.bytes / (dom.total_ms * 1e-3) / 1e9 if dom.total_ms > 0 else 0.0
-    traffic = ncu_traffic(dom_name)
+    traffic = ncu_traffic(dom_name, n)
     launches = int(sum(r.kernel_launches for r in results))
     iters = [r.report.iterations for r in results]
     loop_ms = [r.timings_ms["t_loop_ms"] for r in results]
