@@ -44,7 +44,8 @@ typedef enum ffcz_cuda_status {
     FFCZ_IO_ERROR = 4,         /* ffcz::io_error                                                 */
     FFCZ_CUDA_ERROR = 5,       /* CUDA runtime / launch failure (no reference counterpart)      */
     FFCZ_UNSUPPORTED = 6,      /* shape/size the device engine does not implement yet           */
-    FFCZ_OUT_OF_MEMORY = 7
+    FFCZ_OUT_OF_MEMORY = 7,
+    FFCZ_UNDEFINED_METRIC = 8  /* ffcz::undefined_metric_error (metrics.cpp: psnr/ssnr/rfe)      */
 } ffcz_cuda_status;
 
 /* Sample type of the buffers passed in (the reference always holds doubles; f32 device buffers
@@ -234,6 +235,39 @@ int ffcz_cuda_alternating_projection(ffcz_cuda_ctx* ctx, const ffcz_field_desc* 
                                      const ffcz_cuda_options* opt, double* spatial_edits,
                                      double* frequency_edits, double* final_epsilon,
                                      ffcz_cuda_report* report);
+
+/* ---- device metrics (proj/core/src/metrics.cpp) ----------------------
+ * Field buffers are host pointers, or device pointers with on_device = 1 (then delta_out is a
+ * device pointer too).  dtype per field->dtype; everything is computed in FP64. */
+
+/* Replaces ffcz::spectrum_bound_to_freq_bounds(ffcz::forward_dft(original), rho)
+ * (metrics.cpp:107-128, called at proj/tools/ffcz.cpp:97-102): writes the FULL-spectrum
+ * per-component Delta (N doubles; the Re and Im lanes of the reference's DualBounds are equal).
+ * rho < 0 or non-finite -> FFCZ_VALIDATION_ERROR. */
+int ffcz_cuda_spectrum_bound(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const void* original,
+                             int on_device, double rho, double* delta_out);
+
+/* The quantities `ffcz metrics` reports (proj/tools/ffcz.cpp:246-256): psnr(original,
+ * reconstructed), ssnr(FFT(original), FFT(reconstructed)), max over rfe(FFT(reconstructed -
+ * original), FFT(original)) and max |reconstructed - original|.  psnr / ssnr are +inf for
+ * identical inputs; the reference's undefined_metric_error cases (constant original with
+ * nonzero error, zero-energy or all-zero original spectrum) -> FFCZ_UNDEFINED_METRIC. */
+typedef struct ffcz_cuda_metrics_out {
+    double psnr_db;
+    double ssnr_db;
+    double max_rfe;
+    double max_spatial;
+} ffcz_cuda_metrics_out;
+int ffcz_cuda_metrics(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const void* original,
+                      const void* reconstructed, int on_device, ffcz_cuda_metrics_out* out);
+
+/* Replaces ffcz::power_spectrum (metrics.cpp:11-62): shell-binned power of the normalised
+ * fluctuation spectrum.  *nbins_out = round(|centred Nyquist corner|) + 1; power == NULL is a
+ * size query; capacity < nbins -> FFCZ_VALIDATION_ERROR.  power[b] = sum |X_k|^2, counts[b] =
+ * number of full-spectrum cells in shell b; mean / mean_fallback as PowerSpectrum. */
+int ffcz_cuda_power_spectrum(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const void* x,
+                             int on_device, uint64_t capacity, double* power, uint64_t* counts,
+                             uint64_t* nbins_out, double* mean_out, int* mean_fallback_out);
 
 /* Replaces ffcz::forward_dft (transform.cpp:45-50): FP64, unnormalised; out = FULL spectrum,
  * 2N doubles interleaved.  Host pointers. */

@@ -757,6 +757,74 @@ def correct(original, decompressed, b: DualBounds, m: int = 16, max_iters: int =
 # helpers for the BASELINE configs
 
 
+class UndefinedMetric(ValueError):
+    """errors.hpp undefined_metric_error."""
+
+
+def power_spectrum(field: np.ndarray):
+    """src/metrics.cpp:11-62 -> (k_bins, power, counts, mean_fallback, mean)."""
+    x = np.asarray(field, dtype=np.float64)
+    mean = float(np.sum(x)) / x.size
+    max_abs = float(np.max(np.abs(x)))
+    fallback = abs(mean) <= 1e-12 * max_abs                       # metrics.cpp:21-24
+    fl = (x - mean) if fallback else (x - mean) / mean
+    X = forward_dft(fl)
+    max_bin = int(np.floor(np.sqrt(sum(float(d // 2) ** 2 for d in x.shape)) + 0.5))
+    r2 = np.zeros(x.shape)
+    for a, d in enumerate(x.shape):
+        c = np.arange(d, dtype=np.float64)
+        c[np.arange(d) > d // 2] -= d                                # metrics.cpp:48-52
+        sh = [1] * x.ndim
+        sh[a] = d
+        r2 = r2 + (c * c).reshape(sh)
+    bins = np.floor(np.sqrt(r2) + 0.5).astype(np.int64).ravel()      # llround, non-negative
+    power = np.bincount(bins, weights=np.abs(X.ravel()) ** 2, minlength=max_bin + 1)
+    counts = np.bincount(bins, minlength=max_bin + 1).astype(np.uint64)
+    return np.arange(max_bin + 1), power, counts, fallback, mean
+
+
+def psnr(original: np.ndarray, reconstructed: np.ndarray) -> float:
+    """src/metrics.cpp:64-79."""
+    o = np.asarray(original, dtype=np.float64)
+    d = np.asarray(reconstructed, dtype=np.float64) - o
+    se = float(np.sum(d * d))
+    if se == 0.0:
+        return float("inf")
+    lo, hi = float(o.min()), float(o.max())
+    if hi == lo:
+        raise UndefinedMetric("psnr: constant original has no defined range")
+    return 20.0 * np.log10((hi - lo) / np.sqrt(se / o.size))
+
+
+def ssnr(X: np.ndarray, Y: np.ndarray) -> float:
+    """src/metrics.cpp:81-93 on FULL spectra."""
+    signal = float(np.sum(np.abs(X) ** 2))
+    noise = float(np.sum(np.abs(X - Y) ** 2))
+    if signal == 0.0:
+        raise UndefinedMetric("ssnr: zero-energy original spectrum")
+    return float("inf") if noise == 0.0 else 10.0 * np.log10(signal / noise)
+
+
+def rfe(delta: np.ndarray, X: np.ndarray) -> np.ndarray:
+    """src/metrics.cpp:95-105."""
+    mx = float(np.max(np.abs(X)))
+    if mx == 0.0:
+        raise UndefinedMetric("rfe: all-zero original spectrum")
+    return np.abs(delta) / mx
+
+
+def metrics(original: np.ndarray, reconstructed: np.ndarray):
+    """What `ffcz metrics` reports (proj/tools/ffcz.cpp:246-256): psnr, ssnr, max rfe, max |eps|."""
+    o = np.asarray(original, dtype=np.float64)
+    r = np.asarray(reconstructed, dtype=np.float64)
+    X, Y = forward_dft(o), forward_dft(r)
+    eps = r - o
+    p = psnr(o, r)
+    s = ssnr(X, Y)
+    m = float(np.max(rfe(forward_dft(eps), X)))
+    return p, s, m, float(np.max(np.abs(eps)))
+
+
 def spectrum_bound_to_freq_bounds(X: np.ndarray, rho: float) -> np.ndarray:
     """src/metrics.cpp:107-128 -> per-component Delta (Re lane == Im lane)."""
     mag = np.abs(X)

@@ -7,10 +7,14 @@ from .ffcz import (  # noqa: F401
     Context, CorrectionResult, CudaError, DualBounds, EscapeEntry, FfczError, FormatError,
     ProjectionReport, SymmetryError, UnsupportedError, ValidationError, alternating_projection,
     apply_archive, correct, correct_batch, default_context, forward_dft, inverse_dft,
+    Metrics, PowerSpectrum, UndefinedMetricError, metrics, power_spectrum,
+    spectrum_bound_to_freq_bounds,
 )
 
 __all__ = [
     "Context", "CorrectionResult", "DualBounds", "EscapeEntry", "ProjectionReport", "FfczError",
     "ValidationError", "SymmetryError", "FormatError", "CudaError", "UnsupportedError",
     "correct", "correct_batch", "apply_archive", "alternating_projection", "forward_dft", "inverse_dft", "default_context",
+    "Metrics", "PowerSpectrum", "UndefinedMetricError", "metrics", "power_spectrum",
+    "spectrum_bound_to_freq_bounds",
 ]

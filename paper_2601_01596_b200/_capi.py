@@ -20,6 +20,7 @@ FFCZ_IO_ERROR = 4
 FFCZ_CUDA_ERROR = 5
 FFCZ_UNSUPPORTED = 6
 FFCZ_OUT_OF_MEMORY = 7
+FFCZ_UNDEFINED_METRIC = 8
 
 FFCZ_F32, FFCZ_F64 = 0, 1
 FFCZ_PRECISION_F32, FFCZ_PRECISION_F64 = 0, 1
@@ -41,13 +42,19 @@ EXPORTS = [
     "ffcz_cuda_r2c_device", "ffcz_cuda_c2r_device", "ffcz_cuda_crc32c",
     "ffcz_cuda_profile_enable", "ffcz_cuda_profile_read", "ffcz_cuda_bench_passes",
     "ffcz_cuda_slab", "ffcz_cuda_slab_pitch", "ffcz_cuda_huffman_encode",
-    "ffcz_cuda_apply_archive",
+    "ffcz_cuda_apply_archive", "ffcz_cuda_spectrum_bound", "ffcz_cuda_metrics",
+    "ffcz_cuda_power_spectrum",
 ]
 
 
 class FieldDesc(C.Structure):
     _fields_ = [("ndim", C.c_int32), ("dims", C.c_uint64 * 3), ("dtype", C.c_int32),
                 ("precision", C.c_int32)]
+
+
+class MetricsOut(C.Structure):
+    _fields_ = [("psnr_db", C.c_double), ("ssnr_db", C.c_double), ("max_rfe", C.c_double),
+                ("max_spatial", C.c_double)]
 
 
 class BoundsDesc(C.Structure):
@@ -132,6 +139,12 @@ def load():
         P, C.POINTER(FieldDesc), P, C.POINTER(BoundsDesc), C.c_uint64, C.c_double,
         C.POINTER(Options), P, P, P, C.POINTER(Report)]
     lib.ffcz_cuda_forward_dft.argtypes = [P, C.POINTER(FieldDesc), P, P]
+    lib.ffcz_cuda_spectrum_bound.argtypes = [P, C.POINTER(FieldDesc), P, C.c_int, C.c_double, P]
+    lib.ffcz_cuda_metrics.argtypes = [P, C.POINTER(FieldDesc), P, P, C.c_int,
+                                      C.POINTER(MetricsOut)]
+    lib.ffcz_cuda_power_spectrum.argtypes = [P, C.POINTER(FieldDesc), P, C.c_int, C.c_uint64, P, P,
+                                             C.POINTER(C.c_uint64), C.POINTER(C.c_double),
+                                             C.POINTER(C.c_int)]
     lib.ffcz_cuda_inverse_dft.argtypes = [P, C.POINTER(FieldDesc), P, C.c_int, P]
     lib.ffcz_cuda_r2c_device.argtypes = [P, C.POINTER(FieldDesc), P, P]
     lib.ffcz_cuda_c2r_device.argtypes = [P, C.POINTER(FieldDesc), P, P]

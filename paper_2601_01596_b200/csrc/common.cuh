@@ -19,7 +19,7 @@ struct Error : std::runtime_error {
 };
 
 enum Status { kOk = 0, kValidation = 1, kSymmetry = 2, kFormat = 3, kIo = 4, kCuda = 5,
-              kUnsupported = 6, kOom = 7 };
+              kUnsupported = 6, kOom = 7, kUndefined = 8 };
 
 #define FFCZ_CUDA_CHECK(expr)                                                                  \
     do {                                                                                       \

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <functional>
 #include <atomic>
 #include <map>
@@ -25,6 +26,7 @@
 #include "encode.cuh"
 #include "fft_plan.cuh"
 #include "kernels.cuh"
+#include "metrics.cuh"
 
 using namespace ffcz_gpu;
 
@@ -1724,6 +1726,53 @@ void correct_frames_fused(ffcz_cuda_ctx& c, const ffcz_field_desc& fd, uint64_t 
 
 } // namespace
 
+namespace {
+// the field as FP64 on the device (host buffers copied in; f32 widened)
+const double* metric_field(ffcz_cuda_ctx& c, const std::string& name, const Geometry& g,
+                           int dtype, const void* p, int on_device) {
+    if (!p) throw Error(kValidation, "null field buffer");
+    if (dtype == FFCZ_F64 && on_device) return static_cast<const double*>(p);
+    double* d = c.b<double>(name, g.N);
+    if (dtype == FFCZ_F64) {
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(d, p, g.N * 8, cudaMemcpyHostToDevice, c.st));
+        return d;
+    }
+    const float* f = static_cast<const float*>(p);
+    if (!on_device) {
+        float* t = c.b<float>(name + "_f32", g.N);
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(t, p, g.N * 4, cudaMemcpyHostToDevice, c.st));
+        f = t;
+    }
+    k_cast_to_double<<<grid_for(g.N), 256, 0, c.st>>>(f, d, g.N);
+    FFCZ_LAUNCH_CHECK();
+    return d;
+}
+template <class S>
+S read_stats(ffcz_cuda_ctx& c, const S* d) {
+    S h;
+    FFCZ_CUDA_CHECK(cudaMemcpyAsync(&h, d, sizeof(S), cudaMemcpyDeviceToHost, c.st));
+    c.sync();
+    return h;
+}
+FieldStats* fresh_field_stats(ffcz_cuda_ctx& c) {
+    FieldStats* d = c.b<FieldStats>("m_fstats", 1);
+    FieldStats z{};
+    z.lo = ~0ull;
+    FFCZ_CUDA_CHECK(cudaMemcpyAsync(d, &z, sizeof z, cudaMemcpyHostToDevice, c.st));
+    return d;
+}
+SpecStats* fresh_spec_stats(ffcz_cuda_ctx& c) {
+    SpecStats* d = c.b<SpecStats>("m_sstats", 1);
+    FFCZ_CUDA_CHECK(cudaMemsetAsync(d, 0, sizeof(SpecStats), c.st));
+    return d;
+}
+double bits_to_d(unsigned long long u) {
+    double d;
+    std::memcpy(&d, &u, 8);
+    return d;
+}
+} // namespace
+
 extern "C" {
 
 int ffcz_cuda_abi_version(void) { return FFCZ_CUDA_ABI_VERSION; }
@@ -2235,6 +2284,127 @@ int ffcz_cuda_alternating_projection(ffcz_cuda_ctx* ctx, const ffcz_field_desc* 
             FFCZ_CUDA_CHECK(cudaMemcpyAsync(frequency_edits, full, N * 16, cudaMemcpyDeviceToHost, st));
         }
         c.sync();
+    });
+}
+
+// ---- device metrics (metrics.cu; metrics.cpp) -------------------------------------------------
+
+int ffcz_cuda_spectrum_bound(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const void* original,
+                             int on_device, double rho, double* delta_out) {
+    return guarded(ctx, [&] {
+        if (!(rho >= 0.0) || !std::isfinite(rho))
+            throw Error(kValidation, "spectrum_bound_to_freq_bounds: rho must be >= 0");
+        const Geometry g = make_geometry(field->ndim, field->dims, kPitchAlign);
+        ffcz_cuda_ctx& c = *ctx;
+        const double* x = metric_field(c, "m_x", g, field->dtype, original, on_device);
+        double2* X = c.b<double2>("m_half", g.half_elems());
+        FftPlan<double>{g, &c.tw64}.r2c(x, X, nullptr, c.st);
+        SpecStats* ss = fresh_spec_stats(c);
+        k_spec_sums<<<grid_for(g.Nc()), 256, 0, c.st>>>(X, nullptr, nullptr, g.hg(), ss);
+        FFCZ_LAUNCH_CHECK();
+        const double max_mag = bits_to_d(read_stats(c, ss).max_abs_X);
+        const double floor_v = std::max(1e-12 * max_mag, 1e-300);
+        const double scale = (std::sqrt(1.0 + rho) - 1.0) / std::sqrt(2.0);
+        double* out = on_device ? delta_out : c.b<double>("m_delta", g.N);
+        k_spectrum_bound<<<grid_for(g.N), 256, 0, c.st>>>(X, g.d[0], g.d[1], g.n2, g.P, scale,
+                                                          floor_v, out);
+        FFCZ_LAUNCH_CHECK();
+        if (!on_device)
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(delta_out, out, g.N * 8, cudaMemcpyDeviceToHost, c.st));
+        c.sync();
+    });
+}
+
+int ffcz_cuda_metrics(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const void* original,
+                      const void* reconstructed, int on_device, ffcz_cuda_metrics_out* out) {
+    return guarded(ctx, [&] {
+        if (!out) throw Error(kValidation, "null metrics output");
+        const Geometry g = make_geometry(field->ndim, field->dims, kPitchAlign);
+        ffcz_cuda_ctx& c = *ctx;
+        cudaStream_t st = c.st;
+        const double* x = metric_field(c, "m_x", g, field->dtype, original, on_device);
+        const double* y = metric_field(c, "m_y", g, field->dtype, reconstructed, on_device);
+        double* e = c.b<double>("m_eps", g.N);
+        FieldStats* fs = fresh_field_stats(c);
+        k_field_stats<double><<<grid_for(g.N), 256, 0, st>>>(x, y, g.N, e, fs);
+        FFCZ_LAUNCH_CHECK();
+        FftPlan<double> plan{g, &c.tw64};
+        double2* X = c.b<double2>("m_half", g.half_elems());
+        double2* Y = c.b<double2>("m_half2", g.half_elems());
+        double2* D = c.b<double2>("m_half3", g.half_elems());
+        plan.r2c(x, X, nullptr, st);
+        plan.r2c(y, Y, nullptr, st);
+        plan.r2c(e, D, nullptr, st);
+        SpecStats* ss = fresh_spec_stats(c);
+        k_spec_sums<<<grid_for(g.Nc()), 256, 0, st>>>(X, Y, D, g.hg(), ss);
+        FFCZ_LAUNCH_CHECK();
+        const FieldStats hf = read_stats(c, fs);
+        const SpecStats hs = read_stats(c, ss);
+        const double inf = std::numeric_limits<double>::infinity();
+        out->max_spatial = bits_to_d(hf.max_abs_eps);
+        // psnr (metrics.cpp:64-79): zero error wins over a zero range
+        const double se = hf.sum[0];
+        if (se == 0.0) {
+            out->psnr_db = inf;
+        } else {
+            const double lo = ord_bits_decode(hf.lo), hi = ord_bits_decode(hf.hi);
+            if (hi == lo) throw Error(kUndefined, "psnr: constant original has no defined range");
+            out->psnr_db = 20.0 * std::log10((hi - lo) / std::sqrt(se / static_cast<double>(g.N)));
+        }
+        // ssnr (metrics.cpp:81-93)
+        if (hs.sum[0] == 0.0) throw Error(kUndefined, "ssnr: zero-energy original spectrum");
+        out->ssnr_db = hs.sum[1] == 0.0 ? inf : 10.0 * std::log10(hs.sum[0] / hs.sum[1]);
+        // max over rfe (metrics.cpp:95-105)
+        const double mx = bits_to_d(hs.max_abs_X);
+        if (mx == 0.0) throw Error(kUndefined, "rfe: all-zero original spectrum");
+        out->max_rfe = bits_to_d(hs.max_abs_D) / mx;
+    });
+}
+
+int ffcz_cuda_power_spectrum(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const void* x_in,
+                             int on_device, uint64_t capacity, double* power, uint64_t* counts,
+                             uint64_t* nbins_out, double* mean_out, int* mean_fallback_out) {
+    return guarded(ctx, [&] {
+        const Geometry g = make_geometry(field->ndim, field->dims, kPitchAlign);
+        double r2 = 0.0;
+        for (int a = 0; a < 3; ++a) {
+            const double cc = static_cast<double>(g.d[a] / 2);
+            r2 += cc * cc;
+        }
+        const uint64_t nbins = static_cast<uint64_t>(std::llround(std::sqrt(r2))) + 1;
+        if (nbins_out) *nbins_out = nbins;
+        if (!power) return;  // size query
+        if (capacity < nbins || !counts)
+            throw Error(kValidation, "power_spectrum: output capacity " + std::to_string(capacity) +
+                                         " < " + std::to_string(nbins) + " bins");
+        ffcz_cuda_ctx& c = *ctx;
+        cudaStream_t st = c.st;
+        const double* x = metric_field(c, "m_x", g, field->dtype, x_in, on_device);
+        FieldStats* fs = fresh_field_stats(c);
+        k_field_stats<double><<<grid_for(g.N), 256, 0, st>>>(x, nullptr, g.N, nullptr, fs);
+        FFCZ_LAUNCH_CHECK();
+        const FieldStats hf = read_stats(c, fs);
+        const double mean = hf.sum[1] / static_cast<double>(g.N);
+        const double max_abs = bits_to_d(hf.max_abs_x);
+        const bool fallback = std::abs(mean) <= 1e-12 * max_abs;  // metrics.cpp:21-24
+        double* fl = c.b<double>("m_eps", g.N);
+        k_fluct<double><<<grid_for(g.N), 256, 0, st>>>(x, g.N, mean, fallback ? 1 : 0, fl);
+        FFCZ_LAUNCH_CHECK();
+        double2* X = c.b<double2>("m_half", g.half_elems());
+        FftPlan<double>{g, &c.tw64}.r2c(fl, X, nullptr, st);
+        double* dp = c.b<double>("m_power", nbins);
+        unsigned long long* dc = c.b<unsigned long long>("m_counts", nbins);
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(dp, 0, nbins * 8, st));
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(dc, 0, nbins * 8, st));
+        const int nb = static_cast<int>(nbins);
+        const size_t smem = nbins <= static_cast<uint64_t>(kShellSmemBins) ? nbins * 16 : 0;
+        k_shell_power<<<grid_for(g.Nc()), 256, smem, st>>>(X, g.d[0], g.d[1], g.n2, g.P, nb, dp, dc);
+        FFCZ_LAUNCH_CHECK();
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(power, dp, nbins * 8, cudaMemcpyDeviceToHost, st));
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(counts, dc, nbins * 8, cudaMemcpyDeviceToHost, st));
+        c.sync();
+        if (mean_out) *mean_out = mean;
+        if (mean_fallback_out) *mean_fallback_out = fallback ? 1 : 0;
     });
 }
 

@@ -48,7 +48,11 @@ class UnsupportedError(FfczError):
     pass
 
 
-_STATUS = {capi.FFCZ_VALIDATION_ERROR: ValidationError, capi.FFCZ_SYMMETRY_ERROR: SymmetryError,
+class UndefinedMetricError(FfczError):
+    """ffcz::undefined_metric_error (errors.hpp): psnr / ssnr / rfe without a defined value."""
+
+
+_STATUS = {capi.FFCZ_UNDEFINED_METRIC: UndefinedMetricError, capi.FFCZ_VALIDATION_ERROR: ValidationError, capi.FFCZ_SYMMETRY_ERROR: SymmetryError,
            capi.FFCZ_FORMAT_ERROR: FormatError, capi.FFCZ_IO_ERROR: IoError,
            capi.FFCZ_CUDA_ERROR: CudaError, capi.FFCZ_UNSUPPORTED: UnsupportedError,
            capi.FFCZ_OUT_OF_MEMORY: CudaError}
@@ -456,6 +460,103 @@ def forward_dft(x, *, ctx: Context | None = None) -> np.ndarray:
     _check(capi.load().ffcz_cuda_forward_dft(ctx.handle, C.byref(fd), C.c_void_p(x.ctypes.data),
                                              C.c_void_p(out.ctypes.data)))
     return out
+
+
+def _metric_input(x):
+    """(pointer holder, shape, dtype code, on_device) for a numpy array or a CUDA tensor."""
+    if _is_torch(x):
+        import torch
+        if not x.is_cuda:
+            x = x.numpy()
+        else:
+            x = x.contiguous()
+            if x.dtype not in (torch.float32, torch.float64):
+                x = x.to(torch.float64)
+            return x, tuple(x.shape), capi.FFCZ_F32 if x.dtype == torch.float32 else capi.FFCZ_F64, 1
+    a = np.asarray(x)
+    a = np.ascontiguousarray(a, dtype=np.float32 if a.dtype == np.float32 else np.float64)
+    return a, a.shape, capi.FFCZ_F32 if a.dtype == np.float32 else capi.FFCZ_F64, 0
+
+
+def _vp(a):
+    return C.c_void_p(a.data_ptr() if _is_torch(a) else a.ctypes.data)
+
+
+def spectrum_bound_to_freq_bounds(original, rho: float, *, ctx: Context | None = None):
+    """ffcz::spectrum_bound_to_freq_bounds(forward_dft(original), rho) (metrics.cpp:107-128) on
+    the device: the FULL-spectrum per-component Delta (Re lane == Im lane), shaped like the field.
+    A CUDA tensor in gives a CUDA float64 tensor out."""
+    ctx = ctx or default_context()
+    x, shape, dt, dev = _metric_input(original)
+    if dev:
+        import torch
+        _order_after_torch(x)
+        out = torch.empty(shape, dtype=torch.float64, device=x.device)
+    else:
+        out = np.empty(shape, dtype=np.float64)
+    fd = _field_desc(shape, dt, "f64")
+    _check(capi.load().ffcz_cuda_spectrum_bound(ctx.handle, C.byref(fd), _vp(x), dev, float(rho),
+                                                _vp(out)))
+    return out
+
+
+@dataclass
+class Metrics:
+    """The values `ffcz metrics` prints (proj/tools/ffcz.cpp:246-278)."""
+    psnr_db: float
+    ssnr_db: float
+    max_rfe: float
+    max_spatial: float
+
+
+def metrics(original, reconstructed, *, ctx: Context | None = None) -> Metrics:
+    """psnr, ssnr of the spectra, max relative frequency error and max |eps| (metrics.cpp),
+    computed on the device.  Raises UndefinedMetricError where the reference throws."""
+    ctx = ctx or default_context()
+    x, shape, dt, dev = _metric_input(original)
+    y, shape2, dt2, dev2 = _metric_input(reconstructed)
+    if shape != shape2:
+        raise ValidationError("metrics: dims mismatch")
+    if dt != dt2 or dev != dev2:
+        raise ValidationError("metrics: both fields must have the same dtype and location")
+    _order_after_torch(x, y)
+    fd = _field_desc(shape, dt, "f64")
+    m = capi.MetricsOut()
+    _check(capi.load().ffcz_cuda_metrics(ctx.handle, C.byref(fd), _vp(x), _vp(y), dev,
+                                         C.byref(m)))
+    return Metrics(m.psnr_db, m.ssnr_db, m.max_rfe, m.max_spatial)
+
+
+@dataclass
+class PowerSpectrum:
+    """ffcz::PowerSpectrum (metrics.hpp:12-18)."""
+    k_bins: np.ndarray
+    power: np.ndarray
+    counts: np.ndarray
+    mean_fallback: bool
+    mean: float
+
+
+def power_spectrum(field, *, ctx: Context | None = None) -> PowerSpectrum:
+    """ffcz::power_spectrum (metrics.cpp:11-62) on the device."""
+    ctx = ctx or default_context()
+    x, shape, dt, dev = _metric_input(field)
+    _order_after_torch(x)
+    fd = _field_desc(shape, dt, "f64")
+    lib = capi.load()
+    nb = C.c_uint64()
+    _check(lib.ffcz_cuda_power_spectrum(ctx.handle, C.byref(fd), _vp(x), dev, 0, None, None,
+                                        C.byref(nb), None, None))
+    power = np.zeros(nb.value, dtype=np.float64)
+    counts = np.zeros(nb.value, dtype=np.uint64)
+    mean = C.c_double()
+    fb = C.c_int()
+    _check(lib.ffcz_cuda_power_spectrum(ctx.handle, C.byref(fd), _vp(x), dev, nb.value,
+                                        C.c_void_p(power.ctypes.data),
+                                        C.c_void_p(counts.ctypes.data), C.byref(nb),
+                                        C.byref(mean), C.byref(fb)))
+    return PowerSpectrum(np.arange(nb.value, dtype=np.uint64), power, counts, bool(fb.value),
+                         float(mean.value))
 
 
 def inverse_dft(X, precision: str = "f64", *, ctx: Context | None = None) -> np.ndarray:
