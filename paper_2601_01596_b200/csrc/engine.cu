@@ -211,7 +211,17 @@ constexpr int kPitchAlign = 16;
 // FFCZ_EPS0_FUSION=1: form eps0 inside the first R2C instead of a separate eps0 pass.  Off by
 // default: measured at 512^3 the fused kernel (840 us, 2.5 TB/s) is slower than the two passes
 // it replaces (376 + 343 us), so the separate pass stays.
-inline bool eps0_fusion_enabled() {
+inline // Escape repair on the decoder view (HookRepairVerifyS::dview; default on).  FFCZ_REPAIR_ORDER=
+// reference restores the reference's eps_tilde check plus a separate verify transform.
+bool decoder_view_repair() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_REPAIR_ORDER");
+        return !(e && std::strcmp(e, "reference") == 0);
+    }();
+    return on;
+}
+
+bool eps0_fusion_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("FFCZ_EPS0_FUSION");
         return e && e[0] == '1';
@@ -647,8 +657,9 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
         };
         bool verified = false;
         bool sc_zero = lr.s_zero;  // spat_cur stays zero until a spatial repair
+        const bool dview = decoder_view_repair();
         if (converged) {
-            double* eps_v = c.b<double>("eps_verify", N);
+            double* eps_v = dview ? nullptr : c.b<double>("eps_verify", N);
             for (int round = 0; round < 32; ++round) {                   // pipeline.cpp:116
                 FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->dirty, 0, sizeof(int), st));
                 FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->dirty_s, 0, sizeof(int), st));
@@ -659,7 +670,9 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
                 HookRepairVerifyS<TI> hk{orig, dec, spat_cur, eps, bo.sb, esc_s, corrected, eps_v,
                                          c.ctl};
                 hk.sc_zero = sc_zero;
-                inverse_and_row(hk, 16.0 * Nc + in_bytes - (sc_zero ? 8.0 * N : 0.0) + 24.0 * N);
+                hk.dview = dview;
+                inverse_and_row(hk, 16.0 * Nc + in_bytes - (sc_zero ? 8.0 * N : 0.0) +
+                                        (dview ? 16.0 : 24.0) * N);
                 {
                     Prof p(c, kColFwdCheck, pass);
                     plan.col(za, -1, work, work, nullptr, HookMarkViol{bo.fb, viol, c.ctl}, st);
@@ -671,6 +684,13 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
                 ++o.rounds;
                 const Ctl hr = c.read_ctl();
                 if (hr.dirty_s) sc_zero = false;
+                if (!hr.dirty && dview) {
+                    // clean round on the decoder view: no sample exceeded E and no component of
+                    // its spectrum exceeded Delta (both against the ORIGINAL bounds): that is
+                    // verify_bounds (archive.cpp:275-297), so vs = vf = 0
+                    verified = true;
+                    break;
+                }
                 if (!hr.dirty) {                                         // :161
                     // clean round: spat_cur / freq_cur are final and eps_v is their decoder
                     // view, so its forward transform completes verify_bounds
@@ -1316,6 +1336,7 @@ void gate_frames(ffcz_cuda_ctx& c, const Geometry& gf, const ffcz_field_desc& fd
 
     // escape-repair rounds (pipeline.cpp:111-163) for the converged frames
     std::vector<int> rounds(Gc, 0), verified(Gc, 0);
+    const bool dview = decoder_view_repair();
     std::vector<double> vs(Gc, 0.0), vf(Gc, 0.0);
     std::vector<int> active(Gc);
     for (long long i = 0; i < Gc; ++i) active[i] = hfc[i].converged;
@@ -1334,9 +1355,10 @@ void gate_frames(ffcz_cuda_ctx& c, const Geometry& gf, const ffcz_field_desc& fd
         reset_round();
         FFCZ_CUDA_CHECK(cudaMemsetAsync(viol, 0, vw * sizeof(unsigned), st));
         plan.col(1, +1, freq_cur, work, nullptr, HookMaskB<false>{fmk}, st);
-        launch_row_c2r_hook<double>(n2, work, gb.P, eps_t, n2, gb.rows, invN, c.tw64, nullptr,
-            HookRepairVerifySB<TI>{fmk, dE, fg, orig, dec, spat_cur, eps, esc_s, corrected, eps_v},
-            st);
+        HookRepairVerifySB<TI> hrv{fmk, dE, fg, orig, dec, spat_cur, eps, esc_s, corrected, eps_v};
+        hrv.dview = dview;
+        launch_row_c2r_hook<double>(n2, work, gb.P, eps_t, n2, gb.rows, invN, c.tw64, nullptr, hrv,
+                                    st);
         launch_row_r2c_hook<double>(n2, eps_t, n2, work, gb.P, gb.rows, c.tw64, nullptr,
                                     HookMaskB<true>{fmk}, st);
         plan.col(1, -1, work, work, nullptr, HookMarkViolB{fmk, dD, fg, viol}, st);
@@ -1352,11 +1374,13 @@ void gate_frames(ffcz_cuda_ctx& c, const Geometry& gf, const ffcz_field_desc& fd
             if (!hg_gate[i].dirty) {          // clean round: its decoder view is final (:161)
                 vs[i] = bitsd_host(hg_gate[i].vs_bits);
                 active[i] = 0;
-                verified[i] = 1;
+                // decoder-view repair: the clean round checked v and FFT(v) against the original
+                // bounds, i.e. verify_bounds itself (vf = 0)
+                verified[i] = dview ? 2 : 1;
                 any_clean = true;
             }
         }
-        if (any_clean) {  // verify the frames that came clean on this round's eps_v
+        if (any_clean && !dview) {  // verify the frames that came clean on this round's eps_v
             set_mask([&](long long i) { return verified[i] == 1; });
             launch_row_r2c_hook<double>(n2, eps_v, n2, work, gb.P, gb.rows, c.tw64, nullptr,
                                         HookMaskB<true>{fmk}, st);

@@ -444,6 +444,11 @@ struct HookRepairVerifyS {
     double* eps_v;
     Ctl* ctl;
     bool sc_zero = false;  // spat_cur is identically zero (no spatial edits): skip its load
+    // decoder-view repair: check and repair the decoder's own view v = (dec + S + fpart) - orig
+    // instead of eps_tilde = (dec - orig) + S + fpart (same value up to rounding) and hand v to
+    // the round's forward transform, so a clean round IS verify_bounds (no separate verify
+    // transform, no eps_v store).  Off = the reference's order (pipeline.cpp:134-160).
+    bool dview = false;
     int dirty = 0;
     double m = 0.0;
     // orig / dec rows prefetched into shared memory by the row kernel (hook_prefetch)
@@ -469,12 +474,12 @@ struct HookRepairVerifyS {
         const double c0 = d.x + sc.x + x0, c1 = d.y + sc.y + x1;
         const double v0 = c0 - o.x, v1 = c1 - o.y;
         if (corrected) *reinterpret_cast<double2*>(corrected + n) = make_double2(c0, c1);
-        *reinterpret_cast<double2*>(eps_v + n) = make_double2(v0, v1);
+        if (!dview) *reinterpret_cast<double2*>(eps_v + n) = make_double2(v0, v1);
         const double E0 = sb.at(n), E1 = sb.at(n + 1);
         const double ex0 = fabs(v0) - E0, ex1 = fabs(v1) - E1;
         if (ex0 > 0.0 && ex0 > m) m = ex0;
         if (ex1 > 0.0 && ex1 > m) m = ex1;
-        const double t0 = e0 + sc.x + x0, t1 = e1 + sc.y + x1;
+        const double t0 = dview ? v0 : e0 + sc.x + x0, t1 = dview ? v1 : e1 + sc.y + x1;
         bool w = false;
         if (fabs(t0) > E0) {
             sc.x = sc.x + (final_eps[n] - t0);
@@ -617,6 +622,7 @@ struct HookRepairVerifySB {
     unsigned* esc_words;
     double* corrected;
     double* eps_v;
+    bool dview = false;  // HookRepairVerifyS::dview
     long long frame = 0;
     double e = 0.0, m = 0.0;
     int dirty = 0;
@@ -635,11 +641,11 @@ struct HookRepairVerifySB {
         const double c0 = d.x + sc.x + x0, c1 = d.y + sc.y + x1;
         const double v0 = c0 - o.x, v1 = c1 - o.y;
         if (corrected) *reinterpret_cast<double2*>(corrected + n) = make_double2(c0, c1);
-        *reinterpret_cast<double2*>(eps_v + n) = make_double2(v0, v1);
+        if (!dview) *reinterpret_cast<double2*>(eps_v + n) = make_double2(v0, v1);
         const double ex0 = fabs(v0) - e, ex1 = fabs(v1) - e;
         if (ex0 > 0.0 && ex0 > m) m = ex0;
         if (ex1 > 0.0 && ex1 > m) m = ex1;
-        const double t0 = e0 + sc.x + x0, t1 = e1 + sc.y + x1;
+        const double t0 = dview ? v0 : e0 + sc.x + x0, t1 = dview ? v1 : e1 + sc.y + x1;
         bool w = false;
         if (fabs(t0) > e) {
             sc.x = sc.x + (final_eps[n] - t0);
