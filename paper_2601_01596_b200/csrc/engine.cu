@@ -211,7 +211,18 @@ constexpr int kPitchAlign = 16;
 // FFCZ_EPS0_FUSION=1: form eps0 inside the first R2C instead of a separate eps0 pass.  Off by
 // default: measured at 512^3 the fused kernel (840 us, 2.5 TB/s) is slower than the two passes
 // it replaces (376 + 343 us), so the separate pass stays.
-inline // Escape repair on the decoder view (HookRepairVerifyS::dview; default on).  FFCZ_REPAIR_ORDER=
+inline // Frequency gate and code compaction in one pass (k_gate_codes_freq, decoupled look-back) is
+// opt-in (FFCZ_GATE_CODES=1pass): at 512^3 it measured 1.74 ms per call against 1.46 ms for the
+// two-pass flags -> scan -> codes kernels it would replace (profiles/r01_summary.md).
+bool gate_codes_one_pass() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_GATE_CODES");
+        return e && std::strcmp(e, "1pass") == 0;
+    }();
+    return on;
+}
+
+// Escape repair on the decoder view (HookRepairVerifyS::dview; default on).  FFCZ_REPAIR_ORDER=
 // reference restores the reference's eps_tilde check plus a separate verify transform.
 bool decoder_view_repair() {
     static const bool on = [] {
@@ -557,8 +568,9 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
         c.launches += three_d ? 4 : 3;
     }
     FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->act_s, 0, 2 * sizeof(unsigned long long), st));
+    const bool one_pass = gate_codes_one_pass();
     {
-        Prof p(c, kElemGate, (lr.s_zero ? 0.0 : 16.0 * N) + 32.0 * Nc);
+        Prof p(c, kElemGate, (lr.s_zero ? 0.0 : 16.0 * N) + (one_pass ? 0.0 : 32.0 * Nc));
         if (lr.s_zero) {
             // S is identically zero (no spatial clip moved a sample): no spatial edits, no
             // overflow escapes, spat_cur = 0 (editset.cpp:43-66 on an all-zero S)
@@ -570,7 +582,18 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
                                                         c.ctl);
             ++c.launches;
         }
-        k_gate_freq<<<grid_for(Nc), 256, 0, st>>>(F, hg, bo.fb, m, freq_cur, keep_f, esc_f, c.ctl);
+        if (!one_pass)
+            k_gate_freq<<<grid_for(Nc), 256, 0, st>>>(F, hg, bo.fb, m, freq_cur, keep_f, esc_f,
+                                                       c.ctl);
+    }
+    if (one_pass) {
+        Prof p(c, kElemGate, 32.0 * Nc + 8.0 * Nc);  // F + Delta in, freq_cur + codes out
+        const long long nt = std::max<long long>(1, (Nc + kGateCodesTile - 1) / kGateCodesTile);
+        unsigned long long* tstat = c.b<unsigned long long>("gc_status", nt + 1);
+        unsigned* ticket = reinterpret_cast<unsigned*>(tstat + nt);
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(tstat, 0, (nt + 1) * sizeof(unsigned long long), st));
+        k_gate_codes_freq<<<static_cast<unsigned>(nt), 256, 0, st>>>(
+            F, hg, bo.fb, m, freq_cur, keep_f, esc_f, codes_f, tstat, ticket, nt, c.ctl);
     }
     FFCZ_LAUNCH_CHECK();
     ++c.launches;
@@ -597,9 +620,12 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
     o.n_keep_s = lr.s_zero ? 0 : codes_from(keep_s, ws, "blk_counts_s", [&](unsigned nb, unsigned long long* off) {
         k_codes_spatial_bits<<<nb, 1024, 0, st>>>(keep_s, ws, off, S, bo.sb, m, codes_s);
     });
-    o.n_keep_f = codes_from(keep_f, wf, "blk_counts_f", [&](unsigned nb, unsigned long long* off) {
-        k_codes_freq_bits<<<nb, 1024, 0, st>>>(keep_f, wf, off, F, hg, bo.fb, m, codes_f);
-    });
+    if (one_pass)
+        o.n_keep_f = c.read_ctl().count_b;  // count_a is the spatial compaction's
+    else
+        o.n_keep_f = codes_from(keep_f, wf, "blk_counts_f", [&](unsigned nb, unsigned long long* off) {
+            k_codes_freq_bits<<<nb, 1024, 0, st>>>(keep_f, wf, off, F, hg, bo.fb, m, codes_f);
+        });
     (void)idx;
     // flags and codes are final here (repair rounds only add escapes): hand them to the copy
     // stream so their D2H overlaps the repair / verify passes

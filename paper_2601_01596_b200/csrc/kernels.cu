@@ -410,6 +410,125 @@ __global__ void k_gate_freq(const double2* __restrict__ F, HalfGeom g, FreqB fb,
     block_sum_atomic(nz_acc, &ctl->act_f);
 }
 
+// k_gate_freq + k_codes_freq_bits in ONE pass (single-pass compaction with decoupled look-back):
+// each CTA takes the next tile of kGcTile half entries by ticket (so every predecessor tile is
+// already resident), quantises, writes flags / freq_cur, ranks its kept entries in ascending h,
+// publishes its count, looks back for its exclusive offset, and stores the int32 code pairs —
+// F and Delta are read once instead of twice.  Same values as the two-pass kernels.
+constexpr int kGcItems = 16, kGcThreads = 256, kGcTile = kGcItems * kGcThreads;
+constexpr unsigned long long kGcAgg = 1ull << 62, kGcIncl = 2ull << 62, kGcMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kGcThreads) k_gate_codes_freq(
+    const double2* __restrict__ F, HalfGeom g, FreqB fb, int m, double2* freq_cur,
+    unsigned* keep_words, unsigned* esc_words, int* codes, unsigned long long* tile_status,
+    unsigned* tile_ticket, long long ntiles, Ctl* ctl) {
+    __shared__ long long s_tile;
+    __shared__ unsigned s_cnt[kGcItems][kGcThreads / 32];
+    __shared__ unsigned long long s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ticket, 1u);
+    __syncthreads();
+    const long long t = s_tile;
+    const long long total = g.rows * g.H;
+    const long long base = t * kGcTile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned kmask[kGcItems];
+    int2 code[kGcItems];
+    unsigned long long nz_acc = 0;
+#pragma unroll
+    for (int u = 0; u < kGcItems; ++u) {
+        const long long h = base + u * kGcThreads + threadIdx.x;
+        bool keep = false, ovf = false;
+        code[u] = make_int2(0, 0);
+        if (h < total) {
+            long long q = static_cast<long long>(static_cast<double>(h) * g.invH);
+            long long r = h - q * g.H;
+            if (r < 0) { --q; r += g.H; } else if (r >= g.H) { ++q; r -= g.H; }
+            const long long off = q * g.P + r;
+            const double2 v = F[off];
+            const bool nz = v.x != 0.0 || v.y != 0.0;
+            const double2 db = fb.at2(off);
+            const double sre = ldexp(2.0 * db.x, -m);   // editset.cpp:35-41
+            const double sim = ldexp(2.0 * db.y, -m);
+            ovf = nz && (fabs(v.x) / sre > kMaxIndex || fabs(v.y) / sim > kMaxIndex);  // :68-69
+            keep = nz && !ovf;
+            double2 cur = make_double2(0.0, 0.0);
+            if (keep) {
+                code[u] = make_int2(static_cast<int>(llround(v.x / sre)),
+                                    static_cast<int>(llround(v.y / sim)));
+                cur.x = static_cast<double>(code[u].x) * sre;
+                cur.y = static_cast<double>(code[u].y) * sim;
+            } else if (ovf) {
+                cur = v;
+            }
+            freq_cur[off] = cur;
+            if (nz) nz_acc += plane_weight(static_cast<int>(r), g.n2);
+        }
+        const unsigned bk = __ballot_sync(0xffffffffu, keep);
+        const unsigned be = __ballot_sync(0xffffffffu, ovf);
+        if (lane == 0 && h < total) {
+            keep_words[h >> 5] = bk;
+            esc_words[h >> 5] = be;
+            s_cnt[u][warp] = __popc(bk);
+        } else if (lane == 0) {
+            s_cnt[u][warp] = 0;
+        }
+        kmask[u] = bk;
+    }
+    __syncthreads();
+    // tile-local exclusive offsets in ascending h: (item u, warp w) in u-major order
+    if (threadIdx.x == 0) {
+        unsigned acc = 0;
+        for (int u = 0; u < kGcItems; ++u)
+            for (int w = 0; w < kGcThreads / 32; ++w) {
+                const unsigned c = s_cnt[u][w];
+                s_cnt[u][w] = acc;
+                acc += c;
+            }
+        s_prefix = acc;  // the tile's aggregate, until the look-back below replaces it
+        atomicExch(&tile_status[t], (t == 0 ? kGcIncl : kGcAgg) | acc);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // warp-parallel look-back over 32 predecessors at a time (decoupled look-back)
+        const unsigned long long agg = s_prefix;
+        unsigned long long excl = 0;
+        long long hi = t - 1;
+        while (hi >= 0) {
+            const long long i = hi - lane;
+            unsigned long long st = kGcIncl;  // lanes past tile 0: an inclusive zero
+            if (i >= 0) {
+                do {
+                    st = *reinterpret_cast<volatile unsigned long long*>(&tile_status[i]);
+                } while ((st >> 62) == 0);
+            }
+            const unsigned incl = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+            // nearest inclusive predecessor: the lowest lane with one; sum lanes up to it
+            const int stop = incl ? __ffs(incl) - 1 : 31;
+            unsigned long long v = lane <= stop ? (st & kGcMask) : 0;
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            excl += v;
+            if (incl) break;
+            hi -= 32;
+        }
+        if (lane == 0) {
+            if (t > 0) {
+                __threadfence();
+                atomicExch(&tile_status[t], kGcIncl | (excl + agg));
+            }
+            if (t == ntiles - 1) ctl->count_b = excl + agg;
+            s_prefix = excl;
+        }
+    }
+    __syncthreads();
+    const unsigned long long p0 = s_prefix;
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int u = 0; u < kGcItems; ++u)
+        if (kmask[u] >> lane & 1u)
+            reinterpret_cast<int2*>(codes)[p0 + s_cnt[u][warp] + __popc(kmask[u] & lt)] = code[u];
+    block_sum_atomic(nz_acc, &ctl->act_f);
+}
+
 __global__ void k_popc_blocks(const unsigned* __restrict__ words, long long nwords,
                               unsigned long long* block_counts) {
     __shared__ unsigned long long s[32];

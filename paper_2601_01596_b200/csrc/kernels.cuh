@@ -822,6 +822,11 @@ __global__ void k_expand_full(const double2* __restrict__ half, double2* full, i
 __global__ void k_gate_spatial(const double* __restrict__ S, long long N, SpatialB sb, int m,
                                double* spat_cur, unsigned* keep_words, unsigned* esc_words,
                                Ctl* ctl);
+__global__ void k_gate_codes_freq(const double2* __restrict__ F, HalfGeom g, FreqB fb, int m,
+                                  double2* freq_cur, unsigned* keep_words, unsigned* esc_words,
+                                  int* codes, unsigned long long* tile_status,
+                                  unsigned* tile_ticket, long long ntiles, Ctl* ctl);
+constexpr long long kGateCodesTile = 4096;  // k_gate_codes_freq: half entries per tile
 __global__ void k_gate_freq(const double2* __restrict__ F, HalfGeom g, FreqB fb, int m,
                             double2* freq_cur, unsigned* keep_words, unsigned* esc_words,
                             Ctl* ctl);
