@@ -387,12 +387,15 @@ __global__ void k_gate_freq(const double2* __restrict__ F, HalfGeom g, FreqB fb,
             const double2 db = fb.at2(off);
             const double sre = ldexp(2.0 * db.x, -m);   // editset.cpp:35-41
             const double sim = ldexp(2.0 * db.y, -m);
-            ovf = nz && (fabs(v.x) / sre > kMaxIndex || fabs(v.y) / sim > kMaxIndex);  // :68-69
+            // v / step == ldexp(v / Delta, m - 1) bit for bit (step = Delta 2^(1-m); scaling by a
+            // power of two commutes with rounding): one division per lane instead of two
+            const double qx = ldexp(v.x / db.x, m - 1), qy = ldexp(v.y / db.y, m - 1);
+            ovf = nz && (fabs(qx) > kMaxIndex || fabs(qy) > kMaxIndex);  // :68-69
             keep = nz && !ovf;
             double2 cur = make_double2(0.0, 0.0);
             if (keep) {
-                cur.x = static_cast<double>(static_cast<int>(llround(v.x / sre))) * sre;
-                cur.y = static_cast<double>(static_cast<int>(llround(v.y / sim))) * sim;
+                cur.x = static_cast<double>(static_cast<int>(llround(qx))) * sre;
+                cur.y = static_cast<double>(static_cast<int>(llround(qy))) * sim;
             } else if (ovf) {
                 cur = v;
             }
@@ -732,19 +735,19 @@ struct EmitCodesF {
         for (int u = 0; u < 4; ++u)
             if (act[u])
                 reinterpret_cast<int2*>(codes)[pos[u]] =
-                    make_int2(static_cast<int>(llround(v[u].x / ldexp(2.0 * d[u].x, -m))),
-                              static_cast<int>(llround(v[u].y / ldexp(2.0 * d[u].y, -m))));
+                    make_int2(static_cast<int>(llround(ldexp(v[u].x / d[u].x, m - 1))),
+                              static_cast<int>(llround(ldexp(v[u].y / d[u].y, m - 1))));
     }
 };
 } // namespace
 
-__global__ void k_codes_spatial_bits(const unsigned* __restrict__ keep_words, long long nwords,
+__global__ void __launch_bounds__(1024) k_codes_spatial_bits(const unsigned* __restrict__ keep_words, long long nwords,
                                      const unsigned long long* __restrict__ block_offsets,
                                      const double* __restrict__ S, SpatialB sb, int m, int* codes) {
     codes_from_bits(keep_words, nwords, block_offsets, EmitCodesS{S, sb, m, codes});
 }
 
-__global__ void k_codes_freq_bits(const unsigned* __restrict__ keep_words, long long nwords,
+__global__ void __launch_bounds__(1024) k_codes_freq_bits(const unsigned* __restrict__ keep_words, long long nwords,
                                   const unsigned long long* __restrict__ block_offsets,
                                   const double2* __restrict__ F, HalfGeom g, FreqB fb, int m,
                                   int* codes) {
@@ -762,7 +765,7 @@ __global__ void k_dequant_spatial_bits(const unsigned* __restrict__ keep_words, 
     });
 }
 
-__global__ void k_dequant_freq_bits(const unsigned* __restrict__ keep_words, long long nwords,
+__global__ void __launch_bounds__(1024) k_dequant_freq_bits(const unsigned* __restrict__ keep_words, long long nwords,
                                     const unsigned long long* __restrict__ block_offsets,
                                     const int* __restrict__ codes, HalfGeom g, FreqB fb, int m,
                                     double2* freq) {
@@ -1114,7 +1117,7 @@ __global__ void k_codes_spatial_frames(const unsigned* __restrict__ keep_words, 
     });
 }
 
-__global__ void k_codes_freq_frames(const unsigned* __restrict__ keep_words, long long nwords,
+__global__ void __launch_bounds__(1024) k_codes_freq_frames(const unsigned* __restrict__ keep_words, long long nwords,
                                     const unsigned long long* __restrict__ block_offsets,
                                     const double2* __restrict__ F, HalfGeom g, long long n1,
                                     const double* __restrict__ D, int m, int* codes) {

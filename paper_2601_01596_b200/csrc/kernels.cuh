@@ -846,10 +846,10 @@ __global__ void k_codes_freq(const unsigned long long* __restrict__ idx, long lo
                              int* codes);
 // the same codes straight from the keep bitmap + k_popc_blocks/k_scan_blocks offsets (1024
 // words per CTA, 1024 threads): no index list round trip
-__global__ void k_codes_spatial_bits(const unsigned* __restrict__ keep_words, long long nwords,
+__global__ void __launch_bounds__(1024) k_codes_spatial_bits(const unsigned* __restrict__ keep_words, long long nwords,
                                      const unsigned long long* __restrict__ block_offsets,
                                      const double* __restrict__ S, SpatialB sb, int m, int* codes);
-__global__ void k_codes_freq_bits(const unsigned* __restrict__ keep_words, long long nwords,
+__global__ void __launch_bounds__(1024) k_codes_freq_bits(const unsigned* __restrict__ keep_words, long long nwords,
                                   const unsigned long long* __restrict__ block_offsets,
                                   const double2* __restrict__ F, HalfGeom g, FreqB fb, int m,
                                   int* codes);
@@ -889,7 +889,7 @@ __global__ void k_dequant_spatial_bits(const unsigned* __restrict__ keep_words, 
                                        const unsigned long long* __restrict__ block_offsets,
                                        const int* __restrict__ codes, SpatialB sb, int m,
                                        double* spat);
-__global__ void k_dequant_freq_bits(const unsigned* __restrict__ keep_words, long long nwords,
+__global__ void __launch_bounds__(1024) k_dequant_freq_bits(const unsigned* __restrict__ keep_words, long long nwords,
                                     const unsigned long long* __restrict__ block_offsets,
                                     const int* __restrict__ codes, HalfGeom g, FreqB fb, int m,
                                     double2* freq);
@@ -923,7 +923,7 @@ __global__ void k_codes_spatial_frames(const unsigned* __restrict__ keep_words, 
                                        const unsigned long long* __restrict__ block_offsets,
                                        const double* __restrict__ S, long long frameN,
                                        const double* __restrict__ E, int m, int* codes);
-__global__ void k_codes_freq_frames(const unsigned* __restrict__ keep_words, long long nwords,
+__global__ void __launch_bounds__(1024) k_codes_freq_frames(const unsigned* __restrict__ keep_words, long long nwords,
                                     const unsigned long long* __restrict__ block_offsets,
                                     const double2* __restrict__ F, HalfGeom g, long long n1,
                                     const double* __restrict__ D, int m, int* codes);

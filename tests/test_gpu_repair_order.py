@@ -1,0 +1,65 @@
+"""The reference's escape-repair order (FFCZ_REPAIR_ORDER=reference: check eps_tilde, then a
+separate verify transform, pipeline.cpp:111-176) still reproduces the golden outputs, and both
+orders give identical flags / codes on the same case (decoder-view repair).  The
+switch is read once per process, so the reference-order run is a subprocess."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+_SNIPPET = r"""
+import sys, json, hashlib
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import numpy as np
+import cases
+import paper_2601_01596_b200 as P
+out = {}
+for c in cases.all_cases():
+    if c.name not in %r:
+        continue
+    r = P.correct(c.original, c.decompressed, P.DualBounds(c.E, c.Dre, c.Dim), c.m, c.max_iters,
+                  c.precision)
+    out[c.name] = {"iterations": r.report.iterations, "verify_ok": bool(r.verify_ok),
+                   "escapes": int(r.escape_count),
+                   "flags": hashlib.sha256(r.frequency_flags.tobytes() + r.spatial_flags.tobytes()).hexdigest(),
+                   "codes": hashlib.sha256(r.frequency_codes.tobytes() + r.spatial_codes.tobytes()).hexdigest()}
+print(json.dumps(out))
+"""
+
+NAMES = ["config1_c1.0", "config1_c0.6", "config2_rho32", "accept_05", "odd_12x10x9"]
+
+
+def _run(order):
+    env = dict(os.environ)
+    if order:
+        env["FFCZ_REPAIR_ORDER"] = order
+    else:
+        env.pop("FFCZ_REPAIR_ORDER", None)
+    code = _SNIPPET % (ROOT, os.path.join(ROOT, "tests"), NAMES)
+    p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    return json.loads(p.stdout.strip().splitlines()[-1])
+
+
+def test_repair_orders_agree_with_golden():
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
+    ref_order = _run("reference")
+    dview = _run(None)
+    assert set(ref_order) == set(dview) and ref_order
+    for name in ref_order:
+        a, b, g = ref_order[name], dview[name], gold[name]
+        assert a["iterations"] == b["iterations"] == g["iterations"]
+        assert a["verify_ok"] == g["verify_ok"]
+        if g["converged"]:
+            assert b["verify_ok"]
+        assert a["flags"] == b["flags"] and a["codes"] == b["codes"]
+        assert abs(a["escapes"] - g["escape_count"]) <= max(2, g["escape_count"] // 10)
+        assert abs(b["escapes"] - g["escape_count"]) <= max(2, g["escape_count"] // 10)
