@@ -2356,8 +2356,8 @@ int ffcz_cuda_spectrum_bound(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, c
         const double floor_v = std::max(1e-12 * max_mag, 1e-300);
         const double scale = (std::sqrt(1.0 + rho) - 1.0) / std::sqrt(2.0);
         double* out = on_device ? delta_out : c.b<double>("m_delta", g.N);
-        k_spectrum_bound<<<grid_for(g.N), 256, 0, c.st>>>(X, g.d[0], g.d[1], g.n2, g.P, scale,
-                                                          floor_v, out);
+        k_spectrum_bound<<<grid_for(g.Nc()), 256, 0, c.st>>>(X, g.d[0], g.d[1], g.n2, g.P, scale,
+                                                            floor_v, out);
         FFCZ_LAUNCH_CHECK();
         if (!on_device)
             FFCZ_CUDA_CHECK(cudaMemcpyAsync(delta_out, out, g.N * 8, cudaMemcpyDeviceToHost, c.st));

@@ -142,31 +142,29 @@ __global__ void k_spec_sums(const double2* __restrict__ X, const double2* __rest
     block_reduce_max(mxD, &st->max_abs_D);
 }
 
-// spectrum_bound_to_freq_bounds on the FULL grid from the half spectrum: Delta_k =
-// max(min(|X_k|, |X_mirror(k)|) * scale, floor); a full index whose own entry is not stored
-// reads its mirror (same magnitude), a stored one whose mirror is also stored takes the min.
+// spectrum_bound_to_freq_bounds on the FULL grid from the half spectrum, one thread per STORED
+// entry: Delta = max(min(|X_k|, |X_mirror(k)|) * scale, floor) written at k and at its mirror
+// (the mirror of a stored entry off the self-mirror planes is not stored and has the same
+// magnitude; on the planes k2 = 0 and k2 = n2/2 both partners are stored and the min is taken,
+// each thread writing its own k).
 __global__ void k_spectrum_bound(const double2* __restrict__ X, long long d0, long long d1,
                                  long long n2, int P, double scale, double floor_v,
                                  double* __restrict__ delta) {
-    const long long H = n2 / 2 + 1, N = d0 * d1 * n2;
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < N;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long k2 = i % n2, r = i / n2, k1 = r % d1, k0 = r / d1;
-        const long long m2 = k2 == 0 ? 0 : n2 - k2, m1 = k1 == 0 ? 0 : d1 - k1,
-                        m0 = k0 == 0 ? 0 : d0 - k0;
-        double mag;
-        if (k2 < H) {
-            const double2 a = X[(k0 * d1 + k1) * P + k2];
-            mag = hypot(a.x, a.y);
-            if (m2 < H) {
-                const double2 b = X[(m0 * d1 + m1) * P + m2];
-                mag = fmin(mag, hypot(b.x, b.y));
-            }
-        } else {
+    const long long H = n2 / 2 + 1, Nc = d0 * d1 * H;
+    for (long long h = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; h < Nc;
+         h += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long k2 = h % H, r = h / H, k1 = r % d1, k0 = r / d1;
+        const long long m1 = k1 == 0 ? 0 : d1 - k1, m0 = k0 == 0 ? 0 : d0 - k0;
+        const long long m2 = k2 == 0 ? 0 : n2 - k2;
+        const double2 a = X[r * P + k2];
+        double mag = hypot(a.x, a.y);
+        if (m2 < H) {  // self-mirror plane: the partner is stored too
             const double2 b = X[(m0 * d1 + m1) * P + m2];
-            mag = hypot(b.x, b.y);
+            mag = fmin(mag, hypot(b.x, b.y));
         }
-        delta[i] = fmax(mag * scale, floor_v);
+        const double v = fmax(mag * scale, floor_v);
+        delta[r * n2 + k2] = v;
+        if (m2 >= H) delta[(m0 * d1 + m1) * n2 + m2] = v;
     }
 }
 
