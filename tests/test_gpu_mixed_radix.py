@@ -10,7 +10,7 @@ from oracle import ffcz_oracle as O
 pytestmark = pytest.mark.gpu
 
 # radix-2/3/4/5/7 products, generic primes (11, 13, 17, 97), a prime row (97), a 6000-point row
-# (two 96 KB ping-pong buffers) and a 7000-point row (above the mixed limit: direct pass)
+# (packed: two 3001-point ping-pong buffers) and a 7000-point row
 SHAPES = [(2,), (3,), (6,), (2, 3), (420,), (143,), (97,), (2310,), (6000,), (7000,), (100, 120), (250, 96), (60, 50, 48),
           (27, 25, 49), (11, 13, 17), (125, 36, 30), (3, 5, 7)]
 
