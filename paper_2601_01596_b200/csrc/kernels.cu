@@ -345,7 +345,7 @@ __global__ void k_gate_spatial(const double* __restrict__ S, long long N, Spatia
             bool keep = false, ovf = false;
             if (n < N) {
                 const bool nz = v[u] != 0.0;
-                const double step = ldexp(2.0 * E[u], -m);       // editset.cpp:31-33
+                const double step = ((E[u]) * pow2i(1 - m));       // editset.cpp:31-33
                 ovf = nz && (fabs(v[u]) / step > kMaxIndex);     // pipeline.cpp:63-64
                 keep = nz && !ovf;
                 double cur = 0.0;
@@ -385,11 +385,11 @@ __global__ void k_gate_freq(const double2* __restrict__ F, HalfGeom g, FreqB fb,
             const double2 v = F[off];
             const bool nz = v.x != 0.0 || v.y != 0.0;
             const double2 db = fb.at2(off);
-            const double sre = ldexp(2.0 * db.x, -m);   // editset.cpp:35-41
-            const double sim = ldexp(2.0 * db.y, -m);
-            // v / step == ldexp(v / Delta, m - 1) bit for bit (step = Delta 2^(1-m); scaling by a
+            const double sre = ((db.x) * pow2i(1 - m));   // editset.cpp:35-41
+            const double sim = ((db.y) * pow2i(1 - m));
+            // v / step == (v / Delta) 2^(m-1) bit for bit (step = Delta 2^(1-m); scaling by a
             // power of two commutes with rounding): one division per lane instead of two
-            const double qx = ldexp(v.x / db.x, m - 1), qy = ldexp(v.y / db.y, m - 1);
+            const double qx = ((v.x / db.x) * pow2i(m - 1)), qy = ((v.y / db.y) * pow2i(m - 1));
             ovf = nz && (fabs(qx) > kMaxIndex || fabs(qy) > kMaxIndex);  // :68-69
             keep = nz && !ovf;
             double2 cur = make_double2(0.0, 0.0);
@@ -450,8 +450,8 @@ __global__ void __launch_bounds__(kGcThreads) k_gate_codes_freq(
             const double2 v = F[off];
             const bool nz = v.x != 0.0 || v.y != 0.0;
             const double2 db = fb.at2(off);
-            const double sre = ldexp(2.0 * db.x, -m);   // editset.cpp:35-41
-            const double sim = ldexp(2.0 * db.y, -m);
+            const double sre = ((db.x) * pow2i(1 - m));   // editset.cpp:35-41
+            const double sim = ((db.y) * pow2i(1 - m));
             ovf = nz && (fabs(v.x) / sre > kMaxIndex || fabs(v.y) / sim > kMaxIndex);  // :68-69
             keep = nz && !ovf;
             double2 cur = make_double2(0.0, 0.0);
@@ -602,7 +602,7 @@ __global__ void k_codes_spatial(const unsigned long long* __restrict__ idx, long
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const long long k = idx[i];
-        const double step = ldexp(2.0 * sb.at(k), -m);
+        const double step = ((sb.at(k)) * pow2i(1 - m));
         codes[i] = static_cast<int>(llround(S[k] / step));
     }
 }
@@ -614,8 +614,8 @@ __global__ void k_codes_freq(const unsigned long long* __restrict__ idx, long lo
          i += (long long)gridDim.x * blockDim.x) {
         const long long off = g.offset_of(static_cast<long long>(idx[i]));
         const double2 v = F[off];
-        const double sre = ldexp(2.0 * fb.re_at(off), -m);
-        const double sim = ldexp(2.0 * fb.im_at(off), -m);
+        const double sre = ((fb.re_at(off)) * pow2i(1 - m));
+        const double sim = ((fb.im_at(off)) * pow2i(1 - m));
         codes[2 * i] = static_cast<int>(llround(v.x / sre));
         codes[2 * i + 1] = static_cast<int>(llround(v.y / sim));
     }
@@ -710,7 +710,7 @@ struct EmitCodesS {
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            if (act[u]) codes[pos[u]] = static_cast<int>(llround(v[u] / ldexp(2.0 * e[u], -m)));
+            if (act[u]) codes[pos[u]] = static_cast<int>(llround(v[u] / ((e[u]) * pow2i(1 - m))));
     }
 };
 
@@ -735,8 +735,8 @@ struct EmitCodesF {
         for (int u = 0; u < 4; ++u)
             if (act[u])
                 reinterpret_cast<int2*>(codes)[pos[u]] =
-                    make_int2(static_cast<int>(llround(ldexp(v[u].x / d[u].x, m - 1))),
-                              static_cast<int>(llround(ldexp(v[u].y / d[u].y, m - 1))));
+                    make_int2(static_cast<int>(llround(((v[u].x / d[u].x) * pow2i(m - 1)))),
+                              static_cast<int>(llround(((v[u].y / d[u].y) * pow2i(m - 1)))));
     }
 };
 } // namespace
@@ -761,7 +761,7 @@ __global__ void k_dequant_spatial_bits(const unsigned* __restrict__ keep_words, 
                                        const int* __restrict__ codes, SpatialB sb, int m,
                                        double* spat) {
     codes_from_bits(keep_words, nwords, block_offsets, [&](long long n, unsigned long long pos) {
-        spat[n] = static_cast<double>(codes[pos]) * ldexp(2.0 * sb.at(n), -m);
+        spat[n] = static_cast<double>(codes[pos]) * ((sb.at(n)) * pow2i(1 - m));
     });
 }
 
@@ -773,8 +773,8 @@ __global__ void __launch_bounds__(1024) k_dequant_freq_bits(const unsigned* __re
         const long long off = g.offset_of(h);
         const double2 d = fb.at2(off);
         const int2 c = reinterpret_cast<const int2*>(codes)[pos];
-        freq[off] = make_double2(static_cast<double>(c.x) * ldexp(2.0 * d.x, -m),
-                                 static_cast<double>(c.y) * ldexp(2.0 * d.y, -m));
+        freq[off] = make_double2(static_cast<double>(c.x) * ((d.x) * pow2i(1 - m)),
+                                 static_cast<double>(c.y) * ((d.y) * pow2i(1 - m)));
     });
 }
 
@@ -1049,7 +1049,7 @@ __global__ void k_gate_spatial_frames(const double* __restrict__ S, long long N,
         if (n < N) {
             const double v = S[n];
             const bool nz = v != 0.0;
-            const double step = ldexp(2.0 * E[f], -m);           // editset.cpp:31-33
+            const double step = ((E[f]) * pow2i(1 - m));           // editset.cpp:31-33
             ovf = nz && (fabs(v) / step > kMaxIndex);            // pipeline.cpp:63-64
             keep = nz && !ovf;
             double cur = 0.0;
@@ -1082,7 +1082,7 @@ __global__ void k_gate_freq_frames(const double2* __restrict__ F, HalfGeom g, lo
             const long long off = hw.row * g.P + k2;
             const double2 v = F[off];
             const bool nz = v.x != 0.0 || v.y != 0.0;
-            const double st = ldexp(2.0 * D[frame], -m);          // editset.cpp:35-41
+            const double st = ((D[frame]) * pow2i(1 - m));          // editset.cpp:35-41
             ovf = nz && (fabs(v.x) / st > kMaxIndex || fabs(v.y) / st > kMaxIndex);
             keep = nz && !ovf;
             double2 cur = make_double2(0.0, 0.0);
@@ -1112,7 +1112,7 @@ __global__ void k_codes_spatial_frames(const unsigned* __restrict__ keep_words, 
                                        const double* __restrict__ S, long long frameN,
                                        const double* __restrict__ E, int m, int* codes) {
     codes_from_bits(keep_words, nwords, block_offsets, [&](long long n, unsigned long long pos) {
-        const double step = ldexp(2.0 * E[n / frameN], -m);
+        const double step = ((E[n / frameN]) * pow2i(1 - m));
         codes[pos] = static_cast<int>(llround(S[n] / step));
     });
 }
@@ -1124,7 +1124,7 @@ __global__ void __launch_bounds__(1024) k_codes_freq_frames(const unsigned* __re
     codes_from_bits(keep_words, nwords, block_offsets, [&](long long h, unsigned long long pos) {
         const long long off = g.offset_of(h);
         const double2 v = F[off];
-        const double st = ldexp(2.0 * D[(off / g.P) / n1], -m);
+        const double st = ((D[(off / g.P) / n1]) * pow2i(1 - m));
         reinterpret_cast<int2*>(codes)[pos] = make_int2(static_cast<int>(llround(v.x / st)),
                                                         static_cast<int>(llround(v.y / st)));
     });

@@ -10,6 +10,11 @@
 namespace ffcz_gpu {
 
 constexpr double kMaxIndex = 2147483520.0;  // pipeline.cpp:57 (overflow escapes)
+// 2^e as a double (|e| < 1022) by its bit pattern: x * pow2i(e) == ldexp(x, e) bit for bit
+// (both are the correctly rounded x 2^e), without ldexp's range-check sequence
+__device__ __forceinline__ double pow2i(int e) {
+    return __longlong_as_double(static_cast<long long>(1023 + e) << 52);
+}
 
 // ---- bounds ------------------------------------------------------------------------------------
 
