@@ -78,7 +78,10 @@ def test_metrics_edge_cases(ffcz):
         ffcz.metrics(np.zeros(8), np.zeros(9))
 
 
-@pytest.mark.parametrize("shape", SHAPES + [(8, 8, 8)], ids=[str(s) for s in SHAPES + [(8, 8, 8)]])
+PS_SHAPES = SHAPES + [(8, 8, 8), (8192,)]  # (8192,): 4097 shells, past the shared-memory bins
+
+
+@pytest.mark.parametrize("shape", PS_SHAPES, ids=[str(s) for s in PS_SHAPES])
 def test_power_spectrum_vs_oracle(ffcz, shape):
     x = cases.noise(shape, 31) + 2.0
     ps = ffcz.power_spectrum(x)
