@@ -1954,12 +1954,27 @@ int ffcz_cuda_correct_batch(ffcz_cuda_ctx* ctx, const ffcz_field_desc* frame, ui
             fused = !bounds[i].spatial_per_point && !bounds[i].freq_per_component;
         try {
             if (fused) {
+                // kernel launches of the shared loop and gate (context + lanes), spread over the
+                // frames' results so that their sum is the batch's total
+                auto all_launches = [&] {
+                    unsigned long long t = ctx->launches;
+                    for (auto* l : ctx->lanes) t += l->launches;
+                    return t;
+                };
+                const unsigned long long L0 = all_launches();
                 if (frame->dtype == FFCZ_F32)
                     correct_frames_fused<float>(*ctx, *frame, nframes, original, decompressed,
                                                 bounds, m, max_iters, opt, nl, out);
                 else
                     correct_frames_fused<double>(*ctx, *frame, nframes, original, decompressed,
                                                  bounds, m, max_iters, opt, nl, out);
+                unsigned long long tot = all_launches() - L0, given = 0;
+                for (uint64_t i = 0; i < nframes; ++i) given += out[i].kernel_launches;
+                if (tot > given) {
+                    const unsigned long long extra = tot - given;
+                    for (uint64_t i = 0; i < nframes; ++i)
+                        out[i].kernel_launches += extra / nframes + (i < extra % nframes ? 1 : 0);
+                }
                 return;
             }
             run_on_lanes(ctx, nl, nframes, [&](ffcz_cuda_ctx& l, uint64_t i) {
