@@ -21,6 +21,7 @@
 #include "ffcz/bounds.hpp"
 #include "ffcz/errors.hpp"
 #include "ffcz/field.hpp"
+#include "ffcz/metrics.hpp"
 #include "ffcz/pipeline.hpp"
 #include "ffcz/projection.hpp"
 #include "ffcz_cuda.h"
@@ -36,6 +37,7 @@ inline void check(int status) {
         case FFCZ_SYMMETRY_ERROR: throw ffcz::symmetry_error(msg);
         case FFCZ_FORMAT_ERROR: throw ffcz::format_error(msg);
         case FFCZ_IO_ERROR: throw ffcz::io_error(msg);
+        case FFCZ_UNDEFINED_METRIC: throw ffcz::undefined_metric_error(msg);
         default: throw ffcz::error("ffcz_cuda: " + msg);
     }
 }
@@ -166,6 +168,60 @@ inline ScalarField inverse_dft(const ComplexSpectrum& spectrum,
                                                                 : FFCZ_PRECISION_F64,
                                 f.values.data()));
     return f;
+}
+
+// ffcz::spectrum_bound_to_freq_bounds(ffcz::forward_dft(original), rho) (metrics.cpp:107-128) on
+// the GPU.  Takes the ORIGINAL field (the device transforms it), as the CLI's --rho path does
+// (proj/tools/ffcz.cpp:97-102).
+inline FrequencyBounds spectrum_bound_to_freq_bounds(const ScalarField& original, double rho,
+                                                     int device = 0) {
+    validate_dims(original.dims);
+    const ffcz_field_desc fd = describe(original.dims, Precision::f64);
+    std::vector<double> d(original.size());
+    check(ffcz_cuda_spectrum_bound(context(device), &fd, original.values.data(), 0, rho,
+                                   d.data()));
+    std::vector<double> im = d;
+    return DualBounds::frequency_per_component(original.dims, std::move(d), std::move(im));
+}
+
+// ffcz::power_spectrum (metrics.cpp:11-62) on the GPU.
+inline PowerSpectrum power_spectrum(const ScalarField& field, int device = 0) {
+    validate_dims(field.dims);
+    const ffcz_field_desc fd = describe(field.dims, Precision::f64);
+    uint64_t nb = 0;
+    check(ffcz_cuda_power_spectrum(context(device), &fd, field.values.data(), 0, 0, nullptr,
+                                   nullptr, &nb, nullptr, nullptr));
+    PowerSpectrum ps;
+    ps.power.assign(nb, 0.0);
+    std::vector<uint64_t> counts(nb, 0);
+    int fb = 0;
+    check(ffcz_cuda_power_spectrum(context(device), &fd, field.values.data(), 0, nb,
+                                   ps.power.data(), counts.data(), &nb, &ps.mean, &fb));
+    ps.mean_fallback = fb != 0;
+    ps.k_bins.resize(nb);
+    ps.counts.resize(nb);
+    for (uint64_t b = 0; b < nb; ++b) {
+        ps.k_bins[b] = b;
+        ps.counts[b] = static_cast<std::size_t>(counts[b]);
+    }
+    return ps;
+}
+
+// The `ffcz metrics` quantities (proj/tools/ffcz.cpp:246-256) in one device pass set:
+// psnr(original, reconstructed), ssnr(FFT(original), FFT(reconstructed)), max over
+// rfe(FFT(reconstructed - original), FFT(original)), max |reconstructed - original|.
+struct Metrics {
+    double psnr_db, ssnr_db, max_rfe, max_spatial;
+};
+inline Metrics metrics(const ScalarField& original, const ScalarField& reconstructed,
+                       int device = 0) {
+    if (original.dims != reconstructed.dims) throw validation_error("metrics: dims mismatch");
+    validate_dims(original.dims);
+    const ffcz_field_desc fd = describe(original.dims, Precision::f64);
+    ffcz_cuda_metrics_out m{};
+    check(ffcz_cuda_metrics(context(device), &fd, original.values.data(),
+                            reconstructed.values.data(), 0, &m));
+    return Metrics{m.psnr_db, m.ssnr_db, m.max_rfe, m.max_spatial};
 }
 
 } // namespace ffcz::cuda

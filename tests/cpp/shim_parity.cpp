@@ -11,6 +11,7 @@
 
 #include "ffcz/archive.hpp"
 #include "ffcz/baseline.hpp"
+#include "ffcz/metrics.hpp"
 #include "ffcz/pipeline.hpp"
 #include "ffcz/projection.hpp"
 #include "ffcz/transform.hpp"
@@ -125,6 +126,54 @@ int main() {
         }
         if (!vthrew) ++failures;
         std::printf("{\"case\": \"validation_error\", \"ok\": %s}\n", vthrew ? "true" : "false");
+    }
+    {
+        // device metrics through the shim against the reference's own metrics.cpp
+        ScalarField o = noise({24, 20, 18}, 91, Precision::f64);
+        for (double& v : o.values) v += 2.0;
+        ScalarField r = o;
+        std::mt19937_64 rng(92);
+        std::uniform_real_distribution<double> u(-1e-3, 1e-3);
+        for (double& v : r.values) v += u(rng);
+        const ComplexSpectrum X = forward_dft(o), Y = forward_dft(r);
+        FrequencyBounds fr = spectrum_bound_to_freq_bounds(X, 1e-3);
+        FrequencyBounds fg = ffcz::cuda::spectrum_bound_to_freq_bounds(o, 1e-3);
+        double dmax = 0, bmax = 0;
+        for (std::size_t k = 0; k < fr.re.size(); ++k) {
+            dmax = std::max(dmax, std::abs(fr.re[k] - fg.re[k]));
+            bmax = std::max(bmax, fr.re[k]);
+        }
+        PowerSpectrum pr = power_spectrum(o), pg = ffcz::cuda::power_spectrum(o);
+        double pmax = 0, perr = 0;
+        for (std::size_t b = 0; b < pr.power.size(); ++b) pmax = std::max(pmax, pr.power[b]);
+        bool counts_equal = pr.counts == pg.counts && pr.mean_fallback == pg.mean_fallback;
+        for (std::size_t b = 0; b < pr.power.size() && b < pg.power.size(); ++b)
+            perr = std::max(perr, std::abs(pr.power[b] - pg.power[b]));
+        ffcz::cuda::Metrics mg = ffcz::cuda::metrics(o, r);
+        const double p_ref = psnr(o, r), s_ref = ssnr(X, Y);
+        ScalarField eps = compute_error(o, r);
+        double rfe_ref = 0;
+        for (double v : rfe(forward_dft(eps), X)) rfe_ref = std::max(rfe_ref, v);
+        const bool ok = dmax <= 1e-12 * bmax && counts_equal && perr <= 1e-12 * pmax &&
+                        std::abs(mg.psnr_db - p_ref) <= 1e-10 * std::abs(p_ref) &&
+                        std::abs(mg.ssnr_db - s_ref) <= 1e-9 * std::abs(s_ref) &&
+                        std::abs(mg.max_rfe - rfe_ref) <= 1e-9 * rfe_ref;
+        if (!ok) ++failures;
+        std::printf("{\"case\": \"metrics\", \"ok\": %s, \"delta_maxdiff_rel\": %.3g, "
+                    "\"counts_equal\": %s, \"power_maxdiff_rel\": %.3g, \"psnr\": [%.12g, %.12g], "
+                    "\"ssnr\": [%.12g, %.12g], \"max_rfe\": [%.12g, %.12g]}\n",
+                    ok ? "true" : "false", dmax / bmax, counts_equal ? "true" : "false",
+                    perr / pmax, p_ref, mg.psnr_db, s_ref, mg.ssnr_db, rfe_ref, mg.max_rfe);
+        bool uthrew = false;
+        try {
+            ffcz::cuda::metrics(ScalarField::create({2}, {3.0, 3.0}),
+                                ScalarField::create({2}, {3.0, 3.5}));
+        } catch (const undefined_metric_error&) {
+            uthrew = true;
+        }
+        if (!uthrew) ++failures;
+        std::printf("{\"case\": \"undefined_metric_error\", \"ok\": %s}\n",
+                    uthrew ? "true" : "false");
     }
     std::printf("{\"failures\": %d}\n", failures);
     return failures;
