@@ -199,7 +199,9 @@ typedef enum ffcz_cuda_slab_opcode {
                                      project_onto_scube vs e*fscale -> p1 eps, S p2 */
     FFCZ_SLAB_INV_REPAIR_VERIFY = 9, /* p0 half (clobbered) -> p1 eps_tilde; p2 orig, p3 dec,
                                      p4 spat_cur (repaired in place), p5 final eps, p6 escape
-                                     bitmap, p7 corrected, p8 eps_v -> out: dirty, spatial excess */
+                                     bitmap, p7 corrected, p8 eps_v -> out: dirty, spatial excess;
+                                     p8 NULL: decoder-view repair (p1 receives the decoder view
+                                     and the repair checks it) */
     FFCZ_SLAB_INV_VERIFY = 10,    /* p0 half -> p1 eps_v; p2 orig, p3 dec, p4 spat_cur,
                                      p5 corrected -> out: spatial excess */
     FFCZ_SLAB_RESIDUAL_S = 11,    /* p0 eps -> out: max(|eps| - e*fscale, 0) */

@@ -2205,10 +2205,12 @@ int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4
                 using TI = decltype(tag);
                 const TI* o = static_cast<const TI*>(P(2));
                 const TI* d = static_cast<const TI*>(P(3));
-                if (op->op == FFCZ_SLAB_INV_REPAIR_VERIFY)
+                if (op->op == FFCZ_SLAB_INV_REPAIR_VERIFY) {
+                    HookRepairVerifyS<TI> hk{o, d, dd(4), dd(5), sb, ww(6), dd(7), dd(8), c.ctl};
+                    hk.dview = P(8) == nullptr;  // no eps_v buffer: decoder-view repair
                     launch_row_c2r_hook<double>(g.n2, d2(0), g.P, dd(1), g.n2, g.rows, invN, c.tw64,
-                        nullptr, HookRepairVerifyS<TI>{o, d, dd(4), dd(5), sb, ww(6), dd(7), dd(8),
-                                                       c.ctl}, st);
+                                                nullptr, hk, st);
+                }
                 else
                     launch_row_c2r_hook<double>(g.n2, d2(0), g.P, dd(1), g.n2, g.rows, invN, c.tw64,
                         nullptr, HookVerifyS<TI>{o, d, dd(4), dd(5), sb, c.ctl}, st);

@@ -26,6 +26,8 @@ single-volume path's.
 """
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -265,12 +267,16 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E: float, Delta: float, m: in
         Bw = _transpose_ab(be, comm, Aw, n0, c0, c1)
         return Bw
 
+    # decoder-view repair: the round checks the decoder's own view, so a clean
+    # round is verify_bounds; FFCZ_REPAIR_ORDER=reference keeps the reference's eps_tilde order
+    dview = os.environ.get("FFCZ_REPAIR_ORDER") != "reference"
     if converged:
         for _ in range(MAX_ESCAPE_ROUNDS):                   # pipeline.cpp:116
             rounds += 1
             Aw = inverse_to_spatial(freq_cur_B)
             dirty_s, vs_r = be.inv_local_repair_verify(Aw, eps_t, N, orig, dec, spat_cur, eps, E,
-                                                       esc_s, corrected, eps_v)
+                                                       esc_s, corrected,
+                                                       None if dview else eps_v)
             Bt = forward_to_b(eps_t)
             viol = be.col0_mark(Bt, Delta)                  # FFT axis 0, |delta~| > Delta
             pos = be.positions(viol)                        # B storage offsets, ascending
@@ -280,8 +286,11 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E: float, Delta: float, m: in
             dirty = comm.sum_i64([int(dirty_s) + int(pos.numel() > 0)], dev)[0]
             if dirty == 0:                                  # :161, clean round
                 vs = comm.max_f64([vs_r], dev)[0]
-                Bv = forward_to_b(eps_v)
-                vf = comm.max_f64([be.col0_verify(Bv, Delta)], dev)[0]
+                if dview:
+                    vf = 0.0    # the round's own forward transform was of the decoder view
+                else:
+                    Bv = forward_to_b(eps_v)
+                    vf = comm.max_f64([be.col0_verify(Bv, Delta)], dev)[0]
                 verified = True
                 break
     if not verified:

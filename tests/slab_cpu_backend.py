@@ -138,9 +138,10 @@ class CpuSlabBackend:
         c = (d + sc) + x
         v = c - o
         corrected.copy_(c)
-        eps_v.copy_(v)
+        if eps_v is not None:
+            eps_v.copy_(v)
         vs = max(float((v.abs() - E).max()), 0.0)
-        t = (e0 + sc) + x
+        t = v if eps_v is None else (e0 + sc) + x  # eps_v None: decoder-view repair
         bad = t.abs() > E
         spat_cur.copy_(torch.where(bad, sc + (final_eps - t), sc))
         esc_s |= bad
