@@ -7,6 +7,7 @@
 #include <zlib.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <cstring>
 #include <queue>
 #include <stdexcept>
@@ -140,7 +141,34 @@ void encode_block(std::vector<std::uint8_t>& out, const std::uint32_t* data, std
 
 } // namespace
 
+#if defined(__x86_64__)
+// SSE4.2 `crc32` computes exactly CRC-32C (Castagnoli, reflected 0x82F63B78): 8 bytes per
+// instruction instead of one table lookup per byte (the 2 GB per-component Delta header of a
+// 512^3 config-2 archive: ~0.3 s instead of ~4 s).
+__attribute__((target("sse4.2"))) static std::uint32_t crc32c_sse42(const std::uint8_t* p,
+                                                                    std::size_t n) {
+    std::uint64_t c = 0xFFFFFFFFu;
+    while (n && (reinterpret_cast<std::uintptr_t>(p) & 7u)) {
+        c = __builtin_ia32_crc32qi(static_cast<std::uint32_t>(c), *p++);
+        --n;
+    }
+    while (n >= 8) {
+        std::uint64_t v;
+        std::memcpy(&v, p, 8);
+        c = __builtin_ia32_crc32di(c, v);
+        p += 8;
+        n -= 8;
+    }
+    while (n--) c = __builtin_ia32_crc32qi(static_cast<std::uint32_t>(c), *p++);
+    return static_cast<std::uint32_t>(c) ^ 0xFFFFFFFFu;
+}
+#endif
+
 std::uint32_t crc32c(const std::uint8_t* data, std::size_t len) {
+#if defined(__x86_64__)
+    static const bool hw = __builtin_cpu_supports("sse4.2");
+    if (hw) return crc32c_sse42(data, len);
+#endif
     static std::uint32_t table[256];
     static bool init = [] {
         for (std::uint32_t i = 0; i < 256; ++i) {
