@@ -242,10 +242,9 @@ std::vector<std::uint8_t> write_archive(const ArchiveInput& in) {
     if (in.freq_per_component) tags |= 2u;
     if (in.converged) tags |= 4u;
     put<std::uint8_t>(w, tags);
-    auto put_doubles = [&](const double* v, std::uint64_t n) {
-        const std::size_t off = w.size();
-        w.resize(off + n * sizeof(double));
-        std::memcpy(w.data() + off, v, n * sizeof(double));
+    auto put_doubles = [&](const double* v, std::uint64_t n) {  // one copy, no zero-fill
+        const auto* b = reinterpret_cast<const std::uint8_t*>(v);
+        w.insert(w.end(), b, b + n * sizeof(double));
     };
     if (in.spatial_per_point) put_doubles(in.spatial_values, N);
     else put<double>(w, in.spatial_global);
