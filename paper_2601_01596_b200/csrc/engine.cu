@@ -1603,7 +1603,11 @@ void correct_frames_fused(ffcz_cuda_ctx& c, const ffcz_field_desc& fd, uint64_t 
     // (the batched gate runs in the main thread: one buffer set, its own stack buffers)
     const bool batched_gate = frames_batched_gate_enabled();
     const double per_frame_all = per_frame + (batched_gate ? 36.0 * Nf + 32.0 * Hf + 12.0 * Nf : 0.0);
-    const double budget = batched_gate ? 60e9 : 24e9;
+    static const double budget_env = [] {  // FFCZ_FRAMES_BUDGET_GB: group-size sweeps
+        const char* e = std::getenv("FFCZ_FRAMES_BUDGET_GB");
+        return e ? std::atof(e) * 1e9 : 0.0;
+    }();
+    const double budget = budget_env > 0 ? budget_env : (batched_gate ? 60e9 : 24e9);
     uint64_t G = std::max<uint64_t>(1, std::min<uint64_t>(
         nframes, static_cast<uint64_t>(budget / per_frame_all)));
     if (!batched_gate && nframes >= 64 && G >= nframes) G = (nframes + 1) / 2;  // overlap
