@@ -50,3 +50,19 @@ def test_create_fails_loudly_without_gpu():
     lib = capi.load()
     h = ctypes.c_void_p()
     assert lib.ffcz_cuda_create(ctypes.byref(h), 0, None) != 0
+
+
+def test_metrics_struct_layout():
+    assert ctypes.sizeof(capi.MetricsOut) == 32
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    # no CPU fallback: without the shared object the package refuses to run
+    import subprocess
+    import sys
+    env = dict(os.environ, FFCZ_CUDA_LIB=str(tmp_path / "absent.so"))
+    code = "from paper_2601_01596_b200 import _capi; _capi.load()"
+    p = subprocess.run([sys.executable, "-c", code], env=env, cwd=ROOT, capture_output=True,
+                       text=True, timeout=300)
+    assert p.returncode != 0
+    assert "absent.so" in p.stderr
