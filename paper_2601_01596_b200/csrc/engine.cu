@@ -222,6 +222,15 @@ bool gate_codes_one_pass() {
     return on;
 }
 
+// Gate rounds: C2R -> repair -> R2C as one fused row pass (FFCZ_GATE_ROW_FUSED=1, A/B).
+bool gate_row_fused() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_GATE_ROW_FUSED");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 // Escape repair on the decoder view (HookRepairVerifyS::dview; default on).  FFCZ_REPAIR_ORDER=
 // reference restores the reference's eps_tilde check plus a separate verify transform.
 bool decoder_view_repair() {
@@ -654,14 +663,27 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
                 Prof p(c, kColPass, pass);
                 plan.col(mid, +1, work, work, nullptr, HookNone{}, st);
             }
-            {
-                Prof p(c, kRowC2R, row_bytes);
-                launch_row_c2r_hook<double>(g.n2, work, g.P, eps_t, g.n2, g.rows, invN, c.tw64,
-                                            nullptr, row_hook, st);
-            }
-            {
-                Prof p(c, kRowR2C, 8.0 * g.N + 16.0 * Nc);
-                launch_row_r2c<double>(g.n2, eps_t, g.n2, work, g.P, g.rows, c.tw64, nullptr, st);
+            bool fused_row = false;
+            if constexpr (std::is_same_v<decltype(row_hook), HookRepairVerifyS<TI>>)
+                fused_row = row_hook.dview && gate_row_fused() && plan.fused_ok();
+            if (fused_row) {
+                // C2R -> repair on the decoder view -> R2C in one row pass: v never leaves the SM
+                Prof p(c, kRowC2R, row_bytes - 8.0 * N + 16.0 * Nc);
+                if constexpr (std::is_same_v<decltype(row_hook), HookRepairVerifyS<TI>>)
+                    launch_row_fused<double>(g.n2, work, g.P, g.rows, g.n2, invN, c.tw64, nullptr,
+                                             row_hook, st);
+                c.launches -= 1;
+            } else {
+                {
+                    Prof p(c, kRowC2R, row_bytes);
+                    launch_row_c2r_hook<double>(g.n2, work, g.P, eps_t, g.n2, g.rows, invN, c.tw64,
+                                                nullptr, row_hook, st);
+                }
+                {
+                    Prof p(c, kRowR2C, 8.0 * g.N + 16.0 * Nc);
+                    launch_row_r2c<double>(g.n2, eps_t, g.n2, work, g.P, g.rows, c.tw64, nullptr,
+                                           st);
+                }
             }
             if (three_d) {
                 Prof p(c, kColPass, pass);
