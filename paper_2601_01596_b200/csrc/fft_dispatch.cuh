@@ -317,7 +317,9 @@ void row_fused_radix(cplx<T>* data, long long stride, long long nrows, long long
                      T scale, Twiddles<T>& tw, const int* gate, Hook hook, cudaStream_t st) {
     constexpr int E = RowCfg<T, M>::E, TT = RowCfg<T, M>::TT;
     const int R = rows_per_cta<T, M>(nrows);
-    const size_t smem = row_smem_bytes<T, M, E>(R);
+    size_t smem = row_smem_bytes<T, M, E>(R);
+    if constexpr (hook_prefetch<Hook>())  // two input fields' rows + the mbarrier
+        if (TT <= 32) smem += 2 * static_cast<size_t>(2 * M) * R * Hook::prefetch_scalar_bytes() + 16;
     auto k = TT <= 32 ? k_row_c2r_r2c_sh<T, M, E, Hook> : k_row_c2r_r2c<T, M, E, Hook>;
     set_smem(k, smem);
     k<<<persistent_grid(k, TT * R, smem, (nrows + R - 1) / R), TT * R, smem, st>>>(

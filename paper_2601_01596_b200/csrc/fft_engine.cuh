@@ -1244,12 +1244,39 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     const int rb = threadIdx.x / TT;
     const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
     HookNone none;
+    // input fields of the hook prefetched per tile by bulk copies (as k_row_c2r_sh)
+    constexpr bool kPf = hook_prefetch<Hook>();
+    const int R = blockDim.x / TT;
+    unsigned char* pf_base = smem_raw + static_cast<size_t>(row_smem_elems<M, E>()) * R * sizeof(cplx<T>);
+    uint64_t* pf_bar = nullptr;
+    size_t pf_bytes_row = 0;
+    if constexpr (kPf) {
+        pf_bytes_row = static_cast<size_t>(2LL * M) * hook.prefetch_scalar_bytes();
+        pf_bar = reinterpret_cast<uint64_t*>(pf_base + 2 * pf_bytes_row * R);
+        if (threadIdx.x == 0) {
+            mbar_init(pf_bar, 1);
+            fence_mbar_init();
+        }
+    }
+    unsigned pf_phase = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         __syncthreads();
         if constexpr (hook_tiled<Hook>()) {
             const long long u = tile * (blockDim.x / TT);
             if (hook.tile_skip(u)) continue;
             hook.tile_begin(u);
+        }
+        if constexpr (kPf) {
+            const long long row0 = tile * R;
+            if (threadIdx.x == 0) {
+                const long long nr = nrows - row0 < R ? nrows - row0 : R;
+                const unsigned bytes = static_cast<unsigned>(pf_bytes_row * nr);
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx(pf_bar, 2 * bytes);
+                bulk_load(pf_base, hook.prefetch_src(0, row0 * real_stride), bytes, pf_bar);
+                bulk_load(pf_base + pf_bytes_row * R, hook.prefetch_src(1, row0 * real_stride),
+                          bytes, pf_bar);
+            }
         }
         const long long row = tile * (blockDim.x / TT) + rb;
         const bool valid = row < nrows;
@@ -1261,6 +1288,11 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
         merge_pairs<T, M, E>(v, mid, t, twp);
         pairs_to_natural<T, M, E>(v, mid, t);
         stockham<T, M, E, 1, +1>(v, t, tw, x);
+        if constexpr (kPf) {
+            mbar_wait(pf_bar, pf_phase);
+            pf_phase ^= 1u;
+            hook.use_prefetch(pf_base, pf_base + pf_bytes_row * R, tile * R * real_stride);
+        }
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const int j = t + TT * m;
