@@ -393,6 +393,10 @@ void launch_col(long long L, int dir, const cplx<T>* src, cplx<T>* dst, long lon
                     return e ? std::atoll(e) : 96LL;
                 }();
                 long long Bm = std::max<long long>(1, static_cast<long long>(kb * 1024 / per));
+                // at least 4 columns (64-B runs for FP64) while they fit: L = 1000 FP64 measured
+                // 0.29 / 0.20 of HBM at 2 columns, 0.31 / 0.28 at 4 (r01_passbench_mixed_1000)
+                Bm = std::max<long long>(
+                    Bm, std::min<long long>(4, static_cast<long long>(detail::kMixedSmemMax / per)));
                 Bm = std::min<long long>({Bm, 16, static_cast<long long>(ncols)});
                 const size_t smem = per * Bm;
                 const long long ntiles = nplanes * ((ncols + Bm - 1) / Bm);
