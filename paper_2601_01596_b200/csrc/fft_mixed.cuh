@@ -26,7 +26,7 @@ struct MixedPlan {
     unsigned mul[kMixedMaxStages] = {};
 };
 
-// Factor L: radix 4 first (fewest stages), then 2, 3, 5, 7, then the remaining primes ascending.
+// Factor L: radix 8 then 4 first (fewest stages), then 2, 3, 5, 7, then the remaining primes.
 inline MixedPlan make_mixed_plan(long long L) {
     MixedPlan p;
     p.L = static_cast<int>(L);
@@ -37,6 +37,7 @@ inline MixedPlan make_mixed_plan(long long L) {
             rem /= r;
         }
     };
+    take(8);
     take(4);
     take(2);
     take(3);
@@ -63,6 +64,22 @@ __device__ __forceinline__ void bfly(cplx<T>* a) {
         const cplx<T> s = cadd(a[0], a[1]), d = csub(a[0], a[1]);
         a[0] = s;
         a[1] = d;
+    } else if constexpr (R == 8) {
+        // two radix-4 DFTs of the even / odd samples, merged with W8^k = exp(-i pi k / 4)
+        cplx<T> e[4] = {a[0], a[2], a[4], a[6]}, o[4] = {a[1], a[3], a[5], a[7]};
+        bfly<T, 4>(e);
+        bfly<T, 4>(o);
+        const T c = T(0.70710678118654752440);
+        cplx<T> w[4];
+        w[0] = o[0];
+        w[1] = mkc<T>(c * (o[1].x + o[1].y), c * (o[1].y - o[1].x));   // o (1 - i) / sqrt2
+        w[2] = mkc<T>(o[2].y, -o[2].x);                                  // o (-i)
+        w[3] = mkc<T>(c * (o[3].y - o[3].x), -c * (o[3].x + o[3].y));  // o (-1 - i) / sqrt2
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            a[k] = cadd(e[k], w[k]);
+            a[k + 4] = csub(e[k], w[k]);
+        }
     } else if constexpr (R == 4) {
         const cplx<T> s02 = cadd(a[0], a[2]), d02 = csub(a[0], a[2]);
         const cplx<T> s13 = cadd(a[1], a[3]), d13 = cmulmi(csub(a[1], a[3]));  // -i (a1 - a3)
@@ -88,7 +105,7 @@ __device__ __forceinline__ void bfly(cplx<T>* a) {
 #pragma unroll
             for (int k = 0; k < 5; ++k) cs[k] = c[k], sn[k] = s[k];
         } else {
-            static_assert(R == 7, "register butterflies exist for radix 2, 3, 4, 5, 7");
+            static_assert(R == 7, "register butterflies exist for radix 2, 3, 4, 5, 7, 8");
             const double c[7] = {1.0,
                                  0.62348980185873353053,
                                  -0.22252093395631440429,
@@ -218,6 +235,7 @@ __device__ cplx<T>* run_stages(cplx<T>* A, cplx<T>* B, const MixedPlan& p, int s
                 case 2: stage_reg<T, 2>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
                 case 3: stage_reg<T, 3>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
                 case 4: stage_reg<T, 4>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
+                case 8: stage_reg<T, 8>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
                 case 5: stage_reg<T, 5>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
                 case 7: stage_reg<T, 7>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
                 default: stage_gen<T>(A, B, p.L, r, ns, mul, si, sl, tl, wl, wmul, cin); break;
