@@ -92,6 +92,20 @@ typedef enum ffcz_cuda_policy { FFCZ_POLICY_FP64 = 0, FFCZ_POLICY_MIXED = 1 } ff
 #define FFCZ_FORCE_UNFUSED (1u << 4)    /* use the per-op (unfused) loop even for 2^k shapes    */
 #define FFCZ_DEVICE_ENCODE (1u << 5)    /* archive: zigzag + canonical Huffman on the device (same
                                            payload bytes as huffman.cpp); zlib_level 0 = stored  */
+#define FFCZ_BOUNDS_VALIDATED (1u << 6) /* the caller guarantees DualBounds' invariants (every
+                                           per-point / per-component entry > 0 and finite, Re/Im
+                                           lanes Hermitian-consistent: bounds.cpp:10-59), e.g.
+                                           the C++ shim, whose ffcz::DualBounds was built by the
+                                           reference's factories; otherwise they are checked
+                                           (FFCZ_VALIDATION_ERROR with the reference's message) */
+#define FFCZ_REPAIR_REFERENCE_ORDER (1u << 7) /* escape repair in the reference's order: check
+                                           eps_tilde = eps0 + S_dq + IFFT(F_dq) each round
+                                           (pipeline.cpp:134-160), then a separate verify_bounds
+                                           transform; default: repair the decoder's own view
+                                            */
+#define FFCZ_F_ACCUMULATE (1u << 8)     /* accumulate F += displacement in every f-clip
+                                           (projection.cpp:117-119); default: mark the clipped
+                                           components and rebuild F once at the gate */
 
 typedef struct ffcz_cuda_options {
     uint32_t flags;

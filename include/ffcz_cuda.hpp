@@ -92,7 +92,7 @@ inline CorrectionResult correct(const ScalarField& original, const ScalarField& 
     const ffcz_bounds_desc bd = describe(bounds_original);
     ffcz_cuda_options opt;
     ffcz_cuda_default_options(&opt);
-    opt.flags = FFCZ_WANT_ARCHIVE;
+    opt.flags = FFCZ_WANT_ARCHIVE | FFCZ_BOUNDS_VALIDATED;  // built by DualBounds' factories
     ffcz_cuda_result r{};
     const int st = ffcz_cuda_correct(context(device), &fd, original.values.data(),
                                      decompressed.values.data(), &bd, m, max_iters, &opt, &r);
@@ -132,8 +132,11 @@ inline ProjectionOutcome alternating_projection(const ScalarField& epsilon0,
     out.edits.frequency.assign(n, {0.0, 0.0});
     out.final_epsilon = ScalarField{epsilon0.dims, std::vector<double>(n), epsilon0.precision};
     ffcz_cuda_report rep{};
+    ffcz_cuda_options opt;
+    ffcz_cuda_default_options(&opt);
+    opt.flags = FFCZ_BOUNDS_VALIDATED;  // built by DualBounds' factories (and shrink_bounds)
     check(ffcz_cuda_alternating_projection(
-        context(device), &fd, epsilon0.values.data(), &bd, max_iters, precondition_slack, nullptr,
+        context(device), &fd, epsilon0.values.data(), &bd, max_iters, precondition_slack, &opt,
         out.edits.spatial.data(), reinterpret_cast<double*>(out.edits.frequency.data()),
         out.final_epsilon.values.data(), &rep));
     out.report.iterations = rep.iterations;

@@ -456,12 +456,19 @@ class Archive:
 
 def write_archive(a: Archive, level: int = 9) -> bytes:
     """src/archive.cpp:73-135."""
-    def streams(flags, codes):
-        return (outer_compress(pack_flags(flags), level),
-                outer_compress(huffman_encode(zigzag(codes)), level))
+    return write_archive_raw_flags(a, pack_flags(a.spatial_flags), pack_flags(a.frequency_flags),
+                                   level)
 
-    sf, si = streams(a.spatial_flags, a.spatial_codes)
-    ff, fi = streams(a.frequency_flags, a.frequency_codes)
+
+def write_archive_raw_flags(a: Archive, sflag_bytes: bytes, fflag_bytes: bytes,
+                            level: int = 9) -> bytes:
+    """write_archive with the flag streams given as raw bytes (test hook for malformed or
+    padding-bit archives); the header counts stay the flags' own counts (a.spatial_flags /
+    a.frequency_flags)."""
+    sf = outer_compress(bytes(sflag_bytes), level)
+    si = outer_compress(huffman_encode(zigzag(a.spatial_codes)), level)
+    ff = outer_compress(bytes(fflag_bytes), level)
+    fi = outer_compress(huffman_encode(zigzag(a.frequency_codes)), level)
     w = bytearray(b"FFCZ") + struct.pack("<HB", 1, len(a.dims))
     for d in a.dims:
         w += struct.pack("<Q", d)

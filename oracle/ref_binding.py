@@ -11,7 +11,21 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_ref", "libffcz_ref.so")
+# FFT provider behind the reference's fftw_* calls (oracle/Makefile): "mkl" = MKL DFTI
+# (shim/fftw_mkl.cpp, FFTW-class speed; the default when built), "radix2" = the dependency-free
+# stand-in (shim/fftw_shim.cpp).  FFCZ_REF_FFT selects; the choice is reported by fft_backend().
+_LIBS = {"radix2": os.path.join(HERE, "_ref", "libffcz_ref.so"),
+         "mkl": os.path.join(HERE, "_ref", "libffcz_ref_mkl.so")}
+
+
+def fft_backend() -> str:
+    want = os.environ.get("FFCZ_REF_FFT", "")
+    if want in _LIBS:
+        return want
+    return "mkl" if os.path.exists(_LIBS["mkl"]) else "radix2"
+
+
+LIB_PATH = _LIBS[fft_backend()]
 
 _ERRS = {1: "ValidationError", 2: "SymmetryError", 3: "FormatError", 4: "IoError", 5: "Error",
          6: "Exception"}
@@ -182,3 +196,43 @@ def rho_bounds(original, rho):
     _check(lib().ffcz_ref_rho_bounds(C.c_int(o.ndim), _dims(o.shape), _dp(o.ravel()),
                                      C.c_double(rho), _dp(out)))
     return out
+
+
+class _ArchiveEdits(C.Structure):
+    _fields_ = [("spatial_flags", C.POINTER(C.c_uint8)), ("spatial_flag_bytes", C.c_uint64),
+                ("frequency_flags", C.POINTER(C.c_uint8)), ("frequency_flag_bytes", C.c_uint64),
+                ("spatial_codes", C.POINTER(C.c_int32)), ("n_spatial", C.c_uint64),
+                ("frequency_codes", C.POINTER(C.c_int32)), ("n_frequency", C.c_uint64),
+                ("escape_index", C.POINTER(C.c_uint64)), ("escape_freq", C.POINTER(C.c_int32)),
+                ("n_escapes", C.c_uint64), ("converged", C.c_int32)]
+
+
+@dataclass
+class RefEdits:
+    spatial_flags: np.ndarray     # packed LSB-first bytes, as the archive carries them
+    frequency_flags: np.ndarray
+    spatial_codes: np.ndarray     # int32
+    frequency_codes: np.ndarray   # int32, interleaved Re, Im
+    escape_index: np.ndarray      # uint64, the reference's std::map order
+    escape_frequency: np.ndarray  # int32 (1 = frequency entry)
+    converged: bool
+
+
+def archive_edits(data: bytes) -> RefEdits:
+    """The reference's read_archive (archive.cpp:137-225) of `data` as flag bytes / int32 codes /
+    escape indices (codes re-quantised exactly from the dequantised values)."""
+    buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data if data else b"\0")
+    out = _ArchiveEdits()
+    _check(lib().ffcz_ref_archive_edits(buf, C.c_uint64(len(data)), C.byref(out)))
+
+    def take(p, n, dt):
+        a = np.ctypeslib.as_array(p, shape=(max(1, n),))[:n].astype(dt, copy=True)
+        lib().ffcz_ref_free(C.cast(p, C.c_void_p))
+        return a
+
+    return RefEdits(take(out.spatial_flags, out.spatial_flag_bytes, np.uint8),
+                    take(out.frequency_flags, out.frequency_flag_bytes, np.uint8),
+                    take(out.spatial_codes, out.n_spatial, np.int32),
+                    take(out.frequency_codes, 2 * out.n_frequency, np.int32),
+                    take(out.escape_index, out.n_escapes, np.uint64),
+                    take(out.escape_freq, out.n_escapes, np.int32), bool(out.converged))

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "ffcz/archive.hpp"
+#include "ffcz/editset.hpp"
 #include "ffcz/metrics.hpp"
 #include "ffcz/pipeline.hpp"
 #include "ffcz/projection.hpp"
@@ -82,6 +83,13 @@ DualBounds make_bounds(int ndim, const std::uint64_t* dims, int spatial_per_poin
                                                             std::vector<double>(d_im, d_im + n))
                       : DualBounds::frequency_global(d_global);
     return b;
+}
+
+template <typename T>
+T* dup_vec(const std::vector<T>& v) {
+    T* p = static_cast<T*>(std::malloc(v.size() * sizeof(T) + 8));
+    if (!v.empty()) std::memcpy(p, v.data(), v.size() * sizeof(T));
+    return p;
 }
 
 } // namespace
@@ -242,6 +250,46 @@ int ffcz_ref_rho_bounds(int ndim, const std::uint64_t* dims, const double* origi
         ScalarField f = make_field(ndim, dims, original, 1);
         FrequencyBounds fb = spectrum_bound_to_freq_bounds(forward_dft(f), rho);
         std::memcpy(delta_out, fb.re.data(), fb.re.size() * sizeof(double));
+    });
+}
+
+// read_archive (proj/core/src/archive.cpp:137-225) -> the edit set as the archive carries it:
+// flag bytes (LSB-first), int32 codes (re-quantised from the dequantised values with the
+// reference's own quantize_edits, editset.cpp:86-119 — exact, value = code * step), escapes.
+// Buffers malloc'd; free each with ffcz_ref_free.  Used to pin flags / codes of large goldens
+// by digest (tests/golden/make_golden.py) without a Python Huffman decoder.
+struct ref_archive_edits {
+    std::uint8_t* spatial_flags;   std::uint64_t spatial_flag_bytes;
+    std::uint8_t* frequency_flags; std::uint64_t frequency_flag_bytes;
+    std::int32_t* spatial_codes;   std::uint64_t n_spatial;
+    std::int32_t* frequency_codes; std::uint64_t n_frequency;   // 2 lanes per entry
+    std::uint64_t* escape_index;   std::int32_t* escape_freq;   std::uint64_t n_escapes;
+    std::int32_t converged;
+};
+
+int ffcz_ref_archive_edits(const std::uint8_t* bytes, std::uint64_t len, ref_archive_edits* out) {
+    return guarded([&] {
+        DecodedArchive a = read_archive(std::vector<std::uint8_t>(bytes, bytes + len));
+        out->spatial_flags = dup_vec(a.edits.spatial_flags.bytes());
+        out->spatial_flag_bytes = a.edits.spatial_flags.bytes().size();
+        out->frequency_flags = dup_vec(a.edits.frequency_flags.bytes());
+        out->frequency_flag_bytes = a.edits.frequency_flags.bytes().size();
+        auto si = flagged_indices(a.edits.spatial_flags);
+        auto fi = flagged_indices(a.edits.frequency_flags);
+        out->spatial_codes = dup_vec(quantize_edits(a.edits.spatial_values, si, a.params));
+        out->n_spatial = si.size();
+        out->frequency_codes = dup_vec(quantize_edits(a.dims, a.edits.frequency_values, fi, a.params));
+        out->n_frequency = fi.size();
+        std::vector<std::uint64_t> ei;
+        std::vector<std::int32_t> ef;
+        for (const auto& e : a.escapes) {
+            ei.push_back(e.index);
+            ef.push_back(e.frequency ? 1 : 0);
+        }
+        out->escape_index = dup_vec(ei);
+        out->escape_freq = dup_vec(ef);
+        out->n_escapes = ei.size();
+        out->converged = a.converged;
     });
 }
 

@@ -32,6 +32,9 @@ FFCZ_WANT_EDITS = 1 << 2
 FFCZ_WANT_CORRECTED = 1 << 3
 FFCZ_DEVICE_ENCODE = 1 << 5
 FFCZ_FORCE_UNFUSED = 1 << 4
+FFCZ_BOUNDS_VALIDATED = 1 << 6
+FFCZ_REPAIR_REFERENCE_ORDER = 1 << 7
+FFCZ_F_ACCUMULATE = 1 << 8
 
 # every symbol include/ffcz_cuda.h declares
 EXPORTS = [

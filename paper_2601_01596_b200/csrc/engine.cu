@@ -7,6 +7,7 @@
 // The projection loop is enqueued speculatively in chunks; every loop kernel returns at once
 // after the on-device decision kernel has set ctl->done, so the host never syncs per iteration.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -104,6 +105,7 @@ struct ffcz_cuda_ctx {
         double bytes;
     };
     bool prof_on = false;
+    uint32_t call_flags = 0;  // ffcz_cuda_options.flags of the call in progress (per-call switches)
     std::vector<ProfRec> prof;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -233,12 +235,13 @@ bool gate_row_fused() {
 
 // Escape repair on the decoder view (HookRepairVerifyS::dview; default on).  FFCZ_REPAIR_ORDER=
 // reference restores the reference's eps_tilde check plus a separate verify transform.
-bool decoder_view_repair() {
+// Per call: FFCZ_REPAIR_REFERENCE_ORDER in ffcz_cuda_options.flags selects the reference order.
+bool decoder_view_repair(const ffcz_cuda_ctx& c) {
     static const bool on = [] {
         const char* e = std::getenv("FFCZ_REPAIR_ORDER");
         return !(e && std::strcmp(e, "reference") == 0);
     }();
-    return on;
+    return on && !(c.call_flags & FFCZ_REPAIR_REFERENCE_ORDER);
 }
 
 bool eps0_fusion_enabled() {
@@ -251,11 +254,13 @@ bool eps0_fusion_enabled() {
 
 // FFCZ_F_REBUILD=0: accumulate F in every clip pass (read-modify-write) instead of marking the
 // moved components and rebuilding F once at the gate (HookFClip::moved, HookFRebuild).
-inline bool f_rebuild_enabled() {
+// Per call: FFCZ_F_ACCUMULATE in ffcz_cuda_options.flags selects the accumulation.
+inline bool f_rebuild_enabled(const ffcz_cuda_ctx& c) {
     static const bool on = [] {
         const char* e = std::getenv("FFCZ_F_REBUILD");
         return !(e && e[0] == '0');
     }();
+    if (c.call_flags & FFCZ_F_ACCUMULATE) return false;
     return on;
 }
 
@@ -272,8 +277,95 @@ struct Bounds {
     FreqB fb{nullptr, nullptr, 0.0};
 };
 
+// DualBounds' invariants (bounds.cpp:10-18,43-59): every per-point E and per-component Delta
+// entry strictly positive and finite, and the Re / Im lanes Hermitian-consistent
+// (lane[k] == lane[mirror(k)], field.cpp:41-50).  The reference enforces them when a DualBounds
+// is built; a C-ABI caller hands raw arrays, so they are checked here unless the caller sets
+// FFCZ_BOUNDS_VALIDATED (the C++ shim: its ffcz::DualBounds was built by those factories).
+// Device arrays: one pass (bad[0] = first non-positive index, bad[1] = first asymmetric index).
+__global__ void k_check_bounds(const double* __restrict__ e, const double* __restrict__ re,
+                               const double* __restrict__ im, long long d0, long long d1,
+                               long long d2, unsigned long long* bad) {
+    const long long N = d0 * d1 * d2;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        if (e) {
+            const double v = e[i];
+            if (!(v > 0.0) || !isfinite(v)) atomicMin(&bad[0], (unsigned long long)i);
+        }
+        if (re) {
+            const long long i2 = i % d2, t = i / d2, i1 = t % d1, i0 = t / d1;
+            const long long m = (((d0 - i0) % d0) * d1 + (d1 - i1) % d1) * d2 + (d2 - i2) % d2;
+            const double a = re[i], b = im[i];
+            if (!(a > 0.0) || !isfinite(a) || !(b > 0.0) || !isfinite(b))
+                atomicMin(&bad[0], (unsigned long long)(N + i));
+            if (a != re[m] || b != im[m]) atomicMin(&bad[1], (unsigned long long)i);
+        }
+    }
+}
+
+void validate_bounds(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_bounds_desc& bd, bool on_dev) {
+    const bool pp = bd.spatial_per_point, pc = bd.freq_per_component;
+    if (!pp && !pc) return;
+    if (pp && !bd.spatial_values) throw Error(kValidation, "per-point spatial bound array is null");
+    if (pc && (!bd.freq_re || !bd.freq_im))
+        throw Error(kValidation, "per-component frequency bound arrays are null");
+    const long long N = g.N, d0 = g.d[0], d1 = g.d[1], d2 = g.d[2];
+    unsigned long long bad[2] = {~0ull, ~0ull};
+    if (on_dev) {
+        unsigned long long* db = c.b<unsigned long long>("bounds_bad", 2);
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(db, bad, sizeof(bad), cudaMemcpyHostToDevice, c.st));
+        k_check_bounds<<<grid_for(N), 256, 0, c.st>>>(pp ? bd.spatial_values : nullptr,
+                                                      pc ? bd.freq_re : nullptr,
+                                                      pc ? bd.freq_im : nullptr, d0, d1, d2, db);
+        FFCZ_LAUNCH_CHECK();
+        ++c.launches;
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(bad, db, sizeof(bad), cudaMemcpyDeviceToHost, c.st));
+        c.sync();
+    } else {
+        const int nt = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+        std::vector<std::array<unsigned long long, 2>> part(nt, {~0ull, ~0ull});
+        auto work = [&](int t) {
+            const long long lo = N * t / nt, hi = N * (t + 1) / nt;
+            auto& b = part[t];
+            for (long long i = lo; i < hi; ++i) {
+                if (pp) {
+                    const double v = bd.spatial_values[i];
+                    if (!(v > 0.0) || !std::isfinite(v)) b[0] = std::min<unsigned long long>(b[0], i);
+                }
+                if (pc) {
+                    const long long i2 = i % d2, q = i / d2, i1 = q % d1, i0 = q / d1;
+                    const long long m = (((d0 - i0) % d0) * d1 + (d1 - i1) % d1) * d2 + (d2 - i2) % d2;
+                    const double a = bd.freq_re[i], bb = bd.freq_im[i];
+                    if (!(a > 0.0) || !std::isfinite(a) || !(bb > 0.0) || !std::isfinite(bb))
+                        b[0] = std::min<unsigned long long>(b[0], N + i);
+                    if (a != bd.freq_re[m] || bb != bd.freq_im[m])
+                        b[1] = std::min<unsigned long long>(b[1], i);
+                }
+            }
+        };
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+        work(0);
+        for (auto& t : th) t.join();
+        for (auto& p : part) {
+            bad[0] = std::min(bad[0], p[0]);
+            bad[1] = std::min(bad[1], p[1]);
+        }
+    }
+    if (bad[0] != ~0ull) {
+        if (bad[0] < static_cast<unsigned long long>(N))
+            throw Error(kValidation, "per-point spatial bound must be strictly positive and finite");
+        throw Error(kValidation, "per-component frequency bound must be strictly positive and finite");
+    }
+    if (bad[1] != ~0ull)
+        throw Error(kValidation, "per-component frequency bounds are not Hermitian-consistent");
+}
+
 // Copies / restricts the caller's bounds onto the device (per-component arrays -> half layout).
-Bounds upload_bounds(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_bounds_desc& bd, bool on_dev) {
+Bounds upload_bounds(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_bounds_desc& bd, bool on_dev,
+                     bool validate = false) {
+    if (validate) validate_bounds(c, g, bd, on_dev);
     Bounds b;
     const long long N = g.N;
     if (bd.spatial_per_point) {
@@ -355,7 +447,7 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
     }
     const bool three_d = g.d[0] > 1;
     unsigned char* moved = nullptr;
-    if (fused && (keep_moved || (allow_rebuild && f_rebuild_enabled()))) {
+    if (fused && (keep_moved || (allow_rebuild && f_rebuild_enabled(c)))) {
         moved = c.b<unsigned char>("f_moved", g.half_elems());
         if (!keep_moved) FFCZ_CUDA_CHECK(cudaMemsetAsync(moved, 0, g.half_elems(), st));
     }
@@ -705,7 +797,7 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
         };
         bool verified = false;
         bool sc_zero = lr.s_zero;  // spat_cur stays zero until a spatial repair
-        const bool dview = decoder_view_repair();
+        const bool dview = decoder_view_repair(c);
         if (converged) {
             double* eps_v = dview ? nullptr : c.b<double>("eps_verify", N);
             for (int round = 0; round < 32; ++round) {                   // pipeline.cpp:116
@@ -907,7 +999,7 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
         orig = o;
         dec = d;
     }
-    const Bounds bo = upload_bounds(c, g, bd, on_dev);
+    const Bounds bo = upload_bounds(c, g, bd, on_dev, !(opt.flags & FFCZ_BOUNDS_VALIDATED));
     FFCZ_CUDA_CHECK(cudaEventRecord(c.ev[1], st));  // inputs resident
     dbg.mark(c, "inputs resident");
 
@@ -1225,6 +1317,7 @@ void run_on_lanes(ffcz_cuda_ctx* ctx, int nl, uint64_t n,
     for (int i = 0; i < nl; ++i) {
         ffcz_cuda_ctx* l = ctx->lanes[i];
         FFCZ_CUDA_CHECK(cudaStreamWaitEvent(l->st, start, 0));
+        l->call_flags = ctx->call_flags;
         if (l->prof_on != ctx->prof_on) {
             l->prof_on = ctx->prof_on;
             l->prof.clear();
@@ -1384,7 +1477,7 @@ void gate_frames(ffcz_cuda_ctx& c, const Geometry& gf, const ffcz_field_desc& fd
 
     // escape-repair rounds (pipeline.cpp:111-163) for the converged frames
     std::vector<int> rounds(Gc, 0), verified(Gc, 0);
-    const bool dview = decoder_view_repair();
+    const bool dview = decoder_view_repair(c);
     std::vector<double> vs(Gc, 0.0), vf(Gc, 0.0);
     std::vector<int> active(Gc);
     for (long long i = 0; i < Gc; ++i) active[i] = hfc[i].converged;
@@ -1936,6 +2029,7 @@ int ffcz_cuda_correct(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, const vo
             throw Error(kValidation, "mixed policy: tau_switch must be in (0, 1)");
         const Geometry g = make_geometry(field->ndim, field->dims, kPitchAlign);
         const unsigned long long l0 = ctx->launches;
+        ctx->call_flags = opt.flags;
         if (field->dtype == FFCZ_F32)
             correct_typed<float>(*ctx, g, *field, original, decompressed, *bounds_original, m,
                                  max_iters, opt, out);
@@ -1968,6 +2062,7 @@ int ffcz_cuda_correct_batch(ffcz_cuda_ctx* ctx, const ffcz_field_desc* frame, ui
             throw Error(kValidation, "unknown precision policy");
         for (uint64_t i = 0; i < nframes; ++i) std::memset(&out[i], 0, sizeof(out[i]));
         if (nframes == 0) return;
+        ctx->call_flags = opt.flags;
         const Geometry g = make_geometry(frame->ndim, frame->dims, kPitchAlign);
         const size_t esz = frame->dtype == FFCZ_F32 ? 4 : 8;
         if (lanes <= 0) lanes = 8;
@@ -2062,6 +2157,20 @@ int ffcz_cuda_apply_archive(ffcz_cuda_ctx* ctx, const uint8_t* archive, uint64_t
         const long long ws = (N + 31) / 32, wf = (Nc + 31) / 32;
         unsigned* ks = c.b<unsigned>("ap_keep_s", ws);
         unsigned* kf = c.b<unsigned>("ap_keep_f", wf);
+        // BitVector semantics (bitvector.hpp:24-29): only bits < nbits exist, so padding bits of
+        // the last flag byte are cleared; the flag count must equal the code count before any
+        // scatter is launched (archive.cpp:205-208), so a malformed archive never indexes past
+        // N / Nc or past the decoded codes
+        auto clean_flags = [&](std::vector<uint8_t>& f, long long nbits, unsigned long long want) {
+            if (static_cast<long long>(f.size()) != (nbits + 7) / 8)
+                throw Error(kFormat, "read_archive: flag stream size mismatch");
+            if ((nbits & 7) && !f.empty()) f.back() &= static_cast<uint8_t>((1u << (nbits & 7)) - 1);
+            unsigned long long pc = 0;
+            for (uint8_t v : f) pc += static_cast<unsigned>(__builtin_popcount(v));
+            if (pc != want) throw Error(kFormat, "read_archive: edit count mismatch");
+        };
+        clean_flags(a.spatial_flags, N, a.n_spatial);
+        clean_flags(a.frequency_flags, Nc, a.n_frequency);
         FFCZ_CUDA_CHECK(cudaMemsetAsync(ks, 0, 4 * ws, st));
         FFCZ_CUDA_CHECK(cudaMemsetAsync(kf, 0, 4 * wf, st));
         FFCZ_CUDA_CHECK(cudaMemcpyAsync(ks, a.spatial_flags.data(), a.spatial_flags.size(),
@@ -2100,8 +2209,7 @@ int ffcz_cuda_apply_archive(ffcz_cuda_ctx* ctx, const uint8_t* archive, uint64_t
             k_scan_blocks<<<1, 1024, 0, st>>>(cnt, nblk, &c.ctl->count_a);
             launch(static_cast<unsigned>(nblk), cnt);
             FFCZ_LAUNCH_CHECK();
-            if (c.read_ctl().count_a != want)                        // archive.cpp:205-208
-                throw Error(kFormat, "read_archive: edit count mismatch");
+            (void)want;  // checked on the host flags above
         };
         scatter(ks, ws, a.n_spatial, "ap_cnt_s", [&](unsigned nb, unsigned long long* o) {
             k_dequant_spatial_bits<<<nb, 1024, 0, st>>>(ks, ws, o, cs, b.sb, a.m, spat);
@@ -2317,7 +2425,8 @@ int ffcz_cuda_alternating_projection(ffcz_cuda_ctx* ctx, const ffcz_field_desc* 
         cudaStream_t st = c.st;
         const bool on_dev = opt.flags & FFCZ_INPUTS_ON_DEVICE;
         const long long N = g.N;
-        const Bounds bw = upload_bounds(c, g, *bw_desc, on_dev);
+        c.call_flags = opt.flags;
+        const Bounds bw = upload_bounds(c, g, *bw_desc, on_dev, !(opt.flags & FFCZ_BOUNDS_VALIDATED));
         double* eps = c.b<double>("eps", N);
         const size_t esz = field->dtype == FFCZ_F32 ? 4 : 8;
         const void* src = eps0_in;

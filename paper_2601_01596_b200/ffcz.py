@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import threading
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -107,6 +107,16 @@ class DualBounds:
     spatial: float | np.ndarray
     freq_re: float | np.ndarray
     freq_im: float | np.ndarray | None = None
+    # the field shape these arrays were validated for (DualBounds' invariants: entries > 0 and
+    # finite, Hermitian-consistent lanes, bounds.cpp:10-59).  The reference checks them once,
+    # when a DualBounds is built; here the engine checks them on the first call that uses the
+    # arrays and later calls pass FFCZ_BOUNDS_VALIDATED.  Arrays are treated as immutable
+    # afterwards, like the reference's vectors.
+    _validated_for: tuple | None = field(default=None, repr=False, compare=False)
+
+    def _arrays(self):
+        return tuple(id(a) for a in (self.spatial, self.freq_re, self.freq_im)
+                     if a is not None and not isinstance(a, (float, int, np.floating)))
 
     @staticmethod
     def global_(e: float, delta: float) -> "DualBounds":
@@ -209,41 +219,80 @@ class _Marshal:
     def __init__(self):
         self.keep = []
 
-    def ptr(self, a, dtype=np.float64):
+    def ptr(self, a, dtype=np.float64, on_dev=None, what="array"):
+        """Pointer to `a` as a contiguous `dtype` buffer.  Torch tensors must already have that
+        dtype (a float32 tensor is never reinterpreted as float64) and live where the call's
+        inputs live (on_dev); numpy arrays are converted (a copy when needed)."""
         if a is None:
             return None
         if _is_torch(a):
+            import torch
+            want = torch.float64 if dtype == np.float64 else torch.float32
+            if a.dtype != want:
+                raise ValidationError(f"{what}: expected a {want} tensor, got {a.dtype}")
+            if on_dev is not None and bool(a.is_cuda) != bool(on_dev):
+                raise ValidationError(f"{what}: must be a {'CUDA' if on_dev else 'host'} array "
+                                      "like the fields")
+            if not a.is_cuda:
+                return self.ptr(a.numpy(), dtype, on_dev, what)
+            a = a.contiguous()
             self.keep.append(a)
             return C.c_void_p(a.data_ptr())
+        if on_dev:
+            raise ValidationError(f"{what}: must be a CUDA tensor like the fields")
         arr = np.ascontiguousarray(a, dtype=dtype)
         self.keep.append(arr)
         return C.c_void_p(arr.ctypes.data)
 
 
-def _bounds_desc(b: DualBounds, m: _Marshal):
+def _numel(a) -> int:
+    return int(a.numel()) if _is_torch(a) else int(np.size(a))
+
+
+def _bounds_desc(b: DualBounds, m: _Marshal, shape=None, on_dev=None):
+    """ffcz_bounds_desc of `b`; with `shape`, DualBounds::validate_for (bounds.cpp:65-71): array
+    bounds must cover every sample / the full spectrum (the engine reads N doubles from each)."""
     bd = capi.BoundsDesc()
+    total = int(np.prod(shape)) if shape is not None else None
     sp = b.spatial
     if isinstance(sp, (float, int, np.floating)):
         bd.spatial_per_point, bd.spatial_global = 0, float(sp)
     else:
-        bd.spatial_per_point, bd.spatial_values = 1, m.ptr(sp)
+        if total is not None and _numel(sp) != total:
+            raise ValidationError("per-point spatial bound length does not match field size")
+        bd.spatial_per_point = 1
+        bd.spatial_values = m.ptr(sp, np.float64, on_dev, "per-point spatial bound")
     re = b.freq_re
     im = b.freq_im if b.freq_im is not None else b.freq_re
     if isinstance(re, (float, int, np.floating)):
         bd.freq_per_component, bd.freq_global = 0, float(re)
     else:
+        if isinstance(im, (float, int, np.floating)):
+            raise ValidationError("per-component frequency bounds need both Re and Im lanes")
+        if total is not None and (_numel(re) != total or _numel(im) != total):
+            raise ValidationError("per-component frequency bound length does not match field size")
         bd.freq_per_component = 1
-        bd.freq_re = m.ptr(re)
-        bd.freq_im = bd.freq_re if im is re else m.ptr(im)
+        bd.freq_re = m.ptr(re, np.float64, on_dev, "per-component frequency bound (Re)")
+        bd.freq_im = bd.freq_re if im is re else m.ptr(im, np.float64, on_dev,
+                                                         "per-component frequency bound (Im)")
     return bd
 
 
 def _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level,
-             device_encode=False, policy="fp64", tau=1e-4):
+             device_encode=False, policy="fp64", tau=1e-4, repair_order="decoder",
+             f_update="rebuild"):
     lib = capi.load()
     opt = capi.Options()
     lib.ffcz_cuda_default_options(C.byref(opt))
     flags = 0
+    if repair_order not in ("decoder", "reference"):
+        raise ValidationError(f"unknown repair order {repair_order!r}")
+    if f_update not in ("rebuild", "accumulate"):
+        raise ValidationError(f"unknown F update {f_update!r}")
+    if repair_order == "reference":
+        flags |= capi.FFCZ_REPAIR_REFERENCE_ORDER
+    if f_update == "accumulate":
+        flags |= capi.FFCZ_F_ACCUMULATE
     if on_dev:
         flags |= capi.FFCZ_INPUTS_ON_DEVICE
     if want_archive:
@@ -322,17 +371,34 @@ def _convert(holder, shape, want_archive, want_edits, want_corrected, copy):
 
 
 def _field_of(original, decompressed):
-    """(on_dev, is32, shape, original, decompressed) of numpy / CUDA torch inputs."""
+    """(on_dev, is32, shape, original, decompressed) of numpy / CUDA torch inputs, with the
+    reference's compute_error check (projection.cpp:20-22): same dims and sample type."""
+    if _is_torch(original) != _is_torch(decompressed):
+        raise ValidationError("compute_error: original and decompressed must both be host arrays "
+                              "or both CUDA tensors")
     on_dev = _is_torch(original)
     if on_dev:
         import torch
+        if not (original.is_cuda and decompressed.is_cuda):
+            original, decompressed = original.cpu().numpy(), decompressed.cpu().numpy()
+            return _field_of(original, decompressed)
+        if original.dtype not in (torch.float32, torch.float64):
+            raise ValidationError(f"fields must be float32 or float64, got {original.dtype}")
+        if tuple(original.shape) != tuple(decompressed.shape) or \
+                original.dtype != decompressed.dtype:
+            raise ValidationError("compute_error: dims/precision mismatch")
         is32 = original.dtype == torch.float32
         shape = tuple(original.shape)
+        original, decompressed = original.contiguous(), decompressed.contiguous()
     else:
         original = np.asarray(original)
         decompressed = np.asarray(decompressed)
+        if original.shape != decompressed.shape or original.dtype != decompressed.dtype:
+            raise ValidationError("compute_error: dims/precision mismatch")
         is32 = original.dtype == np.float32
         shape = original.shape
+    if not 1 <= len(shape) <= 3 or any(int(n) == 0 for n in shape):
+        raise ValidationError("field must have 1 to 3 non-empty axes")
     return on_dev, is32, shape, original, decompressed
 
 
@@ -340,7 +406,8 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
             precision: str | None = None, *, want_archive: bool = True, want_edits: bool = True,
             want_corrected: bool = True, zlib_level: int = 9, fused: bool = True,
             copy: bool = True, device_encode: bool = False, policy: str = "fp64",
-            tau: float = 1e-4, ctx: Context | None = None) -> CorrectionResult:
+            tau: float = 1e-4, repair_order: str = "decoder", f_update: str = "rebuild",
+            ctx: Context | None = None) -> CorrectionResult:
     """ffcz::correct (pipeline.cpp:26-178) on the GPU.
 
     original / decompressed: numpy arrays (host; float32 or float64) or CUDA torch tensors (then
@@ -351,8 +418,11 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
     payload bytes as huffman.cpp); zlib_level then sets the host outer stage (0 = stored).
     policy: "fp64" (reference control flow in FP64, default) or "mixed" (FP32 passes while
     max_excess / peak > tau, then FP64; iterations within +-1 of the reference).
+    repair_order: "decoder" (default: repair the decoder's own view) or
+    "reference" (check eps_tilde each round + a separate verify, pipeline.cpp:134-160 — the
+    reference's escape lists).  f_update: "rebuild" (default: F rebuilt once at the gate) or
+    "accumulate" (F += displacement in every clip, projection.cpp:117-119).
     """
-    ctx = ctx or default_context()
     lib = capi.load()
     on_dev, is32, shape, original, decompressed = _field_of(original, decompressed)
     if precision is None:
@@ -360,9 +430,13 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
     dt = np.float32 if is32 else np.float64
     mar = _Marshal()
     fd = _field_desc(shape, capi.FFCZ_F32 if is32 else capi.FFCZ_F64, precision)
-    bd = _bounds_desc(bounds, mar)
+    bd = _bounds_desc(bounds, mar, shape, on_dev)
     opt = _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level,
-                   device_encode, policy, tau)
+                   device_encode, policy, tau, repair_order, f_update)
+    ctx = ctx or default_context()   # after the argument checks (they need no device)
+    key = (tuple(shape), bool(on_dev), bounds._arrays())
+    if bounds._validated_for == key:
+        opt.flags |= capi.FFCZ_BOUNDS_VALIDATED
     if on_dev:
         _order_after_torch(original, decompressed, bounds.spatial, bounds.freq_re, bounds.freq_im)
     holder = _ResultHolder()
@@ -374,6 +448,7 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
     except Exception:
         holder.free()
         raise
+    bounds._validated_for = key
     return _convert(holder, shape, want_archive, want_edits, want_corrected, copy)
 
 
@@ -381,6 +456,7 @@ def correct_batch(original, decompressed, bounds, m: int = 16, max_iters: int = 
                   precision: str | None = None, *, lanes: int = 8, want_archive: bool = True,
                   want_edits: bool = True, want_corrected: bool = True, zlib_level: int = 9,
                   fused: bool = True, copy: bool = True, policy: str = "fp64", tau: float = 1e-4,
+                  repair_order: str = "decoder", f_update: str = "rebuild",
                   ctx: Context | None = None) -> list[CorrectionResult]:
     """Independent ffcz::correct() of every frame of a batch (BASELINE config 3).
 
@@ -403,9 +479,9 @@ def correct_batch(original, decompressed, bounds, m: int = 16, max_iters: int = 
     fd = _field_desc(frame, capi.FFCZ_F32 if is32 else capi.FFCZ_F64, precision)
     bds = (capi.BoundsDesc * max(1, nf))()
     for i, b in enumerate(bounds):
-        bds[i] = _bounds_desc(b, mar)
+        bds[i] = _bounds_desc(b, mar, frame, on_dev)
     opt = _options(on_dev, want_archive, want_edits, want_corrected, fused, zlib_level,
-                   False, policy, tau)
+                   False, policy, tau, repair_order, f_update)
     if on_dev:
         _order_after_torch(original, decompressed)
     res = (capi.Result * max(1, nf))()
@@ -433,7 +509,7 @@ def alternating_projection(eps0, bounds_working: DualBounds, max_iters: int,
     shape = eps0.shape
     mar = _Marshal()
     fd = _field_desc(shape, capi.FFCZ_F64, "f64")
-    bd = _bounds_desc(bounds_working, mar)
+    bd = _bounds_desc(bounds_working, mar, shape, False)
     opt = capi.Options()
     lib.ffcz_cuda_default_options(C.byref(opt))
     opt.flags = 0 if fused else capi.FFCZ_FORCE_UNFUSED

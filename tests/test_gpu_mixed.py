@@ -1,7 +1,9 @@
 """Mixed FP32 -> FP64 policy (BASELINE north star: FP32 with
 iteration counts within +-1 and both bounds exact).  Against the reference's golden outputs:
 converged flag equal, iterations within +-1, both bounds hold exactly on the FP64 corrected field
-(the gate is FP64), flags and codes agree on >= 99 % of entries."""
+(the gate is FP64: spatial excess 0.0, every frequency component within 1e-15 of its Delta
+under numpy's FFT), flag counts within 1 % of the reference's digest on every case, and flags
+and codes agreeing on >= 99 % of entries where the reference's archive is stored."""
 import json
 import os
 
@@ -40,7 +42,12 @@ def test_mixed_policy(ffcz, case):
     assert r.verify_ok
     ok, ms, mf = O.verify_bounds(case.original, r.corrected, O.DualBounds(case.E, case.Dre, case.Dim))
     assert ms == 0.0
-    assert mf <= 1e-12 * float(np.max(np.abs(np.asarray(case.Dre))))
+    assert cases.freq_excess_per_component(case.original, r.corrected, case.Dre, case.Dim) <= 1e-15
+    # flags: every case against the reference's digest (flag counts within 1 %, and the full
+    # flag / code comparison where the reference's archive is stored)
+    dg = cases.digest_of_result(r)
+    for k in ("popcount_s", "popcount_f"):
+        assert abs(dg[k] - g["digest"][k]) <= max(1, g["digest"][k] // 100), (k, dg[k], g["digest"][k])
     mine = O.read_archive(r.archive_bytes)
     if case.name in ARCH:
         ref = O.read_archive(ARCH[case.name].tobytes())

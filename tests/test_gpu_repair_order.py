@@ -63,3 +63,32 @@ def test_repair_orders_agree_with_golden():
         assert a["flags"] == b["flags"] and a["codes"] == b["codes"]
         assert abs(a["escapes"] - g["escape_count"]) <= max(2, g["escape_count"] // 10)
         assert abs(b["escapes"] - g["escape_count"]) <= max(2, g["escape_count"] // 10)
+
+
+def test_per_call_options_match_env_switches():
+    """repair_order="reference" / f_update="accumulate" per call (ffcz_cuda_options.flags) give
+    the env-switched results; with both, escape keys follow the reference's order."""
+    import cases
+    import paper_2601_01596_b200 as P
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
+    env_ref = _run("reference")
+    same_keys = 0
+    for c in cases.all_cases():
+        if c.name not in NAMES:
+            continue
+        r = P.correct(c.original, c.decompressed, P.DualBounds(c.E, c.Dre, c.Dim), c.m,
+                      c.max_iters, c.precision, repair_order="reference")
+        import hashlib
+        flags = hashlib.sha256(r.frequency_flags.tobytes() + r.spatial_flags.tobytes()).hexdigest()
+        codes = hashlib.sha256(r.frequency_codes.tobytes() + r.spatial_codes.tobytes()).hexdigest()
+        e = env_ref[c.name]
+        assert (r.report.iterations, flags, codes, int(r.escape_count)) == \
+            (e["iterations"], e["flags"], e["codes"], e["escapes"])
+        ra = P.correct(c.original, c.decompressed, P.DualBounds(c.E, c.Dre, c.Dim), c.m,
+                       c.max_iters, c.precision, repair_order="reference", f_update="accumulate")
+        g = gold[c.name]
+        assert ra.report.iterations == g["iterations"]
+        cmp = cases.compare_digest(cases.digest_of_result(ra), g["digest"])
+        assert cmp["flags"] and cmp["code_blocks_f"] == 0 and cmp["code_blocks_s"] == 0, cmp
+        same_keys += bool(cmp["escapes"])
+    print("escape keys identical to the reference's in", same_keys, "of", len(NAMES), "cases")
