@@ -518,22 +518,38 @@ def ncu_traffic(name, n=None):
     return d.get(name)
 
 
-def cpu_reference_sample(n, threads, steps=1):
-    """Time the unmodified reference correct() (oracle/_ref) on an n^3 sample of the recipe."""
+def numpy_workload(config, n):
+    """(orig, dec, E, Delta) of `config`'s recipe at n^3 on the host, float64 arrays of the FP32
+    fields (the CPU samples)."""
+    if config == "nyx":
+        return make_workload_numpy(n, 11)
+    o, d, E, D = make_workload_combustion(n, 4321, "cpu")
+    return o.numpy().astype(np.float64), d.numpy().astype(np.float64), E, D
+
+
+def cpu_reference_sample(n, threads, steps=1, config="combustion"):
+    """Time the unmodified reference correct() (oracle/_ref, MKL-backed FFTW provider) on an n^3
+    sample of the recipe."""
     env = dict(os.environ, FFCZ_SHIM_THREADS=str(threads))
     code = (
         "import sys, json, time; sys.path.insert(0, %r); import bench; "
         "from oracle import ref_binding as ref; "
-        "o, d, E, D = bench.make_workload_numpy(%d, 11); ts = []\n"
+        "o, d, E, D = bench.numpy_workload(%r, %d); ts = []\n"
         "for _ in range(%d):\n"
         "    r = ref.correct(o, d, E, D, None, 16, 1000, 'f32'); ts.append(r.correct_wall_s)\n"
         "print(json.dumps({'times': ts, 'iterations': r.report.iterations, "
-        "'verify_ok': r.verify_ok}))" % (ROOT, n, steps))
+        "'verify_ok': r.verify_ok, 'fft': ref.fft_backend()}))" % (ROOT, config, n, steps))
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                          timeout=1800)
     if out.returncode != 0:
         raise RuntimeError(out.stderr[-2000:])
     return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+RECIPES = {
+    "nyx": "config2 recipe (Nyx-like log-normal field, rho=1e-3 per-component Delta)",
+    "combustion": "config4 recipe (combustion-like front, global Delta=0.6*mean|delta0|)",
+}
 
 
 def run_reference_arm(args, rank, world):
@@ -545,22 +561,26 @@ def run_reference_arm(args, rank, world):
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    res = cpu_reference_sample(n, threads, steps=args.warmup + args.steps)
+    config = args.config if args.config in RECIPES else "combustion"
+    res = cpu_reference_sample(n, threads, steps=args.warmup + args.steps, config=config)
     ts = res["times"][args.warmup:]
     t = float(np.mean(ts))
     gbs = 4.0 * n ** 3 / t / 1e9
+    sample = (f"{n}^3 of the {RECIPES[config]}: one full ffcz::correct() of the unmodified "
+              f"reference per step (archive with zlib-9 included), FFTW API served by MKL on "
+              f"{threads} threads (the reference itself is single-threaded); the {args.n}^3 field "
+              f"needs ~{int(130 * (args.n / 1024) ** 3) + 1} GB of host RAM in the reference")
     line = {
         "impl": "reference", "metric": "corrected GB/s (input bytes / time to feasibility)",
         "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config2 recipe (512^3 Nyx-like, rho=1e-3) at a bounded {n}^3 sample",
-                   "n": n},
+        "config": {"workload": f"{RECIPES[config]} at a bounded {n}^3 sample", "n": n},
+        "ms_per_iteration": t * 1e3 / max(1, res["iterations"]),
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "reference",
-                         "sample": f"{n}^3 of the config-2 recipe, full ffcz::correct() incl. archive, "
-                                   f"FFT shim on {threads} threads"},
+                         "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "iterations": res["iterations"], "verify_ok": res["verify_ok"],
+        "iterations": res["iterations"], "verify_ok": res["verify_ok"], "fft": res["fft"],
     }
     print(json.dumps(line))
 
@@ -571,10 +591,12 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=512)
-    ap.add_argument("--config", default="nyx", choices=["nyx", "combustion", "frames", "slab"],
-                    help="nyx = BASELINE configs[1] (default); combustion = configs[3] recipe; "
-                         "frames = configs[2] (batched 2-D frames, sharded)")
+    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--config", default="combustion",
+                    choices=["nyx", "combustion", "frames", "slab"],
+                    help="combustion = configs[3] recipe at 1024^3 on one GPU (default: the "
+                         "north_star target); nyx = configs[1] (use --n 512); frames = configs[2] "
+                         "(batched 2-D frames, sharded); slab = configs[3] slab-decomposed")
     ap.add_argument("--frames", type=int, default=1024)
     ap.add_argument("--frame-n", type=int, default=2048)
     ap.add_argument("--lanes", type=int, default=8)
@@ -678,70 +700,56 @@ def main():
     iters = [r.report.iterations for r in results]
     loop_ms = [r.timings_ms["t_loop_ms"] for r in results]
 
-    # e2e through the public API with pinned host buffers (H2D + D2H inside the timed region)
+    # e2e through the public API with pinned host buffers: every step copies the inputs in,
+    # corrects, writes the .ffcz archive (device outer stage, the default) and copies it out
+    # (the reference's correct() returns archive_bytes); the edit-set-only variant beside it
     e2e = None
     if not args.no_e2e:
         h_orig = torch.empty((n, n, n), dtype=torch.float32, pin_memory=True)
         h_dec = torch.empty_like(h_orig, pin_memory=True)
         h_orig.copy_(orig)
         h_dec.copy_(dec)
+        o_np, d_np = h_orig.numpy(), h_dec.numpy()
+        ksteps = max(1, min(args.steps, 3))
         if isinstance(delta, float):
             hb = P.DualBounds(E, delta)
-            h2d_delta = 0
+
+            def e2e_step(archive):
+                return P.correct(o_np, d_np, hb, 16, 1000, "f32", want_archive=archive,
+                                 want_edits=not archive, want_corrected=False, copy=False,
+                                 ctx=ctx)
+            how = "H2D of original+decompressed (f32) from pinned memory, device correct()"
         else:
-            h_delta = torch.empty((n, n, n), dtype=torch.float64, pin_memory=True)
-            h_delta.copy_(delta)
-            hb = P.DualBounds(E, h_delta.numpy())
-            h2d_delta = 8 * (N // n) * (n // 2 + 1)
-        o_np, d_np = h_orig.numpy(), h_dec.numpy()
-        r = None
-        for _ in range(2):  # warm the pinned result pool (two generations of result buffers)
-            r = None
-            r = P.correct(o_np, d_np, hb, 16, 1000, "f32", want_archive=False,
-                          want_corrected=False, copy=False, ctx=ctx)
-        barrier()
-        t0 = time.perf_counter()
-        ksteps = max(1, min(args.steps, 3))
-        for _ in range(ksteps):
-            r = None  # release the previous result's pinned buffers back to the pool
-            r = P.correct(o_np, d_np, hb, 16, 1000, "f32", want_archive=False,
-                          want_corrected=False, copy=False, ctx=ctx)
-        barrier()
-        te = (time.perf_counter() - t0) / ksteps
-        if world > 1:
-            t = torch.tensor([te], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = t.item()
-        d2h = (r.spatial_flags.nbytes + r.frequency_flags.nbytes + r.spatial_codes.nbytes +
-               r.frequency_codes.nbytes + r.escapes.nbytes)
-        e2e_upload = {"value": world * 4.0 * N / te / 1e9, "ms_per_step": te * 1e3,
-                      "h2d_bytes_per_step": 4 * N * 2 + h2d_delta}
-        if not isinstance(delta, float):
-            # the reference CLI's --rho path (proj/tools/ffcz.cpp:97-102 then :170): the Delta lane
-            # is a function of the original, so it is derived on the device from the uploaded
-            # original (spectrum_bound_to_freq_bounds) instead of shipping 0.54 GB of it; the
-            # decompressed field's H2D overlaps that transform on a second copy stream
+            # the reference CLI's --rho path (proj/tools/ffcz.cpp:97-102 then :170): the Delta
+            # lane is a function of the original, so it is derived on the device from the
+            # uploaded original (spectrum_bound_to_freq_bounds) instead of shipping 1 GB of it;
+            # the decompressed field's H2D overlaps that transform on a second copy stream
             cs = torch.cuda.Stream(dev)
             d_orig, d_dec = torch.empty_like(orig), torch.empty_like(dec)
 
-            def e2e_rho_step():
+            def e2e_step(archive):
                 d_orig.copy_(h_orig, non_blocking=True)
                 with torch.cuda.stream(cs):
                     d_dec.copy_(h_dec, non_blocking=True)
                 D = P.spectrum_bound_to_freq_bounds(d_orig, RHO, ctx=ctx)
                 stream.wait_stream(cs)
                 return P.correct(d_orig, d_dec, P.DualBounds(E, D), 16, 1000, "f32",
-                                 want_archive=False, want_corrected=False, copy=False, ctx=ctx), D
+                                 want_archive=archive, want_edits=not archive,
+                                 want_corrected=False, copy=False, ctx=ctx)
+            how = ("H2D of original+decompressed (f32) from pinned memory, the per-component "
+                   "Delta derived on the device from the original (spectrum_bound_to_freq_bounds, "
+                   "rho=1e-3: the reference CLI's --rho path), device correct()")
 
-            for _ in range(2):
+        def timed(archive):
+            r = None
+            for _ in range(2):  # warm the pinned result pool (two generations of buffers)
                 r = None
-                r, Dr = e2e_rho_step()
-            assert bool(torch.equal(Dr, delta)), "device rho bound not reproducible"
+                r = e2e_step(archive)
             barrier()
             t0 = time.perf_counter()
             for _ in range(ksteps):
-                r = None
-                r, _ = e2e_rho_step()
+                r = None  # release the previous result's pinned buffers back to the pool
+                r = e2e_step(archive)
             barrier()
             te = (time.perf_counter() - t0) / ksteps
             if world > 1:
@@ -749,37 +757,39 @@ def main():
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 te = t.item()
             assert r.report.converged and r.verify_ok
-            h2d_delta = 0
+            return te, r
+
+        te, r = timed(True)
+        arch_len = int(len(r.archive_bytes))
         e2e = {"value": world * 4.0 * N / te / 1e9, "unit": "GB/s",
                "lib_timings_ms": r.timings_ms,
-               "h2d_bytes_per_step": 4 * N * 2 + h2d_delta,
-               "d2h_bytes_per_step": int(d2h),
+               "h2d_bytes_per_step": 4 * N * 2, "d2h_bytes_per_step": arch_len,
                "ms_per_step": te * 1e3, "steps": ksteps,
-               "includes": ("H2D of original+decompressed (f32) from pinned memory, the "
-                            "per-component Delta derived on the device from the original "
-                            "(spectrum_bound_to_freq_bounds, rho=1e-3: the reference CLI's --rho "
-                            "path), device correct(), D2H of the edit set (flags + int32 codes + "
-                            "escapes = what the archive carries); archive serialisation reported "
-                            "separately" if not isinstance(delta, float) else
-                            "H2D of original+decompressed (f32) from pinned memory, device "
-                            "correct(), D2H of the edit set (flags + int32 codes + escapes = what "
-                            "the archive carries); archive serialisation reported separately")}
-        if not isinstance(delta, float):
-            e2e["delta_upload"] = dict(e2e_upload, includes=(
-                "the same with the Delta lane uploaded instead (half-grid columns, f64, one "
-                "strided DMA) and no device bound computation"))
+               "includes": how + ", the .ffcz archive assembled from device-encoded streams "
+                                 "(Huffman + deflate blocks on the GPU, header CRC) and its D2H "
+                                 "into pinned memory: the reference correct()'s archive_bytes"}
+        te2, r2 = timed(False)
+        d2h = (r2.spatial_flags.nbytes + r2.frequency_flags.nbytes + r2.spatial_codes.nbytes +
+               r2.frequency_codes.nbytes + r2.escapes.nbytes)
+        e2e["edit_set_only"] = {
+            "value": world * 4.0 * N / te2 / 1e9, "ms_per_step": te2 * 1e3,
+            "h2d_bytes_per_step": 4 * N * 2, "d2h_bytes_per_step": int(d2h),
+            "includes": how + ", D2H of the edit set (flags + int32 codes + escapes), no archive"}
+        r = r2 = None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import ref_binding as ref
             if ref.available():
-                res = cpu_reference_sample(args.cpu_n, 1)
+                res = cpu_reference_sample(args.cpu_n, 1, config=args.config)
                 t = res["times"][0]
                 cpu = {"value": 4.0 * args.cpu_n ** 3 / t / 1e9, "unit": "GB/s", "cores": 1,
                        "kind": "reference",
                        "sample": f"{args.cpu_n}^3 of the same recipe, one ffcz::correct() of the "
-                                 f"unmodified reference (oracle/_ref), single thread, {t:.1f} s"}
+                                 f"unmodified reference (oracle/_ref, MKL-backed FFTW API, "
+                                 f"{res['fft']}), single thread, {t:.1f} s, "
+                                 f"{res['iterations']} iterations"}
         except Exception as e:  # the GPU number stands without it
             cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "reference",
                    "sample": f"failed: {e!s:.200}"}

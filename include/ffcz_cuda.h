@@ -86,7 +86,7 @@ typedef enum ffcz_cuda_policy { FFCZ_POLICY_FP64 = 0, FFCZ_POLICY_MIXED = 1 } ff
 
 /* option flags */
 #define FFCZ_INPUTS_ON_DEVICE (1u << 0) /* original/decompressed/bounds are device pointers      */
-#define FFCZ_WANT_ARCHIVE (1u << 1)     /* serialise the .ffcz archive (host Huffman + zlib)    */
+#define FFCZ_WANT_ARCHIVE (1u << 1)     /* serialise the .ffcz archive (see zlib_level)        */
 #define FFCZ_WANT_EDITS (1u << 2)       /* copy flags, int32 codes and escapes to the host      */
 #define FFCZ_WANT_CORRECTED (1u << 3)   /* copy the FP64 corrected field to the host            */
 #define FFCZ_FORCE_UNFUSED (1u << 4)    /* use the per-op (unfused) loop even for 2^k shapes    */
@@ -107,11 +107,22 @@ typedef enum ffcz_cuda_policy { FFCZ_POLICY_FP64 = 0, FFCZ_POLICY_MIXED = 1 } ff
                                            (projection.cpp:117-119); default: mark the clipped
                                            components and rebuild F once at the gate */
 
+/* zlib_level value: the archive is assembled from device-encoded streams (deflate.cu): Huffman
+ * payloads byte-identical to huffman.cpp, each stream framed as outer_compress does
+ * (streams.cpp:21-32: u64 raw size + a zlib stream) with fixed-Huffman / stored deflate blocks
+ * written on the GPU, header CRC-32C over the bound arrays on the GPU when they are resident
+ * there.  The reference's read_archive (archive.cpp:137-225, zlib uncompress) decodes it to the
+ * same edits; only the outer stage's bytes differ from zlib-9's. */
+#define FFCZ_OUTER_DEVICE (-1)
+
 typedef struct ffcz_cuda_options {
     uint32_t flags;
     int32_t policy;          /* ffcz_cuda_policy */
     double tau_switch;       /* MIXED: switch to FP64 when max_excess/peak <= tau (default 1e-4) */
-    int32_t zlib_level;      /* archive outer stage level; 9 = reference byte-identical (default) */
+    int32_t zlib_level;      /* archive outer stage: FFCZ_OUTER_DEVICE (default) = every stream
+                                encoded on the device; 0..9 = host zlib at that level after the
+                                Huffman stage (host, or device with FFCZ_DEVICE_ENCODE); 9 =
+                                the reference's bytes (streams.cpp:21-32, Z_BEST_COMPRESSION) */
 } ffcz_cuda_options;
 
 /* ffcz::ProjectionReport (projection.hpp:17-25) */
@@ -338,6 +349,17 @@ int ffcz_cuda_apply_archive(ffcz_cuda_ctx* ctx, const uint8_t* archive, uint64_t
  * (huffman.cpp:156-251) of zigzag(codes[0..n)) into out (capacity cap); *len = its length. */
 int ffcz_cuda_huffman_encode(ffcz_cuda_ctx* ctx, const int32_t* codes, uint64_t n, uint8_t* out,
                              uint64_t cap, uint64_t* len);
+
+/* The device outer stage (deflate.cu) on n host bytes: writes outer_compress's framing
+ * (streams.cpp:21-32: u64 raw size + a zlib stream of fixed-Huffman / stored blocks made on the
+ * GPU) into out (capacity cap); *len = its length (out may be NULL to query it). */
+int ffcz_cuda_outer_compress(ffcz_cuda_ctx* ctx, const uint8_t* data, uint64_t n, uint8_t* out,
+                             uint64_t cap, uint64_t* len);
+
+/* CRC-32C (archive.cpp:61-71) of n bytes computed on the device (crc32c_raw_device + the host
+ * combine algebra); data is a device pointer when on_device, else host (copied in first). */
+int ffcz_cuda_crc32c_device(ffcz_cuda_ctx* ctx, const uint8_t* data, uint64_t n, int on_device,
+                            uint32_t* crc);
 
 /* CRC-32C (archive.cpp:61-71), exported for the format tests. */
 uint32_t ffcz_cuda_crc32c(const uint8_t* data, size_t len);

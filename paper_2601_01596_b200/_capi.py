@@ -46,7 +46,7 @@ EXPORTS = [
     "ffcz_cuda_profile_enable", "ffcz_cuda_profile_read", "ffcz_cuda_bench_passes",
     "ffcz_cuda_slab", "ffcz_cuda_slab_pitch", "ffcz_cuda_huffman_encode",
     "ffcz_cuda_apply_archive", "ffcz_cuda_spectrum_bound", "ffcz_cuda_metrics",
-    "ffcz_cuda_power_spectrum",
+    "ffcz_cuda_power_spectrum", "ffcz_cuda_outer_compress", "ffcz_cuda_crc32c_device",
 ]
 
 
@@ -134,6 +134,9 @@ def load():
                                             P]
     lib.ffcz_cuda_huffman_encode.argtypes = [P, P, C.c_uint64, P, C.c_uint64,
                                              C.POINTER(C.c_uint64)]
+    lib.ffcz_cuda_outer_compress.argtypes = [P, P, C.c_uint64, P, C.c_uint64,
+                                             C.POINTER(C.c_uint64)]
+    lib.ffcz_cuda_crc32c_device.argtypes = [P, P, C.c_uint64, C.c_int, C.POINTER(C.c_uint32)]
     lib.ffcz_cuda_slab_pitch.argtypes = [C.c_uint64]
     lib.ffcz_cuda_slab_pitch.restype = C.c_uint64
     lib.ffcz_cuda_result_free.argtypes = [C.POINTER(Result)]

@@ -24,6 +24,8 @@
 
 #include "../../include/ffcz_cuda.h"
 #include "archive.hpp"
+#include "archive_dev.cuh"
+#include "deflate.cuh"
 #include "encode.cuh"
 #include "fft_plan.cuh"
 #include "kernels.cuh"
@@ -1055,6 +1057,17 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     out->t_feasible_ms = event_ms(c.ev[1], c.ev[6]);
 }
 
+// FFCZ_OUTER_DEVICE archives (archive_dev.cu) into the pinned result pool
+void device_archive(ffcz_cuda_ctx& c, const DevArchiveInput& ai, ffcz_cuda_result* r) {
+    DevScratch ds{c.st, [&](const char* nm, size_t b) { return c.buf(nm, b); }};
+    const auto t0 = std::chrono::steady_clock::now();
+    std::uint64_t len = 0;
+    write_archive_device(ds, ai, [](size_t n) { return pinned().get(n); }, &r->archive, &len);
+    r->archive_len = len;
+    r->t_archive_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
 // Residual, FP64 gate and products of one field whose projection loop has run (pipeline.cpp:
 // 46-176): shared by correct() and the batched-frame path (each frame's state in the batch
 // arrays).  Records ev[3] -> ev[6] around the gate.
@@ -1081,7 +1094,12 @@ void finish_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& fd
     // the FP64 corrected field is only materialised when the caller asks for it (the reference's
     // CorrectionResult carries no field; verify needs only its epsilon)
     double* corrected = (opt.flags & FFCZ_WANT_CORRECTED) ? c.b<double>("corrected", N) : nullptr;
-    const bool want_edits = opt.flags & (FFCZ_WANT_EDITS | FFCZ_WANT_ARCHIVE);
+    // flags / codes to the host: asked for, or the host archive writer needs them (the device
+    // archive encodes them where they are); escapes go to the host for either archive
+    const bool device_outer = opt.zlib_level == FFCZ_OUTER_DEVICE;
+    const bool want_edits = (opt.flags & FFCZ_WANT_EDITS) ||
+                            ((opt.flags & FFCZ_WANT_ARCHIVE) && !device_outer);
+    const bool want_escapes = want_edits || (opt.flags & FFCZ_WANT_ARCHIVE);
     const long long ws = (N + 31) / 32, wf = (g.Nc() + 31) / 32;
     bool copy_pending = false;
     auto on_codes = [&](unsigned long long ns, unsigned long long nf) {
@@ -1159,7 +1177,7 @@ void finish_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& fd
     std::vector<ffcz_cuda_escape> escapes;  // only for the archive writer below
     out->escape_count = n_esc;
     dbg.mark(c, "escapes compacted");
-    if (want_edits) {
+    if (want_escapes) {
         out->escapes = static_cast<ffcz_cuda_escape*>(
             pinned().get(sizeof(ffcz_cuda_escape) * (n_esc + 1)));
         if (n_esc)
@@ -1178,6 +1196,35 @@ void finish_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& fd
     out->t_d2h_ms = std::chrono::duration<double, std::milli>(t_d2h1 - t_d2h0).count();
     dbg.mark(c, "corrected to host");
 
+    if ((opt.flags & FFCZ_WANT_ARCHIVE) && opt.zlib_level == FFCZ_OUTER_DEVICE) {
+        // every stream from the resident flags / codes; bound arrays where the caller holds them
+        DevArchiveInput ai{};
+        ai.ndim = fd.ndim;
+        for (int a = 0; a < fd.ndim; ++a) ai.dims[a] = fd.dims[a];
+        ai.precision = fd.precision;
+        ai.spatial_per_point = bd.spatial_per_point;
+        ai.spatial_global = bd.spatial_global;
+        ai.spatial_values = bd.spatial_values;
+        ai.freq_per_component = bd.freq_per_component;
+        ai.freq_global = bd.freq_global;
+        ai.freq_re = bd.freq_re;
+        ai.freq_im = bd.freq_im;
+        ai.bounds_on_device = on_dev;
+        ai.m = m;
+        ai.converged = lr.converged;
+        ai.spatial_flags = reinterpret_cast<const unsigned char*>(c.b<unsigned>("keep_s", ws));
+        ai.spatial_flag_bytes = (N + 7) / 8;
+        ai.frequency_flags = reinterpret_cast<const unsigned char*>(c.b<unsigned>("keep_f", wf));
+        ai.frequency_flag_bytes = (g.Nc() + 7) / 8;
+        ai.n_spatial = go.n_keep_s;
+        ai.n_frequency = go.n_keep_f;
+        ai.spatial_codes = c.b<int>("codes_s", N);
+        ai.frequency_codes = c.b<int>("codes_f", 2 * g.Nc());
+        ai.escapes = out->escapes;
+        ai.n_escapes = n_esc;
+        device_archive(c, ai, out);
+        return;
+    }
     if (opt.flags & FFCZ_WANT_ARCHIVE) {
         // header bounds must be the caller's full arrays (host)
         std::vector<double> e_host, re_host, im_host;
@@ -1656,7 +1703,30 @@ void gate_frames(ffcz_cuda_ctx& c, const Geometry& gf, const ffcz_field_desc& fd
         }
     }
     c.sync();
-    if (opt.flags & FFCZ_WANT_ARCHIVE) {
+    if ((opt.flags & FFCZ_WANT_ARCHIVE) && opt.zlib_level == FFCZ_OUTER_DEVICE) {
+        for (long long i = 0; i < Gc; ++i) {
+            ffcz_cuda_result* r = &out[g0 + i];
+            DevArchiveInput ai{};
+            ai.ndim = fd.ndim;
+            for (int a = 0; a < fd.ndim; ++a) ai.dims[a] = fd.dims[a];
+            ai.precision = fd.precision;
+            ai.spatial_global = hE[i];
+            ai.freq_global = hD[i];
+            ai.m = m;
+            ai.converged = hfc[i].converged;
+            ai.spatial_flags = reinterpret_cast<const unsigned char*>(keep_s) + i * (Nf / 8);
+            ai.spatial_flag_bytes = Nf / 8;
+            ai.frequency_flags = reinterpret_cast<const unsigned char*>(keep_f) + i * (Ncf / 8);
+            ai.frequency_flag_bytes = Ncf / 8;
+            ai.n_spatial = r->n_spatial;
+            ai.n_frequency = r->n_frequency;
+            ai.spatial_codes = codes_s + off_s[i];
+            ai.frequency_codes = codes_f + 2 * off_f[i];
+            ai.escapes = r->escapes;
+            ai.n_escapes = esc[i].size();
+            device_archive(c, ai, r);
+        }
+    } else if (opt.flags & FFCZ_WANT_ARCHIVE) {
         for (long long i = 0; i < Gc; ++i) {
             ffcz_cuda_result* r = &out[g0 + i];
             std::vector<ffcz_host::EscapeRec> er(esc[i].size());
@@ -1951,7 +2021,7 @@ void ffcz_cuda_default_options(ffcz_cuda_options* opt) {
     opt->flags = FFCZ_WANT_EDITS;
     opt->policy = FFCZ_POLICY_FP64;
     opt->tau_switch = 1e-4;
-    opt->zlib_level = 9;
+    opt->zlib_level = FFCZ_OUTER_DEVICE;
 }
 
 int ffcz_cuda_create(ffcz_cuda_ctx** out, int device, void* stream) {
@@ -2701,6 +2771,50 @@ int ffcz_cuda_huffman_encode(ffcz_cuda_ctx* ctx, const int32_t* codes, uint64_t 
             FFCZ_CUDA_CHECK(cudaMemcpyAsync(out, dp, l, cudaMemcpyDeviceToHost, c.st));
         c.sync();
         if (out && cap < l) throw Error(kValidation, "output buffer too small");
+    });
+}
+
+int ffcz_cuda_outer_compress(ffcz_cuda_ctx* ctx, const uint8_t* data, uint64_t n, uint8_t* out,
+                             uint64_t cap, uint64_t* len) {
+    return guarded(ctx, [&] {
+        if ((!data && n) || !len) throw Error(kValidation, "null argument");
+        ffcz_cuda_ctx& c = *ctx;
+        auto* d = c.b<unsigned char>("oc_in", std::max<uint64_t>(n, 1));
+        if (n) FFCZ_CUDA_CHECK(cudaMemcpyAsync(d, data, n, cudaMemcpyHostToDevice, c.st));
+        DevScratch ds{c.st, [&](const char* nm, size_t b) { return c.buf(nm, b); }};
+        auto* dl = c.b<unsigned long long>("oc_len", 1);
+        unsigned char* dp = nullptr;
+        deflate_device(ds, "oc_out", d, n, &dp, dl);
+        unsigned long long l = 0;
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(&l, dl, 8, cudaMemcpyDeviceToHost, c.st));
+        c.sync();
+        *len = l;
+        if (out && cap < l) throw Error(kValidation, "output buffer too small");
+        if (out) {
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(out, dp, l, cudaMemcpyDeviceToHost, c.st));
+            c.sync();
+        }
+    });
+}
+
+int ffcz_cuda_crc32c_device(ffcz_cuda_ctx* ctx, const uint8_t* data, uint64_t n, int on_device,
+                            uint32_t* crc) {
+    return guarded(ctx, [&] {
+        if ((!data && n) || !crc) throw Error(kValidation, "null argument");
+        ffcz_cuda_ctx& c = *ctx;
+        const unsigned char* d = data;
+        if (!on_device && n) {
+            auto* t = c.b<unsigned char>("crc_in", n);
+            FFCZ_CUDA_CHECK(cudaMemcpyAsync(t, data, n, cudaMemcpyHostToDevice, c.st));
+            d = t;
+        }
+        auto* acc = c.b<unsigned>("crc_acc", 1);
+        FFCZ_CUDA_CHECK(cudaMemsetAsync(acc, 0, 4, c.st));
+        crc32c_raw_device(c.st, d, n, acc);
+        unsigned raw = 0;
+        FFCZ_CUDA_CHECK(cudaMemcpyAsync(&raw, acc, 4, cudaMemcpyDeviceToHost, c.st));
+        c.sync();
+        *crc = ffcz_host::crc32c_from_raw(raw, n);
     });
 }
 

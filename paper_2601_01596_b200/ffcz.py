@@ -19,6 +19,10 @@ import numpy as np
 
 from . import _capi as capi
 
+# zlib_level value of correct(): the archive's streams are encoded on the device
+# (include/ffcz_cuda.h FFCZ_OUTER_DEVICE)
+OUTER_DEVICE = -1
+
 
 class FfczError(RuntimeError):
     pass
@@ -353,8 +357,11 @@ def _convert(holder, shape, want_archive, want_edits, want_corrected, copy):
             corrected = corrected.copy()
     data = None
     if want_archive:   # (C.string_at takes an int size: archives can exceed 2 GiB)
-        data = np.ctypeslib.as_array(res.archive, shape=(int(res.archive_len),)).tobytes() \
-            if res.archive_len else b""
+        if not res.archive_len:
+            data = b""
+        else:
+            view = np.ctypeslib.as_array(res.archive, shape=(int(res.archive_len),))
+            data = view.tobytes() if copy else view  # copy=False: a uint8 view of the pinned bytes
     timings = {k: float(getattr(res, k)) for k in ("t_feasible_ms", "t_loop_ms", "t_gate_ms",
                                                    "t_h2d_ms", "t_d2h_ms", "t_archive_ms")}
     out = CorrectionResult(data, rep, int(res.escape_count), bool(res.verify_ok),
@@ -404,7 +411,7 @@ def _field_of(original, decompressed):
 
 def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: int = 1000,
             precision: str | None = None, *, want_archive: bool = True, want_edits: bool = True,
-            want_corrected: bool = True, zlib_level: int = 9, fused: bool = True,
+            want_corrected: bool = True, zlib_level: int = OUTER_DEVICE, fused: bool = True,
             copy: bool = True, device_encode: bool = False, policy: str = "fp64",
             tau: float = 1e-4, repair_order: str = "decoder", f_update: str = "rebuild",
             ctx: Context | None = None) -> CorrectionResult:
@@ -414,8 +421,11 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
     every bound array must be a CUDA tensor too).  precision: the ScalarField precision tag
     written into the archive ("f32" / "f64"; default from the input dtype).  copy=False returns
     views of the library's pinned result buffers, valid while the returned object is alive.
-    device_encode: zigzag + canonical Huffman of the archive's index streams on the GPU (same
-    payload bytes as huffman.cpp); zlib_level then sets the host outer stage (0 = stored).
+    zlib_level: OUTER_DEVICE (default) assembles the archive from streams encoded on the GPU
+    (Huffman payloads identical to huffman.cpp, deflate blocks written on the device, readable by
+    the reference's read_archive); 0..9 runs the outer zlib stage on the host at that level (9 =
+    the reference's own bytes).  device_encode: with a host zlib level, the Huffman stage on the
+    GPU (same payload bytes).
     policy: "fp64" (reference control flow in FP64, default) or "mixed" (FP32 passes while
     max_excess / peak > tau, then FP64; iterations within +-1 of the reference).
     repair_order: "decoder" (default: repair the decoder's own view) or
@@ -454,7 +464,8 @@ def correct(original, decompressed, bounds: DualBounds, m: int = 16, max_iters: 
 
 def correct_batch(original, decompressed, bounds, m: int = 16, max_iters: int = 1000,
                   precision: str | None = None, *, lanes: int = 8, want_archive: bool = True,
-                  want_edits: bool = True, want_corrected: bool = True, zlib_level: int = 9,
+                  want_edits: bool = True, want_corrected: bool = True,
+                  zlib_level: int = OUTER_DEVICE,
                   fused: bool = True, copy: bool = True, policy: str = "fp64", tau: float = 1e-4,
                   repair_order: str = "decoder", f_update: str = "rebuild",
                   ctx: Context | None = None) -> list[CorrectionResult]:
@@ -683,6 +694,39 @@ def huffman_encode_device(codes, *, ctx: Context | None = None) -> bytes:
     _check(lib.ffcz_cuda_huffman_encode(ctx.handle, C.c_void_p(c.ctypes.data), c.size,
                                         C.c_void_p(out.ctypes.data), n.value, C.byref(n)))
     return out[: n.value].tobytes()
+
+
+def outer_compress_device(data, *, ctx: Context | None = None) -> bytes:
+    """The device outer stage (deflate.cu) on host bytes: outer_compress's framing
+    (streams.cpp:21-32: u64 raw size + zlib stream), decodable by zlib / outer_decompress."""
+    ctx = ctx or default_context()
+    lib = capi.load()
+    b = np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else \
+        np.ascontiguousarray(data, dtype=np.uint8).reshape(-1)
+    n = C.c_uint64()
+    ptr = C.c_void_p(b.ctypes.data) if b.size else None
+    _check(lib.ffcz_cuda_outer_compress(ctx.handle, ptr, b.size, None, 0, C.byref(n)))
+    out = np.zeros(max(1, n.value), dtype=np.uint8)
+    _check(lib.ffcz_cuda_outer_compress(ctx.handle, ptr, b.size, C.c_void_p(out.ctypes.data),
+                                        n.value, C.byref(n)))
+    return out[: n.value].tobytes()
+
+
+def crc32c_device(data, *, ctx: Context | None = None) -> int:
+    """CRC-32C (archive.cpp:61-71) computed on the device; data: bytes / numpy (host) or a CUDA
+    torch tensor (device)."""
+    ctx = ctx or default_context()
+    lib = capi.load()
+    out = C.c_uint32()
+    if _is_torch(data):
+        _check(lib.ffcz_cuda_crc32c_device(ctx.handle, C.c_void_p(data.data_ptr()),
+                                           data.numel() * data.element_size(), 1, C.byref(out)))
+        return out.value
+    b = np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else \
+        np.ascontiguousarray(data).view(np.uint8).reshape(-1)
+    ptr = C.c_void_p(b.ctypes.data) if b.size else None
+    _check(lib.ffcz_cuda_crc32c_device(ctx.handle, ptr, b.size, 0, C.byref(out)))
+    return out.value
 
 
 def apply_archive(archive: bytes, decompressed, *, ctx: Context | None = None):

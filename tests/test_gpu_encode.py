@@ -59,9 +59,10 @@ CASES = [c for c in cases.all_cases() if c.name in _NAMES]
 @pytest.mark.parametrize("case", CASES, ids=[c.name for c in CASES])
 def test_device_encoded_archive(ffcz, case):
     b = ffcz.DualBounds(case.E, case.Dre, case.Dim)
-    host = ffcz.correct(case.original, case.decompressed, b, case.m, case.max_iters, case.precision)
+    host = ffcz.correct(case.original, case.decompressed, b, case.m, case.max_iters, case.precision,
+                        zlib_level=9)
     dev9 = ffcz.correct(case.original, case.decompressed, b, case.m, case.max_iters,
-                        case.precision, device_encode=True)
+                        case.precision, device_encode=True, zlib_level=9)
     assert dev9.archive_bytes == host.archive_bytes
     dev0 = ffcz.correct(case.original, case.decompressed, b, case.m, case.max_iters,
                         case.precision, device_encode=True, zlib_level=0)

@@ -57,7 +57,8 @@ def _bounds(P, case):
 def test_correct_matches_reference(ffcz, case, fused):
     g = GOLD[case.name]
     o, d = _inputs(case)
-    r = ffcz.correct(o, d, _bounds(ffcz, case), case.m, case.max_iters, case.precision, fused=fused)
+    r = ffcz.correct(o, d, _bounds(ffcz, case), case.m, case.max_iters, case.precision, fused=fused,
+                     zlib_level=9)
     assert r.report.converged == g["converged"]
     assert r.report.iterations == g["iterations"]
     assert r.report.active_spatial == g["active_spatial"]
