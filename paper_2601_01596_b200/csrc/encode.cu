@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -59,82 +60,108 @@ __global__ void k_block_runs(const unsigned long long* __restrict__ ukeys, const
     }
 }
 
-// One thread per block: Huffman code lengths (huffman.cpp:74-120), canonical order and codes
-// (huffman.cpp:122-154).  Scratch per block (offset = run_start[b], d = distinct):
-//   node weight / tie / parent for 2d-1 nodes, heap of d ints, canonical order of d runs.
-__global__ void k_block_tables(const unsigned long long* __restrict__ ukeys,
-                               const int* __restrict__ counts, const long long* __restrict__ run_start,
-                               long long nb, unsigned long long* nweight, unsigned* ntie,
-                               int* nparent, int* heap, unsigned char* len_of_run,
-                               unsigned* code_of_run, int* canon) {
-    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nb;
-         b += (long long)gridDim.x * blockDim.x) {
+// Leaf keys for the per-block (weight, symbol) order: block << 33 | count << 16 | rank, rank =
+// the run's index inside its block (runs are symbol-ascending, so rank order = symbol order).
+// count <= 65536 < 2^17, rank < 2^16.
+__global__ void k_leaf_keys(const unsigned long long* __restrict__ ukeys,
+                            const int* __restrict__ counts, const long long* __restrict__ run_start,
+                            const int* nruns_p, unsigned long long* lkeys) {
+    const long long R = *nruns_p;
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < R;
+         r += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long b = ukeys[r] >> 32;
+        const unsigned long long rank = static_cast<unsigned long long>(r - run_start[b]);
+        lkeys[r] = (b << 33) | (static_cast<unsigned long long>(counts[r]) << 16) | rank;
+    }
+}
+
+// One thread per block: Huffman code lengths exactly as the reference's heap computes them
+// (huffman.cpp:74-120: repeatedly pair the two lightest subtrees, ties broken by the smallest
+// symbol in the subtree), in O(d) with two queues instead of a heap:
+//   * leaves arrive sorted by (weight, symbol) (the global leaf-key sort);
+//   * internal nodes are created with non-decreasing weights, and a new node weighs more than
+//     the minimum alive weight (w_a + w_b > w_b >= min), so when an internal node of weight w is
+//     first needed (min alive weight == w) every internal node of weight w already exists and
+//     they form one contiguous run at the queue head; that run is put in tie order once
+//     (insertion sort of node ids; runs arrive nearly sorted);
+//   * the head of each queue is then the (weight, tie)-minimum of its queue, so the pairing
+//     sequence is the heap's.
+// Then depths from parent links (parents are created after children), canonical order by a
+// counting sort on length (symbol order kept inside a length) and canonical codes
+// (huffman.cpp:122-154).  Scratch per block (offset r0 = run_start[b], d runs): iw / it / q of
+// d - 1 internal nodes, par of 2d - 1 nodes.
+__device__ void block_table_global(long long b, const unsigned long long* __restrict__ lkeys,
+                                   const long long* __restrict__ run_start, unsigned* iw,
+                                   unsigned* it, int* q, int* par, unsigned char* len_of_run,
+                                   unsigned* code_of_run, int* canon) {
+    {
         const long long r0 = run_start[b];
         const int d = static_cast<int>(run_start[b + 1] - r0);
-        unsigned long long* W = nweight + 2 * r0;
-        unsigned* T = ntie + 2 * r0;
-        int* par = nparent + 2 * r0;
-        int* hp = heap + r0;
         unsigned char* L = len_of_run + r0;
         if (d == 1) {
             L[0] = 1;  // huffman.cpp:76
         } else {
-            auto less = [&](int a, int c) {  // min-heap on (weight, tie)
-                return W[a] != W[c] ? W[a] < W[c] : T[a] < T[c];
-            };
-            auto sift_down = [&](int i, int n) {
-                for (;;) {
-                    int l = 2 * i + 1, s = i;
-                    if (l < n && less(hp[l], hp[s])) s = l;
-                    if (l + 1 < n && less(hp[l + 1], hp[s])) s = l + 1;
-                    if (s == i) return;
-                    const int t = hp[i];
-                    hp[i] = hp[s];
-                    hp[s] = t;
-                    i = s;
+            const unsigned long long* LK = lkeys + r0;
+            unsigned* W = iw + r0;
+            unsigned* T = it + r0;
+            int* Q = q + r0;
+            int* P = par + 2 * r0;  // node ids: leaf = rank (0..d-1), internal k = d + k
+            int li = 0, qh = 0, qn = 0, sorted_to = 0;
+            auto pop = [&](unsigned& w, unsigned& t, int& id) {
+                const bool have_l = li < d;
+                if (qh < qn) {
+                    const unsigned wi = W[Q[qh]];
+                    const unsigned lw = have_l ? static_cast<unsigned>((LK[li] >> 16) & 0x1FFFFu) : 0;
+                    if ((!have_l || lw >= wi) && sorted_to <= qh) {
+                        int e = qh + 1;
+                        while (e < qn && W[Q[e]] == wi) ++e;
+                        for (int i = qh + 1; i < e; ++i) {  // insertion sort by tie
+                            const int v = Q[i];
+                            const unsigned tv = T[v];
+                            int j = i - 1;
+                            while (j >= qh && T[Q[j]] > tv) {
+                                Q[j + 1] = Q[j];
+                                --j;
+                            }
+                            Q[j + 1] = v;
+                        }
+                        sorted_to = e;
+                    }
+                    const int k = Q[qh];
+                    bool take_internal = !have_l;
+                    if (have_l) {
+                        const unsigned lt = static_cast<unsigned>(LK[li] & 0xFFFFu);
+                        take_internal = wi < lw || (wi == lw && T[k] < lt);
+                    }
+                    if (take_internal) {
+                        w = wi;
+                        t = T[k];
+                        id = d + k;
+                        ++qh;
+                        return;
+                    }
                 }
+                w = static_cast<unsigned>((LK[li] >> 16) & 0x1FFFFu);
+                t = static_cast<unsigned>(LK[li] & 0xFFFFu);
+                id = static_cast<int>(t);
+                ++li;
             };
-            auto sift_up = [&](int i) {
-                while (i > 0) {
-                    const int p = (i - 1) >> 1;
-                    if (!less(hp[i], hp[p])) return;
-                    const int t = hp[i];
-                    hp[i] = hp[p];
-                    hp[p] = t;
-                    i = p;
-                }
-            };
-            for (int i = 0; i < d; ++i) {
-                W[i] = static_cast<unsigned long long>(counts[r0 + i]);
-                T[i] = static_cast<unsigned>(ukeys[r0 + i] & 0xffffffffull);
-                par[i] = -1;
-                hp[i] = i;
+            for (int m = 0; m < d - 1; ++m) {
+                unsigned wa, ta, wb, tb;
+                int ia, ib;
+                pop(wa, ta, ia);
+                pop(wb, tb, ib);
+                W[qn] = wa + wb;
+                T[qn] = ta < tb ? ta : tb;
+                Q[qn] = qn;
+                P[ia] = d + qn;
+                P[ib] = d + qn;
+                ++qn;
             }
-            for (int i = d / 2 - 1; i >= 0; --i) sift_down(i, d);
-            int n = d, next = d;
-            while (n > 1) {
-                const int a = hp[0];
-                hp[0] = hp[--n];
-                sift_down(0, n);
-                const int c = hp[0];
-                W[next] = W[a] + W[c];
-                T[next] = T[a] < T[c] ? T[a] : T[c];
-                par[next] = -1;
-                par[a] = next;
-                par[c] = next;
-                hp[0] = next;
-                sift_down(0, n);
-                ++next;
-            }
-            // depths: the root is the last node; parents are created after their children
-            // (reuse W of internal nodes as the depth scratch)
-            W[next - 1] = 0;
-            for (int i = next - 2; i >= 0; --i) {
-                const unsigned long long dep = W[par[i]] + 1;
-                if (i < d) L[i] = static_cast<unsigned char>(dep);
-                else W[i] = dep;
-            }
-            (void)sift_up;
+            // depths: root = internal qn-1; W reused as the depth of internal nodes
+            W[qn - 1] = 0;
+            for (int k = qn - 2; k >= 0; --k) W[k] = W[P[d + k] - d] + 1;
+            for (int i = 0; i < d; ++i) L[i] = static_cast<unsigned char>(W[P[i] - d] + 1);
         }
         // canonical order: stable counting sort of the (symbol-ascending) runs by length
         int cnt[34];
@@ -156,6 +183,208 @@ __global__ void k_block_tables(const unsigned long long* __restrict__ ukeys,
             code_of_run[r0 + i] = code++;
             prev = L[i];
         }
+    }
+}
+
+
+// One CTA per block (the common path): the same pairing sequence, produced in parallel batches.
+// With w0 the smallest alive weight, every node created from now on weighs >= 2 w0, so all
+// alive items lighter than 2 w0 are popped before any new node, in the merged (weight, tie)
+// order of the two queues, and they pair up consecutively.  A batch therefore takes the first
+// B such items (B even, <= kBatch; B = 2 when fewer exist: the two smallest always pair),
+// finds each one's place by a merge-path search over the two queue heads staged in shared
+// memory, and creates B/2 internal nodes at once (one thread per pair).  New nodes keep the
+// internal queue in non-decreasing weight; its (weight, tie) order inside a batch's prefix is
+// checked, and a block whose internal queue is ever out of tie order falls back to
+// block_table_global (never observed; tests force that path).  An all-distinct 65,536-symbol
+// block takes ~260 batches instead of 65,535 dependent steps.
+// Depths then come from pointer jumping over the parent links (ping-pong buffers in global
+// memory), the canonical order from a stable counting sort by length (per-thread chunks,
+// per-length scans) and the canonical codes from first_code[len] + rank in the length.
+constexpr int kBatch = 512;
+constexpr int kTabThreads = 256;
+
+__global__ void __launch_bounds__(kTabThreads)
+k_block_tables_batch(const unsigned long long* __restrict__ lkeys,
+                     const long long* __restrict__ run_start, long long nb, unsigned* iw,
+                     unsigned* it, int* q, int* par, int* pj, unsigned char* len_of_run,
+                     unsigned* code_of_run, int* canon, int mode) {
+    __shared__ unsigned long long sl[kBatch], si[kBatch];  // (weight << 32 | tie) of the heads
+    __shared__ int cntbuf[34 * kTabThreads];
+    __shared__ int s_li, s_qh, s_qn, s_fallback, s_qnf, s_used;
+    __shared__ int first_code[34], len_start[34], len_total[34];
+    const int tid = threadIdx.x;
+    for (long long b = blockIdx.x; b < nb; b += gridDim.x) {
+        const long long r0 = run_start[b];
+        const int d = static_cast<int>(run_start[b + 1] - r0);
+        unsigned char* L = len_of_run + r0;
+        if (d == 1) {
+            if (tid == 0) {
+                L[0] = 1;  // huffman.cpp:76
+                canon[r0] = 0;
+                code_of_run[r0] = 0;
+            }
+            __syncthreads();
+            continue;
+        }
+        int* P = par + 2 * r0;  // node ids: leaf = rank, internal k = d + k
+        unsigned* W = iw + r0;  // internal nodes: weight, tie
+        unsigned* T = it + r0;
+        const unsigned long long* LK = lkeys + r0;
+        if (tid == 0) {
+            s_li = 0;
+            s_qh = 0;
+            s_qn = 0;
+            s_fallback = mode == 2;
+        }
+        __syncthreads();
+        for (;;) {
+            const int li = s_li, qh = s_qh, qn = s_qn;
+            if ((d - li) + (qn - qh) <= 1 || s_fallback) break;
+            const int nL = min(kBatch, d - li), nI = min(kBatch, qn - qh);
+            for (int t = tid; t < kBatch; t += kTabThreads) {
+                if (t < nL) {
+                    const unsigned long long k = LK[li + t];
+                    sl[t] = (((k >> 16) & 0x1FFFFull) << 32) | (k & 0xFFFFull);
+                }
+                if (t < nI) si[t] = (static_cast<unsigned long long>(W[qh + t]) << 32) | T[qh + t];
+            }
+            __syncthreads();
+            const unsigned long long w0 =
+                min(nL ? sl[0] >> 32 : ~0ull, nI ? si[0] >> 32 : ~0ull);
+            const unsigned long long lim = (2 * w0) << 32;  // keys below: weight < 2 w0
+            auto count_below = [&](const unsigned long long* a, int n) {
+                int lo = 0, hi = n;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (a[mid] < lim) lo = mid + 1;
+                    else hi = mid;
+                }
+                return lo;
+            };
+            const int n_l = count_below(sl, nL), n_i = count_below(si, nI);
+            int B = min(n_l + n_i, kBatch) & ~1;
+            if (B < 2) B = 2;
+            // the internal heads this batch may consume must be in (weight, tie) order
+            bool bad = false;
+            for (int t = tid + 1; t < min(B + 1, nI); t += kTabThreads)
+                if (!(si[t - 1] < si[t])) bad = true;
+            if (__syncthreads_or(bad)) {
+                if (tid == 0) s_fallback = 1;
+                __syncthreads();
+                break;
+            }
+            // merge path: number of leaves among the first p merged items
+            auto split = [&](int p) {
+                int lo = max(0, p - nI), hi = min(p, nL);
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (sl[mid] < si[p - mid - 1]) lo = mid + 1;
+                    else hi = mid;
+                }
+                return lo;
+            };
+            auto item = [&](int p, unsigned long long& key, int& id) {
+                const int i = split(p);
+                const bool leaf = i < nL && (p - i >= nI || sl[i] < si[p - i]);
+                if (leaf) {
+                    key = sl[i];
+                    id = static_cast<int>(key & 0xFFFFu);
+                } else {
+                    key = si[p - i];
+                    id = d + qh + (p - i);
+                }
+            };
+            if (tid < B / 2) {
+                unsigned long long ka, kb;
+                int ia, ib;
+                item(2 * tid, ka, ia);
+                item(2 * tid + 1, kb, ib);
+                const int k = qn + tid;
+                W[k] = static_cast<unsigned>((ka >> 32) + (kb >> 32));
+                T[k] = static_cast<unsigned>(min(ka & 0xFFFFFFFFull, kb & 0xFFFFFFFFull));
+                P[ia] = d + k;
+                P[ib] = d + k;
+            }
+            if (tid == 0) s_used = split(B);
+            __syncthreads();
+            if (tid == 0) {
+                s_li = li + s_used;
+                s_qh = qh + (B - s_used);
+                s_qn = qn + B / 2;
+            }
+            __syncthreads();
+        }
+        if (tid == 0) s_qnf = s_qn;
+        __syncthreads();
+        if (s_fallback) {
+            if (tid == 0)
+                block_table_global(b, lkeys, run_start, iw, it, q, par, len_of_run, code_of_run,
+                                   canon);
+            __syncthreads();
+            continue;
+        }
+        const int s_qn_final = s_qnf;
+    // depths of the internal nodes by pointer jumping (root = qn - 1)
+        const int qn = s_qn_final;
+        int* dep0 = reinterpret_cast<int*>(iw + r0);
+        int* anc0 = reinterpret_cast<int*>(it + r0);
+        int* dep1 = q + r0;
+        int* anc1 = pj + r0;
+        for (int k = tid; k < qn; k += kTabThreads) {
+            const bool root = k == qn - 1;
+            dep0[k] = root ? 0 : 1;
+            anc0[k] = root ? k : P[d + k] - d;
+        }
+        __syncthreads();
+        for (int round = 0; round < 6; ++round) {  // depth <= 32 < 2^6
+            for (int k = tid; k < qn; k += kTabThreads) {
+                const int a = anc0[k];
+                dep1[k] = dep0[k] + (a != k ? dep0[a] : 0);
+                anc1[k] = anc0[a];
+            }
+            __syncthreads();
+            int* t0 = dep0; dep0 = dep1; dep1 = t0;
+            int* t1 = anc0; anc0 = anc1; anc1 = t1;
+        }
+        for (int i = tid; i < d; i += kTabThreads) L[i] = static_cast<unsigned char>(dep0[P[i] - d] + 1);
+        __syncthreads();
+        // canonical order: stable counting sort of the symbol-ascending runs by length
+        int* cnt = cntbuf;  // [34][kTabThreads]
+        const int chunk = (d + kTabThreads - 1) / kTabThreads;
+        const int i0 = tid * chunk, i1 = min(d, i0 + chunk);
+        for (int l = 0; l < 34; ++l) cnt[l * kTabThreads + tid] = 0;
+        for (int i = i0; i < i1; ++i) ++cnt[L[i] * kTabThreads + tid];
+        __syncthreads();
+        if (tid < 34) {  // per length: exclusive scan over threads, total
+            int acc = 0;
+            for (int t = 0; t < kTabThreads; ++t) {
+                const int v = cnt[tid * kTabThreads + t];
+                cnt[tid * kTabThreads + t] = acc;
+                acc += v;
+            }
+            len_total[tid] = acc;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int acc = 0;
+            unsigned code = 0;
+            for (int l = 0; l < 34; ++l) {
+                len_start[l] = acc;
+                acc += len_total[l];
+                first_code[l] = static_cast<int>(code);  // huffman.cpp:128-138
+                code = (code + (l ? len_total[l] : 0)) << 1;
+            }
+        }
+        __syncthreads();
+        int* cn = canon + r0;
+        for (int i = i0; i < i1; ++i) {
+            const int l = L[i];
+            const int rank = cnt[l * kTabThreads + tid]++;
+            cn[len_start[l] + rank] = i;
+            code_of_run[r0 + i] = static_cast<unsigned>(first_code[l]) + static_cast<unsigned>(rank);
+        }
+        __syncthreads();
     }
 }
 
@@ -268,6 +497,14 @@ __global__ void k_put_total(unsigned char* out, unsigned long long n) {
     if (threadIdx.x == 0 && blockIdx.x == 0) put_u64(out, n);
 }
 
+// FFCZ_HUFFMAN_TABLES=global: every block through block_table_global (test hook for the
+// fallback path)
+int table_mode() {
+    const char* e = std::getenv("FFCZ_HUFFMAN_TABLES");
+    if (!e) return 0;
+    return std::strcmp(e, "global") == 0 ? 2 : 0;
+}
+
 template <class F>
 void cub_call(DevScratch& s, const char* name, F&& f) {
     size_t bytes = 0;
@@ -317,15 +554,32 @@ unsigned long long huffman_encode_device(DevScratch& s, const int* codes, unsign
     const long long R = h_nruns;
     auto* run_start = static_cast<long long*>(s.get("huf_run_start", 8 * (nb + 1)));
     k_block_runs<<<grid_n(nb + 1), 256, 0, st>>>(ukeys, nruns, nb, run_start);
-    auto* nweight = static_cast<unsigned long long*>(s.get("huf_nw", 16 * R));
-    auto* ntie = static_cast<unsigned*>(s.get("huf_nt", 8 * R));
-    auto* nparent = static_cast<int*>(s.get("huf_np", 8 * R));
-    auto* heap = static_cast<int*>(s.get("huf_heap", 4 * R));
+    // leaves of every block in (weight, symbol) order: one radix sort of the run keys
+    auto* lkeys = static_cast<unsigned long long*>(s.get("huf_lkeys", 8 * R));
+    auto* lkeys_s = static_cast<unsigned long long*>(s.get("huf_lkeys_s", 8 * R));
+    k_leaf_keys<<<grid_n(R), 256, 0, st>>>(ukeys, counts, run_start, nruns, lkeys);
+    FFCZ_LAUNCH_CHECK();
+    int lend = 33;
+    while ((1ll << (lend - 33)) < nb) ++lend;
+    cub_call(s, "huf_tmp_sort2", [&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortKeys(t, b, lkeys, lkeys_s, static_cast<int64_t>(R), 0,
+                                              lend, st);
+    });
+    auto* iw = static_cast<unsigned*>(s.get("huf_iw", 4 * R));
+    auto* it = static_cast<unsigned*>(s.get("huf_it", 4 * R));
+    auto* iq = static_cast<int*>(s.get("huf_iq", 4 * R));
+    auto* par = static_cast<int*>(s.get("huf_par", 8 * R));
     auto* len_of_run = static_cast<unsigned char*>(s.get("huf_len", R));
     auto* code_of_run = static_cast<unsigned*>(s.get("huf_code", 4 * R));
     auto* canon = static_cast<int*>(s.get("huf_canon", 4 * R));
-    k_block_tables<<<static_cast<unsigned>((nb + 63) / 64), 64, 0, st>>>(
-        ukeys, counts, run_start, nb, nweight, ntie, nparent, heap, len_of_run, code_of_run, canon);
+    auto* pj = static_cast<int*>(s.get("huf_pj", 4 * R));
+    int per_sm = 0;
+    FFCZ_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_tables_batch,
+                                                                  kTabThreads, 0));
+    const long long grid = std::min<long long>(nb, 148ll * std::max(1, per_sm));
+    k_block_tables_batch<<<static_cast<unsigned>(grid), kTabThreads, 0, st>>>(
+        lkeys_s, run_start, nb, iw, it, iq, par, pj, len_of_run, code_of_run, canon,
+        table_mode());
     FFCZ_LAUNCH_CHECK();
     auto* sym_code = static_cast<unsigned*>(s.get("huf_sym_code", 4 * n));
     auto* sym_len = static_cast<unsigned long long*>(s.get("huf_sym_len", 8 * n));

@@ -461,6 +461,7 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
     const double dlanes = bw.fb.re ? (bw.fb.im == bw.fb.re ? 1.0 : 2.0) : 0.0;
     const double check_bytes = pass_bytes + 8.0 * g.Nc() * dlanes;
     const double fused_bytes = pass_bytes + 8.0 * g.N + (bw.sb.v ? 8.0 * g.N : 0.0);
+    int nbody = 0;  // bodies enqueued: body k (from 0) is clip pass k + 1 unless gated
     auto body = [&]() {
         if (fused) {
             {
@@ -469,7 +470,10 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
             }
             k_decide<<<1, 1, 0, st>>>(c.ctl);                                              // K4
             {
-                Prof p(c, kColClipInv, check_bytes);
+                // clip pass 1 writes F densely (16 N_c); later passes write the 1-B clip map
+                // where a clamp moved a component (counted as N_c: an upper bound)
+                Prof p(c, kColClipInv, check_bytes + (nbody == 0 ? 16.0 * g.Nc() : 0.0) +
+                                           (moved && nbody > 0 ? 1.0 * g.Nc() : 0.0));
                 plan.col(za, +1, spec, spec, gate,
                          HookFClip<double>{bw.fb, fscale, F, c.ctl, moved}, st);          // K3b
             }
@@ -493,6 +497,7 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
                 plan.col(mid, -1, spec, spec, gate, HookNone{}, st);
             }
             c.launches += three_d ? 7 : 5;
+            ++nbody;
         } else {
             plan.r2c(eps, spec, gate, st);
             k_freduce<<<grid_for(g.Nc()), 256, 0, st>>>(spec, hg, bw.fb, fscale, c.ctl, gate);
@@ -785,7 +790,6 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
             }
             c.launches += three_d ? 5 : 3;
         };
-        const double in_bytes = 2.0 * sizeof(TI) * N + 16.0 * N;  // orig, dec, spat_cur, eps_tilde
         auto forward_row_mid = [&](const double* x) {
             {
                 Prof p(c, kRowR2C, 8.0 * g.N + 16.0 * Nc);
@@ -813,8 +817,11 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
                                          c.ctl};
                 hk.sc_zero = sc_zero;
                 hk.dview = dview;
-                inverse_and_row(hk, 16.0 * Nc + in_bytes - (sc_zero ? 8.0 * N : 0.0) +
-                                        (dview ? 16.0 : 24.0) * N);
+                // half spectrum in, orig + dec, spat_cur (unless still zero), the checked view
+                // out (the R2C's input), eps_v (reference order), corrected, per-point E
+                inverse_and_row(hk, 16.0 * Nc + 2.0 * sizeof(TI) * N + (sc_zero ? 0.0 : 8.0 * N) +
+                                        8.0 * N + (dview ? 0.0 : 8.0 * N) +
+                                        (corrected ? 8.0 * N : 0.0) + (bo.sb.v ? 8.0 * N : 0.0));
                 {
                     Prof p(c, kColFwdCheck, pass);
                     plan.col(za, -1, work, work, nullptr, HookMarkViol{bo.fb, viol, c.ctl}, st);
@@ -850,8 +857,10 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
         if (!verified) {
             // apply_edits + verify_bounds on the decoder view (pipeline.cpp:174-176)
             FFCZ_CUDA_CHECK(cudaMemsetAsync(&c.ctl->vs_bits, 0, 2 * sizeof(unsigned long long), st));
+            // half spectrum in, orig + dec + spat_cur, the view out, corrected, per-point E
             inverse_and_row(HookVerifyS<TI>{orig, dec, spat_cur, corrected, bo.sb, c.ctl},
-                            16.0 * Nc + in_bytes + 8.0 * N);
+                            16.0 * Nc + 2.0 * sizeof(TI) * N + 16.0 * N +
+                                (corrected ? 8.0 * N : 0.0) + (bo.sb.v ? 8.0 * N : 0.0));
             {
                 Prof p(c, kColFwdCheck, 16.0 * Nc);
                 plan.col(za, -1, work, work, nullptr, HookVerifyF{bo.fb, c.ctl}, st);

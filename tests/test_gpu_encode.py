@@ -51,6 +51,17 @@ def test_huffman_payload_matches_reference(ffcz, kind, n):
     assert np.array_equal(O.unzigzag(O.huffman_decode(got)).astype(np.int32), c)
 
 
+@pytest.mark.parametrize("mode", ["global"])
+@pytest.mark.parametrize("kind,n", [("laplace", 300001), ("wide", 70000), ("fib", 50000),
+                                    ("two", 140000)])
+def test_huffman_table_paths(ffcz, monkeypatch, mode, kind, n):
+    """The global-memory fallback of the code-length kernel (encode.cu block_table_global)
+    gives the reference's payload too."""
+    monkeypatch.setenv("FFCZ_HUFFMAN_TABLES", mode)
+    c = _codes(kind, n, 99 + n)
+    assert ffcz.ffcz.huffman_encode_device(c) == O.huffman_encode(O.zigzag(c))
+
+
 _NAMES = ("config1_c1.0", "config1_c0.4", "config2_rho32", "config3_frame256", "config4_comb32",
           "m8_32cube", "accept_05", "odd_12x10x9")
 CASES = [c for c in cases.all_cases() if c.name in _NAMES]
