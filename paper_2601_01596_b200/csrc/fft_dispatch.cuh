@@ -10,6 +10,7 @@
 
 #include "fft_mixed.cuh"
 #include "fft_plan.cuh"
+#include "fft_large.cuh"
 
 namespace ffcz_gpu {
 
@@ -422,9 +423,16 @@ void launch_col(long long L, int dir, const cplx<T>* src, cplx<T>* dst, long lon
         }
         // direct O(L) pass: tile L x B columns in smem
         const size_t per_col = sizeof(cplx<T>) * L;
-        if (per_col > 96 * 1024)
-            throw Error(kUnsupported, "axis extent " + std::to_string(L) +
-                                          " is neither a power of two <= 4096 nor <= 6144");
+        if (per_col > 96 * 1024) {  // longer than shared memory holds: global-memory passes
+            LineAddr a;
+            a.compact = false;
+            a.row_stride = row_stride;
+            a.plane_stride = plane_stride;
+            a.ncols = ncols;
+            a.nl = static_cast<long long>(ncols) * nplanes;
+            large_lines<T>(L, dir, src, a, dst, a, a.nl, tw, gate, st);
+            return;
+        }
         int B = static_cast<int>(std::max<long long>(1, std::min<long long>(48 * 1024 / per_col, 32)));
         B = std::min(B, detail::pow2_ceil(ncols));
         const size_t smem = per_col * B;
@@ -462,7 +470,10 @@ void launch_row_r2c(long long n2, const T* in, long long in_stride, cplx<T>* out
         return;
     }
     const size_t smem = sizeof(T) * n2;
-    if (smem > 96 * 1024) throw Error(kUnsupported, "last-axis extent too large for direct R2C");
+    if (smem > 96 * 1024) {  // longer than shared memory holds: global-memory passes
+        large_row_r2c<T>(n2, in, in_stride, out, out_stride, nrows, tw, gate, st);
+        return;
+    }
     detail::set_smem(k_row_r2c_direct<T>, smem);
     k_row_r2c_direct<T><<<static_cast<unsigned>(nrows), 256, smem, st>>>(
         in, in_stride, out, out_stride, static_cast<int>(n2), tw.table_for(n2), gate);
@@ -542,7 +553,10 @@ void launch_row_c2r(long long n2, const cplx<T>* in, long long in_stride, T* out
         return;
     }
     const size_t smem = sizeof(cplx<T>) * (n2 / 2 + 1);
-    if (smem > 96 * 1024) throw Error(kUnsupported, "last-axis extent too large for direct C2R");
+    if (smem > 96 * 1024) {  // longer than shared memory holds: global-memory passes
+        large_row_c2r<T>(n2, in, in_stride, out, out_stride, nrows, scale, tw, gate, st);
+        return;
+    }
     detail::set_smem(k_row_c2r_direct<T>, smem);
     k_row_c2r_direct<T><<<static_cast<unsigned>(nrows), 256, smem, st>>>(
         in, in_stride, out, out_stride, static_cast<int>(n2), tw.table_for(n2), scale, gate);
