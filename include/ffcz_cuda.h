@@ -205,7 +205,11 @@ int ffcz_cuda_correct_batch(ffcz_cuda_ctx* ctx, const ffcz_field_desc* frame, ui
  * d0 x d1 x n2 FP64 (inputs: `in_dtype`), half spectra d0 x d1 x P complex FP64 with
  * P = round_up(n2/2+1, 16) (ffcz_cuda_slab_pitch), bitmaps uint32 LSB-first.  Bounds are global
  * (E, Delta); `fscale` = 1 - 2^-m for the working bounds.  Ops that reduce synchronise the stream
- * and return their scalars in out[0..3]. */
+ * and return their scalars in out[0..3] -- except in the device-resident loop: FWD_LOCAL,
+ * COL0_CHECK, COL0_CLIP_INV and INV_SCLIP take the loop's int32 done flag in p9 (they return at
+ * once when it is set) and COL0_CHECK with p1 != NULL writes (peak, excess) to the device doubles
+ * p1 instead of returning them, so the orchestrator all-reduces and decides (FFCZ_SLAB_DECIDE)
+ * without a host sync per iteration. */
 typedef enum ffcz_cuda_slab_opcode {
     FFCZ_SLAB_EPS0 = 0,           /* p0 orig, p1 dec, p2 eps -> out: first bad index (E(1+2^-20)),
                                      first bad index (working E * (1+slack), slack = delta), -1 none */
@@ -231,10 +235,13 @@ typedef enum ffcz_cuda_slab_opcode {
                                      p5 corrected -> out: spatial excess */
     FFCZ_SLAB_RESIDUAL_S = 11,    /* p0 eps -> out: max(|eps| - e*fscale, 0) */
     FFCZ_SLAB_EPS0_PLUS_S = 12,   /* p0 orig, p1 dec, p2 S -> p3 (dec - orig) + S */
-    FFCZ_SLAB_GATE = 13           /* p0 S, p1 F (natural half) -> p2 spat_cur, p3 freq_cur,
+    FFCZ_SLAB_GATE = 13,          /* p0 S, p1 F (natural half) -> p2 spat_cur, p3 freq_cur,
                                      p4 keep_s, p5 esc_s, p6 keep_f, p7 esc_f bitmaps, p8 codes_s,
                                      p9 codes_f (editset.cpp:43-133, pipeline.cpp:57-106)
                                      -> out: active_s, active_f, kept_s, kept_f */
+    FFCZ_SLAB_DECIDE = 14         /* device-resident loop: p0 all-reduced (peak, excess) doubles,
+                                     p1 state (passes, residual_f) doubles, p9 int32 (done,
+                                     converged); max_iters in n_total (projection.cpp:106-116) */
 } ffcz_cuda_slab_opcode;
 
 typedef struct ffcz_cuda_slab_op {

@@ -2329,6 +2329,34 @@ int ffcz_cuda_apply_archive(ffcz_cuda_ctx* ctx, const uint8_t* archive, uint64_t
 uint64_t ffcz_cuda_slab_pitch(uint64_t n2) { return round_up(n2 / 2 + 1, kPitchAlign); }
 
 // One per-rank device step of the slab-decomposed correction (paper_2601_01596_b200/slab.py).
+namespace {
+// device-resident slab loop (slab.py): this rank's (peak, excess) of the check pass, unless the
+// loop is already done
+__global__ void k_slab_export(const Ctl* __restrict__ ctl, double* red, const int* gate) {
+    if (gated(gate)) return;
+    red[0] = bitsd(ctl->peak_bits);
+    red[1] = bitsd(ctl->exc_bits);
+}
+// the decision of alternating_projection (projection.cpp:106-116) on the all-reduced
+// (peak, excess): state = (passes, residual_f), gate = (done, converged)
+__global__ void k_slab_decide(const double* __restrict__ red, double* state, int* gate,
+                              unsigned long long max_iters) {
+    if (gate[0]) return;
+    const double peak = red[0], ex = red[1];
+    if (!(ex > 1e-11 * peak)) {                                   // projection.cpp:40,106-111
+        gate[1] = 1;
+        state[1] = 0.0;
+        gate[0] = 1;
+    } else if (state[0] >= static_cast<double>(max_iters)) {     // :112-116
+        gate[1] = 0;
+        state[1] = ex;
+        gate[0] = 1;
+    } else {
+        state[0] += 1.0;
+    }
+}
+}  // namespace
+
 int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4]) {
     return guarded(ctx, [&] {
         if (!op) throw Error(kValidation, "null op");
@@ -2348,6 +2376,10 @@ int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4
         auto ww = [&](int i) { return static_cast<unsigned*>(op->p[i]); };
         double o4[4] = {0, 0, 0, 0};
         auto reset_ctl = [&] { k_ctl_init<<<1, 1, 0, st>>>(c.ctl, 1); FFCZ_LAUNCH_CHECK(); };
+        // loop ops of the device-resident slab loop: p9 = the loop's done flag (NULL: ungated)
+        const bool loop_op = op->op == FFCZ_SLAB_FWD_LOCAL || op->op == FFCZ_SLAB_COL0_CHECK ||
+                             op->op == FFCZ_SLAB_COL0_CLIP_INV || op->op == FFCZ_SLAB_INV_SCLIP;
+        const int* gate = loop_op ? static_cast<const int*>(P(9)) : nullptr;
         const bool f32 = op->in_dtype == FFCZ_F32;
         switch (op->op) {
         case FFCZ_SLAB_EPS0: {
@@ -2365,21 +2397,30 @@ int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4
             break;
         }
         case FFCZ_SLAB_FWD_LOCAL:
-            launch_row_r2c<double>(g.n2, dd(0), g.n2, d2(1), g.P, g.rows, c.tw64, nullptr, st);
-            plan.col(1, -1, d2(1), d2(1), nullptr, HookNone{}, st);
+            launch_row_r2c<double>(g.n2, dd(0), g.n2, d2(1), g.P, g.rows, c.tw64, gate, st);
+            plan.col(1, -1, d2(1), d2(1), gate, HookNone{}, st);
             break;
         case FFCZ_SLAB_COL0_CHECK: {
             reset_ctl();
-            plan.col(0, -1, d2(0), d2(0), nullptr, HookFReduce{fb, op->fscale, c.ctl}, st);
+            plan.col(0, -1, d2(0), d2(0), gate, HookFReduce{fb, op->fscale, c.ctl}, st);
+            if (P(1)) {  // device-resident loop: (peak, excess) stay on the device
+                k_slab_export<<<1, 1, 0, st>>>(c.ctl, dd(1), gate);
+                FFCZ_LAUNCH_CHECK();
+                break;
+            }
             const Ctl h = c.read_ctl();
             o4[0] = bitsd_host(h.peak_bits);
             o4[1] = bitsd_host(h.exc_bits);
             break;
         }
+        case FFCZ_SLAB_DECIDE:
+            k_slab_decide<<<1, 1, 0, st>>>(dd(0), dd(1), static_cast<int*>(P(9)), op->n_total);
+            FFCZ_LAUNCH_CHECK();
+            break;
         case FFCZ_SLAB_COL0_CLIP_INV: {
             HookFClip<double> hk{fb, op->fscale, d2(1), nullptr, static_cast<unsigned char*>(P(2))};
             hk.first = op->first != 0;
-            plan.col(0, +1, d2(0), d2(0), nullptr, hk, st);
+            plan.col(0, +1, d2(0), d2(0), gate, hk, st);
             break;
         }
         case FFCZ_SLAB_COL0_PLAIN:
@@ -2403,11 +2444,11 @@ int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4
             break;
         }
         case FFCZ_SLAB_INV_SCLIP: {
-            plan.col(1, +1, d2(0), d2(0), nullptr, HookNone{}, st);
+            plan.col(1, +1, d2(0), d2(0), gate, HookNone{}, st);
             HookSClip<double> hk{sb, op->fscale, dd(2), nullptr, nullptr};
             hk.first = op->first != 0;
             launch_row_c2r_hook<double>(g.n2, d2(0), g.P, dd(1), g.n2, g.rows, invN, c.tw64,
-                                        nullptr, hk, st);
+                                        gate, hk, st);
             break;
         }
         case FFCZ_SLAB_INV_REPAIR_VERIFY:

@@ -76,6 +76,10 @@ class Comm:
                 self.dist.all_reduce(t, op=op, group=self.group)
         return t
 
+    def max_f64_(self, t):
+        """In-place all-reduce(max) of a float64 device tensor, no host sync (stream ordered)."""
+        return self._reduce(t, self.dist.ReduceOp.MAX)
+
     def max_f64(self, values, device):
         import torch
         t = torch.tensor(list(values), dtype=torch.float64, device=device)
@@ -211,22 +215,37 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E: float, Delta: float, m: in
     moved_B = be.zeros_moved((n0, c1))
     A = be.zeros_half((c0, n1))
     be.fwd_local(eps, A, N)
-    passes, converged, residual_f = 0, False, 0.0
-    while True:
+    ls = be.loop_state()
+    gate = ls["gate"]
+    B = None
+
+    def body(k):
+        """One pass of projection.cpp:96-126 with the decision on the device: check, all-reduce
+        of (peak, excess), decide (:106-116), clip + inverse, forward.  Every device op returns at
+        once when the loop is done; a pass enqueued after that only round-trips the transposes,
+        which leaves B (= delta_star) unchanged.  Pass k (from 0) is clip pass k + 1."""
+        nonlocal A, B
         B = _transpose_ab(be, comm, A, n0, c0, c1)
-        peak, exc = be.col0_check(B, Delta * fw)            # FFT axis 0 + check (in place)
-        peak, exc = comm.max_f64([peak, exc], dev)
-        if not exc > KMAX_ITER_TOL * peak:                  # projection.cpp:106-111
-            converged = True
-            break
-        if passes >= max_iters:                             # :112-116
-            residual_f = exc
-            break
-        passes += 1
-        be.col0_clip_inv(B, Delta * fw, F_B, moved_B, passes == 1)   # :117-119, inverse axis 0
+        be.col0_check_dev(B, Delta * fw, ls["red"], gate)   # FFT axis 0 + check (in place)
+        comm.max_f64_(ls["red"])
+        be.decide(ls["red"], ls["state"], gate, max_iters)
+        be.col0_clip_inv(B, Delta * fw, F_B, moved_B, k == 0, gate=gate)   # :117-119, axis 0
         A = _transpose_ba(be, comm, B, n1, c0, c1)
-        be.inv_local_sclip(A, eps, N, E * fw, S, passes == 1)     # inverse axis 1, C2R, :121-124
-        be.fwd_local(eps, A, N)
+        be.inv_local_sclip(A, eps, N, E * fw, S, k == 0, gate=gate)   # axis 1, C2R, :121-124
+        be.fwd_local(eps, A, N, gate=gate)
+
+    # one pass queued behind the one being decided: the host waits on an event per pass, never
+    # on a value, and the device never idles for the host
+    k = 0
+    body(k)
+    snaps = [be.snapshot(ls)]
+    while True:
+        k += 1
+        body(k)
+        snaps.append(be.snapshot(ls))
+        if be.done(snaps.pop(0)):
+            break
+    passes, converged, residual_f = be.loop_result(ls)
     delta_star = B                                          # FFT(final_eps), pipeline.cpp:114
     residual_s = comm.max_f64([be.residual_s(eps, E, fw)], dev)[0]
 

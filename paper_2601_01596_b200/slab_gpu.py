@@ -22,7 +22,7 @@ class SlabOp(C.Structure):
 
 
 (EPS0, FWD_LOCAL, COL0_CHECK, COL0_CLIP_INV, COL0_PLAIN, COL0_REBUILD, COL0_MARK, COL0_VERIFY,
- INV_SCLIP, INV_REPAIR_VERIFY, INV_VERIFY, RESIDUAL_S, EPS0_PLUS_S, GATE) = range(14)
+ INV_SCLIP, INV_REPAIR_VERIFY, INV_VERIFY, RESIDUAL_S, EPS0_PLUS_S, GATE, DECIDE) = range(15)
 
 
 def _bits_to_bool(words, n):
@@ -63,7 +63,7 @@ class GpuSlabBackend:
         return cm()
 
     # -- plumbing -----------------------------------------------------------------------------
-    def _op(self, code, shape, ptrs, **kw):
+    def _op(self, code, shape, ptrs, gate=None, **kw):
         o = SlabOp()
         o.op = code
         o.d0, o.d1 = int(shape[0]), int(shape[1])
@@ -72,6 +72,8 @@ class GpuSlabBackend:
             setattr(o, k, v)
         for i, t in enumerate(ptrs):
             o.p[i] = None if t is None else t.data_ptr()
+        if gate is not None:   # device-resident loop: the op returns at once once done is set
+            o.p[9] = gate.data_ptr()
         out = (C.c_double * 4)()
         _check(self.lib.ffcz_cuda_slab(self.ctx.handle, C.byref(o), out))
         return list(out)
@@ -103,20 +105,54 @@ class GpuSlabBackend:
                      fscale=fw, slack=slack)
         return int(o[0]), int(o[1])
 
-    def fwd_local(self, x, A, N):
-        self._op(FWD_LOCAL, x.shape, [x, A])
+    def fwd_local(self, x, A, N, gate=None):
+        self._op(FWD_LOCAL, x.shape, [x, A], gate=gate)
 
     def col0_check(self, B, Dw):
         o = self._op(COL0_CHECK, B.shape, [B], delta=Dw, fscale=1.0)
         return o[0], o[1]
 
-    def col0_clip_inv(self, B, Dw, F_B, moved_B, first):
-        self._op(COL0_CLIP_INV, B.shape, [B, F_B, moved_B], delta=Dw, fscale=1.0,
+    def col0_clip_inv(self, B, Dw, F_B, moved_B, first, gate=None):
+        self._op(COL0_CLIP_INV, B.shape, [B, F_B, moved_B], gate=gate, delta=Dw, fscale=1.0,
                  first=int(bool(first)))
 
-    def inv_local_sclip(self, A, eps_out, N, Ew, S, first):
-        self._op(INV_SCLIP, A.shape, [A, eps_out, S], e=Ew, fscale=1.0, n_total=N,
+    def inv_local_sclip(self, A, eps_out, N, Ew, S, first, gate=None):
+        self._op(INV_SCLIP, A.shape, [A, eps_out, S], gate=gate, e=Ew, fscale=1.0, n_total=N,
                  first=int(bool(first)))
+
+    # -- device-resident loop: decisions on the device, the host only waits on events ------------
+    def loop_state(self):
+        torch = self.torch
+        return {"gate": torch.zeros(2, dtype=torch.int32, device=self.device),    # done, conv.
+                "red": torch.zeros(2, dtype=torch.float64, device=self.device),   # peak, excess
+                "state": torch.zeros(2, dtype=torch.float64, device=self.device),  # passes, res.
+                "host": [torch.zeros(2, dtype=torch.int32, pin_memory=True) for _ in range(2)],
+                "slot": 0}
+
+    def col0_check_dev(self, B, Dw, red, gate):
+        self._op(COL0_CHECK, B.shape, [B, red], gate=gate, delta=Dw, fscale=1.0)
+
+    def decide(self, red, state, gate, max_iters):
+        self._op(DECIDE, (1, 1), [red, state], gate=gate, n_total=int(max_iters))
+
+    def snapshot(self, ls):
+        """Queue an async copy of the done flag; returns a handle for done()."""
+        h = ls["host"][ls["slot"]]
+        ls["slot"] ^= 1
+        h.copy_(ls["gate"], non_blocking=True)
+        ev = self.torch.cuda.Event()
+        ev.record(self.torch.cuda.current_stream(self.device))
+        return (ev, h)
+
+    def done(self, snap):
+        ev, h = snap
+        ev.synchronize()
+        return bool(h[0].item())
+
+    def loop_result(self, ls):
+        """(passes, converged, residual_f) after the loop (one sync)."""
+        st, g = ls["state"].cpu().tolist(), ls["gate"].cpu().tolist()
+        return int(st[0]), bool(g[1]), float(st[1])
 
     def residual_s(self, eps, E, fw):
         return self._op(RESIDUAL_S, eps.shape, [eps], e=E, fscale=fw)[0]

@@ -46,7 +46,9 @@ class CpuSlabBackend:
         b2 = torch.nonzero(a > E * fw * (1.0 + slack))
         return (int(b1[0]) if b1.numel() else -1), (int(b2[0]) if b2.numel() else -1)
 
-    def fwd_local(self, x, A, N):
+    def fwd_local(self, x, A, N, gate=None):
+        if gate is not None and int(gate[0]):
+            return
         A.copy_(torch.fft.fft(torch.fft.rfft(x, dim=2), dim=1))
 
     def _fwd0(self, B):
@@ -60,7 +62,39 @@ class CpuSlabBackend:
         exc = float(torch.maximum(ar - Dw, ai - Dw).max())
         return peak, max(exc, 0.0)
 
-    def col0_clip_inv(self, B, Dw, F_B, moved_B, first):
+    # device-resident loop interface (slab_gpu.GpuSlabBackend): the done flag gates the ops
+    def loop_state(self):
+        return {"gate": torch.zeros(2, dtype=torch.int32), "red": torch.zeros(2, dtype=torch.float64),
+                "state": torch.zeros(2, dtype=torch.float64)}
+
+    def col0_check_dev(self, B, Dw, red, gate):
+        if int(gate[0]):
+            return
+        red.copy_(torch.tensor(self.col0_check(B, Dw), dtype=torch.float64))
+
+    def decide(self, red, state, gate, max_iters):
+        if int(gate[0]):
+            return
+        peak, ex = float(red[0]), float(red[1])
+        if not ex > 1e-11 * peak:
+            gate[1], state[1], gate[0] = 1, 0.0, 1
+        elif float(state[0]) >= max_iters:
+            gate[1], state[1], gate[0] = 0, ex, 1
+        else:
+            state[0] += 1.0
+
+    def snapshot(self, ls):
+        return int(ls["gate"][0])
+
+    def done(self, snap):
+        return bool(snap)
+
+    def loop_result(self, ls):
+        return int(ls["state"][0]), bool(int(ls["gate"][1])), float(ls["state"][1])
+
+    def col0_clip_inv(self, B, Dw, F_B, moved_B, first, gate=None):
+        if gate is not None and int(gate[0]):
+            return
         re, im = B.real, B.imag
         cre, cim = re.clamp(-Dw, Dw), im.clamp(-Dw, Dw)
         dre, dim_ = cre - re, cim - im
@@ -73,7 +107,9 @@ class CpuSlabBackend:
         A1 = torch.fft.ifft(A, dim=1, norm="forward")
         return torch.fft.irfft(A1, n=self.n2, dim=2, norm="forward") * (1.0 / N)
 
-    def inv_local_sclip(self, A, eps_out, N, Ew, S, first):
+    def inv_local_sclip(self, A, eps_out, N, Ew, S, first, gate=None):
+        if gate is not None and int(gate[0]):
+            return
         x = self._c2r(A, N)
         c = x.clamp(-Ew, Ew)
         d = c - x
