@@ -204,7 +204,8 @@ int ffcz_cuda_correct_batch(ffcz_cuda_ctx* ctx, const ffcz_field_desc* frame, ui
  * per-rank device step of it on device buffers, on the context stream.  Buffers: real slabs
  * d0 x d1 x n2 FP64 (inputs: `in_dtype`), half spectra d0 x d1 x P complex FP64 with
  * P = round_up(n2/2+1, 16) (ffcz_cuda_slab_pitch), bitmaps uint32 LSB-first.  Bounds are global
- * (E, Delta); `fscale` = 1 - 2^-m for the working bounds.  Ops that reduce synchronise the stream
+ * (e, delta) or per point / per component (e_arr, d_re, d_im); `fscale` scales them to the
+ * working bounds (1 - 2^-m) where an op takes working bounds.  Ops that reduce synchronise the stream
  * and return their scalars in out[0..3] -- except in the device-resident loop: FWD_LOCAL,
  * COL0_CHECK, COL0_CLIP_INV and INV_SCLIP take the loop's int32 done flag in p9 (they return at
  * once when it is set) and COL0_CHECK with p1 != NULL writes (peak, excess) to the device doubles
@@ -255,6 +256,12 @@ typedef struct ffcz_cuda_slab_op {
     uint64_t n_total;    /* global sample count (C2R normalisation) */
     double e, delta, fscale, slack;
     void* p[10];
+    /* per-point E over the op's natural slab (NULL: global e) and per-component Delta lanes in
+     * the pitched half layout of the op's spectrum buffer (NULL: global delta; d_im NULL: the Re
+     * lane serves both, rho mode); bounds.hpp:11-47 across ranks */
+    const double* e_arr;
+    const double* d_re;
+    const double* d_im;
 } ffcz_cuda_slab_op;
 int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4]);
 uint64_t ffcz_cuda_slab_pitch(uint64_t n2);

@@ -133,7 +133,9 @@ def correct(original, decompressed, E, Dre, Dim=None, m=16, max_iters=1000, prec
                                 _dp(o.ravel()), _dp(d.ravel()), *bargs, C.c_int(m),
                                 C.c_uint64(max_iters), C.byref(out))
     _check(rc)
-    data = C.string_at(out.archive, out.archive_len)
+    # (C.string_at takes an int size: a 512^3 rho-mode archive is 2.8 GB)
+    data = np.ctypeslib.as_array(out.archive, shape=(max(1, int(out.archive_len)),))[
+        : int(out.archive_len)].tobytes() if out.archive_len else b""
     lib().ffcz_ref_free(out.archive)
     return RefCorrect(_rep(out.report), int(out.escape_count), bool(out.verify_ok),
                       float(out.verify_max_spatial_excess), float(out.verify_max_freq_excess), data,

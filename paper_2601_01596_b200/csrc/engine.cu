@@ -2368,8 +2368,10 @@ int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4
         const HalfGeom hg = g.hg();
         const long long N = g.N, Nc = g.Nc();
         const double invN = 1.0 / static_cast<double>(op->n_total);
-        const SpatialB sb{nullptr, op->e};
-        const FreqB fb{nullptr, nullptr, op->delta};
+        // per-point E (natural slab layout) / per-component Delta lanes (the pitched half layout
+        // of the buffer the op works on) when given, else the global values
+        const SpatialB sb{op->e_arr, op->e};
+        const FreqB fb{op->d_re, op->d_im ? op->d_im : op->d_re, op->delta};
         auto P = [&](int i) { return op->p[i]; };
         auto d2 = [&](int i) { return static_cast<double2*>(op->p[i]); };
         auto dd = [&](int i) { return static_cast<double*>(op->p[i]); };

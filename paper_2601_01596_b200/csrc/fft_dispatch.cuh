@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <string>
 #include <tuple>
 
 #include "fft_mixed.cuh"
@@ -208,19 +209,25 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
             // FP64 L = 512 runs it at E = 16 (same stage count as E = 8, half the threads per
             // column) so a 16-column (256-B) tile fits 512 threads.  FFCZ_COL_TMA1=0 disables,
             // =1 forces it where it fits.
-            constexpr int E1 = (sizeof(T) == 8 && L == 512) ? 16 : E;
+            // FP32 runs it at E = 16 with 1024 threads (E = 32 at 512 threads spills: 0.70 ->
+            // 0.47 of HBM on the 1024^3 middle axis), so its outer-axis tiles reach 128-B rows
+            // (16 float2) like FP64's 8 double2: 1024^3 outer axis 0.41 (double-buffered, 64-B
+            // rows) -> 0.45 of HBM (E = 32 at 512 threads: 0.47; profiles/r02_passbench_f32.jsonl)
+            constexpr int E1 = sizeof(T) == 4 ? 16 : ((L == 512) ? 16 : E);
             constexpr int TT1 = L / E1;
-            constexpr int NT1 = 512;
+            constexpr int NT1 = sizeof(T) == 4 ? 1024 : 512;
             const int mode = tma1_mode();
             int B1 = std::min(NT1 / TT1, 128);
             while (B1 > 1 && col_tma1_smem_bytes<T, L, E1>(B1) > 220 * 1024) B1 /= 2;
             B1 = std::min(B1, pow2_ceil(ncols));
-            const bool outer = sizeof(T) == 8 && role == TileRole::kFirst;
-            // (FP32 runs E = 32 here, which spills at 512 threads: 0.70 -> 0.47 of HBM on the
-            // 1024^3 middle axis, so FP32 keeps double buffering unless forced)
+            // (FP32 at L = 512 keeps double buffering: 128-B rows already, 0.80 of HBM at 512^3
+            // vs 0.37 in this variant)
+            const bool outer = role == TileRole::kFirst && (sizeof(T) == 8 || L >= 1024);
+            // (FP32: outer axis only; its middle axis keeps double buffering)
             const bool want = !side && mode != 0 && TT1 * B1 >= 32 &&
-                              (mode == 1 || (sizeof(T) == 8 && B1 > Bt &&
-                                             (Bt * sizeof(cplx<T>) < 128 || outer)));
+                              (mode == 1 || (B1 > Bt && (sizeof(T) == 8
+                                                              ? (Bt * sizeof(cplx<T>) < 128 || outer)
+                                                              : outer)));
             CUtensorMap map1;
             if (want && encode_col_map(&map1, src, sizeof(T), ncols, L, row_stride, nplanes,
                                        plane_stride, B1, L < 256 ? L : 256, true)) {

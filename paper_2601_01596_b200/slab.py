@@ -157,7 +157,7 @@ def _transpose_ba(be, comm, B, n1, c0, c1):
     return recv.permute(1, 0, 2, 3).reshape(c0, n1, B.shape[-1])
 
 
-def correct_slab(be, comm: Comm, dims, orig, dec, E: float, Delta: float, m: int = 16,
+def correct_slab(be, comm: Comm, dims, orig, dec, E, Delta, m: int = 16,
                  max_iters: int = 1000) -> SlabResult:
     """ffcz::correct (pipeline.cpp:26-178) of a volume slab-decomposed along axis 0 (see
     _correct_slab); runs on the backend's stream when it has one."""
@@ -167,26 +167,53 @@ def correct_slab(be, comm: Comm, dims, orig, dec, E: float, Delta: float, m: int
         return _correct_slab(be, comm, dims, orig, dec, E, Delta, m, max_iters)
 
 
-def _correct_slab(be, comm: Comm, dims, orig, dec, E: float, Delta: float, m: int = 16,
+def _correct_slab(be, comm: Comm, dims, orig, dec, E, Delta, m: int = 16,
                   max_iters: int = 1000) -> SlabResult:
     """ffcz::correct (pipeline.cpp:26-178) of a volume slab-decomposed along axis 0.
 
-    orig / dec: this rank's (c0, n1, n2) slab (backend tensors, f32 or f64); E, Delta: the
-    global DualBounds (bounds.hpp:11-47; per-point / per-component bounds are not supported
-    across ranks)."""
+    orig / dec: this rank's (c0, n1, n2) slab (backend tensors, f32 or f64).  Bounds as
+    DualBounds holds them (bounds.hpp:11-47), split like the field: E a float or this rank's
+    (c0, n1, n2) per-point slab; Delta a float, this rank's (c0, n1, n2) slab of the
+    per-component lane (Re == Im, rho mode) or a (Re, Im) pair of such slabs (the full-spectrum
+    lanes at this rank's i0 planes).  Array bounds must satisfy DualBounds' invariants (entries
+    > 0 and finite, Hermitian-consistent lanes, bounds.cpp:10-59): the caller built them with
+    the reference's factories (as FFCZ_BOUNDS_VALIDATED)."""
     import torch
     n0, n1, n2 = (int(v) for v in dims)
     W, r = comm.size, comm.rank
     if len(dims) != 3 or n0 % W or n1 % W:
         raise ValueError("slab decomposition needs a 3-D field with n0, n1 divisible by ranks")
-    if not (E > 0.0 and np.isfinite(E)):
+    c0_ = n0 // W
+    e_arr = None if np.isscalar(E) else E
+    if e_arr is None and not (E > 0.0 and np.isfinite(E)):
         raise be.ValidationError("spatial bound E must be strictly positive and finite")
-    if not (Delta > 0.0 and np.isfinite(Delta)):
+    if e_arr is not None and tuple(e_arr.shape) != (c0_, n1, n2):
+        raise be.ValidationError("per-point bounds must match field size")
+    d_lanes = None
+    if not np.isscalar(Delta):
+        d_lanes = tuple(Delta) if isinstance(Delta, (tuple, list)) else (Delta, None)
+        if any(x is not None and tuple(x.shape) != (c0_, n1, n2) for x in d_lanes):
+            raise be.ValidationError("per-component bounds must match field size")
+    elif not (Delta > 0.0 and np.isfinite(Delta)):
         raise be.ValidationError("frequency bound Delta must be strictly positive and finite")
     if m < 1 or m > 24:
         raise be.ValidationError("shrink_bounds requires 1 <= m <= 24")
     if max_iters < 1:
         raise be.ValidationError("alternating_projection: max_iters must be >= 1")
+    if e_arr is not None or d_lanes is not None:
+        # per-component lanes restricted to the half grid on the natural slab (A layout) and
+        # moved to the B layout with the same all-to-all as the spectra
+        c1_ = n1 // W
+        dA = dB = None
+        if d_lanes is not None:
+            dA = tuple(None if x is None else be.half_lane(x) for x in d_lanes)
+            dB = tuple(None if x is None else _transpose_ab(be, comm, x, n0, c0_, c1_).contiguous()
+                       for x in dA)
+        be.set_bounds(e_arr, dA, dB)
+        E = 0.0 if e_arr is not None else E
+        Delta = 0.0 if d_lanes is not None else Delta
+    else:
+        be.set_bounds(None, None, None)
     c0, c1 = n0 // W, n1 // W
     H = n2 // 2 + 1
     N = n0 * n1 * n2
@@ -226,12 +253,12 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E: float, Delta: float, m: in
         which leaves B (= delta_star) unchanged.  Pass k (from 0) is clip pass k + 1."""
         nonlocal A, B
         B = _transpose_ab(be, comm, A, n0, c0, c1)
-        be.col0_check_dev(B, Delta * fw, ls["red"], gate)   # FFT axis 0 + check (in place)
+        be.col0_check_dev(B, Delta, fw, ls["red"], gate)   # FFT axis 0 + check (in place)
         comm.max_f64_(ls["red"])
         be.decide(ls["red"], ls["state"], gate, max_iters)
-        be.col0_clip_inv(B, Delta * fw, F_B, moved_B, k == 0, gate=gate)   # :117-119, axis 0
+        be.col0_clip_inv(B, Delta, fw, F_B, moved_B, k == 0, gate=gate)   # :117-119, axis 0
         A = _transpose_ba(be, comm, B, n1, c0, c1)
-        be.inv_local_sclip(A, eps, N, E * fw, S, k == 0, gate=gate)   # axis 1, C2R, :121-124
+        be.inv_local_sclip(A, eps, N, E, fw, S, k == 0, gate=gate)   # axis 1, C2R, :121-124
         be.fwd_local(eps, A, N, gate=gate)
 
     # one pass queued behind the one being decided: the host waits on an event per pass, never

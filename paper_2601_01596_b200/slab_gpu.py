@@ -18,11 +18,16 @@ class SlabOp(C.Structure):
                 ("in_dtype", C.c_int32), ("m", C.c_int32), ("pad", C.c_int32),
                 ("d0", C.c_uint64), ("d1", C.c_uint64), ("n2", C.c_uint64),
                 ("n_total", C.c_uint64), ("e", C.c_double), ("delta", C.c_double),
-                ("fscale", C.c_double), ("slack", C.c_double), ("p", C.c_void_p * 10)]
+                ("fscale", C.c_double), ("slack", C.c_double), ("p", C.c_void_p * 10),
+                ("e_arr", C.c_void_p), ("d_re", C.c_void_p), ("d_im", C.c_void_p)]
 
 
 (EPS0, FWD_LOCAL, COL0_CHECK, COL0_CLIP_INV, COL0_PLAIN, COL0_REBUILD, COL0_MARK, COL0_VERIFY,
  INV_SCLIP, INV_REPAIR_VERIFY, INV_VERIFY, RESIDUAL_S, EPS0_PLUS_S, GATE, DECIDE) = range(15)
+
+
+_E_OPS = frozenset({EPS0, INV_SCLIP, INV_REPAIR_VERIFY, INV_VERIFY, RESIDUAL_S, GATE})
+_B_OPS = frozenset({COL0_CHECK, COL0_CLIP_INV, COL0_MARK, COL0_VERIFY})
 
 
 def _bits_to_bool(words, n):
@@ -47,6 +52,22 @@ class GpuSlabBackend:
         # create a private stream)
         self.stream = torch.cuda.Stream(self.device)
         self.ctx = ctx or Context(self.device.index or 0, self.stream.cuda_stream)
+        self.e_arr = self.dA = self.dB = None
+
+    # -- per-point / per-component bounds (slab.py set_bounds) ----------------------------------
+    def set_bounds(self, e_arr, dA, dB):
+        """e_arr: (c0, n1, n2) float64 per-point E of this slab; dA / dB: (Re, Im-or-None) lanes
+        in the pitched half layout of the natural slab / of the B layout."""
+        torch = self.torch
+        self.e_arr = None if e_arr is None else e_arr.to(torch.float64).contiguous()
+        self.dA, self.dB = dA, dB
+
+    def half_lane(self, x):
+        """(c0, n1, n2) full-spectrum lane slab -> (c0, n1, P) half layout (k2 <= n2/2)."""
+        torch = self.torch
+        out = torch.zeros(tuple(x.shape[:2]) + (self.P,), dtype=torch.float64, device=self.device)
+        out[..., : self.H] = x[..., : self.H]
+        return out
 
     def stream_context(self):
         """Enter the backend stream (ordered after the caller's current stream) for one call."""
@@ -63,8 +84,16 @@ class GpuSlabBackend:
         return cm()
 
     # -- plumbing -----------------------------------------------------------------------------
+    # which bound arrays an op reads: spatial ops the per-point E, spectrum ops the Delta lanes
+    # of the layout they work in (B: axis-0 ops, A: the gate)
     def _op(self, code, shape, ptrs, gate=None, **kw):
         o = SlabOp()
+        if self.e_arr is not None and code in _E_OPS:
+            o.e_arr = self.e_arr.data_ptr()
+        lanes = self.dB if code in _B_OPS else (self.dA if code == GATE else None)
+        if lanes is not None:
+            o.d_re = lanes[0].data_ptr()
+            o.d_im = None if lanes[1] is None else lanes[1].data_ptr()
         o.op = code
         o.d0, o.d1 = int(shape[0]), int(shape[1])
         o.n2 = self.n2
@@ -112,12 +141,12 @@ class GpuSlabBackend:
         o = self._op(COL0_CHECK, B.shape, [B], delta=Dw, fscale=1.0)
         return o[0], o[1]
 
-    def col0_clip_inv(self, B, Dw, F_B, moved_B, first, gate=None):
-        self._op(COL0_CLIP_INV, B.shape, [B, F_B, moved_B], gate=gate, delta=Dw, fscale=1.0,
+    def col0_clip_inv(self, B, D, fs, F_B, moved_B, first, gate=None):
+        self._op(COL0_CLIP_INV, B.shape, [B, F_B, moved_B], gate=gate, delta=D, fscale=fs,
                  first=int(bool(first)))
 
-    def inv_local_sclip(self, A, eps_out, N, Ew, S, first, gate=None):
-        self._op(INV_SCLIP, A.shape, [A, eps_out, S], gate=gate, e=Ew, fscale=1.0, n_total=N,
+    def inv_local_sclip(self, A, eps_out, N, E, fs, S, first, gate=None):
+        self._op(INV_SCLIP, A.shape, [A, eps_out, S], gate=gate, e=E, fscale=fs, n_total=N,
                  first=int(bool(first)))
 
     # -- device-resident loop: decisions on the device, the host only waits on events ------------
@@ -129,8 +158,8 @@ class GpuSlabBackend:
                 "host": [torch.zeros(2, dtype=torch.int32, pin_memory=True) for _ in range(2)],
                 "slot": 0}
 
-    def col0_check_dev(self, B, Dw, red, gate):
-        self._op(COL0_CHECK, B.shape, [B, red], gate=gate, delta=Dw, fscale=1.0)
+    def col0_check_dev(self, B, D, fs, red, gate):
+        self._op(COL0_CHECK, B.shape, [B, red], gate=gate, delta=D, fscale=fs)
 
     def decide(self, red, state, gate, max_iters):
         self._op(DECIDE, (1, 1), [red, state], gate=gate, n_total=int(max_iters))

@@ -23,6 +23,24 @@ class CpuSlabBackend:
         self.H = n2 // 2 + 1
         self.P = self.H
         self.device = torch.device("cpu")
+        self.e_arr = self.dA = self.dB = None
+
+    # -- per-point / per-component bounds (slab.py set_bounds) -----------------------------
+    def set_bounds(self, e_arr, dA, dB):
+        self.e_arr = None if e_arr is None else e_arr.double()
+        self.dA, self.dB = dA, dB
+
+    def half_lane(self, x):
+        return x[..., : self.H].double().contiguous()
+
+    def _E(self, E):
+        return self.e_arr if self.e_arr is not None else E
+
+    def _D(self, lanes, D):
+        """(Re bound, Im bound) of a layout: tensors when per component, else the scalar."""
+        if lanes is None:
+            return D, D
+        return lanes[0], (lanes[0] if lanes[1] is None else lanes[1])
 
     # -- buffers --------------------------------------------------------------------------
     def empty_like(self, t):
@@ -41,9 +59,11 @@ class CpuSlabBackend:
     def eps0(self, orig, dec, E, fw, slack, eps_out):
         e = dec.double() - orig.double()
         eps_out.copy_(e)
-        a = e.abs().view(-1)
-        b1 = torch.nonzero(a > E * (1.0 + 2.0 ** -20))
-        b2 = torch.nonzero(a > E * fw * (1.0 + slack))
+        a = e.abs().reshape(-1)
+        Ev = self._E(E)
+        Ev = Ev.reshape(-1) if torch.is_tensor(Ev) else Ev
+        b1 = torch.nonzero(a > Ev * (1.0 + 2.0 ** -20))
+        b2 = torch.nonzero(a > Ev * fw * (1.0 + slack))
         return (int(b1[0]) if b1.numel() else -1), (int(b2[0]) if b2.numel() else -1)
 
     def fwd_local(self, x, A, N, gate=None):
@@ -67,10 +87,16 @@ class CpuSlabBackend:
         return {"gate": torch.zeros(2, dtype=torch.int32), "red": torch.zeros(2, dtype=torch.float64),
                 "state": torch.zeros(2, dtype=torch.float64)}
 
-    def col0_check_dev(self, B, Dw, red, gate):
+    def col0_check_dev(self, B, D, fs, red, gate):
         if int(gate[0]):
             return
-        red.copy_(torch.tensor(self.col0_check(B, Dw), dtype=torch.float64))
+        V = self._fwd0(B)
+        B.copy_(V)
+        dre, dim_ = self._D(self.dB, D)
+        ar, ai = V.real.abs(), V.imag.abs()
+        peak = float(torch.maximum(ar, ai).max())
+        exc = float(torch.maximum(ar - dre * fs, ai - dim_ * fs).max())
+        red.copy_(torch.tensor([peak, max(exc, 0.0)], dtype=torch.float64))
 
     def decide(self, red, state, gate, max_iters):
         if int(gate[0]):
@@ -92,11 +118,16 @@ class CpuSlabBackend:
     def loop_result(self, ls):
         return int(ls["state"][0]), bool(int(ls["gate"][1])), float(ls["state"][1])
 
-    def col0_clip_inv(self, B, Dw, F_B, moved_B, first, gate=None):
+    def col0_clip_inv(self, B, D, fs, F_B, moved_B, first, gate=None):
         if gate is not None and int(gate[0]):
             return
         re, im = B.real, B.imag
-        cre, cim = re.clamp(-Dw, Dw), im.clamp(-Dw, Dw)
+        dre, dim_ = self._D(self.dB, D)
+        dre, dim_ = dre * fs, dim_ * fs
+        dre = torch.as_tensor(dre, dtype=torch.float64)
+        dim_ = torch.as_tensor(dim_, dtype=torch.float64)
+        cre = torch.maximum(torch.minimum(re, dre), -dre)
+        cim = torch.maximum(torch.minimum(im, dim_), -dim_)
         dre, dim_ = cre - re, cim - im
         if first:
             F_B.copy_(torch.complex(0.0 + dre, 0.0 + dim_))
@@ -107,11 +138,12 @@ class CpuSlabBackend:
         A1 = torch.fft.ifft(A, dim=1, norm="forward")
         return torch.fft.irfft(A1, n=self.n2, dim=2, norm="forward") * (1.0 / N)
 
-    def inv_local_sclip(self, A, eps_out, N, Ew, S, first, gate=None):
+    def inv_local_sclip(self, A, eps_out, N, E, fs, S, first, gate=None):
         if gate is not None and int(gate[0]):
             return
         x = self._c2r(A, N)
-        c = x.clamp(-Ew, Ew)
+        Ew = torch.as_tensor(self._E(E) * fs, dtype=torch.float64)
+        c = torch.maximum(torch.minimum(x, Ew), -Ew)
         d = c - x
         if first:
             S.copy_(0.0 + d)
@@ -120,7 +152,7 @@ class CpuSlabBackend:
         eps_out.copy_(c)
 
     def residual_s(self, eps, E, fw):
-        return max(float((eps.abs() - E * fw).max()), 0.0)
+        return max(float((eps.abs() - self._E(E) * fw).max()), 0.0)
 
     # -- gate --------------------------------------------------------------------------------
     def eps0_plus_s(self, orig, dec, S, X):
@@ -135,7 +167,8 @@ class CpuSlabBackend:
 
     def gate(self, S, F_A, E, D, m, base_h):
         s = S.view(-1).numpy()
-        step = np.ldexp(2.0 * E, -m)
+        Ev = self._E(E)
+        step = np.ldexp(2.0 * (Ev.reshape(-1).numpy() if torch.is_tensor(Ev) else Ev), -m)
         nz = s != 0.0
         ovf = nz & (np.abs(s) / step > KMAX)
         keep = nz & ~ovf
@@ -143,13 +176,15 @@ class CpuSlabBackend:
         spat = np.where(keep, q.astype(np.int32).astype(np.float64) * step, np.where(ovf, s, 0.0))
         codes_s = q[keep].astype(np.int32)
         f = F_A[..., : self.H].reshape(-1).numpy()
-        fstep = np.ldexp(2.0 * D, -m)
+        dre, dim_ = self._D(self.dA, D)
+        lane = lambda x: x[..., : self.H].reshape(-1).numpy() if torch.is_tensor(x) else x
+        fsr, fsi = np.ldexp(2.0 * lane(dre), -m), np.ldexp(2.0 * lane(dim_), -m)
         fnz = (f.real != 0.0) | (f.imag != 0.0)
-        fovf = fnz & ((np.abs(f.real) / fstep > KMAX) | (np.abs(f.imag) / fstep > KMAX))
+        fovf = fnz & ((np.abs(f.real) / fsr > KMAX) | (np.abs(f.imag) / fsi > KMAX))
         fkeep = fnz & ~fovf
-        qr, qi = O._llround_exact(f.real / fstep), O._llround_exact(f.imag / fstep)
-        cur = np.where(fkeep, qr.astype(np.int32).astype(np.float64) * fstep +
-                       1j * (qi.astype(np.int32).astype(np.float64) * fstep),
+        qr, qi = O._llround_exact(f.real / fsr), O._llround_exact(f.imag / fsi)
+        cur = np.where(fkeep, qr.astype(np.int32).astype(np.float64) * fsr +
+                       1j * (qi.astype(np.int32).astype(np.float64) * fsi),
                        np.where(fovf, f, 0.0))
         codes_f = np.empty(2 * int(fkeep.sum()), dtype=np.int32)
         codes_f[0::2], codes_f[1::2] = qr[fkeep].astype(np.int32), qi[fkeep].astype(np.int32)
@@ -176,9 +211,10 @@ class CpuSlabBackend:
         corrected.copy_(c)
         if eps_v is not None:
             eps_v.copy_(v)
-        vs = max(float((v.abs() - E).max()), 0.0)
+        Ev = self._E(E)
+        vs = max(float((v.abs() - Ev).max()), 0.0)
         t = v if eps_v is None else (e0 + sc) + x  # eps_v None: decoder-view repair
-        bad = t.abs() > E
+        bad = t.abs() > Ev
         spat_cur.copy_(torch.where(bad, sc + (final_eps - t), sc))
         esc_s |= bad
         eps_t.copy_(t)
@@ -191,16 +227,18 @@ class CpuSlabBackend:
         corrected.copy_(c)
         v = c - o
         eps_v.copy_(v)
-        return max(float((v.abs() - E).max()), 0.0)
+        return max(float((v.abs() - self._E(E)).max()), 0.0)
 
     def col0_mark(self, Bt, D):
         V = self._fwd0(Bt)
         Bt.copy_(V)
-        return (V.real.abs() > D) | (V.imag.abs() > D)
+        dre, dim_ = self._D(self.dB, D)
+        return (V.real.abs() > dre) | (V.imag.abs() > dim_)
 
     def col0_verify(self, Bv, D):
         V = self._fwd0(Bv)
-        return max(float(torch.maximum(V.real.abs() - D, V.imag.abs() - D).max()), 0.0)
+        dre, dim_ = self._D(self.dB, D)
+        return max(float(torch.maximum(V.real.abs() - dre, V.imag.abs() - dim_).max()), 0.0)
 
     # -- sparse bookkeeping ------------------------------------------------------------------
     def positions(self, viol):

@@ -32,7 +32,20 @@ def field(n, seed, c):
     return o, d, E, c * cases.mean_abs_delta0(o, d)
 
 
-def _worker(rank, world, port, n, seed, c, out_dir):
+def bound_arrays(n, E, D, seed):
+    """Per-point E (>= the global E of the perturbation) and Hermitian-consistent per-component
+    (Re, Im) Delta lanes."""
+    rng = np.random.default_rng(seed + 50)
+    shape = (n, n, n)
+    def sym(g):  # exactly Hermitian-consistent: g[k] == g[-k] bit for bit (bounds.cpp:50-54)
+        return 0.5 * (g + np.roll(np.flip(g), 1, axis=tuple(range(g.ndim))))
+    g1 = sym(np.abs(np.fft.fftn(rng.standard_normal(shape))))
+    g2 = sym(np.abs(np.fft.fftn(rng.standard_normal(shape))))
+    return (E * (1.0 + rng.uniform(0.0, 1.0, shape)), D * (0.6 + g1 / g1.max()),
+            D * (0.7 + 0.5 * g2 / g2.max()))
+
+
+def _worker(rank, world, port, n, seed, c, out_dir, arrays=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -51,6 +64,10 @@ def _worker(rank, world, port, n, seed, c, out_dir):
         to = torch.from_numpy(o[sl].astype(np.float32)).cuda()
         td = torch.from_numpy(d[sl].astype(np.float32)).cuda()
         be = GpuSlabBackend(n, to.device)
+        if arrays:
+            Ea, Dre, Dim = bound_arrays(n, E, D, seed)
+            E = torch.from_numpy(Ea[sl].copy()).cuda()
+            D = (torch.from_numpy(Dre[sl].copy()).cuda(), torch.from_numpy(Dim[sl].copy()).cuda())
         res = slab.correct_slab(be, slab.Comm(stage_cpu=True), (n, n, n), to, td, E, D)
         torch.cuda.synchronize()
         res.corrected = res.corrected.cpu().numpy()
@@ -72,10 +89,11 @@ def _to_host(res, n):
     res.frequency_codes = res.frequency_codes.cpu().numpy()
 
 
-def run_world(world, n, seed, c):
+def run_world(world, n, seed, c, arrays=False):
     import torch.multiprocessing as mp
     with tempfile.TemporaryDirectory() as tmp:
-        mp.spawn(_worker, args=(world, _free_port(), n, seed, c, tmp), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), n, seed, c, tmp, arrays), nprocs=world,
+                 join=True)
         return [pickle.load(open(os.path.join(tmp, f"r{r}.pkl"), "rb")) for r in range(world)]
 
 
@@ -124,3 +142,29 @@ def test_slab_gpu_worlds_agree(world):
     assert [e[:2] for e in a[0].escapes] == [e[:2] for e in b[0].escapes]
     ca, cb = cat(a, "corrected"), cat(b, "corrected")
     np.testing.assert_allclose(ca, cb, rtol=0, atol=1e-12 * np.abs(ca).max())
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_slab_gpu_bound_arrays(world):
+    """Per-point E and per-component (Re, Im) Delta split across ranks like the field
+    (bounds.hpp:11-47): the ranks' products equal the single-volume engine's with the same
+    DualBounds arrays, and the guarantee holds against those bounds."""
+    import paper_2601_01596_b200 as P
+    n, seed, c = 32, 7, 0.7
+    o, d, E, D = field(n, seed, c)
+    Ea, Dre, Dim = bound_arrays(n, E, D, seed)
+    parts = run_world(world, n, seed, c, arrays=True)
+    eng = P.correct(o.astype(np.float32), d.astype(np.float32), P.DualBounds(Ea, Dre, Dim), 16,
+                    1000, "f32")
+    ref = O.correct(o, d, O.DualBounds(Ea, Dre, Dim), 16, 1000, "f32")
+    r0 = parts[0]
+    for r in (eng.report, ref.report):
+        assert (r0.iterations, r0.converged, r0.active_spatial, r0.active_frequency) == \
+            (r.iterations, r.converged, r.active_spatial, r.active_frequency)
+    assert r0.verify_ok and eng.verify_ok
+    arch = O.read_archive(eng.archive_bytes)
+    assert np.array_equal(cat(parts, "spatial_flags"), arch.spatial_flags.ravel())
+    assert np.array_equal(cat(parts, "frequency_flags"), arch.frequency_flags.ravel())
+    assert np.mean(cat(parts, "frequency_codes") == arch.frequency_codes) >= 0.999
+    ok, ms, mf = O.verify_bounds(o, cat(parts, "corrected"), O.DualBounds(Ea, Dre, Dim))
+    assert ok and ms == 0.0

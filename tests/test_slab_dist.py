@@ -36,7 +36,19 @@ def field(shape, seed, c):
     return o, d, E, D
 
 
-def _worker(rank, world, port, shape, seed, c, m, max_iters, out_dir):
+def bound_arrays(shape, o, E, D, seed):
+    """Per-point E (>= the global E the perturbation respects) and per-component (Re, Im)
+    Delta lanes, Hermitian-consistent (|FFT(real)| is symmetric under k -> -k)."""
+    rng = np.random.default_rng(seed + 50)
+    Ea = E * (1.0 + rng.uniform(0.0, 1.0, shape))
+    def sym(g):  # exactly Hermitian-consistent: g[k] == g[-k] bit for bit (bounds.cpp:50-54)
+        return 0.5 * (g + np.roll(np.flip(g), 1, axis=tuple(range(g.ndim))))
+    g1 = sym(np.abs(np.fft.fftn(rng.standard_normal(shape))))
+    g2 = sym(np.abs(np.fft.fftn(rng.standard_normal(shape))))
+    return Ea, D * (0.6 + g1 / g1.max()), D * (0.7 + 0.5 * g2 / g2.max())
+
+
+def _worker(rank, world, port, shape, seed, c, m, max_iters, out_dir, arrays=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -52,6 +64,10 @@ def _worker(rank, world, port, shape, seed, c, m, max_iters, out_dir):
         c0 = shape[0] // world
         sl = slice(rank * c0, (rank + 1) * c0)
         be = CpuSlabBackend(shape[2])
+        if arrays:
+            Ea, Dre, Dim = bound_arrays(shape, o, E, D, seed)
+            E = torch.from_numpy(Ea[sl].copy())
+            D = (torch.from_numpy(Dre[sl].copy()), torch.from_numpy(Dim[sl].copy()))
         res = slab.correct_slab(be, slab.Comm(), shape, torch.from_numpy(o[sl].copy()),
                                 torch.from_numpy(d[sl].copy()), E, D, m, max_iters)
         res.corrected = res.corrected.numpy()
@@ -61,9 +77,9 @@ def _worker(rank, world, port, shape, seed, c, m, max_iters, out_dir):
         dist.destroy_process_group()
 
 
-def run_world(world, shape, seed=3, c=0.6, m=16, max_iters=1000):
+def run_world(world, shape, seed=3, c=0.6, m=16, max_iters=1000, arrays=False):
     with tempfile.TemporaryDirectory() as tmp:
-        mp.spawn(_worker, args=(world, _free_port(), shape, seed, c, m, max_iters, tmp),
+        mp.spawn(_worker, args=(world, _free_port(), shape, seed, c, m, max_iters, tmp, arrays),
                  nprocs=world, join=True)
         parts = [pickle.load(open(os.path.join(tmp, f"r{r}.pkl"), "rb")) for r in range(world)]
     return parts
@@ -113,6 +129,32 @@ def test_slab_worlds_agree(world, shape, c):
     assert len(a["escapes"]) == len(b["escapes"])
     assert [e[:2] for e in a["escapes"]] == [e[:2] for e in b["escapes"]]
     np.testing.assert_allclose(a["corrected"], b["corrected"], rtol=0, atol=1e-12 * np.abs(a["corrected"]).max())
+
+
+def test_slab_bound_arrays_match_oracle():
+    """Per-point E and per-component (Re, Im) Delta split across ranks like the field
+    (bounds.hpp:11-47): world 1 against the oracle, worlds 2 and 4 against world 1."""
+    shape, c = (16, 16, 16), 0.6
+    o, d, E, D = field(shape, 3, c)
+    Ea, Dre, Dim = bound_arrays(shape, o, E, D, 3)
+    ref = O.correct(o, d, O.DualBounds(Ea, Dre, Dim), 16, 1000, "f32")
+    g = merged(run_world(1, shape, c=c, arrays=True))
+    assert (g["iterations"], g["converged"], g["active_s"], g["active_f"]) == \
+        (ref.report.iterations, ref.report.converged, ref.report.active_spatial,
+         ref.report.active_frequency)
+    arch = ref.archive
+    assert np.array_equal(g["sflags"], arch.spatial_flags.ravel())
+    assert np.array_equal(g["fflags"], arch.frequency_flags.ravel())
+    assert np.mean(g["fcodes"] == arch.frequency_codes) >= 0.999
+    assert g["verify_ok"] and ref.verify_ok
+    ok, ms, mf = O.verify_bounds(o, g["corrected"], O.DualBounds(Ea, Dre, Dim))
+    assert ok and ms == 0.0
+    for world in (2, 4):
+        b = merged(run_world(world, shape, c=c, arrays=True))
+        for k in ("iterations", "converged", "active_s", "active_f", "verify_ok", "rounds"):
+            assert g[k] == b[k], (world, k)
+        for k in ("sflags", "fflags", "scodes", "fcodes"):
+            assert np.array_equal(g[k], b[k]), (world, k)
 
 
 # ---- cross-rank escape repair of conjugate plane partners (pipeline.cpp:140-153) ---------------
