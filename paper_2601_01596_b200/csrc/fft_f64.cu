@@ -1,10 +1,26 @@
 // FP64 instantiations of the FFT engine + shared host helpers (geometry, twiddle tables).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "fft_dispatch.cuh"
 
 namespace ffcz_gpu {
+
+// L2 sector promotion of the column-pass boxes (FFCZ_TMA_PROMO=none|64|128|256, A/B): 128 B
+// measured 1.7 % faster than 256 B on the 1024^3 outer axis (profiles/r02_passbench_promo.jsonl)
+static CUtensorMapL2promotion l2_promotion() {
+    static const CUtensorMapL2promotion p = [] {
+        const char* e = std::getenv("FFCZ_TMA_PROMO");
+        const std::string v = e ? e : "128";
+        if (v == "none") return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+        if (v == "64") return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+        if (v == "128") return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+        return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }();
+    return p;
+}
 
 bool encode_col_map(CUtensorMap* map, const void* base, int scalar_bytes, long long ncols,
                     long long L, long long row_stride, long long nplanes, long long plane_stride,
@@ -34,7 +50,7 @@ bool encode_col_map(CUtensorMap* map, const void* base, int scalar_bytes, long l
                                                      : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                               3, const_cast<void*>(base), dims, strides, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                              l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
