@@ -1,7 +1,11 @@
-// Host-side .ffcz archive writer.  Byte layout follows /root/reference/proj/docs/FORMAT.md and
-// the reference writer (archive.cpp:73-135, streams.cpp:21-55, huffman.cpp:156-251) so that the
-// reference's read_archive decodes it and, with zlib level 9 and identical edits, the bytes are
-// identical.
+// Host-side .ffcz archive writer (the zlib_level 0..9 modes; the default archive is assembled
+// from device-encoded streams, archive_dev.cu).  Byte layout follows
+// /root/reference/proj/docs/FORMAT.md and the reference writer (archive.cpp:73-135,
+// streams.cpp:21-55, huffman.cpp:156-251) so that the reference's read_archive decodes it and,
+// with zlib level 9 and identical edits, the bytes are identical.  The edits themselves follow the
+// engine's defaults (decoder-view escape repair, F rebuilt at the gate: INTEGRATION.md §4), which
+// can differ from the reference's where FP64 round-off straddles a bound; the per-call option
+// flags FFCZ_REPAIR_REFERENCE_ORDER / FFCZ_F_ACCUMULATE select the reference's order.
 #include "archive.hpp"
 
 #include <zlib.h>
