@@ -13,6 +13,9 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <exception>
+#include <future>
+#include <thread>
 #include <queue>
 #include <stdexcept>
 #include <string>
@@ -188,6 +191,28 @@ std::uint32_t crc32c(const std::uint8_t* data, std::size_t len) {
     return crc ^ 0xFFFFFFFFu;
 }
 
+int host_threads() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    return static_cast<int>(std::clamp(hw ? hw : 1u, 1u, 16u));
+}
+
+std::uint32_t crc32c_combine(std::uint32_t crc1, std::uint32_t crc2, std::uint64_t len2);
+
+std::uint32_t crc32c_threads(const std::uint8_t* p, std::uint64_t n) {
+    const int T = n < (std::uint64_t(64) << 20) ? 1 : host_threads();
+    if (T == 1) return crc32c(p, n);
+    std::vector<std::uint32_t> part(T);
+    std::vector<std::uint64_t> lo(T + 1);
+    for (int t = 0; t <= T; ++t) lo[t] = n * t / T;
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+        th.emplace_back([&, t] { part[t] = crc32c(p + lo[t], lo[t + 1] - lo[t]); });
+    for (auto& x : th) x.join();
+    std::uint32_t c = part[0];
+    for (int t = 1; t < T; ++t) c = crc32c_combine(c, part[t], lo[t + 1] - lo[t]);
+    return c;
+}
+
 std::uint32_t zigzag(std::int32_t v) {
     return (static_cast<std::uint32_t>(v) << 1) ^ static_cast<std::uint32_t>(v >> 31);
 }
@@ -357,19 +382,37 @@ ParsedArchive parse_archive(const std::uint8_t* bytes, std::size_t len) {
     const std::uint64_t lsi = r.pod<std::uint64_t>(), lfi = r.pod<std::uint64_t>();
     const std::uint64_t nesc = r.pod<std::uint64_t>();
     const std::size_t header_len = r.off;
-    if (crc32c(bytes, header_len) != r.pod<std::uint32_t>())
+    // (the bound arrays make the header up to 3 x 8 N bytes: CRC on host threads)
+    if (crc32c_threads(bytes, header_len) != r.pod<std::uint32_t>())
         throw ArchiveError("read_archive: header checksum mismatch");
     const std::uint8_t* sf = r.take(lsf);
     const std::uint8_t* ff = r.take(lff);
     const std::uint8_t* si = r.take(lsi);
     const std::uint8_t* fi = r.take(lfi);
-    a.spatial_flags = outer_decompress(sf, lsf);
-    a.frequency_flags = outer_decompress(ff, lff);
+    // the four outer stages inflate concurrently
+    auto fut_si = std::async(std::launch::async, [&] { return outer_decompress(si, lsi); });
+    auto fut_fi = std::async(std::launch::async, [&] { return outer_decompress(fi, lfi); });
+    auto fut_ff = std::async(std::launch::async, [&] { return outer_decompress(ff, lff); });
+    std::exception_ptr err;
+    try {
+        a.spatial_flags = outer_decompress(sf, lsf);
+    } catch (...) {
+        err = std::current_exception();
+    }
+    auto get = [&](auto& fut, std::vector<std::uint8_t>& dst) {
+        try {
+            dst = fut.get();
+        } catch (...) {
+            if (!err) err = std::current_exception();
+        }
+    };
+    get(fut_ff, a.frequency_flags);
+    get(fut_si, a.spatial_payload);
+    get(fut_fi, a.frequency_payload);
+    if (err) std::rethrow_exception(err);
     std::uint64_t Nh = N / a.dims[a.ndim - 1] * (a.dims[a.ndim - 1] / 2 + 1);
     if (a.spatial_flags.size() != (N + 7) / 8 || a.frequency_flags.size() != (Nh + 7) / 8)
         throw ArchiveError("decode_streams: flag payload length mismatch");
-    a.spatial_payload = outer_decompress(si, lsi);
-    a.frequency_payload = outer_decompress(fi, lfi);
     a.escapes.resize(nesc);
     for (auto& e : a.escapes) {
         const std::uint64_t packed = r.pod<std::uint64_t>();

@@ -64,6 +64,9 @@ std::uint64_t huffman_blocks(const std::vector<std::uint8_t>& payload,
                              std::vector<std::uint64_t>& block_first);
 
 std::uint32_t crc32c(const std::uint8_t* data, std::size_t len);
+// the same on up to 16 host threads (pieces joined by crc32c_combine, deflate.cu)
+std::uint32_t crc32c_threads(const std::uint8_t* data, std::uint64_t len);
+int host_threads();
 std::uint32_t zigzag(std::int32_t v);
 // Blockwise canonical Huffman (huffman.cpp:156-251 format)
 std::vector<std::uint8_t> huffman_encode(const std::uint32_t* symbols, std::size_t n);

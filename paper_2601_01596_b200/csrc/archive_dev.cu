@@ -30,29 +30,8 @@ void put(std::vector<std::uint8_t>& out, T v) {
     out.insert(out.end(), b, b + sizeof(T));
 }
 
-int host_threads() {
-    const unsigned hw = std::thread::hardware_concurrency();
-    return static_cast<int>(std::clamp(hw ? hw : 1u, 1u, 16u));
-}
-
-// standard CRC-32C of a host array on up to 16 threads (pieces joined by crc32c_combine)
-std::uint32_t crc32c_threads(const std::uint8_t* p, std::uint64_t n) {
-    const int T = n < (std::uint64_t(64) << 20) ? 1 : host_threads();
-    if (T == 1) return ffcz_host::crc32c(p, n);
-    std::vector<std::uint32_t> part(T);
-    std::vector<std::uint64_t> lo(T + 1);
-    for (int t = 0; t <= T; ++t) lo[t] = n * t / T;
-    std::vector<std::thread> th;
-    for (int t = 0; t < T; ++t)
-        th.emplace_back([&, t] { part[t] = ffcz_host::crc32c(p + lo[t], lo[t + 1] - lo[t]); });
-    for (auto& x : th) x.join();
-    std::uint32_t c = part[0];
-    for (int t = 1; t < T; ++t) c = ffcz_host::crc32c_combine(c, part[t], lo[t + 1] - lo[t]);
-    return c;
-}
-
 void memcpy_threads(std::uint8_t* dst, const std::uint8_t* src, std::uint64_t n) {
-    const int T = n < (std::uint64_t(64) << 20) ? 1 : host_threads();
+    const int T = n < (std::uint64_t(64) << 20) ? 1 : ffcz_host::host_threads();
     if (T == 1) {
         std::memcpy(dst, src, n);
         return;
@@ -86,7 +65,7 @@ void write_archive_device(DevScratch& s, const DevArchiveInput& in,
             for (int k = 0; k < 3; ++k)
                 if (arr[k])
                     host_bcrc[k] =
-                        crc32c_threads(reinterpret_cast<const std::uint8_t*>(arr[k]), 8 * N);
+                        ffcz_host::crc32c_threads(reinterpret_cast<const std::uint8_t*>(arr[k]), 8 * N);
         });
     }
     struct Join {

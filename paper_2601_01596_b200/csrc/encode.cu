@@ -637,6 +637,11 @@ __device__ __forceinline__ unsigned long long get_u64(const unsigned char* p) {
     return v;
 }
 
+// One thread per block: the canonical decode of huffman.cpp:205-243, by limits instead of bit by
+// bit: with the next 32 bits of the stream as a left-aligned window w, the code length is the
+// smallest l with w < lim[l] (lim[l] = first code after the length-l codes, left-aligned), and
+// the symbol is table[first_idx[l] + (w >> (32 - l)) - first_code[l]].  The stream is read
+// through a 64-bit big-endian bit buffer refilled a byte at a time.
 __global__ void k_huff_decode(const unsigned char* __restrict__ payload,
                               const unsigned long long* __restrict__ block_off,
                               const unsigned long long* __restrict__ block_first, long long nb,
@@ -646,9 +651,9 @@ __global__ void k_huff_decode(const unsigned char* __restrict__ payload,
         const unsigned char* p = payload + block_off[b];
         const unsigned n = get_u32(p), d = get_u32(p + 4);
         const unsigned char* tab = p + 8;
-        unsigned count[33], first_code[33], first_idx[33];
+        unsigned count[33];
         for (int l = 0; l <= 32; ++l) count[l] = 0;
-        int max_len = 0;
+        int max_len = 0, min_len = 33;
         unsigned prev_len = 0, prev_sym = 0;
         bool bad = false;
         for (unsigned j = 0; j < d; ++j) {
@@ -660,41 +665,53 @@ __global__ void k_huff_decode(const unsigned char* __restrict__ payload,
             prev_sym = sym;
             if (!bad) ++count[len];
             max_len = len > static_cast<unsigned>(max_len) ? len : max_len;
+            min_len = len < static_cast<unsigned>(min_len) ? len : min_len;
         }
         if (bad) {
             atomicExch(err, 1);
             continue;
         }
+        // canonical first codes / indices (huffman.cpp:205-215) and left-aligned limits
+        unsigned first_code[33], first_idx[33];
+        unsigned long long lim[33];
         unsigned code = 0, idx = 0;
-        for (int l = 1; l <= max_len; ++l) {  // huffman.cpp:205-215
+        for (int l = 1; l <= 32; ++l) {
             code <<= 1;
             first_code[l] = code;
             first_idx[l] = idx;
             code += count[l];
             idx += count[l];
+            lim[l] = static_cast<unsigned long long>(code) << (32 - l);  // may be 2^32
         }
         const unsigned long long nbits = get_u64(tab + 5ull * d);
         const unsigned char* bits = tab + 5ull * d + 8;
-        unsigned long long pos = 0;
+        const unsigned long long nbytes = (nbits + 7) / 8;
+        unsigned long long buf = 0, pos = 0, byte_at = 0;
+        int have = 0;  // valid bits in buf (left-aligned at bit 63)
         int* o = out + block_first[b];
-        for (unsigned i = 0; i < n; ++i) {
-            unsigned c = 0;
-            int l = 1;
-            for (;; ++l) {
-                if (l > max_len || pos >= nbits) {
-                    atomicExch(err, 2);
-                    return;
-                }
-                c = (c << 1) | ((bits[pos >> 3] >> (7 - (pos & 7))) & 1u);
-                ++pos;
-                const unsigned rel = c - first_code[l];
-                if (c >= first_code[l] && rel < count[l]) {
-                    const unsigned sym = get_u32(tab + 5ull * (first_idx[l] + rel));
-                    o[i] = static_cast<int>((sym >> 1) ^ (~(sym & 1u) + 1u));  // unzigzag
-                    break;
-                }
+        bool fail = false;
+        for (unsigned i = 0; i < n && !fail; ++i) {
+            while (have <= 56) {
+                const unsigned long long v = byte_at < nbytes ? bits[byte_at] : 0;
+                ++byte_at;
+                buf |= v << (56 - have);
+                have += 8;
             }
+            const unsigned long long w = buf >> 32;  // next 32 bits
+            int l = min_len;
+            while (l <= max_len && w >= lim[l]) ++l;
+            if (l > max_len || pos + static_cast<unsigned long long>(l) > nbits) {
+                fail = true;
+                break;
+            }
+            const unsigned c = static_cast<unsigned>(w >> (32 - l));
+            const unsigned sym = get_u32(tab + 5ull * (first_idx[l] + (c - first_code[l])));
+            o[i] = static_cast<int>((sym >> 1) ^ (~(sym & 1u) + 1u));  // unzigzag
+            buf <<= l;
+            have -= l;
+            pos += l;
         }
+        if (fail) atomicExch(err, 2);
     }
 }
 

@@ -2202,12 +2202,14 @@ int ffcz_cuda_apply_archive(ffcz_cuda_ctx* ctx, const uint8_t* archive, uint64_t
                             double* corrected) {
     return guarded(ctx, [&] {
         if (!archive || !field || !decompressed || !corrected) throw Error(kValidation, "null argument");
+        DebugClock dbg;
         ffcz_host::ParsedArchive a;
         try {
             a = ffcz_host::parse_archive(archive, len);
         } catch (const std::runtime_error& e) {
             throw Error(kFormat, e.what());
         }
+        dbg.mark(*ctx, "apply: container parsed");
         bool same = field->ndim == a.ndim;
         for (int i = 0; same && i < a.ndim; ++i) same = field->dims[i] == a.dims[i];
         if (!same) throw Error(kValidation, "apply_edits: field dims do not match archive dims");
@@ -2233,6 +2235,7 @@ int ffcz_cuda_apply_archive(ffcz_cuda_ctx* ctx, const uint8_t* archive, uint64_t
         bd.freq_re = reinterpret_cast<const double*>(a.freq_re);
         bd.freq_im = reinterpret_cast<const double*>(a.freq_im);
         const Bounds b = upload_bounds(c, g, bd, false);
+        dbg.mark(c, "apply: bounds uploaded");
         const long long ws = (N + 31) / 32, wf = (Nc + 31) / 32;
         unsigned* ks = c.b<unsigned>("ap_keep_s", ws);
         unsigned* kf = c.b<unsigned>("ap_keep_f", wf);
@@ -2274,8 +2277,10 @@ int ffcz_cuda_apply_archive(ffcz_cuda_ctx* ctx, const uint8_t* archive, uint64_t
                                   static_cast<long long>(off.size()), codes);
             return codes;
         };
+        dbg.mark(c, "apply: flags uploaded");
         int* cs = decode(a.spatial_payload, a.n_spatial, "ap_codes_s");
         int* cf = decode(a.frequency_payload, 2 * a.n_frequency, "ap_codes_f");
+        dbg.mark(c, "apply: huffman decoded");
         double* spat = c.b<double>("ap_spat", N);
         double2* freq = c.b<double2>("ap_freq", g.half_elems());
         FFCZ_CUDA_CHECK(cudaMemsetAsync(spat, 0, 8 * N, st));
@@ -2308,6 +2313,7 @@ int ffcz_cuda_apply_archive(ffcz_cuda_ctx* ctx, const uint8_t* archive, uint64_t
             FFCZ_LAUNCH_CHECK();
             c.sync();  // `er` is pageable and goes out of scope
         }
+        dbg.mark(c, "apply: edits scattered");
         FftPlan<double> plan{g, &c.tw64};
         double* fpart = c.b<double>("ap_fpart", N);
         double2* work = c.b<double2>("ap_work", g.half_elems());
