@@ -273,7 +273,14 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
 }
 
 template <class T, int M> struct RowCfg {
+    // FP64 M = 512 (1024-sample rows) ties at three stages for E = 8 and E = 16; E = 16 gives 32
+    // threads per row, i.e. the warp-shuffle paired split / merge (k_row_*_sh) instead of the
+    // shared-memory round trip (FFCZ_ROW512_E8 at build time restores E = 8)
+#ifdef FFCZ_ROW512_E8
     static constexpr int E = pick_E<T>(M);
+#else
+    static constexpr int E = (sizeof(T) == 8 && M == 512) ? 16 : pick_E<T>(M);
+#endif
     static constexpr int TT = M / E;
     static constexpr int MAXT = max_threads<T, E>();
 };
