@@ -352,7 +352,7 @@ inline bool mixed_enabled() {
     }();
     return on;
 }
-constexpr size_t kMixedSmemMax = 200 * 1024;
+constexpr size_t kMixedSmemMax = 220 * 1024;  // (the padded 1000-point tiles keep 4 columns)
 inline bool mixed_pipe_enabled() {  // FFCZ_MIXED_PIPE=0: the one-tile-per-CTA column pass (A/B)
     static const bool on = [] {
         const char* e = std::getenv("FFCZ_MIXED_PIPE");
@@ -369,8 +369,9 @@ inline size_t mixed_smem_target() {  // FFCZ_MIXED_SMEM=<KB> for tile-size sweep
 }
 // lines per CTA: as many as fit the target (at least one line within the maximum), at most 16
 template <class T>
-inline int mixed_lines(long long L, long long nlines) {
-    const size_t per = 2 * sizeof(cplx<T>) * static_cast<size_t>(L);
+inline int mixed_lines(long long L, long long nlines, bool pad = true) {
+    const size_t per = 2 * sizeof(cplx<T>) *
+                       static_cast<size_t>(pad ? mixed::padded(static_cast<int>(L)) : L);
     if (per > kMixedSmemMax) return 0;
     long long b = std::max<long long>(1, static_cast<long long>(mixed_smem_target() / per));
     b = std::min<long long>({b, 16, std::max<long long>(1, nlines)});
@@ -401,7 +402,8 @@ void launch_col(long long L, int dir, const cplx<T>* src, cplx<T>* dst, long lon
     } else {
         if (detail::mixed_pipe_enabled() && detail::mixed_enabled()) {
             // 3 rotating tile buffers, B columns each (at most 16), within ~96 KB per CTA
-            const size_t per = 3 * sizeof(cplx<T>) * static_cast<size_t>(L);
+            const size_t per =
+                3 * sizeof(cplx<T>) * static_cast<size_t>(mixed::padded(static_cast<int>(L)));
             if (per <= detail::kMixedSmemMax) {
                 static const long long kb = [] {
                     const char* e = std::getenv("FFCZ_MIXED_PIPE_KB");
@@ -426,7 +428,7 @@ void launch_col(long long L, int dir, const cplx<T>* src, cplx<T>* dst, long lon
             }
         }
         if (const int Bm = detail::mixed_enabled() ? detail::mixed_lines<T>(L, ncols) : 0) {
-            const size_t smem = 2 * sizeof(cplx<T>) * L * Bm;
+            const size_t smem = 2 * sizeof(cplx<T>) * mixed::padded(static_cast<int>(L)) * Bm;
             detail::set_smem(k_col_mixed<T>, smem);
             dim3 grid((ncols + Bm - 1) / Bm, static_cast<unsigned>(nplanes));
             k_col_mixed<T><<<grid, 256, smem, st>>>(src, dst, make_mixed_plan(L), row_stride,
@@ -474,7 +476,7 @@ void launch_row_r2c(long long n2, const T* in, long long in_stride, cplx<T>* out
         }
     }
     const long long Lm = (n2 % 2 == 0) ? n2 / 2 : n2;  // packed real row: n2/2 points
-    if (const int R = detail::mixed_enabled() ? detail::mixed_lines<T>(Lm + 1, nrows) : 0) {
+    if (const int R = detail::mixed_enabled() ? detail::mixed_lines<T>(Lm + 1, nrows, false) : 0) {
         const size_t smem = 2 * sizeof(cplx<T>) * (Lm + 1) * R;
         detail::set_smem(k_row_r2c_mixed<T>, smem);
         k_row_r2c_mixed<T><<<static_cast<unsigned>((nrows + R - 1) / R), 256, smem, st>>>(
@@ -557,7 +559,7 @@ void launch_row_c2r(long long n2, const cplx<T>* in, long long in_stride, T* out
         }
     }
     const long long Lm = (n2 % 2 == 0) ? n2 / 2 : n2;
-    if (const int R = detail::mixed_enabled() ? detail::mixed_lines<T>(Lm + 1, nrows) : 0) {
+    if (const int R = detail::mixed_enabled() ? detail::mixed_lines<T>(Lm + 1, nrows, false) : 0) {
         const size_t smem = 2 * sizeof(cplx<T>) * (Lm + 1) * R;
         detail::set_smem(k_row_c2r_mixed<T>, smem);
         k_row_c2r_mixed<T><<<static_cast<unsigned>((nrows + R - 1) / R), 256, smem, st>>>(

@@ -55,6 +55,19 @@ inline MixedPlan make_mixed_plan(long long L) {
 
 namespace mixed {
 
+// Shared-memory position of line element i: one padding slot after every 8 elements.  The early
+// Stockham stages store butterfly j's outputs R elements apart (R = 2, 4, 8), which put the
+// lanes of a warp on the same banks (8-way conflicts: the passes were shared-memory bound at
+// 84.5 % L1/TEX, profiles/r01_ncu_mixed_radix_500_v2.txt); with the pad, rows j*R land on
+// alternating bank halves and every warp access is the minimum number of wavefronts.
+__host__ __device__ __forceinline__ int sw(int i) { return i + (i >> 3); }
+// padded line length (slots) of an L-element line
+__host__ __device__ __forceinline__ int padded(int L) { return L + (L >> 3) + 1; }
+// the column tiles use the padded positions; the row passes (one line per warp group, lanes on
+// consecutive butterflies) measured slower with them (0.35 -> 0.31 of HBM at 500^3) and keep
+// the dense layout
+template <bool PAD> __device__ __forceinline__ int at(int i) { return PAD ? sw(i) : i; }
+
 template <class C> __device__ __forceinline__ C conjc(C a) { a.y = -a.y; return a; }
 
 // forward DFT of R points held in registers
@@ -165,7 +178,7 @@ __device__ __forceinline__ int mod_ns(int j, int ns, unsigned mul) {
 
 // One Stockham stage: butterfly j reads j + t m (t < R), twiddles by W_{ns R}^{k t}
 // (k = j mod ns), writes (j - k) R + k + t ns.
-template <class T, int R>
+template <class T, int R, bool PAD>
 __device__ __forceinline__ void stage_reg(const cplx<T>* __restrict__ in, cplx<T>* __restrict__ out,
                                           int L, int ns, unsigned mul, int si, int sl,
                                           TileLane tl, const cplx<T>* __restrict__ wl, int wmul,
@@ -177,19 +190,19 @@ __device__ __forceinline__ void stage_reg(const cplx<T>* __restrict__ in, cplx<T
         cplx<T> a[R];
 #pragma unroll
         for (int t = 0; t < R; ++t) {
-            a[t] = in[(j + t * m) * si + lo];
+            a[t] = in[at<PAD>(j + t * m) * si + lo];
             if (cin) a[t].y = -a[t].y;
             if (t > 0 && k > 0) a[t] = cmul(a[t], __ldg(&wl[k * t * wstep]));
         }
         bfly<T, R>(a);
         const int o = (j - k) * R + k;
 #pragma unroll
-        for (int t = 0; t < R; ++t) out[(o + t * ns) * si + lo] = a[t];
+        for (int t = 0; t < R; ++t) out[at<PAD>(o + t * ns) * si + lo] = a[t];
     }
 }
 
 // Generic prime radix: each output of a butterfly sums its R twiddled inputs from shared memory.
-template <class T>
+template <class T, bool PAD>
 __device__ __forceinline__ void stage_gen(const cplx<T>* __restrict__ in, cplx<T>* __restrict__ out,
                                           int L, int R, int ns, unsigned mul, int si, int sl,
                                           TileLane tl, const cplx<T>* __restrict__ wl, int wmul,
@@ -204,7 +217,7 @@ __device__ __forceinline__ void stage_gen(const cplx<T>* __restrict__ in, cplx<T
             T ax = 0, ay = 0;
             int q = 0;
             for (int t = 0; t < R; ++t) {
-                cplx<T> x = in[(j + t * m) * si + lo];
+                cplx<T> x = in[at<PAD>(j + t * m) * si + lo];
                 if (cin) x.y = -x.y;
                 const cplx<T> p = cmul(x, __ldg(&wl[q * wmul]));
                 ax += p.x;
@@ -212,7 +225,7 @@ __device__ __forceinline__ void stage_gen(const cplx<T>* __restrict__ in, cplx<T
                 q += step;
                 while (q >= L) q -= L;
             }
-            out[((j - k) * R + k + u * ns) * si + lo] = mkc<T>(ax, ay);
+            out[at<PAD>((j - k) * R + k + u * ns) * si + lo] = mkc<T>(ax, ay);
         }
     }
 }
@@ -220,7 +233,7 @@ __device__ __forceinline__ void stage_gen(const cplx<T>* __restrict__ in, cplx<T
 // Runs every stage; returns the buffer holding the natural-order result.  wl[q * wmul] = W_L^q
 // (wmul = 2 when the table is the 2L-point one of a packed real row).  Every thread of the CTA
 // calls it (idle lanes included: the stage barriers are CTA-wide).
-template <class T>
+template <class T, bool PAD>
 __device__ cplx<T>* run_stages(cplx<T>* A, cplx<T>* B, const MixedPlan& p, int si, int sl,
                                int nlines, TileLane tl, const cplx<T>* __restrict__ wl,
                                int wmul = 1, bool conj_in = false) {
@@ -232,13 +245,13 @@ __device__ cplx<T>* run_stages(cplx<T>* A, cplx<T>* B, const MixedPlan& p, int s
         const bool cin = conj_in && s == 0;
         if (on) {
             switch (r) {
-                case 2: stage_reg<T, 2>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
-                case 3: stage_reg<T, 3>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
-                case 4: stage_reg<T, 4>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
-                case 8: stage_reg<T, 8>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
-                case 5: stage_reg<T, 5>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
-                case 7: stage_reg<T, 7>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
-                default: stage_gen<T>(A, B, p.L, r, ns, mul, si, sl, tl, wl, wmul, cin); break;
+                case 2: stage_reg<T, 2, PAD>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
+                case 3: stage_reg<T, 3, PAD>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
+                case 4: stage_reg<T, 4, PAD>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
+                case 8: stage_reg<T, 8, PAD>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
+                case 5: stage_reg<T, 5, PAD>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
+                case 7: stage_reg<T, 7, PAD>(A, B, p.L, ns, mul, si, sl, tl, wl, wmul, cin); break;
+                default: stage_gen<T, PAD>(A, B, p.L, r, ns, mul, si, sl, tl, wl, wmul, cin); break;
             }
         }
         __syncthreads();
@@ -267,7 +280,7 @@ __global__ void __launch_bounds__(256) k_col_mixed(const cplx<T>* __restrict__ s
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int L = p.L;
     cplx<T>* A = reinterpret_cast<cplx<T>*>(smem_raw);
-    cplx<T>* Bf = A + static_cast<size_t>(L) * B;
+    cplx<T>* Bf = A + static_cast<size_t>(mixed::padded(L)) * B;
     const long long base = static_cast<long long>(blockIdx.y) * plane_stride +
                            static_cast<long long>(blockIdx.x) * B;
     const int nb = min(B, ncols - static_cast<int>(blockIdx.x) * B);
@@ -286,15 +299,16 @@ __global__ void __launch_bounds__(256) k_col_mixed(const cplx<T>* __restrict__ s
 #pragma unroll
             for (int u = 0; u < kMixedU; ++u) {
                 const int i = i0 + u * TL;
-                if (i < L) A[i * B + b] = dir < 0 ? v[u] : mixed::conjc(v[u]);
+                if (i < L) A[mixed::sw(i) * B + b] = dir < 0 ? v[u] : mixed::conjc(v[u]);
             }
         }
     }
     __syncthreads();
-    const cplx<T>* R = mixed::run_stages<T>(A, Bf, p, B, 1, B, tl, wl);
+    const cplx<T>* R = mixed::run_stages<T, true>(A, Bf, p, B, 1, B, tl, wl);
     if (b < nb)
         for (int i = tl.jt; i < L; i += TL)
-            dst[base + i * row_stride + b] = dir < 0 ? R[i * B + b] : mixed::conjc(R[i * B + b]);
+            dst[base + i * row_stride + b] =
+                dir < 0 ? R[mixed::sw(i) * B + b] : mixed::conjc(R[mixed::sw(i) * B + b]);
 }
 
 __device__ __forceinline__ void cp_async_elem(void* dst, const void* src, int bytes, bool valid) {
@@ -324,7 +338,7 @@ __global__ void __launch_bounds__(256) k_col_mixed_pipe(const cplx<T>* __restric
     if (gated(gate)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int L = p.L;
-    const size_t tile_elems = static_cast<size_t>(L) * B;
+    const size_t tile_elems = static_cast<size_t>(mixed::padded(L)) * B;
     cplx<T>* buf0 = reinterpret_cast<cplx<T>*>(smem_raw);
     const int nblk = (ncols + B - 1) / B;
     const int TL = blockDim.x / B;
@@ -344,7 +358,7 @@ __global__ void __launch_bounds__(256) k_col_mixed_pipe(const cplx<T>* __restric
             const bool ok = b < nb;
             const cplx<T>* g = src + base + (ok ? b : 0);
             for (int i = tl.jt; i < L; i += TL)
-                cp_async_elem(&buf[i * B + b], g + i * row_stride, sizeof(cplx<T>), ok);
+                cp_async_elem(&buf[mixed::sw(i) * B + b], g + i * row_stride, sizeof(cplx<T>), ok);
         }
         cp_async_commit();
     };
@@ -360,12 +374,13 @@ __global__ void __launch_bounds__(256) k_col_mixed_pipe(const cplx<T>* __restric
         else cp_async_commit();
         cp_async_wait1();
         __syncthreads();
-        const cplx<T>* R = mixed::run_stages<T>(cur, spare, p, B, 1, B, tl, wl, 1, dir > 0);
+        const cplx<T>* R = mixed::run_stages<T, true>(cur, spare, p, B, 1, B, tl, wl, 1, dir > 0);
         int nb;
         const long long base = tile_base(tile, nb);
         if (b < nb)
             for (int i = tl.jt; i < L; i += TL)
-                dst[base + i * row_stride + b] = dir < 0 ? R[i * B + b] : mixed::conjc(R[i * B + b]);
+                dst[base + i * row_stride + b] =
+                    dir < 0 ? R[mixed::sw(i) * B + b] : mixed::conjc(R[mixed::sw(i) * B + b]);
         __syncthreads();
     }
 }
@@ -414,12 +429,12 @@ __global__ void __launch_bounds__(256) k_row_r2c_mixed(const T* __restrict__ in,
 #pragma unroll
             for (int u = 0; u < kMixedU; ++u) {
                 const int i = i0 + u * tl.TL;
-                if (i < L) A[r * sl + i] = mkc<T>(v0[u], v1[u]);
+                if (i < L) A[r * sl + (i)] = mkc<T>(v0[u], v1[u]);
             }
         }
     }
     __syncthreads();
-    const cplx<T>* Z = mixed::run_stages<T>(A, Bf, p, 1, sl, R, tl, wl, packed ? 2 : 1);
+    const cplx<T>* Z = mixed::run_stages<T, false>(A, Bf, p, 1, sl, R, tl, wl, packed ? 2 : 1);
     if (r < nr) {
         for (int k = tl.jt; k < h; k += tl.TL) {
             cplx<T> X;
@@ -430,7 +445,7 @@ __global__ void __launch_bounds__(256) k_row_r2c_mixed(const T* __restrict__ in,
                 const cplx<T> zo = mkc<T>((zk.y + zn.y) * hf, (zn.x - zk.x) * hf);
                 X = cadd(ze, cmul(zo, __ldg(&wl[k])));
             } else {
-                X = Z[r * sl + k];
+                X = Z[r * sl + (k)];
             }
             out[(row0 + r) * out_stride + k] = X;
         }
@@ -474,10 +489,10 @@ __global__ void __launch_bounds__(256) k_row_c2r_mixed(const cplx<T>* __restrict
                 const int k = k0 + u * tl.TL;
                 if (k >= h) continue;
                 if (packed) {
-                    Bf[r * sl + k] = v[u];
+                    Bf[r * sl + (k)] = v[u];
                 } else {
-                    A[r * sl + k] = mixed::conjc(v[u]);
-                    if (k > 0 && n2 - k >= h) A[r * sl + n2 - k] = v[u];
+                    A[r * sl + (k)] = mixed::conjc(v[u]);
+                    if (k > 0 && n2 - k >= h) A[r * sl + (n2 - k)] = v[u];
                 }
             }
         }
@@ -486,26 +501,26 @@ __global__ void __launch_bounds__(256) k_row_c2r_mixed(const cplx<T>* __restrict
     if (packed) {
         if (r < R) {
             for (int k = tl.jt; k < L; k += tl.TL) {
-                const cplx<T> xk = Bf[r * sl + k], xn = Bf[r * sl + L - k];
+                const cplx<T> xk = Bf[r * sl + (k)], xn = Bf[r * sl + (L - k)];
                 const cplx<T> s = mkc<T>(xk.x + xn.x, xk.y - xn.y);   // X[k] + conj X[M-k]
                 const cplx<T> d = mkc<T>(xk.x - xn.x, xk.y + xn.y);   // X[k] - conj X[M-k]
                 const cplx<T> o = cmulc(d, __ldg(&wl[k]));           // d * conj W^k
-                A[r * sl + k] = mixed::conjc(mkc<T>(s.x - o.y, s.y + o.x));  // conj(s + i o)
+                A[r * sl + (k)] = mixed::conjc(mkc<T>(s.x - o.y, s.y + o.x));  // conj(s + i o)
             }
         }
         __syncthreads();
     }
-    const cplx<T>* z = mixed::run_stages<T>(A, Bf, p, 1, sl, R, tl, wl, packed ? 2 : 1);
+    const cplx<T>* z = mixed::run_stages<T, false>(A, Bf, p, 1, sl, R, tl, wl, packed ? 2 : 1);
     if (r < nr) {
         T* orow = out + (row0 + r) * out_stride;
         if (packed) {
             for (int i = tl.jt; i < L; i += tl.TL) {
-                const cplx<T> v = z[r * sl + i];  // conj z: (x[2i], -x[2i+1])
+                const cplx<T> v = z[r * sl + (i)];  // conj z: (x[2i], -x[2i+1])
                 orow[2 * i] = v.x * scale;
                 orow[2 * i + 1] = -v.y * scale;
             }
         } else {
-            for (int i = tl.jt; i < n2; i += tl.TL) orow[i] = z[r * sl + i].x * scale;
+            for (int i = tl.jt; i < n2; i += tl.TL) orow[i] = z[r * sl + (i)].x * scale;
         }
     }
 }
