@@ -245,13 +245,17 @@ typedef enum ffcz_cuda_slab_opcode {
                                      converged); max_iters in n_total (projection.cpp:106-116) */
 } ffcz_cuda_slab_opcode;
 
+/* ffcz_cuda_slab_op.pad flag: a one-rank slab (B layout == natural layout); the COL0 ops
+ * transform axis 1 and FWD_LOCAL / INV_* transform axis 0 (the single-volume engine's order) */
+#define FFCZ_SLAB_SWAP_AXES 1
+
 typedef struct ffcz_cuda_slab_op {
     int32_t op;          /* ffcz_cuda_slab_opcode */
     int32_t dir;         /* COL0_PLAIN: -1 forward, +1 inverse */
     int32_t first;       /* CLIP passes: the first clip pass (dense F / S write) */
     int32_t in_dtype;    /* ffcz_cuda_dtype of orig / dec */
     int32_t m;           /* GATE: quantiser m */
-    int32_t pad;
+    int32_t pad;         /* flags: FFCZ_SLAB_SWAP_AXES */
     uint64_t d0, d1, n2; /* local geometry of the buffer(s) the op works on */
     uint64_t n_total;    /* global sample count (C2R normalisation) */
     double e, delta, fscale, slack;

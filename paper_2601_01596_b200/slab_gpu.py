@@ -53,6 +53,11 @@ class GpuSlabBackend:
         self.stream = torch.cuda.Stream(self.device)
         self.ctx = ctx or Context(self.device.index or 0, self.stream.cuda_stream)
         self.e_arr = self.dA = self.dB = None
+        self.swap_axes = False
+
+    def set_axes(self, swap):
+        """One-rank slab: the axis-0 ops run on axis 1 and the local ops on axis 0."""
+        self.swap_axes = bool(swap)
 
     # -- per-point / per-component bounds (slab.py set_bounds) ----------------------------------
     def set_bounds(self, e_arr, dA, dB):
@@ -103,6 +108,7 @@ class GpuSlabBackend:
             o.p[i] = None if t is None else t.data_ptr()
         if gate is not None:   # device-resident loop: the op returns at once once done is set
             o.p[9] = gate.data_ptr()
+        o.pad = 1 if self.swap_axes else 0   # FFCZ_SLAB_SWAP_AXES
         out = (C.c_double * 4)()
         _check(self.lib.ffcz_cuda_slab(self.ctx.handle, C.byref(o), out))
         return list(out)
