@@ -114,6 +114,39 @@ class Comm:
         return torch.cat([o[: int(kk.item())] for o, kk in zip(outs, ks)])
 
 
+class EscapeList:
+    """The global escape list in std::map order (spatial by index, then frequency by half index)
+    as columns; iterating / indexing yields (is_freq, global index, re, im) tuples.  (Tuples per
+    element cost 0.19 s for the 263 K escapes of 1024^3 config 4; the columns cost nothing.)"""
+
+    def __init__(self, sp, fr):
+        self.sp_index = sp[:, 0].astype(np.int64)
+        self.sp_value = np.ascontiguousarray(sp[:, 1])
+        self.fr_index = fr[:, 0].astype(np.int64)
+        self.fr_re = np.ascontiguousarray(fr[:, 1])
+        self.fr_im = np.ascontiguousarray(fr[:, 2])
+
+    def __len__(self):
+        return len(self.sp_index) + len(self.fr_index)
+
+    def __getitem__(self, i):
+        if i < 0:
+            i += len(self)
+        ns = len(self.sp_index)
+        if i < ns:
+            return (False, int(self.sp_index[i]), float(self.sp_value[i]), 0.0)
+        j = i - ns
+        if j >= len(self.fr_index):
+            raise IndexError(i)
+        return (True, int(self.fr_index[j]), float(self.fr_re[j]), float(self.fr_im[j]))
+
+    def __iter__(self):
+        yield from zip([False] * len(self.sp_index), self.sp_index.tolist(),
+                       self.sp_value.tolist(), [0.0] * len(self.sp_index))
+        yield from zip([True] * len(self.fr_index), self.fr_index.tolist(), self.fr_re.tolist(),
+                       self.fr_im.tolist())
+
+
 @dataclass
 class SlabResult:
     """This rank's part of ffcz::CorrectionResult (pipeline.hpp:11-16).  Flags and codes cover
@@ -132,7 +165,7 @@ class SlabResult:
     frequency_flags: object          # this rank's c0*n1*H half-grid flags
     spatial_codes: object            # int32, ascending index order (backend tensor / array)
     frequency_codes: object          # int32, interleaved (Re, Im)
-    escapes: list = field(default_factory=list)   # (is_freq, global index, re, im), map order
+    escapes: object = field(default_factory=list)  # EscapeList: (is_freq, index, re, im), map order
     corrected: object = None         # this rank's FP64 corrected slab (backend tensor)
 
 
@@ -376,13 +409,7 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E, Delta, m: int = 16,
     sp_all = comm.all_gather_rows(sp).cpu().numpy()
     fr_all = comm.all_gather_rows(fr).cpu().numpy()
     fr_all = fr_all[np.argsort(fr_all[:, 0], kind="stable")]
-    # (tuples built from whole-column tolist()s: a per-element loop took 0.19 s for the 263 K
-    # escapes of 1024^3 config 4)
-    ns_, nf_ = sp_all.shape[0], fr_all.shape[0]
-    escapes = list(zip([False] * ns_, sp_all[:, 0].astype(np.int64).tolist(),
-                       sp_all[:, 1].tolist(), [0.0] * ns_))
-    escapes += list(zip([True] * nf_, fr_all[:, 0].astype(np.int64).tolist(),
-                        fr_all[:, 1].tolist(), fr_all[:, 2].tolist()))
+    escapes = EscapeList(sp_all, fr_all)
     _phase("escape lists")
     return SlabResult(
         iterations=max(passes, 1), converged=converged, residual_f=residual_f,
