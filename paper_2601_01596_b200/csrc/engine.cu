@@ -817,6 +817,7 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
                                          c.ctl};
                 hk.sc_zero = sc_zero;
                 hk.dview = dview;
+                hk.keep_words = keep_s;
                 // half spectrum in, orig + dec, spat_cur (unless still zero), the checked view
                 // out (the R2C's input), eps_v (reference order), corrected, per-point E
                 inverse_and_row(hk, 16.0 * Nc + 2.0 * sizeof(TI) * N + (sc_zero ? 0.0 : 8.0 * N) +
