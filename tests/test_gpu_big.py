@@ -73,3 +73,30 @@ def test_big_case_matches_reference(P, name):
     assert float(np.max(np.abs(corr - c.original) - c.E)) <= 0.0
     rel = cases.freq_excess_per_component(c.original, corr, c.Dre, c.Dim)
     assert rel <= 1e-15, rel
+
+
+@pytest.mark.parametrize("name", [n for n in ("config4_comb256", "config3_xrd2048") if n in GOLD])
+def test_big_case_mixed_policy(P, name):
+    """The mixed FP32 -> FP64 policy (SURVEY.md §8c parity contract for the FP32 target):
+    iterations within +-1 of the reference, converged and verified, both bounds exact on the
+    FP64 corrected field.  Flags follow the FP32 phase's round-off on borderline components
+    (config 4 at 256^3: a few in 10^5 differ; SURVEY.md §8c(5)-(6) pins them only in FP64
+    mode): active counts within 1e-4 of the reference's."""
+    g = GOLD[name]
+    c = cases.big_case(name)
+    r = P.correct(c.original.astype(np.float32), c.decompressed.astype(np.float32),
+                  P.DualBounds(c.E, c.Dre, c.Dim), c.m, c.max_iters, c.precision,
+                  want_archive=False, want_edits=True, want_corrected=True, policy="mixed")
+    rep = r.report
+    print(name, "mixed: iterations", rep.iterations, "(fp32", r.iterations_fp32, ") ref",
+          g["iterations"])
+    assert abs(rep.iterations - g["iterations"]) <= 1
+    assert rep.converged == g["converged"] and r.verify_ok
+    for k in ("active_spatial", "active_frequency"):
+        mine, ref = getattr(rep, k), g[k]
+        print(name, k, mine, ref)
+        assert abs(mine - ref) <= max(2, 1e-4 * ref), (k, mine, ref)
+    corr = r.corrected
+    del r
+    assert float(np.max(np.abs(corr - c.original) - c.E)) <= 0.0
+    assert cases.freq_excess_per_component(c.original, corr, c.Dre, c.Dim) <= 1e-15
