@@ -233,12 +233,12 @@ struct HookFRebuild {
     template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
     template <class C>
     __device__ __forceinline__ void post(C& v, long long off, int) {
-        double2 f = make_double2(0.0, 0.0);
-        if (moved[off]) {
-            const double2 d = __ldg(&delta[off]);
-            f = make_double2(d.x - v.x, d.y - v.y);
-        }
-        F[off] = f;
+        // both loads unconditional and through the non-coherent path, so the compiler can issue
+        // the tile's loads ahead of its F stores (a plain load of `moved` after each F store
+        // serialised them: 10.3 ms for 26 GB at 1024^3)
+        const unsigned char mv = __ldg(&moved[off]);
+        const double2 d = __ldg(&delta[off]);
+        F[off] = mv ? make_double2(d.x - v.x, d.y - v.y) : make_double2(0.0, 0.0);
     }
     __device__ __forceinline__ void finish() {}
 };
@@ -617,12 +617,9 @@ struct HookFRebuildB {
     template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
     template <class C>
     __device__ __forceinline__ void post(C& v, long long off, int) {
-        double2 f = make_double2(0.0, 0.0);
-        if (moved[off]) {
-            const double2 d = __ldg(&delta[off]);
-            f = make_double2(d.x - v.x, d.y - v.y);
-        }
-        F[off] = f;
+        const unsigned char mv = __ldg(&moved[off]);  // hoistable loads (HookFRebuild)
+        const double2 d = __ldg(&delta[off]);
+        F[off] = mv ? make_double2(d.x - v.x, d.y - v.y) : make_double2(0.0, 0.0);
     }
     __device__ __forceinline__ void finish() {}
 };
