@@ -10,6 +10,9 @@
 // One host sync for the four stream lengths, then every piece lands at its offset in the pinned
 // archive (D2H for device pieces, threaded memcpy for host bound arrays).
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -50,6 +53,16 @@ void write_archive_device(DevScratch& s, const DevArchiveInput& in,
                           const std::function<void*(std::size_t)>& host_alloc, std::uint8_t** out,
                           std::uint64_t* out_len) {
     cudaStream_t st = s.stream;
+    // FFCZ_DEBUG_TIMING=1: host timestamps of the archive's phases on stderr (synchronises)
+    static const bool dbg_on = std::getenv("FFCZ_DEBUG_TIMING") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!dbg_on) return;
+        cudaStreamSynchronize(st);
+        std::fprintf(stderr, "[ffcz] archive: %-22s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                               t_start).count());
+    };
     std::uint64_t N = 1;
     for (int a = 0; a < in.ndim; ++a) N *= in.dims[a];
 
@@ -80,11 +93,15 @@ void write_archive_device(DevScratch& s, const DevArchiveInput& in,
     unsigned char* dst_ptr[4] = {};
     deflate_device(s, "arc_sf", in.spatial_flags, in.spatial_flag_bytes, &dst_ptr[0], lens + 0);
     deflate_device(s, "arc_ff", in.frequency_flags, in.frequency_flag_bytes, &dst_ptr[1], lens + 1);
+    mark("flag streams");
     unsigned char* pay = nullptr;
     unsigned long long pl = huffman_encode_device(s, in.spatial_codes, in.n_spatial, &pay);
     deflate_device(s, "arc_si", pay, pl, &dst_ptr[2], lens + 2);
+    mark("spatial index stream");
     pl = huffman_encode_device(s, in.frequency_codes, 2 * in.n_frequency, &pay);
+    mark("frequency huffman");
     deflate_device(s, "arc_fi", pay, pl, &dst_ptr[3], lens + 3);
+    mark("frequency outer stage");
 
     // ---- bound arrays: raw CRC on the device when resident there ---------------------------
     const double* arrays[3] = {in.spatial_per_point ? in.spatial_values : nullptr,
@@ -152,6 +169,7 @@ void write_archive_device(DevScratch& s, const DevArchiveInput& in,
     const std::uint64_t total = pre.size() + mid.size() + nbnd + tail.size() + hl[0] + hl[1] +
                                 hl[2] + hl[3] + esc_bytes;
     auto* a = static_cast<std::uint8_t*>(host_alloc(total + 1));
+    mark("lengths, CRC, host buffer");
     std::uint64_t off = 0;
     auto put_host = [&](const std::uint8_t* p, std::uint64_t n) {
         std::memcpy(a + off, p, n);
@@ -188,6 +206,7 @@ void write_archive_device(DevScratch& s, const DevArchiveInput& in,
         }
     }
     FFCZ_CUDA_CHECK(cudaStreamSynchronize(st));
+    mark("pieces copied out");
     *out = a;
     *out_len = total;
 }

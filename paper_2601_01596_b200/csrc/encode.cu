@@ -15,6 +15,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -37,6 +39,33 @@ __global__ void k_keys(const int* __restrict__ codes, unsigned long long n,
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x)
         keys[i] = ((i >> kBlockShift) << 32) | zz(codes[i]);
+}
+
+__global__ void k_zz_max(const int* __restrict__ codes, unsigned long long n, unsigned* zmax) {
+    unsigned m = 0;
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        m = max(m, zz(codes[i]));
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(zmax, m);
+}
+
+__global__ void k_keys32(const int* __restrict__ codes, unsigned long long n, int bs,
+                         unsigned* keys) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        keys[i] = static_cast<unsigned>((i >> kBlockShift) << bs) | zz(codes[i]);
+}
+
+__global__ void k_widen_keys(const unsigned* __restrict__ k32, const int* nruns_p, int bs,
+                             unsigned long long* ukeys) {
+    const long long R = *nruns_p;
+    const unsigned mask = bs >= 32 ? ~0u : ((1u << bs) - 1u);
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < R;
+         r += (long long)gridDim.x * blockDim.x) {
+        const unsigned k = k32[r];
+        ukeys[r] = (static_cast<unsigned long long>(k >> bs) << 32) | (k & mask);
+    }
 }
 
 // first run of every block (runs are sorted by (block, symbol)); run_start[nb] = nruns
@@ -523,6 +552,16 @@ unsigned grid_n(unsigned long long n, int t = 256) {
 unsigned long long huffman_encode_device(DevScratch& s, const int* codes, unsigned long long n,
                                          unsigned char** payload) {
     cudaStream_t st = s.stream;
+    // FFCZ_DEBUG_TIMING=1: host timestamps of the encoder's steps on stderr (synchronises)
+    static const bool dbg_on = std::getenv("FFCZ_DEBUG_TIMING") != nullptr;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!dbg_on) return;
+        cudaStreamSynchronize(st);
+        std::fprintf(stderr, "[ffcz] huffman: %-20s %9.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                               t_start).count());
+    };
     const long long nb = static_cast<long long>((n + (1ull << kBlockShift) - 1) >> kBlockShift);
     if (n == 0) {
         unsigned char* out = static_cast<unsigned char*>(s.get("huf_out", 8));
@@ -536,18 +575,49 @@ unsigned long long huffman_encode_device(DevScratch& s, const int* codes, unsign
     auto* ukeys = static_cast<unsigned long long*>(s.get("huf_ukeys", 8 * n));
     auto* counts = static_cast<int*>(s.get("huf_counts", 4 * n));
     auto* nruns = static_cast<int*>(s.get("huf_nruns", 8));
-    k_keys<<<grid_n(n), 256, 0, st>>>(codes, n, keys);
+    // the widest zigzag symbol decides the key layout: when block and symbol bits fit 32 bits
+    // the sort and run-length run on 32-bit keys (block << bs | zz: half the traffic and 4 radix
+    // passes instead of 6 at 1024^3), widened to (block << 32 | zz) for the later steps
+    auto* zmax = static_cast<unsigned*>(s.get("huf_zmax", 4));
+    FFCZ_CUDA_CHECK(cudaMemsetAsync(zmax, 0, 4, st));
+    k_zz_max<<<grid_n(n), 256, 0, st>>>(codes, n, zmax);
     FFCZ_LAUNCH_CHECK();
-    int end_bit = 32;
-    while ((1ll << (end_bit - 32)) < nb) ++end_bit;
-    cub_call(s, "huf_tmp_sort", [&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortKeys(t, b, keys, skeys, static_cast<int64_t>(n), 0,
-                                              end_bit, st);
-    });
-    cub_call(s, "huf_tmp_rle", [&](void* t, size_t& b) {
-        return cub::DeviceRunLengthEncode::Encode(t, b, skeys, ukeys, counts, nruns,
-                                                  static_cast<int64_t>(n), st);
-    });
+    unsigned h_zmax = 0;
+    FFCZ_CUDA_CHECK(cudaMemcpyAsync(&h_zmax, zmax, 4, cudaMemcpyDeviceToHost, st));
+    FFCZ_CUDA_CHECK(cudaStreamSynchronize(st));
+    int bs = 1, bb = 0;
+    while (bs < 32 && (1ull << bs) <= h_zmax) ++bs;
+    while ((1ll << bb) < nb) ++bb;
+    const bool narrow = bs + bb <= 32;
+    if (narrow) {
+        auto* k32 = reinterpret_cast<unsigned*>(keys);
+        auto* s32 = k32 + n;
+        auto* u32k = reinterpret_cast<unsigned*>(skeys);
+        k_keys32<<<grid_n(n), 256, 0, st>>>(codes, n, bs, k32);
+        FFCZ_LAUNCH_CHECK();
+        cub_call(s, "huf_tmp_sort32", [&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortKeys(t, b, k32, s32, static_cast<int64_t>(n), 0,
+                                                  bs + bb, st);
+        });
+        cub_call(s, "huf_tmp_rle32", [&](void* t, size_t& b) {
+            return cub::DeviceRunLengthEncode::Encode(t, b, s32, u32k, counts, nruns,
+                                                      static_cast<int64_t>(n), st);
+        });
+        k_widen_keys<<<grid_n(n), 256, 0, st>>>(u32k, nruns, bs, ukeys);
+        FFCZ_LAUNCH_CHECK();
+    } else {
+        k_keys<<<grid_n(n), 256, 0, st>>>(codes, n, keys);
+        FFCZ_LAUNCH_CHECK();
+        cub_call(s, "huf_tmp_sort", [&](void* t, size_t& b) {
+            return cub::DeviceRadixSort::SortKeys(t, b, keys, skeys, static_cast<int64_t>(n), 0,
+                                                  32 + bb, st);
+        });
+        cub_call(s, "huf_tmp_rle", [&](void* t, size_t& b) {
+            return cub::DeviceRunLengthEncode::Encode(t, b, skeys, ukeys, counts, nruns,
+                                                      static_cast<int64_t>(n), st);
+        });
+    }
+    mark("keys sorted, runs");
     int h_nruns = 0;
     FFCZ_CUDA_CHECK(cudaMemcpyAsync(&h_nruns, nruns, 4, cudaMemcpyDeviceToHost, st));
     FFCZ_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -561,8 +631,10 @@ unsigned long long huffman_encode_device(DevScratch& s, const int* codes, unsign
     FFCZ_LAUNCH_CHECK();
     int lend = 33;
     while ((1ll << (lend - 33)) < nb) ++lend;
+    // sort on (block, count) only: the radix sort is stable and the runs arrive in (block,
+    // symbol) order, so the rank bits [0, 16) ride along already in tie order (6 -> 4 passes)
     cub_call(s, "huf_tmp_sort2", [&](void* t, size_t& b) {
-        return cub::DeviceRadixSort::SortKeys(t, b, lkeys, lkeys_s, static_cast<int64_t>(R), 0,
+        return cub::DeviceRadixSort::SortKeys(t, b, lkeys, lkeys_s, static_cast<int64_t>(R), 16,
                                               lend, st);
     });
     auto* iw = static_cast<unsigned*>(s.get("huf_iw", 4 * R));
@@ -581,6 +653,7 @@ unsigned long long huffman_encode_device(DevScratch& s, const int* codes, unsign
         lkeys_s, run_start, nb, iw, it, iq, par, pj, len_of_run, code_of_run, canon,
         table_mode());
     FFCZ_LAUNCH_CHECK();
+    mark("code tables");
     auto* sym_code = static_cast<unsigned*>(s.get("huf_sym_code", 4 * n));
     auto* sym_len = static_cast<unsigned long long*>(s.get("huf_sym_len", 8 * n));
     auto* len_incl = keys;  // keys are consumed
@@ -605,6 +678,7 @@ unsigned long long huffman_encode_device(DevScratch& s, const int* codes, unsign
     cub_call(s, "huf_tmp_scan3", [&](void* t, size_t& b) {
         return cub::DeviceScan::ExclusiveSum(t, b, words, word_off, nb + 1, st);
     });
+    mark("symbol codes, scans");
     unsigned long long tot[2];
     FFCZ_CUDA_CHECK(cudaMemcpyAsync(&tot[0], rec_off + nb, 8, cudaMemcpyDeviceToHost, st));
     FFCZ_CUDA_CHECK(cudaMemcpyAsync(&tot[1], word_off + nb, 8, cudaMemcpyDeviceToHost, st));
@@ -619,6 +693,7 @@ unsigned long long huffman_encode_device(DevScratch& s, const int* codes, unsign
     k_write_blocks<<<static_cast<unsigned>(std::min<long long>(nb, 148 * 8)), 256, 0, st>>>(
         ukeys, run_start, len_of_run, canon, nbits, rec_off, word_off, wbuf, n, nb, out);
     FFCZ_LAUNCH_CHECK();
+    mark("bits packed, written");
     *payload = out;
     return total;
 }

@@ -1067,9 +1067,47 @@ void correct_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& f
     out->t_feasible_ms = event_ms(c.ev[1], c.ev[6]);
 }
 
-// FFCZ_OUTER_DEVICE archives (archive_dev.cu) into the pinned result pool
-void device_archive(ffcz_cuda_ctx& c, const DevArchiveInput& ai, ffcz_cuda_result* r) {
-    DevScratch ds{c.st, [&](const char* nm, size_t b) { return c.buf(nm, b); }};
+// Engine buffers whose contents are dead once the escape records are on the host (the loop and
+// gate state; every call re-initialises them before reading) lent to the archive encoder: at
+// 1024^3 its sort / code-length / bit-packing scratch is ~55 GB, which would otherwise sit on top
+// of the ~100 GB of engine state.  Requests by name are served first-fit from the donors (a name
+// asked again with a size that fits gets the same region, as c.buf does); what does not fit
+// falls back to engine buffers of its own.
+struct DonorArena {
+    ffcz_cuda_ctx& c;
+    std::vector<std::pair<char*, size_t>> blocks;
+    std::vector<size_t> used;
+    std::map<std::string, std::pair<void*, size_t>> named;
+    void donate(const char* name) {
+        auto it = c.bufs.find(name);
+        if (it == c.bufs.end()) return;
+        blocks.emplace_back(static_cast<char*>(it->second.first), it->second.second);
+        used.push_back(0);
+    }
+    void* get(const char* nm, size_t bytes) {
+        auto it = named.find(nm);
+        if (it != named.end() && it->second.second >= bytes) return it->second.first;
+        bytes = round_up(std::max<size_t>(bytes, 256), 256);
+        for (size_t i = 0; i < blocks.size(); ++i)
+            if (blocks[i].second - used[i] >= bytes) {
+                void* p = blocks[i].first + used[i];
+                used[i] += bytes;
+                named[nm] = {p, bytes};
+                return p;
+            }
+        void* p = c.buf(std::string("arc_own_") + nm, bytes);
+        named[nm] = {p, bytes};
+        return p;
+    }
+};
+
+// FFCZ_OUTER_DEVICE archives (archive_dev.cu) into the pinned result pool; `donors` names engine
+// buffers that are dead at this point (DonorArena)
+void device_archive(ffcz_cuda_ctx& c, const DevArchiveInput& ai, ffcz_cuda_result* r,
+                    std::initializer_list<const char*> donors = {}) {
+    DonorArena arena{c, {}, {}, {}};
+    for (const char* d : donors) arena.donate(d);
+    DevScratch ds{c.st, [&](const char* nm, size_t b) { return arena.get(nm, b); }};
     const auto t0 = std::chrono::steady_clock::now();
     std::uint64_t len = 0;
     write_archive_device(ds, ai, [](size_t n) { return pinned().get(n); }, &r->archive, &len);
@@ -1232,7 +1270,10 @@ void finish_typed(ffcz_cuda_ctx& c, const Geometry& g, const ffcz_field_desc& fd
         ai.frequency_codes = c.b<int>("codes_f", 2 * g.Nc());
         ai.escapes = out->escapes;
         ai.n_escapes = n_esc;
-        device_archive(c, ai, out);
+        // (escape records and the corrected field are on the host: c.sync() above)
+        device_archive(c, ai, out,
+                       {"eps_tilde", "spat_cur", "freq_cur", "spec", "F", "S", "eps", "idx",
+                        "eps_verify", "esc_recs", "esc_recs_all", "real_tmp"});
         return;
     }
     if (opt.flags & FFCZ_WANT_ARCHIVE) {
