@@ -132,7 +132,12 @@ template <class T, int L, class Hook>
 void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
                long long plane_stride, long long nplanes, int ncols, Twiddles<T>& tw,
                const int* gate, Hook hook, cudaStream_t st) {
-    constexpr int E = pick_E<T>(L);
+    // FP32 passes that carry hooks (the mixed policy's check / clip, FP64 S / F bookkeeping)
+    // run at E = 16: at E = 32 the line's 64 registers plus the hooks' FP64 temporaries spill
+    constexpr int E = (sizeof(T) == 4 && !std::is_same_v<Hook, HookNone> && L >= 512 &&
+                       pick_E<T>(L) > 16)
+                          ? 16
+                          : pick_E<T>(L);
     constexpr int TT = L / E;
     constexpr int MAXT = max_threads<T, E>();
     const TileRole role = row_stride > plane_stride && nplanes > 1 ? TileRole::kFirst : TileRole::kMid;
@@ -285,10 +290,22 @@ template <class T, int M> struct RowCfg {
     static constexpr int MAXT = max_threads<T, E>();
 };
 
-template <class T, int M>
+// E of a row pass carrying `Hook`: FP32 C2R passes with real-output hooks (the mixed policy's
+// s-clip: FP64 S bookkeeping on FP32 values) run at E = 16 — at E = 32 the 64 registers of line
+// data plus the hook's FP64 temporaries spill (3.2 ms vs 1.4 ms for the plain pass at 1024^3)
+template <class T, int M, class Hook>
+constexpr int row_E() {
+    if constexpr (sizeof(T) == 4 && !std::is_same_v<Hook, RealHookNone> &&
+                  !std::is_same_v<Hook, HookNone> && RowCfg<T, M>::E > 16 && M / 16 <= 32)
+        return 16;
+    else
+        return RowCfg<T, M>::E;
+}
+
+template <class T, int M, int E = RowCfg<T, M>::E>
 int rows_per_cta(long long nrows) {
-    constexpr int TT = RowCfg<T, M>::TT;
-    long long r = std::min<long long>(tile_budget<T>(TileRole::kRow) / M, RowCfg<T, M>::MAXT / TT);
+    constexpr int TT = M / E;
+    long long r = std::min<long long>(tile_budget<T>(TileRole::kRow) / M, max_threads<T, E>() / TT);
     r = std::min<long long>(r, pow2_ceil(nrows));
     // whole warps only: the paired split/merge and the block reductions use full-mask shuffles
     r = std::max<long long>(r, (32 + TT - 1) / TT);
@@ -314,8 +331,8 @@ template <class T, int M, class Hook = RealHookNone>
 void row_c2r_radix(const cplx<T>* in, long long in_stride, T* out, long long out_stride,
                    long long nrows, T scale, Twiddles<T>& tw, const int* gate, cudaStream_t st,
                    Hook hook = Hook{}) {
-    constexpr int E = RowCfg<T, M>::E, TT = RowCfg<T, M>::TT;
-    const int R = rows_per_cta<T, M>(nrows);
+    constexpr int E = row_E<T, M, Hook>(), TT = M / E;
+    const int R = rows_per_cta<T, M, E>(nrows);
     size_t smem = row_smem_bytes<T, M, E>(R);
     if constexpr (hook_prefetch<Hook>())  // two input fields' rows + the mbarrier (k_row_c2r_sh)
         if (TT <= 32) smem += 2 * static_cast<size_t>(2 * M) * R * Hook::prefetch_scalar_bytes() + 16;
