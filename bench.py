@@ -317,7 +317,8 @@ def run_frames(args, rank, world, local):
 
 def run_slab(args, rank, world, local):
     """Configs 4/5: ONE combustion-like volume slab-decomposed along axis 0 across the ranks
-    (paper_2601_01596_b200/slab.py: two NCCL all-to-alls + one all-reduce per iteration);
+    (paper_2601_01596_b200/slab.py: per iteration two transposes -- fused into the passes as
+    peer stores, or NCCL all-to-alls under FFCZ_SLAB_PEER=0 -- and one all-reduce);
     strong scaling (the volume is fixed).  One step = one distributed correct()."""
     import torch
     import torch.distributed as dist
@@ -360,6 +361,8 @@ def run_slab(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
     ms_step = ms / args.steps
+    transpose = ("fused peer-store all-to-all" if world > 1 and be.peer_ok((n, n, n), world)
+                 and os.environ.get("FFCZ_SLAB_PEER", "1") != "0" else "NCCL all-to-all")
     if rank == 0:
         print(json.dumps({
             "metric": "corrected GB/s (input bytes / time to feasibility)",
@@ -371,7 +374,7 @@ def run_slab(args, rank, world, local):
                                    "Delta=0.6*mean|delta0|, slab-decomposed along axis 0",
                        "n": n, "m": 16, "policy": "fp64 (reference control flow)",
                        "l2": f"inputs larger than L2 ({4 * n ** 3 / world / 1e9:.2f} GB per rank)",
-                       "parallelism": f"slab x{world} (NCCL all-to-all)"},
+                       "parallelism": f"slab x{world} ({transpose})"},
             "iterations": r.iterations, "escape_rounds": r.escape_rounds,
             "escapes": len(r.escapes), "e2e": None, "cpu_baseline": None,
             "clocks": clk.summary()}))

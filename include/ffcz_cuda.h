@@ -240,9 +240,18 @@ typedef enum ffcz_cuda_slab_opcode {
                                      p4 keep_s, p5 esc_s, p6 keep_f, p7 esc_f bitmaps, p8 codes_s,
                                      p9 codes_f (editset.cpp:43-133, pipeline.cpp:57-106)
                                      -> out: active_s, active_f, kept_s, kept_f */
-    FFCZ_SLAB_DECIDE = 14         /* device-resident loop: p0 all-reduced (peak, excess) doubles,
+    FFCZ_SLAB_DECIDE = 14,        /* device-resident loop: p0 all-reduced (peak, excess) doubles,
                                      p1 state (passes, residual_f) doubles, p9 int32 (done,
                                      converged); max_iters in n_total (projection.cpp:106-116) */
+    /* fused all-to-all (slab.py peer path, world >= 2): the pass stores its outputs straight into
+     * the receive buffers of the ranks that own them in the other layout; p8 = device array of the
+     * `world` receive buffers (IPC-mapped, ffcz_cuda_ipc_*), this rank's own at [rank].  The
+     * orchestrator orders the ranks (a device-side barrier) after each such op. */
+    FFCZ_SLAB_FWD_LOCAL_PEER = 15, /* p0 real x -> p1 half A (c0, n1, P) work buffer: R2C rows,
+                                     forward axis 1 scattered into the B (n0, c1, P) buffers p8 */
+    FFCZ_SLAB_COL0_CLIP_INV_PEER = 16 /* p0 B half (read only): COL0_CLIP_INV (F p1, map p2)
+                                     with the inverse axis-0 outputs scattered into the A
+                                     (c0, n1, P) buffers p8 */
 } ffcz_cuda_slab_opcode;
 
 /* ffcz_cuda_slab_op.pad flag: a one-rank slab (B layout == natural layout); the COL0 ops
@@ -266,9 +275,18 @@ typedef struct ffcz_cuda_slab_op {
     const double* e_arr;
     const double* d_re;
     const double* d_im;
+    int32_t rank, world; /* *_PEER ops: this rank and the slab world size */
 } ffcz_cuda_slab_op;
 int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4]);
 uint64_t ffcz_cuda_slab_pitch(uint64_t n2);
+
+/* CUDA IPC of the slab receive buffers (the *_PEER ops): handle of the allocation holding `ptr`
+ * plus ptr's byte offset in it; open maps another process's handle (its base address), close
+ * unmaps it.  No reference counterpart: the reference runs one volume per process. */
+int ffcz_cuda_ipc_handle(ffcz_cuda_ctx* ctx, const void* ptr, unsigned char handle[64],
+                         uint64_t* offset);
+int ffcz_cuda_ipc_open(ffcz_cuda_ctx* ctx, const unsigned char handle[64], void** base);
+int ffcz_cuda_ipc_close(ffcz_cuda_ctx* ctx, void* base);
 
 /* Replaces ffcz::alternating_projection (projection.cpp:81-142).  eps0 is a field of
  * field->dtype; bounds are the WORKING bounds.  Outputs (host, caller-allocated, may be NULL):

@@ -22,6 +22,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "../../include/ffcz_cuda.h"
 #include "archive.hpp"
 #include "archive_dev.cuh"
@@ -2376,6 +2378,49 @@ int ffcz_cuda_apply_archive(ffcz_cuda_ctx* ctx, const uint8_t* archive, uint64_t
 
 uint64_t ffcz_cuda_slab_pitch(uint64_t n2) { return round_up(n2 / 2 + 1, kPitchAlign); }
 
+// CUDA IPC for the slab path's fused all-to-all: each rank exports its receive buffers, every
+// other rank maps them (NVLink peer memory on a multi-GPU node; the same device across processes
+// in the tests) and the scattering passes store into them directly.
+int ffcz_cuda_ipc_handle(ffcz_cuda_ctx* ctx, const void* ptr, unsigned char handle[64],
+                         uint64_t* offset) {
+    return guarded(ctx, [&] {
+        if (!ptr || !handle || !offset) throw Error(kValidation, "ipc_handle: null argument");
+        // the handle names the whole allocation (a torch cache block may start inside it)
+        using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+        static GetRange get_range = [] {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) !=
+                    cudaSuccess || q != cudaDriverEntryPointSuccess)
+                fn = nullptr;
+            return reinterpret_cast<GetRange>(fn);
+        }();
+        if (!get_range) throw Error(kCuda, "ipc_handle: cuMemGetAddressRange unavailable");
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+            throw Error(kValidation, "ipc_handle: not a device allocation");
+        cudaIpcMemHandle_t h;
+        FFCZ_CUDA_CHECK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+        static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+        std::memcpy(handle, &h, 64);
+        *offset = reinterpret_cast<uint64_t>(ptr) - static_cast<uint64_t>(base);
+    });
+}
+
+int ffcz_cuda_ipc_open(ffcz_cuda_ctx* ctx, const unsigned char handle[64], void** base) {
+    return guarded(ctx, [&] {
+        if (!handle || !base) throw Error(kValidation, "ipc_open: null argument");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, 64);
+        FFCZ_CUDA_CHECK(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int ffcz_cuda_ipc_close(ffcz_cuda_ctx* ctx, void* base) {
+    return guarded(ctx, [&] { FFCZ_CUDA_CHECK(cudaIpcCloseMemHandle(base)); });
+}
+
 // One per-rank device step of the slab-decomposed correction (paper_2601_01596_b200/slab.py).
 namespace {
 // device-resident slab loop (slab.py): this rank's (peak, excess) of the check pass, unless the
@@ -2428,7 +2473,9 @@ int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4
         auto reset_ctl = [&] { k_ctl_init<<<1, 1, 0, st>>>(c.ctl, 1); FFCZ_LAUNCH_CHECK(); };
         // loop ops of the device-resident slab loop: p9 = the loop's done flag (NULL: ungated)
         const bool loop_op = op->op == FFCZ_SLAB_FWD_LOCAL || op->op == FFCZ_SLAB_COL0_CHECK ||
-                             op->op == FFCZ_SLAB_COL0_CLIP_INV || op->op == FFCZ_SLAB_INV_SCLIP;
+                             op->op == FFCZ_SLAB_COL0_CLIP_INV || op->op == FFCZ_SLAB_INV_SCLIP ||
+                             op->op == FFCZ_SLAB_FWD_LOCAL_PEER ||
+                             op->op == FFCZ_SLAB_COL0_CLIP_INV_PEER;
         const int* gate = loop_op ? static_cast<const int*>(P(9)) : nullptr;
         // FFCZ_SLAB_SWAP_AXES (a one-rank slab: the B layout is the natural one): the "axis-0"
         // ops transform the middle axis and the local ops the outer one, the fused engine's
@@ -2475,6 +2522,53 @@ int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4
             HookFClip<double> hk{fb, op->fscale, d2(1), nullptr, static_cast<unsigned char*>(P(2))};
             hk.first = op->first != 0;
             plan.col(ax0, +1, d2(0), d2(0), gate, hk, st);
+            break;
+        }
+        case FFCZ_SLAB_FWD_LOCAL_PEER:
+        case FFCZ_SLAB_COL0_CLIP_INV_PEER: {
+            // fused all-to-all (kernels.cuh PeerScatter): the pass stores into the receive
+            // buffers of the ranks that own its outputs in the other layout
+            const unsigned W = static_cast<unsigned>(op->world), r = static_cast<unsigned>(op->rank);
+            if (op->world < 2 || op->rank < 0 || r >= W || !P(8) || (op->pad & FFCZ_SLAB_SWAP_AXES))
+                throw Error(kValidation, "slab peer op: needs world >= 2, 0 <= rank < world, p8");
+            if (g.half_elems() >= (1LL << 32))
+                throw Error(kUnsupported, "slab peer op: slab above 2^32 half-spectrum elements");
+            const bool fwd = op->op == FFCZ_SLAB_FWD_LOCAL_PEER;
+            // forward: this buffer is A (c0, n1, P); backward: B (n0, c1, P)
+            const unsigned d0 = static_cast<unsigned>(g.d[0]), d1 = static_cast<unsigned>(g.d[1]);
+            if ((fwd ? d1 : d0) % W)
+                throw Error(kValidation, "slab peer op: the exchanged axis must divide by world");
+            auto lg2 = [](unsigned v) {
+                if (!v || (v & (v - 1)))
+                    throw Error(kUnsupported, "slab peer op: power-of-two slab extents only");
+                int l = 0;
+                while ((1u << l) < v) ++l;
+                return l;
+            };
+            PeerScatter ps;
+            ps.peers = static_cast<double2* const*>(P(8));
+            ps.row = FastDiv::make(static_cast<unsigned>(g.P));
+            ps.d1_sh = lg2(d1);
+            ps.fwd = fwd ? 1 : 0;
+            if (fwd) {   // (c0, n1) -> (n0, c1): c1 = n1 / W
+                ps.part_sh = lg2(d1 / W);
+                ps.width_sh = lg2(d1 / W);
+                ps.base = r * d0;
+                launch_row_r2c<double>(g.n2, dd(0), g.n2, d2(1), g.P, g.rows, c.tw64, gate, st);
+                plan.col(1, -1, d2(1), d2(1), gate, HookScatter{ps}, st);
+            } else {     // (n0, c1) -> (c0, n1): c0 = n0 / W, n1 = W c1
+                ps.part_sh = lg2(d0 / W);
+                ps.width_sh = lg2(W * d1);
+                ps.base = r * d1;
+                HookFClipScatter<double> hk;
+                hk.fb = fb;
+                hk.fscale = op->fscale;
+                hk.F = d2(1);
+                hk.moved = static_cast<unsigned char*>(P(2));
+                hk.first = op->first != 0;
+                hk.ps = ps;
+                plan.col(0, +1, d2(0), d2(0), gate, hk, st);
+            }
             break;
         }
         case FFCZ_SLAB_COL0_PLAIN:

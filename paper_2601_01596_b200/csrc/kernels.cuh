@@ -185,6 +185,80 @@ struct HookFClip {
     __device__ __forceinline__ void finish() {}
 };
 
+// ---- fused slab transpose (slab.py peer path) ---------------------------------------------------
+// n / d for n < 2^32 by multiply-high (Granlund-Montgomery round-up method): the scatter decodes
+// element offsets at every store, where a hardware-less 32-bit division would cost ~20 ops.
+struct FastDiv {
+    unsigned d = 1, m = 1;
+    int l = 0;
+    __host__ static FastDiv make(unsigned d) {
+        FastDiv f;
+        f.d = d;
+        while ((1ull << f.l) < d) ++f.l;
+        f.m = static_cast<unsigned>((((1ull << 32) * ((1ull << f.l) - d)) / d) + 1);
+        return f;
+    }
+    __device__ __forceinline__ unsigned div(unsigned n) const {
+        return static_cast<unsigned>((static_cast<unsigned long long>(__umulhi(n, m)) + n) >> l);
+    }
+};
+
+// The all-to-all of slab.py (_transpose_ab / _transpose_ba) as the store of the pass that
+// produces the data: element `off` of this rank's (d0, d1, P) buffer goes straight into the
+// receive buffer of the rank that owns it in the other layout (CUDA IPC mappings; NVLink peer
+// stores across GPUs).  Forward (A (c0, n1, P) -> B (n0, c1, P)): (i0, i1, k) -> rank i1 / c1,
+// row (r c0 + i0) c1 + i1 mod c1.  Backward (B -> A): (i0, i1l, k) -> rank i0 / c0, row
+// (i0 mod c0) n1 + r c1 + i1l.  Offsets of one slab fit 32 bits (checked on the host).
+struct PeerScatter {
+    double2* const* peers;  // W receive buffers, this rank's own at [r]
+    FastDiv row;            // P
+    // powers of two (the slab's hooked passes need power-of-two axes, so n1, c1 and c0 are):
+    int d1_sh;              // d1 of this buffer (forward: n1; backward: c1)
+    int part_sh;            // forward: c1; backward: c0
+    int width_sh;           // forward: c1; backward: n1
+    unsigned base;          // forward: r c0; backward: r c1
+    int fwd;
+    __device__ __forceinline__ void store(double2 v, long long off) const {
+        const unsigned o = static_cast<unsigned>(off);
+        const unsigned q = row.div(o), k = o - q * row.d;
+        const unsigned a = q >> d1_sh, b = q & ((1u << d1_sh) - 1u);
+        const unsigned x = fwd ? b : a;  // the exchanged index
+        const unsigned s = x >> part_sh, xl = x & ((1u << part_sh) - 1u);
+        const unsigned drow = fwd ? ((base + a) << width_sh) + xl : (xl << width_sh) + base + b;
+        double2* dst = reinterpret_cast<double2*>(
+            __ldg(reinterpret_cast<const unsigned long long*>(peers) + s));
+        dst[static_cast<size_t>(drow) * row.d + k] = v;
+    }
+};
+
+// plain pass whose outputs are scattered (FFCZ_SLAB_FWD_LOCAL_PEER: forward axis 1 of A)
+struct HookScatter {
+    static constexpr bool kNoStore = true;
+    PeerScatter ps;
+    template <class C> __device__ __forceinline__ void pre(C&, long long, int) {}
+    template <class C> __device__ __forceinline__ void post(C& v, long long off, int) {
+        ps.store(make_double2(v.x, v.y), off);
+    }
+    // the peer stores are performed system-wide before the pass ends (the orchestrator's barrier
+    // then orders them with the receiving rank's next pass)
+    __device__ __forceinline__ void finish() { __threadfence_system(); }
+};
+
+// project_onto_fcube + inverse axis 0 (HookFClip) whose outputs are scattered back to the natural
+// slabs (FFCZ_SLAB_COL0_CLIP_INV_PEER)
+template <class T>
+struct HookFClipScatter : HookFClip<T> {
+    static constexpr bool kNoStore = true;
+    PeerScatter ps;
+    template <class C> __device__ __forceinline__ void post_d(C& v, long long off, int, double2) {
+        ps.store(make_double2(v.x, v.y), off);
+    }
+    template <class C> __device__ __forceinline__ void post(C& v, long long off, int) {
+        ps.store(make_double2(v.x, v.y), off);
+    }
+    __device__ __forceinline__ void finish() { __threadfence_system(); }
+};
+
 // project_onto_scube + S accumulation (projection.cpp:68-79, 121-124) on the real outputs of a
 // C2R row pass; writes the clipped epsilon (the reference's `eps = sc.clipped`).
 // Same first-pass dense write of S as HookFClip (S is zero before the first s-clip).

@@ -67,6 +67,21 @@ class Comm:
         if dst is not out:
             dst.copy_(out)
 
+    def barrier_dev(self):
+        """Order every rank's device work so far before any rank's next op (the fused all-to-all's
+        receive buffers): a one-element all-reduce on the stream (NCCL), or a host barrier after a
+        device sync when the collectives are staged on the host."""
+        if self.size == 1:
+            return
+        import torch
+        if self.stage_cpu:
+            torch.cuda.synchronize()
+            self.dist.barrier(group=self.group)
+            return
+        if getattr(self, "_tick", None) is None:
+            self._tick = torch.zeros(1, dtype=torch.int32, device=torch.cuda.current_device())
+        self.dist.all_reduce(self._tick, group=self.group)
+
     def _reduce(self, t, op):
         if self.size > 1:
             if self.stage_cpu:
@@ -290,11 +305,37 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E, Delta, m: int = 16,
     S = be.zeros_real((c0, n1, n2))
     F_B = be.zeros_half((n0, c1))
     moved_B = be.zeros_moved((n0, c1))
-    A = be.zeros_half((c0, n1))
-    be.fwd_local(eps, A, N)
     ls = be.loop_state()
     gate = ls["gate"]
-    B = None
+    # fused all-to-all (FFCZ_SLAB_PEER=0 disables): the forward axis-1 pass and the clip +
+    # inverse axis-0 pass store straight into the receive buffers of the ranks that own their
+    # outputs in the other layout (CUDA IPC / NVLink peer memory), no pack copy, no NCCL buffers
+    peer = None
+    if (W > 1 and os.environ.get("FFCZ_SLAB_PEER", "1") != "0" and hasattr(be, "peer_ok")
+            and be.peer_ok((n0, n1, n2), W)):
+        peer = be.peer_setup(comm, (n0, n1, n2))
+    if peer is not None:
+        A, B = peer["A"], peer["B"]
+        be.fwd_local_peer(eps, peer)
+        comm.barrier_dev()
+    else:
+        A = be.zeros_half((c0, n1))
+        be.fwd_local(eps, A, N)
+        B = None
+
+    def body_peer(k):
+        """body() with the transposes fused into the passes; a device barrier after each
+        scattering pass orders it with the receiving ranks' next pass (and their previous pass
+        on the same buffer).  Once done, the scattering passes are gated off with the rest, so B
+        keeps the last check's spectrum (delta_star)."""
+        be.col0_check_dev(B, Delta, fw, ls["red"], gate)
+        comm.max_f64_(ls["red"])
+        be.decide(ls["red"], ls["state"], gate, max_iters)
+        be.col0_clip_inv_peer(Delta, fw, F_B, moved_B, k == 0, peer, gate=gate)
+        comm.barrier_dev()
+        be.inv_local_sclip(A, eps, N, E, fw, S, k == 0, gate=gate)
+        be.fwd_local_peer(eps, peer, gate=gate)
+        comm.barrier_dev()
 
     def body(k):
         """One pass of projection.cpp:96-126 with the decision on the device: check, all-reduce
@@ -313,16 +354,20 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E, Delta, m: int = 16,
 
     # one pass queued behind the one being decided: the host waits on an event per pass, never
     # on a value, and the device never idles for the host
+    run = body_peer if peer is not None else body
     k = 0
-    body(k)
+    run(k)
     snaps = [be.snapshot(ls)]
     while True:
         k += 1
-        body(k)
+        run(k)
         snaps.append(be.snapshot(ls))
         if be.done(snaps.pop(0)):
             break
     passes, converged, residual_f = be.loop_result(ls)
+    if peer is not None:
+        comm.barrier_dev()      # every rank is past its last (gated) scattering pass
+        be.peer_close(peer)
     _phase("loop")
     delta_star = B                                          # FFT(final_eps), pipeline.cpp:114
     residual_s = comm.max_f64([be.residual_s(eps, E, fw)], dev)[0]

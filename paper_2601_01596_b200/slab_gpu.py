@@ -19,15 +19,21 @@ class SlabOp(C.Structure):
                 ("d0", C.c_uint64), ("d1", C.c_uint64), ("n2", C.c_uint64),
                 ("n_total", C.c_uint64), ("e", C.c_double), ("delta", C.c_double),
                 ("fscale", C.c_double), ("slack", C.c_double), ("p", C.c_void_p * 10),
-                ("e_arr", C.c_void_p), ("d_re", C.c_void_p), ("d_im", C.c_void_p)]
+                ("e_arr", C.c_void_p), ("d_re", C.c_void_p), ("d_im", C.c_void_p),
+                ("rank", C.c_int32), ("world", C.c_int32)]
 
 
 (EPS0, FWD_LOCAL, COL0_CHECK, COL0_CLIP_INV, COL0_PLAIN, COL0_REBUILD, COL0_MARK, COL0_VERIFY,
- INV_SCLIP, INV_REPAIR_VERIFY, INV_VERIFY, RESIDUAL_S, EPS0_PLUS_S, GATE, DECIDE) = range(15)
+ INV_SCLIP, INV_REPAIR_VERIFY, INV_VERIFY, RESIDUAL_S, EPS0_PLUS_S, GATE, DECIDE,
+ FWD_LOCAL_PEER, COL0_CLIP_INV_PEER) = range(17)
 
 
 _E_OPS = frozenset({EPS0, INV_SCLIP, INV_REPAIR_VERIFY, INV_VERIFY, RESIDUAL_S, GATE})
-_B_OPS = frozenset({COL0_CHECK, COL0_CLIP_INV, COL0_MARK, COL0_VERIFY})
+_B_OPS = frozenset({COL0_CHECK, COL0_CLIP_INV, COL0_CLIP_INV_PEER, COL0_MARK, COL0_VERIFY})
+
+
+def _pow2(v):
+    return v > 0 and v & (v - 1) == 0
 
 
 def _bits_to_bool(words, n):
@@ -154,6 +160,72 @@ class GpuSlabBackend:
     def inv_local_sclip(self, A, eps_out, N, E, fs, S, first, gate=None):
         self._op(INV_SCLIP, A.shape, [A, eps_out, S], gate=gate, e=E, fscale=fs, n_total=N,
                  first=int(bool(first)))
+
+    # -- fused all-to-all: the loop's two transposes as peer stores of the passes -------------------
+    def peer_ok(self, dims, W):
+        """The scattering passes carry hooks (power-of-two axes 0 and 1, in [16, 4096]) and
+        decode 32-bit offsets."""
+        n0, n1, _ = dims
+        c0, c1 = n0 // W, n1 // W
+        return (W >= 2 and not self.swap_axes and _pow2(W)
+                and all(_pow2(v) and 16 <= v <= 4096 for v in (n0, n1))
+                and c0 * n1 * self.P < 2 ** 32 and n0 * c1 * self.P < 2 ** 32)
+
+    def peer_setup(self, comm, dims):
+        """This rank's receive buffers A (c0, n1, P) and B (n0, c1, P), exported over CUDA IPC and
+        mapped by every rank; returns the state the *_peer ops and peer_close take."""
+        torch = self.torch
+        n0, n1, _ = dims
+        W, r = comm.size, comm.rank
+        c0, c1 = n0 // W, n1 // W
+        A = self.zeros_half((c0, n1))
+        B = self.zeros_half((n0, c1))
+        row = np.zeros(2 * 72, dtype=np.uint8)
+        for j, t in enumerate((A, B)):
+            h = (C.c_ubyte * 64)()
+            off = C.c_uint64()
+            _check(self.lib.ffcz_cuda_ipc_handle(self.ctx.handle, C.c_void_p(t.data_ptr()),
+                                                 C.cast(h, C.c_void_p), C.byref(off)))
+            row[72 * j: 72 * j + 64] = np.frombuffer(bytes(h), dtype=np.uint8)
+            row[72 * j + 64: 72 * j + 72] = np.frombuffer(np.uint64(off.value).tobytes(),
+                                                          dtype=np.uint8)
+        dev_row = torch.as_tensor(row).view(1, -1).to(self.device)
+        rows = comm.all_gather_rows(dev_row).cpu().numpy()
+        opened, ptrs = [], {0: [], 1: []}
+        for s in range(W):
+            for j, t in enumerate((A, B)):
+                if s == r:
+                    ptrs[j].append(t.data_ptr())
+                    continue
+                h = (C.c_ubyte * 64).from_buffer_copy(rows[s, 72 * j: 72 * j + 64].tobytes())
+                off = int(rows[s, 72 * j + 64: 72 * j + 72].view(np.uint64)[0])
+                base = C.c_void_p()
+                _check(self.lib.ffcz_cuda_ipc_open(self.ctx.handle, C.cast(h, C.c_void_p),
+                                                   C.byref(base)))
+                opened.append(base.value)
+                ptrs[j].append(base.value + off)
+        return {"A": A, "B": B, "W": W, "r": r, "opened": opened,
+                # each op scatters into the OTHER layout's buffers
+                "to_A": torch.tensor(ptrs[0], dtype=torch.int64, device=self.device),
+                "to_B": torch.tensor(ptrs[1], dtype=torch.int64, device=self.device)}
+
+    def peer_close(self, peer):
+        for base in peer["opened"]:
+            _check(self.lib.ffcz_cuda_ipc_close(self.ctx.handle, C.c_void_p(base)))
+        peer["opened"] = []
+
+    def fwd_local_peer(self, x, peer, gate=None):
+        """R2C rows + forward axis 1 of x into peer A, scattered into every rank's B."""
+        A = peer["A"]
+        self._op(FWD_LOCAL_PEER, A.shape, [x, A] + [None] * 6 + [peer["to_B"]], gate=gate,
+                 rank=peer["r"], world=peer["W"])
+
+    def col0_clip_inv_peer(self, D, fs, F_B, moved_B, first, peer, gate=None):
+        """project_onto_fcube + inverse axis 0 of peer B, scattered into every rank's A."""
+        B = peer["B"]
+        self._op(COL0_CLIP_INV_PEER, B.shape, [B, F_B, moved_B] + [None] * 5 + [peer["to_A"]],
+                 gate=gate, delta=D, fscale=fs, first=int(bool(first)), rank=peer["r"],
+                 world=peer["W"])
 
     # -- device-resident loop: decisions on the device, the host only waits on events ------------
     def loop_state(self):
