@@ -361,7 +361,58 @@ def run_slab(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
     ms_step = ms / args.steps
-    transpose = ("fused peer-store all-to-all" if world > 1 and be.peer_ok((n, n, n), world)
+    launches0 = int(be.lib.ffcz_cuda_launch_count(be.ctx.handle))
+    r = step()
+    launches = int(be.lib.ffcz_cuda_launch_count(be.ctx.handle)) - launches0
+
+    # e2e through the slab API with host buffers: every step copies this rank's slabs of the two
+    # fields in from pinned memory, corrects, and copies this rank's edit set (flag bitmaps and
+    # int32 codes) out
+    e2e = None
+    if not args.no_e2e:
+        h_o = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
+        h_d = torch.empty_like(h_o, pin_memory=True)
+        h_o.copy_(o)
+        h_d.copy_(d)
+        d_o, d_d = torch.empty_like(o), torch.empty_like(d)
+        nbytes = {"out": 0}
+        pinned = {}   # pinned result buffers, reused across steps (sizes repeat)
+
+        def e2e_step():
+            d_o.copy_(h_o, non_blocking=True)
+            d_d.copy_(h_d, non_blocking=True)
+            rr = slab.correct_slab(be, comm, (n, n, n), d_o, d_d, E, D)
+            outs = [rr.spatial_flags, rr.frequency_flags, rr.spatial_codes, rr.frequency_codes]
+            nbytes["out"] = sum(t.numel() * t.element_size() for t in outs)
+            cur = torch.cuda.current_stream(dev)
+            for i, t in enumerate(outs):
+                hb = pinned.get(i)
+                if hb is None or hb.numel() < t.numel():
+                    hb = pinned[i] = torch.empty(t.numel(), dtype=t.dtype, pin_memory=True)
+                hb[: t.numel()].copy_(t.reshape(-1), non_blocking=True)
+            cur.synchronize()
+            return rr
+        e2e_step()
+        barrier()
+        ke = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            e2e_step()
+        barrier()
+        te = (time.perf_counter() - t0) / ke
+        if world > 1:
+            t = torch.tensor([te], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = t.item()
+        e2e = {"value": 4.0 * n ** 3 / te / 1e9, "unit": "GB/s", "ms_per_step": 1e3 * te,
+               "steps": ke,
+               "h2d_bytes_per_step": 2 * o.numel() * o.element_size(),
+               "d2h_bytes_per_step": nbytes["out"],
+               "how": "per rank: H2D of its original + decompressed slabs (f32) from pinned "
+                      "memory, slab correct(), D2H of its flag bitmaps and codes; wall clock, "
+                      "max over ranks"}
+    transpose = ("no exchange" if world == 1 else
+                 "fused peer-store all-to-all" if be.peer_ok((n, n, n), world)
                  and os.environ.get("FFCZ_SLAB_PEER", "1") != "0" else "NCCL all-to-all")
     if rank == 0:
         print(json.dumps({
@@ -376,8 +427,8 @@ def run_slab(args, rank, world, local):
                        "l2": f"inputs larger than L2 ({4 * n ** 3 / world / 1e9:.2f} GB per rank)",
                        "parallelism": f"slab x{world} ({transpose})"},
             "iterations": r.iterations, "escape_rounds": r.escape_rounds,
-            "escapes": len(r.escapes), "e2e": None, "cpu_baseline": None,
-            "clocks": clk.summary()}))
+            "escapes": len(r.escapes), "e2e": e2e, "cpu_baseline": None,
+            "gpu_launches": launches * args.steps, "clocks": clk.summary()}))
     be.ctx.close()
 
 
@@ -595,11 +646,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=1024)
-    ap.add_argument("--config", default="combustion",
+    ap.add_argument("--config", default=None,
                     choices=["nyx", "combustion", "frames", "slab"],
-                    help="combustion = configs[3] recipe at 1024^3 on one GPU (default: the "
-                         "north_star target); nyx = configs[1] (use --n 512); frames = configs[2] "
-                         "(batched 2-D frames, sharded); slab = configs[3] slab-decomposed")
+                    help="combustion = configs[3] recipe at 1024^3 on one GPU (default at N=1: "
+                         "the north_star target); slab = the same volume slab-decomposed across "
+                         "the N ranks (default at N>1: strong scaling of one volume); nyx = "
+                         "configs[1] (use --n 512); frames = configs[2] (batched 2-D frames, "
+                         "sharded)")
     ap.add_argument("--frames", type=int, default=1024)
     ap.add_argument("--frame-n", type=int, default=2048)
     ap.add_argument("--lanes", type=int, default=8)
@@ -621,6 +674,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config is None:
+        args.config = "slab" if world > 1 else "combustion"
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return

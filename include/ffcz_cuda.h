@@ -279,6 +279,8 @@ typedef struct ffcz_cuda_slab_op {
 } ffcz_cuda_slab_op;
 int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4]);
 uint64_t ffcz_cuda_slab_pitch(uint64_t n2);
+/* Kernels this context has launched so far (every correct / slab op; bench.py's gpu_launches). */
+uint64_t ffcz_cuda_launch_count(ffcz_cuda_ctx* ctx);
 
 /* CUDA IPC of the slab receive buffers (the *_PEER ops): handle of the allocation holding `ptr`
  * plus ptr's byte offset in it; open maps another process's handle (its base address), close

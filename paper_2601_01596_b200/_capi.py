@@ -48,6 +48,7 @@ EXPORTS = [
     "ffcz_cuda_apply_archive", "ffcz_cuda_spectrum_bound", "ffcz_cuda_metrics",
     "ffcz_cuda_power_spectrum", "ffcz_cuda_outer_compress", "ffcz_cuda_crc32c_device",
     "ffcz_cuda_ipc_handle", "ffcz_cuda_ipc_open", "ffcz_cuda_ipc_close",
+    "ffcz_cuda_launch_count",
 ]
 
 
@@ -142,6 +143,8 @@ def load():
     lib.ffcz_cuda_ipc_handle.argtypes = [P, P, P, C.POINTER(C.c_uint64)]
     lib.ffcz_cuda_ipc_open.argtypes = [P, P, C.POINTER(C.c_void_p)]
     lib.ffcz_cuda_ipc_close.argtypes = [P, P]
+    lib.ffcz_cuda_launch_count.argtypes = [P]
+    lib.ffcz_cuda_launch_count.restype = C.c_uint64
     lib.ffcz_cuda_slab_pitch.restype = C.c_uint64
     lib.ffcz_cuda_result_free.argtypes = [C.POINTER(Result)]
     lib.ffcz_cuda_result_free.restype = None

@@ -18,6 +18,11 @@ struct Error : std::runtime_error {
     Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
 };
 
+inline unsigned long long& launch_ticks() {
+    static thread_local unsigned long long t = 0;
+    return t;
+}
+
 enum Status { kOk = 0, kValidation = 1, kSymmetry = 2, kFormat = 3, kIo = 4, kCuda = 5,
               kUnsupported = 6, kOom = 7, kUndefined = 8 };
 
@@ -33,7 +38,12 @@ enum Status { kOk = 0, kValidation = 1, kSymmetry = 2, kFormat = 3, kIo = 4, kCu
         }                                                                                      \
     } while (0)
 
-#define FFCZ_LAUNCH_CHECK() FFCZ_CUDA_CHECK(cudaGetLastError())
+// kernel launches checked on this host thread (the slab ops report their count from it)
+#define FFCZ_LAUNCH_CHECK()                                                                    \
+    do {                                                                                       \
+        ++::ffcz_gpu::launch_ticks();                                                          \
+        FFCZ_CUDA_CHECK(cudaGetLastError());                                                   \
+    } while (0)
 
 // ---- complex ---------------------------------------------------------------------------------
 

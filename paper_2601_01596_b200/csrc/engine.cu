@@ -2470,6 +2470,7 @@ int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4
         auto dd = [&](int i) { return static_cast<double*>(op->p[i]); };
         auto ww = [&](int i) { return static_cast<unsigned*>(op->p[i]); };
         double o4[4] = {0, 0, 0, 0};
+        const unsigned long long ticks0 = launch_ticks();  // launches of this op (c.launches)
         auto reset_ctl = [&] { k_ctl_init<<<1, 1, 0, st>>>(c.ctl, 1); FFCZ_LAUNCH_CHECK(); };
         // loop ops of the device-resident slab loop: p9 = the loop's done flag (NULL: ungated)
         const bool loop_op = op->op == FFCZ_SLAB_FWD_LOCAL || op->op == FFCZ_SLAB_COL0_CHECK ||
@@ -2671,10 +2672,13 @@ int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4
         default:
             throw Error(kValidation, "unknown slab op " + std::to_string(op->op));
         }
-        FFCZ_LAUNCH_CHECK();
+        FFCZ_CUDA_CHECK(cudaGetLastError());
+        c.launches += launch_ticks() - ticks0;
         if (out) std::memcpy(out, o4, sizeof(o4));
     });
 }
+
+uint64_t ffcz_cuda_launch_count(ffcz_cuda_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 int ffcz_cuda_alternating_projection(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field,
                                      const void* eps0_in, const ffcz_bounds_desc* bw_desc,
