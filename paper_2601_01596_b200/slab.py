@@ -368,8 +368,12 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E, Delta, m: int = 16,
     if peer is not None:
         comm.barrier_dev()      # every rank is past its last (gated) scattering pass
         be.peer_close(peer)
+        peer = None
     _phase("loop")
     delta_star = B                                          # FFT(final_eps), pipeline.cpp:114
+    # the gate's working set is the peak of the call: drop every loop buffer it does not read
+    # (the natural-layout spectrum here, F / the clip map / F_A / freq_cur(A) once consumed)
+    A = B = None
     residual_s = comm.max_f64([be.residual_s(eps, E, fw)], dev)[0]
 
     # ---- FP64 gate (pipeline.cpp:46-176) ---------------------------------------------------
@@ -382,11 +386,14 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E, Delta, m: int = 16,
         B2 = _transpose_ab(be, comm, A2, n0, c0, c1)
         be.col0_rebuild(B2, delta_star, moved_B, F_B)
         del X, A2, B2
+    moved_B = None
     F_A = _transpose_ba(be, comm, F_B, n1, c0, c1)
+    F_B = None
     g = be.gate(S, F_A, E, Delta, m, base_h=r * c0 * n1 * H)
+    del F_A
     act_s, act_f = comm.sum_i64([g["act_s"], g["act_f"]], dev)
     spat_cur = g["spat_cur"]
-    freq_cur_B = _transpose_ab(be, comm, g["freq_cur"], n0, c0, c1)
+    freq_cur_B = _transpose_ab(be, comm, g.pop("freq_cur"), n0, c0, c1)
     esc_s = g["esc_s"]                                     # bool (c0, n1, n2): spatial escapes
     # frequency escapes as global half indices owned (in B) by this rank
     ovf_h = comm.all_gather_rows(g["esc_f_h"].view(-1, 1)).view(-1)
@@ -395,7 +402,8 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E, Delta, m: int = 16,
     rounds, verified = 0, False
     vs = vf = 0.0
     corrected = be.zeros_real((c0, n1, n2))
-    eps_v = be.zeros_real((c0, n1, n2))
+    dview = os.environ.get("FFCZ_REPAIR_ORDER") != "reference"
+    eps_v = None if dview else be.zeros_real((c0, n1, n2))   # decoder view: only if unverified
     eps_t = be.zeros_real((c0, n1, n2))
 
     def inverse_to_spatial(fc_B):
@@ -411,14 +419,16 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E, Delta, m: int = 16,
 
     # decoder-view repair: the round checks the decoder's own view, so a clean
     # round is verify_bounds; FFCZ_REPAIR_ORDER=reference keeps the reference's eps_tilde order
-    dview = os.environ.get("FFCZ_REPAIR_ORDER") != "reference"
     if converged:
+        Aw = Bt = None
         for _ in range(MAX_ESCAPE_ROUNDS):                   # pipeline.cpp:116
             rounds += 1
+            Aw = Bt = None                                   # last round's spectra
             Aw = inverse_to_spatial(freq_cur_B)
             dirty_s, vs_r = be.inv_local_repair_verify(Aw, eps_t, N, orig, dec, spat_cur, eps, E,
                                                        esc_s, corrected,
                                                        None if dview else eps_v)
+            Aw = None
             Bt = forward_to_b(eps_t)
             viol = be.col0_mark(Bt, Delta)                  # FFT axis 0, |delta~| > Delta
             pos = be.positions(viol)                        # B storage offsets, ascending
@@ -437,6 +447,8 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E, Delta, m: int = 16,
                 break
     if not verified:
         # apply_edits + verify_bounds on the decoder view (archive.cpp:262-297)
+        if eps_v is None:
+            eps_v = eps_t                                    # the rounds' scratch is free now
         Aw = inverse_to_spatial(freq_cur_B)
         vs_r = be.inv_local_verify(Aw, eps_v, N, orig, dec, spat_cur, E, corrected)
         vs = comm.max_f64([vs_r], dev)[0]

@@ -173,7 +173,9 @@ class GpuSlabBackend:
 
     def peer_setup(self, comm, dims):
         """This rank's receive buffers A (c0, n1, P) and B (n0, c1, P), exported over CUDA IPC and
-        mapped by every rank; returns the state the *_peer ops and peer_close take."""
+        mapped by every rank; returns the state the *_peer ops and peer_close take, or None on
+        every rank when some rank cannot export or map them (the loop then uses the
+        all-to-alls)."""
         torch = self.torch
         n0, n1, _ = dims
         W, r = comm.size, comm.rank
@@ -181,29 +183,43 @@ class GpuSlabBackend:
         A = self.zeros_half((c0, n1))
         B = self.zeros_half((n0, c1))
         row = np.zeros(2 * 72, dtype=np.uint8)
+        ok = 1
         for j, t in enumerate((A, B)):
             h = (C.c_ubyte * 64)()
             off = C.c_uint64()
-            _check(self.lib.ffcz_cuda_ipc_handle(self.ctx.handle, C.c_void_p(t.data_ptr()),
-                                                 C.cast(h, C.c_void_p), C.byref(off)))
+            # (fails e.g. on expandable-segment allocations: then every rank takes the
+            # all-to-all path, decided together below)
+            if self.lib.ffcz_cuda_ipc_handle(self.ctx.handle, C.c_void_p(t.data_ptr()),
+                                             C.cast(h, C.c_void_p), C.byref(off)) != 0:
+                ok = 0
+                break
             row[72 * j: 72 * j + 64] = np.frombuffer(bytes(h), dtype=np.uint8)
             row[72 * j + 64: 72 * j + 72] = np.frombuffer(np.uint64(off.value).tobytes(),
                                                           dtype=np.uint8)
+        if comm.min_i64([ok], self.device)[0] == 0:
+            return None
         dev_row = torch.as_tensor(row).view(1, -1).to(self.device)
         rows = comm.all_gather_rows(dev_row).cpu().numpy()
         opened, ptrs = [], {0: [], 1: []}
         for s in range(W):
             for j, t in enumerate((A, B)):
+                if not ok:
+                    break
                 if s == r:
                     ptrs[j].append(t.data_ptr())
                     continue
                 h = (C.c_ubyte * 64).from_buffer_copy(rows[s, 72 * j: 72 * j + 64].tobytes())
                 off = int(rows[s, 72 * j + 64: 72 * j + 72].view(np.uint64)[0])
                 base = C.c_void_p()
-                _check(self.lib.ffcz_cuda_ipc_open(self.ctx.handle, C.cast(h, C.c_void_p),
-                                                   C.byref(base)))
+                if self.lib.ffcz_cuda_ipc_open(self.ctx.handle, C.cast(h, C.c_void_p),
+                                               C.byref(base)) != 0:
+                    ok = 0   # e.g. no peer access between these GPUs
+                    break
                 opened.append(base.value)
                 ptrs[j].append(base.value + off)
+        if comm.min_i64([ok], self.device)[0] == 0:
+            self.peer_close({"opened": opened})
+            return None
         return {"A": A, "B": B, "W": W, "r": r, "opened": opened,
                 # each op scatters into the OTHER layout's buffers
                 "to_A": torch.tensor(ptrs[0], dtype=torch.int64, device=self.device),
