@@ -838,6 +838,11 @@ def main():
                    "rho=1e-3: the reference CLI's --rho path), device correct()")
 
         def timed(archive):
+            if os.environ.get("FFCZ_BENCH_MEMDIAG"):
+                free, total = torch.cuda.mem_get_info(dev)
+                print(f"[memdiag] e2e start: free {free / 1e9:.1f} GB of {total / 1e9:.1f}, torch "
+                      f"reserved {torch.cuda.memory_reserved(dev) / 1e9:.1f} GB, allocated "
+                      f"{torch.cuda.memory_allocated(dev) / 1e9:.1f} GB", file=sys.stderr)
             r = None
             for _ in range(2):  # warm the pinned result pool (two generations of buffers)
                 r = None

@@ -151,11 +151,11 @@ struct ffcz_cuda_ctx {
 namespace {
 
 enum ProfClass { kColFwdCheck = 0, kColClipInv, kColPass, kRowR2C, kRowC2R, kRowFused,
-                 kElemPre, kElemGate, kElemCompact, kElemCodes, kNumProf };
+                 kElemPre, kElemGate, kElemCompact, kElemCodes, kColRoundTrip, kNumProf };
 const char* kProfNames[kNumProf] = {"col_fwd_check (K3a)", "col_clip_inv (K3b)", "col_pass",
                                     "row_r2c", "row_c2r", "row_c2r_sclip_r2c (K1)",
                                     "elem_bounds_eps0_residual", "elem_gate_quantize",
-                                    "elem_compact", "elem_codes"};
+                                    "elem_compact", "elem_codes", "col_check_clip_rt (K3)"};
 
 // RAII event pair around one launch when profiling is on
 struct Prof {
@@ -265,6 +265,25 @@ inline bool f_rebuild_enabled(const ffcz_cuda_ctx& c) {
         return !(e && e[0] == '0');
     }();
     if (c.call_flags & FFCZ_F_ACCUMULATE) return false;
+    return on;
+}
+
+// FFCZ_LOOP_RT=0: the loop's check and clip as two passes (K3a, K3b) instead of one round trip
+inline bool loop_rt_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_LOOP_RT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// FFCZ_LOOP_K1=0: the loop's last-axis step as C2R (+ s-clip, eps written) then R2C instead of
+// one fused row pass
+inline bool loop_k1_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_LOOP_K1");
+        return !(e && e[0] == '0');
+    }();
     return on;
 }
 
@@ -458,6 +477,16 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
     const int za = complete_axis(three_d);  // the pass that completes the forward transform
     const int mid = 1 - za;                   // the other column axis (3-D only)
     double* tmp = fused ? nullptr : c.b<double>("real_tmp", g.N);
+    // K3a + K3b as one round trip (HookRT): the forward chain ends in `spec`, the inverse chain
+    // starts from `spec_rt`; the last check's clip is speculative and undone after the loop
+    // (global Delta only: per-component lanes would add 16 dependent loads per thread to the
+    // check / clip; those keep the K3a / K3b pair with its TMA side tile)
+    const bool rt = fused && moved && !keep_moved && !bw.fb.re && loop_rt_enabled() &&
+                    plan.rt_ok(za);
+    double2* spec_rt = rt ? c.b<double2>("spec_rt", g.half_elems()) : nullptr;
+    double2* inv_src = rt ? spec_rt : spec;
+    // fused K1 on the radix row path (power-of-two last axis)
+    const bool k1 = fused && loop_k1_enabled() && radix_row_ok(g.n2);
 
     const double pass_bytes = 32.0 * g.Nc();
     const double dlanes = bw.fb.re ? (bw.fb.im == bw.fb.re ? 1.0 : 2.0) : 0.0;
@@ -465,7 +494,16 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
     const double fused_bytes = pass_bytes + 8.0 * g.N + (bw.sb.v ? 8.0 * g.N : 0.0);
     int nbody = 0;  // bodies enqueued: body k (from 0) is clip pass k + 1 unless gated
     auto body = [&]() {
-        if (fused) {
+        if (rt) {
+            {
+                // read + write of the spectrum, Delta, the 1-B marks (read; written where a clamp
+                // moved: counted as N_c), F written densely by the first clip
+                Prof p(c, kColRoundTrip,
+                       check_bytes + 2.0 * g.Nc() + (nbody == 0 ? 16.0 * g.Nc() : 0.0));
+                plan.col_rt(za, spec, spec_rt, gate, HookRT{bw.fb, fscale, c.ctl, F, moved}, st);
+            }
+            k_decide<<<1, 1, 0, st>>>(c.ctl);                                              // K4
+        } else if (fused) {
             {
                 Prof p(c, kColFwdCheck, check_bytes);
                 plan.col(za, -1, spec, spec, gate, HookFReduce{bw.fb, fscale, c.ctl}, st);   // K3a
@@ -479,18 +517,30 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
                 plan.col(za, +1, spec, spec, gate,
                          HookFClip<double>{bw.fb, fscale, F, c.ctl, moved}, st);          // K3b
             }
+        }
+        if (fused) {
             if (three_d) {
                 Prof p(c, kColPass, pass_bytes);
-                plan.col(mid, +1, spec, spec, gate, HookNone{}, st);
+                plan.col(mid, +1, inv_src, inv_src, gate, HookNone{}, st);
             }
-            {   // K1 as C2R(+s-clip, eps written) then R2C: two 90%-of-HBM passes beat one
-                // register-bound fused pass (profiles/r01_passbench.md)
+            if (k1) {
+                // K1: C2R -> s-clip (eps written, S) -> R2C in one row pass, from the inverse
+                // chain's buffer into the forward chain's: half rows read + written, eps written,
+                // S written densely by the first clip (later: read-modify-write where a clamp
+                // moved, not counted), per-point E read
+                Prof p(c, kRowFused, 32.0 * g.Nc() + 8.0 * g.N + (nbody == 0 ? 8.0 * g.N : 0.0) +
+                                         (bw.sb.v ? 8.0 * g.N : 0.0));
+                launch_row_fused<double>(g.n2, inv_src, g.P, g.rows, g.n2, invN, c.tw64, gate,
+                                         HookSClip<double>{bw.sb, fscale, S, eps, c.ctl}, st,
+                                         inv_src == spec ? nullptr : spec);
+            } else {   // K1 as C2R(+s-clip, eps written) then R2C
                 Prof p(c, kRowC2R, 16.0 * g.Nc() + 8.0 * g.N + (bw.sb.v ? 8.0 * g.N : 0.0));
-                launch_row_c2r_hook<double>(g.n2, spec, g.P, eps, g.n2, g.rows, invN, c.tw64, gate,
+                launch_row_c2r_hook<double>(g.n2, inv_src, g.P, eps, g.n2, g.rows, invN, c.tw64,
+                                            gate,
                                             HookSClip<double>{bw.sb, fscale, S, nullptr, c.ctl},
                                             st);
             }
-            {
+            if (!k1) {
                 Prof p(c, kRowR2C, 8.0 * g.N + 16.0 * g.Nc());
                 launch_row_r2c<double>(g.n2, eps, g.n2, spec, g.P, g.rows, c.tw64, gate, st);
             }
@@ -498,7 +548,7 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
                 Prof p(c, kColPass, pass_bytes);
                 plan.col(mid, -1, spec, spec, gate, HookNone{}, st);
             }
-            c.launches += three_d ? 7 : 5;
+            c.launches += (three_d ? 7 : 5) - (rt ? 1 : 0) - (k1 ? 1 : 0);
             ++nbody;
         } else {
             plan.r2c(eps, spec, gate, st);
@@ -550,6 +600,15 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
         inflight.erase(inflight.begin());
         FFCZ_CUDA_CHECK(cudaEventSynchronize(p.ev));
         if (c.hctl[1 + p.slot].done) break;
+    }
+    if (rt) {
+        // the last check's clip never happened in the reference: re-form delta_final in `spec`
+        // and clear the marks only that clip set (HookRT)
+        Prof p(c, kColRoundTrip, check_bytes + 2.0 * g.Nc());
+        HookRT hk{bw.fb, fscale, c.ctl, F, moved};
+        hk.recover = 1;
+        plan.col_rt(za, spec, spec, nullptr, hk, st);
+        ++c.launches;
     }
     const Ctl h = c.read_ctl();
     if (fused && h.passes == 0) {  // converged at the first check: no clip ever wrote S / F

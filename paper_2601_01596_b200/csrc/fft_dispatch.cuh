@@ -346,7 +346,8 @@ void row_c2r_radix(const cplx<T>* in, long long in_stride, T* out, long long out
 
 template <class T, int M, class Hook>
 void row_fused_radix(cplx<T>* data, long long stride, long long nrows, long long real_stride,
-                     T scale, Twiddles<T>& tw, const int* gate, Hook hook, cudaStream_t st) {
+                     T scale, Twiddles<T>& tw, const int* gate, Hook hook, cudaStream_t st,
+                     cplx<T>* out) {
     constexpr int E = RowCfg<T, M>::E, TT = RowCfg<T, M>::TT;
     const int R = rows_per_cta<T, M>(nrows);
     size_t smem = row_smem_bytes<T, M, E>(R);
@@ -356,7 +357,7 @@ void row_fused_radix(cplx<T>* data, long long stride, long long nrows, long long
     set_smem(k, smem);
     k<<<persistent_grid(k, TT * R, smem, (nrows + R - 1) / R), TT * R, smem, st>>>(
         data, stride, nrows, real_stride, tw.stage_table(M, E), tw.post_table(M), scale, gate,
-        hook);
+        hook, out);
     FFCZ_LAUNCH_CHECK();
 }
 
@@ -395,7 +396,56 @@ inline int mixed_lines(long long L, long long nlines, bool pad = true) {
     return static_cast<int>(b);
 }
 
+template <class T, int L, class Hook>
+void col_rt_radix(const cplx<T>* src, cplx<T>* dst, long long row_stride, long long plane_stride,
+                  long long nplanes, int ncols, Twiddles<T>& tw, const int* gate, Hook hook,
+                  cudaStream_t st) {
+    // k_col_tma1's tile: E = 16, 512 threads, B columns of 128-B+ rows within one SM's smem, plus
+    // the marks' landing tile (>= 16 columns: TMA boxes are 16-B multiples)
+    constexpr int E1 = 16, TT1 = L / E1, NT1 = 512;
+    int B1 = std::min(NT1 / TT1, 128);
+    B1 = std::min(B1, pow2_ceil(ncols));
+    B1 = std::max(B1, (32 + TT1 - 1) / TT1);  // whole warps (the hook's block reduction)
+    auto mbw = [](int b) { return std::max(b, 16); };
+    while (B1 > 1 && TT1 * (B1 / 2) >= 32 && col_rt_smem_bytes<T, L, E1>(B1, mbw(B1)) > 220 * 1024)
+        B1 /= 2;
+    const int MB = mbw(B1);
+    CUtensorMap map1, mmap;
+    if (col_rt_smem_bytes<T, L, E1>(B1, MB) > 220 * 1024 ||
+        !encode_col_map(&map1, src, sizeof(T), ncols, L, row_stride, nplanes, plane_stride, B1,
+                        L < 256 ? L : 256, true) ||
+        !encode_col_map(&mmap, hook.moved, 1, ncols, L, row_stride, nplanes, plane_stride, MB,
+                        L < 256 ? L : 256, false))
+        throw Error(kUnsupported, "round-trip column pass: no TMA tile for this axis");
+    auto kt = k_col_tma1_rt<T, L, E1, Hook, NT1>;
+    const size_t sm1 = col_rt_smem_bytes<T, L, E1>(B1, MB);
+    set_smem(kt, sm1);
+    const long long nt = static_cast<long long>((ncols + B1 - 1) / B1) * nplanes;
+    const unsigned grid = persistent_grid(kt, TT1 * B1, sm1, nt);
+    kt<<<grid, TT1 * B1, sm1, st>>>(map1, mmap, dst, row_stride, plane_stride, ncols, B1, MB, nt,
+                                    tw.stage_table(L, E1), gate, hook);
+    FFCZ_LAUNCH_CHECK();
+}
+
 } // namespace detail
+
+// Round-trip column pass (k_col_tma1_rt): power-of-two lines of 16..4096 points.
+template <class T, class Hook>
+void launch_col_rt(long long L, const cplx<T>* src, cplx<T>* dst, long long row_stride,
+                   long long plane_stride, long long nplanes, int ncols, Twiddles<T>& tw,
+                   const int* gate, Hook hook, cudaStream_t st) {
+    switch (L) {
+#define X(n)                                                                                   \
+    case n:                                                                                    \
+        detail::col_rt_radix<T, n, Hook>(src, dst, row_stride, plane_stride, nplanes, ncols,   \
+                                         tw, gate, hook, st);                                  \
+        return;
+        X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
+#undef X
+    default:
+        throw Error(kUnsupported, "round-trip column pass needs a power-of-two extent in [16, 4096]");
+    }
+}
 
 #define FFCZ_POW2_CASES(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
 
@@ -617,13 +667,13 @@ void launch_row_c2r_hook(long long n2, const cplx<T>* in, long long in_stride, T
 template <class T, class Hook>
 void launch_row_fused(long long n2, cplx<T>* data, long long stride, long long nrows,
                       long long real_stride, T scale, Twiddles<T>& tw, const int* gate, Hook hook,
-                      cudaStream_t st) {
+                      cudaStream_t st, cplx<T>* out) {
     if (radix_row_ok(n2)) {
         switch (n2 / 2) {
 #define X(n)                                                                                   \
     case n:                                                                                    \
         detail::row_fused_radix<T, n, Hook>(data, stride, nrows, real_stride, scale, tw, gate, \
-                                            hook, st);                                         \
+                                            hook, st, out);                                    \
         return;
             FFCZ_POW2_CASES(X)
 #undef X

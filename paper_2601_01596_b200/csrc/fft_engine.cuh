@@ -566,6 +566,125 @@ __global__ void __launch_bounds__(NT, 1)
     hook.finish();
 }
 
+// Round trip along one column axis (k_col_tma1's tile walk): forward L-point transform, the
+// hook's check / clip on the spectrum values (hook.mid), inverse transform, store into another
+// buffer — the loop's K3a (check) and K3b (clip + first inverse pass) as ONE read and ONE write
+// of the half spectrum instead of two of each.  The hook's 1-B marks of the tile land by TMA too
+// (a second map, MB >= 16 columns wide, its own mbarrier): they are read from shared memory in
+// the check / clip, and the next tile's marks are requested right after it, so they land during
+// the inverse transform and the stores (no dependent global load, no registers held across the
+// forward transform).  hook.fwd_only() (CTA-uniform) stores the forward values instead:
+// the same instructions re-form the spectrum bit for bit (the recovery launch after the loop's
+// last, discarded clip; HookRT).
+// smem: L x B complex (landing) + (L + L/E) x B scalars (exchange) + L x MB marks + 2 mbarriers.
+template <class T, int L, int E>
+constexpr size_t col_rt_smem_bytes(int B, int MB) {
+    return ((static_cast<size_t>(L) * B * sizeof(cplx<T>) +
+             static_cast<size_t>(L + L / E) * B * sizeof(T) + static_cast<size_t>(L) * MB + 15) &
+            ~size_t(15)) + 32;
+}
+
+template <class T, int L, int E, class Hook, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    k_col_tma1_rt(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap mmap,
+                  cplx<T>* __restrict__ dst, long long row_stride, long long plane_stride,
+                  int ncols, int B, int MB, long long ntiles, const cplx<T>* __restrict__ tw,
+                  const int* gate, const Hook hook) {
+    static_assert(E == 16, "marks are packed 4 per register, 16 per thread");
+    if (gated(gate)) return;
+    const bool first = hook.is_first();
+    double peak = 0.0, ex = 0.0;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int TT = L / E;
+    constexpr int LB = L < 256 ? L : 256;
+    const int b = threadIdx.x % B;
+    const int t = threadIdx.x / B;
+    const int tiles_c = (ncols + B - 1) / B;
+    const bool fwd_only = hook.fwd_only();
+    cplx<T>* land = reinterpret_cast<cplx<T>*>(smem_raw);
+    T* xs = reinterpret_cast<T*>(land + L * B);
+    unsigned char* mk = reinterpret_cast<unsigned char*>(xs + (L + L / E) * B);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(
+        smem_raw + ((static_cast<size_t>(L) * B * sizeof(cplx<T>) +
+                     static_cast<size_t>(L + L / E) * B * sizeof(T) + static_cast<size_t>(L) * MB +
+                     15) & ~size_t(15)));
+    uint64_t* mbar = bar + 1;
+    auto issue = [&](long long tile) {
+        const long long plane = tile / tiles_c;
+        const int c0 = static_cast<int>(tile - plane * tiles_c) * B;
+        mbar_arrive_expect_tx(bar, static_cast<unsigned>(L) * B * sizeof(cplx<T>));
+#pragma unroll
+        for (int j = 0; j < L / LB; ++j)
+            tma_load_3d(land + j * LB * B, &map, bar, 2 * c0, j * LB, static_cast<int>(plane));
+    };
+    auto issue_marks = [&](long long tile) {
+        const long long plane = tile / tiles_c;
+        const int c0 = static_cast<int>(tile - plane * tiles_c) * B;
+        mbar_arrive_expect_tx(mbar, static_cast<unsigned>(L) * MB);
+#pragma unroll
+        for (int j = 0; j < L / LB; ++j)
+            tma_load_3d(mk + j * LB * MB, &mmap, mbar, c0 - c0 % MB, j * LB,
+                        static_cast<int>(plane));
+    };
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&map);
+        tma_prefetch_desc(&mmap);
+        mbar_init(bar, 1);
+        mbar_init(mbar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < ntiles) {
+        issue(blockIdx.x);
+        issue_marks(blockIdx.x);
+    }
+    unsigned phase = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        mbar_wait(bar, phase);
+        const long long plane = tile / tiles_c;
+        const int c0 = static_cast<int>(tile - plane * tiles_c) * B;
+        const int c = c0 + b;
+        const bool valid = c < ncols;
+        const long long base = plane * plane_stride + c;
+        const int mcol = c0 % MB + b;
+        cplx<T> v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = land[(t + TT * m) * B + b];
+        fence_proxy_async_smem();  // generic reads of the landing buffer before the async refill
+        __syncthreads();
+        if (threadIdx.x == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x);
+        stockham<T, L, E, 1, -1>(v, t, tw, XchColS<T, E>{xs + b, B});
+        mbar_wait(mbar, phase);
+        phase ^= 1u;
+        if (valid) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const long long off = base + static_cast<long long>(t + TT * m) * row_stride;
+                hook.mid(v[m], off, hook.fb.at2(off), mk[(t + TT * m) * MB + mcol], first, peak,
+                         ex);
+            }
+        }
+        fence_proxy_async_smem();  // generic reads of the marks before their async refill
+        __syncthreads();
+        if (threadIdx.x == 0 && tile + gridDim.x < ntiles) issue_marks(tile + gridDim.x);
+        if (!fwd_only) {
+            // a fresh twiddle pointer: keeps the compiler from carrying the forward transform's
+            // twiddle powers across the hook into the inverse (CSE; 560 B of spills)
+            const cplx<T>* twi;
+            asm volatile("mov.b64 %0, %1;" : "=l"(twi) : "l"(tw));
+            stockham<T, L, E, 1, +1>(v, t, twi, XchColS<T, E>{xs + b, B});
+        }
+        if (valid) {
+            // (the store addresses re-formed from an opaque base: not the hook's 16 live offsets)
+            cplx<T>* out;
+            asm volatile("mov.b64 %0, %1;" : "=l"(out) : "l"(dst + base));
+#pragma unroll
+            for (int m = 0; m < E; ++m) out[static_cast<long long>(t + TT * m) * row_stride] = v[m];
+        }
+    }
+    hook.finish(peak, ex);
+}
+
 // Column pass of an L-point line split over a 2-CTA cluster (DSMEM): CTA h of the pair lands
 // rows [h L/2, (h+1) L/2) of a B-column tile by TMA, so a tile can be twice as wide as one SM's
 // shared memory allows (FP64: L = 1024 at 16 columns = 256-B rows, L = 2048 at 8 columns =
@@ -862,14 +981,14 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
 }
 
 // Fused last-axis pass of the projection loop: C2R -> (scale, s-cube clip via hook) -> R2C,
-// in place on the half spectrum.  The real epsilon never round-trips HBM except for the hook's
+// in place on the half spectrum (or into `out`).  The real epsilon never round-trips HBM except for the hook's
 // own write.
 // Launched with blockDim.x = (M/E) * rows-per-CTA threads, row_smem_elems() per row of smem.
 template <class T, int M, int E, class Hook>
 __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>())
     k_row_c2r_r2c(cplx<T>* data, long long stride, long long nrows, long long real_stride,
                   const cplx<T>* __restrict__ tw, const cplx<T>* __restrict__ twp, T scale,
-                  const int* gate, Hook hook) {
+                  const int* gate, Hook hook, cplx<T>* out) {
     if (gated(gate)) return;
     hook_begin(hook);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -913,14 +1032,15 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
         for (int m = 0; m < E; ++m) x.st(t + TT * m, v[m]);
         __syncthreads();
         if (valid) {
+            cplx<T>* rowo = out ? out + row * stride : rowp;
     #pragma unroll
             for (int m = 0; m < E; ++m) {
                 const int k = t + TT * m;
-                rowp[k] = r2c_split<T, M, E>(s, k, twp);
+                rowo[k] = r2c_split<T, M, E>(s, k, twp);
             }
             if (t == 0) {
                 const cplx<T> z0 = s[0];
-                rowp[M] = mkc<T>(z0.x - z0.y, T(0));
+                rowo[M] = mkc<T>(z0.x - z0.y, T(0));
             }
         }
         if constexpr (hook_tiled<Hook>()) hook.tile_end();
@@ -1235,7 +1355,7 @@ template <class T, int M, int E, class Hook>
 __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>())
     k_row_c2r_r2c_sh(cplx<T>* data, long long stride, long long nrows, long long real_stride,
                      const cplx<T>* __restrict__ tw, const cplx<T>* __restrict__ twp, T scale,
-                     const int* gate, Hook hook) {
+                     const int* gate, Hook hook, cplx<T>* out) {
     if (gated(gate)) return;
     hook_begin(hook);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1300,9 +1420,16 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
             if (valid) hook.post_real(x0, x1, row * real_stride + 2 * j);
             v[m] = mkc<T>(x0, x1);
         }
-        stockham<T, M, E, 1, -1>(v, t, tw, x);
+        // fresh twiddle pointers for the forward half: otherwise the compiler keeps the inverse
+        // half's stage twiddles and split factors (same indices) live across both transforms
+        // (CSE: 816 B of spills at M = 512, E = 16)
+        const cplx<T>*tw2, *twp2;
+        asm volatile("mov.b64 %0, %1;" : "=l"(tw2) : "l"(tw));
+        asm volatile("mov.b64 %0, %1;" : "=l"(twp2) : "l"(twp));
+        stockham<T, M, E, 1, -1>(v, t, tw2, x);
         mid = natural_to_pairs<T, M, E>(v, t);
-        split_store<T, M, E>(v, mid, t, valid, rowp, row * stride, twp, none);
+        split_store<T, M, E>(v, mid, t, valid, out ? out + (valid ? row : 0) * stride : rowp,
+                             row * stride, twp2, none);
         if constexpr (hook_tiled<Hook>()) hook.tile_end();
     }
     hook.finish();

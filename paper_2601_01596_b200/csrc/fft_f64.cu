@@ -46,8 +46,9 @@ bool encode_col_map(CUtensorMap* map, const void* base, int scalar_bytes, long l
                                    static_cast<cuuint64_t>(plane_stride * eb)};
     const cuuint32_t box[3] = {static_cast<cuuint32_t>(per * B), static_cast<cuuint32_t>(LB), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = encode(map, scalar_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
-                                                     : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+    const CUresult r = encode(map, scalar_bytes == 8   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                   : scalar_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                       : CU_TENSOR_MAP_DATA_TYPE_UINT8,
                               3, const_cast<void*>(base), dims, strides, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -167,5 +168,5 @@ template void launch_row_c2r<double>(long long, const double2*, long long, doubl
 template void launch_row_fused<double, HookSClip<double>>(long long, double2*, long long,
                                                           long long, long long, double,
                                                           Twiddles<double>&, const int*,
-                                                          HookSClip<double>, cudaStream_t);
+                                                          HookSClip<double>, cudaStream_t, double2*);
 } // namespace ffcz_gpu

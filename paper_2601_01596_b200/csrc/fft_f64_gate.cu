@@ -28,8 +28,8 @@ template void launch_col<double, HookVerifyF>(long long, int, const double2*, do
 // gate rounds with FFCZ_GATE_ROW_FUSED=1: C2R -> repair -> R2C in one row pass
 template void launch_row_fused<double, HookRepairVerifyS<float>>(
     long long, double2*, long long, long long, long long, double, Twiddles<double>&, const int*,
-    HookRepairVerifyS<float>, cudaStream_t);
+    HookRepairVerifyS<float>, cudaStream_t, double2*);
 template void launch_row_fused<double, HookRepairVerifyS<double>>(
     long long, double2*, long long, long long, long long, double, Twiddles<double>&, const int*,
-    HookRepairVerifyS<double>, cudaStream_t);
+    HookRepairVerifyS<double>, cudaStream_t, double2*);
 } // namespace ffcz_gpu

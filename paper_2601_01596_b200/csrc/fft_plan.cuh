@@ -71,6 +71,11 @@ template <class T, class Hook>
 void launch_col(long long L, int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
                 long long plane_stride, long long nplanes, int ncols, Twiddles<T>& tw,
                 const int* gate, Hook hook, cudaStream_t st);
+// Round-trip column pass (k_col_tma1_rt: forward, hook.mid, inverse) into dst != src.
+template <class T, class Hook>
+void launch_col_rt(long long L, const cplx<T>* src, cplx<T>* dst, long long row_stride,
+                   long long plane_stride, long long nplanes, int ncols, Twiddles<T>& tw,
+                   const int* gate, Hook hook, cudaStream_t st);
 // Row R2C: real rows (stride in_stride) -> half rows (stride out_stride).
 template <class T>
 void launch_row_r2c(long long n2, const T* in, long long in_stride, cplx<T>* out,
@@ -96,11 +101,12 @@ template <class T, class Hook>
 void launch_row_c2r_hook(long long n2, const cplx<T>* in, long long in_stride, T* out,
                          long long out_stride, long long nrows, T scale, Twiddles<T>& tw,
                          const int* gate, Hook hook, cudaStream_t st);
-// Fused C2R -> hook(real) -> R2C, in place on the half rows (radix path only).
+// Fused C2R -> hook(real) -> R2C, in place on the half rows or into `out` (radix path only).
 template <class T, class Hook>
 void launch_row_fused(long long n2, cplx<T>* data, long long stride, long long nrows,
                       long long real_stride, T scale, Twiddles<T>& tw, const int* gate, Hook hook,
-                      cudaStream_t st);
+                      cudaStream_t st,
+                      cplx<T>* out = nullptr);
 
 // Whole-field transforms built from the passes.
 template <class T>
@@ -135,6 +141,31 @@ struct FftPlan {
         }
         launch_col<T, Hook>(L, dir, src, dst, row_stride, plane_stride, nplanes, g.H, *tw, gate,
                             hook, st);
+    }
+    // column axis `axis3` as one round trip (forward, hook.mid, inverse) from src into dst
+    template <class Hook>
+    void col_rt(int axis3, const cplx<T>* src, cplx<T>* dst, const int* gate, Hook hook,
+                cudaStream_t st) const {
+        long long row_stride, plane_stride, nplanes;
+        axis_strides(axis3, row_stride, plane_stride, nplanes);
+        launch_col_rt<T, Hook>(g.d[axis3], src, dst, row_stride, plane_stride, nplanes, g.H, *tw,
+                               gate, hook, st);
+    }
+    bool rt_ok(int axis3) const {
+        const long long L = g.d[axis3];
+        return sizeof(T) == 8 && is_pow2(L) && L >= 16 && L <= 4096;
+    }
+    void axis_strides(int axis3, long long& row_stride, long long& plane_stride,
+                      long long& nplanes) const {
+        if (axis3 == 1) {
+            row_stride = g.P;
+            plane_stride = g.d[1] * g.P;
+            nplanes = g.d[0];
+        } else {
+            row_stride = g.d[1] * g.P;
+            plane_stride = g.P;
+            nplanes = g.d[1];
+        }
     }
     bool fused_ok() const;
 };

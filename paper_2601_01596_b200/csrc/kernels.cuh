@@ -185,6 +185,56 @@ struct HookFClip {
     __device__ __forceinline__ void finish() {}
 };
 
+// check_convergence (HookFReduce) and project_onto_fcube (HookFClip, rebuild mode) on the same
+// spectrum values, between the forward and the inverse transform of the completing axis
+// (k_col_tma1_rt): the loop's K3a + K3b as one HBM round trip from the forward chain's buffer
+// into the inverse chain's (`old` = the component's mark, landed with the tile).  The clip is speculative: when the decision after the pass (k_decide)
+// ends the loop at this check, the reference does not clip (projection.cpp:104-116), so the
+// clipped output is dropped and the recovery launch (recover = 1, same kernel: the forward values
+// are re-formed bit for bit) stores the spectrum and clears the marks only that clip set.
+// Marks: 0 never moved, 1 moved by a committed clip, 2 first moved by the latest clip.  A clip
+// that moves a component writes old ? 1 : 2 — every clip before the latest one is committed,
+// since the loop went on past it; recovery turns a 2 the last clip set back into 0.
+// F is written densely by the first clip (passes == 0 before its decision), as HookFClip does.
+struct HookRT {
+    FreqB fb;
+    double fscale;
+    Ctl* ctl;
+    double2* F;
+    unsigned char* moved;
+    int recover = 0;
+    // (const members only: the kernel keeps the first flag and the reduction in registers, so
+    // the hook object never needs a local-memory copy)
+    __device__ __forceinline__ bool fwd_only() const { return recover != 0; }
+    __device__ __forceinline__ bool is_first() const {
+        return *reinterpret_cast<const volatile unsigned long long*>(&ctl->passes) == 0;
+    }
+    template <class C>
+    __device__ __forceinline__ void mid(C& v, long long off, double2 d, unsigned old, bool first,
+                                        double& peak, double& ex) const {
+        const double re = v.x, im = v.y;
+        const double dre = d.x * fscale, dim = d.y * fscale;
+        const double cre = clamp_abs(re, dre), cim = clamp_abs(im, dim);
+        const double xre = cre - re, xim = cim - im;
+        const bool mv = xre != 0.0 || xim != 0.0;
+        if (recover) {
+            if (mv && old == 2) moved[off] = 0;
+            return;
+        }
+        const double ar = fabs(re), ai = fabs(im);
+        peak = fmax(peak, fmax(ar, ai));
+        const double e = fmax(ar - dre, ai - dim);
+        if (e > ex) ex = e;
+        if (first) F[off] = make_double2(0.0 + xre, 0.0 + xim);
+        if (mv) moved[off] = old ? 1 : 2;
+        v.x = cre;
+        v.y = cim;
+    }
+    __device__ __forceinline__ void finish(double peak, double ex) const {
+        if (!recover) block_max2_atomic(peak, ex, &ctl->peak_bits, &ctl->exc_bits);
+    }
+};
+
 // ---- fused slab transpose (slab.py peer path) ---------------------------------------------------
 // n / d for n < 2^32 by multiply-high (Granlund-Montgomery round-up method): the scatter decodes
 // element offsets at every store, where a hardware-less 32-bit division would cost ~20 ops.

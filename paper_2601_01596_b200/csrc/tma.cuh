@@ -62,7 +62,8 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
 // Host: encode a 3-D tiled tensor map over a pitched half-spectrum layout viewed as
 // (ncols elements, L rows at row_stride, nplanes at plane_stride) [strides in elements], box =
 // (B elements, LB rows, 1 plane).  complex = true: elements are (re, im) pairs of scalar_bytes
-// each (the map is over 2*ncols scalars); false: one scalar per element (a bound lane).
+// each (the map is over 2*ncols scalars); false: one scalar per element (a bound lane;
+// scalar_bytes 1: a byte map such as the loop's clip marks).
 // Returns false when the geometry is not TMA-legal.
 bool encode_col_map(CUtensorMap* map, const void* base, int scalar_bytes, long long ncols,
                     long long L, long long row_stride, long long nplanes, long long plane_stride,
