@@ -717,13 +717,22 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
         const int za = complete_axis(three_d);
         double* x = eps_t;
         double2* work = freq_cur;  // free until k_gate_freq below
-        {
-            Prof p(c, kElemPre, (2.0 * sizeof(TI) + 16.0) * N);
-            k_eps0_plus_s<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, S, x, N);
+        bool fused_in = false;
+        {   // eps0 + S formed inside the R2C (orig, dec, S rows in; no eps0 + S round trip)
+            Prof p(c, kRowR2C, (2.0 * sizeof(TI) + 8.0) * N + 16.0 * Nc);
+            fused_in = launch_row_r2c_eps0<TI>(g.n2, orig, dec, work, g.P, g.rows, c.tw64, bo.sb,
+                                               1.0, 0.0, nullptr, st, S);
+            if (!fused_in) p.bytes = 0.0;
         }
-        {
-            Prof p(c, kRowR2C, 8.0 * g.N + 16.0 * Nc);
-            launch_row_r2c<double>(g.n2, x, g.n2, work, g.P, g.rows, c.tw64, nullptr, st);
+        if (!fused_in) {
+            {
+                Prof p(c, kElemPre, (2.0 * sizeof(TI) + 16.0) * N);
+                k_eps0_plus_s<TI><<<grid_for(N), 256, 0, st>>>(orig, dec, S, x, N);
+            }
+            {
+                Prof p(c, kRowR2C, 8.0 * g.N + 16.0 * Nc);
+                launch_row_r2c<double>(g.n2, x, g.n2, work, g.P, g.rows, c.tw64, nullptr, st);
+            }
         }
         if (three_d) {
             Prof p(c, kColPass, 32.0 * Nc);
@@ -731,7 +740,10 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
         }
         {
             Prof p(c, kColFwdCheck, 48.0 * Nc + Nc);
-            plan.col(za, -1, work, work, nullptr, HookFRebuild{spec, F, lr.moved}, st);
+            if (plan.rt_ok(za) && loop_rt_enabled())  // marks + delta_final landed by TMA
+                plan.col_frebuild(za, work, spec, F, lr.moved, st);
+            else
+                plan.col(za, -1, work, work, nullptr, HookFRebuild{spec, F, lr.moved}, st);
         }
         FFCZ_LAUNCH_CHECK();
         c.launches += three_d ? 4 : 3;

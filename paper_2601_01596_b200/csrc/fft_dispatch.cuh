@@ -427,6 +427,38 @@ void col_rt_radix(const cplx<T>* src, cplx<T>* dst, long long row_stride, long l
     FFCZ_LAUNCH_CHECK();
 }
 
+template <class T, int L>
+void col_frebuild_radix(const cplx<T>* src, const cplx<T>* delta, cplx<T>* F,
+                        const unsigned char* moved, long long row_stride, long long plane_stride,
+                        long long nplanes, int ncols, Twiddles<T>& tw, cudaStream_t st) {
+    constexpr int E1 = 16, TT1 = L / E1, NT1 = 512;
+    int B1 = std::min(NT1 / TT1, 128);
+    B1 = std::min(B1, pow2_ceil(ncols));
+    B1 = std::max(B1, (32 + TT1 - 1) / TT1);
+    auto mbw = [](int b) { return std::max(b, 16); };
+    while (B1 > 1 && TT1 * (B1 / 2) >= 32 && col_rt_smem_bytes<T, L, E1>(B1, mbw(B1)) > 220 * 1024)
+        B1 /= 2;
+    const int MB = mbw(B1);
+    const int LB = L < 256 ? L : 256;
+    CUtensorMap map1, mmap, dmap;
+    if (col_rt_smem_bytes<T, L, E1>(B1, MB) > 220 * 1024 ||
+        !encode_col_map(&map1, src, sizeof(T), ncols, L, row_stride, nplanes, plane_stride, B1, LB,
+                        true) ||
+        !encode_col_map(&mmap, moved, 1, ncols, L, row_stride, nplanes, plane_stride, MB, LB,
+                        false) ||
+        !encode_col_map(&dmap, delta, sizeof(T), ncols, L, row_stride, nplanes, plane_stride, B1,
+                        LB, true))
+        throw Error(kUnsupported, "F rebuild pass: no TMA tile for this axis");
+    auto kt = k_col_tma1_frebuild<T, L, E1, NT1>;
+    const size_t sm1 = col_rt_smem_bytes<T, L, E1>(B1, MB);
+    set_smem(kt, sm1);
+    const long long nt = static_cast<long long>((ncols + B1 - 1) / B1) * nplanes;
+    const unsigned grid = persistent_grid(kt, TT1 * B1, sm1, nt);
+    kt<<<grid, TT1 * B1, sm1, st>>>(map1, mmap, dmap, F, row_stride, plane_stride, ncols, B1, MB,
+                                    nt, tw.stage_table(L, E1));
+    FFCZ_LAUNCH_CHECK();
+}
+
 } // namespace detail
 
 // Round-trip column pass (k_col_tma1_rt): power-of-two lines of 16..4096 points.
@@ -444,6 +476,24 @@ void launch_col_rt(long long L, const cplx<T>* src, cplx<T>* dst, long long row_
 #undef X
     default:
         throw Error(kUnsupported, "round-trip column pass needs a power-of-two extent in [16, 4096]");
+    }
+}
+
+// The gate's F rebuild on the completing axis (k_col_tma1_frebuild): lines of 16..4096 points.
+template <class T>
+void launch_col_frebuild(long long L, const cplx<T>* src, const cplx<T>* delta, cplx<T>* F,
+                         const unsigned char* moved, long long row_stride, long long plane_stride,
+                         long long nplanes, int ncols, Twiddles<T>& tw, cudaStream_t st) {
+    switch (L) {
+#define X(n)                                                                                    \
+    case n:                                                                                     \
+        detail::col_frebuild_radix<T, n>(src, delta, F, moved, row_stride, plane_stride, nplanes, \
+                                         ncols, tw, st);                                        \
+        return;
+        X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
+#undef X
+    default:
+        throw Error(kUnsupported, "F rebuild pass needs a power-of-two extent in [16, 4096]");
     }
 }
 
@@ -568,7 +618,7 @@ void launch_row_r2c(long long n2, const T* in, long long in_stride, cplx<T>* out
 template <class TI>
 bool launch_row_r2c_eps0(long long n2, const TI* orig, const TI* dec, double2* out,
                          long long out_stride, long long nrows, Twiddles<double>& tw, SpatialB sb,
-                         double fscale, double slack, Ctl* ctl, cudaStream_t st) {
+                         double fscale, double slack, Ctl* ctl, cudaStream_t st, const double* S) {
     if (!radix_row_ok(n2)) return false;
     bool done = false;
     switch (n2 / 2) {
@@ -582,7 +632,7 @@ bool launch_row_r2c_eps0(long long n2, const TI* orig, const TI* dec, double2* o
             detail::set_smem(k, smem);                                                         \
             k<<<detail::persistent_grid(k, TT * R, smem, (nrows + R - 1) / R), TT * R, smem,   \
                 st>>>(orig, dec, n2, out, out_stride, nrows, tw.stage_table(n, E),             \
-                      tw.post_table(n), sb, fscale, slack, ctl);                               \
+                      tw.post_table(n), sb, fscale, slack, ctl, S);                            \
             FFCZ_LAUNCH_CHECK();                                                               \
             done = true;                                                                       \
         }                                                                                      \

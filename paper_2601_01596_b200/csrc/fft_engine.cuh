@@ -685,6 +685,98 @@ __global__ void __launch_bounds__(NT, 1)
     hook.finish(peak, ex);
 }
 
+// The gate's F rebuild on the completing axis (HookFRebuild's arithmetic, k_col_tma1's tile walk):
+// forward transform of FFT(eps0 + S)'s partial spectrum, then F = mark ? delta_final - v : 0, no
+// store of v.  The tile's marks land with it (UINT8 map); delta_final's tile lands in the same
+// landing buffer once the tile is in registers (during the transform), so the hook issues no
+// dependent global load — HookFRebuild's two per-element loads held the pass at 10.3 ms at 1024^3
+// (2.6 TB/s).  The next tile is requested after the F stores (no overlap of its load with this
+// tile's transform: the landing buffer holds delta until then).
+// smem: as k_col_tma1_rt (landing + exchange + L x MB marks + 2 mbarriers).
+template <class T, int L, int E, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    k_col_tma1_frebuild(const __grid_constant__ CUtensorMap map,
+                        const __grid_constant__ CUtensorMap mmap,
+                        const __grid_constant__ CUtensorMap dmap, cplx<T>* __restrict__ F,
+                        long long row_stride, long long plane_stride, int ncols, int B, int MB,
+                        long long ntiles, const cplx<T>* __restrict__ tw) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr int TT = L / E;
+    constexpr int LB = L < 256 ? L : 256;
+    const int b = threadIdx.x % B;
+    const int t = threadIdx.x / B;
+    const int tiles_c = (ncols + B - 1) / B;
+    cplx<T>* land = reinterpret_cast<cplx<T>*>(smem_raw);
+    T* xs = reinterpret_cast<T*>(land + L * B);
+    unsigned char* mk = reinterpret_cast<unsigned char*>(xs + (L + L / E) * B);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(
+        smem_raw + ((static_cast<size_t>(L) * B * sizeof(cplx<T>) +
+                     static_cast<size_t>(L + L / E) * B * sizeof(T) + static_cast<size_t>(L) * MB +
+                     15) & ~size_t(15)));
+    uint64_t* dbar = bar + 1;
+    const unsigned data_bytes = static_cast<unsigned>(L) * B * sizeof(cplx<T>);
+    auto issue = [&](long long tile) {  // the tile's partial spectrum + its marks
+        const long long plane = tile / tiles_c;
+        const int c0 = static_cast<int>(tile - plane * tiles_c) * B;
+        mbar_arrive_expect_tx(bar, data_bytes + static_cast<unsigned>(L) * MB);
+#pragma unroll
+        for (int j = 0; j < L / LB; ++j) {
+            tma_load_3d(land + j * LB * B, &map, bar, 2 * c0, j * LB, static_cast<int>(plane));
+            tma_load_3d(mk + j * LB * MB, &mmap, bar, c0 - c0 % MB, j * LB,
+                        static_cast<int>(plane));
+        }
+    };
+    auto issue_delta = [&](long long tile) {
+        const long long plane = tile / tiles_c;
+        const int c0 = static_cast<int>(tile - plane * tiles_c) * B;
+        mbar_arrive_expect_tx(dbar, data_bytes);
+#pragma unroll
+        for (int j = 0; j < L / LB; ++j)
+            tma_load_3d(land + j * LB * B, &dmap, dbar, 2 * c0, j * LB, static_cast<int>(plane));
+    };
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&map);
+        tma_prefetch_desc(&mmap);
+        tma_prefetch_desc(&dmap);
+        mbar_init(bar, 1);
+        mbar_init(dbar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < ntiles) issue(blockIdx.x);
+    unsigned phase = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        mbar_wait(bar, phase);
+        const long long plane = tile / tiles_c;
+        const int c0 = static_cast<int>(tile - plane * tiles_c) * B;
+        const int c = c0 + b;
+        const bool valid = c < ncols;
+        const long long base = plane * plane_stride + c;
+        const int mcol = c0 % MB + b;
+        cplx<T> v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = land[(t + TT * m) * B + b];
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) issue_delta(tile);
+        stockham<T, L, E, 1, -1>(v, t, tw, XchColS<T, E>{xs + b, B});
+        mbar_wait(dbar, phase);
+        phase ^= 1u;
+        if (valid) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int i = t + TT * m;
+                const cplx<T> d = land[i * B + b];
+                F[base + static_cast<long long>(i) * row_stride] =
+                    mk[i * MB + mcol] ? mkc<T>(d.x - v[m].x, d.y - v[m].y) : mkc<T>(T(0), T(0));
+            }
+        }
+        fence_proxy_async_smem();  // generic reads of delta / marks before the next async fill
+        __syncthreads();
+        if (threadIdx.x == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x);
+    }
+}
+
 // Column pass of an L-point line split over a 2-CTA cluster (DSMEM): CTA h of the pair lands
 // rows [h L/2, (h+1) L/2) of a B-column tile by TMA, so a tile can be twice as wide as one SM's
 // shared memory allows (FP64: L = 1024 at 16 columns = 256-B rows, L = 2048 at 8 columns =
@@ -1227,7 +1319,7 @@ __global__ void __launch_bounds__(max_threads<double, E>(), 512 / max_threads<do
     k_row_r2c_eps0_sh(const TI* __restrict__ orig, const TI* __restrict__ dec, long long n2,
                       double2* __restrict__ out, long long out_stride, long long nrows,
                       const double2* __restrict__ tw, const double2* __restrict__ twp, SB sb,
-                      double fscale, double slack, CTL* ctl) {
+                      double fscale, double slack, CTL* ctl, const double* __restrict__ S) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int TT = M / E;
     const int t = threadIdx.x % TT;
@@ -1257,6 +1349,13 @@ __global__ void __launch_bounds__(max_threads<double, E>(), 512 / max_threads<do
                     e0 = d.x - o.x;
                     e1 = d.y - o.y;
                 }
+                if (S) {  // the gate's F rebuild input eps0 + S (k_eps0_plus_s), no checks
+                    const double2 sv = *reinterpret_cast<const double2*>(S + n);
+                    e0 += sv.x;
+                    e1 += sv.y;
+                    v[m] = make_double2(e0, e1);
+                    continue;
+                }
                 const double E0 = sb.at(n), E1 = sb.at(n + 1);
                 if (fabs(e0) > E0 * (1.0 + 0x1p-20) && static_cast<unsigned long long>(n) < bad1) bad1 = n;
                 if (fabs(e1) > E1 * (1.0 + 0x1p-20) && static_cast<unsigned long long>(n + 1) < bad1) bad1 = n + 1;
@@ -1270,8 +1369,8 @@ __global__ void __launch_bounds__(max_threads<double, E>(), 512 / max_threads<do
         split_store<double, M, E>(v, mid, t, valid, out + (valid ? row : 0) * out_stride,
                                   row * out_stride, twp, none);
     }
-    if (bad1 != ~0ull) atomicMin(&ctl->bad1, bad1);
-    if (bad2 != ~0ull) atomicMin(&ctl->bad2, bad2);
+    if (bad1 != ~0ull && ctl) atomicMin(&ctl->bad1, bad1);
+    if (bad2 != ~0ull && ctl) atomicMin(&ctl->bad2, bad2);
 }
 
 template <class T, int M, int E, class Hook>

@@ -156,10 +156,10 @@ template void launch_col<double, HookFClip<double>>(long long, int, const double
                                                     HookFClip<double>, cudaStream_t);
 template bool launch_row_r2c_eps0<float>(long long, const float*, const float*, double2*,
                                          long long, long long, Twiddles<double>&, SpatialB, double,
-                                         double, Ctl*, cudaStream_t);
+                                         double, Ctl*, cudaStream_t, const double*);
 template bool launch_row_r2c_eps0<double>(long long, const double*, const double*, double2*,
                                           long long, long long, Twiddles<double>&, SpatialB,
-                                          double, double, Ctl*, cudaStream_t);
+                                          double, double, Ctl*, cudaStream_t, const double*);
 template void launch_row_r2c<double>(long long, const double*, long long, double2*, long long,
                                      long long, Twiddles<double>&, const int*, cudaStream_t);
 template void launch_row_c2r<double>(long long, const double2*, long long, double*, long long,

@@ -7,4 +7,7 @@ namespace ffcz_gpu {
 template void launch_col_rt<double, HookRT>(long long, const double2*, double2*, long long,
                                             long long, long long, int, Twiddles<double>&,
                                             const int*, HookRT, cudaStream_t);
+template void launch_col_frebuild<double>(long long, const double2*, const double2*, double2*,
+                                          const unsigned char*, long long, long long, long long,
+                                          int, Twiddles<double>&, cudaStream_t);
 } // namespace ffcz_gpu

@@ -76,6 +76,11 @@ template <class T, class Hook>
 void launch_col_rt(long long L, const cplx<T>* src, cplx<T>* dst, long long row_stride,
                    long long plane_stride, long long nplanes, int ncols, Twiddles<T>& tw,
                    const int* gate, Hook hook, cudaStream_t st);
+// F = moved ? delta - FFT_axis(src) : 0 along one column axis (k_col_tma1_frebuild).
+template <class T>
+void launch_col_frebuild(long long L, const cplx<T>* src, const cplx<T>* delta, cplx<T>* F,
+                         const unsigned char* moved, long long row_stride, long long plane_stride,
+                         long long nplanes, int ncols, Twiddles<T>& tw, cudaStream_t st);
 // Row R2C: real rows (stride in_stride) -> half rows (stride out_stride).
 template <class T>
 void launch_row_r2c(long long n2, const T* in, long long in_stride, cplx<T>* out,
@@ -86,11 +91,13 @@ template <class T, class Hook>
 void launch_row_r2c_hook(long long n2, const T* in, long long in_stride, cplx<T>* out,
                          long long out_stride, long long nrows, Twiddles<T>& tw, const int* gate,
                          Hook hook, cudaStream_t st);
-// First R2C of correct() with compute_error + preconditions fused in (FP64 output).
+// First R2C of correct() with compute_error + preconditions fused in (FP64 output); with S,
+// the R2C of eps0 + S instead (the gate's F rebuild), no checks.
 template <class TI>
 bool launch_row_r2c_eps0(long long n2, const TI* orig, const TI* dec, double2* out,
                          long long out_stride, long long nrows, Twiddles<double>& tw, SpatialB sb,
-                         double fscale, double slack, Ctl* ctl, cudaStream_t st);
+                         double fscale, double slack, Ctl* ctl, cudaStream_t st,
+                         const double* S = nullptr);
 // Row C2R: half rows -> real rows, scaled.
 template <class T>
 void launch_row_c2r(long long n2, const cplx<T>* in, long long in_stride, T* out,
@@ -150,6 +157,13 @@ struct FftPlan {
         axis_strides(axis3, row_stride, plane_stride, nplanes);
         launch_col_rt<T, Hook>(g.d[axis3], src, dst, row_stride, plane_stride, nplanes, g.H, *tw,
                                gate, hook, st);
+    }
+    void col_frebuild(int axis3, const cplx<T>* src, const cplx<T>* delta, cplx<T>* F,
+                      const unsigned char* moved, cudaStream_t st) const {
+        long long row_stride, plane_stride, nplanes;
+        axis_strides(axis3, row_stride, plane_stride, nplanes);
+        launch_col_frebuild<T>(g.d[axis3], src, delta, F, moved, row_stride, plane_stride, nplanes,
+                               g.H, *tw, st);
     }
     bool rt_ok(int axis3) const {
         const long long L = g.d[axis3];

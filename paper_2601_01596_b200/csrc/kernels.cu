@@ -204,10 +204,14 @@ __global__ void k_decide32(Ctl* ctl) {
     if (ctl->switch_now) return;
     const double peak = bitsd(ctl->peak_bits);
     const double ex = bitsd(ctl->exc_bits);
-    if (!(ex > ctl->tau * peak) || ctl->passes >= ctl->max_iters) {
+    // (also when the FP32 excess stopped shrinking: FP32 round-off floor reached before tau —
+    // a tau below it otherwise keeps the FP32 phase running to max_iters)
+    const bool stalled = ctl->passes32 >= 1 && !(ex < ctl->ex32_prev);
+    if (!(ex > ctl->tau * peak) || ctl->passes >= ctl->max_iters || stalled) {
         ctl->switch_now = 1;
         ctl->phase = 1;
     } else {
+        ctl->ex32_prev = ex;
         ctl->passes += 1;
         ctl->passes32 += 1;
     }

@@ -72,6 +72,7 @@ struct Ctl {
     double tau;
     int s_any;    // a spatial clip moved some sample (S is not identically zero)
     int dirty_s;  // escape repair: a spatial component was repaired this round
+    double ex32_prev;  // mixed policy: max excess at the previous FP32 check
 };
 
 __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* p, double v) {
