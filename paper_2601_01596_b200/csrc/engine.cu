@@ -287,6 +287,15 @@ inline bool loop_k1_enabled() {
     return on;
 }
 
+// FFCZ_LOOP_EPS_LATE=0: the fused row pass stores epsilon every iteration instead of once
+inline bool loop_eps_late_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_LOOP_EPS_LATE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 inline int complete_axis(bool three_d) {
     static const int v = [] {
         const char* e = std::getenv("FFCZ_COMPLETE_AXIS");
@@ -487,6 +496,11 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
     double2* inv_src = rt ? spec_rt : spec;
     // fused K1 on the radix row path (power-of-two last axis)
     const bool k1 = fused && loop_k1_enabled() && radix_row_ok(g.n2);
+    // K1 without the epsilon store: the inverse chain alternates between two buffers, so the
+    // last executed K1's input is intact after the loop and its C2R half re-forms the final
+    // epsilon once (same kernel, same bits) instead of every iteration storing it
+    const bool eps_late = rt && k1 && loop_eps_late_enabled();
+    double2* spec_rt2 = eps_late ? c.b<double2>("spec_rt2", g.half_elems()) : nullptr;
 
     const double pass_bytes = 32.0 * g.Nc();
     const double dlanes = bw.fb.re ? (bw.fb.im == bw.fb.re ? 1.0 : 2.0) : 0.0;
@@ -500,7 +514,8 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
                 // moved: counted as N_c), F written densely by the first clip
                 Prof p(c, kColRoundTrip,
                        check_bytes + 2.0 * g.Nc() + (nbody == 0 ? 16.0 * g.Nc() : 0.0));
-                plan.col_rt(za, spec, spec_rt, gate, HookRT{bw.fb, fscale, c.ctl, F, moved}, st);
+                if (eps_late) inv_src = (nbody & 1) ? spec_rt2 : spec_rt;
+                plan.col_rt(za, spec, inv_src, gate, HookRT{bw.fb, fscale, c.ctl, F, moved}, st);
             }
             k_decide<<<1, 1, 0, st>>>(c.ctl);                                              // K4
         } else if (fused) {
@@ -528,11 +543,13 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
                 // chain's buffer into the forward chain's: half rows read + written, eps written,
                 // S written densely by the first clip (later: read-modify-write where a clamp
                 // moved, not counted), per-point E read
-                Prof p(c, kRowFused, 32.0 * g.Nc() + 8.0 * g.N + (nbody == 0 ? 8.0 * g.N : 0.0) +
+                Prof p(c, kRowFused, 32.0 * g.Nc() + (eps_late ? 0.0 : 8.0 * g.N) +
+                                         (nbody == 0 ? 8.0 * g.N : 0.0) +
                                          (bw.sb.v ? 8.0 * g.N : 0.0));
                 launch_row_fused<double>(g.n2, inv_src, g.P, g.rows, g.n2, invN, c.tw64, gate,
-                                         HookSClip<double>{bw.sb, fscale, S, eps, c.ctl}, st,
-                                         inv_src == spec ? nullptr : spec);
+                                         HookSClip<double>{bw.sb, fscale, S,
+                                                           eps_late ? nullptr : eps, c.ctl},
+                                         st, inv_src == spec ? nullptr : spec);
             } else {   // K1 as C2R(+s-clip, eps written) then R2C
                 Prof p(c, kRowC2R, 16.0 * g.Nc() + 8.0 * g.N + (bw.sb.v ? 8.0 * g.N : 0.0));
                 launch_row_c2r_hook<double>(g.n2, inv_src, g.P, eps, g.n2, g.rows, invN, c.tw64,
@@ -609,6 +626,19 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
         hk.recover = 1;
         plan.col_rt(za, spec, spec, nullptr, hk, st);
         ++c.launches;
+    }
+    if (eps_late) {
+        // the final epsilon = the s-clipped C2R of the last executed K1's input (body passes - 1;
+        // with no clip at all eps still holds epsilon0)
+        const unsigned long long passes = c.read_ctl().passes;
+        if (passes >= 1) {
+            Prof p(c, kRowC2R, 16.0 * g.Nc() + 8.0 * g.N + (bw.sb.v ? 8.0 * g.N : 0.0));
+            HookSClip<double> hs{bw.sb, fscale, nullptr, eps, nullptr};
+            hs.c2r_only = 1;
+            launch_row_fused<double>(g.n2, ((passes - 1) & 1) ? spec_rt2 : spec_rt, g.P, g.rows,
+                                     g.n2, invN, c.tw64, nullptr, hs, st, nullptr);
+            ++c.launches;
+        }
     }
     const Ctl h = c.read_ctl();
     if (fused && h.passes == 0) {  // converged at the first check: no clip ever wrote S / F

@@ -87,6 +87,16 @@ inline int tma1_mode() {
     return m;
 }
 
+// FFCZ_TMA1_E8=1: plain FP64 single-landing column passes of >= 1024 points at E = 8 / 1024
+// threads instead of E = 16 / 512 (A/B)
+inline bool tma1_e8() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_TMA1_E8");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 // raises a kernel's dynamic shared-memory limit once (a driver call per launch otherwise)
 template <class K>
 void set_smem(K kernel, size_t bytes) {
@@ -233,6 +243,30 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
                               (mode == 1 || (B1 > Bt && (sizeof(T) == 8
                                                               ? (Bt * sizeof(cplx<T>) < 128 || outer)
                                                               : outer)));
+            if constexpr (sizeof(T) == 8 && L >= 1024 && std::is_same_v<Hook, HookNone>) {
+                // plain FP64 passes at E = 8 with 1024 threads (FFCZ_TMA1_E8): 64 registers, 32
+                // warps per SM instead of 16 (the E = 16 pass issues on 28 % of cycles: latency-
+                // bound, profiles/r02_ncu_full_outer_tma1_1024.csv); one more exchange per line
+                constexpr int E8 = 8, TT8 = L / E8, NT8 = 1024;
+                int B8 = std::min(NT8 / TT8, 128);
+                while (B8 > 1 && col_tma1_smem_bytes<T, L, E8>(B8) > 220 * 1024) B8 /= 2;
+                B8 = std::min(B8, pow2_ceil(ncols));
+                CUtensorMap map8;
+                if (want && tma1_e8() && TT8 * B8 >= 32 && B8 >= B1 &&
+                    encode_col_map(&map8, src, sizeof(T), ncols, L, row_stride, nplanes,
+                                   plane_stride, B8, L < 256 ? L : 256, true)) {
+                    auto kt = dir < 0 ? k_col_tma1<T, L, E8, -1, Hook, NT8>
+                                      : k_col_tma1<T, L, E8, +1, Hook, NT8>;
+                    const size_t sm8 = col_tma1_smem_bytes<T, L, E8>(B8);
+                    set_smem(kt, sm8);
+                    const long long nt = static_cast<long long>((ncols + B8 - 1) / B8) * nplanes;
+                    const unsigned grid = persistent_grid(kt, TT8 * B8, sm8, nt);
+                    kt<<<grid, TT8 * B8, sm8, st>>>(map8, dst, row_stride, plane_stride, ncols, B8,
+                                                    nt, tw.stage_table(L, E8), gate, hook);
+                    FFCZ_LAUNCH_CHECK();
+                    return;
+                }
+            }
             CUtensorMap map1;
             if (want && encode_col_map(&map1, src, sizeof(T), ncols, L, row_stride, nplanes,
                                        plane_stride, B1, L < 256 ? L : 256, true)) {
@@ -396,13 +430,13 @@ inline int mixed_lines(long long L, long long nlines, bool pad = true) {
     return static_cast<int>(b);
 }
 
-template <class T, int L, class Hook>
-void col_rt_radix(const cplx<T>* src, cplx<T>* dst, long long row_stride, long long plane_stride,
-                  long long nplanes, int ncols, Twiddles<T>& tw, const int* gate, Hook hook,
-                  cudaStream_t st) {
-    // k_col_tma1's tile: E = 16, 512 threads, B columns of 128-B+ rows within one SM's smem, plus
-    // the marks' landing tile (>= 16 columns: TMA boxes are 16-B multiples)
-    constexpr int E1 = 16, TT1 = L / E1, NT1 = 512;
+template <class T, int L, class Hook, int E1, int NT1>
+void col_rt_radix_e(const cplx<T>* src, cplx<T>* dst, long long row_stride,
+                    long long plane_stride, long long nplanes, int ncols, Twiddles<T>& tw,
+                    const int* gate, Hook hook, cudaStream_t st) {
+    // k_col_tma1's tile: B columns of 128-B+ rows within one SM's smem, plus the marks' landing
+    // tile (>= 16 columns: TMA boxes are 16-B multiples)
+    constexpr int TT1 = L / E1;
     int B1 = std::min(NT1 / TT1, 128);
     B1 = std::min(B1, pow2_ceil(ncols));
     B1 = std::max(B1, (32 + TT1 - 1) / TT1);  // whole warps (the hook's block reduction)
@@ -425,6 +459,31 @@ void col_rt_radix(const cplx<T>* src, cplx<T>* dst, long long row_stride, long l
     kt<<<grid, TT1 * B1, sm1, st>>>(map1, mmap, dst, row_stride, plane_stride, ncols, B1, MB, nt,
                                     tw.stage_table(L, E1), gate, hook);
     FFCZ_LAUNCH_CHECK();
+}
+
+// FFCZ_RT_E8=1: the round trip of >= 1024-point lines at E = 8 / 1024 threads (64 registers,
+// 32 warps per SM) instead of E = 16 / 512 (A/B)
+inline bool rt_e8() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_RT_E8");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+template <class T, int L, class Hook>
+void col_rt_radix(const cplx<T>* src, cplx<T>* dst, long long row_stride, long long plane_stride,
+                  long long nplanes, int ncols, Twiddles<T>& tw, const int* gate, Hook hook,
+                  cudaStream_t st) {
+    if constexpr (L >= 1024) {
+        if (rt_e8()) {
+            col_rt_radix_e<T, L, Hook, 8, 1024>(src, dst, row_stride, plane_stride, nplanes, ncols,
+                                                tw, gate, hook, st);
+            return;
+        }
+    }
+    col_rt_radix_e<T, L, Hook, 16, 512>(src, dst, row_stride, plane_stride, nplanes, ncols, tw,
+                                        gate, hook, st);
 }
 
 template <class T, int L>

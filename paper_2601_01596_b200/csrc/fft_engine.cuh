@@ -590,7 +590,6 @@ __global__ void __launch_bounds__(NT, 1)
                   cplx<T>* __restrict__ dst, long long row_stride, long long plane_stride,
                   int ncols, int B, int MB, long long ntiles, const cplx<T>* __restrict__ tw,
                   const int* gate, const Hook hook) {
-    static_assert(E == 16, "marks are packed 4 per register, 16 per thread");
     if (gated(gate)) return;
     const bool first = hook.is_first();
     double peak = 0.0, ex = 0.0;
@@ -1519,6 +1518,8 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
             if (valid) hook.post_real(x0, x1, row * real_stride + 2 * j);
             v[m] = mkc<T>(x0, x1);
         }
+        if constexpr (requires { hook.c2r_only; })
+            if (hook.c2r_only) continue;  // (CTA-uniform)
         // fresh twiddle pointers for the forward half: otherwise the compiler keeps the inverse
         // half's stage twiddles and split factors (same indices) live across both transforms
         // (CSE: 816 B of spills at M = 512, E = 16)

@@ -334,6 +334,7 @@ __global__ void k_gate_spatial(const double* __restrict__ S, long long N, Spatia
                                Ctl* ctl) {
     unsigned long long nz_acc = 0;
     const long long stride = (long long)gridDim.x * blockDim.x;
+    const double rstep = 1.0 / (sb.g * pow2i(1 - m));
     for (long long base = blockIdx.x * (long long)blockDim.x; base < N; base += kGateU * stride) {
         double v[kGateU], E[kGateU];
 #pragma unroll
@@ -350,11 +351,13 @@ __global__ void k_gate_spatial(const double* __restrict__ S, long long N, Spatia
             if (n < N) {
                 const bool nz = v[u] != 0.0;
                 const double step = ((E[u]) * pow2i(1 - m));       // editset.cpp:31-33
-                ovf = nz && (fabs(v[u]) / step > kMaxIndex);     // pipeline.cpp:63-64
+                // v / step (global E: by the hoisted reciprocal, the same bits)
+                const double qv = sb.v ? v[u] / step : div_rn(v[u], step, rstep);
+                ovf = nz && (fabs(qv) > kMaxIndex);               // pipeline.cpp:63-64
                 keep = nz && !ovf;
                 double cur = 0.0;
                 if (keep) {
-                    const long long q = llround(v[u] / step);    // editset.cpp:76-84
+                    const long long q = llround(qv);              // editset.cpp:76-84
                     cur = static_cast<double>(static_cast<int>(q)) * step;  // editset.cpp:102
                 } else if (ovf) {
                     cur = v[u];
@@ -378,6 +381,7 @@ __global__ void k_gate_freq(const double2* __restrict__ F, HalfGeom g, FreqB fb,
                             Ctl* ctl) {
     unsigned long long nz_acc = 0;
     const long long total = g.rows * g.H;
+    const double rD = 1.0 / fb.g;  // (global Delta: the reciprocal of div_rn)
     for (HalfWalk hw(g); hw.block_ok(); hw.next()) {
         const long long h = hw.i;
         bool keep = false, ovf = false;
@@ -393,7 +397,8 @@ __global__ void k_gate_freq(const double2* __restrict__ F, HalfGeom g, FreqB fb,
             const double sim = ((db.y) * pow2i(1 - m));
             // v / step == (v / Delta) 2^(m-1) bit for bit (step = Delta 2^(1-m); scaling by a
             // power of two commutes with rounding): one division per lane instead of two
-            const double qx = ((v.x / db.x) * pow2i(m - 1)), qy = ((v.y / db.y) * pow2i(m - 1));
+            const double qx = ((fb.re ? v.x / db.x : div_rn(v.x, db.x, rD)) * pow2i(m - 1)),
+                         qy = ((fb.re ? v.y / db.y : div_rn(v.y, db.y, rD)) * pow2i(m - 1));
             ovf = nz && (fabs(qx) > kMaxIndex || fabs(qy) > kMaxIndex);  // :68-69
             keep = nz && !ovf;
             double2 cur = make_double2(0.0, 0.0);
@@ -714,7 +719,11 @@ struct EmitCodesS {
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            if (act[u]) codes[pos[u]] = static_cast<int>(llround(v[u] / ((e[u]) * pow2i(1 - m))));
+            if (act[u]) {
+                const double step = (e[u]) * pow2i(1 - m);
+                codes[pos[u]] = static_cast<int>(
+                    llround(sb.v ? v[u] / step : div_rn(v[u], step, 1.0 / (sb.g * pow2i(1 - m)))));
+            }
     }
 };
 
@@ -739,8 +748,10 @@ struct EmitCodesF {
         for (int u = 0; u < 4; ++u)
             if (act[u])
                 reinterpret_cast<int2*>(codes)[pos[u]] =
-                    make_int2(static_cast<int>(llround(((v[u].x / d[u].x) * pow2i(m - 1)))),
-                              static_cast<int>(llround(((v[u].y / d[u].y) * pow2i(m - 1)))));
+                    fb.re ? make_int2(static_cast<int>(llround(((v[u].x / d[u].x) * pow2i(m - 1)))),
+                                      static_cast<int>(llround(((v[u].y / d[u].y) * pow2i(m - 1)))))
+                          : make_int2(static_cast<int>(llround(div_rn(v[u].x, fb.g, 1.0 / fb.g) * pow2i(m - 1))),
+                                      static_cast<int>(llround(div_rn(v[u].y, fb.g, 1.0 / fb.g) * pow2i(m - 1))));
     }
 };
 } // namespace

@@ -42,6 +42,17 @@ struct FreqB {
     }
 };
 
+// a / b correctly rounded, given rb = RN(1/b) (one true division per kernel for a global bound):
+// q0 = RN(a rb) is within an ulp of a / b, the remainder a - b q0 is exact under FMA, and one
+// correction step RN(q0 + r rb) is the correctly rounded quotient (Markstein's final-step
+// theorem; finite a, normal b and quotient, as the gate's values are) — bit for bit a / b,
+// without the division's Newton sequence and range checks per element
+__device__ __forceinline__ double div_rn(double a, double b, double rb) {
+    const double q0 = a * rb;
+    const double r = fma(-q0, b, a);
+    return fma(r, rb, q0);
+}
+
 // std::clamp(v, -b, b) (projection.cpp:14-16)
 template <class T>
 __device__ __forceinline__ T clamp_abs(T v, T b) {
@@ -322,6 +333,9 @@ struct HookSClip {
     const Ctl* ctl = nullptr;
     bool first = false;
     int any = 0;  // a clip moved some sample of this CTA (reported as ctl->s_any)
+    // fused row pass only: stop after the C2R half (re-forming the last iteration's epsilon after
+    // the loop, with S == nullptr: no accumulation)
+    int c2r_only = 0;
     __device__ __forceinline__ void begin() {  // without ctl, `first` is the caller's value
         if (ctl) first = *reinterpret_cast<const volatile unsigned long long*>(&ctl->passes) == 1;
     }
@@ -331,8 +345,10 @@ struct HookSClip {
         const double e = sb.at(n) * fscale;
         const double c = clamp_abs(xd, e);
         const double d = c - xd;
-        if (first) S[n] = 0.0 + d;
-        else if (d != 0.0) S[n] = __ldg(&S[n]) + d;  // see HookFClip
+        if (S) {
+            if (first) S[n] = 0.0 + d;
+            else if (d != 0.0) S[n] = __ldg(&S[n]) + d;  // see HookFClip
+        }
         any |= d != 0.0;
         return static_cast<T>(c);
     }
