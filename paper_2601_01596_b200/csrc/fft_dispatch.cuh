@@ -97,6 +97,16 @@ inline bool tma1_e8() {
     return on;
 }
 
+// FFCZ_TMA1_HALF=1: plain FP64 single-landing column passes of >= 1024 points as two 256-thread
+// CTAs per SM on 4-column tiles (A/B)
+inline bool tma1_half() {
+    static const bool on = [] {
+        const char* e = std::getenv("FFCZ_TMA1_HALF");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 // raises a kernel's dynamic shared-memory limit once (a driver call per launch otherwise)
 template <class K>
 void set_smem(K kernel, size_t bytes) {
@@ -243,6 +253,29 @@ void col_radix(int dir, const cplx<T>* src, cplx<T>* dst, long long row_stride,
                               (mode == 1 || (B1 > Bt && (sizeof(T) == 8
                                                               ? (Bt * sizeof(cplx<T>) < 128 || outer)
                                                               : outer)));
+            if constexpr (sizeof(T) == 8 && L >= 1024 && std::is_same_v<Hook, HookNone>) {
+                // plain FP64 passes as two 256-thread CTAs per SM on half-width tiles
+                // (FFCZ_TMA1_HALF, A/B): consecutive CTAs take adjacent 64-B column halves, two
+                // independent tile pipelines per SM instead of one
+                constexpr int EH = 16, TTH = L / EH, NTH = 256;
+                const int BH = std::min(NTH / TTH, pow2_ceil(ncols));
+                CUtensorMap maph;
+                if (want && tma1_half() && BH >= 1 && TTH * BH >= 32 &&
+                    col_tma1_smem_bytes<T, L, EH>(BH) <= 110 * 1024 &&
+                    encode_col_map(&maph, src, sizeof(T), ncols, L, row_stride, nplanes,
+                                   plane_stride, BH, L < 256 ? L : 256, true)) {
+                    auto kt = dir < 0 ? k_col_tma1<T, L, EH, -1, Hook, NTH>
+                                      : k_col_tma1<T, L, EH, +1, Hook, NTH>;
+                    const size_t smh = col_tma1_smem_bytes<T, L, EH>(BH);
+                    set_smem(kt, smh);
+                    const long long nt = static_cast<long long>((ncols + BH - 1) / BH) * nplanes;
+                    const unsigned grid = persistent_grid(kt, TTH * BH, smh, nt);
+                    kt<<<grid, TTH * BH, smh, st>>>(maph, dst, row_stride, plane_stride, ncols, BH,
+                                                    nt, tw.stage_table(L, EH), gate, hook);
+                    FFCZ_LAUNCH_CHECK();
+                    return;
+                }
+            }
             if constexpr (sizeof(T) == 8 && L >= 1024 && std::is_same_v<Hook, HookNone>) {
                 // plain FP64 passes at E = 8 with 1024 threads (FFCZ_TMA1_E8): 64 registers, 32
                 // warps per SM instead of 16 (the E = 16 pass issues on 28 % of cycles: latency-

@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 1)
 // memory (the per-component side tile stays with k_col_tma).
 // smem: L x B complex + (L + L/E) x B scalars + 1 mbarrier.
 template <class T, int L, int E, int DIR, class Hook, int NT>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1))
     k_col_tma1(const __grid_constant__ CUtensorMap map, cplx<T>* __restrict__ dst,
                long long row_stride, long long plane_stride, int ncols, int B, long long ntiles,
                const cplx<T>* __restrict__ tw, const int* gate, Hook hook) {
