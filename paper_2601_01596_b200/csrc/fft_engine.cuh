@@ -162,6 +162,18 @@ struct XchRow {
     __device__ __forceinline__ cplx<T> ld(int i) const { return s[pos(i)]; }
 };
 
+// Row passes whose line fits one warp (the warp-shuffle kernels, L/E <= 32 threads per row): the
+// row's padded buffer is private to its warp, so its exchanges need only a warp barrier — the
+// rows of a CTA no longer wait for each other at every Stockham stage.
+template <class T, int E>
+struct XchRowW {
+    cplx<T>* s;
+    __device__ __forceinline__ static int pos(int i) { return i + i / E; }
+    __device__ __forceinline__ void sync() const { __syncwarp(); }
+    __device__ __forceinline__ void st(int i, cplx<T> v) const { s[pos(i)] = v; }
+    __device__ __forceinline__ cplx<T> ld(int i) const { return s[pos(i)]; }
+};
+
 // ---- Stockham radix-E passes over a line of L points held as v[m] = x[t + T*m] ---------------
 // Stage radices are E, E, ..., E, L/E^k (remainder last so stage 1 writes have stride E, the
 // pattern the padding is built for).  Inter-stage twiddles: one load of w = exp(-2 pi i k/(NS R))
@@ -197,12 +209,24 @@ __device__ __forceinline__ void stockham(cplx<T> (&v)[E], int t, const cplx<T>* 
             const int k = j & (NS - 1);
             constexpr int OFF = stage_tw_offset<L, E>(NS);
             const cplx<T> w1 = tw[OFF + k];
+#ifndef FFCZ_TW_TREE
             cplx<T> w = w1;
 #pragma unroll
             for (int r = 1; r < R; ++r) {
                 a[r] = DIR < 0 ? cmul(a[r], w) : cmulc(a[r], w);
                 if (r + 1 < R) w = cmul(w, w1);
             }
+#else
+            // powers by squaring where r is even (w^r = (w^(r/2))^2): dependency depth 6 for
+            // R = 16 instead of the 14 of successive products, which left the transform's
+            // twiddle step latency-bound at 16 warps per SM
+            cplx<T> w[R];
+            w[1] = w1;
+#pragma unroll
+            for (int r = 2; r < R; ++r) w[r] = (r & 1) ? cmul(w[r - 1], w1) : cmul(w[r / 2], w[r / 2]);
+#pragma unroll
+            for (int r = 1; r < R; ++r) a[r] = DIR < 0 ? cmul(a[r], w[r]) : cmulc(a[r], w[r]);
+#endif
         }
         dft_reg<DIR, R>(a);
 #pragma unroll
@@ -1287,7 +1311,9 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     const int rb = threadIdx.x / TT;
     const long long ntiles = (nrows + (blockDim.x / TT) - 1) / (blockDim.x / TT);
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        __syncthreads();
+        // (a CTA barrier only where the tile is shared: prefetch buffers, per-frame skips)
+        if constexpr (hook_tiled<Hook>()) __syncthreads();
+        else __syncwarp();
         if constexpr (hook_tiled<Hook>()) {
             const long long u = tile * (blockDim.x / TT);
             if (hook.tile_skip(u)) continue;
@@ -1300,7 +1326,7 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
         cplx<T> v[E];
 #pragma unroll
         for (int m = 0; m < E; ++m) v[m] = valid ? src[t + TT * m] : mkc<T>(T(0), T(0));
-        stockham<T, M, E, 1, -1>(v, t, tw, XchRow<T, E>{s});
+        stockham<T, M, E, 1, -1>(v, t, tw, XchRowW<T, E>{s});
         const cplx<T> mid = natural_to_pairs<T, M, E>(v, t);
         split_store<T, M, E>(v, mid, t, valid, out + (valid ? row : 0) * out_stride,
                              row * out_stride, twp, hook);
@@ -1327,7 +1353,7 @@ __global__ void __launch_bounds__(max_threads<double, E>(), 512 / max_threads<do
     HookNone none;
     unsigned long long bad1 = ~0ull, bad2 = ~0ull;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        __syncthreads();
+        __syncwarp();  // (each warp's rows use only its own buffer)
         const long long row = tile * (blockDim.x / TT) + rb;
         const bool valid = row < nrows;
         double2* s = reinterpret_cast<double2*>(smem_raw) + rb * row_smem_elems<M, E>();
@@ -1363,7 +1389,7 @@ __global__ void __launch_bounds__(max_threads<double, E>(), 512 / max_threads<do
             }
             v[m] = make_double2(e0, e1);
         }
-        stockham<double, M, E, 1, -1>(v, t, tw, XchRow<double, E>{s});
+        stockham<double, M, E, 1, -1>(v, t, tw, XchRowW<double, E>{s});
         const double2 mid = natural_to_pairs<double, M, E>(v, t);
         split_store<double, M, E>(v, mid, t, valid, out + (valid ? row : 0) * out_stride,
                                   row * out_stride, twp, none);
@@ -1403,7 +1429,9 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     }
     unsigned pf_phase = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        __syncthreads();
+        // (a CTA barrier only where the tile is shared: prefetch buffers, per-frame skips)
+        if constexpr (hook_prefetch<Hook>() || hook_tiled<Hook>()) __syncthreads();
+        else __syncwarp();
         if constexpr (hook_tiled<Hook>()) {
             const long long u = tile * (blockDim.x / TT);
             if (hook.tile_skip(u)) continue;
@@ -1428,7 +1456,7 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
         load_pairs<T, M, E>(in + (valid ? row : 0) * in_stride, t, valid, v, mid);
         merge_pairs<T, M, E>(v, mid, t, twp);
         pairs_to_natural<T, M, E>(v, mid, t);
-        stockham<T, M, E, 1, +1>(v, t, tw, XchRow<T, E>{s});
+        stockham<T, M, E, 1, +1>(v, t, tw, XchRowW<T, E>{s});
         if constexpr (kPf) {
             mbar_wait(pf_bar, pf_phase);
             pf_phase ^= 1u;
@@ -1478,7 +1506,9 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
     }
     unsigned pf_phase = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        __syncthreads();
+        // (a CTA barrier only where the tile is shared: prefetch buffers, per-frame skips)
+        if constexpr (hook_prefetch<Hook>() || hook_tiled<Hook>()) __syncthreads();
+        else __syncwarp();
         if constexpr (hook_tiled<Hook>()) {
             const long long u = tile * (blockDim.x / TT);
             if (hook.tile_skip(u)) continue;
@@ -1499,7 +1529,7 @@ __global__ void __launch_bounds__(max_threads<T, E>(), 512 / max_threads<T, E>()
         const long long row = tile * (blockDim.x / TT) + rb;
         const bool valid = row < nrows;
         cplx<T>* s = reinterpret_cast<cplx<T>*>(smem_raw) + rb * row_smem_elems<M, E>();
-        const XchRow<T, E> x{s};
+        const XchRowW<T, E> x{s};
         cplx<T>* rowp = data + (valid ? row : 0) * stride;
         cplx<T> v[E], mid;
         load_pairs<T, M, E>(rowp, t, valid, v, mid);
