@@ -645,13 +645,14 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--n", type=int, default=None,
+                    help="volume edge (default 1024; 512 for --config nyx, configs[1]'s size)")
     ap.add_argument("--config", default=None,
                     choices=["nyx", "combustion", "frames", "slab"],
                     help="combustion = configs[3] recipe at 1024^3 on one GPU (default at N=1: "
                          "the north_star target); slab = the same volume slab-decomposed across "
                          "the N ranks (default at N>1: strong scaling of one volume); nyx = "
-                         "configs[1] (use --n 512); frames = configs[2] (batched 2-D frames, "
+                         "configs[1] at 512^3; frames = configs[2] (batched 2-D frames, "
                          "sharded)")
     ap.add_argument("--frames", type=int, default=1024)
     ap.add_argument("--frame-n", type=int, default=2048)
@@ -668,6 +669,8 @@ def main():
     ap.add_argument("--no-other-policy", action="store_true",
                     help="skip timing the other precision policy beside the headline")
     args = ap.parse_args()
+    if args.n is None:  # configs[1] (Nyx) is quoted at 512^3; everything else at 1024^3
+        args.n = 512 if args.config == "nyx" else 1024
 
     if args.policy is None:
         args.policy = "fp64"

@@ -167,6 +167,7 @@ struct XchRow {
 // rows of a CTA no longer wait for each other at every Stockham stage.
 template <class T, int E>
 struct XchRowW {
+    static constexpr bool kTwTree = true;  // twiddle powers by squaring (see stockham)
     cplx<T>* s;
     __device__ __forceinline__ static int pos(int i) { return i + i / E; }
     __device__ __forceinline__ void sync() const { __syncwarp(); }
@@ -192,6 +193,18 @@ __host__ __device__ constexpr int stage_tw_offset(int NS) {
     return off;
 }
 
+template <class X>
+constexpr bool tw_tree() {
+#ifdef FFCZ_TW_TREE
+    return true;
+#else
+    if constexpr (requires { X::kTwTree; })
+        return X::kTwTree;
+    else
+        return false;
+#endif
+}
+
 template <class T, int L, int E, int NS, int DIR, class X>
 __device__ __forceinline__ void stockham(cplx<T> (&v)[E], int t, const cplx<T>* __restrict__ tw,
                                          const X& xch) {
@@ -209,24 +222,26 @@ __device__ __forceinline__ void stockham(cplx<T> (&v)[E], int t, const cplx<T>* 
             const int k = j & (NS - 1);
             constexpr int OFF = stage_tw_offset<L, E>(NS);
             const cplx<T> w1 = tw[OFF + k];
-#ifndef FFCZ_TW_TREE
-            cplx<T> w = w1;
+            if constexpr (!tw_tree<X>()) {
+                cplx<T> w = w1;
 #pragma unroll
-            for (int r = 1; r < R; ++r) {
-                a[r] = DIR < 0 ? cmul(a[r], w) : cmulc(a[r], w);
-                if (r + 1 < R) w = cmul(w, w1);
+                for (int r = 1; r < R; ++r) {
+                    a[r] = DIR < 0 ? cmul(a[r], w) : cmulc(a[r], w);
+                    if (r + 1 < R) w = cmul(w, w1);
+                }
+            } else {
+                // powers by squaring where r is even (w^r = (w^(r/2))^2): dependency depth 6
+                // for R = 16 instead of the 14 of successive products (the warp-per-row passes:
+                // fused row pass -3 %; the column passes measured +2-3 % and keep the chain,
+                // profiles/r02_ab_twiddle_tree.txt)
+                cplx<T> w[R];
+                w[1] = w1;
+#pragma unroll
+                for (int r = 2; r < R; ++r)
+                    w[r] = (r & 1) ? cmul(w[r - 1], w1) : cmul(w[r / 2], w[r / 2]);
+#pragma unroll
+                for (int r = 1; r < R; ++r) a[r] = DIR < 0 ? cmul(a[r], w[r]) : cmulc(a[r], w[r]);
             }
-#else
-            // powers by squaring where r is even (w^r = (w^(r/2))^2): dependency depth 6 for
-            // R = 16 instead of the 14 of successive products, which left the transform's
-            // twiddle step latency-bound at 16 warps per SM
-            cplx<T> w[R];
-            w[1] = w1;
-#pragma unroll
-            for (int r = 2; r < R; ++r) w[r] = (r & 1) ? cmul(w[r - 1], w1) : cmul(w[r / 2], w[r / 2]);
-#pragma unroll
-            for (int r = 1; r < R; ++r) a[r] = DIR < 0 ? cmul(a[r], w[r]) : cmulc(a[r], w[r]);
-#endif
         }
         dft_reg<DIR, R>(a);
 #pragma unroll
