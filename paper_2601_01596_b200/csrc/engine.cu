@@ -2656,7 +2656,8 @@ int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4
                 ps.part_sh = lg2(d1 / W);
                 ps.width_sh = lg2(d1 / W);
                 ps.base = r * d0;
-                launch_row_r2c<double>(g.n2, dd(0), g.n2, d2(1), g.P, g.rows, c.tw64, gate, st);
+                if (P(0))  // (p0 NULL: the rows of A were transformed by INV_SCLIP's fused pass)
+                    launch_row_r2c<double>(g.n2, dd(0), g.n2, d2(1), g.P, g.rows, c.tw64, gate, st);
                 plan.col(1, -1, d2(1), d2(1), gate, HookScatter{ps}, st);
             } else {     // (n0, c1) -> (c0, n1): c0 = n0 / W, n1 = W c1
                 ps.part_sh = lg2(d0 / W);
@@ -2697,6 +2698,23 @@ int ffcz_cuda_slab(ffcz_cuda_ctx* ctx, const ffcz_cuda_slab_op* op, double out[4
             plan.col(axl, +1, d2(0), d2(0), gate, HookNone{}, st);
             HookSClip<double> hk{sb, op->fscale, dd(2), nullptr, nullptr};
             hk.first = op->first != 0;
+            if (P(3)) {
+                // + the forward row step into p3 (the single-volume loop's fused K1: C2R ->
+                // s-clip -> R2C in one row pass, eps still written), and the forward local pass
+                // on p3 when p4 is set (else the caller's peer pass follows)
+                if (radix_row_ok(g.n2)) {
+                    hk.eps = dd(1);
+                    launch_row_fused<double>(g.n2, d2(0), g.P, g.rows, g.n2, invN, c.tw64, gate,
+                                             hk, st, P(3) == P(0) ? nullptr : d2(3));
+                } else {
+                    launch_row_c2r_hook<double>(g.n2, d2(0), g.P, dd(1), g.n2, g.rows, invN,
+                                                c.tw64, gate, hk, st);
+                    launch_row_r2c<double>(g.n2, dd(1), g.n2, d2(3), g.P, g.rows, c.tw64, gate,
+                                           st);
+                }
+                if (P(4)) plan.col(axl, -1, d2(3), d2(3), gate, HookNone{}, st);
+                break;
+            }
             launch_row_c2r_hook<double>(g.n2, d2(0), g.P, dd(1), g.n2, g.rows, invN, c.tw64,
                                         gate, hk, st);
             break;

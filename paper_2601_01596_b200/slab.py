@@ -323,6 +323,9 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E, Delta, m: int = 16,
         be.fwd_local(eps, A, N)
         B = None
 
+    # the row step as one fused pass (the single-volume loop's K1) where the backend has it
+    fused_row = hasattr(be, "inv_sclip_fwd") and os.environ.get("FFCZ_SLAB_FUSED_ROW", "1") != "0"
+
     def body_peer(k):
         """body() with the transposes fused into the passes; a device barrier after each
         scattering pass orders it with the receiving ranks' next pass (and their previous pass
@@ -333,8 +336,12 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E, Delta, m: int = 16,
         be.decide(ls["red"], ls["state"], gate, max_iters)
         be.col0_clip_inv_peer(Delta, fw, F_B, moved_B, k == 0, peer, gate=gate)
         comm.barrier_dev()
-        be.inv_local_sclip(A, eps, N, E, fw, S, k == 0, gate=gate)
-        be.fwd_local_peer(eps, peer, gate=gate)
+        if fused_row:
+            be.inv_sclip_fwd(A, eps, N, E, fw, S, k == 0, gate=gate, col=False)
+            be.fwd_local_peer(None, peer, gate=gate)
+        else:
+            be.inv_local_sclip(A, eps, N, E, fw, S, k == 0, gate=gate)
+            be.fwd_local_peer(eps, peer, gate=gate)
         comm.barrier_dev()
 
     def body(k):
@@ -349,8 +356,11 @@ def _correct_slab(be, comm: Comm, dims, orig, dec, E, Delta, m: int = 16,
         be.decide(ls["red"], ls["state"], gate, max_iters)
         be.col0_clip_inv(B, Delta, fw, F_B, moved_B, k == 0, gate=gate)   # :117-119, axis 0
         A = _transpose_ba(be, comm, B, n1, c0, c1)
-        be.inv_local_sclip(A, eps, N, E, fw, S, k == 0, gate=gate)   # axis 1, C2R, :121-124
-        be.fwd_local(eps, A, N, gate=gate)
+        if fused_row:   # axis 1, C2R -> s-clip (:121-124) -> R2C, axis 1 forward
+            be.inv_sclip_fwd(A, eps, N, E, fw, S, k == 0, gate=gate)
+        else:
+            be.inv_local_sclip(A, eps, N, E, fw, S, k == 0, gate=gate)   # axis 1, C2R, :121-124
+            be.fwd_local(eps, A, N, gate=gate)
 
     # one pass queued behind the one being decided: the host waits on an event per pass, never
     # on a value, and the device never idles for the host

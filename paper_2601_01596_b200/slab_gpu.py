@@ -161,6 +161,13 @@ class GpuSlabBackend:
         self._op(INV_SCLIP, A.shape, [A, eps_out, S], gate=gate, e=E, fscale=fs, n_total=N,
                  first=int(bool(first)))
 
+    def inv_sclip_fwd(self, A, eps_out, N, E, fs, S, first, gate=None, col=True):
+        """inv_local_sclip + the forward row step in ONE row pass (C2R -> s-clip -> R2C, eps still
+        written) back into A, then (col=True) the forward local pass — fwd_local(eps_out, A)
+        without the eps round trip; col=False leaves the column pass to fwd_local_peer(None)."""
+        self._op(INV_SCLIP, A.shape, [A, eps_out, S, A, A if col else None], gate=gate, e=E,
+                 fscale=fs, n_total=N, first=int(bool(first)))
+
     # -- fused all-to-all: the loop's two transposes as peer stores of the passes -------------------
     def peer_ok(self, dims, W):
         """The scattering passes carry hooks (power-of-two axes 0 and 1, in [16, 4096]) and
@@ -232,7 +239,7 @@ class GpuSlabBackend:
 
     def fwd_local_peer(self, x, peer, gate=None):
         """R2C rows + forward axis 1 of x into peer A, scattered into every rank's B."""
-        A = peer["A"]
+        A = peer["A"]   # (x None: A's rows are already transformed, inv_sclip_fwd(col=False))
         self._op(FWD_LOCAL_PEER, A.shape, [x, A] + [None] * 6 + [peer["to_B"]], gate=gate,
                  rank=peer["r"], world=peer["W"])
 
