@@ -51,17 +51,22 @@ void stage(int r, const cplx<T>* in, LineAddr ai, cplx<T>* out, LineAddr ao, lon
 }
 
 template <class T>
-struct Scratch {  // stream-ordered device scratch
+// Device scratch of one call: plain allocations, released after the stream has drained (these
+// passes are a correctness path for rare extents; a stream-ordered pool allocation here was the
+// one suspect left for an intermittent wrong Bluestein result seen in two full-suite runs)
+struct Scratch {
     cudaStream_t st;
     std::vector<void*> bufs;
     cplx<T>* get(long long n) {
         void* p = nullptr;
-        FFCZ_CUDA_CHECK(cudaMallocAsync(&p, sizeof(cplx<T>) * std::max<long long>(1, n), st));
+        FFCZ_CUDA_CHECK(cudaMalloc(&p, sizeof(cplx<T>) * std::max<long long>(1, n)));
         bufs.push_back(p);
         return static_cast<cplx<T>*>(p);
     }
     ~Scratch() {
-        for (void* p : bufs) cudaFreeAsync(p, st);
+        if (bufs.empty()) return;
+        cudaStreamSynchronize(st);
+        for (void* p : bufs) cudaFree(p);
     }
 };
 

@@ -268,8 +268,8 @@ __global__ void k_unpack_rows(const cplx<T>* __restrict__ z, T* __restrict__ x,
 }  // namespace large
 
 // Complex transform of nl lines of length L (dir -1 forward, +1 inverse, unnormalised) from the
-// `ai` layout of src to the `ao` layout of dst (src == dst allowed).  Scratch is stream-ordered
-// (cudaMallocAsync).
+// `ai` layout of src to the `ao` layout of dst (src == dst allowed).  Scratch: per call,
+// (plain cudaMalloc, freed after the stream drains).
 template <class T>
 void large_lines(long long L, int dir, const cplx<T>* src, LineAddr ai, cplx<T>* dst, LineAddr ao,
                  long long nl, Twiddles<T>& tw, const int* gate, cudaStream_t st);
