@@ -296,12 +296,18 @@ inline bool loop_eps_late_enabled() {
     return on;
 }
 
-inline int complete_axis(bool three_d) {
+// The column axis whose pass completes the forward transform (and carries the check / clip):
+// FFCZ_COMPLETE_AXIS=0 / 1 forces the outer / middle axis; by default the outer axis with a global
+// frequency bound (the round trip there and the plain passes on the middle axis: 464.6 vs 467.9
+// ms at 1024^3 config 4) and the middle axis with per-component lanes (config 2 at 512^3: 41.1 vs
+// 27.3 GB/s on the outer axis), profiles/r02_ab_complete_axis.txt
+inline int complete_axis(bool three_d, bool global_delta) {
     static const int v = [] {
         const char* e = std::getenv("FFCZ_COMPLETE_AXIS");
-        return (e && e[0] == '0') ? 0 : 1;
+        return e ? (e[0] == '0' ? 0 : 1) : -1;
     }();
-    return three_d ? v : 1;
+    if (!three_d) return 1;
+    return v >= 0 ? v : (global_delta ? 0 : 1);
 }
 
 struct Bounds {
@@ -483,7 +489,7 @@ LoopResult run_loop(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Boun
         moved = c.b<unsigned char>("f_moved", g.half_elems());
         if (!keep_moved) FFCZ_CUDA_CHECK(cudaMemsetAsync(moved, 0, g.half_elems(), st));
     }
-    const int za = complete_axis(three_d);  // the pass that completes the forward transform
+    const int za = complete_axis(three_d, !bw.fb.re);  // the pass that completes the forward transform
     const int mid = 1 - za;                   // the other column axis (3-D only)
     double* tmp = fused ? nullptr : c.b<double>("real_tmp", g.N);
     // K3a + K3b as one round trip (HookRT): the forward chain ends in `spec`, the inverse chain
@@ -744,7 +750,7 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
         // F = mask(delta_final - FFT(eps0 + S)): one forward transform replaces the F
         // read-modify-writes of clip passes 2.. (HookFClip::moved); delta_final is `spec`
         const bool three_d = g.d[0] > 1;
-        const int za = complete_axis(three_d);
+        const int za = complete_axis(three_d, !bo.fb.re);
         double* x = eps_t;
         double2* work = freq_cur;  // free until k_gate_freq below
         bool fused_in = false;
@@ -851,7 +857,7 @@ GateOut run_gate(ffcz_cuda_ctx& c, const Geometry& g, const TI* orig, const TI* 
     if (fused) {
         // fused rounds: [Z inv] [Y inv] [C2R -> repair_s -> R2C] [Y fwd] [Z fwd + mark] + sparse
         const bool three_d = g.d[0] > 1;
-        const int za = complete_axis(three_d);
+        const int za = complete_axis(three_d, !bo.fb.re);
         const int mid = 1 - za;
         const long long vw = (g.half_elems() + 31) / 32;
         unsigned* viol = c.b<unsigned>("viol", vw);
@@ -1040,7 +1046,7 @@ bool run_phase32(ffcz_cuda_ctx& c, const Geometry& g, double* eps, const Bounds&
     FftPlan<float> plan{g, &c.tw32};
     if (!plan.fused_ok()) return false;
     const bool three_d = g.d[0] > 1;
-    const int za = complete_axis(three_d), mid = 1 - za;
+    const int za = complete_axis(three_d, !bw.fb.re), mid = 1 - za;
     float* eps32 = c.b<float>("eps32", g.N);
     float2* spec = c.b<float2>("spec32", g.half_elems());
     unsigned char* moved = c.b<unsigned char>("f_moved", g.half_elems());
@@ -3248,7 +3254,7 @@ int ffcz_cuda_bench_passes(ffcz_cuda_ctx* ctx, const ffcz_field_desc* field, int
                 timed(("col_inv " + ax).c_str(), 32 * Nc, [&] {
                     plan.col(a, +1, h, h, nullptr, HookNone{}, st); });
             }
-            const int za = complete_axis(g.d[0] > 1);
+            const int za = complete_axis(g.d[0] > 1, true);
             if (g.d[za] > 1 && plan.fused_ok()) {
                 timed("K3a col_fwd_check", 32 * Nc, [&] {
                     plan.col(za, -1, h, h, nullptr, HookFReduce{b.fb, 1.0, c.ctl}, st); });
